@@ -1,0 +1,1005 @@
+/*
+ * oracle/ftlz_oracle.c -- TEST INFRASTRUCTURE ONLY (the checker, never the product).
+ *
+ * A plain-C restatement of the reference `ftlz` 0.1.0 compress/serialize/parse/decompress path
+ * (/root/reference/pkg/src/ftlz), written from the reference's documented behaviour.  Only
+ * tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg may load
+ * it.  Parity is pinned against the Python reference itself: tests/golden/ holds archives,
+ * outputs and reports produced by importing the reference (tools/make_golden.py), and
+ * tests/test_oracle_golden.py checks this file against every one of them.
+ *
+ * Third-party arithmetic restated here: numpy 2.3.5 float64 `add.reduce` (np.sum / np.mean
+ * over contiguous rows) = 0.0 + pairwise_sum(x) with PW_BLOCKSIZE 128 (8 strided accumulators
+ * per leaf, split n2 = n/2 - (n/2 % 8)).  The pin is numpy's own source semantics; verified
+ * bit-exact against fit_regression_batch / sample_select_batch via the golden fixtures.
+ *
+ * Built with -ffp-contract=off (no FMA contraction) and SSE2 doubles: every float64 operation
+ * rounds once, in the operand order the reference writes.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#include "../include/ftlz_b200.h"
+
+#define MAX_CODE_BITS 57 /* encode.py:21 */
+#define SAMPLE_STRIDE 8  /* predict.py:17 */
+
+typedef struct {
+    int64_t nx, ny, nz;
+    int e;
+    int64_t cx, cy, cz, nb;
+} grid_t;
+
+static int grid_init(grid_t* g, int64_t nx, int64_t ny, int64_t nz, int e) {
+    /* core.py:29-35, 133-157 */
+    if (nx < 1 || ny < 1 || nz < 1 || e < 2 || e > 64) return -1;
+    g->nx = nx; g->ny = ny; g->nz = nz; g->e = e;
+    g->cx = (nx + e - 1) / e; g->cy = (ny + e - 1) / e; g->cz = (nz + e - 1) / e;
+    g->nb = g->cx * g->cy * g->cz;
+    return 0;
+}
+
+static void block_geom(const grid_t* g, int64_t b, int64_t org[3], int ext[3]) {
+    /* row-major block index (bi*cy + bj)*cz + bk (core.py:113-122) */
+    int64_t bk = b % g->cz, t = b / g->cz, bj = t % g->cy, bi = t / g->cy;
+    org[0] = bi * g->e; org[1] = bj * g->e; org[2] = bk * g->e;
+    ext[0] = (int)((g->nx - org[0]) < g->e ? (g->nx - org[0]) : g->e);
+    ext[1] = (int)((g->ny - org[1]) < g->e ? (g->ny - org[1]) : g->e);
+    ext[2] = (int)((g->nz - org[2]) < g->e ? (g->nz - org[2]) : g->e);
+}
+
+static int ext_cmp(const int a[3], const int b[3]) {
+    for (int d = 0; d < 3; d++) {
+        if (a[d] != b[d]) return a[d] < b[d] ? -1 : 1;
+    }
+    return 0;
+}
+
+static inline uint32_t f2w(float f) { uint32_t w; memcpy(&w, &f, 4); return w; }
+static inline float w2f(uint32_t w) { float f; memcpy(&f, &w, 4); return f; }
+static inline uint64_t d2w(double d) { uint64_t w; memcpy(&w, &d, 8); return w; }
+static inline double w2d(uint64_t w) { double d; memcpy(&d, &w, 8); return d; }
+
+/* ---------------------------------------------------------------- numpy add.reduce model */
+static double pw_sum(const double* a, int64_t n) {
+    if (n < 8) {
+        double r = 0.0;
+        for (int64_t i = 0; i < n; i++) r += a[i];
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; j++) r[j] = a[j];
+        int64_t i;
+        for (i = 8; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; j++) r[j] += a[i + j];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; i++) res += a[i];
+        return res;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return pw_sum(a, n2) + pw_sum(a + n2, n - n2);
+}
+static double np_sum(const double* a, int64_t n) { return 0.0 + pw_sum(a, n); }
+
+/* ---------------------------------------------------------------- checksums (checksum.py) */
+static void checksum_words(const uint32_t* w, int64_t n, uint64_t* s, uint64_t* si) {
+    uint64_t a = 0, b = 0;
+    for (int64_t i = 0; i < n; i++) {
+        a += (uint64_t)w[i];
+        b += (uint64_t)i * (uint64_t)w[i];
+    }
+    *s = a; *si = b;
+}
+
+/* correct_words (checksum.py:109-142): 0 clean, 1 corrected, 2 uncorrectable */
+static int correct_words(uint32_t* w, int64_t n, uint64_t st_s, uint64_t st_si) {
+    uint64_t s, si;
+    checksum_words(w, n, &s, &si);
+    if (s == st_s && si == st_si) return 0;
+    uint64_t ds = s - st_s, dsi = si - st_si;
+    if (ds == 0) return 2;
+    for (int64_t j = 0; j < n; j++) {
+        if ((uint64_t)j * ds != dsi) continue;
+        uint64_t old = w[j];
+        uint64_t restored = old - ds;
+        if (restored >> 32) continue;
+        w[j] = (uint32_t)restored;
+        uint64_t s2, si2;
+        checksum_words(w, n, &s2, &si2);
+        if (s2 == st_s && si2 == st_si) return 1;
+        w[j] = (uint32_t)old;
+    }
+    return 2;
+}
+
+/* ---------------------------------------------------------------- predictors (predict.py) */
+/* fit_regression_batch (predict.py:81-104) for one block; tmp holds 2*vol doubles */
+static void fit_block(const float* v, const int ext[3], float coef[4], double* tmp) {
+    int64_t vol = (int64_t)ext[0] * ext[1] * ext[2];
+    double* d = tmp;
+    double* t = tmp + vol;
+    for (int64_t p = 0; p < vol; p++) d[p] = (double)v[p];
+    double out0 = np_sum(d, vol) / (double)vol;
+    double slope[3];
+    for (int ax = 0; ax < 3; ax++) {
+        int e = ext[ax];
+        if (e == 1) { slope[ax] = 0.0; continue; }
+        double half = (double)(e - 1) / 2.0;
+        int64_t p = 0;
+        for (int i = 0; i < ext[0]; i++)
+            for (int j = 0; j < ext[1]; j++)
+                for (int k = 0; k < ext[2]; k++, p++) {
+                    int idx = ax == 0 ? i : (ax == 1 ? j : k);
+                    t[p] = ((double)idx - half) * d[p];
+                }
+        double denom = (double)(vol * ((int64_t)e * e - 1)) / 12.0;
+        slope[ax] = np_sum(t, vol) / denom;
+        out0 -= slope[ax] * (double)(e - 1) / 2.0;
+    }
+    coef[0] = (float)out0;
+    coef[1] = (float)slope[0];
+    coef[2] = (float)slope[1];
+    coef[3] = (float)slope[2];
+}
+
+static inline double reg_pred(const float c[4], int i, int j, int k) {
+    /* ((b0 + b1*i) + b2*j) + b3*k, float32 coefficients upcast (pipeline.py:259-268) */
+    return (((double)c[0] + (double)c[1] * (double)i) + (double)c[2] * (double)j) +
+           (double)c[3] * (double)k;
+}
+
+/* 7-term Lorenzo on a zero-padded float64 buffer P of shape (bx+1, by+1, bz+1)
+ * (pipeline.py:246-256; predict.py:114-134, operand order fixed) */
+static inline double lor_pred(const double* P, int py, int pz, int i, int j, int k) {
+#define PP(a, b, c) P[((int64_t)(a) * py + (b)) * pz + (c)]
+    return PP(i, j + 1, k + 1) + PP(i + 1, j, k + 1) + PP(i + 1, j + 1, k) - PP(i, j, k + 1) -
+           PP(i, j + 1, k) - PP(i + 1, j, k) + PP(i, j, k);
+#undef PP
+}
+
+/* sample_select_batch (predict.py:196-231); tmp >= 2*vol + (bx+1)(by+1)(bz+1) doubles */
+static void select_block(const float* v, const int ext[3], const float coef[4], double* e_reg,
+                         double* e_lor, double* tmp) {
+    int bx = ext[0], by = ext[1], bz = ext[2];
+    int64_t vol = (int64_t)bx * by * bz;
+    int py = by + 1, pz = bz + 1;
+    double* P = tmp;
+    int64_t psz = (int64_t)(bx + 1) * py * pz;
+    double* ar = tmp + psz;
+    double* al = ar + vol;
+    memset(P, 0, sizeof(double) * psz);
+    int64_t p = 0;
+    for (int i = 0; i < bx; i++)
+        for (int j = 0; j < by; j++)
+            for (int k = 0; k < bz; k++, p++) P[((int64_t)(i + 1) * py + j + 1) * pz + k + 1] = (double)v[p];
+    int64_t ns = 0;
+    for (int64_t s = SAMPLE_STRIDE; s < vol; s += SAMPLE_STRIDE) {
+        int i = (int)(s / ((int64_t)by * bz)), rem = (int)(s % ((int64_t)by * bz));
+        int j = rem / bz, k = rem % bz;
+        double x = (double)v[s];
+        ar[ns] = fabs(x - reg_pred(coef, i, j, k));
+        al[ns] = fabs(x - lor_pred(P, py, pz, i, j, k));
+        ns++;
+    }
+    *e_reg = np_sum(ar, ns);
+    *e_lor = np_sum(al, ns);
+}
+
+/* ---------------------------------------------------------------- quantizer (quantize.py) */
+typedef struct {
+    double eb, twoeb, capd;
+    uint32_t cap, center;
+} quant_t;
+
+/* _quantize_batch (pipeline.py:271-279) == quantize_diff (quantize.py:37-52) */
+static inline uint32_t quantize(const quant_t* q, double diff, int* ok) {
+    double h = fabs(diff) / q->twoeb;
+    int small = h <= 2.0 * q->capd;
+    double qq = floor((small ? h : 0.0) + 0.5);
+    if (diff < 0) qq = -qq;
+    double b = (double)q->center + qq;
+    *ok = small && b >= 1.0 && b <= (double)(q->cap - 1);
+    return *ok ? (uint32_t)b : 0u;
+}
+
+/* stage (c) for one block, sequential per point in row-major order (a valid topological
+ * order of the Lorenzo wavefront, pipeline.py:196-213; == test_pipeline.py reference_block).
+ * Outputs bins[vol], recon words, unpredictable words (count returned). */
+static int64_t compress_block(const quant_t* q, const float* x, const int ext[3], int kind,
+                              const float coef[4], uint32_t* bins, uint32_t* unp, uint64_t* dc_sum,
+                              double* P) {
+    int bx = ext[0], by = ext[1], bz = ext[2];
+    int py = by + 1, pz = bz + 1;
+    if (kind == 0) memset(P, 0, sizeof(double) * (size_t)(bx + 1) * py * pz);
+    int64_t p = 0, nu = 0;
+    uint64_t dc = 0;
+    for (int i = 0; i < bx; i++)
+        for (int j = 0; j < by; j++)
+            for (int k = 0; k < bz; k++, p++) {
+                double pred = kind == 1 ? reg_pred(coef, i, j, k) : lor_pred(P, py, pz, i, j, k);
+                double x64 = (double)x[p];
+                double diff = x64 - pred;
+                int ok;
+                uint32_t bin = quantize(q, diff, &ok);
+                double offs = (double)bin - (double)q->center;
+                double dcmp = pred + q->twoeb * offs;
+                float d32 = (float)dcmp;
+                int keep = ok && fabs(x64 - (double)d32) <= q->eb;
+                float r32 = keep ? d32 : x[p];
+                bins[p] = keep ? bin : 0u;
+                if (!keep) unp[nu++] = f2w(x[p]);
+                dc += (uint64_t)f2w(r32);
+                if (kind == 0) P[((int64_t)(i + 1) * py + j + 1) * pz + k + 1] = (double)r32;
+            }
+    *dc_sum = dc;
+    return nu;
+}
+
+/* ---------------------------------------------------------------- Huffman (encode.py:26-71) */
+typedef struct { uint64_t w, tie; int32_t id; } hnode_t;
+
+static int h_less(const hnode_t* a, const hnode_t* b) {
+    return a->w < b->w || (a->w == b->w && a->tie < b->tie);
+}
+static void h_push(hnode_t* h, int64_t* n, hnode_t x) {
+    int64_t i = (*n)++;
+    h[i] = x;
+    while (i > 0) {
+        int64_t par = (i - 1) / 2;
+        if (!h_less(&h[i], &h[par])) break;
+        hnode_t t = h[i]; h[i] = h[par]; h[par] = t;
+        i = par;
+    }
+}
+static hnode_t h_pop(hnode_t* h, int64_t* n) {
+    hnode_t top = h[0];
+    h[0] = h[--(*n)];
+    int64_t i = 0;
+    for (;;) {
+        int64_t l = 2 * i + 1, r = l + 1, m = i;
+        if (l < *n && h_less(&h[l], &h[m])) m = l;
+        if (r < *n && h_less(&h[r], &h[m])) m = r;
+        if (m == i) break;
+        hnode_t t = h[i]; h[i] = h[m]; h[m] = t;
+        i = m;
+    }
+    return top;
+}
+
+/* lengths for symbols (ascending) with weights; heap keyed (weight, tiebreak): leaves get
+ * tie = rank in symbol order, merged nodes tie = n, n+1, ... in creation order. */
+static void huffman_lengths(const uint64_t* w, int64_t n, uint8_t* len_out, int* maxlen) {
+    if (n == 1) { len_out[0] = 1; *maxlen = 1; return; }
+    hnode_t* heap = (hnode_t*)calloc((size_t)n, sizeof(hnode_t));
+    int32_t* kid = (int32_t*)malloc(sizeof(int32_t) * (size_t)(2 * n) * 2);
+    int32_t* depth = (int32_t*)malloc(sizeof(int32_t) * (size_t)(2 * n));
+    int64_t hn = 0;
+    for (int64_t s = 0; s < n; s++) h_push(heap, &hn, (hnode_t){w[s], (uint64_t)s, (int32_t)s});
+    int64_t next = n;
+    while (hn > 1) {
+        hnode_t a = h_pop(heap, &hn), b = h_pop(heap, &hn);
+        kid[2 * next] = a.id; kid[2 * next + 1] = b.id;
+        h_push(heap, &hn, (hnode_t){a.w + b.w, (uint64_t)next, (int32_t)next});
+        next++;
+    }
+    int64_t root = (int64_t)heap[0].id;
+    depth[root] = 0;
+    for (int64_t k = root; k >= n; k--) {  /* children are always created before parents */
+        depth[kid[2 * k]] = depth[k] + 1;
+        depth[kid[2 * k + 1]] = depth[k] + 1;
+    }
+    int m = 0;
+    for (int64_t s = 0; s < n; s++) {
+        int d = depth[s];
+        len_out[s] = (uint8_t)(d > 255 ? 255 : d);
+        if (d > m) m = d;
+    }
+    *maxlen = m;
+    free(heap); free(kid); free(depth);
+}
+
+typedef struct { uint8_t len; uint8_t pad[3]; uint32_t sym; uint64_t code; } cw_t;
+static int cw_cmp(const void* a, const void* b) {
+    const cw_t* x = (const cw_t*)a; const cw_t* y = (const cw_t*)b;
+    if (x->len != y->len) return x->len < y->len ? -1 : 1;
+    return x->sym < y->sym ? -1 : (x->sym > y->sym);
+}
+/* canonical code words by (length, symbol) (encode.py:61-71); sorts `cw` in place */
+static void canonical(cw_t* cw, int64_t n) {
+    qsort(cw, (size_t)n, sizeof(cw_t), cw_cmp);
+    uint64_t code = 0;
+    int prev = 0;
+    for (int64_t t = 0; t < n; t++) {
+        code <<= (cw[t].len - prev);
+        cw[t].code = code;
+        code += 1;
+        prev = cw[t].len;
+    }
+}
+
+/* ---------------------------------------------------------------- byte writer */
+typedef struct { uint8_t* p; size_t n, cap; } buf_t;
+static void bw_need(buf_t* b, size_t k) {
+    if (b->n + k <= b->cap) return;
+    size_t nc = b->cap ? b->cap : 4096;
+    while (nc < b->n + k) nc *= 2;
+    b->p = (uint8_t*)realloc(b->p, nc);
+    b->cap = nc;
+}
+static void bw_put(buf_t* b, const void* src, size_t k) { bw_need(b, k); memcpy(b->p + b->n, src, k); b->n += k; }
+static void bw_u8(buf_t* b, uint8_t v) { bw_put(b, &v, 1); }
+static void bw_u32(buf_t* b, uint32_t v) { bw_put(b, &v, 4); }
+static void bw_u64(buf_t* b, uint64_t v) { bw_put(b, &v, 8); }
+
+static void set_info(ftlz_info* in, int code, int kind, int64_t off, int64_t blk, int64_t a, int64_t b) {
+    in->code = code; in->kind = kind; in->offset = off; in->block = blk; in->a = a; in->b = b;
+}
+
+static void emit_list(int64_t* dst, int64_t cap, int64_t* n_out, const uint8_t* flag, int64_t nb) {
+    int64_t n = 0;
+    for (int64_t b = 0; b < nb; b++)
+        if (flag[b]) { if (dst && n < cap) dst[n] = b; n++; }
+    *n_out = n;
+}
+
+/* first flagged block in extent-sorted group order, ids ascending (pipeline.py:216-224) */
+static int64_t first_in_group_order(const grid_t* g, const uint8_t* flag) {
+    int64_t best = -1;
+    int bext[3] = {0, 0, 0};
+    for (int64_t b = 0; b < g->nb; b++) {
+        if (!flag[b]) continue;
+        int64_t org[3]; int ext[3];
+        block_geom(g, b, org, ext);
+        if (best < 0 || ext_cmp(ext, bext) < 0) { best = b; memcpy(bext, ext, sizeof ext); }
+    }
+    return best;
+}
+
+/* ================================================================= compress (pipeline.py:287) */
+int oc_compress(const float* x, int64_t nx, int64_t ny, int64_t nz, int32_t eb_mode,
+                double eb_value, const ftlz_config* cfg, const ftlz_fault* faults, int64_t nf,
+                const int8_t* override, int32_t threads, uint8_t** out, size_t* out_len,
+                ftlz_report* rep) {
+    *out = NULL; *out_len = 0;
+    memset(&rep->info, 0, sizeof rep->info);
+    rep->info.offset = -1; rep->info.block = -1;
+    rep->n_input_corrected = rep->n_bins_corrected = rep->n_dup_mismatch = rep->n_reexecuted = 0;
+    rep->sdc = 0;
+    grid_t g;
+    if (nx < 1 || ny < 1 || nz < 1) {
+        set_info(&rep->info, FTLZ_ERR_INVALID_GEOMETRY, 0, -1, -1, 0, 0);
+        return FTLZ_ERR_INVALID_GEOMETRY;
+    }
+    uint32_t cap = cfg->bin_capacity;
+    if (cap < 4 || (cap & (cap - 1))) {
+        set_info(&rep->info, FTLZ_ERR_INVALID_ARGUMENT, 0, -1, -1, cap, 0);
+        return FTLZ_ERR_INVALID_ARGUMENT;
+    }
+    if (cfg->codec_id != 0) {
+        set_info(&rep->info, FTLZ_ERR_UNSUPPORTED_CODEC, 0, -1, -1, cfg->codec_id, 0);
+        return FTLZ_ERR_UNSUPPORTED_CODEC;
+    }
+#ifdef _OPENMP
+    if (threads > 0) omp_set_num_threads(threads);
+#else
+    (void)threads;
+#endif
+    int64_t N = nx * ny * nz;
+
+    /* resolve_error_bound (core.py:182-193), Field.value_range (core.py:72-74) */
+    double eb = eb_value;
+    if (eb_mode == 1) {
+        float mx = x[0], mn = x[0];
+        int nan = 0;
+        for (int64_t i = 0; i < N; i++) {
+            float v = x[i];
+            if (v != v) nan = 1;
+            if (v > mx) mx = v;
+            if (v < mn) mn = v;
+        }
+        double range = nan ? NAN : (double)mx - (double)mn;
+        eb = eb_value * range;
+    }
+    rep->eb = eb;
+    if (!(eb > 0.0) || !isfinite(eb)) {
+        set_info(&rep->info, FTLZ_ERR_DEGENERATE_BOUND, FTLZ_K_DEGENERATE, -1, -1, 0, 0);
+        return FTLZ_ERR_DEGENERATE_BOUND;
+    }
+    /* partition after the bound (pipeline.py:303-304) */
+    if (grid_init(&g, nx, ny, nz, cfg->block_edge) != 0) {
+        set_info(&rep->info, FTLZ_ERR_INVALID_GEOMETRY, 0, -1, -1, 0, 0);
+        return FTLZ_ERR_INVALID_GEOMETRY;
+    }
+    quant_t q = {eb, 2.0 * eb, (double)cap, cap, cap / 2};
+    int64_t nb = g.nb;
+    int e = g.e;
+    int64_t vmax = (int64_t)e * e * e;
+
+    /* per-block fault lists: count per (block, target) via a simple sorted scan */
+    float* coefs = (float*)malloc(sizeof(float) * 4 * (size_t)nb);
+    uint8_t* ind = (uint8_t*)malloc((size_t)nb);
+    uint8_t* in_fix = (uint8_t*)calloc((size_t)nb, 1);
+    uint8_t* in_bad = (uint8_t*)calloc((size_t)nb, 1);
+    uint8_t* bin_fix = (uint8_t*)calloc((size_t)nb, 1);
+    uint8_t* bin_bad = (uint8_t*)calloc((size_t)nb, 1);
+    int64_t* unp_cnt = (int64_t*)malloc(sizeof(int64_t) * (size_t)nb);
+    uint64_t* bsum = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)nb);
+    uint64_t* bisum = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)nb);
+    uint64_t* dcs = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)nb);
+    uint32_t* bins = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)N);      /* block-major */
+    uint32_t* unpw = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)N);      /* block-major slots */
+    int64_t* boff = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nb + 1)); /* element offset per block */
+    boff[0] = 0;
+    for (int64_t b = 0; b < nb; b++) {
+        int64_t org[3]; int ext[3];
+        block_geom(&g, b, org, ext);
+        boff[b + 1] = boff[b] + (int64_t)ext[0] * ext[1] * ext[2];
+    }
+
+#pragma omp parallel
+    {
+        float* blk = (float*)malloc(sizeof(float) * (size_t)vmax);
+        double* tmp = (double*)malloc(sizeof(double) * (size_t)(3 * vmax + (e + 1) * (e + 1) * (e + 1)));
+        uint32_t* wtmp = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)vmax);
+#pragma omp for schedule(dynamic, 64)
+        for (int64_t b = 0; b < nb; b++) {
+            int64_t org[3]; int ext[3];
+            block_geom(&g, b, org, ext);
+            int64_t vol = (int64_t)ext[0] * ext[1] * ext[2];
+            int64_t p = 0;
+            for (int i = 0; i < ext[0]; i++)
+                for (int j = 0; j < ext[1]; j++) {
+                    const float* row = x + ((org[0] + i) * ny + org[1] + j) * nz + org[2];
+                    for (int k = 0; k < ext[2]; k++) blk[p++] = row[k];
+                }
+            /* stage (a): coefficients + input checksum (pipeline.py:317-327) */
+            float* c = coefs + 4 * b;
+            fit_block(blk, ext, c, tmp);
+            uint64_t s0 = 0, si0 = 0;
+            if (cfg->protect_input) {
+                memcpy(wtmp, blk, sizeof(float) * (size_t)vol);
+                checksum_words(wtmp, vol, &s0, &si0);
+            }
+            /* hooks after stage (a): COEFFS_FITTED, INPUT_AFTER_CHECKSUM (pipeline.py:328-329) */
+            for (int64_t f = 0; f < nf; f++) {
+                if (faults[f].block != b) continue;
+                if (faults[f].target == FTLZ_FAULT_COEFF) {
+                    uint32_t w = f2w(c[faults[f].element]) ^ (1u << faults[f].bit);
+                    c[faults[f].element] = w2f(w);
+                } else if (faults[f].target == FTLZ_FAULT_INPUT) {
+                    uint32_t w = f2w(blk[faults[f].element]) ^ (1u << faults[f].bit);
+                    blk[faults[f].element] = w2f(w);
+                }
+            }
+            /* stage (b): verify/correct then sampled selection (pipeline.py:354-373) */
+            if (cfg->protect_input) {
+                memcpy(wtmp, blk, sizeof(float) * (size_t)vol);
+                int st = correct_words(wtmp, vol, s0, si0);
+                if (st == 2) { in_bad[b] = 1; continue; }
+                if (st == 1) { in_fix[b] = 1; memcpy(blk, wtmp, sizeof(float) * (size_t)vol); }
+            }
+            double er, el;
+            select_block(blk, ext, c, &er, &el, tmp);
+            for (int64_t f = 0; f < nf; f++) {
+                if (faults[f].block != b || faults[f].target != FTLZ_FAULT_ESTIMATE) continue;
+                uint64_t bit = 1ull << faults[f].bit;
+                if (faults[f].element == 0) er = w2d(d2w(er) ^ bit); else el = w2d(d2w(el) ^ bit);
+            }
+            int kind = er < el ? 1 : 0;
+            if (override && override[b] >= 0) kind = override[b];
+            ind[b] = (uint8_t)kind;
+            /* stage (c) (pipeline.py:455-467); stage-(c) verification is a no-op after (b) */
+            uint32_t* bb = bins + boff[b];
+            uint64_t dc;
+            unp_cnt[b] = compress_block(&q, blk, ext, kind, c, bb, unpw + boff[b], &dc, tmp);
+            checksum_words(bb, vol, &bsum[b], &bisum[b]);
+            dcs[b] = dc;
+            /* hook STAGE_BINS_FINALIZED (pipeline.py:468) */
+            for (int64_t f = 0; f < nf; f++)
+                if (faults[f].block == b && faults[f].target == FTLZ_FAULT_BINS)
+                    bb[faults[f].element] ^= (1u << faults[f].bit);
+            /* stage (d) verification (pipeline.py:473-485) */
+            if (cfg->protect_bins) {
+                int st = correct_words(bb, vol, bsum[b], bisum[b]);
+                if (st == 2) bin_bad[b] = 1;
+                if (st == 1) bin_fix[b] = 1;
+            }
+        }
+        free(blk); free(tmp); free(wtmp);
+    }
+
+    int status = FTLZ_OK;
+    int64_t badb = first_in_group_order(&g, in_bad);
+    if (badb >= 0) {
+        set_info(&rep->info, FTLZ_ERR_UNCORRECTABLE, FTLZ_K_UNCORR_INPUT, -1, badb, 0, 0);
+        status = FTLZ_ERR_UNCORRECTABLE;
+        goto done;
+    }
+    for (int64_t b = 0; b < nb; b++)
+        if (bin_bad[b]) {
+            set_info(&rep->info, FTLZ_ERR_UNCORRECTABLE, FTLZ_K_UNCORR_BINS_HIST, -1, b, 0, 0);
+            status = FTLZ_ERR_UNCORRECTABLE;
+            goto done;
+        }
+    {
+        /* histogram + codebook (pipeline.py:486-493) */
+        uint64_t* hist = (uint64_t*)calloc(cap, sizeof(uint64_t));
+        for (int64_t i = 0; i < N; i++) {
+            if (bins[i] >= cap) {
+                free(hist);
+                set_info(&rep->info, FTLZ_ERR_INVARIANT, FTLZ_K_BIN_RANGE, -1, -1, 0, 0);
+                status = FTLZ_ERR_INVARIANT;
+                goto done;
+            }
+            hist[bins[i]]++;
+        }
+        int64_t nsym = 0;
+        for (uint32_t s = 0; s < cap; s++) nsym += (hist[s] || s == 0);
+        uint32_t* syms = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)nsym);
+        uint64_t* wts = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)nsym);
+        uint8_t* lens = (uint8_t*)malloc((size_t)nsym);
+        int64_t t = 0;
+        for (uint32_t s = 0; s < cap; s++)
+            if (hist[s] || s == 0) { syms[t] = s; wts[t] = hist[s]; t++; }
+        int maxlen;
+        huffman_lengths(wts, nsym, lens, &maxlen);
+        if (maxlen > MAX_CODE_BITS) {
+            set_info(&rep->info, FTLZ_ERR_INVARIANT, FTLZ_K_CODE_LEN, -1, -1, maxlen, 0);
+            status = FTLZ_ERR_INVARIANT;
+            free(hist); free(syms); free(wts); free(lens);
+            goto done;
+        }
+        cw_t* cw = (cw_t*)malloc(sizeof(cw_t) * (size_t)nsym);
+        for (int64_t i = 0; i < nsym; i++) { cw[i].len = lens[i]; cw[i].sym = syms[i]; cw[i].code = 0; }
+        canonical(cw, nsym);
+        uint64_t* lut_code = (uint64_t*)calloc(cap, sizeof(uint64_t));
+        uint8_t* lut_len = (uint8_t*)calloc(cap, 1);
+        for (int64_t i = 0; i < nsym; i++) { lut_code[cw[i].sym] = cw[i].code; lut_len[cw[i].sym] = cw[i].len; }
+
+        /* per-block bit lengths, offsets, MSB-first packing (pipeline.py:498-509; encode.py:117-140) */
+        uint64_t* blen = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)nb);
+        uint64_t* bofs = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(nb + 1));
+#pragma omp parallel for schedule(static)
+        for (int64_t b = 0; b < nb; b++) {
+            uint64_t s = 0;
+            for (int64_t i = boff[b]; i < boff[b + 1]; i++) s += lut_len[bins[i]];
+            blen[b] = s;
+        }
+        bofs[0] = 0;
+        for (int64_t b = 0; b < nb; b++) bofs[b + 1] = bofs[b] + blen[b];
+        uint64_t total_bits = bofs[nb];
+        size_t pay_bytes = (size_t)((total_bits + 7) / 8);
+        uint8_t* pay = (uint8_t*)calloc(pay_bytes + 16, 1);
+#pragma omp parallel for schedule(static)
+        for (int64_t b = 0; b < nb; b++) {
+            uint64_t pos = bofs[b];
+            for (int64_t i = boff[b]; i < boff[b + 1]; i++) {
+                uint64_t code = lut_code[bins[i]];
+                int L = lut_len[bins[i]];
+                for (int k = L - 1; k >= 0; k--, pos++) {
+                    if ((code >> k) & 1) __atomic_fetch_or(&pay[pos >> 3], (uint8_t)(0x80u >> (pos & 7)), __ATOMIC_RELAXED);
+                }
+            }
+        }
+
+        /* container (container.py:109-147) */
+        buf_t o = {0};
+        int64_t nreg = 0, nunp = 0;
+        bw_put(&o, "FTLZ", 4);
+        bw_u8(&o, 1);
+        bw_u8(&o, (uint8_t)cfg->codec_id);
+        bw_u64(&o, (uint64_t)nx); bw_u64(&o, (uint64_t)ny); bw_u64(&o, (uint64_t)nz);
+        bw_u32(&o, (uint32_t)e);
+        bw_u8(&o, (uint8_t)(eb_mode ? 1 : 0));
+        bw_put(&o, &eb, 8);
+        bw_u32(&o, cap);
+        bw_u64(&o, (uint64_t)nb);
+        for (int64_t b = 0; b < nb; b++) {
+            bw_u8(&o, ind[b]);
+            if (ind[b] == 1) { bw_put(&o, coefs + 4 * b, 16); nreg++; }
+            bw_u32(&o, (uint32_t)unp_cnt[b]);
+            bw_u32(&o, (uint32_t)blen[b]);
+            nunp += unp_cnt[b];
+        }
+        bw_u32(&o, (uint32_t)nsym);
+        for (int64_t i = 0; i < nsym; i++) { bw_u32(&o, syms[i]); bw_u8(&o, lens[i]); }
+        bw_u64(&o, (uint64_t)pay_bytes);
+        bw_put(&o, pay, pay_bytes);
+        for (int64_t b = 0; b < nb; b++) bw_put(&o, unpw + boff[b], sizeof(uint32_t) * (size_t)unp_cnt[b]);
+        if (cfg->store_sum_dc) {
+            bw_u64(&o, (uint64_t)(8 * nb)); bw_u64(&o, (uint64_t)(8 * nb));
+            bw_put(&o, dcs, sizeof(uint64_t) * (size_t)nb);
+        } else {
+            bw_u64(&o, 0); bw_u64(&o, 0);
+        }
+        *out = o.p; *out_len = o.n;
+        rep->archive_len = (int64_t)o.n;
+        rep->n_blocks = nb; rep->n_regression = nreg; rep->n_unpredictable = nunp;
+        rep->n_symbols = nsym; rep->payload_bits = (int64_t)total_bits; rep->max_code_len = maxlen;
+        free(hist); free(syms); free(wts); free(lens); free(cw); free(lut_code); free(lut_len);
+        free(blen); free(bofs); free(pay);
+    }
+    emit_list(rep->input_corrected, rep->capacity, &rep->n_input_corrected, in_fix, nb);
+    emit_list(rep->bins_corrected, rep->capacity, &rep->n_bins_corrected, bin_fix, nb);
+done:
+    free(coefs); free(ind); free(in_fix); free(in_bad); free(bin_fix); free(bin_bad); free(unp_cnt);
+    free(bsum); free(bisum); free(dcs); free(bins); free(unpw); free(boff);
+    rep->info.code = status;
+    return status;
+}
+
+void oc_free(void* p) { free(p); }
+
+/* ================================================================= parse (container.py:173-285) */
+typedef struct {
+    ftlz_stream_info si;
+    uint8_t* ind;          /* nb */
+    int64_t* rec_off;      /* nb: offset of record start */
+    uint32_t* unpc;        /* nb */
+    uint32_t* blen;        /* nb */
+    uint32_t* syms;        /* n_symbols, ascending */
+    uint8_t* lens;         /* n_symbols */
+} parsed_t;
+
+static void parsed_free(parsed_t* p) {
+    free(p->ind); free(p->rec_off); free(p->unpc); free(p->blen); free(p->syms); free(p->lens);
+    memset(p, 0, sizeof *p);
+}
+
+static inline uint64_t rd64(const uint8_t* p) { uint64_t v; memcpy(&v, p, 8); return v; }
+static inline uint32_t rd32(const uint8_t* p) { uint32_t v; memcpy(&v, p, 4); return v; }
+
+static int parse_impl(const uint8_t* d, size_t len, parsed_t* P, ftlz_info* err) {
+    memset(P, 0, sizeof *P);
+    set_info(err, FTLZ_OK, 0, -1, -1, 0, 0);
+#define FAIL(kind, off, a_, b_) do { set_info(err, FTLZ_ERR_CORRUPT_STREAM, kind, (int64_t)(off), -1, (int64_t)(a_), (int64_t)(b_)); return FTLZ_ERR_CORRUPT_STREAM; } while (0)
+#define TAKE(n, what) do { if ((unsigned __int128)pos + (unsigned __int128)(n) > (unsigned __int128)len) FAIL(FTLZ_K_TRUNCATED, pos, what, 0); } while (0)
+    size_t pos = 0;
+    TAKE(55, FTLZ_F_HEADER);
+    ftlz_header* h = &P->si.hdr;
+    h->version = d[4]; h->codec_id = d[5];
+    uint64_t nx = rd64(d + 6), ny = rd64(d + 14), nz = rd64(d + 22);
+    uint32_t edge = rd32(d + 30);
+    uint8_t mode = d[34];
+    double eb; memcpy(&eb, d + 35, 8);
+    uint32_t cap = rd32(d + 43);
+    uint64_t nb = rd64(d + 47);
+    pos = 55;
+    if (memcmp(d, "FTLZ", 4) != 0) FAIL(FTLZ_K_BAD_MAGIC, 0, 0, 0);
+    if (d[4] != 1) FAIL(FTLZ_K_BAD_VERSION, 4, d[4], 0);
+    if (nx < 1 || ny < 1 || nz < 1) FAIL(FTLZ_K_BAD_DIMS, 6, 0, 0);
+    if (edge < 2 || edge > 64) FAIL(FTLZ_K_BAD_EDGE, 30, edge, 0);
+    if (mode > 1) FAIL(FTLZ_K_BAD_MODE, 34, mode, 0);
+    if (!(eb > 0.0 && isfinite(eb))) FAIL(FTLZ_K_BAD_EB, 35, 0, 0);
+    if (cap < 4 || (cap & (cap - 1))) FAIL(FTLZ_K_BAD_CAPACITY, 43, cap, 0);
+    {
+        unsigned __int128 expect = 1;
+        uint64_t dd[3] = {nx, ny, nz};
+        int over = 0;
+        for (int i = 0; i < 3; i++) {
+            expect *= (unsigned __int128)(dd[i] / edge + (dd[i] % edge != 0));
+            if (expect >> 64) over = 1;
+        }
+        if (over || (uint64_t)expect != nb) FAIL(FTLZ_K_BLOCK_COUNT, 47, nb, 0);
+    }
+    h->nx = (int64_t)nx; h->ny = (int64_t)ny; h->nz = (int64_t)nz;
+    h->block_edge = (int32_t)edge; h->eb_mode = mode; h->eb_value = eb;
+    h->bin_capacity = cap; h->block_count = (int64_t)nb;
+    /* records; allocation bounded by what the bytes can hold */
+    size_t maxrec = (len - pos) / 9 + 1;
+    size_t nalloc = nb < maxrec ? (size_t)nb : maxrec;
+    P->ind = (uint8_t*)malloc(nalloc ? nalloc : 1);
+    P->rec_off = (int64_t*)malloc(sizeof(int64_t) * (nalloc ? nalloc : 1));
+    P->unpc = (uint32_t*)malloc(sizeof(uint32_t) * (nalloc ? nalloc : 1));
+    P->blen = (uint32_t*)malloc(sizeof(uint32_t) * (nalloc ? nalloc : 1));
+    P->si.table_off = (int64_t)pos;
+    unsigned __int128 tot_bits = 0, tot_unp = 0;
+    int64_t nreg = 0;
+    for (uint64_t r = 0; r < nb; r++) {
+        TAKE(1, FTLZ_F_INDICATOR);
+        uint8_t ib = d[pos];
+        size_t rs = pos;
+        pos += 1;
+        if (ib > 1) FAIL(FTLZ_K_BAD_INDICATOR, pos - 1, ib, 0);
+        if (ib) { TAKE(16, FTLZ_F_COEFFS); pos += 16; nreg++; }
+        TAKE(8, FTLZ_F_RECORD);
+        P->ind[r] = ib; P->rec_off[r] = (int64_t)rs;
+        P->unpc[r] = rd32(d + pos); P->blen[r] = rd32(d + pos + 4);
+        tot_unp += P->unpc[r]; tot_bits += P->blen[r];
+        pos += 8;
+    }
+    P->si.table_len = (int64_t)pos - P->si.table_off;
+    P->si.n_regression = nreg;
+    TAKE(4, FTLZ_F_BOOK_SIZE);
+    uint32_t nsym = rd32(d + pos);
+    pos += 4;
+    P->si.book_off = (int64_t)pos - 4;
+    size_t maxsym = (len - pos) / 5 + 1;
+    size_t salloc = nsym < maxsym ? nsym : maxsym;
+    P->syms = (uint32_t*)malloc(sizeof(uint32_t) * (salloc ? salloc : 1));
+    P->lens = (uint8_t*)malloc(salloc ? salloc : 1);
+    int64_t prev = -1;
+    unsigned __int128 kraft = 0;
+    int maxlen = 0;
+    for (uint32_t t = 0; t < nsym; t++) {
+        TAKE(5, FTLZ_F_BOOK_ENTRY);
+        uint32_t s = rd32(d + pos);
+        uint8_t l = d[pos + 4];
+        pos += 5;
+        if ((int64_t)s <= prev) FAIL(FTLZ_K_SYM_ORDER, pos - 5, 0, 0);
+        if (s >= cap) FAIL(FTLZ_K_SYM_RANGE, pos - 5, s, 0);
+        if (l < 1 || l > 57) FAIL(FTLZ_K_BAD_LEN, pos - 1, l, 0);
+        P->syms[t] = s; P->lens[t] = l;
+        kraft += (unsigned __int128)1 << (57 - l);
+        if (l > maxlen) maxlen = l;
+        prev = s;
+    }
+    if (nsym == 0) FAIL(FTLZ_K_EMPTY_BOOK, pos, 0, 0);
+    if (kraft > ((unsigned __int128)1 << 57)) FAIL(FTLZ_K_KRAFT, pos, 0, 0);
+    P->si.n_symbols = nsym;
+    P->si.max_code_len = maxlen;
+    TAKE(8, FTLZ_F_PAYLOAD_LEN);
+    uint64_t plen = rd64(d + pos);
+    pos += 8;
+    TAKE(plen, FTLZ_F_PAYLOAD);
+    if (h->codec_id != 0) {  /* backend_invert of codecs 1/2 is not on this path */
+        set_info(err, FTLZ_ERR_UNSUPPORTED_CODEC, 0, -1, -1, h->codec_id, 0);
+        return FTLZ_ERR_UNSUPPORTED_CODEC;
+    }
+    P->si.payload_off = (int64_t)pos;
+    P->si.payload_len = (int64_t)plen;
+    pos += plen;
+    if (tot_bits > (unsigned __int128)8 * plen) FAIL(FTLZ_K_BITS_EXCEED, pos, 0, 0);
+    P->si.total_bits = (int64_t)tot_bits;
+    TAKE(tot_unp * 4, FTLZ_F_UNPRED);
+    P->si.unpred_off = (int64_t)pos;
+    P->si.n_unpred = (int64_t)tot_unp;
+    pos += (size_t)(tot_unp * 4);
+    TAKE(16, FTLZ_F_SUMDC_LENS);
+    uint64_t raw_len = rd64(d + pos), st_len = rd64(d + pos + 8);
+    pos += 16;
+    if (raw_len != 0 && raw_len != 8 * nb) FAIL(FTLZ_K_SUMDC_LEN, pos - 16, raw_len, 0);
+    P->si.sumdc_off = -1;
+    if (raw_len) {
+        TAKE(st_len, FTLZ_F_SUMDC);
+        P->si.sumdc_off = (int64_t)pos;
+        pos += st_len;
+        if (st_len != raw_len) FAIL(FTLZ_K_SUMDC_MISMATCH, pos, 0, 0);
+        P->si.has_sum_dc = 1;
+    } else if (st_len) {
+        FAIL(FTLZ_K_ORPHAN, pos - 8, 0, 0);
+    }
+    if (pos != len) FAIL(FTLZ_K_TRAILING, pos, (int64_t)(len - pos), 0);
+    return FTLZ_OK;
+#undef FAIL
+#undef TAKE
+}
+
+int oc_parse(const uint8_t* data, size_t len, ftlz_stream_info* info, ftlz_info* err) {
+    parsed_t P;
+    int st = parse_impl(data, len, &P, err);
+    if (info) *info = P.si;
+    parsed_free(&P);
+    return st;
+}
+
+/* ================================================================= decompress (pipeline.py:645) */
+typedef struct {
+    int maxlen;
+    uint64_t first[MAX_CODE_BITS + 2];
+    int64_t cnt[MAX_CODE_BITS + 2], base[MAX_CODE_BITS + 2];
+    uint32_t* sym_sorted;  /* by (len, sym) */
+} dtab_t;
+
+static inline int getbit(const uint8_t* pay, uint64_t pos, uint64_t limit_bits) {
+    if (pos >= limit_bits) return 0; /* chunk padded with zero bytes (encode.py:214) */
+    return (pay[pos >> 3] >> (7 - (pos & 7))) & 1;
+}
+
+/* _Decoder.decode (encode.py:198-256) + zero-count check (pipeline.py:565-578).
+ * Returns 0 or a FTLZ_K_D_* kind with aux values. */
+static int decode_block(const dtab_t* T, const uint8_t* pay, uint64_t pay_len, uint64_t off,
+                        uint64_t blen, int64_t count, uint32_t* outb, int64_t* a, int64_t* bb) {
+    if (count == 0) return blen != 0 ? FTLZ_K_D_EMPTY : 0;
+    uint64_t first_byte = off >> 3, last_byte = (off + blen + 7) >> 3;
+    if (last_byte > pay_len) return FTLZ_K_D_PAST_END;
+    (void)first_byte;
+    uint64_t limit = last_byte * 8;
+    uint64_t consumed = 0;
+    for (int64_t idx = 0; idx < count; idx++) {
+        if (consumed > blen) return FTLZ_K_D_RAN_PAST;
+        uint64_t code = 0;
+        int found = 0;
+        for (int l = 1; l <= T->maxlen; l++) {
+            code = (code << 1) | (uint64_t)getbit(pay, off + consumed + l - 1, limit);
+            if (T->cnt[l] && code >= T->first[l] && code - T->first[l] < (uint64_t)T->cnt[l]) {
+                outb[idx] = T->sym_sorted[T->base[l] + (int64_t)(code - T->first[l])];
+                consumed += (uint64_t)l;
+                found = 1;
+                break;
+            }
+        }
+        if (!found) return FTLZ_K_D_OUTSIDE;
+    }
+    if (consumed != blen) { *a = (int64_t)consumed; *bb = (int64_t)blen; return FTLZ_K_D_CONSUMED; }
+    return 0;
+}
+
+/* _reconstruct_group (pipeline.py:586-638) for one block */
+static void reconstruct_block(const quant_t* q, const uint32_t* bins, const uint32_t* raw,
+                              const int ext[3], int kind, const float c[4], float* out, double* P) {
+    int bx = ext[0], by = ext[1], bz = ext[2];
+    int py = by + 1, pz = bz + 1;
+    if (kind == 0) memset(P, 0, sizeof(double) * (size_t)(bx + 1) * py * pz);
+    int64_t p = 0, r = 0;
+    for (int i = 0; i < bx; i++)
+        for (int j = 0; j < by; j++)
+            for (int k = 0; k < bz; k++, p++) {
+                double pred = kind == 1 ? reg_pred(c, i, j, k) : lor_pred(P, py, pz, i, j, k);
+                float v;
+                if (bins[p] > 0) {
+                    double offs = (double)bins[p] - (double)q->center;
+                    v = (float)(pred + q->twoeb * offs);
+                } else {
+                    v = w2f(raw[r++]);
+                }
+                out[p] = v;
+                if (kind == 0) P[((int64_t)(i + 1) * py + j + 1) * pz + k + 1] = (double)v;
+            }
+}
+
+int oc_decompress(const uint8_t* data, size_t len, float* out, const ftlz_fault* faults,
+                  int64_t nf, int32_t threads, ftlz_report* rep) {
+    memset(&rep->info, 0, sizeof rep->info);
+    rep->info.offset = -1; rep->info.block = -1;
+    rep->n_input_corrected = rep->n_bins_corrected = rep->n_dup_mismatch = rep->n_reexecuted = 0;
+    rep->sdc = 0;
+#ifdef _OPENMP
+    if (threads > 0) omp_set_num_threads(threads);
+#else
+    (void)threads;
+#endif
+    parsed_t P;
+    int st = parse_impl(data, len, &P, &rep->info);
+    if (st != FTLZ_OK) { parsed_free(&P); return st; }
+    ftlz_header* h = &P.si.hdr;
+    grid_t g;
+    grid_init(&g, h->nx, h->ny, h->nz, h->block_edge);
+    int64_t nb = g.nb, e = g.e, vmax = e * e * e;
+    quant_t q = {h->eb_value, 2.0 * h->eb_value, (double)h->bin_capacity, h->bin_capacity, h->bin_capacity / 2};
+    rep->eb = h->eb_value;
+    rep->n_blocks = nb;
+    rep->n_symbols = P.si.n_symbols;
+    rep->n_regression = P.si.n_regression;
+    rep->n_unpredictable = P.si.n_unpred;
+    rep->payload_bits = P.si.total_bits;
+    rep->max_code_len = P.si.max_code_len;
+
+    /* decode tables: canonical codes by (len, sym) */
+    dtab_t T;
+    memset(&T, 0, sizeof T);
+    int64_t ns = P.si.n_symbols;
+    cw_t* cw = (cw_t*)malloc(sizeof(cw_t) * (size_t)ns);
+    for (int64_t i = 0; i < ns; i++) { cw[i].len = P.lens[i]; cw[i].sym = P.syms[i]; }
+    canonical(cw, ns);
+    T.sym_sorted = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)ns);
+    T.maxlen = 0;
+    for (int64_t i = 0; i < ns; i++) {
+        int l = cw[i].len;
+        if (T.cnt[l] == 0) { T.first[l] = cw[i].code; T.base[l] = i; }
+        T.cnt[l]++;
+        T.sym_sorted[i] = cw[i].sym;
+        if (l > T.maxlen) T.maxlen = l;
+    }
+    free(cw);
+
+    const uint8_t* pay = data + P.si.payload_off;
+    const uint32_t* unp_all = (const uint32_t*)malloc(4 * (size_t)(P.si.n_unpred + 1));
+    memcpy((void*)unp_all, data + P.si.unpred_off, 4 * (size_t)P.si.n_unpred);
+    uint64_t* bofs = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(nb + 1));
+    int64_t* uofs = (int64_t*)malloc(sizeof(int64_t) * (size_t)(nb + 1));
+    bofs[0] = 0; uofs[0] = 0;
+    for (int64_t b = 0; b < nb; b++) { bofs[b + 1] = bofs[b] + P.blen[b]; uofs[b + 1] = uofs[b] + P.unpc[b]; }
+    uint8_t* dkind = (uint8_t*)calloc((size_t)nb, 1);
+    int64_t* da = (int64_t*)calloc((size_t)nb, sizeof(int64_t));
+    int64_t* db = (int64_t*)calloc((size_t)nb, sizeof(int64_t));
+    uint8_t* mism = (uint8_t*)calloc((size_t)nb, 1);
+    int64_t ny = h->ny, nz = h->nz;
+    int has = P.si.has_sum_dc;
+
+#pragma omp parallel
+    {
+        uint32_t* bb = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)vmax);
+        float* rb = (float*)malloc(sizeof(float) * (size_t)vmax);
+        double* Pb = (double*)malloc(sizeof(double) * (size_t)((e + 1) * (e + 1) * (e + 1)));
+#pragma omp for schedule(dynamic, 64)
+        for (int64_t b = 0; b < nb; b++) {
+            int64_t org[3]; int ext[3];
+            block_geom(&g, b, org, ext);
+            int64_t vol = (int64_t)ext[0] * ext[1] * ext[2];
+            int64_t a = 0, c2 = 0;
+            int k = decode_block(&T, pay, (uint64_t)P.si.payload_len, bofs[b], P.blen[b], vol, bb, &a, &c2);
+            if (!k) {
+                int64_t z = 0;
+                for (int64_t i = 0; i < vol; i++) z += bb[i] == 0;
+                if (z != (int64_t)P.unpc[b]) { k = FTLZ_K_D_ZEROS; a = z; c2 = P.unpc[b]; }
+            }
+            if (k) { dkind[b] = (uint8_t)k; da[b] = a; db[b] = c2; continue; }
+            float c[4] = {0, 0, 0, 0};
+            if (P.ind[b]) memcpy(c, data + P.rec_off[b] + 1, 16);
+            reconstruct_block(&q, bb, unp_all + uofs[b], ext, P.ind[b], c, rb, Pb);
+            /* hook STAGE_DECOMP_BEFORE_VERIFY (pipeline.py:690), applied once */
+            for (int64_t f = 0; f < nf; f++)
+                if (faults[f].target == FTLZ_FAULT_DECOMP && faults[f].block == b)
+                    rb[faults[f].element] = w2f(f2w(rb[faults[f].element]) ^ (1u << faults[f].bit));
+            uint64_t s = 0;
+            int64_t p = 0;
+            for (int i = 0; i < ext[0]; i++)
+                for (int j = 0; j < ext[1]; j++) {
+                    float* row = out + ((org[0] + i) * ny + org[1] + j) * nz + org[2];
+                    for (int kk = 0; kk < ext[2]; kk++, p++) { row[kk] = rb[p]; s += f2w(rb[p]); }
+                }
+            if (has && s != rd64(data + P.si.sumdc_off + 8 * b)) {
+                /* _reexecute_block (pipeline.py:713-723): decode + reconstruct again, no hook */
+                decode_block(&T, pay, (uint64_t)P.si.payload_len, bofs[b], P.blen[b], vol, bb, &a, &c2);
+                reconstruct_block(&q, bb, unp_all + uofs[b], ext, P.ind[b], c, rb, Pb);
+                uint64_t s2 = 0;
+                p = 0;
+                for (int i = 0; i < ext[0]; i++)
+                    for (int j = 0; j < ext[1]; j++) {
+                        float* row = out + ((org[0] + i) * ny + org[1] + j) * nz + org[2];
+                        for (int kk = 0; kk < ext[2]; kk++, p++) { row[kk] = rb[p]; s2 += f2w(rb[p]); }
+                    }
+                mism[b] = s2 == rd64(data + P.si.sumdc_off + 8 * b) ? 1 : 2;
+            }
+        }
+        free(bb); free(rb); free(Pb);
+    }
+    /* lowest undecodable block wins (pipeline.py:673-677) */
+    for (int64_t b = 0; b < nb; b++)
+        if (dkind[b]) {
+            rep->sdc = 1;
+            set_info(&rep->info, FTLZ_OK, dkind[b], -1, b, da[b], db[b]);
+            goto finish;
+        }
+    {
+        /* verification walks extent groups in sorted order, ids ascending (pipeline.py:692-708) */
+        uint8_t* fail = (uint8_t*)calloc((size_t)nb, 1);
+        for (int64_t b = 0; b < nb; b++) fail[b] = mism[b] == 2;
+        int64_t fb = first_in_group_order(&g, fail);
+        uint8_t* ok = (uint8_t*)calloc((size_t)nb, 1);
+        if (fb >= 0) {
+            int64_t org[3]; int fext[3];
+            block_geom(&g, fb, org, fext);
+            for (int64_t b = 0; b < nb; b++) {
+                if (mism[b] != 1) continue;
+                int ext[3];
+                block_geom(&g, b, org, ext);
+                int c = ext_cmp(ext, fext);
+                if (c < 0 || (c == 0 && b < fb)) ok[b] = 1;
+            }
+            rep->sdc = 1;
+            set_info(&rep->info, FTLZ_OK, FTLZ_K_D_MISMATCH, -1, fb, 0, 0);
+        } else {
+            for (int64_t b = 0; b < nb; b++) ok[b] = mism[b] == 1;
+        }
+        emit_list(rep->reexecuted, rep->capacity, &rep->n_reexecuted, ok, nb);
+        free(fail); free(ok);
+    }
+finish:
+    free((void*)unp_all); free(bofs); free(uofs); free(dkind); free(da); free(db); free(mism);
+    free(T.sym_sorted);
+    parsed_free(&P);
+    rep->info.code = FTLZ_OK;
+    return FTLZ_OK;
+}
+
+int oc_version(void) { return 1; }

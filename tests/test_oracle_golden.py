@@ -1,0 +1,65 @@
+"""Pin the CPU oracle (oracle/ftlz_oracle.c) against the reference's own outputs.
+
+Every fixture in tests/golden was produced by running the reference Python package
+(tools/make_golden.py).  The oracle must reproduce each archive byte-for-byte, every
+report list, every decompressed word and every exception class + message.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.golden_util import faults_of, load, manifest, override_of, sha
+
+M = manifest()
+
+
+@pytest.mark.parametrize("name", sorted(M["cases"]))
+def test_oracle_compress_decompress_matches_reference(name):
+    e = M["cases"][name]
+    z = load(name)
+    x = z["input"]
+    assert sha(x) == e["input_sha256"]
+    faults = faults_of(e)
+    if "compress_error" in e:
+        with pytest.raises(O.OracleError) as ei:
+            O.compress(x, e["mode"], e["value"], e["cfg"], faults, override_of(e))
+        assert ei.value.cls == e["compress_error"]["cls"]
+        assert str(ei.value) == e["compress_error"]["msg"]
+        return
+    data, rep = O.compress(x, e["mode"], e["value"], e["cfg"], faults, override_of(e))
+    assert data == z["archive"].tobytes()
+    for k in ("status", "input_corrected", "bins_corrected", "dup_mismatch_resolved",
+              "decomp_block_reexecuted", "detail"):
+        assert rep[k] == e["compress_report"][k], k
+    out, drep = O.decompress(data, faults)
+    for k in ("status", "decomp_block_reexecuted", "detail"):
+        assert drep[k] == e["decompress_report"][k], k
+    if "output_sha256" in e:
+        assert out is not None and sha(out) == e["output_sha256"]
+        np.testing.assert_array_equal(out.view(np.uint32), z["output"].view(np.uint32))
+    else:
+        assert out is None
+
+
+def _corrupt_cases():
+    for src, cases in sorted(M["corrupt"].items()):
+        for name in sorted(cases):
+            yield src, name
+
+
+@pytest.mark.parametrize("src,name", list(_corrupt_cases()))
+def test_oracle_parse_and_sdc_match_reference(src, name):
+    e = M["corrupt"][src][name]
+    blob = load(f"corrupt_{src}")[name].tobytes()
+    assert sha(np.frombuffer(blob, np.uint8)) == e["sha256"]
+    if "error" in e:
+        with pytest.raises(O.OracleError) as ei:
+            O.decompress(blob)
+        assert ei.value.cls == e["error"]["cls"]
+        assert str(ei.value) == e["error"]["msg"]
+        return
+    out, rep = O.decompress(blob)
+    for k in ("status", "decomp_block_reexecuted", "detail"):
+        assert rep[k] == e["decompress_report"][k], k
+    assert (None if out is None else sha(out)) == e["output_sha256"]

@@ -1,0 +1,373 @@
+"""Generate tests/golden/ by running the reference `ftlz` package (Python) in this container.
+
+    PYTHONPATH=/root/reference/pkg/src python tools/make_golden.py [--large]
+
+The reference cannot travel to the GPU box, so its outputs are committed as fixtures:
+  tests/golden/<case>.npz   input field, archive bytes, decompressed output (small cases)
+  tests/golden/manifest.json  per case: request, config, faults, expected reports/errors,
+                              SHA-256 of input / archive / output (all cases)
+`--large` adds the BASELINE configs c1..c5 at full size (hash-only; c3 takes minutes).
+
+Faults are applied through the reference's own hook seam with the semantics of
+faults.py:157-189 (one XOR per (block, element, bit); decomp hook armed once=True).
+"""
+
+from __future__ import annotations
+
+import argparse
+import hashlib
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+
+import ftlz  # noqa: E402
+from ftlz import hooks  # noqa: E402
+from ftlz.errors import FtlzError  # noqa: E402
+
+from tools import synth  # noqa: E402
+
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden")
+
+
+def sha(buf) -> str:
+    return hashlib.sha256(memoryview(np.ascontiguousarray(buf)).cast("B")).hexdigest()
+
+
+def cfg_obj(cfg: dict):
+    base = dict(protect_input=True, protect_bins=True, duplicate_eval=True, store_sum_dc=True,
+                block_edge=10)
+    base.update(cfg)
+    cap = base.pop("bin_capacity", None)
+    if cap is not None:
+        base["quant"] = ftlz.QuantConfig(cap)
+    return ftlz.FtConfig(**base)
+
+
+def run_compress(values, mode, value, cfg, faults, override):
+    field = ftlz.Field.from_array(values)
+    eb = ftlz.ErrorBound(mode, value)
+    armed = []
+    byt = {}
+    for t, b, e, bit in faults:
+        byt.setdefault(t, []).append((b, e, bit))
+
+    def h_input(working, grid):
+        for b, e, bit in byt["input"]:
+            i, j, k = grid.cell_of_block(b, e)
+            working[i, j, k: k + 1].view(np.uint32)[0] ^= np.uint32(1 << bit)
+
+    def h_bins(bins_list, grid):
+        for b, e, bit in byt["bins"]:
+            bins_list[b][e] ^= np.uint32(1 << bit)
+
+    def h_coef(coeffs_all, grid):
+        for b, e, bit in byt["regression"]:
+            coeffs_all[b: b + 1].view(np.uint32)[0, e] ^= np.uint32(1 << bit)
+
+    def h_est(est_reg, est_lor):
+        for b, e, bit in byt["sampling"]:
+            arr = est_reg if e == 0 else est_lor
+            arr[b: b + 1].view(np.uint64)[0] ^= np.uint64(1 << bit)
+
+    if "input" in byt:
+        hooks.arm(hooks.STAGE_INPUT_AFTER_CHECKSUM, h_input)
+    if "bins" in byt:
+        hooks.arm(hooks.STAGE_BINS_FINALIZED, h_bins)
+    if "regression" in byt:
+        hooks.arm(hooks.STAGE_COEFFS_FITTED, h_coef)
+    if "sampling" in byt:
+        hooks.arm(hooks.STAGE_ESTIMATES, h_est)
+    try:
+        ov = None
+        if override:
+            ov = {int(b): ftlz.PredictorKind(int(k)) for b, k in override.items()}
+        stream, rep = ftlz.compress(field, eb, cfg_obj(cfg), predictor_override=ov)
+        return ftlz.serialize(stream), rep.to_dict(), None
+    except FtlzError as exc:
+        return None, None, {"cls": type(exc).__name__, "msg": str(exc)}
+    finally:
+        hooks.disarm_all()
+        del armed
+
+
+def run_decompress(data, faults):
+    dec = [(b, e, bit) for t, b, e, bit in faults if t == "decomp"]
+    try:
+        stream = ftlz.parse(data)
+    except FtlzError as exc:
+        return None, None, {"cls": type(exc).__name__, "msg": str(exc)}
+
+    def h_dec(out, grid):
+        for b, e, bit in dec:
+            i, j, k = grid.cell_of_block(b, e)
+            out[i, j, k: k + 1].view(np.uint32)[0] ^= np.uint32(1 << bit)
+
+    if dec:
+        hooks.arm(hooks.STAGE_DECOMP_BEFORE_VERIFY, h_dec, once=True)
+    try:
+        out, rep = ftlz.decompress(stream)
+    finally:
+        hooks.disarm_all()
+    return (None if out is None else np.array(out.values)), rep.to_dict(), None
+
+
+def small_cases():
+    S = ftlz.synth_field
+    cases = []
+
+    def add(name, values, mode, value, cfg=None, faults=(), override=None, extra=None):
+        # keep every fault inside its block (faults.py:_pick draws element < volume)
+        vols = synth.block_volumes(np.shape(values), (cfg or {}).get("block_edge", 10))
+        faults = [(t, b, e % (4 if t == "regression" else 2 if t == "sampling" else int(vols[b])),
+                   bit) for t, b, e, bit in faults]
+        cases.append(dict(name=name, values=np.ascontiguousarray(values, np.float32), mode=mode,
+                          value=value, cfg=cfg or {}, faults=list(faults), override=override,
+                          extra=extra or {}))
+
+    A, R = "absolute", "value_range_relative"
+    # test_pipeline.py:78-104 awkward dims with edge 5
+    for kind, ebv in (("mixed", 1e-3), ("noise", 1e-4), ("sine", 1e-2)):
+        add(f"pipe_{kind}_13x11x10_e5", S(kind, (13, 11, 10), seed=31).values, A, ebv,
+            {"block_edge": 5})
+    add("payload_14x10x9_e4", S("mixed", (14, 10, 9), seed=8).values, A, 1e-3, {"block_edge": 4})
+    add("constant_40", S("constant", (40, 40, 40), seed=1).values, A, 1e-3)
+    add("degenerate_rel_constant", S("constant", (12, 12, 12), seed=1).values, R, 1e-3)
+    add("flat2d_1x32x24", S("mixed", (1, 32, 24), seed=19).values, A, 1e-3)
+    add("relative_sine_16", S("sine", (16, 16, 16), seed=9).values, R, 1e-3)
+    add("transparency_on_24x20x22", S("mixed", (24, 20, 22), seed=3).values, A, 1e-2)
+    add("transparency_off_24x20x22", S("mixed", (24, 20, 22), seed=3).values, A, 1e-2,
+        {"protect_input": False, "protect_bins": False, "duplicate_eval": False,
+         "store_sum_dc": False})
+    add("noise_16_e8_1e-4", S("noise", (16, 16, 16), seed=7).values, A, 1e-4, {"block_edge": 8})
+    add("noise_20_1e-6_bigalphabet", S("noise", (20, 20, 20), seed=5).values, A, 1e-6)
+    add("mixed_12x9x7_e4_unprot", S("mixed", (12, 9, 7), seed=21).values, A, 1e-3,
+        {"block_edge": 4, "protect_input": False, "protect_bins": False,
+         "duplicate_eval": False, "store_sum_dc": False})
+    add("sine_20_e2", S("sine", (20, 20, 20), seed=2).values, A, 1e-3, {"block_edge": 2})
+    add("mixed_33x17x70_e16", S("mixed", (33, 17, 70), seed=4).values, R, 1e-4, {"block_edge": 16})
+    add("mixed_20x20x20_e64", S("mixed", (20, 20, 20), seed=4).values, A, 1e-3, {"block_edge": 64})
+    add("cap_256_noise", S("noise", (16, 16, 16), seed=3).values, A, 1e-2, {"bin_capacity": 256})
+    # lognormal with wide dynamic range (regression-heavy, like c3) at reduced size
+    g = synth.grf((32, 32, 48), 2.5, 11)
+    add("lognormal_32x32x48", np.exp(g), R, 1e-3)
+    add("grf2d_1x90x180", (synth.grf((90, 180), 3.0, 4, std=5.0) + 250.0).reshape(1, 90, 180), R, 1e-4)
+    # special values (absolute bound): NaN / inf / -0.0 / huge / subnormal
+    rng = np.random.default_rng(77)
+    sp = rng.standard_normal((15, 14, 13)).astype(np.float32)
+    sp[0, 0, :] = -0.0
+    sp[:10, :10, :10][3, 3, 3] = np.nan
+    sp[11, 2, 7] = np.inf
+    sp[12, 5, 1] = -np.inf
+    sp[4, 13, 12] = 3.0e38
+    sp[5, 5, 5] = 1e-42
+    sp[10:, 10:, 10:] = -0.0   # an all-negative-zero block
+    add("special_values_abs", sp, A, 1e-3)
+    add("special_values_rel", sp, R, 1e-3)
+    # fault injection through the hook seam (faults.py:157-189)
+    base = S("mixed", (16, 14, 12), seed=2).values
+    fa = [("input", 3, 17, 30), ("input", 7, 0, 5), ("input", 20, 99, 31)]
+    add("fault_input_protected", base, A, 1e-3, {"block_edge": 5}, fa)
+    add("fault_input_unprotected", base, A, 1e-3, {"block_edge": 5, "protect_input": False}, fa)
+    fb = [("bins", 1, 4, 3), ("bins", 9, 60, 17), ("bins", 22, 0, 31)]
+    add("fault_bins_protected", base, A, 1e-3, {"block_edge": 5}, fb)
+    add("fault_bins_unprotected_range", base, A, 1e-3, {"block_edge": 5, "protect_bins": False}, fb)
+    add("fault_bins_unprotected_low", base, A, 1e-3, {"block_edge": 5, "protect_bins": False},
+        [("bins", 4, 10, 1), ("bins", 11, 3, 0)])
+    add("fault_bins_double_uncorrectable", base, A, 1e-3, {"block_edge": 5},
+        [("bins", 6, 2, 1), ("bins", 6, 9, 4)])
+    add("fault_input_double_uncorrectable", base, A, 1e-3, {"block_edge": 5},
+        [("input", 8, 2, 1), ("input", 8, 9, 4), ("input", 2, 5, 6), ("input", 2, 6, 6)])
+    add("fault_coeff", base, A, 1e-3, {"block_edge": 5},
+        [("regression", 0, 0, 30), ("regression", 5, 1, 22), ("regression", 13, 3, 2)])
+    add("fault_estimate", base, A, 1e-3, {"block_edge": 5},
+        [("sampling", 2, 0, 62), ("sampling", 4, 1, 63), ("sampling", 17, 0, 10)])
+    add("fault_decomp_protected", base, A, 1e-3, {"block_edge": 5},
+        [("decomp", 3, 10, 22), ("decomp", 12, 0, 31), ("decomp", 30, 124, 0)])
+    add("fault_decomp_unprotected", base, A, 1e-3,
+        {"block_edge": 5, "protect_input": False, "protect_bins": False,
+         "duplicate_eval": False, "store_sum_dc": False},
+        [("decomp", 3, 10, 30)])
+    add("override_mix", S("mixed", (20, 15, 10), seed=14).values, A, 1e-3, {"block_edge": 5},
+        override={0: 1, 3: 0, 7: 1, 11: 0, 23: 1})
+    # c5-style plan at reduced size: 10% of blocks, bits 0..31, three targets
+    c5v = S("mixed", (30, 30, 30), seed=5).values
+    vols = synth.block_volumes((30, 30, 30), 10)
+    plan = synth.fault_plan(len(vols), vols, seed=12345, frac=0.1)
+    for tgt in ("input", "bins", "decomp"):
+        add(f"c5mini_{tgt}", c5v, R, 1e-3, {}, [(tgt, b, e, t) for b, e, t in plan])
+    # the full c1 config (64^3, relative 1e-3)
+    add("c1", synth.c1(), R, 1e-3)
+    return cases
+
+
+def corrupt_cases(archive: bytes):
+    """(name, bytes) variants of a valid archive for parse/decompress error parity."""
+    out = []
+    n = len(archive)
+    cuts = sorted(set([0, 1, 4, 30, 54, 55, 56, 60, 100, n // 3, n // 2, n - 30, n - 17, n - 16,
+                       n - 9, n - 8, n - 1]))
+    for c in cuts:
+        if 0 <= c < n:
+            out.append((f"cut_{c}", archive[:c]))
+    out.append(("trailing", archive + b"\x00"))
+    b = bytearray(archive); b[0:4] = b"XTLZ"; out.append(("magic", bytes(b)))
+    b = bytearray(archive); b[4] = 99; out.append(("version", bytes(b)))
+    b = bytearray(archive); b[6:14] = (0).to_bytes(8, "little"); out.append(("dims", bytes(b)))
+    b = bytearray(archive); b[30:34] = (1).to_bytes(4, "little"); out.append(("edge", bytes(b)))
+    b = bytearray(archive); b[34] = 7; out.append(("mode", bytes(b)))
+    b = bytearray(archive); b[35:43] = np.float64(-1.0).tobytes(); out.append(("eb", bytes(b)))
+    b = bytearray(archive); b[35:43] = np.float64(np.inf).tobytes(); out.append(("eb_inf", bytes(b)))
+    b = bytearray(archive); b[43:47] = (1000).to_bytes(4, "little"); out.append(("cap", bytes(b)))
+    b = bytearray(archive); b[47:55] = (999).to_bytes(8, "little"); out.append(("count", bytes(b)))
+    b = bytearray(archive); b[55] = 2; out.append(("indicator0", bytes(b)))
+    b = bytearray(archive); b[5] = 9; out.append(("codec", bytes(b)))
+    return out
+
+
+def payload_flip_cases(archive: bytes, stream):
+    table = sum(9 + (16 if r.predictor == 1 else 0) for r in stream.records)
+    book = 4 + 5 * len(stream.code_lengths)
+    off = 55 + table + book + 8
+    plen = len(stream.payload)
+    res = []
+    for pos in sorted(set(np.linspace(0, plen - 1, 12).astype(int).tolist())):
+        b = bytearray(archive)
+        b[off + pos] ^= 0xFF
+        res.append((f"payflip_{pos}", bytes(b)))
+    # codebook damage: swap first two symbols, bad length, kraft
+    boff = 55 + table
+    b = bytearray(archive); b[boff + 4: boff + 8] = (70000).to_bytes(4, "little")
+    res.append(("book_symrange", bytes(b)))
+    b = bytearray(archive); b[boff + 8] = 0
+    res.append(("book_len0", bytes(b)))
+    b = bytearray(archive); b[boff + 8] = 60
+    res.append(("book_len60", bytes(b)))
+    b = bytearray(archive)
+    for t in range(min(4, len(stream.code_lengths))):
+        b[boff + 4 + 5 * t + 4] = 1
+    res.append(("book_kraft", bytes(b)))
+    b = bytearray(archive); b[boff + 4 + 5: boff + 4 + 9] = (0).to_bytes(4, "little")
+    res.append(("book_order", bytes(b)))
+    # sum_dc section lengths
+    b = bytearray(archive); b[-8 * len(stream.records) - 16] ^= 1
+    res.append(("sumdc_rawlen", bytes(b)))
+    b = bytearray(archive); b[-8 * len(stream.records) - 8] ^= 1
+    res.append(("sumdc_storedlen", bytes(b)))
+    # sum_dc value flip -> re-execution cannot fix -> terminal SDC at that block
+    b = bytearray(archive); b[-8 * 3] ^= 0x10
+    res.append(("sumdc_value", bytes(b)))
+    # record bit_length/unpred_count tampering
+    b = bytearray(archive); b[55 + 1 + (16 if stream.records[0].predictor else 0)] ^= 1
+    res.append(("rec0_unpred", bytes(b)))
+    b = bytearray(archive); b[55 + 5 + (16 if stream.records[0].predictor else 0)] ^= 1
+    res.append(("rec0_bitlen", bytes(b)))
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--large", action="store_true")
+    ap.add_argument("--only", default=None)
+    args = ap.parse_args()
+    os.makedirs(OUT, exist_ok=True)
+    mpath = os.path.join(OUT, "manifest.json")
+    manifest = json.load(open(mpath)) if os.path.exists(mpath) else {"cases": {}, "corrupt": {}, "large": {}}
+    manifest["generator"] = {"numpy": np.__version__, "ftlz": ftlz.__version__,
+                             "script": "tools/make_golden.py"}
+    if not args.large:
+        for c in small_cases():
+            if args.only and args.only not in c["name"]:
+                continue
+            t0 = time.time()
+            data, crep, cerr = run_compress(c["values"], c["mode"], c["value"], c["cfg"],
+                                            c["faults"], c["override"])
+            entry = {k: c[k] for k in ("mode", "value", "cfg", "faults")}
+            entry["override"] = {str(k): v for k, v in (c["override"] or {}).items()}
+            entry["dims"] = list(c["values"].shape)
+            entry["input_sha256"] = sha(c["values"])
+            arrays = {"input": c["values"]}
+            if cerr:
+                entry["compress_error"] = cerr
+            else:
+                entry["archive_sha256"] = sha(np.frombuffer(data, np.uint8))
+                entry["archive_len"] = len(data)
+                entry["compress_report"] = crep
+                arrays["archive"] = np.frombuffer(data, np.uint8)
+                out, drep, derr = run_decompress(data, c["faults"])
+                entry["decompress_report"] = drep
+                if out is not None:
+                    entry["output_sha256"] = sha(out)
+                    arrays["output"] = out
+            np.savez_compressed(os.path.join(OUT, c["name"] + ".npz"), **arrays)
+            manifest["cases"][c["name"]] = entry
+            print(c["name"], f"{time.time() - t0:.2f}s", entry.get("archive_len"), cerr or "")
+        # parse / decompress error parity on two archives (protected + unprotected)
+        for src in ("payload_14x10x9_e4", "pipe_noise_13x11x10_e5", "mixed_12x9x7_e4_unprot"):
+            z = np.load(os.path.join(OUT, src + ".npz"))
+            arch = z["archive"].tobytes()
+            stream = ftlz.parse(arch)
+            variants = corrupt_cases(arch) + payload_flip_cases(arch, stream)
+            res = {}
+            blobs = {}
+            for name, blob in variants:
+                out, drep, derr = run_decompress(blob, [])
+                r = {"len": len(blob), "sha256": sha(np.frombuffer(blob, np.uint8))}
+                if derr:
+                    r["error"] = derr
+                else:
+                    r["decompress_report"] = drep
+                    r["output_sha256"] = None if out is None else sha(out)
+                res[name] = r
+                blobs[name] = np.frombuffer(blob, np.uint8)
+            manifest["corrupt"][src] = res
+            np.savez_compressed(os.path.join(OUT, f"corrupt_{src}.npz"), **blobs)
+            print("corrupt", src, len(res))
+    else:
+        for name in ("c1", "c4", "c2", "c2_1e-4", "c3", "c5"):
+            if args.only and args.only != name:
+                continue
+            t0 = time.time()
+            f = synth.field(name)
+            mode, v = synth.CONFIGS[name]["eb"]
+            entry = {"dims": list(f.shape), "mode": mode, "value": v, "input_sha256": sha(f)}
+            if name == "c5":
+                vols = synth.block_volumes(f.shape, 10)
+                plan = synth.fault_plan(len(vols), vols)
+                entry["plan_sha256"] = hashlib.sha256(json.dumps(plan).encode()).hexdigest()
+                entry["n_faults"] = len(plan)
+                for tgt in ("input", "bins", "decomp"):
+                    fl = [(tgt, b, e, t) for b, e, t in plan]
+                    data, crep, cerr = run_compress(f, mode, v, {}, fl, None)
+                    out, drep, _ = run_decompress(data, fl)
+                    entry[tgt] = {"archive_sha256": sha(np.frombuffer(data, np.uint8)),
+                                  "archive_len": len(data),
+                                  "n_input_corrected": len(crep["input_corrected"]),
+                                  "n_bins_corrected": len(crep["bins_corrected"]),
+                                  "input_corrected_sha256": hashlib.sha256(json.dumps(crep["input_corrected"]).encode()).hexdigest(),
+                                  "bins_corrected_sha256": hashlib.sha256(json.dumps(crep["bins_corrected"]).encode()).hexdigest(),
+                                  "n_reexecuted": len(drep["decomp_block_reexecuted"]),
+                                  "reexecuted_sha256": hashlib.sha256(json.dumps(drep["decomp_block_reexecuted"]).encode()).hexdigest(),
+                                  "status_c": crep["status"], "status_d": drep["status"],
+                                  "output_sha256": None if out is None else sha(out)}
+                    print(name, tgt, entry[tgt], flush=True)
+            else:
+                data, crep, cerr = run_compress(f, mode, v, {}, [], None)
+                out, drep, _ = run_decompress(data, [])
+                entry.update({"archive_sha256": sha(np.frombuffer(data, np.uint8)),
+                              "archive_len": len(data), "compress_report": crep,
+                              "decompress_report": drep, "output_sha256": sha(out)})
+            entry["seconds"] = round(time.time() - t0, 1)
+            manifest["large"][name] = entry
+            json.dump(manifest, open(mpath, "w"), indent=1, sort_keys=True)
+            print(name, entry.get("archive_len"), entry["seconds"], flush=True)
+    json.dump(manifest, open(mpath, "w"), indent=1, sort_keys=True)
+
+
+if __name__ == "__main__":
+    main()
