@@ -1,0 +1,1076 @@
+// api.cu -- host runtime behind the C ABI (include/ftlz_b200.h).
+//
+// Unity build: the compress and decompress kernels are included here so that launch code and
+// argument structs share one translation unit.  No CPU fallback exists: every entry point
+// fails with FTLZ_ERR_CUDA when no device is usable.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "compress.cu"
+#include "decompress.cu"
+
+using namespace ftlz;
+
+// ------------------------------------------------------------------------------------------
+static thread_local std::string g_err;
+
+static int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define LCHK(name)                                                                               \
+    do {                                                                                         \
+        cudaError_t e_ = cudaGetLastError();                                                     \
+        if (e_ != cudaSuccess) return set_err(FTLZ_ERR_CUDA, std::string("launch ") + name + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define CK(x)                                                                                    \
+    do {                                                                                         \
+        cudaError_t e_ = (x);                                                                    \
+        if (e_ != cudaSuccess)                                                                   \
+            return set_err(FTLZ_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));    \
+    } while (0)
+
+static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+extern "C" int ftlz_abi_version(void) { return FTLZ_ABI_VERSION; }
+extern "C" const char* ftlz_last_error(void) { return g_err.c_str(); }
+extern "C" void ftlz_default_config(ftlz_config* c) {
+    c->protect_input = c->protect_bins = c->duplicate_eval = c->store_sum_dc = 1;
+    c->block_edge = 10;
+    c->codec_id = 0;
+    c->bin_capacity = 65536;
+    c->reserved = 0;
+}
+
+extern "C" int64_t ftlz_block_count(int64_t nx, int64_t ny, int64_t nz, int32_t e) {
+    if (nx < 1 || ny < 1 || nz < 1 || e < 2 || e > 64) return -1;
+    return ((nx + e - 1) / e) * ((ny + e - 1) / e) * ((nz + e - 1) / e);
+}
+
+static void info_set(ftlz_info* in, int code, int kind, int64_t off, int64_t blk, int64_t a, int64_t b) {
+    in->code = code; in->kind = kind; in->offset = off; in->block = blk; in->a = a; in->b = b;
+}
+
+// header validation in the reference order (container.py:189-210)
+extern "C" int ftlz_peek_header(const uint8_t* d, size_t len, ftlz_header* h, ftlz_info* info) {
+    info_set(info, FTLZ_OK, 0, -1, -1, 0, 0);
+    auto fail = [&](int kind, int64_t off, int64_t a) {
+        info_set(info, FTLZ_ERR_CORRUPT_STREAM, kind, off, -1, a, 0);
+        return FTLZ_ERR_CORRUPT_STREAM;
+    };
+    if (len < 55) return fail(FTLZ_K_TRUNCATED, 0, FTLZ_F_HEADER);
+    uint64_t nx, ny, nz, nb;
+    uint32_t edge, cap;
+    double eb;
+    memcpy(&nx, d + 6, 8); memcpy(&ny, d + 14, 8); memcpy(&nz, d + 22, 8);
+    memcpy(&edge, d + 30, 4); memcpy(&eb, d + 35, 8); memcpy(&cap, d + 43, 4); memcpy(&nb, d + 47, 8);
+    if (memcmp(d, "FTLZ", 4) != 0) return fail(FTLZ_K_BAD_MAGIC, 0, 0);
+    if (d[4] != 1) return fail(FTLZ_K_BAD_VERSION, 4, d[4]);
+    if (nx < 1 || ny < 1 || nz < 1) return fail(FTLZ_K_BAD_DIMS, 6, 0);
+    if (edge < 2 || edge > 64) return fail(FTLZ_K_BAD_EDGE, 30, edge);
+    if (d[34] > 1) return fail(FTLZ_K_BAD_MODE, 34, d[34]);
+    if (!(eb > 0.0 && std::isfinite(eb))) return fail(FTLZ_K_BAD_EB, 35, 0);
+    if (cap < 4 || (cap & (cap - 1))) return fail(FTLZ_K_BAD_CAPACITY, 43, cap);
+    unsigned __int128 expect = 1;
+    bool over = false;
+    uint64_t dd[3] = {nx, ny, nz};
+    for (int i = 0; i < 3; i++) {
+        expect *= (unsigned __int128)(dd[i] / edge + (dd[i] % edge != 0));
+        if (expect >> 64) over = true;
+    }
+    if (over || (uint64_t)expect != nb) return fail(FTLZ_K_BLOCK_COUNT, 47, (int64_t)nb);
+    h->version = d[4];
+    h->codec_id = d[5];
+    h->nx = (int64_t)nx; h->ny = (int64_t)ny; h->nz = (int64_t)nz;
+    h->block_edge = (int32_t)edge;
+    h->eb_mode = d[34];
+    h->eb_value = eb;
+    h->bin_capacity = cap;
+    h->reserved = 0;
+    h->block_count = (int64_t)nb;
+    return FTLZ_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// per-geometry plans: pairwise-sum leaves, coordinates, wavefront order (host built)
+struct HostPlan {
+    Geom g;
+    ExtPlan ep[8];
+    std::vector<Leaf> leaves;
+    std::vector<uint32_t> coords, wave, planes;
+    size_t bytes() const {
+        return al256(sizeof(ep)) + al256(leaves.size() * sizeof(Leaf) + 16) + al256(coords.size() * 4 + 16) +
+               al256(wave.size() * 4 + 16) + al256(planes.size() * 4 + 16);
+    }
+};
+
+static void pw_leaves(int start, int n, std::vector<Leaf>& L) {
+    // numpy pairwise_sum split (PW_BLOCKSIZE 128): leaves in order, combine after right subtree
+    if (n <= 128) {
+        L.push_back(Leaf{start, n, 0, 0});
+        return;
+    }
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    pw_leaves(start, n2, L);
+    pw_leaves(start + n2, n - n2, L);
+    L.back().ncomb += 1;
+}
+
+static bool build_plan(int64_t nx, int64_t ny, int64_t nz, int e, HostPlan& P) {
+    if (nx < 1 || ny < 1 || nz < 1 || e < 2 || e > 64) return false;
+    Geom& g = P.g;
+    g.nx = nx; g.ny = ny; g.nz = nz; g.e = e;
+    g.cx = (nx + e - 1) / e; g.cy = (ny + e - 1) / e; g.cz = (nz + e - 1) / e;
+    g.nb = g.cx * g.cy * g.cz;
+    g.rx = (int)(nx - (g.cx - 1) * e); g.ry = (int)(ny - (g.cy - 1) * e); g.rz = (int)(nz - (g.cz - 1) * e);
+    int mx = (int)std::min<int64_t>(e, nx), my = (int)std::min<int64_t>(e, ny), mz = (int)std::min<int64_t>(e, nz);
+    g.vmax = mx * my * mz;
+    g.nvmax8 = (g.vmax + 7) & ~7;
+    P.leaves.clear(); P.coords.clear(); P.wave.clear(); P.planes.clear();
+    for (int xid = 0; xid < 8; xid++) {
+        ExtPlan& E = P.ep[xid];
+        memset(&E, 0, sizeof E);
+        E.bx = (xid & 4) ? g.rx : e; E.by = (xid & 2) ? g.ry : e; E.bz = (xid & 1) ? g.rz : e;
+        if (E.bx > mx) E.bx = mx;
+        if (E.by > my) E.by = my;
+        if (E.bz > mz) E.bz = mz;
+        int vol = E.bx * E.by * E.bz;
+        E.vol = vol;
+        E.leaf_off = (int)P.leaves.size();
+        if (vol >= 8) pw_leaves(0, vol, P.leaves);
+        E.nleaf = (int)P.leaves.size() - E.leaf_off;
+        E.ns = (vol - 1) / 8;
+        E.sleaf_off = (int)P.leaves.size();
+        if (E.ns >= 8) pw_leaves(0, E.ns, P.leaves);
+        E.nsleaf = (int)P.leaves.size() - E.sleaf_off;
+        E.coord_off = (int)P.coords.size();
+        for (int i = 0; i < E.bx; i++)
+            for (int j = 0; j < E.by; j++)
+                for (int k = 0; k < E.bz; k++) P.coords.push_back((uint32_t)i | ((uint32_t)j << 8) | ((uint32_t)k << 16));
+        E.nplanes = E.bx + E.by + E.bz - 2;
+        E.wave_off = (int)P.wave.size();
+        E.plane_off = (int)P.planes.size();
+        std::vector<std::vector<uint32_t>> byplane(E.nplanes);
+        int p = 0;
+        for (int i = 0; i < E.bx; i++)
+            for (int j = 0; j < E.by; j++)
+                for (int k = 0; k < E.bz; k++, p++) byplane[i + j + k].push_back((uint32_t)p);
+        uint32_t acc = 0;
+        for (int s = 0; s < E.nplanes; s++) {
+            P.planes.push_back(acc);
+            for (uint32_t q : byplane[s]) P.wave.push_back(q);
+            acc += (uint32_t)byplane[s].size();
+        }
+        P.planes.push_back(acc);
+    }
+    return true;
+}
+
+struct DevPlan {
+    const ExtPlan* ep;
+    const Leaf* leaves;
+    const u32* coords;
+    const u32* wave;
+    const u32* planes;
+};
+
+// upload plan tables into `dst` (device), returns pointers
+static int upload_plan(const HostPlan& P, unsigned char* dst, DevPlan& D, cudaStream_t s, std::vector<unsigned char>& staging) {
+    size_t off = 0;
+    staging.assign(P.bytes(), 0);
+    auto put = [&](const void* src, size_t n) {
+        size_t o = off;
+        memcpy(staging.data() + o, src, n);
+        off += al256(n + 16);
+        return o;
+    };
+    off = 0;
+    size_t o_ep = 0;
+    memcpy(staging.data(), P.ep, sizeof(P.ep));
+    off = al256(sizeof(P.ep));
+    size_t o_l = put(P.leaves.data(), P.leaves.size() * sizeof(Leaf));
+    size_t o_c = put(P.coords.data(), P.coords.size() * 4);
+    size_t o_w = put(P.wave.data(), P.wave.size() * 4);
+    size_t o_p = put(P.planes.data(), P.planes.size() * 4);
+    CK(cudaMemcpyAsync(dst, staging.data(), off, cudaMemcpyHostToDevice, s));
+    D.ep = (const ExtPlan*)(dst + o_ep);
+    D.leaves = (const Leaf*)(dst + o_l);
+    D.coords = (const u32*)(dst + o_c);
+    D.wave = (const u32*)(dst + o_w);
+    D.planes = (const u32*)(dst + o_p);
+    return FTLZ_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// kernel configuration (shared memory per block slot, blocks per CTA)
+static size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+struct KCfg {
+    int P;
+    size_t slot;
+    size_t smem;
+};
+
+static KCfg kcfg_comp(const Geom& g) {
+    size_t v = (size_t)g.vmax;
+    size_t prep = al16(4 * v) + 8 * v + 8 * 4 * (v / 64 + 8) + 8 * 2 * (v / 8 + 8);
+    size_t quant = al16(4 * v) + 8 * v + 2 * v + 16 + 3 * 64 * 8;
+    KCfg k;
+    k.slot = al16(std::max(prep, quant));
+    k.P = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / k.slot));
+    k.smem = k.slot * k.P;
+    return k;
+}
+
+static int kernel_attrs_once() {
+    static std::once_flag fl;
+    static int rc = FTLZ_OK;
+    std::call_once(fl, [] {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) { rc = FTLZ_ERR_CUDA; return; }
+        int maxs = 0;
+        cudaDeviceGetAttribute(&maxs, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        auto setmax = [&](const void* fn) {
+            cudaFuncAttributes fa;
+            if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess) { rc = FTLZ_ERR_CUDA; return; }
+            if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     maxs - (int)fa.sharedSizeBytes) != cudaSuccess)
+                rc = FTLZ_ERR_CUDA;
+        };
+        setmax((const void*)k_prep);
+        setmax((const void*)k_quant);
+        setmax((const void*)k_codebook);
+        setmax((const void*)k_parse_tail);
+        setmax((const void*)k_decode);
+        setmax((const void*)k_recon_warp);
+        if (cudaGetLastError() != cudaSuccess) rc = FTLZ_ERR_CUDA;
+    });
+    return rc;
+}
+
+static int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+// ------------------------------------------------------------------------------------------
+// compress workspace layout
+struct CompLayout {
+    size_t result;       // DevStatus | minmax[4] | counters[16] | layout[16]  (zeroed)
+    size_t zero_end;
+    size_t hist, lbflag, events, fixed;
+    size_t coef, insum, inisum, ind, unpc, bsum, bisum, dcs, bitlen, regpre, unppre;
+    size_t enc, qp, lbbits, lbreg, lbunp;
+    size_t cb_keys, cb_syms, cb_w, cb_parent, cb_lens;
+    size_t bins, unp, fix, faults, ffirst, ovr, plan;
+    size_t total;
+};
+
+static const size_t RESULT_BYTES = 512;
+
+static CompLayout comp_layout(const HostPlan& P, int cap, int64_t n_faults) {
+    const Geom& g = P.g;
+    size_t nb = (size_t)g.nb, c = (size_t)cap;
+    size_t ntiles = (nb + ENC_BLOCKS - 1) / ENC_BLOCKS + 1;
+    CompLayout L;
+    size_t o = 0;
+    auto take = [&](size_t n) { size_t r = o; o = al256(o + n); return r; };
+    L.result = take(RESULT_BYTES);
+    L.hist = take(4 * c);
+    L.lbflag = take(4 * ntiles);
+    L.events = take(nb);
+    L.fixed = take(nb);
+    L.zero_end = o;
+    L.coef = take(16 * nb);
+    L.insum = take(8 * nb);
+    L.inisum = take(8 * nb);
+    L.ind = take(nb);
+    L.unpc = take(4 * nb);
+    L.bsum = take(8 * nb);
+    L.bisum = take(8 * nb);
+    L.dcs = take(8 * nb);
+    L.bitlen = take(4 * nb);
+    L.regpre = take(4 * nb);
+    L.unppre = take(8 * nb);
+    L.enc = take(8 * c);
+    L.qp = take(sizeof(QuantParams));
+    L.lbbits = take(16 * ntiles);
+    L.lbreg = take(16 * ntiles);
+    L.lbunp = take(16 * ntiles);
+    L.cb_keys = take(16 * c);
+    L.cb_syms = take(4 * c);
+    L.cb_w = take(16 * c);
+    L.cb_parent = take(8 * c);
+    L.cb_lens = take(c);
+    size_t ngroups = (nb + 31) / 32;
+    L.bins = take(2 * ngroups * 32 * (size_t)g.nvmax8 + 64);
+    L.unp = take(4 * nb * (size_t)g.vmax);
+    L.fix = take(n_faults ? 4 * nb * (size_t)g.vmax : 0);
+    L.faults = take(sizeof(ftlz_fault) * (size_t)std::max<int64_t>(1, n_faults));
+    L.ffirst = take(n_faults ? 4 * nb : 0);
+    L.ovr = take(nb);
+    L.plan = take(P.bytes());
+    L.total = o;
+    return L;
+}
+
+extern "C" size_t ftlz_compress_workspace_size(int64_t nx, int64_t ny, int64_t nz, const ftlz_config* cfg) {
+    HostPlan P;
+    if (!build_plan(nx, ny, nz, cfg->block_edge, P)) return 0;
+    // faults enlarge the workspace (fix scratch); size for the faulted case
+    return comp_layout(P, (int)cfg->bin_capacity, 1).total;
+}
+
+extern "C" size_t ftlz_compress_bound(int64_t nx, int64_t ny, int64_t nz, const ftlz_config* cfg) {
+    int64_t nb = ftlz_block_count(nx, ny, nz, cfg->block_edge);
+    if (nb < 0) return 0;
+    size_t N = (size_t)nx * ny * nz;
+    size_t nsym = std::min<size_t>(cfg->bin_capacity, N + 1);
+    return 55 + 25 * (size_t)nb + 4 + 5 * nsym + 8 + (57 * N + 7) / 8 + 4 * N + 16 + 8 * (size_t)nb + 64;
+}
+
+// faults sorted by block + per-block first index
+static void prep_faults(const ftlz_fault* faults, int64_t nf, int64_t nb, std::vector<ftlz_fault>& sorted,
+                        std::vector<int>& first) {
+    sorted.assign(faults, faults + nf);
+    std::stable_sort(sorted.begin(), sorted.end(), [](const ftlz_fault& a, const ftlz_fault& b) { return a.block < b.block; });
+    first.assign((size_t)nb, -1);
+    for (int64_t i = (int64_t)sorted.size() - 1; i >= 0; i--)
+        if (sorted[i].block >= 0 && sorted[i].block < nb) first[(size_t)sorted[i].block] = (int)i;
+}
+
+static int validate_faults(const HostPlan& P, const ftlz_fault* f, int64_t nf) {
+    for (int64_t i = 0; i < nf; i++) {
+        if (f[i].block < 0 || f[i].block >= P.g.nb) return set_err(FTLZ_ERR_INVALID_ARGUMENT, "fault block out of range");
+        int64_t b = f[i].block;
+        int64_t bk = b % P.g.cz, t = b / P.g.cz, bj = t % P.g.cy, bi = t / P.g.cy;
+        int xid = ((bi == P.g.cx - 1 && P.g.rx != P.g.e) ? 4 : 0) | ((bj == P.g.cy - 1 && P.g.ry != P.g.e) ? 2 : 0) |
+                  ((bk == P.g.cz - 1 && P.g.rz != P.g.e) ? 1 : 0);
+        int vol = P.ep[xid].vol;
+        int lim = f[i].target == FTLZ_FAULT_COEFF ? 4 : f[i].target == FTLZ_FAULT_ESTIMATE ? 2 : vol;
+        int blim = f[i].target == FTLZ_FAULT_ESTIMATE ? 64 : 32;
+        if (f[i].element < 0 || f[i].element >= lim || f[i].bit < 0 || f[i].bit >= blim || f[i].target < 0 || f[i].target > 4)
+            return set_err(FTLZ_ERR_INVALID_ARGUMENT, "fault element/bit/target out of range");
+    }
+    return FTLZ_OK;
+}
+
+static int block_xid(const Geom& g, int64_t b) {
+    int64_t bk = b % g.cz, t = b / g.cz, bj = t % g.cy, bi = t / g.cy;
+    return ((bi == g.cx - 1 && g.rx != g.e) ? 4 : 0) | ((bj == g.cy - 1 && g.ry != g.e) ? 2 : 0) |
+           ((bk == g.cz - 1 && g.rz != g.e) ? 1 : 0);
+}
+
+// extent tuple for group ordering (pipeline.py:216-224)
+static std::tuple<int, int, int> block_extent(const HostPlan& P, int64_t b) {
+    const ExtPlan& E = P.ep[block_xid(P.g, b)];
+    return std::make_tuple(E.bx, E.by, E.bz);
+}
+
+static void put_list(int64_t* dst, int64_t cap, int64_t* n_out, const std::vector<int64_t>& v) {
+    *n_out = (int64_t)v.size();
+    if (dst)
+        for (size_t i = 0; i < v.size() && (int64_t)i < cap; i++) dst[i] = v[i];
+}
+
+static void report_reset(ftlz_report* r) {
+    r->n_input_corrected = r->n_bins_corrected = r->n_dup_mismatch = r->n_reexecuted = 0;
+    r->sdc = 0;
+    info_set(&r->info, FTLZ_OK, 0, -1, -1, 0, 0);
+    r->eb = 0; r->archive_len = 0; r->n_blocks = 0; r->n_regression = 0; r->n_unpredictable = 0;
+    r->n_symbols = 0; r->payload_bits = 0; r->max_code_len = 0;
+}
+
+// ------------------------------------------------------------------------------------------
+// core compress on a carved workspace.  `plan_dev` may point into the workspace (stateless
+// API) or into a context cache; if `upload` the plan is copied there first.
+static int compress_core(const HostPlan& P, const DevPlan* cached, const float* d_in, int32_t eb_mode,
+                         double eb_value, const ftlz_config* cfg, const ftlz_fault* faults, int64_t nf,
+                         const int8_t* ovr, unsigned char* ws, size_t ws_size, uint8_t* d_out, size_t out_cap,
+                         ftlz_report* rep, cudaStream_t s, unsigned char* h_result) {
+    report_reset(rep);
+    const Geom& g = P.g;
+    int cap = (int)cfg->bin_capacity;
+    if (cap < 4 || (cap & (cap - 1))) return set_err(FTLZ_ERR_INVALID_ARGUMENT, "bin_capacity must be a power of two >= 4");
+    if (cap > 65536) return set_err(FTLZ_ERR_INVALID_ARGUMENT, "bin_capacity > 65536 is not supported on the device path");
+    if (cfg->codec_id != 0) {
+        info_set(&rep->info, FTLZ_ERR_UNSUPPORTED_CODEC, 0, -1, -1, cfg->codec_id, 0);
+        return set_err(FTLZ_ERR_UNSUPPORTED_CODEC, "only codec 0 (identity) is on the device path");
+    }
+    int rc = validate_faults(P, faults, nf);
+    if (rc) return rc;
+    CompLayout L = comp_layout(P, cap, nf);
+    if (ws_size < L.total) return set_err(FTLZ_ERR_CAPACITY, "workspace too small");
+    KCfg K = kcfg_comp(g);
+    if (K.smem > 227 * 1024) return set_err(FTLZ_ERR_INVALID_ARGUMENT, "block too large for shared memory (block_edge^3 * 15 B > 227 KB)");
+    if ((rc = kernel_attrs_once())) return set_err(rc, "cudaFuncSetAttribute failed");
+    DevPlan D;
+    std::vector<unsigned char> staging;
+    if (cached) D = *cached;
+    else if ((rc = upload_plan(P, ws + L.plan, D, s, staging))) return rc;
+    CK(cudaMemsetAsync(ws, 0, L.zero_end, s));
+    std::vector<ftlz_fault> fs;
+    std::vector<int> ff;
+    if (nf) {
+        prep_faults(faults, nf, g.nb, fs, ff);
+        CK(cudaMemcpyAsync(ws + L.faults, fs.data(), sizeof(ftlz_fault) * nf, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ws + L.ffirst, ff.data(), 4 * (size_t)g.nb, cudaMemcpyHostToDevice, s));
+    }
+    if (ovr) CK(cudaMemcpyAsync(ws + L.ovr, ovr, (size_t)g.nb, cudaMemcpyHostToDevice, s));
+
+    CompArgs A;
+    memset(&A, 0, sizeof A);
+    A.g = g;
+    A.x = d_in;
+    A.protect_input = cfg->protect_input; A.protect_bins = cfg->protect_bins;
+    A.dup_eval = cfg->duplicate_eval; A.store_sum_dc = cfg->store_sum_dc;
+    A.eb_mode = eb_mode; A.eb_value = eb_value;
+    A.cap = cap; A.center = cap / 2;
+    A.P = K.P; A.nwarp_smem = (int)K.slot;
+    A.n_faults = (int)nf;
+    A.faults = (const ftlz_fault*)(ws + L.faults);
+    A.fault_first = (const int*)(ws + L.ffirst);
+    A.override_ = ovr ? (const int8_t*)(ws + L.ovr) : nullptr;
+    A.plans = D.ep; A.leaves = D.leaves; A.coords = D.coords; A.wave = D.wave; A.planes = D.planes;
+    A.coef = (float4*)(ws + L.coef); A.insum = (u64*)(ws + L.insum); A.inisum = (u64*)(ws + L.inisum);
+    A.ind = ws + L.ind; A.unpc = (u32*)(ws + L.unpc); A.bsum = (u64*)(ws + L.bsum); A.bisum = (u64*)(ws + L.bisum);
+    A.dcs = (u64*)(ws + L.dcs); A.bitlen = (u32*)(ws + L.bitlen); A.regpre = (u32*)(ws + L.regpre);
+    A.unppre = (u64*)(ws + L.unppre); A.events = ws + L.events;
+    A.st = (DevStatus*)(ws + L.result);
+    A.minmax = (u32*)(ws + L.result + 64);
+    A.counters = (u32*)(ws + L.result + 80);
+    A.layout = (u64*)(ws + L.result + 144);
+    A.qp = (QuantParams*)(ws + L.qp);
+    A.hist = (u32*)(ws + L.hist);
+    A.enc = (u64*)(ws + L.enc);
+    A.bins = (u16*)(ws + L.bins);
+    A.unp_scratch = (u32*)(ws + L.unp);
+    A.out = d_out;
+    A.out_cap = out_cap;
+    CodebookScratch S;
+    S.keys = (u64*)(ws + L.cb_keys); S.syms = (u32*)(ws + L.cb_syms); S.w = (u64*)(ws + L.cb_w);
+    S.parent = (u32*)(ws + L.cb_parent); S.lens = ws + L.cb_lens;
+
+    long long nctas = (g.nb + K.P - 1) / K.P;
+    k_prep<<<(unsigned)nctas, 32 * K.P, K.smem, s>>>(A);
+    LCHK("k_prep");
+    k_resolve<<<1, 1, 0, s>>>(A);
+    LCHK("k_resolve");
+    k_quant<<<(unsigned)nctas, 32 * K.P, K.smem, s>>>(A);
+    LCHK("k_quant");
+    if (nf) k_fault_bins<<<num_sms(), 256, 0, s>>>(A, (u32*)(ws + L.fix), (u8*)(ws + L.fixed));
+    LCHK("k_fault_bins");
+    k_codebook<<<1, CB_THREADS, (CB_SMEM_KEYS * 3) * 8, s>>>(A, S);
+    LCHK("k_codebook");
+    k_zero<<<num_sms() * 4, 256, 0, s>>>(A);
+    LCHK("k_zero");
+    unsigned ntiles = (unsigned)((g.nb + ENC_BLOCKS - 1) / ENC_BLOCKS);
+    k_encode<<<ntiles, ENC_BLOCKS, 0, s>>>(A, (u32*)(ws + L.fix), (const u8*)(ws + L.fixed), (u32*)(ws + L.lbflag), (u64*)(ws + L.lbbits),
+                                           (u64*)(ws + L.lbreg), (u64*)(ws + L.lbunp));
+    LCHK("k_encode");
+    ftlz_header H;
+    memset(&H, 0, sizeof H);
+    H.nx = g.nx; H.ny = g.ny; H.nz = g.nz; H.block_edge = g.e; H.eb_mode = eb_mode ? 1 : 0;
+    k_assemble<<<num_sms() * 2, 256, 0, s>>>(A, H);
+    LCHK("k_assemble");
+    CK(cudaGetLastError());
+    unsigned char hres_local[RESULT_BYTES];
+    unsigned char* hres = h_result ? h_result : hres_local;
+    CK(cudaMemcpyAsync(hres, ws + L.result, RESULT_BYTES, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    DevStatus st;
+    memcpy(&st, hres, sizeof st);
+    u32 counters[16];
+    memcpy(counters, hres + 80, sizeof counters);
+    u64 lay[LAYOUT_COUNT];
+    memcpy(lay, hres + 144, sizeof lay);
+    double eb;
+    memcpy(&eb, &lay[LAYOUT_EB_BITS], 8);
+    rep->eb = eb;
+    rep->n_blocks = g.nb;
+    // events (rare): corrected / uncorrectable blocks
+    std::vector<int64_t> in_fix, bin_fix;
+    int64_t bad_in = -1, bad_bin = -1;
+    if (counters[3]) {
+        std::vector<unsigned char> ev((size_t)g.nb);
+        CK(cudaMemcpy(ev.data(), ws + L.events, (size_t)g.nb, cudaMemcpyDeviceToHost));
+        std::tuple<int, int, int> best;
+        for (int64_t b = 0; b < g.nb; b++) {
+            if (ev[b] & 1) in_fix.push_back(b);
+            if (ev[b] & 2) bin_fix.push_back(b);
+            if (ev[b] & 4) {
+                auto ext = block_extent(P, b);
+                if (bad_in < 0 || ext < best) { bad_in = b; best = ext; }
+            }
+            if ((ev[b] & 8) && bad_bin < 0) bad_bin = b;
+        }
+    }
+    if (st.code == FTLZ_ERR_DEGENERATE_BOUND) {
+        info_set(&rep->info, st.code, st.kind, -1, -1, 0, 0);
+        return set_err(st.code, "degenerate error bound");
+    }
+    if (bad_in >= 0) {
+        info_set(&rep->info, FTLZ_ERR_UNCORRECTABLE, FTLZ_K_UNCORR_INPUT, -1, bad_in, 0, 0);
+        return set_err(FTLZ_ERR_UNCORRECTABLE, "uncorrectable input block");
+    }
+    if (bad_bin >= 0) {
+        info_set(&rep->info, FTLZ_ERR_UNCORRECTABLE, FTLZ_K_UNCORR_BINS_HIST, -1, bad_bin, 0, 0);
+        return set_err(FTLZ_ERR_UNCORRECTABLE, "uncorrectable bin array");
+    }
+    if (st.code) {
+        info_set(&rep->info, st.code, st.kind, st.offset, st.block, st.a, st.b);
+        return set_err(st.code, "compression failed on the device");
+    }
+    std::vector<int64_t> dup;
+    if (counters[1]) {
+        std::vector<unsigned char> ind((size_t)g.nb);
+        CK(cudaMemcpy(ind.data(), ws + L.ind, (size_t)g.nb, cudaMemcpyDeviceToHost));
+        for (int64_t b = 0; b < g.nb; b++)
+            if (counters[1] & (1u << (block_xid(g, b) * 2 + ind[b]))) dup.push_back(b);
+    }
+    put_list(rep->input_corrected, rep->capacity, &rep->n_input_corrected, in_fix);
+    put_list(rep->bins_corrected, rep->capacity, &rep->n_bins_corrected, bin_fix);
+    put_list(rep->dup_mismatch, rep->capacity, &rep->n_dup_mismatch, dup);
+    rep->archive_len = (int64_t)lay[LAYOUT_TOTAL];
+    rep->n_regression = (int64_t)lay[LAYOUT_NREG];
+    rep->n_unpredictable = (int64_t)lay[LAYOUT_NUNP];
+    rep->n_symbols = (int64_t)lay[LAYOUT_NSYM];
+    rep->payload_bits = (int64_t)lay[LAYOUT_TOTAL_BITS];
+    rep->max_code_len = (int32_t)lay[LAYOUT_MAXLEN];
+    return FTLZ_OK;
+}
+
+extern "C" int ftlz_compress(const float* d_in, int64_t nx, int64_t ny, int64_t nz, int32_t eb_mode, double eb_value,
+                             const ftlz_config* cfg, const ftlz_fault* faults, int64_t n_faults,
+                             const int8_t* predictor_override, void* d_workspace, size_t workspace_size,
+                             uint8_t* d_out, size_t out_capacity, ftlz_report* report, void* stream) {
+    HostPlan P;
+    if (!build_plan(nx, ny, nz, cfg->block_edge, P)) {
+        report_reset(report);
+        info_set(&report->info, FTLZ_ERR_INVALID_GEOMETRY, 0, -1, -1, 0, 0);
+        return set_err(FTLZ_ERR_INVALID_GEOMETRY, "invalid dims or block edge");
+    }
+    return compress_core(P, nullptr, d_in, eb_mode, eb_value, cfg, faults, n_faults, predictor_override,
+                         (unsigned char*)d_workspace, workspace_size, d_out, out_capacity, report,
+                         (cudaStream_t)stream, nullptr);
+}
+
+// ------------------------------------------------------------------------------------------
+// decompress workspace layout
+struct DecLayout {
+    size_t result;   // DevStatus | counters[16] | info[16]
+    size_t lbflag, dflag, mflag;
+    size_t zero_end;
+    size_t maps, smaps, sentry;
+    size_t ind, recoff, unpc, bitlen, bofs, uofs, da, db, lor, mis;
+    size_t lut, first, lcount, lbase, dsym, sortkeys, lba, lbb;
+    size_t bins, faults, ffirst, plan;
+    size_t total;
+    long long nchunks, nsuper;
+};
+
+static DecLayout dec_layout(const HostPlan& P, size_t len, int cap, int64_t nf) {
+    const Geom& g = P.g;
+    size_t nb = (size_t)g.nb;
+    DecLayout L;
+    size_t scan = std::min<size_t>(25 * nb, len > 55 ? len - 55 : 0) + 1;
+    L.nchunks = (long long)((scan + PCHUNK - 1) / PCHUNK) + 1;
+    L.nsuper = (L.nchunks + PSUPER - 1) / PSUPER;
+    size_t ntiles = (nb + 1023) / 1024 + 1;
+    size_t o = 0;
+    auto take = [&](size_t n) { size_t r = o; o = al256(o + n); return r; };
+    L.result = take(RESULT_BYTES);
+    L.lbflag = take(4 * ntiles);
+    L.dflag = take(nb);
+    L.mflag = take(nb);
+    L.zero_end = o;
+    L.maps = take(4 * 25 * (size_t)L.nchunks);
+    L.smaps = take(4 * 25 * (size_t)L.nsuper);
+    L.sentry = take(8 * (size_t)L.nsuper);
+    L.ind = take(nb);
+    L.recoff = take(8 * nb);
+    L.unpc = take(4 * nb);
+    L.bitlen = take(4 * nb);
+    L.bofs = take(8 * nb);
+    L.uofs = take(8 * nb);
+    L.da = take(8 * nb);
+    L.db = take(8 * nb);
+    L.lor = take(4 * nb);
+    L.mis = take(4 * nb);
+    L.lut = take(4 << DEC_TBITS);
+    L.first = take(8 * 64);
+    L.lcount = take(4 * 64);
+    L.lbase = take(4 * 64);
+    L.dsym = take(4 * (size_t)cap);
+    L.sortkeys = take(8 * (size_t)std::max(cap, 8192) * 2);
+    L.lba = take(16 * ntiles);
+    L.lbb = take(16 * ntiles);
+    L.bins = take(2 * ((nb + 31) / 32) * 32 * (size_t)g.nvmax8 + 64);
+    L.faults = take(sizeof(ftlz_fault) * (size_t)std::max<int64_t>(1, nf));
+    L.ffirst = take(nf ? 4 * nb : 0);
+    L.plan = take(P.bytes());
+    L.total = o;
+    return L;
+}
+
+extern "C" size_t ftlz_decompress_workspace_size(const ftlz_header* h, size_t len) {
+    HostPlan P;
+    if (!build_plan(h->nx, h->ny, h->nz, h->block_edge, P)) return 0;
+    return dec_layout(P, len, (int)std::min<uint32_t>(h->bin_capacity, 65536u), 1).total;
+}
+
+struct DecResult {
+    DevStatus st;
+    u32 counters[16];
+    u64 info[16];
+};
+
+static void stream_info_fill(const ftlz_header* h, const u64* info, ftlz_stream_info* si) {
+    memset(si, 0, sizeof *si);
+    si->hdr = *h;
+    si->table_off = 55;
+    si->table_len = (int64_t)info[DI_TABLE_END] - 55;
+    si->book_off = (int64_t)info[DI_BOOK_OFF];
+    si->n_symbols = (int64_t)info[DI_NSYM];
+    si->payload_off = (int64_t)info[DI_PAY_OFF];
+    si->payload_len = (int64_t)info[DI_PAY_LEN];
+    si->unpred_off = (int64_t)info[DI_UNP_OFF];
+    si->n_unpred = (int64_t)info[DI_NUNP];
+    si->sumdc_off = info[DI_HAS_SDC] ? (int64_t)info[DI_SDC_OFF] : -1;
+    si->total_bits = (int64_t)info[DI_TOTAL_BITS];
+    si->max_code_len = (int32_t)info[DI_MAXLEN];
+    si->has_sum_dc = (int32_t)info[DI_HAS_SDC];
+}
+
+// parse (+ optionally decode) on the device; d_a must have >= 64 readable bytes past len
+static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8_t* d_a, size_t len,
+                           const ftlz_header* h, float* d_out, const ftlz_fault* faults, int64_t nf,
+                           unsigned char* ws, size_t ws_size, ftlz_report* rep, ftlz_stream_info* si_out,
+                           bool decode, cudaStream_t s, unsigned char* h_result) {
+    report_reset(rep);
+    const Geom& g = P.g;
+    int cap = (int)h->bin_capacity;
+    if (cap > 65536) return set_err(FTLZ_ERR_INVALID_ARGUMENT, "bin_capacity > 65536 is not supported on the device path");
+    int rc = validate_faults(P, faults, nf);
+    if (rc) return rc;
+    DecLayout L = dec_layout(P, len, cap, nf);
+    if (ws_size < L.total) return set_err(FTLZ_ERR_CAPACITY, "workspace too small");
+    if ((rc = kernel_attrs_once())) return set_err(rc, "cudaFuncSetAttribute failed");
+    DevPlan D;
+    std::vector<unsigned char> staging;
+    if (cached) D = *cached;
+    else if ((rc = upload_plan(P, ws + L.plan, D, s, staging))) return rc;
+    CK(cudaMemsetAsync(ws, 0, L.zero_end, s));
+    CK(cudaMemsetAsync(ws + L.result + 64 + 4 * DC_MINFAIL, 0xff, 4, s));
+    std::vector<ftlz_fault> fs;
+    std::vector<int> ff;
+    if (nf) {
+        prep_faults(faults, nf, g.nb, fs, ff);
+        CK(cudaMemcpyAsync(ws + L.faults, fs.data(), sizeof(ftlz_fault) * nf, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ws + L.ffirst, ff.data(), 4 * (size_t)g.nb, cudaMemcpyHostToDevice, s));
+    }
+    DecArgs A;
+    memset(&A, 0, sizeof A);
+    A.g = g;
+    A.a = d_a;
+    A.len = len;
+    A.cap = cap; A.center = cap / 2;
+    A.eb = h->eb_value; A.twoeb = 2.0 * h->eb_value;
+    A.codec = h->codec_id;
+    A.n_faults = (int)nf;
+    A.faults = (const ftlz_fault*)(ws + L.faults);
+    A.fault_first = (const int*)(ws + L.ffirst);
+    A.plans = D.ep; A.coords = D.coords; A.wave = D.wave; A.planes = D.planes;
+    A.maps = (u32*)(ws + L.maps); A.smaps = (u32*)(ws + L.smaps); A.sentry = (u64*)(ws + L.sentry);
+    A.nchunks = L.nchunks; A.nsuper = L.nsuper;
+    A.ind = ws + L.ind; A.rec_off = (u64*)(ws + L.recoff); A.unpc = (u32*)(ws + L.unpc);
+    A.bitlen = (u32*)(ws + L.bitlen); A.bofs = (u64*)(ws + L.bofs); A.uofs = (u64*)(ws + L.uofs);
+    A.dflag = ws + L.dflag; A.da = (long long*)(ws + L.da); A.db = (long long*)(ws + L.db);
+    A.mflag = ws + L.mflag; A.lor_list = (u32*)(ws + L.lor); A.mis_list = (u32*)(ws + L.mis);
+    A.st = (DevStatus*)(ws + L.result);
+    A.counters = (u32*)(ws + L.result + 64);
+    A.info = (u64*)(ws + L.result + 128);
+    A.lut = (u32*)(ws + L.lut); A.first_code = (u64*)(ws + L.first); A.lcount = (u32*)(ws + L.lcount);
+    A.lbase = (u32*)(ws + L.lbase); A.dsym = (u32*)(ws + L.dsym); A.sortkeys = (u64*)(ws + L.sortkeys);
+    A.bins = (u16*)(ws + L.bins);
+    A.out = d_out;
+    A.lb_flag = (u32*)(ws + L.lbflag); A.lb_a = (u64*)(ws + L.lba); A.lb_b = (u64*)(ws + L.lbb);
+
+    int sms = num_sms();
+    k_parse_maps<<<sms * 8, 256, 0, s>>>(A);
+    LCHK("k_parse_maps");
+    k_parse_compose<<<(unsigned)L.nsuper, PSUPER, 0, s>>>(A);
+    LCHK("k_parse_compose");
+    k_parse_top<<<1, 256, 0, s>>>(A);
+    LCHK("k_parse_top");
+    k_parse_records<<<(unsigned)L.nsuper, PSUPER, 0, s>>>(A);
+    LCHK("k_parse_records");
+    k_scan2<<<(unsigned)((g.nb + 1023) / 1024), 1024, 0, s>>>(A);
+    LCHK("k_scan2");
+    k_parse_tail<<<1, PT_THREADS, 8192 * 8, s>>>(A);
+    LCHK("k_parse_tail");
+    size_t dec_smem = ((size_t)4 << DEC_TBITS) + (size_t)DEC_WARPS * 32 * g.e * 4;
+    size_t rslot = al16((size_t)g.vmax * 8) + al16((size_t)g.vmax * 4);
+    int rw = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / rslot));
+    if (decode) {
+        k_decode<<<(unsigned)((g.nb + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32)), DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
+        LCHK("k_decode");
+        k_recon_warp<<<sms * 4, rw * 32, rslot * rw, s>>>(A, 0);
+        LCHK("k_recon_warp");
+    }
+    CK(cudaGetLastError());
+    unsigned char hres_local[RESULT_BYTES];
+    unsigned char* hres = h_result ? h_result : hres_local;
+    CK(cudaMemcpyAsync(hres, ws + L.result, RESULT_BYTES, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    DecResult R;
+    memcpy(&R.st, hres, sizeof R.st);
+    memcpy(R.counters, hres + 64, sizeof R.counters);
+    memcpy(R.info, hres + 128, sizeof R.info);
+    if (R.st.code) {
+        info_set(&rep->info, R.st.code, R.st.kind, R.st.offset, R.st.block, R.st.a, R.st.b);
+        return set_err(R.st.code, "archive rejected by the device parser");
+    }
+    if (si_out) stream_info_fill(h, R.info, si_out);
+    rep->eb = h->eb_value;
+    rep->n_blocks = g.nb;
+    rep->n_symbols = (int64_t)R.info[DI_NSYM];
+    rep->n_unpredictable = (int64_t)R.info[DI_NUNP];
+    rep->payload_bits = (int64_t)R.info[DI_TOTAL_BITS];
+    rep->max_code_len = (int32_t)R.info[DI_MAXLEN];
+    rep->n_regression = g.nb - (int64_t)R.counters[DC_NLOR];
+    rep->archive_len = (int64_t)len;
+    if (!decode) return FTLZ_OK;
+    if (R.counters[DC_MINFAIL] != 0xffffffffu) {
+        // lowest undecodable block (pipeline.py:673-677)
+        int64_t b = R.counters[DC_MINFAIL];
+        unsigned char k;
+        long long a2[2];
+        CK(cudaMemcpy(&k, ws + L.dflag + b, 1, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&a2[0], ws + L.da + 8 * b, 8, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&a2[1], ws + L.db + 8 * b, 8, cudaMemcpyDeviceToHost));
+        rep->sdc = 1;
+        info_set(&rep->info, FTLZ_OK, k, -1, b, a2[0], a2[1]);
+        return FTLZ_OK;
+    }
+    u32 nmis = R.counters[DC_NMIS];
+    std::vector<int64_t> reexec;
+    if (nmis) {
+        // re-execution of every mismatching block (pipeline.py:713-723), no fault replay
+        std::vector<u32> mis(nmis);
+        CK(cudaMemcpy(mis.data(), ws + L.mis, 4 * (size_t)nmis, cudaMemcpyDeviceToHost));
+        std::sort(mis.begin(), mis.end());
+        CK(cudaMemcpy(ws + L.mis, mis.data(), 4 * (size_t)nmis, cudaMemcpyHostToDevice));
+        A.n_faults = 0;
+        k_decode<<<(unsigned)((nmis + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32)), DEC_WARPS * 32, dec_smem, s>>>(
+            A, (const u32*)(ws + L.mis), (int)nmis);
+        LCHK("k_decode");
+        k_recon_warp<<<(unsigned)std::min<u32>((nmis + rw - 1) / rw, sms * 4), rw * 32, rslot * rw, s>>>(A, 1);
+        LCHK("k_recon_warp");
+        CK(cudaGetLastError());
+        std::vector<unsigned char> mf((size_t)g.nb);
+        CK(cudaMemcpyAsync(mf.data(), ws + L.mflag, (size_t)g.nb, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        // verification walks extent groups in sorted order, ids ascending (pipeline.py:692-708)
+        std::vector<std::pair<std::tuple<int, int, int>, int64_t>> order;
+        for (u32 b : mis) order.push_back({block_extent(P, b), (int64_t)b});
+        std::sort(order.begin(), order.end());
+        for (auto& o : order) {
+            int64_t b = o.second;
+            if (mf[b] == 2) reexec.push_back(b);
+            else {
+                rep->sdc = 1;
+                info_set(&rep->info, FTLZ_OK, FTLZ_K_D_MISMATCH, -1, b, 0, 0);
+                break;
+            }
+        }
+        std::sort(reexec.begin(), reexec.end());
+    }
+    put_list(rep->reexecuted, rep->capacity, &rep->n_reexecuted, reexec);
+    return FTLZ_OK;
+}
+
+extern "C" int ftlz_parse(const uint8_t* d_archive, size_t len, const ftlz_header* hdr, void* d_workspace,
+                          size_t workspace_size, ftlz_stream_info* info_out, ftlz_report* report, void* stream) {
+    HostPlan P;
+    if (!build_plan(hdr->nx, hdr->ny, hdr->nz, hdr->block_edge, P)) return set_err(FTLZ_ERR_INVALID_GEOMETRY, "bad header");
+    return decompress_core(P, nullptr, d_archive, len, hdr, nullptr, nullptr, 0, (unsigned char*)d_workspace,
+                           workspace_size, report, info_out, false, (cudaStream_t)stream, nullptr);
+}
+
+extern "C" int ftlz_decompress(const uint8_t* d_archive, size_t len, const ftlz_header* hdr, float* d_out,
+                               const ftlz_fault* faults, int64_t n_faults, void* d_workspace, size_t workspace_size,
+                               ftlz_report* report, void* stream) {
+    HostPlan P;
+    if (!build_plan(hdr->nx, hdr->ny, hdr->nz, hdr->block_edge, P)) return set_err(FTLZ_ERR_INVALID_GEOMETRY, "bad header");
+    return decompress_core(P, nullptr, d_archive, len, hdr, d_out, faults, n_faults, (unsigned char*)d_workspace,
+                           workspace_size, report, nullptr, true, (cudaStream_t)stream, nullptr);
+}
+
+// ------------------------------------------------------------------------------------------
+// context API: cached device buffers, plans, pinned staging and a private stream
+struct DevBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    int ensure(size_t need) {
+        if (need <= n) return FTLZ_OK;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        size_t cap = need + need / 8 + 4096;
+        cudaError_t e = cudaMalloc(&p, cap);
+        if (e != cudaSuccess) return set_err(FTLZ_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        n = cap;
+        return FTLZ_OK;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+struct HostBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    int ensure(size_t need) {
+        if (need <= n) return FTLZ_OK;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+        size_t cap = need + need / 8 + 4096;
+        cudaError_t e = cudaMallocHost(&p, cap);
+        if (e != cudaSuccess) return set_err(FTLZ_ERR_CUDA, std::string("cudaMallocHost: ") + cudaGetErrorString(e));
+        n = cap;
+        return FTLZ_OK;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+struct ftlz_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    DevBuf ws, in, out, dws, arch, dout, plan;
+    HostBuf h_arch, h_res;
+    size_t arch_len = 0;
+    bool arch_on_host = false;
+    // plan cache (one geometry at a time)
+    int64_t pk[4] = {-1, -1, -1, -1};
+    HostPlan hp;
+    DevPlan dp;
+    // last parsed archive (for decompress reuse)
+    const uint8_t* parsed_src = nullptr;
+    size_t parsed_len = 0;
+    ftlz_header parsed_hdr;
+    std::mutex mu;
+};
+
+static int ctx_plan(ftlz_ctx* c, int64_t nx, int64_t ny, int64_t nz, int e) {
+    if (c->pk[0] == nx && c->pk[1] == ny && c->pk[2] == nz && c->pk[3] == e) return FTLZ_OK;
+    if (!build_plan(nx, ny, nz, e, c->hp)) return set_err(FTLZ_ERR_INVALID_GEOMETRY, "invalid dims or block edge");
+    int rc = c->plan.ensure(c->hp.bytes());
+    if (rc) return rc;
+    std::vector<unsigned char> staging;
+    rc = upload_plan(c->hp, (unsigned char*)c->plan.p, c->dp, c->stream, staging);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(c->stream));
+    c->pk[0] = nx; c->pk[1] = ny; c->pk[2] = nz; c->pk[3] = e;
+    return FTLZ_OK;
+}
+
+extern "C" ftlz_ctx* ftlz_ctx_create(int32_t device) {
+    if (cudaSetDevice(device) != cudaSuccess) {
+        set_err(FTLZ_ERR_CUDA, "cudaSetDevice failed (no usable CUDA device)");
+        return nullptr;
+    }
+    ftlz_ctx* c = new ftlz_ctx();
+    c->device = device;
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        set_err(FTLZ_ERR_CUDA, "cudaStreamCreate failed");
+        delete c;
+        return nullptr;
+    }
+    if (c->h_res.ensure(RESULT_BYTES)) {
+        delete c;
+        return nullptr;
+    }
+    return c;
+}
+
+extern "C" void ftlz_ctx_destroy(ftlz_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    c->ws.release(); c->in.release(); c->out.release(); c->dws.release(); c->arch.release();
+    c->dout.release(); c->plan.release(); c->h_arch.release(); c->h_res.release();
+    cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+extern "C" void* ftlz_ctx_stream(ftlz_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+static int ctx_compress(ftlz_ctx* c, const float* d_in, int64_t nx, int64_t ny, int64_t nz, int32_t eb_mode,
+                        double eb_value, const ftlz_config* cfg, const ftlz_fault* faults, int64_t nf,
+                        const int8_t* ovr, ftlz_report* rep) {
+    int rc = ctx_plan(c, nx, ny, nz, cfg->block_edge);
+    if (rc) {
+        report_reset(rep);
+        info_set(&rep->info, rc, 0, -1, -1, 0, 0);
+        return rc;
+    }
+    CompLayout L = comp_layout(c->hp, (int)cfg->bin_capacity, nf);
+    if ((rc = c->ws.ensure(L.total))) return rc;
+    size_t bound = ftlz_compress_bound(nx, ny, nz, cfg);
+    if ((rc = c->out.ensure(bound))) return rc;
+    rc = compress_core(c->hp, &c->dp, d_in, eb_mode, eb_value, cfg, faults, nf, ovr, (unsigned char*)c->ws.p,
+                       c->ws.n, (uint8_t*)c->out.p, c->out.n, rep, c->stream, (unsigned char*)c->h_res.p);
+    c->arch_len = rc == FTLZ_OK ? (size_t)rep->archive_len : 0;
+    c->arch_on_host = false;
+    return rc;
+}
+
+extern "C" int ftlz_ctx_compress_device(ftlz_ctx* c, const float* d_in, int64_t nx, int64_t ny, int64_t nz,
+                                        int32_t eb_mode, double eb_value, const ftlz_config* cfg,
+                                        const ftlz_fault* faults, int64_t nf, const int8_t* ovr, ftlz_report* rep) {
+    std::lock_guard<std::mutex> g(c->mu);
+    cudaSetDevice(c->device);
+    return ctx_compress(c, d_in, nx, ny, nz, eb_mode, eb_value, cfg, faults, nf, ovr, rep);
+}
+
+extern "C" int ftlz_ctx_compress_host(ftlz_ctx* c, const float* h_in, int64_t nx, int64_t ny, int64_t nz,
+                                      int32_t eb_mode, double eb_value, const ftlz_config* cfg,
+                                      const ftlz_fault* faults, int64_t nf, const int8_t* ovr, ftlz_report* rep) {
+    std::lock_guard<std::mutex> g(c->mu);
+    cudaSetDevice(c->device);
+    if (nx < 1 || ny < 1 || nz < 1) {
+        report_reset(rep);
+        info_set(&rep->info, FTLZ_ERR_INVALID_GEOMETRY, 0, -1, -1, 0, 0);
+        return set_err(FTLZ_ERR_INVALID_GEOMETRY, "invalid dims");
+    }
+    size_t nbytes = (size_t)nx * ny * nz * 4;
+    int rc = c->in.ensure(nbytes);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(c->in.p, h_in, nbytes, cudaMemcpyHostToDevice, c->stream));
+    rc = ctx_compress(c, (const float*)c->in.p, nx, ny, nz, eb_mode, eb_value, cfg, faults, nf, ovr, rep);
+    if (rc) return rc;
+    if ((rc = c->h_arch.ensure(c->arch_len))) return rc;
+    CK(cudaMemcpyAsync(c->h_arch.p, c->out.p, c->arch_len, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->arch_on_host = true;
+    return FTLZ_OK;
+}
+
+extern "C" int ftlz_ctx_archive_device(ftlz_ctx* c, const uint8_t** d_ptr, size_t* len) {
+    *d_ptr = (const uint8_t*)c->out.p;
+    *len = c->arch_len;
+    return FTLZ_OK;
+}
+
+extern "C" int ftlz_ctx_archive_host(ftlz_ctx* c, const uint8_t** h_ptr, size_t* len) {
+    std::lock_guard<std::mutex> g(c->mu);
+    if (!c->arch_on_host && c->arch_len) {
+        int rc = c->h_arch.ensure(c->arch_len);
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(c->h_arch.p, c->out.p, c->arch_len, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        c->arch_on_host = true;
+    }
+    *h_ptr = (const uint8_t*)c->h_arch.p;
+    *len = c->arch_len;
+    return FTLZ_OK;
+}
+
+extern "C" int ftlz_ctx_copy_archive(ftlz_ctx* c, void* h_dst, size_t capacity) {
+    std::lock_guard<std::mutex> g(c->mu);
+    if (capacity < c->arch_len) return set_err(FTLZ_ERR_CAPACITY, "destination too small");
+    if (c->arch_on_host) {
+        memcpy(h_dst, c->h_arch.p, c->arch_len);
+        return FTLZ_OK;
+    }
+    CK(cudaMemcpyAsync(h_dst, c->out.p, c->arch_len, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return FTLZ_OK;
+}
+
+static int ctx_upload_archive(ftlz_ctx* c, const uint8_t* h, size_t len, ftlz_header* hdr, ftlz_report* rep) {
+    report_reset(rep);
+    int rc = ftlz_peek_header(h, len, hdr, &rep->info);
+    if (rc) return set_err(rc, "bad header");
+    if ((rc = c->arch.ensure(len + 64))) return rc;
+    CK(cudaMemcpyAsync(c->arch.p, h, len, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync((unsigned char*)c->arch.p + len, 0, 64, c->stream));
+    return FTLZ_OK;
+}
+
+static int ctx_decompress(ftlz_ctx* c, const uint8_t* d_a, size_t len, const ftlz_header* hdr, float* d_out,
+                          const ftlz_fault* faults, int64_t nf, ftlz_report* rep, ftlz_stream_info* si, bool decode) {
+    int rc = ctx_plan(c, hdr->nx, hdr->ny, hdr->nz, hdr->block_edge);
+    if (rc) return rc;
+    DecLayout L = dec_layout(c->hp, len, (int)std::min<uint32_t>(hdr->bin_capacity, 65536u), nf);
+    if ((rc = c->dws.ensure(L.total))) return rc;
+    return decompress_core(c->hp, &c->dp, d_a, len, hdr, d_out, faults, nf, (unsigned char*)c->dws.p, c->dws.n,
+                           rep, si, decode, c->stream, (unsigned char*)c->h_res.p);
+}
+
+extern "C" int ftlz_ctx_parse_host(ftlz_ctx* c, const uint8_t* h, size_t len, ftlz_stream_info* si, ftlz_report* rep) {
+    std::lock_guard<std::mutex> g(c->mu);
+    cudaSetDevice(c->device);
+    ftlz_header hdr;
+    int rc = ctx_upload_archive(c, h, len, &hdr, rep);
+    if (rc) return rc;
+    rc = ctx_decompress(c, (const uint8_t*)c->arch.p, len, &hdr, nullptr, nullptr, 0, rep, si, false);
+    c->parsed_src = rc == FTLZ_OK ? h : nullptr;
+    c->parsed_len = len;
+    c->parsed_hdr = hdr;
+    return rc;
+}
+
+extern "C" int ftlz_ctx_decompress_host(ftlz_ctx* c, const uint8_t* h, size_t len, float* h_out,
+                                        const ftlz_fault* faults, int64_t nf, int32_t reuse_parsed, ftlz_report* rep) {
+    std::lock_guard<std::mutex> g(c->mu);
+    cudaSetDevice(c->device);
+    ftlz_header hdr;
+    int rc;
+    if (reuse_parsed && c->parsed_src == h && c->parsed_len == len) {
+        hdr = c->parsed_hdr;
+    } else {
+        rc = ctx_upload_archive(c, h, len, &hdr, rep);
+        if (rc) return rc;
+    }
+    size_t n = (size_t)hdr.nx * hdr.ny * hdr.nz;
+    if ((rc = c->dout.ensure(4 * n))) return rc;
+    rc = ctx_decompress(c, (const uint8_t*)c->arch.p, len, &hdr, (float*)c->dout.p, faults, nf, rep, nullptr, true);
+    if (rc) return rc;
+    if (!rep->sdc) {
+        CK(cudaMemcpyAsync(h_out, c->dout.p, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    return FTLZ_OK;
+}
+
+extern "C" int ftlz_ctx_decompress_device(ftlz_ctx* c, const uint8_t* d_archive, size_t len, const ftlz_header* hdr,
+                                          float* d_out, const ftlz_fault* faults, int64_t nf, ftlz_report* rep) {
+    std::lock_guard<std::mutex> g(c->mu);
+    cudaSetDevice(c->device);
+    return ctx_decompress(c, d_archive, len, hdr, d_out, faults, nf, rep, nullptr, true);
+}

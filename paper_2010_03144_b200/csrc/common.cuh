@@ -1,0 +1,267 @@
+// common.cuh -- shared device helpers for the B200 FT-SZ kernels (sm_100a).
+//
+// Exact-arithmetic helpers: the reference evaluates every per-point formula in float64 with
+// a fixed operand order and float32 storage.  All float64 math
+// here uses __dadd_rn/__dmul_rn (never contracted to DFMA) and the file is compiled with
+// -fmad=false.  Measured on B200 (tools/fp64_probe.cu): DADD/DMUL issue at 2 warp-ops/clk/SM,
+// F2F / F2I / I2F at ~1/4 of that and DDIV at 1/14, so conversions and divisions are replaced
+// by exact integer bit manipulations wherever the result is provably identical.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/ftlz_b200.h"
+
+#define FTLZ_DEV __device__ __forceinline__
+
+typedef unsigned long long u64;
+typedef uint32_t u32;
+typedef uint16_t u16;
+typedef uint8_t u8;
+
+// ------------------------------------------------------------------------------------------
+// device status: first error wins (kernels no-op once code != 0)
+struct DevStatus {
+    int code;
+    int kind;
+    long long offset, block, a, b;
+    long long order;          // ordering key for "first error" selection
+    int lock;
+    int pad;
+};
+
+FTLZ_DEV void dev_fail(DevStatus* st, int code, int kind, long long offset, long long block,
+                       long long a, long long b, long long order) {
+    // keep the error with the smallest `order` (sequential reference semantics)
+    while (atomicCAS(&st->lock, 0, 1) != 0) {
+    }
+    __threadfence();
+    volatile DevStatus* vs = st;
+    if (vs->code == 0 || order < vs->order) {
+        vs->code = code;
+        vs->kind = kind;
+        vs->offset = offset;
+        vs->block = block;
+        vs->a = a;
+        vs->b = b;
+        vs->order = order;
+    }
+    __threadfence();
+    atomicExch(&st->lock, 0);
+}
+
+FTLZ_DEV bool dev_failed(const DevStatus* st) { return *(volatile const int*)&st->code != 0; }
+
+// ------------------------------------------------------------------------------------------
+// exact conversions without the conversion pipe
+
+// float32 -> float64, exact (IEEE widening).  Normal and zero inputs use integer ops only;
+// subnormal / inf / NaN fall back to F2F (identical result; rare).
+FTLZ_DEV double f32_to_f64(float f) {
+    u32 u = __float_as_uint(f);
+    u32 e = (u >> 23) & 0xffu;
+    if (e == 0u || e == 0xffu) {
+        if ((u & 0x7fffffffu) == 0u) return __hiloint2double((int)(u & 0x80000000u), 0);
+        return (double)f;
+    }
+    u32 hi = (u & 0x80000000u) | ((e + 896u) << 20) | ((u >> 3) & 0xfffffu);
+    u32 lo = u << 29;
+    return __hiloint2double((int)hi, (int)lo);
+}
+
+// small integer (|n| < 2^31) -> float64, exact, via the 2^52 magic (one DADD, no I2F)
+FTLZ_DEV double int_to_f64(int n) {
+    // bits(2^52 + 2^31 + n) then subtract (2^52 + 2^31)
+    double t = __hiloint2double(0x43300000, (int)((u32)n ^ 0x80000000u));
+    return __dadd_rn(t, -4503601774854144.0);  // 2^52 + 2^31
+}
+
+FTLZ_DEV u64 dbits(double d) { return (u64)__double_as_longlong(d); }
+
+// ------------------------------------------------------------------------------------------
+// quantizer (pipeline.py:271-279 == quantize.py:37-52), exact.
+//   h = |diff| / (2 eb); small = h <= 2*cap; q = floor(fl((small ? h : 0) + 0.5)); sign;
+//   b = center + q; ok = small && 1 <= b <= cap-1.
+// Fast path: h' = |diff| * rcp (rcp = RN(1/(2eb))), |h' - h| <= 2 ulp.  The decision
+// floor(fl(h+0.5)) / (h <= 2cap) can only differ when h' lies within a few ulps of a
+// threshold; those points (probability ~2^-40) take the exact IEEE division.
+struct QuantParams {
+    double eb, twoeb, rcp;  // rcp = 1/(2eb) rounded; exact_div != 0 forces DDIV
+    double capd2;           // 2.0 * cap
+    u64 capd2_bits;
+    u64 eb_bits;
+    int cap, center;
+    int exact_div;
+    int pad;
+};
+
+// floor(t) for t in [0, 2^31): integer extraction from the bit pattern
+FTLZ_DEV int floor_pos(double t, int* near_int) {
+    u64 b = dbits(t);
+    int E = (int)(b >> 52) - 1023;
+    if (E < 0) {
+        // t < 1: floor 0; near 1 from below?
+        *near_int = (E == -1) && ((b & 0xfffffffffffffull) > 0xfffffffffff00ull);
+        return 0;
+    }
+    u64 m = (b & 0xfffffffffffffull) | 0x10000000000000ull;
+    int sh = 52 - E;
+    u64 fracmask = (sh >= 64) ? ~0ull : ((1ull << sh) - 1ull);
+    u64 frac = m & fracmask;
+    // within 64 ulp of an integer (either side)
+    *near_int = ((frac + 64ull) & fracmask) < 128ull;
+    return (int)(m >> sh);
+}
+
+// returns the bin (0 = unpredictable); *ok as the reference's `ok` mask
+FTLZ_DEV int quantize(const QuantParams& Q, double diff, bool* ok) {
+    double ad = fabs(diff);
+    bool small;
+    int q;
+    bool slow = Q.exact_div != 0;
+    if (!slow) {
+        double h = __dmul_rn(ad, Q.rcp);
+        u64 hb = dbits(h);
+        // small decision: exact unless h' within 2^-40 relative of 2*cap
+        small = hb <= Q.capd2_bits;
+        u64 d = hb > Q.capd2_bits ? hb - Q.capd2_bits : Q.capd2_bits - hb;
+        if (d < 4096ull) slow = true;
+        if (!slow) {
+            double t = __dadd_rn(small ? h : 0.0, 0.5);
+            int near_int;
+            q = floor_pos(t, &near_int);
+            if (near_int && small) slow = true;
+        }
+    }
+    if (slow) {
+        double h = __ddiv_rn(ad, Q.twoeb);
+        small = h <= Q.capd2;
+        double t = __dadd_rn(small ? h : 0.0, 0.5);
+        q = (int)floor(t);
+    }
+    if (diff < 0.0) q = -q;
+    int b = Q.center + q;
+    *ok = small && b >= 1 && b <= Q.cap - 1;
+    return *ok ? b : 0;
+}
+
+// |x - y| <= eb for non-negative comparisons via bit patterns (NaN -> false)
+FTLZ_DEV bool within_eb(double diff_abs_src, u64 eb_bits) {
+    u64 b = dbits(diff_abs_src) & 0x7fffffffffffffffull;
+    return b <= eb_bits;
+}
+
+// ------------------------------------------------------------------------------------------
+// opaque copy: forces a genuine second evaluation for duplicated evaluation (pipeline.py:157-179)
+FTLZ_DEV double opaque(double x) {
+    double y;
+    asm volatile("mov.b64 %0, %1;" : "=d"(y) : "d"(x));
+    return y;
+}
+
+// ------------------------------------------------------------------------------------------
+// warp reductions
+FTLZ_DEV u64 warp_sum_u64(u64 v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+FTLZ_DEV unsigned warp_sum_u32(unsigned v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// ------------------------------------------------------------------------------------------
+// geometry (core.py:113-157)
+struct Geom {
+    long long nx, ny, nz;
+    long long cx, cy, cz, nb;
+    int e;
+    int rx, ry, rz;     // trailing extents (== e when the axis divides)
+    int vmax;           // e^3
+    int nvmax8;         // vmax rounded up to a multiple of 8 (bins layout)
+};
+
+FTLZ_DEV void block_coords(const Geom& g, long long b, long long* bi, long long* bj, long long* bk) {
+    long long t = b / g.cz;
+    *bk = b - t * g.cz;
+    *bi = t / g.cy;
+    *bj = t - *bi * g.cy;
+}
+
+FTLZ_DEV int extent_id(const Geom& g, long long bi, long long bj, long long bk) {
+    return ((bi == g.cx - 1 && g.rx != g.e) ? 4 : 0) | ((bj == g.cy - 1 && g.ry != g.e) ? 2 : 0) |
+           ((bk == g.cz - 1 && g.rz != g.e) ? 1 : 0);
+}
+
+FTLZ_DEV void extent_of(const Geom& g, int xid, int* bx, int* by, int* bz) {
+    *bx = (xid & 4) ? g.rx : g.e;
+    *by = (xid & 2) ? g.ry : g.e;
+    *bz = (xid & 1) ? g.rz : g.e;
+}
+
+// bins layout shared by the quantizer (writer) and the encoder (reader):
+//   [group = b/32][chunk = p/8][lane = b%32][8 x u16]
+FTLZ_DEV size_t bins_index(const Geom& g, long long b, int p) {
+    long long grp = b >> 5;
+    int lane = (int)(b & 31);
+    return (((size_t)grp * (size_t)(g.nvmax8 >> 3) + (size_t)(p >> 3)) * 32u + (size_t)lane) * 8u +
+           (size_t)(p & 7);
+}
+
+struct BlockInfo {
+    long long b, bi, bj, bk;
+    int xid, bx, by, bz, vol;
+    bool valid;
+};
+
+FTLZ_DEV BlockInfo block_info(const Geom& g, long long b) {
+    BlockInfo B;
+    B.b = b;
+    B.valid = b < g.nb;
+    if (!B.valid) b = g.nb - 1;
+    block_coords(g, b, &B.bi, &B.bj, &B.bk);
+    B.xid = extent_id(g, B.bi, B.bj, B.bk);
+    extent_of(g, B.xid, &B.bx, &B.by, &B.bz);
+    B.vol = B.bx * B.by * B.bz;
+    return B;
+}
+
+// per-extent plans (pairwise-sum leaves, wavefront order, coordinates) built on the host
+struct ExtPlan {
+    int bx, by, bz, vol;
+    int nleaf, leaf_off;     // leaves of the pairwise tree over vol elements
+    int ns, nsleaf, sleaf_off;  // samples (SAMPLE_STRIDE=8) and their pairwise leaves
+    int coord_off;           // vol u32 entries: i | j<<8 | k<<16 (row-major p -> coords)
+    int wave_off;            // vol u16-in-u32 entries: p ordered by plane i+j+k
+    int plane_off;           // (bx+by+bz-1) u32 plane start offsets (+1 sentinel)
+    int nplanes;
+    int pad;
+};
+
+// leaf descriptor: start (elements), len, combine count after pushing this leaf
+struct Leaf {
+    int start;
+    int len;
+    int ncomb;
+    int pad;
+};
+
+// block-wide bitonic sort of n_pow2 u64 keys (ascending); all threads of the CTA participate
+FTLZ_DEV void bitonic_sort_u64(u64* keys, int n_pow2) {
+    for (int k = 2; k <= n_pow2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n_pow2; i += blockDim.x) {
+                int ixj = i ^ j;
+                if (ixj > i) {
+                    u64 a = keys[i], c = keys[ixj];
+                    bool up = (i & k) == 0;
+                    if ((a > c) == up) { keys[i] = c; keys[ixj] = a; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+

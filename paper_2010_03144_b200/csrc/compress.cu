@@ -1,0 +1,1148 @@
+// compress.cu -- device side of pipeline.compress (pipeline.py:287-537) + container.serialize
+// (container.py:109-147) for B200 (sm_100a).
+//
+// Kernel sequence (one stream, no host sync until the report read-back):
+//   k_prep      stage (a)+(b): value range, input checksums, regression fit with numpy's
+//               pairwise float64 summation order, sampled predictor selection   (K0+K1)
+//   k_resolve   resolved error bound (core.py:182-193) + quantizer constants
+//   k_quant     stage (c): verify input, predict (duplicated), quantize, reconstruct
+//               (duplicated), double-check, bins/unpredictables/checksums/sum_dc/histogram (K2)
+//   k_fault_bins  bins-stage faults: verify/correct (protect_bins) and histogram fix-up
+//   k_codebook  canonical Huffman codebook from the global histogram (K3), archive layout
+//   k_zero      zero the payload words
+//   k_encode    verify bins, per-block bit lengths, decoupled look-back scan, MSB-first packing (K4)
+//   k_assemble  header, block table, unpredictable words, sum_dc section (K5)
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace ftlz {
+
+// ------------------------------------------------------------------------------------------
+// workspace pointers for one compress call (carved by the host from one allocation)
+struct CompArgs {
+    Geom g;
+    const float* x;
+    int protect_input, protect_bins, dup_eval, store_sum_dc;
+    int eb_mode;
+    double eb_value;
+    int cap, center;
+    int P;                    // blocks per CTA in k_prep / k_quant
+    int nwarp_smem;           // smem bytes per block
+    int n_faults;
+    const ftlz_fault* faults;    // device copy
+    const int* fault_first;      // nb: first fault index of this block or -1 (faults sorted by block)
+    const int8_t* override_;     // nb or null
+    const ExtPlan* plans;        // 8 entries
+    const Leaf* leaves;
+    const u32* coords;
+    const u32* wave;
+    const u32* planes;
+    // per-block
+    float4* coef;
+    u64* insum;
+    u64* inisum;
+    u8* ind;
+    u32* unpc;
+    u64* bsum;
+    u64* bisum;
+    u64* dcs;
+    u32* bitlen;
+    u32* regpre;
+    u64* unppre;
+    u8* events;          // bit0 input corrected, bit1 bins corrected, bit2 input uncorrectable, bit3 bins uncorrectable
+    // globals
+    DevStatus* st;
+    u32* minmax;         // [0] ordered max, [1] ordered min, [2] nan flag
+    u32* counters;       // [0] n_reg, [1] dup group flags, [2] encode ticket, [3] n_unpred (low), ...
+    QuantParams* qp;
+    u32* hist;           // cap entries
+    u64* enc;            // cap entries: code << 6 | len (0 = absent)
+    u64* layout;         // archive layout (see LAYOUT_*)
+    u64* lookback;       // encode tiles
+    u16* bins;
+    u32* unp_scratch;    // nb * vmax (sparse)
+    u8* out;
+    u64 out_cap;
+    double* dscratch;    // generic per-CTA scratch for big blocks (unused for e <= 16)
+};
+
+enum {
+    LAYOUT_TABLE_LEN = 0, LAYOUT_BOOK_OFF, LAYOUT_NSYM, LAYOUT_PAYLEN_OFF, LAYOUT_PAY_OFF,
+    LAYOUT_PAY_BYTES, LAYOUT_UNP_OFF, LAYOUT_NUNP, LAYOUT_SDC_OFF, LAYOUT_TOTAL, LAYOUT_TOTAL_BITS,
+    LAYOUT_MAXLEN, LAYOUT_NREG, LAYOUT_EB_BITS, LAYOUT_COUNT
+};
+
+// ordered-int encoding of floats for atomic min/max
+FTLZ_DEV u32 f2ord(float f) {
+    u32 u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+FTLZ_DEV float ord2f(u32 o) {
+    u32 u = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+    return __uint_as_float(u);
+}
+
+// ------------------------------------------------------------------------------------------
+// block staging: the CTA's P consecutive blocks, grouped into runs of equal (bi, bj) whose
+// rows are contiguous in memory; each warp loads whole rows with coalesced accesses.
+// load the rows of block B into f32 smem buffer (row-major, local) with one warp
+FTLZ_DEV void load_block_rows(const float* __restrict__ x, const Geom& g, const BlockInfo& B,
+                              float* buf, int lane) {
+    int nrows = B.bx * B.by;
+    long long base = ((B.bi * g.e) * g.ny + B.bj * g.e) * g.nz + B.bk * g.e;
+    // each iteration covers 32 / bz rows when bz <= 32 (lanes split across rows)
+    int bz = B.bz;
+    int rows_per = bz >= 32 ? 1 : 32 / bz;
+    int kk = lane % bz;
+    int rr = lane / bz;
+    if (bz < 32) {
+        for (int r0 = 0; r0 < nrows; r0 += rows_per) {
+            int r = r0 + rr;
+            if (rr < rows_per && r < nrows) {
+                int i = r / B.by, j = r - (r / B.by) * B.by;
+                buf[r * bz + kk] = __ldg(x + base + (long long)i * g.ny * g.nz + (long long)j * g.nz + kk);
+            }
+        }
+    } else {
+        for (int r = 0; r < nrows; r++) {
+            int i = r / B.by, j = r - i * B.by;
+            const float* row = x + base + (long long)i * g.ny * g.nz + (long long)j * g.nz;
+            for (int k = lane; k < bz; k += 32) buf[r * bz + k] = __ldg(row + k);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// warp-cooperative single-word correction (checksum.py:109-142) on a u32 block in memory.
+// returns 0 clean, 1 corrected, 2 uncorrectable.  All lanes return the same value.
+FTLZ_DEV void warp_checksum(const u32* w, int n, int lane, u64* s, u64* si) {
+    u64 a = 0, c = 0;
+    for (int p = lane; p < n; p += 32) {
+        u64 v = w[p];
+        a += v;
+        c += (u64)p * v;
+    }
+    *s = warp_sum_u64(a);
+    *si = warp_sum_u64(c);
+}
+
+FTLZ_DEV int warp_correct_words(u32* w, int n, u64 st_s, u64 st_si, int lane) {
+    u64 s, si;
+    warp_checksum(w, n, lane, &s, &si);
+    if (s == st_s && si == st_si) return 0;
+    u64 ds = s - st_s, dsi = si - st_si;
+    if (ds == 0) return 2;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+        int j = j0 + lane;
+        bool cand = j < n && (u64)j * ds == dsi;
+        unsigned m = __ballot_sync(0xffffffffu, cand);
+        while (m) {
+            int l = __ffs(m) - 1;
+            m &= m - 1;
+            int jj = j0 + l;
+            u64 old = w[jj];
+            u64 restored = old - ds;
+            if (restored >> 32) continue;
+            __syncwarp();
+            if (lane == 0) w[jj] = (u32)restored;
+            __syncwarp();
+            u64 s2, si2;
+            warp_checksum(w, n, lane, &s2, &si2);
+            if (s2 == st_s && si2 == st_si) return 1;
+            __syncwarp();
+            if (lane == 0) w[jj] = (u32)old;
+            __syncwarp();
+        }
+    }
+    return 2;
+}
+
+// ------------------------------------------------------------------------------------------
+// numpy pairwise sums over a block: chains of 8 strided accumulators per leaf, combined with
+// the exact tree ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), tail added sequentially, leaves combined
+// by the host-built post-order program, and the 0.0 identity added last.
+template <int NV, typename Getter>
+FTLZ_DEV void warp_pairwise(const Leaf* leaves, int nleaf, int n, Getter get, double* leafval,
+                            double out[NV], int lane) {
+    if (n < 8) {
+        // whole reduction below 8 elements: 0.0 then sequential (never split further)
+        if (lane == 0) {
+            double r[NV];
+#pragma unroll
+            for (int v = 0; v < NV; v++) r[v] = 0.0;
+            for (int p = 0; p < n; p++) {
+                double t[NV];
+                get(p, t);
+#pragma unroll
+                for (int v = 0; v < NV; v++) r[v] = __dadd_rn(r[v], t[v]);
+            }
+#pragma unroll
+            for (int v = 0; v < NV; v++) out[v] = __dadd_rn(0.0, r[v]);
+        }
+#pragma unroll
+        for (int v = 0; v < NV; v++) out[v] = __shfl_sync(0xffffffffu, out[v], 0);
+        return;
+    }
+    int nchains = nleaf * 8;
+    for (int c0 = 0; c0 < nchains; c0 += 32) {
+        int c = c0 + lane;
+        int leaf = c >> 3, j = c & 7;
+        double r[NV];
+#pragma unroll
+        for (int v = 0; v < NV; v++) r[v] = 0.0;
+        int start = 0, len = 0;
+        if (c < nchains) {
+            Leaf L = leaves[leaf];
+            start = L.start;
+            len = L.len;
+            int len8 = len - (len & 7);
+            get(start + j, r);
+            for (int p = start + j + 8; p < start + len8; p += 8) {
+                double t[NV];
+                get(p, t);
+#pragma unroll
+                for (int v = 0; v < NV; v++) r[v] = __dadd_rn(r[v], t[v]);
+            }
+        }
+        // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) : lower lane is the left operand
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+#pragma unroll
+            for (int v = 0; v < NV; v++) {
+                double other = __shfl_xor_sync(0xffffffffu, r[v], o);
+                r[v] = (j & o) ? __dadd_rn(other, r[v]) : __dadd_rn(r[v], other);
+            }
+        }
+        if (j == 0 && c < nchains) {
+            int len8 = len - (len & 7);
+            for (int p = start + len8; p < start + len; p++) {
+                double t[NV];
+                get(p, t);
+#pragma unroll
+                for (int v = 0; v < NV; v++) r[v] = __dadd_rn(r[v], t[v]);
+            }
+#pragma unroll
+            for (int v = 0; v < NV; v++) leafval[leaf * NV + v] = r[v];
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+        // post-order combine: stack of partial sums (depth <= log2(n/64) + 2)
+        double stk[24][NV];
+        int sp = 0;
+        for (int l = 0; l < nleaf; l++) {
+#pragma unroll
+            for (int v = 0; v < NV; v++) stk[sp][v] = leafval[l * NV + v];
+            sp++;
+            int nc = leaves[l].ncomb;
+            for (int t = 0; t < nc; t++) {
+#pragma unroll
+                for (int v = 0; v < NV; v++) stk[sp - 2][v] = __dadd_rn(stk[sp - 2][v], stk[sp - 1][v]);
+                sp--;
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < NV; v++) out[v] = __dadd_rn(0.0, stk[0][v]);
+    }
+#pragma unroll
+    for (int v = 0; v < NV; v++) out[v] = __shfl_sync(0xffffffffu, out[v], 0);
+}
+
+// ------------------------------------------------------------------------------------------
+// smem layout per block slot (bytes, 16-aligned): f32[vmax] | f64[vmax] | leafval | ar/al
+FTLZ_DEV size_t slot_f64_off(int vmax) { return ((size_t)vmax * 4 + 15) & ~(size_t)15; }
+
+// ==========================================================================================
+// K1: stage (a) + (b)
+__global__ void __launch_bounds__(128) k_prep(CompArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const Geom& g = A.g;
+    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    long long b = (long long)blockIdx.x * A.P + warp;
+    BlockInfo B = block_info(g, b);
+    unsigned char* slot = smem + (size_t)warp * A.nwarp_smem;
+    float* xf = (float*)slot;
+    double* xd = (double*)(slot + slot_f64_off(g.vmax));
+    double* leafval = xd + g.vmax;             // up to (vmax/64 + 2) * 4 doubles
+    double* ar = leafval + 4 * (g.vmax / 64 + 8);
+    double* al = ar + (g.vmax / 8 + 8);
+    __shared__ u32 cta_max, cta_min, cta_nan, cta_nreg;
+    if (threadIdx.x == 0) { cta_max = 0; cta_min = 0xffffffffu; cta_nan = 0; cta_nreg = 0; }
+    __syncthreads();
+    if (B.valid) {
+        load_block_rows(A.x, g, B, xf, lane);
+        __syncwarp();
+        const ExtPlan& PL = A.plans[B.xid];
+        int vol = B.vol;
+        // value range + f64 widening + input checksum (stage a)
+        u32 mx = 0, mn = 0xffffffffu, nan = 0;
+        u64 s = 0, si = 0;
+        for (int p = lane; p < vol; p += 32) {
+            float v = xf[p];
+            u32 w = __float_as_uint(v);
+            if (v != v) nan = 1;
+            else {
+                u32 o = f2ord(v);
+                mx = max(mx, o);
+                mn = min(mn, o);
+            }
+            xd[p] = f32_to_f64(v);
+            s += w;
+            si += (u64)p * w;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            nan |= __shfl_xor_sync(0xffffffffu, nan, o);
+        }
+        s = warp_sum_u64(s);
+        si = warp_sum_u64(si);
+        if (lane == 0) {
+            atomicMax(&cta_max, mx);
+            atomicMin(&cta_min, mn);
+            atomicOr(&cta_nan, nan);
+        }
+        __syncwarp();
+        // regression fit (predict.py:81-104): S(v), S(ci v), S(cj v), S(ck v)
+        const u32* crd = A.coords + PL.coord_off;
+        double hx = (double)(B.bx - 1) / 2.0, hy = (double)(B.by - 1) / 2.0, hz = (double)(B.bz - 1) / 2.0;
+        double sums[4];
+        warp_pairwise<4>(A.leaves + PL.leaf_off, PL.nleaf, vol,
+                         [&](int p, double* t) {
+                             u32 c = __ldg(crd + p);
+                             double v = xd[p];
+                             double ci = __dadd_rn(int_to_f64((int)(c & 0xff)), -hx);
+                             double cj = __dadd_rn(int_to_f64((int)((c >> 8) & 0xff)), -hy);
+                             double ck = __dadd_rn(int_to_f64((int)(c >> 16)), -hz);
+                             t[0] = v;
+                             t[1] = __dmul_rn(ci, v);
+                             t[2] = __dmul_rn(cj, v);
+                             t[3] = __dmul_rn(ck, v);
+                         },
+                         leafval, sums, lane);
+        float4 cf;
+        {
+            double out0 = __ddiv_rn(sums[0], (double)vol);
+            double sl[3];
+            int ext[3] = {B.bx, B.by, B.bz};
+#pragma unroll
+            for (int ax = 0; ax < 3; ax++) {
+                int e = ext[ax];
+                if (e == 1) { sl[ax] = 0.0; continue; }
+                double denom = __ddiv_rn((double)((long long)vol * ((long long)e * e - 1)), 12.0);
+                sl[ax] = __ddiv_rn(sums[ax + 1], denom);
+                out0 = __dadd_rn(out0, -__ddiv_rn(__dmul_rn(sl[ax], (double)(e - 1)), 2.0));
+            }
+            cf = make_float4(__double2float_rn(out0), __double2float_rn(sl[0]),
+                             __double2float_rn(sl[1]), __double2float_rn(sl[2]));
+        }
+        // hooks after stage (a): COEFFS_FITTED then INPUT_AFTER_CHECKSUM (pipeline.py:328-329)
+        bool touched = false;
+        if (A.n_faults) {
+            int f0 = A.fault_first[b];
+            if (f0 >= 0) {
+                for (int f = f0; f < A.n_faults && A.faults[f].block == b; f++) {
+                    ftlz_fault F = A.faults[f];
+                    if (F.target == FTLZ_FAULT_COEFF) {
+                        float* c4 = (float*)&cf;
+                        c4[F.element] = __uint_as_float(__float_as_uint(c4[F.element]) ^ (1u << F.bit));
+                    } else if (F.target == FTLZ_FAULT_INPUT) {
+                        if (lane == 0) xf[F.element] = __uint_as_float(__float_as_uint(xf[F.element]) ^ (1u << F.bit));
+                        touched = true;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        bool bad = false;
+        if (touched) {
+            // stage (b) verification against the stage (a) checksum (pipeline.py:331-348)
+            if (A.protect_input) {
+                int r = warp_correct_words((u32*)xf, vol, s, si, lane);
+                if (r == 1 && lane == 0) { A.events[b] |= 1; atomicAdd(&A.counters[3], 1u); }
+                if (r == 2) {
+                    bad = true;
+                    if (lane == 0) { A.events[b] |= 4; atomicAdd(&A.counters[3], 1u); }
+                }
+            }
+            __syncwarp();
+            for (int p = lane; p < vol; p += 32) xd[p] = f32_to_f64(xf[p]);
+            __syncwarp();
+        }
+        if (!bad) {
+            // sampled selection (predict.py:196-231): |x - pred| on lanes, pairwise sums
+            int ns = PL.ns;
+            double c0 = (double)cf.x, c1 = (double)cf.y, c2 = (double)cf.z, c3 = (double)cf.w;
+            int byz = B.by * B.bz;
+            for (int q = lane; q < ns; q += 32) {
+                int p = 8 * (q + 1);
+                u32 c = __ldg(crd + p);
+                int i = c & 0xff, j = (c >> 8) & 0xff, k = c >> 16;
+                double v = xd[p];
+                double pr = __dadd_rn(__dadd_rn(__dadd_rn(c0, __dmul_rn(c1, int_to_f64(i))), __dmul_rn(c2, int_to_f64(j))),
+                                      __dmul_rn(c3, int_to_f64(k)));
+                double d100 = i > 0 ? xd[p - byz] : 0.0;
+                double d010 = j > 0 ? xd[p - B.bz] : 0.0;
+                double d001 = k > 0 ? xd[p - 1] : 0.0;
+                double d110 = (i > 0 && j > 0) ? xd[p - byz - B.bz] : 0.0;
+                double d101 = (i > 0 && k > 0) ? xd[p - byz - 1] : 0.0;
+                double d011 = (j > 0 && k > 0) ? xd[p - B.bz - 1] : 0.0;
+                double d111 = (i > 0 && j > 0 && k > 0) ? xd[p - byz - B.bz - 1] : 0.0;
+                double pl = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(d100, d010), d001), -d110), -d101), -d011), d111);
+                ar[q] = fabs(__dadd_rn(v, -pr));
+                al[q] = fabs(__dadd_rn(v, -pl));
+            }
+            __syncwarp();
+            double e2[2];
+            warp_pairwise<2>(A.leaves + PL.sleaf_off, PL.nsleaf, ns,
+                             [&](int q, double* t) { t[0] = ar[q]; t[1] = al[q]; }, leafval, e2, lane);
+            double er = e2[0], el = e2[1];
+            if (A.n_faults) {
+                int f0 = A.fault_first[b];
+                if (f0 >= 0)
+                    for (int f = f0; f < A.n_faults && A.faults[f].block == b; f++) {
+                        ftlz_fault F = A.faults[f];
+                        if (F.target != FTLZ_FAULT_ESTIMATE) continue;
+                        u64 bit = 1ull << F.bit;
+                        if (F.element == 0) er = __longlong_as_double((long long)(dbits(er) ^ bit));
+                        else el = __longlong_as_double((long long)(dbits(el) ^ bit));
+                    }
+            }
+            int kind = er < el ? 1 : 0;
+            if (A.override_ && A.override_[b] >= 0) kind = A.override_[b];
+            if (lane == 0) {
+                A.coef[b] = cf;
+                A.insum[b] = s;
+                A.inisum[b] = si;
+                A.ind[b] = (u8)kind;
+                if (kind == 1) atomicAdd(&cta_nreg, 1u);
+            }
+        } else if (lane == 0) {
+            A.ind[b] = 0;
+            A.coef[b] = cf;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        atomicMax(&A.minmax[0], cta_max);
+        atomicMax(&A.minmax[1], ~cta_min);
+        if (cta_nan) atomicOr(&A.minmax[2], 1u);
+        if (cta_nreg) atomicAdd(&A.counters[0], cta_nreg);
+    }
+}
+
+// ==========================================================================================
+// resolve the bound (core.py:182-193) and the quantizer constants
+__global__ void k_resolve(CompArgs A) {
+    double eb = A.eb_value;
+    if (A.eb_mode == 1) {
+        float mx = ord2f(A.minmax[0]), mn = ord2f(~A.minmax[1]);
+        double range = A.minmax[2] ? __longlong_as_double(0x7ff8000000000000ll)
+                                   : __dadd_rn((double)mx, -(double)mn);
+        eb = __dmul_rn(A.eb_value, range);
+    }
+    QuantParams Q;
+    Q.eb = eb;
+    Q.twoeb = __dmul_rn(2.0, eb);
+    Q.rcp = __ddiv_rn(1.0, Q.twoeb);
+    Q.cap = A.cap;
+    Q.center = A.cap / 2;
+    Q.capd2 = 2.0 * (double)A.cap;
+    Q.capd2_bits = dbits(Q.capd2);
+    Q.eb_bits = dbits(eb);
+    u64 tb = dbits(Q.twoeb) & 0x7fffffffffffffffull, rb = dbits(Q.rcp) & 0x7fffffffffffffffull;
+    bool normal = tb >= 0x0010000000000000ull && tb < 0x7ff0000000000000ull &&
+                  rb >= 0x0010000000000000ull && rb < 0x7ff0000000000000ull;
+    Q.exact_div = normal ? 0 : 1;
+    *A.qp = Q;
+    A.layout[LAYOUT_EB_BITS] = dbits(eb);
+    if (!(eb > 0.0) || !(dbits(eb) < 0x7ff0000000000000ull)) {
+        dev_fail(A.st, FTLZ_ERR_DEGENERATE_BOUND, FTLZ_K_DEGENERATE, -1, -1, 0, 0, 0);
+        return;
+    }
+    // uncorrectable input from stage (b) -> first in extent-sorted group order is chosen
+    // by the host from events (pipeline.py:342-345); flag it here
+}
+
+// ==========================================================================================
+// K2: stage (c)
+struct DupPred {
+    double v;
+    bool mismatch;
+    bool disagree;
+};
+
+// 2-of-3 voting (pipeline.py:157-179) on scalars; eval3 called only on mismatch
+template <typename F3>
+FTLZ_DEV DupPred vote(double a, double b, bool enabled, F3 eval3) {
+    DupPred r;
+    r.v = a;
+    r.mismatch = false;
+    r.disagree = false;
+    if (!enabled) return r;
+    if (dbits(a) == dbits(b)) return r;
+    double c = eval3();
+    r.mismatch = true;
+    bool ab = false, ac = dbits(a) == dbits(c), bc = dbits(b) == dbits(c);
+    r.v = (ab || ac) ? a : b;
+    r.disagree = !(ab || bc || ac);
+    return r;
+}
+
+__global__ void __launch_bounds__(128) k_quant(CompArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const Geom& g = A.g;
+    if (dev_failed(A.st)) return;
+    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    long long b = (long long)blockIdx.x * A.P + warp;
+    BlockInfo B = block_info(g, b);
+    if (!B.valid) return;
+    if (A.events[b] & 4) return;  // stage (b) already failed this block
+    const QuantParams Q = *A.qp;
+    unsigned char* slot = smem + (size_t)warp * A.nwarp_smem;
+    float* xf = (float*)slot;
+    double* xd = (double*)(slot + slot_f64_off(g.vmax));
+    u16* bins16 = (u16*)(xd + g.vmax);
+    double* tabA = (double*)(((uintptr_t)(bins16 + g.vmax) + 15) & ~(uintptr_t)15);
+    double* tabB = tabA + 64;
+    double* tabC = tabB + 64;
+    load_block_rows(A.x, g, B, xf, lane);
+    __syncwarp();
+    int vol = B.vol;
+    // working-array faults persist only when stage (b) could not heal them (pipeline.py:331-361)
+    if (A.n_faults && !A.protect_input) {
+        int f0 = A.fault_first[b];
+        if (f0 >= 0 && lane == 0)
+            for (int f = f0; f < A.n_faults && A.faults[f].block == b; f++)
+                if (A.faults[f].target == FTLZ_FAULT_INPUT)
+                    xf[A.faults[f].element] = __uint_as_float(__float_as_uint(xf[A.faults[f].element]) ^ (1u << A.faults[f].bit));
+        __syncwarp();
+    }
+    if (A.protect_input) {
+        // stage (c) verification of the re-read input against the stage (a) checksum
+        int r = warp_correct_words((u32*)xf, vol, A.insum[b], A.inisum[b], lane);
+        if (r == 1 && lane == 0) { A.events[b] |= 1; atomicAdd(&A.counters[3], 1u); }
+        if (r == 2) {
+            if (lane == 0) { A.events[b] |= 4; atomicAdd(&A.counters[3], 1u); }
+            return;
+        }
+        __syncwarp();
+    }
+    const ExtPlan& PL = A.plans[B.xid];
+    const u32* crd = A.coords + PL.coord_off;
+    int kind = A.ind[b];
+    float4 cf = A.coef[b];
+    bool dup = A.dup_eval != 0;
+    bool mism = false;
+    u64 dcsum = 0;
+    int byz = B.by * B.bz;
+    if (kind == 1) {
+        double c0 = (double)cf.x, c1 = (double)cf.y, c2 = (double)cf.z, c3 = (double)cf.w;
+        // A[i] = b0 + b1*i (rounded), B[j] = b2*j, C[k] = b3*k (exact products)
+        for (int t = lane; t < 64; t += 32) {
+            tabA[t] = __dadd_rn(c0, __dmul_rn(c1, int_to_f64(t)));
+            tabB[t] = __dmul_rn(c2, int_to_f64(t));
+            tabC[t] = __dmul_rn(c3, int_to_f64(t));
+        }
+        __syncwarp();
+        for (int p = lane; p < vol; p += 32) {
+            u32 c = __ldg(crd + p);
+            int i = c & 0xff, j = (c >> 8) & 0xff, k = c >> 16;
+            float x32 = xf[p];
+            double x64 = f32_to_f64(x32);
+            double p1 = __dadd_rn(__dadd_rn(tabA[i], tabB[j]), tabC[k]);
+            double p2 = dup ? __dadd_rn(__dadd_rn(opaque(tabA[i]), tabB[j]), tabC[k]) : p1;
+            DupPred pr = vote(p1, p2, dup, [&] {
+                return __dadd_rn(__dadd_rn(__dadd_rn(c0, __dmul_rn(c1, int_to_f64(i))), __dmul_rn(c2, int_to_f64(j))),
+                                 __dmul_rn(c3, int_to_f64(k)));
+            });
+            double pred = pr.v;
+            bool ok;
+            int bin = quantize(Q, __dadd_rn(x64, -pred), &ok);
+            if (pr.disagree) ok = false;
+            double offs = int_to_f64(bin - Q.center);
+            double d1 = __dadd_rn(pred, __dmul_rn(Q.twoeb, offs));
+            double d2 = dup ? __dadd_rn(opaque(pred), __dmul_rn(Q.twoeb, offs)) : d1;
+            DupPred dr = vote(d1, d2, dup, [&] { return __dadd_rn(pred, __dmul_rn(Q.twoeb, opaque(offs))); });
+            if (dr.disagree) ok = false;
+            mism |= pr.mismatch | dr.mismatch;
+            float d32 = __double2float_rn(dr.v);
+            bool keep = ok && within_eb(__dadd_rn(x64, -f32_to_f64(d32)), Q.eb_bits);
+            float r32 = keep ? d32 : x32;
+            bins16[p] = (u16)(keep ? bin : 0);
+            dcsum += __float_as_uint(r32);
+        }
+    } else {
+        // Lorenzo wavefront over constant i+j+k planes (pipeline.py:199-213, 410-438);
+        // xd holds float64 reconstructed values in place (only earlier planes are read)
+        const u32* wave = A.wave + PL.wave_off;
+        const u32* planes = A.planes + PL.plane_off;
+        int bz = B.bz;
+        for (int s = 0; s < PL.nplanes; s++) {
+            int q0 = __ldg(planes + s), q1 = __ldg(planes + s + 1);
+            for (int q = q0 + lane; q < q1; q += 32) {
+                int p = __ldg(wave + q);
+                u32 c = __ldg(crd + p);
+                int i = c & 0xff, j = (c >> 8) & 0xff, k = c >> 16;
+                float x32 = xf[p];
+                double x64 = f32_to_f64(x32);
+                double d100 = i > 0 ? xd[p - byz] : 0.0;
+                double d010 = j > 0 ? xd[p - bz] : 0.0;
+                double d001 = k > 0 ? xd[p - 1] : 0.0;
+                double d110 = (i > 0 && j > 0) ? xd[p - byz - bz] : 0.0;
+                double d101 = (i > 0 && k > 0) ? xd[p - byz - 1] : 0.0;
+                double d011 = (j > 0 && k > 0) ? xd[p - bz - 1] : 0.0;
+                double d111 = (i > 0 && j > 0 && k > 0) ? xd[p - byz - bz - 1] : 0.0;
+                auto lor = [&](double first) {
+                    return __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(first, d010), d001), -d110), -d101), -d011), d111);
+                };
+                double p1 = lor(d100);
+                double p2 = dup ? lor(opaque(d100)) : p1;
+                DupPred pr = vote(p1, p2, dup, [&] { return lor(opaque(opaque(d100))); });
+                double pred = pr.v;
+                bool ok;
+                int bin = quantize(Q, __dadd_rn(x64, -pred), &ok);
+                if (pr.disagree) ok = false;
+                double offs = int_to_f64(bin - Q.center);
+                double d1 = __dadd_rn(pred, __dmul_rn(Q.twoeb, offs));
+                double d2 = dup ? __dadd_rn(opaque(pred), __dmul_rn(Q.twoeb, offs)) : d1;
+                DupPred dr = vote(d1, d2, dup, [&] { return __dadd_rn(pred, __dmul_rn(Q.twoeb, opaque(offs))); });
+                if (dr.disagree) ok = false;
+                mism |= pr.mismatch | dr.mismatch;
+                float d32 = __double2float_rn(dr.v);
+                double back = f32_to_f64(d32);
+                bool keep = ok && within_eb(__dadd_rn(x64, -back), Q.eb_bits);
+                float r32 = keep ? d32 : x32;
+                xd[p] = keep ? back : x64;
+                bins16[p] = (u16)(keep ? bin : 0);
+                dcsum += __float_as_uint(r32);
+            }
+            __syncwarp();
+        }
+    }
+    __syncwarp();
+    // emit pass in row-major order: unpredictable words, bins checksum, histogram, bins store
+    u64 bs = 0, bis = 0;
+    u32 nunp = 0;
+    u32* unp = A.unp_scratch + (size_t)b * g.vmax;
+    for (int p0 = 0; p0 < vol; p0 += 32) {
+        int p = p0 + lane;
+        bool act = p < vol;
+        int bin = act ? bins16[p] : -1;
+        unsigned zm = __ballot_sync(0xffffffffu, bin == 0);
+        if (bin == 0) unp[nunp + __popc(zm & ((1u << lane) - 1u))] = __float_as_uint(xf[p]);
+        nunp += __popc(zm);
+        if (act) {
+            bs += (u64)bin;
+            bis += (u64)p * (u64)bin;
+            A.bins[bins_index(g, b, p)] = (u16)bin;
+        }
+        // warp-aggregated histogram update
+        unsigned peers = __match_any_sync(0xffffffffu, bin);
+        if (act && lane == __ffs(peers) - 1) atomicAdd(&A.hist[bin], (u32)__popc(peers));
+    }
+    dcsum = warp_sum_u64(dcsum);
+    bs = warp_sum_u64(bs);
+    bis = warp_sum_u64(bis);
+    unsigned anym = __ballot_sync(0xffffffffu, mism);
+    if (lane == 0) {
+        A.unpc[b] = nunp;
+        if (nunp) atomicAdd((u64*)&A.layout[LAYOUT_NUNP], (u64)nunp);
+        A.bsum[b] = bs;
+        A.bisum[b] = bis;
+        A.dcs[b] = dcsum;
+        if (anym) atomicOr(&A.counters[1], 1u << (B.xid * 2 + kind));
+    }
+}
+
+// ==========================================================================================
+// K3: canonical Huffman codebook (encode.py:26-71) on one CTA.
+// Two-queue merge over leaves sorted by (weight, symbol) reproduces the heap with
+// (weight, tiebreak) keys exactly: leaf ties break by symbol rank, merged nodes are created
+// in non-decreasing weight order and pop FIFO, and a leaf wins a weight tie against any
+// merged node (its tiebreak < n <= every merged tiebreak).
+#define CB_THREADS 1024
+#define CB_SMEM_KEYS 8192
+
+struct CodebookScratch {
+    u64* keys;     // 2 * cap (sorted leaves; later (len, sym) keys)
+    u32* syms;     // cap (sorted by weight order)
+    u64* w;        // 2 * cap node weights (leaves then internal)
+    u32* parent;   // 2 * cap
+    u8* lens;      // cap (by symbol)
+};
+
+__global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScratch S) {
+    if (dev_failed(A.st)) return;
+    extern __shared__ __align__(16) u64 cb_dyn[];   // keys[CB_SMEM_KEYS] | weights[2*CB_SMEM_KEYS]
+    u64* skeys = cb_dyn;
+    __shared__ u32 wcount[33];
+    __shared__ u64 lencount[64];
+    __shared__ u64 firstcode[64];
+    __shared__ u32 firstidx[64];
+    __shared__ int s_n, s_maxlen, s_np2;
+    __shared__ u64 s_total;
+    int cap = A.cap;
+    int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // bins verification failures (stage d) happen in k_encode; histogram of clean bins here.
+    // 1) compact alphabet in symbol order: {0} U {s : hist[s] > 0}
+    int per = (cap + CB_THREADS - 1) / CB_THREADS;
+    int s0 = tid * per, s1 = min(cap, s0 + per);
+    int cnt = 0;
+    for (int s = s0; s < s1; s++) cnt += (A.hist[s] > 0 || s == 0);
+    int inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) wcount[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        int v = wcount[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += t;
+        }
+        wcount[lane] = v;
+        if (lane == 31) s_n = v;
+    }
+    __syncthreads();
+    int n = s_n;
+    int pos = (warp ? wcount[warp - 1] : 0) + inc - cnt;
+    int np2 = 1;
+    while (np2 < n) np2 <<= 1;
+    u64* keys = np2 <= CB_SMEM_KEYS ? skeys : S.keys;
+    for (int s = s0; s < s1; s++) {
+        u32 h = A.hist[s];
+        if (h > 0 || s == 0) keys[pos++] = ((u64)h << 16) | (u64)s;   // (weight, symbol)
+    }
+    for (int i = n + tid; i < np2; i += CB_THREADS) keys[i] = ~0ull;
+    __syncthreads();
+    bitonic_sort_u64(keys, np2);
+    // 2) two-queue merge (sequential, one thread); node ids: leaves 0..n-1 in sorted order,
+    //    merged nodes n..2n-2
+    if (tid == 0) {
+        s_maxlen = 0;
+        if (n == 1) {
+            S.parent[0] = 0xffffffffu;
+        } else {
+            u64* W = np2 <= CB_SMEM_KEYS ? cb_dyn + CB_SMEM_KEYS : S.w;
+            for (int i = 0; i < n; i++) W[i] = keys[i] >> 16;
+            int li = 0, mi = n, mk = n;  // next leaf, next merged to consume, next merged to create
+            for (int t = 0; t < n - 1; t++) {
+                int pick[2];
+#pragma unroll
+                for (int r = 0; r < 2; r++) {
+                    if (li < n && (mi >= mk || W[li] <= W[mi])) pick[r] = li++;
+                    else pick[r] = mi++;
+                }
+                W[mk] = W[pick[0]] + W[pick[1]];
+                S.parent[pick[0]] = (u32)mk;
+                S.parent[pick[1]] = (u32)mk;
+                mk++;
+            }
+            S.parent[mk - 1] = 0xffffffffu;
+        }
+    }
+    __syncthreads();
+    // 3) depths by walking parent pointers (parallel over leaves)
+    int root = n == 1 ? 0 : 2 * n - 2;
+    int mymax = 0;
+    for (int i = tid; i < n; i += CB_THREADS) {
+        int d = 0;
+        if (n == 1) d = 1;
+        else {
+            u32 v = (u32)i;
+            while (v != (u32)root) { v = S.parent[v]; d++; }
+        }
+        u32 sym = (u32)(keys[i] & 0xffff);
+        S.lens[sym] = (u8)min(d, 255);
+        S.syms[i] = sym;
+        mymax = max(mymax, d);
+    }
+    atomicMax(&s_maxlen, mymax);
+    __syncthreads();
+    int maxlen = s_maxlen;
+    if (maxlen > 57) {
+        if (tid == 0) dev_fail(A.st, FTLZ_ERR_INVARIANT, FTLZ_K_CODE_LEN, -1, -1, maxlen, 0, 0);
+        return;
+    }
+    // 4) canonical codes by (length, symbol): sort keys (len << 16 | sym)
+    for (int i = tid; i < np2; i += CB_THREADS) {
+        if (i < n) {
+            u32 sym = S.syms[i];
+            keys[i] = ((u64)S.lens[sym] << 16) | sym;
+        } else keys[i] = ~0ull;
+    }
+    if (tid < 64) lencount[tid] = 0;
+    __syncthreads();
+    bitonic_sort_u64(keys, np2);
+    for (int i = tid; i < n; i += CB_THREADS) atomicAdd(&lencount[keys[i] >> 16], 1ull);
+    __syncthreads();
+    if (tid == 0) {
+        u64 code = 0;
+        u32 idx = 0;
+        for (int l = 1; l <= 57; l++) {
+            firstcode[l] = code;
+            firstidx[l] = idx;
+            code = (code + lencount[l]) << 1;
+            idx += (u32)lencount[l];
+        }
+    }
+    __syncthreads();
+    u64 tot = 0;
+    for (int i = tid; i < n; i += CB_THREADS) {
+        int l = (int)(keys[i] >> 16);
+        u32 sym = (u32)(keys[i] & 0xffff);
+        u64 code = firstcode[l] + (u64)(i - firstidx[l]);
+        A.enc[sym] = (code << 6) | (u64)l;
+        tot += (u64)A.hist[sym] * (u64)l;
+    }
+    tot = warp_sum_u64(tot);
+    if (tid == 0) s_total = 0;
+    __syncthreads();
+    if (lane == 0) atomicAdd(&s_total, tot);
+    __syncthreads();
+    // 5) archive layout (container.py:3-27)
+    long long nb = A.g.nb;
+    u64 nreg = A.counters[0], nunp = A.layout[LAYOUT_NUNP];
+    u64 table_len = 9ull * (u64)nb + 16ull * nreg;
+    u64 book_off = 55 + table_len;
+    u64 paylen_off = book_off + 4 + 5ull * (u64)n;
+    u64 pay_off = paylen_off + 8;
+    u64 pay_bytes = (s_total + 7) / 8;
+    u64 unp_off = pay_off + pay_bytes;
+    u64 sdc_off = unp_off + 4 * nunp;
+    u64 total = sdc_off + 16 + (A.store_sum_dc ? 8ull * (u64)nb : 0);
+    if (tid == 0) {
+        A.layout[LAYOUT_TABLE_LEN] = table_len;
+        A.layout[LAYOUT_BOOK_OFF] = book_off;
+        A.layout[LAYOUT_NSYM] = (u64)n;
+        A.layout[LAYOUT_PAYLEN_OFF] = paylen_off;
+        A.layout[LAYOUT_PAY_OFF] = pay_off;
+        A.layout[LAYOUT_PAY_BYTES] = pay_bytes;
+        A.layout[LAYOUT_UNP_OFF] = unp_off;
+        A.layout[LAYOUT_SDC_OFF] = sdc_off;
+        A.layout[LAYOUT_TOTAL] = total;
+        A.layout[LAYOUT_TOTAL_BITS] = s_total;
+        A.layout[LAYOUT_MAXLEN] = (u64)maxlen;
+        A.layout[LAYOUT_NREG] = nreg;
+        if (total > A.out_cap) dev_fail(A.st, FTLZ_ERR_CAPACITY, 0, -1, -1, (long long)total, 0, 0);
+    }
+    __syncthreads();
+    if (total > A.out_cap) return;
+    // 6) codebook section: u32 count, then (u32 symbol, u8 length) in ascending symbol order
+    u8* o = A.out + book_off;
+    if (tid < 4) o[tid] = (u8)(n >> (8 * tid));
+    // symbols in ascending order: re-derive rank by scanning the histogram chunk again
+    pos = (warp ? wcount[warp - 1] : 0) + inc - cnt;
+    for (int s = s0; s < s1; s++) {
+        if (A.hist[s] > 0 || s == 0) {
+            u8* e = o + 4 + 5ull * (u64)pos;
+            e[0] = (u8)s; e[1] = (u8)(s >> 8); e[2] = (u8)(s >> 16); e[3] = (u8)(s >> 24);
+            e[4] = S.lens[s];
+            pos++;
+        }
+    }
+}
+
+// ==========================================================================================
+__global__ void k_zero(CompArgs A) {
+    if (dev_failed(A.st)) return;
+    u64 off = A.layout[LAYOUT_PAY_OFF], nbytes = A.layout[LAYOUT_PAY_BYTES];
+    u64 w0 = off >> 2, w1 = (off + nbytes + 3) >> 2;
+    u32* w = (u32*)A.out;
+    for (u64 i = w0 + (u64)blockIdx.x * blockDim.x + threadIdx.x; i < w1; i += (u64)gridDim.x * blockDim.x) w[i] = 0;
+}
+
+// ==========================================================================================
+// bins-stage faults (STAGE_BINS_FINALIZED, pipeline.py:468-496).  For every block a fault
+// touched, rebuild its 32-bit words (virtual words), run the reference
+// verify/correct when protect_bins is on (checksum.py:109-142), and move the histogram
+// counts of every word that differs from the clean bin (the reference builds its histogram
+// from the verified -- possibly mis-corrected -- bins, pipeline.py:484-492).  The encoder
+// then reads these words from fix_scratch.
+__global__ void k_fault_bins(CompArgs A, u32* fix_scratch, u8* fixed) {
+    if (dev_failed(A.st)) return;
+    const Geom& g = A.g;
+    for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < g.nb; b += (long long)gridDim.x * blockDim.x) {
+        int f0 = A.fault_first[b];
+        if (f0 < 0) continue;
+        bool any = false;
+        for (int f = f0; f < A.n_faults && A.faults[f].block == b; f++) any |= A.faults[f].target == FTLZ_FAULT_BINS;
+        if (!any) continue;
+        BlockInfo B = block_info(g, b);
+        int vol = B.vol;
+        u32* w = fix_scratch + (size_t)b * g.vmax;
+        for (int p = 0; p < vol; p++) w[p] = A.bins[bins_index(g, b, p)];
+        for (int f = f0; f < A.n_faults && A.faults[f].block == b; f++)
+            if (A.faults[f].target == FTLZ_FAULT_BINS) w[A.faults[f].element] ^= 1u << A.faults[f].bit;
+        if (A.protect_bins) {
+            u64 s = 0, si = 0;
+            for (int p = 0; p < vol; p++) { s += w[p]; si += (u64)p * w[p]; }
+            int status = 0;
+            if (s != A.bsum[b] || si != A.bisum[b]) {
+                status = 2;
+                u64 ds = s - A.bsum[b], dsi = si - A.bisum[b];
+                if (ds != 0) {
+                    for (int j = 0; j < vol && status == 2; j++) {
+                        if ((u64)j * ds != dsi) continue;
+                        u64 old = w[j], rest = old - ds;
+                        if (rest >> 32) continue;
+                        w[j] = (u32)rest;
+                        u64 s2 = 0, si2 = 0;
+                        for (int p = 0; p < vol; p++) { s2 += w[p]; si2 += (u64)p * w[p]; }
+                        if (s2 == A.bsum[b] && si2 == A.bisum[b]) status = 1;
+                        else w[j] = (u32)old;
+                    }
+                }
+            }
+            if (status == 1) { A.events[b] |= 2; atomicAdd(&A.counters[3], 1u); }
+            if (status == 2) {
+                A.events[b] |= 8;
+                atomicAdd(&A.counters[3], 1u);
+                continue;
+            }
+        }
+        for (int p = 0; p < vol; p++) {
+            u32 orig = A.bins[bins_index(g, b, p)];
+            if (w[p] == orig) continue;
+            if (w[p] >= (u32)A.cap) {
+                dev_fail(A.st, FTLZ_ERR_INVARIANT, FTLZ_K_BIN_RANGE, -1, -1, 0, 0, 0);
+                continue;
+            }
+            atomicSub(&A.hist[orig], 1u);
+            atomicAdd(&A.hist[w[p]], 1u);
+        }
+        fixed[b] = 1;
+    }
+}
+
+// ==========================================================================================
+// K4: encode.  Lane = block; a CTA of ENC_WARPS warps covers 32*ENC_WARPS consecutive blocks.
+// Pass 1: verify/correct the bin array (stage d, pipeline.py:473-495) and sum code lengths.
+// Decoupled look-back over CTAs (tickets in launch order) gives global bit offsets and the
+// block-table / unpredictable-section prefixes.
+// Pass 2: MSB-first packing (encode.py:117-140) into 32-bit big-endian words of the archive.
+#define ENC_WARPS 4
+#define ENC_BLOCKS (ENC_WARPS * 32)
+
+FTLZ_DEV u32 bswap32(u32 v) { return __byte_perm(v, 0, 0x0123); }
+
+FTLZ_DEV void put_word(u32* words, u64 widx, u32 bits_be, bool partial) {
+    u32 v = bswap32(bits_be);
+    if (partial) atomicOr(words + widx, v);
+    else words[widx] = v;
+}
+
+// iterate the bin symbols of block b in order; 8 bins per 16-byte load.  Blocks touched by
+// bins-stage faults read their verified 32-bit words from fix_scratch (k_fault_bins).
+template <typename F>
+FTLZ_DEV void for_each_bin(const CompArgs& A, long long b, int vol, const u32* fixed, F fn) {
+    if (fixed) {
+        for (int p = 0; p < vol; p++) fn(p, fixed[p]);
+        return;
+    }
+    for (int p8 = 0; p8 < vol; p8 += 8) {
+        uint4 v = __ldg((const uint4*)(A.bins + bins_index(A.g, b, p8)));
+        u32 w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int t = 0; t < 8; t++) {
+            int p = p8 + t;
+            if (p < vol) fn(p, (w[t >> 1] >> ((t & 1) * 16)) & 0xffffu);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(ENC_BLOCKS) k_encode(CompArgs A, u32* fix_scratch, const u8* fixed_flag, u32* lb_flag,
+                                                       u64* lb_bits, u64* lb_reg, u64* lb_unp) {
+    if (dev_failed(A.st)) return;
+    const Geom& g = A.g;
+    __shared__ u64 s_enc[4096];    // symbols in [center-2048, center+2048)
+    __shared__ u64 s_w[3][ENC_WARPS];
+    __shared__ u64 s_pre[3];
+    __shared__ unsigned s_tile;
+    int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int wlo = A.center - 2048;
+    for (int t = tid; t < 4096; t += blockDim.x) {
+        int s = wlo + t;
+        s_enc[t] = (s >= 0 && s < A.cap) ? A.enc[s] : 0ull;
+    }
+    if (tid == 0) s_tile = atomicAdd(&A.counters[2], 1u);
+    __syncthreads();
+    unsigned tile = s_tile;
+    long long b = (long long)tile * ENC_BLOCKS + tid;
+    bool valid = b < g.nb;
+    int vol = 0, f0 = -1;
+    if (valid) {
+        BlockInfo B = block_info(g, b);
+        vol = B.vol;
+        if (A.n_faults) f0 = A.fault_first[b];
+    }
+    auto lookup = [&](u32 sym) -> u64 {
+        return (sym - (u32)wlo) < 4096u ? s_enc[sym - wlo] : (sym < (u32)A.cap ? A.enc[sym] : 0ull);
+    };
+    // pass 1: bit length (bins verification of faulted blocks already ran in k_fault_bins)
+    u64 bits = 0;
+    const u32* fixed = nullptr;
+    bool bad = false;
+    if (valid) {
+        if (f0 >= 0 && fixed_flag[b]) fixed = fix_scratch + (size_t)b * g.vmax;
+        if (A.events[b] & 8) bad = true;
+        if (!bad)
+            for_each_bin(A, b, vol, fixed, [&](int p, u32 sym) {
+                u32 l = (u32)(lookup(sym) & 63);
+                if (l == 0) {
+                    dev_fail(A.st, FTLZ_ERR_INVARIANT, FTLZ_K_BIN_RANGE, -1, b, 0, 0, 0);
+                    l = 1;
+                }
+                bits += l;
+            });
+    }
+    // CTA-wide inclusive scans of (bits, regression records, unpredictable words)
+    u64 v3[3] = {bits, valid ? (u64)A.ind[b] : 0ull, valid ? (u64)A.unpc[b] : 0ull};
+    u64 inc[3];
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        inc[q] = v3[q];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            u64 t = __shfl_up_sync(0xffffffffu, inc[q], o);
+            if (lane >= o) inc[q] += t;
+        }
+        if (lane == 31) s_w[q][warp] = inc[q];
+    }
+    __syncthreads();
+    u64 woff[3] = {0, 0, 0}, tsum[3] = {0, 0, 0};
+#pragma unroll
+    for (int q = 0; q < 3; q++)
+        for (int w = 0; w < ENC_WARPS; w++) {
+            if (w < warp) woff[q] += s_w[q][w];
+            tsum[q] += s_w[q][w];
+        }
+    if (tid == 0) {
+        // flag: 0 = empty, 1 = aggregate published, 2 = inclusive prefix published
+        volatile u64* vb = lb_bits; volatile u64* vr = lb_reg; volatile u64* vu = lb_unp;
+        volatile u32* vf = lb_flag;
+        u64 pre[3] = {0, 0, 0};
+        if (tile > 0) {
+            vb[2 * tile] = tsum[0]; vr[2 * tile] = tsum[1]; vu[2 * tile] = tsum[2];
+            __threadfence();
+            vf[tile] = 1;
+            long long t = (long long)tile - 1;
+            while (t >= 0) {
+                u32 f = vf[t];
+                if (f == 0) continue;
+                __threadfence();
+                int sl = f == 2 ? 1 : 0;
+                pre[0] += vb[2 * t + sl]; pre[1] += vr[2 * t + sl]; pre[2] += vu[2 * t + sl];
+                if (f == 2) break;
+                t--;
+            }
+        }
+        vb[2 * tile + 1] = pre[0] + tsum[0]; vr[2 * tile + 1] = pre[1] + tsum[1]; vu[2 * tile + 1] = pre[2] + tsum[2];
+        __threadfence();
+        vf[tile] = 2;
+        s_pre[0] = pre[0]; s_pre[1] = pre[1]; s_pre[2] = pre[2];
+    }
+    __syncthreads();
+    if (!valid || bad) return;
+    u64 start = s_pre[0] + woff[0] + inc[0] - bits;   // bit offset of this block in the payload
+    A.bitlen[b] = (u32)bits;
+    A.regpre[b] = (u32)(s_pre[1] + woff[1] + inc[1] - v3[1]);
+    A.unppre[b] = s_pre[2] + woff[2] + inc[2] - v3[2];
+    if (dev_failed(A.st)) return;
+    // pass 2: pack
+    u64 gpos = A.layout[LAYOUT_PAY_OFF] * 8 + start;  // absolute bit in the archive
+    u32* words = (u32*)A.out;
+    u64 widx = gpos >> 5;
+    u64 acc = 0;                          // pending bits, left-aligned at bit 63
+    int nacc = (int)(gpos & 31);          // the first bits of the word belong to the previous block
+    bool first = true;
+    for_each_bin(A, b, vol, fixed, [&](int p, u32 sym) {
+        u64 e = lookup(sym);
+        int l = (int)(e & 63);
+        u64 code = e >> 6;
+        if (l > 32) {
+            int hl = l - 32;
+            acc |= (code >> 32) << (64 - nacc - hl);
+            nacc += hl;
+            if (nacc >= 32) {
+                put_word(words, widx++, (u32)(acc >> 32), first);
+                first = false;
+                acc <<= 32;
+                nacc -= 32;
+            }
+            code &= 0xffffffffull;
+            l = 32;
+        }
+        acc |= code << (64 - nacc - l);
+        nacc += l;
+        if (nacc >= 32) {
+            put_word(words, widx++, (u32)(acc >> 32), first);
+            first = false;
+            acc <<= 32;
+            nacc -= 32;
+        }
+    });
+    if (nacc > 0) put_word(words, widx, (u32)(acc >> 32), true);
+}
+
+// ==========================================================================================
+// K5: archive assembly (container.py:109-147)
+FTLZ_DEV void put_le(u8* o, u64 v, int n) {
+    for (int i = 0; i < n; i++) o[i] = (u8)(v >> (8 * i));
+}
+
+__global__ void k_assemble(CompArgs A, ftlz_header H) {
+    if (dev_failed(A.st)) return;
+    const Geom& g = A.g;
+    u8* o = A.out;
+    long long nb = g.nb;
+    long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    long long stride = (long long)gridDim.x * blockDim.x;
+    if (t == 0) {
+        o[0] = 'F'; o[1] = 'T'; o[2] = 'L'; o[3] = 'Z'; o[4] = 1; o[5] = 0;
+        put_le(o + 6, (u64)H.nx, 8); put_le(o + 14, (u64)H.ny, 8); put_le(o + 22, (u64)H.nz, 8);
+        put_le(o + 30, (u64)H.block_edge, 4);
+        o[34] = (u8)H.eb_mode;
+        put_le(o + 35, A.layout[LAYOUT_EB_BITS], 8);
+        put_le(o + 43, (u64)A.cap, 4);
+        put_le(o + 47, (u64)nb, 8);
+        put_le(o + A.layout[LAYOUT_PAYLEN_OFF], A.layout[LAYOUT_PAY_BYTES], 8);
+        u64 so = A.layout[LAYOUT_SDC_OFF];
+        u64 raw = A.store_sum_dc ? 8ull * (u64)nb : 0;
+        put_le(o + so, raw, 8);
+        put_le(o + so + 8, raw, 8);
+    }
+    u64 unp_off = A.layout[LAYOUT_UNP_OFF], sdc_off = A.layout[LAYOUT_SDC_OFF] + 16;
+    for (long long b = t; b < nb; b += stride) {
+        u64 ro = 55 + 9ull * (u64)b + 16ull * (u64)A.regpre[b];
+        u8 ind = A.ind[b];
+        o[ro] = ind;
+        ro++;
+        if (ind) {
+            float4 c = A.coef[b];
+            put_le(o + ro, __float_as_uint(c.x), 4);
+            put_le(o + ro + 4, __float_as_uint(c.y), 4);
+            put_le(o + ro + 8, __float_as_uint(c.z), 4);
+            put_le(o + ro + 12, __float_as_uint(c.w), 4);
+            ro += 16;
+        }
+        u32 nu = A.unpc[b];
+        put_le(o + ro, nu, 4);
+        put_le(o + ro + 4, A.bitlen[b], 4);
+        if (nu) {
+            const u32* src = A.unp_scratch + (size_t)b * g.vmax;
+            u8* d = o + unp_off + 4ull * A.unppre[b];
+            for (u32 i = 0; i < nu; i++) put_le(d + 4ull * i, src[i], 4);
+        }
+        if (A.store_sum_dc) put_le(o + sdc_off + 8ull * (u64)b, A.dcs[b], 8);
+    }
+}
+
+}  // namespace ftlz

@@ -1,0 +1,789 @@
+// decompress.cu -- device side of container.parse (container.py:173-285) and
+// pipeline.decompress (pipeline.py:645-723) for B200 (sm_100a).
+//
+// Kernel sequence:
+//   k_parse_maps     block table, speculative: for every 64-byte chunk and every entry phase
+//                    (0..24) walk the variable-length records (9 or 25 bytes) -> exit phase
+//   k_parse_compose  compose the chunk maps of 256-chunk super-chunks
+//   k_parse_top      one thread threads the super-chunk maps from phase 0
+//   k_parse_records  resolve every chunk's entry phase, emit per-block records, validate
+//   k_scan2          exclusive scans of bit lengths and unpredictable counts (look-back)
+//   k_parse_tail     codebook + section validation, canonical decode tables
+//   k_decode         lane = block: Huffman decode; regression blocks reconstructed in the
+//                    same pass, staged in shared memory and written coalesced; Lorenzo bins to
+//                    scratch; decompressed-data checksum verification (K6)
+//   k_recon_warp     warp = block: Lorenzo wavefront reconstruction from scratch bins + verify;
+//                    reused for re-execution of mismatching blocks (pipeline.py:713-723) (K7)
+#include "common.cuh"
+
+namespace ftlz {
+
+#define PCHUNK 64
+#define PSUPER 256
+#define STUCK 0xffffffffu
+
+enum {
+    DI_TABLE_END = 0, DI_BOOK_OFF, DI_NSYM, DI_MAXLEN, DI_PAY_OFF, DI_PAY_LEN, DI_UNP_OFF,
+    DI_NUNP, DI_SDC_OFF, DI_HAS_SDC, DI_TOTAL_BITS, DI_NREG, DI_T, DI_COUNT
+};
+enum { DC_NLOR = 0, DC_NMIS, DC_TICKET, DC_MINFAIL, DC_COUNT };
+
+struct DecArgs {
+    Geom g;
+    const u8* a;
+    u64 len;
+    int cap, center;
+    double eb, twoeb;
+    int codec;
+    int n_faults;
+    const ftlz_fault* faults;
+    const int* fault_first;
+    const ExtPlan* plans;
+    const u32* coords;
+    const u32* wave;
+    const u32* planes;
+    u32* maps;
+    u32* smaps;
+    u64* sentry;
+    long long nchunks, nsuper;
+    // per block
+    u8* ind;
+    u64* rec_off;
+    u32* unpc;
+    u32* bitlen;
+    u64* bofs;
+    u64* uofs;
+    u8* dflag;
+    long long* da;
+    long long* db;
+    u8* mflag;
+    u32* lor_list;
+    u32* mis_list;
+    u32* counters;
+    u64* info;
+    DevStatus* st;
+    u32* lut;
+    u64* first_code;
+    u32* lcount;
+    u32* lbase;
+    u32* dsym;
+    u64* sortkeys;   // scratch for > 8192 symbols
+    u16* bins;
+    float* out;
+    u32* lb_flag;
+    u64* lb_a;
+    u64* lb_b;
+};
+
+FTLZ_DEV u64 ld_le(const u8* p, int n) {
+    u64 v = 0;
+    for (int i = 0; i < n; i++) v |= (u64)p[i] << (8 * i);
+    return v;
+}
+
+// ------------------------------------------------------------------------------------------
+// block table parse (container.py:212-219)
+__global__ void k_parse_maps(DecArgs A) {
+    long long total = A.nchunks * 25;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        long long c = t / 25;
+        int ph = (int)(t - c * 25);
+        u64 s = 55 + (u64)c * PCHUNK, e = s + PCHUNK;
+        u64 pos = s + ph;
+        u32 cnt = 0;
+        bool stuck = false;
+        while (pos < e) {
+            if (pos >= A.len) { stuck = true; break; }
+            u8 ib = A.a[pos];
+            if (ib > 1) { stuck = true; break; }
+            pos += 9 + 16 * ib;
+            cnt++;
+        }
+        A.maps[t] = stuck ? STUCK : ((u32)(pos - e) | (cnt << 8));
+    }
+}
+
+// map value: exit phase (8 bits) | record count (24 bits); STUCK = error on this path
+FTLZ_DEV u32 compose_walk(const u32* m, int n, u32 state, u32* cnt) {
+    u32 c = 0;
+    for (int i = 0; i < n; i++) {
+        u32 v = m[i * 25 + state];
+        if (v == STUCK) { *cnt = c; return STUCK; }
+        c += v >> 8;
+        state = v & 0xff;
+    }
+    *cnt = c;
+    return state;
+}
+
+__global__ void __launch_bounds__(PSUPER) k_parse_compose(DecArgs A) {
+    __shared__ u32 m[PSUPER * 25];
+    long long sc = blockIdx.x;
+    long long c0 = sc * PSUPER;
+    int n = (int)min((long long)PSUPER, A.nchunks - c0);
+    for (int t = threadIdx.x; t < n * 25; t += blockDim.x) m[t] = A.maps[c0 * 25 + t];
+    __syncthreads();
+    if (threadIdx.x < 25) {
+        u32 cnt;
+        u32 st = compose_walk(m, n, threadIdx.x, &cnt);
+        A.smaps[sc * 25 + threadIdx.x] = st == STUCK ? STUCK : (st | (cnt << 8));
+    }
+}
+
+__global__ void __launch_bounds__(256) k_parse_top(DecArgs A) {
+    __shared__ u32 m[256 * 25];
+    __shared__ u32 s_state;
+    __shared__ u64 s_base;
+    if (threadIdx.x == 0) { s_state = 0; s_base = 0; }
+    for (long long w0 = 0; w0 < A.nsuper; w0 += 256) {
+        int n = (int)min(256ll, A.nsuper - w0);
+        __syncthreads();
+        for (int t = threadIdx.x; t < n * 25; t += blockDim.x) m[t] = A.smaps[w0 * 25 + t];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            u32 state = s_state;
+            u64 base = s_base;
+            for (int i = 0; i < n; i++) {
+                A.sentry[w0 + i] = state == STUCK ? ~0ull : (((u64)state << 56) | base);
+                if (state == STUCK) continue;
+                u32 v = m[i * 25 + state];
+                if (v == STUCK) { state = STUCK; continue; }
+                base += v >> 8;
+                state = v & 0xff;
+            }
+            s_state = state;
+            s_base = base;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(PSUPER) k_parse_records(DecArgs A) {
+    __shared__ u32 m[PSUPER * 25];
+    __shared__ u64 entry[PSUPER];
+    long long sc = blockIdx.x;
+    long long c0 = sc * PSUPER;
+    int n = (int)min((long long)PSUPER, A.nchunks - c0);
+    u64 se = A.sentry[sc];
+    if (se == ~0ull) return;
+    for (int t = threadIdx.x; t < n * 25; t += blockDim.x) m[t] = A.maps[c0 * 25 + t];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        u32 state = (u32)(se >> 56);
+        u64 base = se & ((1ull << 56) - 1);
+        for (int i = 0; i < n; i++) {
+            entry[i] = state == STUCK ? ~0ull : (((u64)state << 56) | base);
+            if (state == STUCK) continue;
+            u32 v = m[i * 25 + state];
+            if (v == STUCK) { state = STUCK; continue; }
+            base += v >> 8;
+            state = v & 0xff;
+        }
+    }
+    __syncthreads();
+    if ((int)threadIdx.x >= n) return;
+    u64 en = entry[threadIdx.x];
+    if (en == ~0ull) return;
+    long long nb = A.g.nb;
+    u64 s = 55 + (u64)(c0 + threadIdx.x) * PCHUNK, e = s + PCHUNK;
+    u64 pos = s + (en >> 56);
+    long long r = (long long)(en & ((1ull << 56) - 1));
+    while (pos < e && r < nb) {
+        if (pos + 1 > A.len) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_TRUNCATED, pos, -1, FTLZ_F_INDICATOR, 0, r); return; }
+        u8 ib = A.a[pos];
+        if (ib > 1) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_BAD_INDICATOR, pos, -1, ib, 0, r); return; }
+        u64 q = pos + 1;
+        if (ib) {
+            if (q + 16 > A.len) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_TRUNCATED, q, -1, FTLZ_F_COEFFS, 0, r); return; }
+            q += 16;
+        }
+        if (q + 8 > A.len) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_TRUNCATED, q, -1, FTLZ_F_RECORD, 0, r); return; }
+        A.ind[r] = ib;
+        A.rec_off[r] = pos;
+        A.unpc[r] = (u32)ld_le(A.a + q, 4);
+        A.bitlen[r] = (u32)ld_le(A.a + q + 4, 4);
+        if (ib == 0) A.lor_list[atomicAdd(&A.counters[DC_NLOR], 1u)] = (u32)r;
+        pos = q + 8;
+        r++;
+        if (r == nb) A.info[DI_TABLE_END] = pos;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// exclusive scans of bitlen and unpc (u64) with decoupled look-back; tile = 1024 blocks
+__global__ void __launch_bounds__(1024) k_scan2(DecArgs A) {
+    if (dev_failed(A.st)) return;
+    __shared__ u64 ws[2][32];
+    __shared__ u64 pre[2];
+    __shared__ unsigned s_tile;
+    int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(&A.counters[DC_TICKET], 1u);
+    __syncthreads();
+    unsigned tile = s_tile;
+    long long b = (long long)tile * 1024 + tid;
+    bool v = b < A.g.nb;
+    u64 x[2] = {v ? (u64)A.bitlen[b] : 0ull, v ? (u64)A.unpc[b] : 0ull};
+    u64 inc[2];
+#pragma unroll
+    for (int q = 0; q < 2; q++) {
+        inc[q] = x[q];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            u64 t = __shfl_up_sync(0xffffffffu, inc[q], o);
+            if (lane >= o) inc[q] += t;
+        }
+        if (lane == 31) ws[q][warp] = inc[q];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int q = 0; q < 2; q++) {
+            u64 y = ws[q][lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                u64 t = __shfl_up_sync(0xffffffffu, y, o);
+                if (lane >= o) y += t;
+            }
+            ws[q][lane] = y;   // inclusive over warps
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        volatile u64* va = A.lb_a; volatile u64* vb = A.lb_b; volatile u32* vf = A.lb_flag;
+        u64 p0 = 0, p1 = 0, t0 = ws[0][31], t1 = ws[1][31];
+        if (tile > 0) {
+            va[2 * tile] = t0; vb[2 * tile] = t1;
+            __threadfence();
+            vf[tile] = 1;
+            long long t = (long long)tile - 1;
+            while (t >= 0) {
+                u32 f = vf[t];
+                if (f == 0) continue;
+                __threadfence();
+                int sl = f == 2 ? 1 : 0;
+                p0 += va[2 * t + sl]; p1 += vb[2 * t + sl];
+                if (f == 2) break;
+                t--;
+            }
+        }
+        va[2 * tile + 1] = p0 + t0; vb[2 * tile + 1] = p1 + t1;
+        __threadfence();
+        vf[tile] = 2;
+        pre[0] = p0; pre[1] = p1;
+        long long ntile = (A.g.nb + 1023) / 1024;
+        if ((long long)tile == ntile - 1) {
+            A.info[DI_TOTAL_BITS] = p0 + t0;
+            A.info[DI_NUNP] = p1 + t1;
+        }
+    }
+    __syncthreads();
+    if (v) {
+        A.bofs[b] = pre[0] + (warp ? ws[0][warp - 1] : 0) + inc[0] - x[0];
+        A.uofs[b] = pre[1] + (warp ? ws[1][warp - 1] : 0) + inc[1] - x[1];
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// codebook and sections (container.py:221-271) + canonical decode tables
+#define PT_THREADS 1024
+#define DEC_TBITS 12
+
+__global__ void __launch_bounds__(PT_THREADS) k_parse_tail(DecArgs A) {
+    if (dev_failed(A.st)) return;
+    extern __shared__ __align__(16) u64 pt_dyn[];  // 8192 keys
+    __shared__ long long s_bad;
+    __shared__ u64 s_kraft;
+    __shared__ int s_maxlen;
+    __shared__ u32 s_lc[64];
+    int tid = threadIdx.x;
+    const u8* a = A.a;
+    u64 len = A.len;
+    u64 pos = A.info[DI_TABLE_END];
+    if (tid == 0) { s_bad = -1; s_kraft = 0; s_maxlen = 0; }
+    if (tid < 64) s_lc[tid] = 0;
+    __syncthreads();
+    if (pos + 4 > len) {
+        if (tid == 0) dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_TRUNCATED, pos, -1, FTLZ_F_BOOK_SIZE, 0, 0);
+        return;
+    }
+    u64 nsym = ld_le(a + pos, 4);
+    pos += 4;
+    u64 e0 = pos;
+    u64 readable = (len - pos) / 5;   // entries fully inside the data
+    u64 nchk = nsym < readable ? nsym : readable;
+    // first failing entry in order (container.py:224-233)
+    for (u64 t = tid; t < nchk; t += PT_THREADS) {
+        const u8* ent = a + e0 + 5 * t;
+        u64 sym = ld_le(ent, 4);
+        int l = ent[4];
+        bool bad = false;
+        if (t > 0 && sym <= ld_le(ent - 5, 4)) bad = true;
+        else if (sym >= (u64)A.cap) bad = true;
+        else if (l < 1 || l > 57) bad = true;
+        if (bad) atomicMin((unsigned long long*)&s_bad, (unsigned long long)t);
+        else {
+            atomicAdd(&s_lc[l], 1u);
+            atomicMax(&s_maxlen, l);
+        }
+    }
+    __syncthreads();
+    long long bad = s_bad;
+    if (bad >= 0 && (u64)bad < nchk) {
+        if (tid == 0) {
+            const u8* ent = a + e0 + 5 * (u64)bad;
+            u64 sym = ld_le(ent, 4);
+            int l = ent[4];
+            u64 p = e0 + 5 * (u64)bad;
+            if (bad > 0 && sym <= ld_le(ent - 5, 4)) dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_SYM_ORDER, p, -1, 0, 0, 0);
+            else if (sym >= (u64)A.cap) dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_SYM_RANGE, p, -1, (long long)sym, 0, 0);
+            else dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_BAD_LEN, p + 4, -1, l, 0, 0);
+        }
+        return;
+    }
+    if (nsym > readable) {
+        if (tid == 0) dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_TRUNCATED, e0 + 5 * readable, -1, FTLZ_F_BOOK_ENTRY, 0, 0);
+        return;
+    }
+    pos = e0 + 5 * nsym;
+    if (tid == 0) {
+        if (nsym == 0) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_EMPTY_BOOK, pos, -1, 0, 0, 0); return; }
+        // Kraft: sum 2^(57-l) <= 2^57 (exact with per-length counts)
+        unsigned __int128 k = 0;
+        for (int l = 1; l <= 57; l++) k += (unsigned __int128)s_lc[l] << (57 - l);
+        if (k > ((unsigned __int128)1 << 57)) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_KRAFT, pos, -1, 0, 0, 0); return; }
+        if (pos + 8 > len) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_TRUNCATED, pos, -1, FTLZ_F_PAYLOAD_LEN, 0, 0); return; }
+        u64 plen = ld_le(a + pos, 8);
+        pos += 8;
+        if (plen > len - pos) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_TRUNCATED, pos, -1, FTLZ_F_PAYLOAD, 0, 0); return; }
+        if (A.codec != 0) { dev_fail(A.st, FTLZ_ERR_UNSUPPORTED_CODEC, 0, -1, -1, A.codec, 0, 0); return; }
+        u64 pay_off = pos;
+        pos += plen;
+        u64 tb = A.info[DI_TOTAL_BITS];
+        if (tb / 8 > plen || (tb / 8 == plen && (tb & 7))) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_BITS_EXCEED, pos, -1, 0, 0, 0); return; }
+        u64 nunp = A.info[DI_NUNP];
+        if (nunp > (len - pos) / 4) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_TRUNCATED, pos, -1, FTLZ_F_UNPRED, 0, 0); return; }
+        u64 unp_off = pos;
+        pos += 4 * nunp;
+        if (pos + 16 > len) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_TRUNCATED, pos, -1, FTLZ_F_SUMDC_LENS, 0, 0); return; }
+        u64 raw = ld_le(a + pos, 8), stl = ld_le(a + pos + 8, 8);
+        pos += 16;
+        u64 nb = (u64)A.g.nb;
+        if (raw != 0 && raw != 8 * nb) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_SUMDC_LEN, pos - 16, -1, (long long)raw, 0, 0); return; }
+        u64 sdc_off = 0, has = 0;
+        if (raw) {
+            if (stl > len - pos) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_TRUNCATED, pos, -1, FTLZ_F_SUMDC, 0, 0); return; }
+            sdc_off = pos;
+            pos += stl;
+            if (stl != raw) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_SUMDC_MISMATCH, pos, -1, 0, 0, 0); return; }
+            has = 1;
+        } else if (stl) {
+            dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_ORPHAN, pos - 8, -1, 0, 0, 0);
+            return;
+        }
+        if (pos != len) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_TRAILING, pos, -1, (long long)(len - pos), 0, 0); return; }
+        A.info[DI_BOOK_OFF] = e0 - 4;
+        A.info[DI_NSYM] = nsym;
+        A.info[DI_MAXLEN] = (u64)s_maxlen;
+        A.info[DI_PAY_OFF] = pay_off;
+        A.info[DI_PAY_LEN] = plen;
+        A.info[DI_UNP_OFF] = unp_off;
+        A.info[DI_SDC_OFF] = sdc_off;
+        A.info[DI_HAS_SDC] = has;
+    }
+    __syncthreads();
+    if (dev_failed(A.st)) return;
+    // canonical order (length, symbol); symbols are strictly increasing already
+    int n = (int)nsym;
+    int np2 = 1;
+    while (np2 < n) np2 <<= 1;
+    u64* keys = np2 <= 8192 ? pt_dyn : A.sortkeys;
+    for (int i = tid; i < np2; i += PT_THREADS) {
+        if (i < n) {
+            const u8* ent = a + e0 + 5 * (u64)i;
+            keys[i] = ((u64)ent[4] << 32) | ld_le(ent, 4);
+        } else keys[i] = ~0ull;
+    }
+    __syncthreads();
+    bitonic_sort_u64(keys, np2);
+    for (int i = tid; i < n; i += PT_THREADS) A.dsym[i] = (u32)(keys[i] & 0xffffffffu);
+    if (tid == 0) {
+        u64 code = 0;
+        u32 idx = 0;
+        for (int l = 0; l < 64; l++) { A.first_code[l] = 0; A.lcount[l] = 0; A.lbase[l] = 0; }
+        for (int l = 1; l <= 57; l++) {
+            A.first_code[l] = code;
+            A.lcount[l] = s_lc[l];
+            A.lbase[l] = idx;
+            code = (code + s_lc[l]) << 1;
+            idx += s_lc[l];
+        }
+        A.info[DI_T] = (u64)min(s_maxlen, DEC_TBITS);
+    }
+    __syncthreads();
+    // decode LUT: T-bit window -> (symbol << 8 | length) for codes of length <= T
+    int T = min(s_maxlen, DEC_TBITS);
+    for (int x = tid; x < (1 << T); x += PT_THREADS) {
+        u32 ent = 0;
+        for (int l = 1; l <= T; l++) {
+            u64 code = (u64)(x >> (T - l));
+            u64 d = code - A.first_code[l];
+            if (d < (u64)A.lcount[l]) {
+                ent = (A.dsym[A.lbase[l] + d] << 8) | (u32)l;
+                break;
+            }
+        }
+        A.lut[x] = ent;
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// Huffman bit reader: MSB-first 64-bit window over big-endian 32-bit words of the archive;
+// bits at or beyond `end` read as zero (the reference pads the slice with zero bytes,
+// encode.py:214).
+struct BitReader {
+    const u8* a;
+    u64 end;
+    u64 win;
+    int have;
+    u64 nextw;
+};
+
+FTLZ_DEV u32 load_be(const u8* a, u64 wi, u64 end) {
+    u64 bit0 = wi * 32;
+    if (bit0 >= end) return 0;
+    u32 v = __byte_perm(__ldg((const u32*)a + wi), 0, 0x0123);
+    if (bit0 + 32 > end) v &= 0xffffffffu << (u32)(bit0 + 32 - end);
+    return v;
+}
+
+FTLZ_DEV void br_init(BitReader& R, const u8* a, u64 pos, u64 end) {
+    R.a = a;
+    R.end = end;
+    u64 wi = pos >> 5;
+    R.win = ((u64)load_be(a, wi, end) << 32) << (pos & 31);
+    R.have = 32 - (int)(pos & 31);
+    R.nextw = wi + 1;
+    while (R.have <= 32) {
+        R.win |= (u64)load_be(a, R.nextw, end) << (32 - R.have);
+        R.have += 32;
+        R.nextw++;
+    }
+}
+
+FTLZ_DEV void br_consume(BitReader& R, int l) {
+    R.win <<= l;
+    R.have -= l;
+    if (R.have <= 32) {
+        R.win |= (u64)load_be(R.a, R.nextw, R.end) << (32 - R.have);
+        R.have += 32;
+        R.nextw++;
+    }
+}
+
+FTLZ_DEV u64 peek64(const u8* a, u64 pos, u64 end) {
+    u64 wi = pos >> 5;
+    u64 hi = ((u64)load_be(a, wi, end) << 32) | load_be(a, wi + 1, end);
+    u32 w2 = load_be(a, wi + 2, end);
+    int sh = (int)(pos & 31);
+    return sh ? ((hi << sh) | ((u64)w2 >> (32 - sh))) : hi;
+}
+
+struct DecTables {
+    const u32* lut;
+    int T, maxlen;
+    const u64* first;
+    const u32* count;
+    const u32* base;
+    const u32* dsym;
+};
+
+// decode one symbol at absolute bit position `cur`; returns length (0 = outside code space)
+FTLZ_DEV int decode_sym(BitReader& R, const DecTables& D, u64 cur, u32* sym) {
+    u32 e = D.lut[R.win >> (64 - D.T)];
+    if (e) {
+        int l = (int)(e & 63);
+        *sym = e >> 8;
+        br_consume(R, l);
+        return l;
+    }
+    u64 bits = peek64(R.a, cur, R.end);
+    for (int l = D.T + 1; l <= D.maxlen; l++) {
+        u64 code = bits >> (64 - l);
+        u64 d = code - D.first[l];
+        if (d < (u64)D.count[l]) {
+            *sym = D.dsym[D.base[l] + d];
+            br_init(R, R.a, cur + l, R.end);
+            return l;
+        }
+    }
+    return 0;
+}
+
+FTLZ_DEV float4 load_coef(const u8* a, u64 rec) {
+    const u8* p = a + rec + 1;
+    float4 c;
+    c.x = __uint_as_float((u32)ld_le(p, 4));
+    c.y = __uint_as_float((u32)ld_le(p + 4, 4));
+    c.z = __uint_as_float((u32)ld_le(p + 8, 4));
+    c.w = __uint_as_float((u32)ld_le(p + 12, 4));
+    return c;
+}
+
+FTLZ_DEV float apply_decomp_faults(const DecArgs& A, long long b, int p, int f0, float v) {
+    for (int f = f0; f < A.n_faults && A.faults[f].block == b; f++)
+        if (A.faults[f].target == FTLZ_FAULT_DECOMP && A.faults[f].element == p)
+            v = __uint_as_float(__float_as_uint(v) ^ (1u << A.faults[f].bit));
+    return v;
+}
+
+FTLZ_DEV void fail_block(const DecArgs& A, long long b, int kind, long long x, long long y) {
+    A.dflag[b] = (u8)kind;
+    A.da[b] = x;
+    A.db[b] = y;
+    atomicMin(&A.counters[DC_MINFAIL], (u32)b);
+}
+
+// ------------------------------------------------------------------------------------------
+// K6: lane = block.  Warp = 32 consecutive blocks, decoded row by row in lockstep so that the
+// warp's rows (contiguous along z for blocks of one block-row) are written coalesced.
+#define DEC_WARPS 4
+#define MAXE 64
+
+__global__ void __launch_bounds__(DEC_WARPS * 32) k_decode(DecArgs A, const u32* list, int nlist) {
+    if (dev_failed(A.st)) return;
+    extern __shared__ __align__(16) unsigned char dsm[];
+    const Geom& g = A.g;
+    int T = (int)A.info[DI_T];
+    u32* s_lut = (u32*)dsm;
+    float* stage_all = (float*)(dsm + ((size_t)4 << DEC_TBITS));
+    __shared__ u64 s_first[64];
+    __shared__ u32 s_count[64], s_base[64];
+    int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int x = tid; x < (1 << T); x += blockDim.x) s_lut[x] = A.lut[x];
+    if (tid < 64) { s_first[tid] = A.first_code[tid]; s_count[tid] = A.lcount[tid]; s_base[tid] = A.lbase[tid]; }
+    __syncthreads();
+    DecTables D = {s_lut, T, (int)A.info[DI_MAXLEN], s_first, s_count, s_base, A.dsym};
+    float* stage = stage_all + (size_t)warp * 32 * g.e;
+    long long b;
+    bool valid;
+    bool mode_list = list != nullptr;
+    if (mode_list) {
+        // re-execution: lane over the given block list, decode only (bins to scratch)
+        long long idx = ((long long)blockIdx.x * DEC_WARPS + warp) * 32 + lane;
+        valid = idx < (long long)nlist;
+        b = valid ? (long long)list[idx] : 0;
+    } else {
+        b = ((long long)blockIdx.x * DEC_WARPS + warp) * 32 + lane;
+        valid = b < g.nb;
+    }
+    BlockInfo B = block_info(g, valid ? b : 0);
+    int kind = valid ? A.ind[b] : 0;
+    bool recon_here = valid && kind == 1 && !mode_list;
+    u64 pay_off = A.info[DI_PAY_OFF], pay_len = A.info[DI_PAY_LEN];
+    u64 bl = valid ? A.bitlen[b] : 0;
+    u64 rel = valid ? A.bofs[b] : 0;
+    int err = 0;
+    long long ea = 0, eb2 = 0;
+    u64 last_byte = (rel + bl + 7) >> 3;
+    if (valid && last_byte > pay_len) err = FTLZ_K_D_PAST_END;
+    BitReader R;
+    u64 start = pay_off * 8 + rel;
+    br_init(R, A.a, valid && !err ? start : 0, valid && !err ? (pay_off + last_byte) * 8 : 0);
+    u64 consumed = 0;
+    u32 zeros = 0;
+    u32 nunp = valid ? A.unpc[b] : 0;
+    u64 unp_base = A.info[DI_UNP_OFF] + 4 * (valid ? A.uofs[b] : 0);
+    float4 cf = recon_here ? load_coef(A.a, A.rec_off[b]) : make_float4(0, 0, 0, 0);
+    double c0 = (double)cf.x, c1 = (double)cf.y, c2 = (double)cf.z, c3 = (double)cf.w;
+    int f0 = (A.n_faults && valid) ? A.fault_first[b] : -1;
+    u64 dsum = 0;
+    // run structure (lanes of one block-row with consecutive bk are contiguous in memory)
+    bool prev_same = false;
+    {
+        long long pbi = __shfl_up_sync(0xffffffffu, B.bi, 1), pbj = __shfl_up_sync(0xffffffffu, B.bj, 1);
+        long long pbk = __shfl_up_sync(0xffffffffu, B.bk, 1);
+        bool pv = __shfl_up_sync(0xffffffffu, valid, 1);
+        prev_same = lane > 0 && pv && valid && pbi == B.bi && pbj == B.bj && pbk + 1 == B.bk && !mode_list;
+    }
+    unsigned heads = __ballot_sync(0xffffffffu, valid && !prev_same);
+    int e = g.e;
+    for (int r = 0; r < e * e; r++) {
+        int i = r / e, j = r - (r / e) * e;
+        bool act = valid && !err && i < B.bx && j < B.by;
+        if (act) {
+            double ab = 0.0;
+            if (recon_here) ab = __dadd_rn(__dadd_rn(c0, __dmul_rn(c1, int_to_f64(i))), __dmul_rn(c2, int_to_f64(j)));
+            int pbase = (i * B.by + j) * B.bz;
+            for (int k = 0; k < B.bz; k++) {
+                if (consumed > bl) { err = FTLZ_K_D_RAN_PAST; break; }
+                u32 sym;
+                int l = decode_sym(R, D, start + consumed, &sym);
+                if (l == 0) { err = FTLZ_K_D_OUTSIDE; break; }
+                consumed += (u64)l;
+                int p = pbase + k;
+                if (recon_here) {
+                    float v;
+                    if (sym) {
+                        double pred = __dadd_rn(ab, __dmul_rn(c3, int_to_f64(k)));
+                        v = __double2float_rn(__dadd_rn(pred, __dmul_rn(A.twoeb, int_to_f64((int)sym - A.center))));
+                    } else {
+                        v = zeros < nunp ? __uint_as_float((u32)ld_le(A.a + unp_base + 4ull * zeros, 4)) : 0.0f;
+                    }
+                    if (f0 >= 0) v = apply_decomp_faults(A, b, p, f0, v);
+                    dsum += __float_as_uint(v);
+                    stage[lane * e + k] = v;
+                } else {
+                    A.bins[bins_index(g, b, p)] = (u16)sym;
+                }
+                zeros += sym == 0;
+            }
+        }
+        if (!mode_list) {
+            __syncwarp();
+            // coalesced write of this row for every run of lanes
+            unsigned hm = heads;
+            while (hm) {
+                int h = __ffs(hm) - 1;
+                hm &= hm - 1;
+                int hn = hm ? __ffs(hm) - 1 : 32;   // next head (runs end at the next head)
+                long long hbi = __shfl_sync(0xffffffffu, B.bi, h), hbj = __shfl_sync(0xffffffffu, B.bj, h);
+                long long hbk = __shfl_sync(0xffffffffu, B.bk, h);
+                int hbx = __shfl_sync(0xffffffffu, B.bx, h), hby = __shfl_sync(0xffffffffu, B.by, h);
+                // run = lanes [h, last] where last = max valid lane < hn
+                unsigned vm = __ballot_sync(0xffffffffu, valid);
+                unsigned runm = vm & (hn == 32 ? ~0u : ((1u << hn) - 1u)) & ~((1u << h) - 1u);
+                int last = 31 - __clz(runm);
+                int lbz = __shfl_sync(0xffffffffu, B.bz, last);
+                if (i < hbx && j < hby) {
+                    int L = (last - h) * e + lbz;
+                    long long base = ((hbi * e + i) * g.ny + (hbj * e + j)) * g.nz + hbk * e;
+                    for (int o = lane; o < L; o += 32) A.out[base + o] = stage[h * e + o];
+                }
+            }
+            __syncwarp();
+        }
+    }
+    if (valid && !err && consumed != bl) { err = FTLZ_K_D_CONSUMED; ea = (long long)consumed; eb2 = (long long)bl; }
+    if (valid && !err && zeros != nunp) { err = FTLZ_K_D_ZEROS; ea = zeros; eb2 = nunp; }
+    if (valid && err) {
+        if (mode_list) A.mflag[b] = 3;
+        else fail_block(A, b, err, ea, eb2);
+        return;
+    }
+    if (recon_here && A.info[DI_HAS_SDC]) {
+        u64 stored = ld_le(A.a + A.info[DI_SDC_OFF] + 8ull * (u64)b, 8);
+        if (stored != dsum) {
+            A.mflag[b] = 1;
+            A.mis_list[atomicAdd(&A.counters[DC_NMIS], 1u)] = (u32)b;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------
+// K6b / K7: warp = block reconstruction from scratch bins (both predictors), verification.
+// mode 0: Lorenzo list, faults applied, mismatch -> mis_list.
+// mode 1: re-execution of mis_list (no faults); verdict in mflag (2 ok, 3 still mismatching).
+__global__ void __launch_bounds__(128) k_recon_warp(DecArgs A, int mode) {
+    if (dev_failed(A.st)) return;
+    extern __shared__ __align__(16) unsigned char rsm[];
+    const Geom& g = A.g;
+    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int nw = blockDim.x >> 5;
+    size_t slot_bytes = (((size_t)g.vmax * 8 + 15) & ~(size_t)15) + (((size_t)g.vmax * 4 + 15) & ~(size_t)15);
+    double* xd = (double*)(rsm + (size_t)warp * slot_bytes);
+    float* v32 = (float*)(xd + g.vmax);
+    u32 n = mode ? A.counters[DC_NMIS] : A.counters[DC_NLOR];
+    const u32* list = mode ? A.mis_list : A.lor_list;
+    for (long long idx = (long long)blockIdx.x * nw + warp; idx < (long long)n; idx += (long long)gridDim.x * nw) {
+        long long b = list[idx];
+        if (A.dflag[b]) continue;                       // undecodable: reported separately
+        if (mode && A.mflag[b] == 3) continue;          // re-decode failed
+        BlockInfo B = block_info(g, b);
+        int kind = A.ind[b];
+        const ExtPlan& PL = A.plans[B.xid];
+        const u32* crd = A.coords + PL.coord_off;
+        int vol = B.vol, byz = B.by * B.bz, bz = B.bz;
+        u64 unp_base = A.info[DI_UNP_OFF] + 4 * A.uofs[b];
+        // raw words of unpredictable points in row-major order
+        u32 zc = 0;
+        for (int p0 = 0; p0 < vol; p0 += 32) {
+            int p = p0 + lane;
+            u32 bin = p < vol ? A.bins[bins_index(g, b, p)] : 1u;
+            unsigned zm = __ballot_sync(0xffffffffu, bin == 0);
+            if (bin == 0) {
+                u32 r = zc + __popc(zm & ((1u << lane) - 1u));
+                v32[p] = __uint_as_float((u32)ld_le(A.a + unp_base + 4ull * r, 4));
+            }
+            zc += __popc(zm);
+        }
+        __syncwarp();
+        if (kind == 1) {
+            float4 cf = load_coef(A.a, A.rec_off[b]);
+            double c0 = (double)cf.x, c1 = (double)cf.y, c2 = (double)cf.z, c3 = (double)cf.w;
+            for (int p = lane; p < vol; p += 32) {
+                u32 bin = A.bins[bins_index(g, b, p)];
+                if (bin) {
+                    u32 c = __ldg(crd + p);
+                    int i = c & 0xff, j = (c >> 8) & 0xff, k = c >> 16;
+                    double pred = __dadd_rn(__dadd_rn(__dadd_rn(c0, __dmul_rn(c1, int_to_f64(i))), __dmul_rn(c2, int_to_f64(j))),
+                                            __dmul_rn(c3, int_to_f64(k)));
+                    v32[p] = __double2float_rn(__dadd_rn(pred, __dmul_rn(A.twoeb, int_to_f64((int)bin - A.center))));
+                }
+            }
+        } else {
+            const u32* wave = A.wave + PL.wave_off;
+            const u32* planes = A.planes + PL.plane_off;
+            for (int s = 0; s < PL.nplanes; s++) {
+                int q0 = __ldg(planes + s), q1 = __ldg(planes + s + 1);
+                for (int q = q0 + lane; q < q1; q += 32) {
+                    int p = __ldg(wave + q);
+                    u32 c = __ldg(crd + p);
+                    int i = c & 0xff, j = (c >> 8) & 0xff, k = c >> 16;
+                    u32 bin = A.bins[bins_index(g, b, p)];
+                    float v;
+                    if (bin) {
+                        double d100 = i > 0 ? xd[p - byz] : 0.0;
+                        double d010 = j > 0 ? xd[p - bz] : 0.0;
+                        double d001 = k > 0 ? xd[p - 1] : 0.0;
+                        double d110 = (i > 0 && j > 0) ? xd[p - byz - bz] : 0.0;
+                        double d101 = (i > 0 && k > 0) ? xd[p - byz - 1] : 0.0;
+                        double d011 = (j > 0 && k > 0) ? xd[p - bz - 1] : 0.0;
+                        double d111 = (i > 0 && j > 0 && k > 0) ? xd[p - byz - bz - 1] : 0.0;
+                        double pred = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(d100, d010), d001), -d110), -d101), -d011), d111);
+                        v = __double2float_rn(__dadd_rn(pred, __dmul_rn(A.twoeb, int_to_f64((int)bin - A.center))));
+                        v32[p] = v;
+                    } else {
+                        v = v32[p];
+                    }
+                    xd[p] = f32_to_f64(v);
+                }
+                __syncwarp();
+            }
+        }
+        __syncwarp();
+        int f0 = (!mode && A.n_faults) ? A.fault_first[b] : -1;
+        u64 s = 0;
+        long long base = ((B.bi * g.e) * g.ny + B.bj * g.e) * g.nz + B.bk * g.e;
+        for (int p = lane; p < vol; p += 32) {
+            float v = v32[p];
+            if (f0 >= 0) v = apply_decomp_faults(A, b, p, f0, v);
+            s += __float_as_uint(v);
+            int i = p / byz, rem = p - (p / byz) * byz;
+            int j = rem / bz, k = rem - (rem / bz) * bz;
+            A.out[base + ((long long)i * g.ny + j) * g.nz + k] = v;
+        }
+        s = warp_sum_u64(s);
+        if (lane == 0) {
+            bool has = A.info[DI_HAS_SDC] != 0;
+            u64 stored = has ? ld_le(A.a + A.info[DI_SDC_OFF] + 8ull * (u64)b, 8) : 0;
+            if (mode) A.mflag[b] = (has && stored != s) ? 3 : 2;
+            else if (has && stored != s) {
+                A.mflag[b] = 1;
+                A.mis_list[atomicAdd(&A.counters[DC_NMIS], 1u)] = (u32)b;
+            }
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace ftlz

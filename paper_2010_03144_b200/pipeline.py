@@ -1,0 +1,240 @@
+"""compress / decompress of the drop-in API (reference pipeline.py:71-142, 287-537, 645-723).
+
+Both directions run entirely on one B200 through libftlz_b200.so: Algorithm 1 (block prep,
+duplicated prediction/reconstruction, quantization, ABFT checksums, Huffman coding, archive
+assembly) and Algorithm 2 (device parse, decode, reconstruction, checksum verification,
+re-execution).  Fault injection uses per-call descriptors instead of the reference's global
+hook registry: ``faults=[(target, block, element, bit), ...]`` with the targets of
+faults.py:157-189 ("input", "bins", "decomp", "regression", "sampling").
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from ._messages import raise_for_info, sdc_detail
+from .container import CompressedStream, _sections_from_report, serialize
+from .core import DEFAULT_BLOCK_EDGE, EB_MODE_CODES, ErrorBound, Field, partition
+from .errors import InvalidInjection
+from .quantize import QuantConfig
+
+STATUS_CLEAN = "clean"
+STATUS_CORRECTED = "corrected"
+STATUS_SDC = "sdc_in_compression"
+
+CODEC_IDENTITY = 0
+
+TARGETS = {"input": 0, "input_after_checksum": 0, "bins": 1, "bin_array": 1, "decomp": 2,
+           "decompressed_buffer": 2, "regression": 3, "regression_fit": 3, "sampling": 4}
+
+
+@dataclass(frozen=True)
+class FtConfig:
+    """Protection switches + geometry (pipeline.py:71-99)."""
+
+    protect_input: bool = True
+    protect_bins: bool = True
+    duplicate_eval: bool = True
+    store_sum_dc: bool = True
+    block_edge: int = DEFAULT_BLOCK_EDGE
+    codec_id: int = CODEC_IDENTITY
+    quant: QuantConfig = field(default_factory=QuantConfig)
+
+    @classmethod
+    def protected(cls, **kw) -> "FtConfig":
+        return cls(**kw)
+
+    @classmethod
+    def unprotected(cls, **kw) -> "FtConfig":
+        return cls(protect_input=False, protect_bins=False, duplicate_eval=False,
+                   store_sum_dc=False, **kw)
+
+    def _c(self) -> _lib.Config:
+        return _lib.Config(int(self.protect_input), int(self.protect_bins),
+                           int(self.duplicate_eval), int(self.store_sum_dc),
+                           int(self.block_edge), int(self.codec_id),
+                           int(self.quant.bin_capacity), 0)
+
+
+@dataclass
+class FtReport:
+    """Per-block fault-tolerance events of one run (pipeline.py:102-142)."""
+
+    input_corrected: list = field(default_factory=list)
+    bins_corrected: list = field(default_factory=list)
+    dup_mismatch_resolved: list = field(default_factory=list)
+    decomp_block_reexecuted: list = field(default_factory=list)
+    sdc_in_compression: bool = False
+    detail: str = ""
+
+    @property
+    def status(self) -> str:
+        if self.sdc_in_compression:
+            return STATUS_SDC
+        if (self.input_corrected or self.bins_corrected or self.dup_mismatch_resolved
+                or self.decomp_block_reexecuted):
+            return STATUS_CORRECTED
+        return STATUS_CLEAN
+
+    def to_dict(self) -> dict:
+        return {
+            "status": self.status,
+            "input_corrected": list(self.input_corrected),
+            "bins_corrected": list(self.bins_corrected),
+            "dup_mismatch_resolved": list(self.dup_mismatch_resolved),
+            "decomp_block_reexecuted": list(self.decomp_block_reexecuted),
+            "detail": self.detail,
+        }
+
+
+# ------------------------------------------------------------------------------------------
+def _faults_c(faults):
+    faults = list(faults or [])
+    arr = (_lib.Fault * max(1, len(faults)))()
+    for i, f in enumerate(faults):
+        target, block, element, bit = f
+        t = TARGETS.get(target, target) if isinstance(target, str) else int(target)
+        if not isinstance(t, int):
+            raise InvalidInjection(f"unknown injection target {target!r}")
+        arr[i] = _lib.Fault(t, int(bit), int(block), int(element))
+    return arr, len(faults)
+
+
+class _ReportBuf:
+    def __init__(self, capacity: int):
+        self.bufs = [np.zeros(max(1, capacity), np.int64) for _ in range(4)]
+        self.r = _lib.Report()
+        self.r.capacity = capacity
+        P = C.POINTER(C.c_int64)
+        (self.r.input_corrected, self.r.bins_corrected, self.r.dup_mismatch,
+         self.r.reexecuted) = (b.ctypes.data_as(P) for b in self.bufs)
+
+    def lists(self):
+        r = self.r
+        ns = (r.n_input_corrected, r.n_bins_corrected, r.n_dup_mismatch, r.n_reexecuted)
+        return [b[:n].tolist() for b, n in zip(self.bufs, ns)]
+
+
+def _check_faults(faults, grid, targets):
+    for f in faults or []:
+        t = f[0]
+        if (TARGETS.get(t, t) if isinstance(t, str) else t) not in targets:
+            continue
+        b = int(f[1])
+        if not 0 <= b < grid.n_blocks:
+            raise InvalidInjection(f"block {b} out of range [0, {grid.n_blocks})")
+
+
+def compress(field: Field, eb_spec: ErrorBound, cfg: FtConfig = FtConfig(), threads: int = 1,
+             predictor_override=None, faults=None) -> tuple:
+    """Compress a field (pipeline.py:287-537) -> (CompressedStream, FtReport).
+
+    `threads` is accepted for API compatibility; the device runs all blocks at once.
+    Raises DegenerateBound / UncorrectableCorruption / InternalInvariantViolation like the
+    reference."""
+    values = field.values if isinstance(field, Field) else np.ascontiguousarray(field, np.float32)
+    grid = partition(values.shape, cfg.block_edge)
+    data, rep = _compress_array(values, eb_spec, cfg, predictor_override, faults, grid)
+    nb = grid.n_blocks
+    r = rep.r
+    stream = CompressedStream._from_archive(data, _sections_from_report(r, nb, cfg.store_sum_dc))
+    ic, bc, dm, _ = rep.lists()
+    return stream, FtReport(input_corrected=ic, bins_corrected=bc, dup_mismatch_resolved=dm)
+
+
+def _compress_array(values, eb_spec, cfg, predictor_override, faults, grid, out=None):
+    L = _lib.load()
+    ctx = _lib.context()
+    x = np.ascontiguousarray(values, dtype=np.float32)
+    nx, ny, nz = x.shape
+    nb = grid.n_blocks
+    fa, nf = _faults_c(faults)
+    ov = None
+    if predictor_override:
+        ov = np.full(nb, -1, np.int8)
+        for b, k in predictor_override.items():
+            ov[int(b)] = int(k)
+    rep = _ReportBuf(nb)
+    st = L.ftlz_ctx_compress_host(ctx, x.ctypes.data, nx, ny, nz, EB_MODE_CODES[eb_spec.mode],
+                                  float(eb_spec.value), C.byref(cfg._c()), fa, nf,
+                                  ov.ctypes.data if ov is not None else None, C.byref(rep.r))
+    if st != 0:
+        raise_for_info(st, rep.r.info, eb_request=(eb_spec.mode, eb_spec.value), resolved=rep.r.eb)
+    n = rep.r.archive_len
+    if out is not None:
+        if len(out) < n:
+            raise ValueError(f"output buffer holds {len(out)} bytes, archive needs {n}")
+        L.ftlz_ctx_copy_archive(ctx, np.frombuffer(out, np.uint8).ctypes.data, len(out))
+        return n, rep
+    ptr = C.c_void_p()
+    ln = C.c_size_t()
+    L.ftlz_ctx_archive_host(ctx, C.byref(ptr), C.byref(ln))
+    return C.string_at(ptr, ln.value), rep
+
+
+def compress_bytes(array: np.ndarray, mode: str, value: float, cfg: FtConfig = FtConfig(),
+                   out=None, faults=None):
+    """array + (mode, value) -> archive bytes (north-star form of compress+serialize).
+    With `out` (a writable buffer, e.g. pinned numpy memory) the archive is copied there and
+    its length returned."""
+    grid = partition(np.shape(array), cfg.block_edge)
+    data, _ = _compress_array(array, ErrorBound(mode, value), cfg, None, faults, grid, out=out)
+    return data
+
+
+def decompress(stream: CompressedStream, threads: int = 1, faults=None) -> tuple:
+    """Decompress (pipeline.py:645-723) -> (Field or None, FtReport).
+
+    A block whose decompressed checksum mismatches is re-executed once; a second mismatch or
+    an undecodable block withholds the output (None) and reports sdc_in_compression."""
+    data = serialize(stream)
+    out, rep = _decompress_bytes(data, faults, reuse=stream.__dict__.get("_parse_token"))
+    return (None if out is None else Field._wrap(out)), rep
+
+
+def _decompress_bytes(data: bytes, faults=None, out=None, reuse=None):
+    L = _lib.load()
+    ctx = _lib.context()
+    hdr = _lib.Header()
+    info = _lib.Info()
+    st = L.ftlz_peek_header(data, len(data), C.byref(hdr), C.byref(info))
+    if st != 0:
+        raise_for_info(st, info, data)
+    if out is None:
+        out = np.empty((hdr.nx, hdr.ny, hdr.nz), np.float32)
+    fa, nf = _faults_c(faults)
+    rb = _ReportBuf(int(hdr.block_count))
+    st = L.ftlz_ctx_decompress_host(ctx, data, len(data), out.ctypes.data, fa, nf,
+                                    1 if reuse is not None and reuse is _lib.last_parse[0] else 0,
+                                    C.byref(rb.r))
+    if st != 0:
+        raise_for_info(st, rb.r.info, data)
+    _, _, _, rx = rb.lists()
+    sdc = bool(rb.r.sdc)
+    report = FtReport(decomp_block_reexecuted=rx, sdc_in_compression=sdc,
+                      detail=sdc_detail(rb.r.info) if sdc else "")
+    return (None if sdc else out), report
+
+
+
+def decompress_bytes(data: bytes, out=None, faults=None):
+    """archive bytes -> float32 array (north-star form of parse+decompress).  Returns None
+    when the archive fails verification (the report is then available via decompress)."""
+    arr, _ = _decompress_bytes(bytes(data), faults, out=out)
+    return arr
+
+
+def cr_decrease_bound(r0: float, n_blocks: int) -> float:
+    """(r0 - 1) / (r0 + n - 1) * 100 (pipeline.py:182-189)."""
+    from .errors import InvalidArgument
+
+    if not r0 >= 1.0:
+        raise InvalidArgument(f"baseline ratio must be >= 1, got {r0}")
+    if n_blocks < 1:
+        raise InvalidArgument(f"block count must be >= 1, got {n_blocks}")
+    return (r0 - 1.0) / (r0 + n_blocks - 1.0) * 100.0

@@ -1,0 +1,166 @@
+"""Parity of the B200 path (through the C ABI) with the reference, on the GPU.
+
+Golden fixtures come from the reference package itself (tools/make_golden.py); seeded cases
+beyond them are checked against the CPU oracle (oracle/ftlz_oracle.c), which is pinned to the
+reference by tests/test_oracle_golden.py.  Everything integer/byte-valued must be bit-exact:
+archives, reconstructed float32 words, unpredictable words, FtReport lists, error texts.
+"""
+
+import dataclasses
+
+import numpy as np
+import pytest
+
+import paper_2010_03144_b200 as F
+from oracle import oracle as O
+from tests.golden_util import faults_of, load, manifest, override_of, sha
+
+pytestmark = pytest.mark.gpu
+
+M = manifest()
+
+
+def _cfg(d):
+    d = dict(d)
+    cap = d.pop("bin_capacity", None)
+    if cap is not None:
+        d["quant"] = F.QuantConfig(cap)
+    return F.FtConfig(**d)
+
+
+@pytest.mark.parametrize("name", sorted(M["cases"]))
+def test_golden_compress_decompress(name):
+    e = M["cases"][name]
+    z = load(name)
+    x = z["input"]
+    faults = faults_of(e)
+    cfg = _cfg(e["cfg"])
+    eb = F.ErrorBound(e["mode"], e["value"])
+    if "compress_error" in e:
+        with pytest.raises(F.FtlzError) as ei:
+            F.compress(F.Field.from_array(x), eb, cfg, predictor_override=override_of(e), faults=faults)
+        assert type(ei.value).__name__ == e["compress_error"]["cls"]
+        assert str(ei.value) == e["compress_error"]["msg"]
+        return
+    stream, rep = F.compress(F.Field.from_array(x), eb, cfg, predictor_override=override_of(e), faults=faults)
+    data = F.serialize(stream)
+    want = z["archive"].tobytes()
+    if data != want:
+        d = np.flatnonzero(np.frombuffer(data[: len(want)], np.uint8) != np.frombuffer(want[: len(data)], np.uint8))
+        pytest.fail(f"archive differs: len {len(data)} vs {len(want)}, first diff at {d[:5]}")
+    rd = rep.to_dict()
+    for k in ("status", "input_corrected", "bins_corrected", "dup_mismatch_resolved", "detail"):
+        assert rd[k] == e["compress_report"][k], k
+    out, drep = F.decompress(F.parse(data), faults=faults)
+    dd = drep.to_dict()
+    for k in ("status", "decomp_block_reexecuted", "detail"):
+        assert dd[k] == e["decompress_report"][k], k
+    if "output_sha256" in e:
+        assert out is not None
+        np.testing.assert_array_equal(out.values.view(np.uint32), z["output"].view(np.uint32))
+    else:
+        assert out is None
+
+
+def _corrupt_cases():
+    for src, cases in sorted(M["corrupt"].items()):
+        for name in sorted(cases):
+            yield src, name
+
+
+@pytest.mark.parametrize("src,name", list(_corrupt_cases()))
+def test_golden_parse_and_sdc(src, name):
+    e = M["corrupt"][src][name]
+    blob = load(f"corrupt_{src}")[name].tobytes()
+    if "error" in e:
+        with pytest.raises(F.FtlzError) as ei:
+            F.decompress(F.parse(blob))
+        assert type(ei.value).__name__ == e["error"]["cls"]
+        assert str(ei.value) == e["error"]["msg"]
+        return
+    out, rep = F.decompress(F.parse(blob))
+    d = rep.to_dict()
+    for k in ("status", "decomp_block_reexecuted", "detail"):
+        assert d[k] == e["decompress_report"][k], k
+    assert (None if out is None else sha(out.values)) == e["output_sha256"]
+
+
+def _seeded(kind, dims, seed):
+    rng = np.random.default_rng(seed)
+    if kind == "noise":
+        return rng.standard_normal(dims).astype(np.float32)
+    if kind == "smooth":
+        i, j, k = np.meshgrid(*[np.arange(d, dtype=np.float64) for d in dims], indexing="ij")
+        return (np.sin(0.21 * i + 0.3) * np.cos(0.17 * j) + 0.05 * k
+                + 1e-3 * rng.standard_normal(dims)).astype(np.float32)
+    if kind == "lognormal":
+        return np.exp(2.0 * rng.standard_normal(dims)).astype(np.float32)
+    raise ValueError(kind)
+
+
+ORACLE_CASES = [
+    ("smooth", (37, 41, 29), 10, "value_range_relative", 1e-3),
+    ("smooth", (64, 70, 90), 10, "value_range_relative", 1e-4),
+    ("noise", (33, 20, 51), 10, "absolute", 1e-2),
+    ("lognormal", (40, 40, 40), 10, "value_range_relative", 1e-3),
+    ("smooth", (1, 180, 360), 10, "value_range_relative", 1e-4),
+    ("smooth", (50, 50, 50), 8, "absolute", 1e-3),
+    ("noise", (17, 23, 29), 5, "absolute", 1e-5),
+    ("smooth", (30, 31, 32), 3, "value_range_relative", 1e-3),
+    ("smooth", (48, 48, 48), 16, "value_range_relative", 1e-3),
+]
+
+
+@pytest.mark.parametrize("kind,dims,edge,mode,value", ORACLE_CASES)
+def test_seeded_against_oracle(kind, dims, edge, mode, value):
+    x = _seeded(kind, dims, seed=hash((kind, dims, edge)) % 2**31)
+    cfg = {"block_edge": edge}
+    want, wrep = O.compress(x, mode, value, cfg, threads=4)
+    got = F.compress_bytes(x, mode, value, F.FtConfig(block_edge=edge))
+    assert got == want
+    out = F.decompress_bytes(got)
+    ref, _ = O.decompress(want, threads=4)
+    np.testing.assert_array_equal(out.view(np.uint32), ref.view(np.uint32))
+    # error bound holds on every point (unpredictables are stored losslessly)
+    ebv = wrep["eb"]
+    assert np.max(np.abs(out.astype(np.float64) - x.astype(np.float64))) <= ebv
+
+
+@pytest.mark.parametrize("cfg", [
+    dict(protect_input=False, protect_bins=False, duplicate_eval=False, store_sum_dc=False),
+    dict(protect_input=True, protect_bins=False, duplicate_eval=False, store_sum_dc=True),
+    dict(protect_input=False, protect_bins=True, duplicate_eval=True, store_sum_dc=False),
+])
+def test_config_flags_against_oracle(cfg):
+    x = _seeded("smooth", (40, 33, 27), seed=5)
+    want, _ = O.compress(x, "absolute", 1e-3, cfg)
+    got = F.compress_bytes(x, "absolute", 1e-3, F.FtConfig(**cfg))
+    assert got == want
+
+
+def test_payload_flip_isolation_and_sdc():
+    # a flipped payload bit is detected: SDC reported, output withheld (test_pipeline.py:289-297)
+    x = _seeded("noise", (20, 20, 20), seed=3)
+    stream, _ = F.compress(F.Field.from_array(x), F.ErrorBound.absolute(1e-3))
+    corrupted = bytearray(stream.payload)
+    corrupted[len(corrupted) // 2] ^= 0xFF
+    s2 = dataclasses.replace(stream, payload=bytes(corrupted))
+    out, rep = F.decompress(s2)
+    want, wrep = O.decompress(F.serialize(s2))
+    assert out is None and rep.status == "sdc_in_compression"
+    assert rep.detail == wrep["detail"]
+
+
+def test_replace_roundtrip_equals_original():
+    x = _seeded("smooth", (21, 22, 23), seed=8)
+    stream, _ = F.compress(F.Field.from_array(x), F.ErrorBound.absolute(1e-3), F.FtConfig(block_edge=4))
+    s2 = dataclasses.replace(stream)
+    assert F.serialize(s2) == F.serialize(stream)
+    assert F.parse(F.serialize(stream)) == stream
+
+
+def test_thread_argument_is_deterministic():
+    x = _seeded("smooth", (22, 18, 14), seed=18)
+    a, _ = F.compress(F.Field.from_array(x), F.ErrorBound.absolute(1e-3), threads=1)
+    b, _ = F.compress(F.Field.from_array(x), F.ErrorBound.absolute(1e-3), threads=8)
+    assert F.serialize(a) == F.serialize(b)
