@@ -242,6 +242,12 @@ int ftlz_ctx_decompress_device(ftlz_ctx* ctx, const uint8_t* d_archive, size_t l
                                const ftlz_header* hdr, float* d_out,
                                const ftlz_fault* faults, int64_t n_faults, ftlz_report* report);
 
+/* ---- instrumentation (bench.py): per-kernel CUDA-event timing on the context stream ------- */
+int ftlz_ctx_profile(ftlz_ctx* ctx, int32_t enable);   /* enable/disable and reset totals */
+/* up to max_n kernels: '\n'-separated names, accumulated ms and launch counts; returns count */
+int ftlz_ctx_profile_read(ftlz_ctx* ctx, char* names, size_t names_cap, double* ms, int64_t* counts,
+                          int32_t max_n);
+
 #ifdef __cplusplus
 }
 #endif

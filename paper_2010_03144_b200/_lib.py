@@ -76,6 +76,7 @@ EXPORTS = [
     "ftlz_ctx_destroy", "ftlz_ctx_stream", "ftlz_ctx_compress_device", "ftlz_ctx_compress_host",
     "ftlz_ctx_archive_device", "ftlz_ctx_archive_host", "ftlz_ctx_copy_archive",
     "ftlz_ctx_parse_host", "ftlz_ctx_decompress_host", "ftlz_ctx_decompress_device",
+    "ftlz_ctx_profile", "ftlz_ctx_profile_read",
 ]
 
 _lib = None
@@ -128,6 +129,8 @@ def load():
         L.ftlz_ctx_parse_host.argtypes = [vp, vp, sz, C.POINTER(StreamInfo), PR]
         L.ftlz_ctx_decompress_host.argtypes = [vp, vp, sz, vp, PF, i64, i32, PR]
         L.ftlz_ctx_decompress_device.argtypes = [vp, vp, sz, PH, vp, PF, i64, PR]
+        L.ftlz_ctx_profile.argtypes = [vp, i32]
+        L.ftlz_ctx_profile_read.argtypes = [vp, C.c_char_p, sz, C.POINTER(dbl), C.POINTER(i64), i32]
         _lib = L
         return L
 
@@ -155,3 +158,19 @@ def context(device: int = 0):
 
 def last_error() -> str:
     return load().ftlz_last_error().decode(errors="replace")
+
+
+def profile(enable: bool, device: int = 0) -> None:
+    """Enable per-kernel CUDA-event timing in the library context (resets totals)."""
+    load().ftlz_ctx_profile(context(device), 1 if enable else 0)
+
+
+def profile_read(device: int = 0) -> dict:
+    """{kernel: (total_ms, launches)} accumulated since profile(True)."""
+    L = load()
+    names = C.create_string_buffer(8192)
+    ms = (C.c_double * 64)()
+    cnt = (C.c_int64 * 64)()
+    n = L.ftlz_ctx_profile_read(context(device), names, 8192, ms, cnt, 64)
+    keys = names.value.decode().split("\n")[:max(n, 0)]
+    return {k: (ms[i], int(cnt[i])) for i, k in enumerate(keys)}

@@ -26,6 +26,39 @@ static int set_err(int code, const std::string& msg) {
     return code;
 }
 
+// optional per-kernel CUDA-event timing (bench.py); events are recorded on the launch stream
+struct Profiler {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    std::vector<std::pair<std::string, cudaEvent_t>> marks;
+    std::map<std::string, std::pair<double, long long>> totals;
+    void mark(const char* name, cudaStream_t s) {
+        if (!on) return;
+        if (used == pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            pool.push_back(e);
+        }
+        cudaEvent_t e = pool[used++];
+        cudaEventRecord(e, s);
+        marks.push_back({name, e});
+    }
+    void collect() {  // after a stream sync
+        if (!on) return;
+        for (size_t i = 0; i + 1 < marks.size(); i++) {
+            if (marks[i].first.empty()) continue;
+            float ms = 0;
+            cudaEventElapsedTime(&ms, marks[i].second, marks[i + 1].second);
+            auto& t = totals[marks[i].first];
+            t.first += ms;
+            t.second += 1;
+        }
+        marks.clear();
+        used = 0;
+    }
+};
+
 #define LCHK(name)                                                                               \
     do {                                                                                         \
         cudaError_t e_ = cudaGetLastError();                                                     \
@@ -403,7 +436,9 @@ static void report_reset(ftlz_report* r) {
 static int compress_core(const HostPlan& P, const DevPlan* cached, const float* d_in, int32_t eb_mode,
                          double eb_value, const ftlz_config* cfg, const ftlz_fault* faults, int64_t nf,
                          const int8_t* ovr, unsigned char* ws, size_t ws_size, uint8_t* d_out, size_t out_cap,
-                         ftlz_report* rep, cudaStream_t s, unsigned char* h_result) {
+                         ftlz_report* rep, cudaStream_t s, unsigned char* h_result, Profiler* prof = nullptr) {
+    Profiler noprof;
+    Profiler& PF = prof ? *prof : noprof;
     report_reset(rep);
     const Geom& g = P.g;
     int cap = (int)cfg->bin_capacity;
@@ -468,32 +503,42 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     S.parent = (u32*)(ws + L.cb_parent); S.lens = ws + L.cb_lens;
 
     long long nctas = (g.nb + K.P - 1) / K.P;
+    PF.mark("k_prep", s);
     k_prep<<<(unsigned)nctas, 32 * K.P, K.smem, s>>>(A);
     LCHK("k_prep");
+    PF.mark("k_resolve", s);
     k_resolve<<<1, 1, 0, s>>>(A);
     LCHK("k_resolve");
+    PF.mark("k_quant", s);
     k_quant<<<(unsigned)nctas, 32 * K.P, K.smem, s>>>(A);
     LCHK("k_quant");
+    if (nf) PF.mark("k_fault_bins", s);
     if (nf) k_fault_bins<<<num_sms(), 256, 0, s>>>(A, (u32*)(ws + L.fix), (u8*)(ws + L.fixed));
     LCHK("k_fault_bins");
+    PF.mark("k_codebook", s);
     k_codebook<<<1, CB_THREADS, (CB_SMEM_KEYS * 3) * 8, s>>>(A, S);
     LCHK("k_codebook");
+    PF.mark("k_zero", s);
     k_zero<<<num_sms() * 4, 256, 0, s>>>(A);
     LCHK("k_zero");
     unsigned ntiles = (unsigned)((g.nb + ENC_BLOCKS - 1) / ENC_BLOCKS);
+    PF.mark("k_encode", s);
     k_encode<<<ntiles, ENC_BLOCKS, 0, s>>>(A, (u32*)(ws + L.fix), (const u8*)(ws + L.fixed), (u32*)(ws + L.lbflag), (u64*)(ws + L.lbbits),
                                            (u64*)(ws + L.lbreg), (u64*)(ws + L.lbunp));
     LCHK("k_encode");
     ftlz_header H;
     memset(&H, 0, sizeof H);
     H.nx = g.nx; H.ny = g.ny; H.nz = g.nz; H.block_edge = g.e; H.eb_mode = eb_mode ? 1 : 0;
+    PF.mark("k_assemble", s);
     k_assemble<<<num_sms() * 2, 256, 0, s>>>(A, H);
     LCHK("k_assemble");
     CK(cudaGetLastError());
+    PF.mark("", s);
     unsigned char hres_local[RESULT_BYTES];
     unsigned char* hres = h_result ? h_result : hres_local;
     CK(cudaMemcpyAsync(hres, ws + L.result, RESULT_BYTES, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    PF.collect();
     DevStatus st;
     memcpy(&st, hres, sizeof st);
     u32 counters[16];
@@ -662,7 +707,9 @@ static void stream_info_fill(const ftlz_header* h, const u64* info, ftlz_stream_
 static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8_t* d_a, size_t len,
                            const ftlz_header* h, float* d_out, const ftlz_fault* faults, int64_t nf,
                            unsigned char* ws, size_t ws_size, ftlz_report* rep, ftlz_stream_info* si_out,
-                           bool decode, cudaStream_t s, unsigned char* h_result) {
+                           bool decode, cudaStream_t s, unsigned char* h_result, Profiler* prof = nullptr) {
+    Profiler noprof;
+    Profiler& PF = prof ? *prof : noprof;
     report_reset(rep);
     const Geom& g = P.g;
     int cap = (int)h->bin_capacity;
@@ -713,32 +760,42 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     A.lb_flag = (u32*)(ws + L.lbflag); A.lb_a = (u64*)(ws + L.lba); A.lb_b = (u64*)(ws + L.lbb);
 
     int sms = num_sms();
+    PF.mark("k_parse_maps", s);
     k_parse_maps<<<sms * 8, 256, 0, s>>>(A);
     LCHK("k_parse_maps");
+    PF.mark("k_parse_compose", s);
     k_parse_compose<<<(unsigned)L.nsuper, PSUPER, 0, s>>>(A);
     LCHK("k_parse_compose");
+    PF.mark("k_parse_top", s);
     k_parse_top<<<1, 256, 0, s>>>(A);
     LCHK("k_parse_top");
+    PF.mark("k_parse_records", s);
     k_parse_records<<<(unsigned)L.nsuper, PSUPER, 0, s>>>(A);
     LCHK("k_parse_records");
+    PF.mark("k_scan2", s);
     k_scan2<<<(unsigned)((g.nb + 1023) / 1024), 1024, 0, s>>>(A);
     LCHK("k_scan2");
+    PF.mark("k_parse_tail", s);
     k_parse_tail<<<1, PT_THREADS, 8192 * 8, s>>>(A);
     LCHK("k_parse_tail");
     size_t dec_smem = ((size_t)4 << DEC_TBITS) + (size_t)DEC_WARPS * 32 * g.e * 4;
     size_t rslot = al16((size_t)g.vmax * 8) + al16((size_t)g.vmax * 4);
     int rw = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / rslot));
     if (decode) {
+        PF.mark("k_decode", s);
         k_decode<<<(unsigned)((g.nb + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32)), DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
         LCHK("k_decode");
+        PF.mark("k_recon_warp", s);
         k_recon_warp<<<sms * 4, rw * 32, rslot * rw, s>>>(A, 0);
         LCHK("k_recon_warp");
     }
     CK(cudaGetLastError());
+    PF.mark("", s);
     unsigned char hres_local[RESULT_BYTES];
     unsigned char* hres = h_result ? h_result : hres_local;
     CK(cudaMemcpyAsync(hres, ws + L.result, RESULT_BYTES, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    PF.collect();
     DecResult R;
     memcpy(&R.st, hres, sizeof R.st);
     memcpy(R.counters, hres + 64, sizeof R.counters);
@@ -882,6 +939,7 @@ struct ftlz_ctx {
     const uint8_t* parsed_src = nullptr;
     size_t parsed_len = 0;
     ftlz_header parsed_hdr;
+    Profiler prof;
     std::mutex mu;
 };
 
@@ -943,7 +1001,7 @@ static int ctx_compress(ftlz_ctx* c, const float* d_in, int64_t nx, int64_t ny, 
     size_t bound = ftlz_compress_bound(nx, ny, nz, cfg);
     if ((rc = c->out.ensure(bound))) return rc;
     rc = compress_core(c->hp, &c->dp, d_in, eb_mode, eb_value, cfg, faults, nf, ovr, (unsigned char*)c->ws.p,
-                       c->ws.n, (uint8_t*)c->out.p, c->out.n, rep, c->stream, (unsigned char*)c->h_res.p);
+                       c->ws.n, (uint8_t*)c->out.p, c->out.n, rep, c->stream, (unsigned char*)c->h_res.p, &c->prof);
     c->arch_len = rc == FTLZ_OK ? (size_t)rep->archive_len : 0;
     c->arch_on_host = false;
     return rc;
@@ -1029,7 +1087,7 @@ static int ctx_decompress(ftlz_ctx* c, const uint8_t* d_a, size_t len, const ftl
     DecLayout L = dec_layout(c->hp, len, (int)std::min<uint32_t>(hdr->bin_capacity, 65536u), nf);
     if ((rc = c->dws.ensure(L.total))) return rc;
     return decompress_core(c->hp, &c->dp, d_a, len, hdr, d_out, faults, nf, (unsigned char*)c->dws.p, c->dws.n,
-                           rep, si, decode, c->stream, (unsigned char*)c->h_res.p);
+                           rep, si, decode, c->stream, (unsigned char*)c->h_res.p, &c->prof);
 }
 
 extern "C" int ftlz_ctx_parse_host(ftlz_ctx* c, const uint8_t* h, size_t len, ftlz_stream_info* si, ftlz_report* rep) {
@@ -1073,4 +1131,31 @@ extern "C" int ftlz_ctx_decompress_device(ftlz_ctx* c, const uint8_t* d_archive,
     std::lock_guard<std::mutex> g(c->mu);
     cudaSetDevice(c->device);
     return ctx_decompress(c, d_archive, len, hdr, d_out, faults, nf, rep, nullptr, true);
+}
+
+// ------------------------------------------------------------------------------------------
+// profiling (bench.py): per-kernel event timing accumulated across calls
+extern "C" int ftlz_ctx_profile(ftlz_ctx* c, int32_t enable) {
+    std::lock_guard<std::mutex> g(c->mu);
+    c->prof.on = enable != 0;
+    c->prof.totals.clear();
+    return FTLZ_OK;
+}
+
+// writes up to max_n entries: names as '\n'-separated text, total ms and launch counts
+extern "C" int ftlz_ctx_profile_read(ftlz_ctx* c, char* names, size_t names_cap, double* ms, int64_t* counts,
+                                     int32_t max_n) {
+    std::lock_guard<std::mutex> g(c->mu);
+    std::string all;
+    int n = 0;
+    for (auto& kv : c->prof.totals) {
+        if (n >= max_n) break;
+        all += kv.first + "\n";
+        ms[n] = kv.second.first;
+        counts[n] = kv.second.second;
+        n++;
+    }
+    if (all.size() + 1 > names_cap) return -1;
+    memcpy(names, all.c_str(), all.size() + 1);
+    return n;
 }

@@ -197,19 +197,24 @@ def decompress(stream: CompressedStream, threads: int = 1, faults=None) -> tuple
     return (None if out is None else Field._wrap(out)), rep
 
 
-def _decompress_bytes(data: bytes, faults=None, out=None, reuse=None):
+def _decompress_bytes(data, faults=None, out=None, reuse=None):
     L = _lib.load()
     ctx = _lib.context()
     hdr = _lib.Header()
     info = _lib.Info()
-    st = L.ftlz_peek_header(data, len(data), C.byref(hdr), C.byref(info))
+    if not isinstance(data, bytes):
+        # any contiguous byte buffer (e.g. pinned numpy memory) is read in place
+        data = np.frombuffer(data, np.uint8)
+    buf = data if isinstance(data, bytes) else data.ctypes.data
+    head = bytes(data[:64])
+    st = L.ftlz_peek_header(head, len(data), C.byref(hdr), C.byref(info))
     if st != 0:
         raise_for_info(st, info, data)
     if out is None:
         out = np.empty((hdr.nx, hdr.ny, hdr.nz), np.float32)
     fa, nf = _faults_c(faults)
     rb = _ReportBuf(int(hdr.block_count))
-    st = L.ftlz_ctx_decompress_host(ctx, data, len(data), out.ctypes.data, fa, nf,
+    st = L.ftlz_ctx_decompress_host(ctx, buf, len(data), out.ctypes.data, fa, nf,
                                     1 if reuse is not None and reuse is _lib.last_parse[0] else 0,
                                     C.byref(rb.r))
     if st != 0:
@@ -225,7 +230,7 @@ def _decompress_bytes(data: bytes, faults=None, out=None, reuse=None):
 def decompress_bytes(data: bytes, out=None, faults=None):
     """archive bytes -> float32 array (north-star form of parse+decompress).  Returns None
     when the archive fails verification (the report is then available via decompress)."""
-    arr, _ = _decompress_bytes(bytes(data), faults, out=out)
+    arr, _ = _decompress_bytes(data, faults, out=out)
     return arr
 
 
