@@ -322,12 +322,13 @@ def run_ours(args, world, rank, local):
     kern = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
             for k, v in prof.items()}
     launches = int(round(sum(v[1] for v in prof.values()) / max(1, args.steps)))
-    comp_k = {k: v for k, v in kern.items() if k in ("k_prep", "k_resolve", "k_quant", "k_fault_bins", "k_codebook",
-                                                        "k_zero", "k_encode", "k_assemble")}
+    dec_names = ("k_parse_maps", "k_parse_compose", "k_parse_top", "k_parse_records", "k_scan2", "k_parse_tail",
+                 "k_decode", "k_recon_warp")
+    comp_k = {k: v for k, v in kern.items() if k not in dec_names}
     dec_k = {k: v for k, v in kern.items() if k not in comp_k}
     dom = max(kern.items(), key=lambda kv: kv[1]["ms_per_step"])[0] if kern else None
     # algorithmic bytes per launch of each kernel: input/archive reads + output writes
-    alg = {"k_prep": 4.0 * N, "k_quant": 4.0 * N, "k_encode": float(S), "k_decode": float(S) + 4.0 * N,
+    alg = {"k_prep": 4.0 * N, "k_quant_reg": 4.0 * N, "k_encode": float(S), "k_decode": float(S) + 4.0 * N,
            "k_recon_warp": 0.0}
     roof = None
     if dom:

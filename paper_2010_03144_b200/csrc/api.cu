@@ -14,6 +14,8 @@
 #include <vector>
 
 #include "compress.cu"
+#include "blocks.cu"
+#include "quant_reg.cu"
 #include "decompress.cu"
 
 using namespace ftlz;
@@ -249,19 +251,38 @@ static int upload_plan(const HostPlan& P, unsigned char* dst, DevPlan& D, cudaSt
 static size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 struct KCfg {
-    int P;
-    size_t slot;
-    size_t smem;
+    int P;               // blocks per pencil
+    long long npz;       // pencils per block row
+    long long npencils;
+    int stride;          // padded floats per staged row
+    size_t tile_bytes;
+    size_t prep_smem, reg_smem, lor_smem, lor_slot;
+    int reg_threads, lor_warps;
 };
 
 static KCfg kcfg_comp(const Geom& g) {
-    size_t v = (size_t)g.vmax;
-    size_t prep = al16(4 * v) + 8 * v + 8 * 4 * (v / 64 + 8) + 8 * 2 * (v / 8 + 8);
-    size_t quant = al16(4 * v) + 8 * v + 2 * v + 16 + 3 * 64 * 8;
     KCfg k;
-    k.slot = al16(std::max(prep, quant));
-    k.P = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / k.slot));
-    k.smem = k.slot * k.P;
+    int rows = (int)std::min<int64_t>(g.e, g.nx) * (int)std::min<int64_t>(g.e, g.ny);
+    int P = std::max(1, std::min(12, 400 / std::max(rows, 1)));   // k_quant_reg: a warp per block in setup
+    if (P > 1 && ((P * g.e) & 3)) P &= ~1;                 // keep pencil rows 16-byte multiples
+    P = std::max(1, (int)std::min<int64_t>(P, g.cz));
+    k.P = P;
+    k.npz = (g.cz + P - 1) / P;
+    k.npencils = g.cx * g.cy * k.npz;
+    int L = (int)std::min<int64_t>((int64_t)P * g.e, g.nz);   // longest pencil row
+    int st = (L + 3) & ~3;
+    if ((st & 7) == 0) st += 4;                            // stride/4 odd: conflict-free 16B phases
+    k.stride = st;
+    k.tile_bytes = al16((size_t)rows * st * 4);
+    size_t v = (size_t)g.vmax;
+    size_t per_warp = (4 * (v / 64 + 8) + 2 * (v / 8 + 8) + 3 * 64) * 8;
+    k.prep_smem = k.tile_bytes + per_warp * P;
+    k.reg_smem = 2 * k.tile_bytes + al16(2 * (size_t)g.nvmax8 * P) + 64 * 8 * (size_t)P + 4 * HWIN +
+                 sizeof(RowAcc) * (size_t)rows * P;
+    k.reg_threads = std::min(416, std::max((rows * P + 31) & ~31, 32 * P));   // __launch_bounds__(416, 2)
+    k.lor_slot = al16(4 * v) + 8 * v + al16(2 * v);
+    k.lor_warps = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / k.lor_slot));
+    k.lor_smem = k.lor_slot * k.lor_warps + 4 * HWIN;
     return k;
 }
 
@@ -281,7 +302,8 @@ static int kernel_attrs_once() {
                 rc = FTLZ_ERR_CUDA;
         };
         setmax((const void*)k_prep);
-        setmax((const void*)k_quant);
+        setmax((const void*)k_quant_reg);
+        setmax((const void*)k_quant_lor);
         setmax((const void*)k_codebook);
         setmax((const void*)k_parse_tail);
         setmax((const void*)k_decode);
@@ -311,7 +333,7 @@ struct CompLayout {
     size_t coef, insum, inisum, ind, unpc, bsum, bisum, dcs, bitlen, regpre, unppre;
     size_t enc, qp, lbbits, lbreg, lbunp;
     size_t cb_keys, cb_syms, cb_w, cb_parent, cb_lens;
-    size_t bins, unp, fix, faults, ffirst, ovr, plan;
+    size_t bins, unp, fix, faults, ffirst, ovr, plan, lor;
     size_t total;
 };
 
@@ -358,6 +380,7 @@ static CompLayout comp_layout(const HostPlan& P, int cap, int64_t n_faults) {
     L.faults = take(sizeof(ftlz_fault) * (size_t)std::max<int64_t>(1, n_faults));
     L.ffirst = take(n_faults ? 4 * nb : 0);
     L.ovr = take(nb);
+    L.lor = take(4 * nb);
     L.plan = take(P.bytes());
     L.total = o;
     return L;
@@ -453,7 +476,8 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     CompLayout L = comp_layout(P, cap, nf);
     if (ws_size < L.total) return set_err(FTLZ_ERR_CAPACITY, "workspace too small");
     KCfg K = kcfg_comp(g);
-    if (K.smem > 227 * 1024) return set_err(FTLZ_ERR_INVALID_ARGUMENT, "block too large for shared memory (block_edge^3 * 15 B > 227 KB)");
+    if (std::max(K.prep_smem, std::max(K.reg_smem, K.lor_smem)) > 227 * 1024 || K.reg_threads > 1024)
+        return set_err(FTLZ_ERR_INVALID_ARGUMENT, "block too large for the shared-memory path (block_edge <= 24)");
     if ((rc = kernel_attrs_once())) return set_err(rc, "cudaFuncSetAttribute failed");
     DevPlan D;
     std::vector<unsigned char> staging;
@@ -477,7 +501,19 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     A.dup_eval = cfg->duplicate_eval; A.store_sum_dc = cfg->store_sum_dc;
     A.eb_mode = eb_mode; A.eb_value = eb_value;
     A.cap = cap; A.center = cap / 2;
-    A.P = K.P; A.nwarp_smem = (int)K.slot;
+    A.P = K.P; A.npz = K.npz; A.npencils = K.npencils;
+    A.fd_npz = make_fastdiv((u32)K.npz); A.fd_cy = make_fastdiv((u32)g.cy);
+    A.fd_e = make_fastdiv((u32)g.e); A.fd_ry = make_fastdiv((u32)g.ry); A.tile_stride = K.stride; A.tile_bytes = (int)K.tile_bytes;
+    {
+        int vec = (g.nz % 4 == 0) && ((g.e * K.P) % 4 == 0) && (((uintptr_t)d_in & 15) == 0);
+        auto per = [&](int L) { return vec ? L / 4 + L % 4 : L; };
+        int nlast = (int)(g.cz - (int64_t)(K.npz - 1) * K.P);
+        A.pio.vec = vec;
+        A.pio.per_full = make_fastdiv((u32)per(K.P * g.e));
+        A.pio.per_last = make_fastdiv((u32)per((nlast - 1) * g.e + g.rz));
+    }
+    A.lor_slot = (int)K.lor_slot;
+    A.lor_list = (u32*)(ws + L.lor);
     A.n_faults = (int)nf;
     A.faults = (const ftlz_fault*)(ws + L.faults);
     A.fault_first = (const int*)(ws + L.ffirst);
@@ -502,16 +538,26 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     S.keys = (u64*)(ws + L.cb_keys); S.syms = (u32*)(ws + L.cb_syms); S.w = (u64*)(ws + L.cb_w);
     S.parent = (u32*)(ws + L.cb_parent); S.lens = ws + L.cb_lens;
 
-    long long nctas = (g.nb + K.P - 1) / K.P;
     PF.mark("k_prep", s);
-    k_prep<<<(unsigned)nctas, 32 * K.P, K.smem, s>>>(A);
+    k_prep<<<(unsigned)K.npencils, 32 * K.P, K.prep_smem, s>>>(A);
     LCHK("k_prep");
     PF.mark("k_resolve", s);
     k_resolve<<<1, 1, 0, s>>>(A);
     LCHK("k_resolve");
-    PF.mark("k_quant", s);
-    k_quant<<<(unsigned)nctas, 32 * K.P, K.smem, s>>>(A);
-    LCHK("k_quant");
+    PF.mark("k_quant_reg", s);
+    {
+        static int occ_reg = 0;
+        if (!occ_reg) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_reg, k_quant_reg, K.reg_threads, K.reg_smem);
+            if (occ_reg < 1) occ_reg = 1;
+        }
+        long long grid = std::min<long long>(K.npencils, (long long)num_sms() * occ_reg);
+        k_quant_reg<<<(unsigned)grid, K.reg_threads, K.reg_smem, s>>>(A);
+    }
+    LCHK("k_quant_reg");
+    PF.mark("k_quant_lor", s);
+    k_quant_lor<<<num_sms() * 4, 32 * K.lor_warps, K.lor_smem, s>>>(A);
+    LCHK("k_quant_lor");
     if (nf) PF.mark("k_fault_bins", s);
     if (nf) k_fault_bins<<<num_sms(), 256, 0, s>>>(A, (u32*)(ws + L.fix), (u8*)(ws + L.fixed));
     LCHK("k_fault_bins");

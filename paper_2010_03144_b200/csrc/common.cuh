@@ -78,6 +78,37 @@ FTLZ_DEV double int_to_f64(int n) {
 
 FTLZ_DEV u64 dbits(double d) { return (u64)__double_as_longlong(d); }
 
+// exact u32 division by a launch-constant divisor: q = hi64(n * ceil(2^64 / d)), which is
+// floor(n / d) for every n, d < 2^32 (error < n / 2^64 < 1/d); d == 1 is passed through.
+struct FastDiv {
+    u64 m;
+    u32 d;
+    u32 pad;
+};
+FTLZ_DEV u32 fdiv(u32 n, const FastDiv& f) { return f.d == 1u ? n : (u32)__umul64hi((u64)n, f.m); }
+struct PencilIO {
+    FastDiv per_full, per_last;   // cp.async items per row for full / last pencils of a block row
+    int vec;                      // 16-byte chunks (rows 16-byte aligned)
+    int pad;
+};
+static inline FastDiv make_fastdiv(u32 d) {
+    FastDiv f;
+    f.d = d;
+    f.m = d <= 1u ? 0ull : (~0ull / d) + 1ull;
+    f.pad = 0;
+    return f;
+}
+
+// ordered-int encoding of float32 for atomic min/max (NaN handled separately)
+FTLZ_DEV u32 f2ord(float f) {
+    u32 u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+FTLZ_DEV float ord2f(u32 o) {
+    u32 u = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+    return __uint_as_float(u);
+}
+
 // ------------------------------------------------------------------------------------------
 // quantizer (pipeline.py:271-279 == quantize.py:37-52), exact.
 //   h = |diff| / (2 eb); small = h <= 2*cap; q = floor(fl((small ? h : 0) + 0.5)); sign;
@@ -93,6 +124,7 @@ struct QuantParams {
     int cap, center;
     int exact_div;
     int pad;
+    double twoeb_dup;       // second copy of 2*eb: the duplicated evaluation loads its own operand
 };
 
 // floor(t) for t in [0, 2^31): integer extraction from the bit pattern
@@ -262,6 +294,25 @@ FTLZ_DEV void bitonic_sort_u64(u64* keys, int n_pow2) {
             }
             __syncthreads();
         }
+    }
+}
+
+
+// ------------------------------------------------------------------------------------------
+#define HWIN 4096   // shared-memory histogram window around the quantizer center
+
+// histogram increment: shared window (flushed once per CTA) or global for outliers
+FTLZ_DEV void hist_add(u32* hwin, u32* ghist, int wlo, int bin, u32 cnt) {
+    unsigned o = (unsigned)(bin - wlo);
+    if (o < HWIN) atomicAdd(&hwin[o], cnt);
+    else atomicAdd(&ghist[bin], cnt);
+}
+
+FTLZ_DEV void hist_flush(u32* hwin, u32* ghist, int wlo, int cap) {
+    for (int t = threadIdx.x; t < HWIN; t += blockDim.x) {
+        u32 v = hwin[t];
+        int s = wlo + t;
+        if (v && s >= 0 && s < cap) atomicAdd(&ghist[s], v);
     }
 }
 

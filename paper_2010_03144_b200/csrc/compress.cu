@@ -2,10 +2,10 @@
 // (container.py:109-147) for B200 (sm_100a).
 //
 // Kernel sequence (one stream, no host sync until the report read-back):
-//   k_prep      stage (a)+(b): value range, input checksums, regression fit with numpy's
+//   k_prep      (blocks.cu) stage (a)+(b): value range, input checksums, regression fit with numpy's
 //               pairwise float64 summation order, sampled predictor selection   (K0+K1)
 //   k_resolve   resolved error bound (core.py:182-193) + quantizer constants
-//   k_quant     stage (c): verify input, predict (duplicated), quantize, reconstruct
+//   k_quant_*   (blocks.cu) stage (c): verify input, predict (duplicated), quantize, reconstruct
 //               (duplicated), double-check, bins/unpredictables/checksums/sum_dc/histogram (K2)
 //   k_fault_bins  bins-stage faults: verify/correct (protect_bins) and histogram fix-up
 //   k_codebook  canonical Huffman codebook from the global histogram (K3), archive layout
@@ -27,8 +27,15 @@ struct CompArgs {
     int eb_mode;
     double eb_value;
     int cap, center;
-    int P;                    // blocks per CTA in k_prep / k_quant
-    int nwarp_smem;           // smem bytes per block
+    int P;                    // blocks per pencil (CTA) in k_prep / k_quant_reg
+    long long npz;            // pencils per block row
+    long long npencils;
+    FastDiv fd_npz, fd_cy, fd_e, fd_ry;   // launch-constant divisors (pencil / row decomposition)
+    PencilIO pio;
+    int tile_stride;          // floats per staged row (padded)
+    int tile_bytes;           // bytes of the staged pencil tile
+    int lor_slot;             // smem bytes per warp in k_quant_lor
+    u32* lor_list;            // Lorenzo blocks (appended by k_prep)
     int n_faults;
     const ftlz_fault* faults;    // device copy
     const int* fault_first;      // nb: first fault index of this block or -1 (faults sorted by block)
@@ -54,7 +61,7 @@ struct CompArgs {
     // globals
     DevStatus* st;
     u32* minmax;         // [0] ordered max, [1] ordered min, [2] nan flag
-    u32* counters;       // [0] n_reg, [1] dup group flags, [2] encode ticket, [3] n_unpred (low), ...
+    u32* counters;       // [0] n_reg, [1] dup group flags, [2] encode ticket, [3] events, [4] n_lor
     QuantParams* qp;
     u32* hist;           // cap entries
     u64* enc;            // cap entries: code << 6 | len (0 = absent)
@@ -72,91 +79,6 @@ enum {
     LAYOUT_PAY_BYTES, LAYOUT_UNP_OFF, LAYOUT_NUNP, LAYOUT_SDC_OFF, LAYOUT_TOTAL, LAYOUT_TOTAL_BITS,
     LAYOUT_MAXLEN, LAYOUT_NREG, LAYOUT_EB_BITS, LAYOUT_COUNT
 };
-
-// ordered-int encoding of floats for atomic min/max
-FTLZ_DEV u32 f2ord(float f) {
-    u32 u = __float_as_uint(f);
-    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
-FTLZ_DEV float ord2f(u32 o) {
-    u32 u = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
-    return __uint_as_float(u);
-}
-
-// ------------------------------------------------------------------------------------------
-// block staging: the CTA's P consecutive blocks, grouped into runs of equal (bi, bj) whose
-// rows are contiguous in memory; each warp loads whole rows with coalesced accesses.
-// load the rows of block B into f32 smem buffer (row-major, local) with one warp
-FTLZ_DEV void load_block_rows(const float* __restrict__ x, const Geom& g, const BlockInfo& B,
-                              float* buf, int lane) {
-    int nrows = B.bx * B.by;
-    long long base = ((B.bi * g.e) * g.ny + B.bj * g.e) * g.nz + B.bk * g.e;
-    // each iteration covers 32 / bz rows when bz <= 32 (lanes split across rows)
-    int bz = B.bz;
-    int rows_per = bz >= 32 ? 1 : 32 / bz;
-    int kk = lane % bz;
-    int rr = lane / bz;
-    if (bz < 32) {
-        for (int r0 = 0; r0 < nrows; r0 += rows_per) {
-            int r = r0 + rr;
-            if (rr < rows_per && r < nrows) {
-                int i = r / B.by, j = r - (r / B.by) * B.by;
-                buf[r * bz + kk] = __ldg(x + base + (long long)i * g.ny * g.nz + (long long)j * g.nz + kk);
-            }
-        }
-    } else {
-        for (int r = 0; r < nrows; r++) {
-            int i = r / B.by, j = r - i * B.by;
-            const float* row = x + base + (long long)i * g.ny * g.nz + (long long)j * g.nz;
-            for (int k = lane; k < bz; k += 32) buf[r * bz + k] = __ldg(row + k);
-        }
-    }
-}
-
-// ------------------------------------------------------------------------------------------
-// warp-cooperative single-word correction (checksum.py:109-142) on a u32 block in memory.
-// returns 0 clean, 1 corrected, 2 uncorrectable.  All lanes return the same value.
-FTLZ_DEV void warp_checksum(const u32* w, int n, int lane, u64* s, u64* si) {
-    u64 a = 0, c = 0;
-    for (int p = lane; p < n; p += 32) {
-        u64 v = w[p];
-        a += v;
-        c += (u64)p * v;
-    }
-    *s = warp_sum_u64(a);
-    *si = warp_sum_u64(c);
-}
-
-FTLZ_DEV int warp_correct_words(u32* w, int n, u64 st_s, u64 st_si, int lane) {
-    u64 s, si;
-    warp_checksum(w, n, lane, &s, &si);
-    if (s == st_s && si == st_si) return 0;
-    u64 ds = s - st_s, dsi = si - st_si;
-    if (ds == 0) return 2;
-    for (int j0 = 0; j0 < n; j0 += 32) {
-        int j = j0 + lane;
-        bool cand = j < n && (u64)j * ds == dsi;
-        unsigned m = __ballot_sync(0xffffffffu, cand);
-        while (m) {
-            int l = __ffs(m) - 1;
-            m &= m - 1;
-            int jj = j0 + l;
-            u64 old = w[jj];
-            u64 restored = old - ds;
-            if (restored >> 32) continue;
-            __syncwarp();
-            if (lane == 0) w[jj] = (u32)restored;
-            __syncwarp();
-            u64 s2, si2;
-            warp_checksum(w, n, lane, &s2, &si2);
-            if (s2 == st_s && si2 == st_si) return 1;
-            __syncwarp();
-            if (lane == 0) w[jj] = (u32)old;
-            __syncwarp();
-        }
-    }
-    return 2;
-}
 
 // ------------------------------------------------------------------------------------------
 // numpy pairwise sums over a block: chains of 8 strided accumulators per leaf, combined with
@@ -249,190 +171,6 @@ FTLZ_DEV void warp_pairwise(const Leaf* leaves, int nleaf, int n, Getter get, do
     for (int v = 0; v < NV; v++) out[v] = __shfl_sync(0xffffffffu, out[v], 0);
 }
 
-// ------------------------------------------------------------------------------------------
-// smem layout per block slot (bytes, 16-aligned): f32[vmax] | f64[vmax] | leafval | ar/al
-FTLZ_DEV size_t slot_f64_off(int vmax) { return ((size_t)vmax * 4 + 15) & ~(size_t)15; }
-
-// ==========================================================================================
-// K1: stage (a) + (b)
-__global__ void __launch_bounds__(128) k_prep(CompArgs A) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const Geom& g = A.g;
-    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    long long b = (long long)blockIdx.x * A.P + warp;
-    BlockInfo B = block_info(g, b);
-    unsigned char* slot = smem + (size_t)warp * A.nwarp_smem;
-    float* xf = (float*)slot;
-    double* xd = (double*)(slot + slot_f64_off(g.vmax));
-    double* leafval = xd + g.vmax;             // up to (vmax/64 + 2) * 4 doubles
-    double* ar = leafval + 4 * (g.vmax / 64 + 8);
-    double* al = ar + (g.vmax / 8 + 8);
-    __shared__ u32 cta_max, cta_min, cta_nan, cta_nreg;
-    if (threadIdx.x == 0) { cta_max = 0; cta_min = 0xffffffffu; cta_nan = 0; cta_nreg = 0; }
-    __syncthreads();
-    if (B.valid) {
-        load_block_rows(A.x, g, B, xf, lane);
-        __syncwarp();
-        const ExtPlan& PL = A.plans[B.xid];
-        int vol = B.vol;
-        // value range + f64 widening + input checksum (stage a)
-        u32 mx = 0, mn = 0xffffffffu, nan = 0;
-        u64 s = 0, si = 0;
-        for (int p = lane; p < vol; p += 32) {
-            float v = xf[p];
-            u32 w = __float_as_uint(v);
-            if (v != v) nan = 1;
-            else {
-                u32 o = f2ord(v);
-                mx = max(mx, o);
-                mn = min(mn, o);
-            }
-            xd[p] = f32_to_f64(v);
-            s += w;
-            si += (u64)p * w;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-            nan |= __shfl_xor_sync(0xffffffffu, nan, o);
-        }
-        s = warp_sum_u64(s);
-        si = warp_sum_u64(si);
-        if (lane == 0) {
-            atomicMax(&cta_max, mx);
-            atomicMin(&cta_min, mn);
-            atomicOr(&cta_nan, nan);
-        }
-        __syncwarp();
-        // regression fit (predict.py:81-104): S(v), S(ci v), S(cj v), S(ck v)
-        const u32* crd = A.coords + PL.coord_off;
-        double hx = (double)(B.bx - 1) / 2.0, hy = (double)(B.by - 1) / 2.0, hz = (double)(B.bz - 1) / 2.0;
-        double sums[4];
-        warp_pairwise<4>(A.leaves + PL.leaf_off, PL.nleaf, vol,
-                         [&](int p, double* t) {
-                             u32 c = __ldg(crd + p);
-                             double v = xd[p];
-                             double ci = __dadd_rn(int_to_f64((int)(c & 0xff)), -hx);
-                             double cj = __dadd_rn(int_to_f64((int)((c >> 8) & 0xff)), -hy);
-                             double ck = __dadd_rn(int_to_f64((int)(c >> 16)), -hz);
-                             t[0] = v;
-                             t[1] = __dmul_rn(ci, v);
-                             t[2] = __dmul_rn(cj, v);
-                             t[3] = __dmul_rn(ck, v);
-                         },
-                         leafval, sums, lane);
-        float4 cf;
-        {
-            double out0 = __ddiv_rn(sums[0], (double)vol);
-            double sl[3];
-            int ext[3] = {B.bx, B.by, B.bz};
-#pragma unroll
-            for (int ax = 0; ax < 3; ax++) {
-                int e = ext[ax];
-                if (e == 1) { sl[ax] = 0.0; continue; }
-                double denom = __ddiv_rn((double)((long long)vol * ((long long)e * e - 1)), 12.0);
-                sl[ax] = __ddiv_rn(sums[ax + 1], denom);
-                out0 = __dadd_rn(out0, -__ddiv_rn(__dmul_rn(sl[ax], (double)(e - 1)), 2.0));
-            }
-            cf = make_float4(__double2float_rn(out0), __double2float_rn(sl[0]),
-                             __double2float_rn(sl[1]), __double2float_rn(sl[2]));
-        }
-        // hooks after stage (a): COEFFS_FITTED then INPUT_AFTER_CHECKSUM (pipeline.py:328-329)
-        bool touched = false;
-        if (A.n_faults) {
-            int f0 = A.fault_first[b];
-            if (f0 >= 0) {
-                for (int f = f0; f < A.n_faults && A.faults[f].block == b; f++) {
-                    ftlz_fault F = A.faults[f];
-                    if (F.target == FTLZ_FAULT_COEFF) {
-                        float* c4 = (float*)&cf;
-                        c4[F.element] = __uint_as_float(__float_as_uint(c4[F.element]) ^ (1u << F.bit));
-                    } else if (F.target == FTLZ_FAULT_INPUT) {
-                        if (lane == 0) xf[F.element] = __uint_as_float(__float_as_uint(xf[F.element]) ^ (1u << F.bit));
-                        touched = true;
-                    }
-                }
-            }
-        }
-        __syncwarp();
-        bool bad = false;
-        if (touched) {
-            // stage (b) verification against the stage (a) checksum (pipeline.py:331-348)
-            if (A.protect_input) {
-                int r = warp_correct_words((u32*)xf, vol, s, si, lane);
-                if (r == 1 && lane == 0) { A.events[b] |= 1; atomicAdd(&A.counters[3], 1u); }
-                if (r == 2) {
-                    bad = true;
-                    if (lane == 0) { A.events[b] |= 4; atomicAdd(&A.counters[3], 1u); }
-                }
-            }
-            __syncwarp();
-            for (int p = lane; p < vol; p += 32) xd[p] = f32_to_f64(xf[p]);
-            __syncwarp();
-        }
-        if (!bad) {
-            // sampled selection (predict.py:196-231): |x - pred| on lanes, pairwise sums
-            int ns = PL.ns;
-            double c0 = (double)cf.x, c1 = (double)cf.y, c2 = (double)cf.z, c3 = (double)cf.w;
-            int byz = B.by * B.bz;
-            for (int q = lane; q < ns; q += 32) {
-                int p = 8 * (q + 1);
-                u32 c = __ldg(crd + p);
-                int i = c & 0xff, j = (c >> 8) & 0xff, k = c >> 16;
-                double v = xd[p];
-                double pr = __dadd_rn(__dadd_rn(__dadd_rn(c0, __dmul_rn(c1, int_to_f64(i))), __dmul_rn(c2, int_to_f64(j))),
-                                      __dmul_rn(c3, int_to_f64(k)));
-                double d100 = i > 0 ? xd[p - byz] : 0.0;
-                double d010 = j > 0 ? xd[p - B.bz] : 0.0;
-                double d001 = k > 0 ? xd[p - 1] : 0.0;
-                double d110 = (i > 0 && j > 0) ? xd[p - byz - B.bz] : 0.0;
-                double d101 = (i > 0 && k > 0) ? xd[p - byz - 1] : 0.0;
-                double d011 = (j > 0 && k > 0) ? xd[p - B.bz - 1] : 0.0;
-                double d111 = (i > 0 && j > 0 && k > 0) ? xd[p - byz - B.bz - 1] : 0.0;
-                double pl = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(d100, d010), d001), -d110), -d101), -d011), d111);
-                ar[q] = fabs(__dadd_rn(v, -pr));
-                al[q] = fabs(__dadd_rn(v, -pl));
-            }
-            __syncwarp();
-            double e2[2];
-            warp_pairwise<2>(A.leaves + PL.sleaf_off, PL.nsleaf, ns,
-                             [&](int q, double* t) { t[0] = ar[q]; t[1] = al[q]; }, leafval, e2, lane);
-            double er = e2[0], el = e2[1];
-            if (A.n_faults) {
-                int f0 = A.fault_first[b];
-                if (f0 >= 0)
-                    for (int f = f0; f < A.n_faults && A.faults[f].block == b; f++) {
-                        ftlz_fault F = A.faults[f];
-                        if (F.target != FTLZ_FAULT_ESTIMATE) continue;
-                        u64 bit = 1ull << F.bit;
-                        if (F.element == 0) er = __longlong_as_double((long long)(dbits(er) ^ bit));
-                        else el = __longlong_as_double((long long)(dbits(el) ^ bit));
-                    }
-            }
-            int kind = er < el ? 1 : 0;
-            if (A.override_ && A.override_[b] >= 0) kind = A.override_[b];
-            if (lane == 0) {
-                A.coef[b] = cf;
-                A.insum[b] = s;
-                A.inisum[b] = si;
-                A.ind[b] = (u8)kind;
-                if (kind == 1) atomicAdd(&cta_nreg, 1u);
-            }
-        } else if (lane == 0) {
-            A.ind[b] = 0;
-            A.coef[b] = cf;
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        atomicMax(&A.minmax[0], cta_max);
-        atomicMax(&A.minmax[1], ~cta_min);
-        if (cta_nan) atomicOr(&A.minmax[2], 1u);
-        if (cta_nreg) atomicAdd(&A.counters[0], cta_nreg);
-    }
-}
-
 // ==========================================================================================
 // resolve the bound (core.py:182-193) and the quantizer constants
 __global__ void k_resolve(CompArgs A) {
@@ -447,6 +185,7 @@ __global__ void k_resolve(CompArgs A) {
     Q.eb = eb;
     Q.twoeb = __dmul_rn(2.0, eb);
     Q.rcp = __ddiv_rn(1.0, Q.twoeb);
+    Q.twoeb_dup = __dmul_rn(eb, 2.0);
     Q.cap = A.cap;
     Q.center = A.cap / 2;
     Q.capd2 = 2.0 * (double)A.cap;
@@ -464,197 +203,6 @@ __global__ void k_resolve(CompArgs A) {
     }
     // uncorrectable input from stage (b) -> first in extent-sorted group order is chosen
     // by the host from events (pipeline.py:342-345); flag it here
-}
-
-// ==========================================================================================
-// K2: stage (c)
-struct DupPred {
-    double v;
-    bool mismatch;
-    bool disagree;
-};
-
-// 2-of-3 voting (pipeline.py:157-179) on scalars; eval3 called only on mismatch
-template <typename F3>
-FTLZ_DEV DupPred vote(double a, double b, bool enabled, F3 eval3) {
-    DupPred r;
-    r.v = a;
-    r.mismatch = false;
-    r.disagree = false;
-    if (!enabled) return r;
-    if (dbits(a) == dbits(b)) return r;
-    double c = eval3();
-    r.mismatch = true;
-    bool ab = false, ac = dbits(a) == dbits(c), bc = dbits(b) == dbits(c);
-    r.v = (ab || ac) ? a : b;
-    r.disagree = !(ab || bc || ac);
-    return r;
-}
-
-__global__ void __launch_bounds__(128) k_quant(CompArgs A) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const Geom& g = A.g;
-    if (dev_failed(A.st)) return;
-    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    long long b = (long long)blockIdx.x * A.P + warp;
-    BlockInfo B = block_info(g, b);
-    if (!B.valid) return;
-    if (A.events[b] & 4) return;  // stage (b) already failed this block
-    const QuantParams Q = *A.qp;
-    unsigned char* slot = smem + (size_t)warp * A.nwarp_smem;
-    float* xf = (float*)slot;
-    double* xd = (double*)(slot + slot_f64_off(g.vmax));
-    u16* bins16 = (u16*)(xd + g.vmax);
-    double* tabA = (double*)(((uintptr_t)(bins16 + g.vmax) + 15) & ~(uintptr_t)15);
-    double* tabB = tabA + 64;
-    double* tabC = tabB + 64;
-    load_block_rows(A.x, g, B, xf, lane);
-    __syncwarp();
-    int vol = B.vol;
-    // working-array faults persist only when stage (b) could not heal them (pipeline.py:331-361)
-    if (A.n_faults && !A.protect_input) {
-        int f0 = A.fault_first[b];
-        if (f0 >= 0 && lane == 0)
-            for (int f = f0; f < A.n_faults && A.faults[f].block == b; f++)
-                if (A.faults[f].target == FTLZ_FAULT_INPUT)
-                    xf[A.faults[f].element] = __uint_as_float(__float_as_uint(xf[A.faults[f].element]) ^ (1u << A.faults[f].bit));
-        __syncwarp();
-    }
-    if (A.protect_input) {
-        // stage (c) verification of the re-read input against the stage (a) checksum
-        int r = warp_correct_words((u32*)xf, vol, A.insum[b], A.inisum[b], lane);
-        if (r == 1 && lane == 0) { A.events[b] |= 1; atomicAdd(&A.counters[3], 1u); }
-        if (r == 2) {
-            if (lane == 0) { A.events[b] |= 4; atomicAdd(&A.counters[3], 1u); }
-            return;
-        }
-        __syncwarp();
-    }
-    const ExtPlan& PL = A.plans[B.xid];
-    const u32* crd = A.coords + PL.coord_off;
-    int kind = A.ind[b];
-    float4 cf = A.coef[b];
-    bool dup = A.dup_eval != 0;
-    bool mism = false;
-    u64 dcsum = 0;
-    int byz = B.by * B.bz;
-    if (kind == 1) {
-        double c0 = (double)cf.x, c1 = (double)cf.y, c2 = (double)cf.z, c3 = (double)cf.w;
-        // A[i] = b0 + b1*i (rounded), B[j] = b2*j, C[k] = b3*k (exact products)
-        for (int t = lane; t < 64; t += 32) {
-            tabA[t] = __dadd_rn(c0, __dmul_rn(c1, int_to_f64(t)));
-            tabB[t] = __dmul_rn(c2, int_to_f64(t));
-            tabC[t] = __dmul_rn(c3, int_to_f64(t));
-        }
-        __syncwarp();
-        for (int p = lane; p < vol; p += 32) {
-            u32 c = __ldg(crd + p);
-            int i = c & 0xff, j = (c >> 8) & 0xff, k = c >> 16;
-            float x32 = xf[p];
-            double x64 = f32_to_f64(x32);
-            double p1 = __dadd_rn(__dadd_rn(tabA[i], tabB[j]), tabC[k]);
-            double p2 = dup ? __dadd_rn(__dadd_rn(opaque(tabA[i]), tabB[j]), tabC[k]) : p1;
-            DupPred pr = vote(p1, p2, dup, [&] {
-                return __dadd_rn(__dadd_rn(__dadd_rn(c0, __dmul_rn(c1, int_to_f64(i))), __dmul_rn(c2, int_to_f64(j))),
-                                 __dmul_rn(c3, int_to_f64(k)));
-            });
-            double pred = pr.v;
-            bool ok;
-            int bin = quantize(Q, __dadd_rn(x64, -pred), &ok);
-            if (pr.disagree) ok = false;
-            double offs = int_to_f64(bin - Q.center);
-            double d1 = __dadd_rn(pred, __dmul_rn(Q.twoeb, offs));
-            double d2 = dup ? __dadd_rn(opaque(pred), __dmul_rn(Q.twoeb, offs)) : d1;
-            DupPred dr = vote(d1, d2, dup, [&] { return __dadd_rn(pred, __dmul_rn(Q.twoeb, opaque(offs))); });
-            if (dr.disagree) ok = false;
-            mism |= pr.mismatch | dr.mismatch;
-            float d32 = __double2float_rn(dr.v);
-            bool keep = ok && within_eb(__dadd_rn(x64, -f32_to_f64(d32)), Q.eb_bits);
-            float r32 = keep ? d32 : x32;
-            bins16[p] = (u16)(keep ? bin : 0);
-            dcsum += __float_as_uint(r32);
-        }
-    } else {
-        // Lorenzo wavefront over constant i+j+k planes (pipeline.py:199-213, 410-438);
-        // xd holds float64 reconstructed values in place (only earlier planes are read)
-        const u32* wave = A.wave + PL.wave_off;
-        const u32* planes = A.planes + PL.plane_off;
-        int bz = B.bz;
-        for (int s = 0; s < PL.nplanes; s++) {
-            int q0 = __ldg(planes + s), q1 = __ldg(planes + s + 1);
-            for (int q = q0 + lane; q < q1; q += 32) {
-                int p = __ldg(wave + q);
-                u32 c = __ldg(crd + p);
-                int i = c & 0xff, j = (c >> 8) & 0xff, k = c >> 16;
-                float x32 = xf[p];
-                double x64 = f32_to_f64(x32);
-                double d100 = i > 0 ? xd[p - byz] : 0.0;
-                double d010 = j > 0 ? xd[p - bz] : 0.0;
-                double d001 = k > 0 ? xd[p - 1] : 0.0;
-                double d110 = (i > 0 && j > 0) ? xd[p - byz - bz] : 0.0;
-                double d101 = (i > 0 && k > 0) ? xd[p - byz - 1] : 0.0;
-                double d011 = (j > 0 && k > 0) ? xd[p - bz - 1] : 0.0;
-                double d111 = (i > 0 && j > 0 && k > 0) ? xd[p - byz - bz - 1] : 0.0;
-                auto lor = [&](double first) {
-                    return __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(first, d010), d001), -d110), -d101), -d011), d111);
-                };
-                double p1 = lor(d100);
-                double p2 = dup ? lor(opaque(d100)) : p1;
-                DupPred pr = vote(p1, p2, dup, [&] { return lor(opaque(opaque(d100))); });
-                double pred = pr.v;
-                bool ok;
-                int bin = quantize(Q, __dadd_rn(x64, -pred), &ok);
-                if (pr.disagree) ok = false;
-                double offs = int_to_f64(bin - Q.center);
-                double d1 = __dadd_rn(pred, __dmul_rn(Q.twoeb, offs));
-                double d2 = dup ? __dadd_rn(opaque(pred), __dmul_rn(Q.twoeb, offs)) : d1;
-                DupPred dr = vote(d1, d2, dup, [&] { return __dadd_rn(pred, __dmul_rn(Q.twoeb, opaque(offs))); });
-                if (dr.disagree) ok = false;
-                mism |= pr.mismatch | dr.mismatch;
-                float d32 = __double2float_rn(dr.v);
-                double back = f32_to_f64(d32);
-                bool keep = ok && within_eb(__dadd_rn(x64, -back), Q.eb_bits);
-                float r32 = keep ? d32 : x32;
-                xd[p] = keep ? back : x64;
-                bins16[p] = (u16)(keep ? bin : 0);
-                dcsum += __float_as_uint(r32);
-            }
-            __syncwarp();
-        }
-    }
-    __syncwarp();
-    // emit pass in row-major order: unpredictable words, bins checksum, histogram, bins store
-    u64 bs = 0, bis = 0;
-    u32 nunp = 0;
-    u32* unp = A.unp_scratch + (size_t)b * g.vmax;
-    for (int p0 = 0; p0 < vol; p0 += 32) {
-        int p = p0 + lane;
-        bool act = p < vol;
-        int bin = act ? bins16[p] : -1;
-        unsigned zm = __ballot_sync(0xffffffffu, bin == 0);
-        if (bin == 0) unp[nunp + __popc(zm & ((1u << lane) - 1u))] = __float_as_uint(xf[p]);
-        nunp += __popc(zm);
-        if (act) {
-            bs += (u64)bin;
-            bis += (u64)p * (u64)bin;
-            A.bins[bins_index(g, b, p)] = (u16)bin;
-        }
-        // warp-aggregated histogram update
-        unsigned peers = __match_any_sync(0xffffffffu, bin);
-        if (act && lane == __ffs(peers) - 1) atomicAdd(&A.hist[bin], (u32)__popc(peers));
-    }
-    dcsum = warp_sum_u64(dcsum);
-    bs = warp_sum_u64(bs);
-    bis = warp_sum_u64(bis);
-    unsigned anym = __ballot_sync(0xffffffffu, mism);
-    if (lane == 0) {
-        A.unpc[b] = nunp;
-        if (nunp) atomicAdd((u64*)&A.layout[LAYOUT_NUNP], (u64)nunp);
-        A.bsum[b] = bs;
-        A.bisum[b] = bis;
-        A.dcs[b] = dcsum;
-        if (anym) atomicOr(&A.counters[1], 1u << (B.xid * 2 + kind));
-    }
 }
 
 // ==========================================================================================
