@@ -23,7 +23,6 @@ import json
 import math
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -79,56 +78,61 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled every 5 ms through NVML while the timed region runs
+    (the timed region is tens of milliseconds, too short for nvidia-smi's 100 ms loop)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+             ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+             ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+             ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+             ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
     def __init__(self, device: int):
         self.device = device
-        self.proc = None
-        self.lines = []
+        self.sm, self.reasons, self.mx = [], set(), None
+        self.h = None
+        self.stop_ev = threading.Event()
+        try:
+            import pynvml as N
+            import torch
+
+            N.nvmlInit()
+            p = torch.cuda.get_device_properties(device)
+            try:
+                bus = f"{p.pci_domain_id:08X}:{p.pci_bus_id:02X}:{p.pci_device_id:02X}.0"
+                self.h = N.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                self.h = N.nvmlDeviceGetHandleByIndex(device)
+            self.N = N
+            self.mx = float(N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM))
+        except Exception:
+            self.h = None
+
+    def _loop(self):
+        N = self.N
+        while not self.stop_ev.is_set():
+            try:
+                self.sm.append(float(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, attr in self.NAMES:
+                    if r & getattr(N, attr, 0):
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+        if self.h is not None:
+            self.t = threading.Thread(target=self._loop, daemon=True)
             self.t.start()
-        except Exception:
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
 
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.15)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except Exception:
-            self.proc.kill()
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [s.strip() for s in ln.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
-            except ValueError:
-                continue
-            for n, v in zip(names, f[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if self.h is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        self.stop_ev.set()
+        self.t.join()
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.mx,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml, 5 ms"}
 
 
 def dist_setup():
@@ -298,12 +302,14 @@ def run_ours(args, world, rank, local):
 
     # ---- parity of the timed workload against the reference's own archive / output hashes
     parity = {}
+    parity_archive = None
     try:
         ent = json.load(open(os.path.join(ROOT, "tests", "golden", "manifest.json")))["large"][args.workload]
         aptr, alen, _ = c_compress(cfg)
         arch = torch.empty(alen, dtype=torch.uint8, device=f"cuda:{local}")
         ctypes_cuda().cudaMemcpy(C.c_void_p(arch.data_ptr()), C.c_void_p(aptr), C.c_size_t(alen), 3)
         hb = arch.cpu().numpy()
+        parity_archive = hb.tobytes()
         c_decompress(aptr, alen)
         outh = d_out.cpu().numpy()
         parity = {"archive_sha256_match": synth.sha256(hb) == ent["archive_sha256"],
@@ -334,8 +340,11 @@ def run_ours(args, world, rank, local):
     if dom:
         dms = kern[dom]["ms_per_step"]
         a_bytes = alg.get(dom, 0.0)
+        traffic = ncu_traffic().get(dom)
         roof = {"bound": "hbm", "kernel": dom, "achieved": a_bytes / (dms * 1e-3) / 1e9, "peak": peak,
-                "unit": "GB/s", "frac": a_bytes / (dms * 1e-3) / 1e9 / peak, "traffic": None,
+                "unit": "GB/s", "frac": a_bytes / (dms * 1e-3) / 1e9 / peak,
+                "traffic": traffic["dram_bytes"] if traffic else None,
+                "traffic_source": traffic["source"] if traffic else None,
                 "peak_source": peak_kind, "algorithmic_bytes_per_launch": a_bytes}
 
     line = {
@@ -345,7 +354,8 @@ def run_ours(args, world, rank, local):
         "config": {"workload": WORKLOADS[args.workload], "l2": "256 MiB flush between steps; input 512 MiB > L2",
                    "parallelism": f"replicas x{world}"},
         "compress": {"gbs_input": n_bytes / (tc_ms * 1e-3) / 1e9, "ms": tc_ms, "algorithmic_bytes": Bc,
-                     "roofline_frac": ach_c / peak, "kernels": comp_k},
+                     "roofline_frac": ach_c / peak, "single_read_frac": (4.0 * N + S) / (tc_ms * 1e-3) / 1e9 / peak,
+                     "kernels": comp_k},
         "decompress": {"gbs_input": n_bytes / (td_ms * 1e-3) / 1e9, "ms": td_ms, "algorithmic_bytes": Bd,
                        "roofline_frac": ach_d / peak, "kernels": dec_k},
         "roofline": roof,
@@ -391,16 +401,22 @@ def run_ours(args, world, rank, local):
 
         threads = os.cpu_count() or 1
         mode_, v_ = synth.CONFIGS[args.workload]["eb"]
-        t0 = time.perf_counter()
-        data, _ = O.compress(x, mode_, v_, threads=threads)
-        t1 = time.perf_counter()
-        O.decompress(data, threads=threads)
-        t2 = time.perf_counter()
-        cv = n_bytes / ((t1 - t0) + (t2 - t1)) / 1e9
+        tcs, tds, t_start = [], [], time.perf_counter()
+        while len(tcs) < 30 and (time.perf_counter() - t_start < 10.0 or len(tcs) < 2):
+            t0 = time.perf_counter()
+            data, _ = O.compress(x, mode_, v_, threads=threads)
+            t1 = time.perf_counter()
+            O.decompress(data, threads=threads)
+            t2 = time.perf_counter()
+            tcs.append(t1 - t0)
+            tds.append(t2 - t1)
+        tcm, tdm = statistics.median(tcs), statistics.median(tds)
+        cv = n_bytes / (tcm + tdm) / 1e9
         line["cpu_baseline"] = {"value": cv, "unit": "GB/s", "cores": threads, "kind": "port",
-                                "sample": f"full {args.workload} field, one compress+decompress round trip "
-                                          "(oracle/ftlz_oracle.c, OpenMP)",
-                                "compress_s": t1 - t0, "decompress_s": t2 - t1}
+                                "sample": f"full {args.workload} field, {len(tcs)} compress+decompress round trips "
+                                          "(~10 s of CPU work; median), oracle/ftlz_oracle.c with OpenMP",
+                                "compress_s": tcm, "decompress_s": tdm,
+                                "archive_identical_to_gpu": (data == parity_archive) if parity_archive else None}
 
     # ---- c5: seeded 1% single-bit flips on the c2 field at rel 1e-3
     if rank == 0 and not args.quick and not args.no_c5:
@@ -450,6 +466,23 @@ def run_c5(F, L, _lib, torch, local):
             r["reference_archive_match"] = synth.sha256(np.frombuffer(data, np.uint8)) == man[tgt]["archive_sha256"]
         res[tgt] = r
     return res
+
+
+def ncu_traffic() -> dict:
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of each kernel from the
+    newest committed `ncu --set full` summary under profiles/ (tools/profile_round.sh)."""
+    import glob
+
+    out = {}
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_kernels.json"))):
+        try:
+            d = json.load(open(f))
+        except Exception:
+            continue
+        for k, v in d.get("kernels", {}).items():
+            if v.get("dram_bytes") is not None:
+                out[k] = {"dram_bytes": v["dram_bytes"], "source": os.path.relpath(f, ROOT)}
+    return out
 
 
 def rc_eb(data: bytes) -> float:
