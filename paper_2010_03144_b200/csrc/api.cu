@@ -13,9 +13,11 @@
 #include <tuple>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "compress.cu"
 #include "blocks.cu"
-#include "quant_reg.cu"
+#include "quant_block.cu"
 #include "decompress.cu"
 
 using namespace ftlz;
@@ -258,7 +260,36 @@ struct KCfg {
     size_t tile_bytes;
     size_t prep_smem, reg_smem, lor_smem, lor_slot;
     int reg_threads, lor_warps;
+    StageCfg stage;
+    int qr_warps, qr_slot, qr_tab, rmax;
+    size_t qr_smem;
 };
+
+// TMA tensor map of the input field (dims nz, ny, nx innermost first) with a box of one block
+// tile; returns 0 when the field cannot be described (rows not 16-byte aligned) -> cp.async path
+static int make_input_map(CUtensorMap* m, const float* d_in, const Geom& g, const StageCfg& S) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    static std::once_flag fl;
+    std::call_once(fl, [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    });
+    static const bool no_tma = getenv("FTLZ_NO_TMA") != nullptr;   // debugging switch
+    if (no_tma || !enc || (g.nz & 3) || ((uintptr_t)d_in & 15) || g.nz > (1ll << 32) || g.ny > (1ll << 32) ||
+        g.nx > (1ll << 32) || S.tz > 256 || S.tye > 256 || S.tz > g.nz)
+        return 0;
+    cuuint64_t dims[3] = {(cuuint64_t)g.nz, (cuuint64_t)g.ny, (cuuint64_t)g.nx};
+    cuuint64_t strides[2] = {(cuuint64_t)g.nz * 4, (cuuint64_t)g.nz * g.ny * 4};
+    cuuint32_t box[3] = {(cuuint32_t)S.tz, (cuuint32_t)S.tye, (cuuint32_t)(S.box_bytes / (4 * S.tz * S.tye))};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)d_in, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 1 : 0;
+}
 
 static KCfg kcfg_comp(const Geom& g) {
     KCfg k;
@@ -277,9 +308,28 @@ static KCfg kcfg_comp(const Geom& g) {
     size_t v = (size_t)g.vmax;
     size_t per_warp = (4 * (v / 64 + 8) + 2 * (v / 8 + 8) + 3 * 64) * 8;
     k.prep_smem = k.tile_bytes + per_warp * P;
-    k.reg_smem = 2 * k.tile_bytes + al16(2 * (size_t)g.nvmax8 * P) + 64 * 8 * (size_t)P + 4 * HWIN +
-                 sizeof(RowAcc) * (size_t)rows * P;
     k.reg_threads = std::min(416, std::max((rows * P + 31) & ~31, 32 * P));   // __launch_bounds__(416, 2)
+    // k_quant_reg: per-warp slots (2 TMA tiles, bins, row tables, lane histogram, mbarriers)
+    {
+        int ez = (int)std::min<int64_t>(g.e, g.nz);
+        int maxshift = (g.e % 4 == 0) ? 0 : 4 - ((g.e % 2 == 0) ? 2 : 1);   // (bk*e) mod 4 <= this
+        int tz = (ez + maxshift + 3) & ~3;
+        int tye = (int)std::min<int64_t>(g.e, g.ny), txe = (int)std::min<int64_t>(g.e, g.nx);
+        k.stage.use_tma = 0;
+        k.stage.tz = tz;
+        k.stage.tye = tye;
+        k.stage.box_bytes = tz * tye * txe * 4;
+        k.stage.tile_bytes = (int)((k.stage.box_bytes + 127) & ~127);
+        k.stage.pad = 0;
+        k.rmax = txe * tye;
+        k.qr_tab = (int)al16(2 * k.stage.tile_bytes + al16(2 * (size_t)g.nvmax8));
+        size_t slot = (size_t)k.qr_tab + 8 * (2 * (size_t)k.rmax + 64) + 4 * 32 * 32 + 16;
+        slot = (slot + 127) & ~(size_t)127;
+        k.qr_slot = (int)slot;
+        size_t avail = 227 * 1024 - 4 * HWIN_REG - 128;
+        k.qr_warps = (int)std::max<size_t>(1, std::min<size_t>(12, avail / slot));
+        k.qr_smem = slot * k.qr_warps + 4 * HWIN_REG + 128;   // + alignment slack
+    }
     k.lor_slot = al16(4 * v) + 8 * v + al16(2 * v);
     k.lor_warps = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / k.lor_slot));
     k.lor_smem = k.lor_slot * k.lor_warps + 4 * HWIN;
@@ -476,7 +526,7 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     CompLayout L = comp_layout(P, cap, nf);
     if (ws_size < L.total) return set_err(FTLZ_ERR_CAPACITY, "workspace too small");
     KCfg K = kcfg_comp(g);
-    if (std::max(K.prep_smem, std::max(K.reg_smem, K.lor_smem)) > 227 * 1024 || K.reg_threads > 1024)
+    if (std::max(K.prep_smem, std::max(K.qr_smem, K.lor_smem)) > 227 * 1024)
         return set_err(FTLZ_ERR_INVALID_ARGUMENT, "block too large for the shared-memory path (block_edge <= 24)");
     if ((rc = kernel_attrs_once())) return set_err(rc, "cudaFuncSetAttribute failed");
     DevPlan D;
@@ -512,6 +562,15 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
         A.pio.per_full = make_fastdiv((u32)per(K.P * g.e));
         A.pio.per_last = make_fastdiv((u32)per((nlast - 1) * g.e + g.rz));
     }
+    A.fd_rz = make_fastdiv((u32)g.rz);
+    A.stage = K.stage;
+    A.qr_slot = K.qr_slot;
+    A.qr_tab = K.qr_tab;
+    A.rmax = K.rmax;
+    A.dbg = getenv("FTLZ_DBG") ? atoi(getenv("FTLZ_DBG")) : 0;
+    CUtensorMap tmap;
+    memset(&tmap, 0, sizeof tmap);
+    A.stage.use_tma = make_input_map(&tmap, d_in, g, K.stage);
     A.lor_slot = (int)K.lor_slot;
     A.lor_list = (u32*)(ws + L.lor);
     A.n_faults = (int)nf;
@@ -546,13 +605,7 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     LCHK("k_resolve");
     PF.mark("k_quant_reg", s);
     {
-        static int occ_reg = 0;
-        if (!occ_reg) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_reg, k_quant_reg, K.reg_threads, K.reg_smem);
-            if (occ_reg < 1) occ_reg = 1;
-        }
-        long long grid = std::min<long long>(K.npencils, (long long)num_sms() * occ_reg);
-        k_quant_reg<<<(unsigned)grid, K.reg_threads, K.reg_smem, s>>>(A);
+        k_quant_reg<<<(unsigned)num_sms(), 32 * K.qr_warps, K.qr_smem, s>>>(A, tmap);
     }
     LCHK("k_quant_reg");
     PF.mark("k_quant_lor", s);

@@ -84,6 +84,7 @@ FTLZ_DEV void load_pencil(const float* __restrict__ x, const Geom& g, const Penc
 // element p (row-major in block) -> tile address, incremental walker
 struct TileWalk {
     int i, j, k, bx, by, bz, stride, zoff;
+    int bye;  // tile rows per i (== by for pencil tiles, == e for per-block TMA tiles)
     FTLZ_DEV void set(int p) {
         int byz = by * bz;
         i = p / byz;
@@ -91,7 +92,7 @@ struct TileWalk {
         j = rem / bz;
         k = rem - j * bz;
     }
-    FTLZ_DEV int addr() const { return (i * by + j) * stride + zoff + k; }
+    FTLZ_DEV int addr() const { return (i * bye + j) * stride + zoff + k; }
     FTLZ_DEV void advance(int d) {  // p += d
         k += d;
         while (k >= bz) {
@@ -196,7 +197,7 @@ __global__ void __launch_bounds__(512) k_prep(CompArgs A) {
         int xid = ((bx != g.e) ? 4 : 0) | ((by != g.e) ? 2 : 0) | ((bz != g.e) ? 1 : 0);
         const ExtPlan& PL = A.plans[xid];
         TileWalk w0;
-        w0.bx = bx; w0.by = by; w0.bz = bz; w0.stride = A.tile_stride; w0.zoff = warp * g.e;
+        w0.bx = bx; w0.by = by; w0.bz = bz; w0.stride = A.tile_stride; w0.zoff = warp * g.e; w0.bye = by;
         double hx = (double)(bx - 1) / 2.0, hy = (double)(by - 1) / 2.0, hz = (double)(bz - 1) / 2.0;
         for (int t = lane; t < 64; t += 32) {
             cv[t] = __dadd_rn(int_to_f64(t), -hx);
@@ -563,7 +564,7 @@ __global__ void __launch_bounds__(128) k_quant_lor(CompArgs A) {
         long long base = ((B.bi * g.e) * g.ny + B.bj * g.e) * g.nz + B.bk * g.e;
         {
             TileWalk w;
-            w.bx = B.bx; w.by = B.by; w.bz = bz; w.stride = 0; w.zoff = 0;
+            w.bx = B.bx; w.by = B.by; w.bz = bz; w.stride = 0; w.zoff = 0; w.bye = B.by;
             w.set(lane);
             for (int p = lane; p < vol; p += 32) {
                 cp_async4(xf + p, A.x + base + ((long long)w.i * g.ny + w.j) * g.nz + w.k);
@@ -573,7 +574,7 @@ __global__ void __launch_bounds__(128) k_quant_lor(CompArgs A) {
         }
         __syncwarp();
         TileWalk w0;
-        w0.bx = B.bx; w0.by = B.by; w0.bz = bz; w0.stride = bz * B.by; w0.zoff = 0;
+        w0.bx = B.bx; w0.by = B.by; w0.bz = bz; w0.stride = bz * B.by; w0.zoff = 0; w0.bye = B.by;
         // block-local layout: addr = (i*by + j)*bz + k  (stride = bz per row with by rows)
         w0.stride = bz;
         if (!A.protect_input) apply_input_faults(A, b, xf, w0, lane);

@@ -15,6 +15,7 @@
 #include <cstdio>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace ftlz {
 
@@ -32,6 +33,11 @@ struct CompArgs {
     long long npencils;
     FastDiv fd_npz, fd_cy, fd_e, fd_ry;   // launch-constant divisors (pencil / row decomposition)
     PencilIO pio;
+    FastDiv fd_rz;
+    StageCfg stage;           // per-block TMA tiles (k_quant_reg)
+    int qr_slot, qr_tab;      // k_quant_reg: smem bytes per warp, offset of the row tables in a slot
+    int rmax;                 // rows per block (max)
+    int dbg;                  // debugging switches (FTLZ_DBG)
     int tile_stride;          // floats per staged row (padded)
     int tile_bytes;           // bytes of the staged pencil tile
     int lor_slot;             // smem bytes per warp in k_quant_lor
