@@ -18,6 +18,7 @@
 #include "compress.cu"
 #include "blocks.cu"
 #include "quant_block.cu"
+#include "prep_block.cu"
 #include "decompress.cu"
 
 using namespace ftlz;
@@ -173,6 +174,8 @@ static bool build_plan(int64_t nx, int64_t ny, int64_t nz, int e, HostPlan& P) {
     int mx = (int)std::min<int64_t>(e, nx), my = (int)std::min<int64_t>(e, ny), mz = (int)std::min<int64_t>(e, nz);
     g.vmax = mx * my * mz;
     g.nvmax8 = (g.vmax + 7) & ~7;
+    g.fcz = make_fastdiv((u32)std::min<int64_t>(g.cz, 0xffffffffll));
+    g.fcy = make_fastdiv((u32)std::min<int64_t>(g.cy, 0xffffffffll));
     P.leaves.clear(); P.coords.clear(); P.wave.clear(); P.planes.clear();
     for (int xid = 0; xid < 8; xid++) {
         ExtPlan& E = P.ep[xid];
@@ -190,6 +193,11 @@ static bool build_plan(int64_t nx, int64_t ny, int64_t nz, int e, HostPlan& P) {
         E.sleaf_off = (int)P.leaves.size();
         if (E.ns >= 8) pw_leaves(0, E.ns, P.leaves);
         E.nsleaf = (int)P.leaves.size() - E.sleaf_off;
+        {
+            const int ext[3] = {E.bx, E.by, E.bz};
+            for (int ax = 0; ax < 3; ax++)
+                E.den[ax] = (double)((long long)vol * ((long long)ext[ax] * ext[ax] - 1)) / 12.0;
+        }
         E.coord_off = (int)P.coords.size();
         for (int i = 0; i < E.bx; i++)
             for (int j = 0; j < E.by; j++)
@@ -253,16 +261,13 @@ static int upload_plan(const HostPlan& P, unsigned char* dst, DevPlan& D, cudaSt
 static size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 struct KCfg {
-    int P;               // blocks per pencil
-    long long npz;       // pencils per block row
-    long long npencils;
-    int stride;          // padded floats per staged row
-    size_t tile_bytes;
-    size_t prep_smem, reg_smem, lor_smem, lor_slot;
-    int reg_threads, lor_warps;
+    size_t lor_smem, lor_slot;
+    int lor_warps;
     StageCfg stage;
     int qr_warps, qr_slot, qr_tab, rmax;
     size_t qr_smem;
+    int pp_warps, pp_slot, pp_nls, pp_ns;
+    size_t pp_smem;
 };
 
 // TMA tensor map of the input field (dims nz, ny, nx innermost first) with a box of one block
@@ -293,22 +298,7 @@ static int make_input_map(CUtensorMap* m, const float* d_in, const Geom& g, cons
 
 static KCfg kcfg_comp(const Geom& g) {
     KCfg k;
-    int rows = (int)std::min<int64_t>(g.e, g.nx) * (int)std::min<int64_t>(g.e, g.ny);
-    int P = std::max(1, std::min(12, 400 / std::max(rows, 1)));   // k_quant_reg: a warp per block in setup
-    if (P > 1 && ((P * g.e) & 3)) P &= ~1;                 // keep pencil rows 16-byte multiples
-    P = std::max(1, (int)std::min<int64_t>(P, g.cz));
-    k.P = P;
-    k.npz = (g.cz + P - 1) / P;
-    k.npencils = g.cx * g.cy * k.npz;
-    int L = (int)std::min<int64_t>((int64_t)P * g.e, g.nz);   // longest pencil row
-    int st = (L + 3) & ~3;
-    if ((st & 7) == 0) st += 4;                            // stride/4 odd: conflict-free 16B phases
-    k.stride = st;
-    k.tile_bytes = al16((size_t)rows * st * 4);
     size_t v = (size_t)g.vmax;
-    size_t per_warp = (4 * (v / 64 + 8) + 2 * (v / 8 + 8) + 3 * 64) * 8;
-    k.prep_smem = k.tile_bytes + per_warp * P;
-    k.reg_threads = std::min(416, std::max((rows * P + 31) & ~31, 32 * P));   // __launch_bounds__(416, 2)
     // k_quant_reg: per-warp slots (2 TMA tiles, bins, row tables, lane histogram, mbarriers)
     {
         int ez = (int)std::min<int64_t>(g.e, g.nz);
@@ -323,12 +313,20 @@ static KCfg kcfg_comp(const Geom& g) {
         k.stage.pad = 0;
         k.rmax = txe * tye;
         k.qr_tab = (int)al16(2 * k.stage.tile_bytes + al16(2 * (size_t)g.nvmax8));
-        size_t slot = (size_t)k.qr_tab + 8 * (2 * (size_t)k.rmax + 64) + 4 * 32 * 32 + 16;
+        size_t slot = (size_t)k.qr_tab + 8 * (2 * (size_t)k.rmax + 64) + 2 * 32 * 65 + 16;
         slot = (slot + 127) & ~(size_t)127;
         k.qr_slot = (int)slot;
         size_t avail = 227 * 1024 - 4 * HWIN_REG - 128;
         k.qr_warps = (int)std::max<size_t>(1, std::min<size_t>(12, avail / slot));
         k.qr_smem = slot * k.qr_warps + 4 * HWIN_REG + 128;   // + alignment slack
+        // k_prep: 2 tiles, centred-coordinate tables, fold stack, leaf partials, samples
+        k.pp_nls = (int)(v / 64 + 8);
+        k.pp_ns = (int)(v / 8 + 8);
+        size_t ps = 2 * (size_t)k.stage.tile_bytes + 8 * (192 + 128 + 4 * (size_t)k.pp_nls + 2 * (size_t)k.pp_ns) + 16;
+        ps = (ps + 127) & ~(size_t)127;
+        k.pp_slot = (int)ps;
+        k.pp_warps = (int)std::max<size_t>(1, std::min<size_t>(16, (227 * 1024 - 256) / ps));
+        k.pp_smem = ps * k.pp_warps + 128;
     }
     k.lor_slot = al16(4 * v) + 8 * v + al16(2 * v);
     k.lor_warps = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / k.lor_slot));
@@ -526,7 +524,7 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     CompLayout L = comp_layout(P, cap, nf);
     if (ws_size < L.total) return set_err(FTLZ_ERR_CAPACITY, "workspace too small");
     KCfg K = kcfg_comp(g);
-    if (std::max(K.prep_smem, std::max(K.qr_smem, K.lor_smem)) > 227 * 1024)
+    if (std::max(K.pp_smem, std::max(K.qr_smem, K.lor_smem)) > 227 * 1024)
         return set_err(FTLZ_ERR_INVALID_ARGUMENT, "block too large for the shared-memory path (block_edge <= 24)");
     if ((rc = kernel_attrs_once())) return set_err(rc, "cudaFuncSetAttribute failed");
     DevPlan D;
@@ -551,22 +549,13 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     A.dup_eval = cfg->duplicate_eval; A.store_sum_dc = cfg->store_sum_dc;
     A.eb_mode = eb_mode; A.eb_value = eb_value;
     A.cap = cap; A.center = cap / 2;
-    A.P = K.P; A.npz = K.npz; A.npencils = K.npencils;
-    A.fd_npz = make_fastdiv((u32)K.npz); A.fd_cy = make_fastdiv((u32)g.cy);
-    A.fd_e = make_fastdiv((u32)g.e); A.fd_ry = make_fastdiv((u32)g.ry); A.tile_stride = K.stride; A.tile_bytes = (int)K.tile_bytes;
-    {
-        int vec = (g.nz % 4 == 0) && ((g.e * K.P) % 4 == 0) && (((uintptr_t)d_in & 15) == 0);
-        auto per = [&](int L) { return vec ? L / 4 + L % 4 : L; };
-        int nlast = (int)(g.cz - (int64_t)(K.npz - 1) * K.P);
-        A.pio.vec = vec;
-        A.pio.per_full = make_fastdiv((u32)per(K.P * g.e));
-        A.pio.per_last = make_fastdiv((u32)per((nlast - 1) * g.e + g.rz));
-    }
+    A.fd_e = make_fastdiv((u32)g.e); A.fd_ry = make_fastdiv((u32)g.ry);
     A.fd_rz = make_fastdiv((u32)g.rz);
     A.stage = K.stage;
     A.qr_slot = K.qr_slot;
     A.qr_tab = K.qr_tab;
     A.rmax = K.rmax;
+    A.pp_slot = K.pp_slot; A.pp_nls = K.pp_nls; A.pp_ns = K.pp_ns;
     A.dbg = getenv("FTLZ_DBG") ? atoi(getenv("FTLZ_DBG")) : 0;
     CUtensorMap tmap;
     memset(&tmap, 0, sizeof tmap);
@@ -598,7 +587,7 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     S.parent = (u32*)(ws + L.cb_parent); S.lens = ws + L.cb_lens;
 
     PF.mark("k_prep", s);
-    k_prep<<<(unsigned)K.npencils, 32 * K.P, K.prep_smem, s>>>(A);
+    k_prep<<<(unsigned)num_sms(), 32 * K.pp_warps, K.pp_smem, s>>>(A, tmap);
     LCHK("k_prep");
     PF.mark("k_resolve", s);
     k_resolve<<<1, 1, 0, s>>>(A);

@@ -86,11 +86,6 @@ struct FastDiv {
     u32 pad;
 };
 FTLZ_DEV u32 fdiv(u32 n, const FastDiv& f) { return f.d == 1u ? n : (u32)__umul64hi((u64)n, f.m); }
-struct PencilIO {
-    FastDiv per_full, per_last;   // cp.async items per row for full / last pencils of a block row
-    int vec;                      // 16-byte chunks (rows 16-byte aligned)
-    int pad;
-};
 static inline FastDiv make_fastdiv(u32 d) {
     FastDiv f;
     f.d = d;
@@ -213,9 +208,18 @@ struct Geom {
     int rx, ry, rz;     // trailing extents (== e when the axis divides)
     int vmax;           // e^3
     int nvmax8;         // vmax rounded up to a multiple of 8 (bins layout)
+    FastDiv fcz, fcy;   // divisors for block coordinates (used when nb < 2^32)
 };
 
 FTLZ_DEV void block_coords(const Geom& g, long long b, long long* bi, long long* bj, long long* bk) {
+    if (g.nb < (1ll << 32)) {
+        u32 t = fdiv((u32)b, g.fcz);
+        *bk = (long long)((u32)b - t * (u32)g.cz);
+        u32 i = fdiv(t, g.fcy);
+        *bi = i;
+        *bj = (long long)(t - i * (u32)g.cy);
+        return;
+    }
     long long t = b / g.cz;
     *bk = b - t * g.cz;
     *bi = t / g.cy;
@@ -270,6 +274,7 @@ struct ExtPlan {
     int plane_off;           // (bx+by+bz-1) u32 plane start offsets (+1 sentinel)
     int nplanes;
     int pad;
+    double den[3];           // regression denominators vol * (n^2 - 1) / 12.0 per axis (predict.py:98)
 };
 
 // leaf descriptor: start (elements), len, combine count after pushing this leaf

@@ -2,10 +2,10 @@
 // (container.py:109-147) for B200 (sm_100a).
 //
 // Kernel sequence (one stream, no host sync until the report read-back):
-//   k_prep      (blocks.cu) stage (a)+(b): value range, input checksums, regression fit with numpy's
+//   k_prep      (prep_block.cu) stage (a)+(b): value range, input checksums, regression fit with numpy's
 //               pairwise float64 summation order, sampled predictor selection   (K0+K1)
 //   k_resolve   resolved error bound (core.py:182-193) + quantizer constants
-//   k_quant_*   (blocks.cu) stage (c): verify input, predict (duplicated), quantize, reconstruct
+//   k_quant_*   (quant_block.cu, blocks.cu) stage (c): verify input, predict (duplicated), quantize, reconstruct
 //               (duplicated), double-check, bins/unpredictables/checksums/sum_dc/histogram (K2)
 //   k_fault_bins  bins-stage faults: verify/correct (protect_bins) and histogram fix-up
 //   k_codebook  canonical Huffman codebook from the global histogram (K3), archive layout
@@ -28,18 +28,12 @@ struct CompArgs {
     int eb_mode;
     double eb_value;
     int cap, center;
-    int P;                    // blocks per pencil (CTA) in k_prep / k_quant_reg
-    long long npz;            // pencils per block row
-    long long npencils;
-    FastDiv fd_npz, fd_cy, fd_e, fd_ry;   // launch-constant divisors (pencil / row decomposition)
-    PencilIO pio;
-    FastDiv fd_rz;
+    FastDiv fd_e, fd_ry, fd_rz;   // launch-constant divisors (row decomposition)
     StageCfg stage;           // per-block TMA tiles (k_quant_reg)
     int qr_slot, qr_tab;      // k_quant_reg: smem bytes per warp, offset of the row tables in a slot
     int rmax;                 // rows per block (max)
+    int pp_slot, pp_nls, pp_ns;   // k_prep: smem bytes per warp, leaf / sample slots
     int dbg;                  // debugging switches (FTLZ_DBG)
-    int tile_stride;          // floats per staged row (padded)
-    int tile_bytes;           // bytes of the staged pencil tile
     int lor_slot;             // smem bytes per warp in k_quant_lor
     u32* lor_list;            // Lorenzo blocks (appended by k_prep)
     int n_faults;

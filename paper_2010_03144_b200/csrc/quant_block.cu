@@ -90,7 +90,17 @@ struct RegAcc {
     u64 cs, csi, bis, dc;
     u32 bs, nz;
     u32 flagged;   // some point of this lane needs the exact formulation
+    u32 outwin;    // some bin of this lane lies outside the lane-private window
 };
+
+// lane-private counter of an in-window bin; out-of-window bins go to the sink row LH_BINS
+FTLZ_DEV void lh_bump(u16* lh16, int lhlo, int bin, int lane, u32& outwin) {
+    unsigned o = (unsigned)(bin - lhlo);
+    const bool in = o < LH_BINS;
+    outwin |= (u32)!in;
+    o = in ? o : LH_BINS;
+    lh16[o * 32 + lane] += 1;
+}
 
 // position of a point inside the block / tile
 struct RegPos {
@@ -132,11 +142,11 @@ FTLZ_DEV u32 reg_point_fast(const QuantParams& Q, float x32, double ab, double a
 template <bool DUP, bool PIN, bool FULLJ>
 FTLZ_DEV void reg_points(const QuantParams& Q, const RegBlk& K, RegPos P, int p0, int pend, int lane, u16* lh16,
                          u32* hwin, u32* ghist, int lhlo, int wlo, RegAcc& acc) {
-    double ab = K.abt[P.rp], ab2 = DUP ? K.abt2[P.rp] : ab;
-    u32 flag = 0;
+    u32 flag = 0, outw = 0;
 #pragma unroll 4
     for (int p = p0; p < pend; p++) {
         const float x32 = K.tile[P.t];
+        const double ab = K.abt[P.rp], ab2 = DUP ? K.abt2[P.rp] : ab;
         if (PIN) {
             const u32 u = __float_as_uint(x32);
             acc.cs += (u64)u;
@@ -151,7 +161,7 @@ FTLZ_DEV void reg_points(const QuantParams& Q, const RegBlk& K, RegPos P, int p0
         acc.bis += (u64)(u32)p * (u64)fb;
         acc.dc += (u64)__float_as_uint(r32);
         acc.nz += fb == 0u;
-        reg_hist_add(lh16, hwin, ghist, lhlo, wlo, (int)fb, lane, 1);
+        lh_bump(lh16, lhlo, (int)fb, lane, outw);
         // walk (branch-free): k, then the row (j), then i
         P.k++;
         P.t++;
@@ -165,12 +175,17 @@ FTLZ_DEV void reg_points(const QuantParams& Q, const RegBlk& K, RegPos P, int p0
             P.j = w2 ? 0 : P.j;
             P.t += w2 ? K.ijump : 0;
         }
-        if (w) {
-            ab = K.abt[P.rp];
-            if (DUP) ab2 = K.abt2[P.rp];
-        }
     }
     acc.flagged = flag;
+    acc.outwin = outw;
+}
+
+// out-of-window bins of this lane's range (after any fixup): CTA window / global atomics
+FTLZ_DEV void reg_hist_outwin(const u16* bins16, int p0, int pend, u32* hwin, u32* ghist, int lhlo, int wlo) {
+    for (int p = p0; p < pend; p++) {
+        const int bin = bins16[p];
+        if ((unsigned)(bin - lhlo) >= LH_BINS) reg_hist_out(hwin, ghist, wlo, bin, 1u);
+    }
 }
 
 // exact recomputation of the ambiguous points of this lane (rare): rescan the range with the
@@ -202,8 +217,12 @@ FTLZ_DEV void reg_fixup(const QuantParams& Q, const RegBlk& K, const float4& cf,
         acc.bis += (u64)(u32)p * (u64)fb - (u64)(u32)p * (u64)fb_fast;
         acc.dc += (u64)__float_as_uint(rx) - (u64)__float_as_uint(rf);
         acc.nz += (u32)(fb == 0u) - (u32)(fb_fast == 0u);
-        reg_hist_add(lh16, hwin, ghist, lhlo, wlo, (int)fb_fast, lane, -1);
-        reg_hist_add(lh16, hwin, ghist, lhlo, wlo, (int)fb, lane, 1);
+        // lane window: drop the fast bin, count the exact one (out-of-window: post pass)
+        unsigned of = (unsigned)((int)fb_fast - lhlo), ox = (unsigned)((int)fb - lhlo);
+        if (of < LH_BINS) lh16[of * 32 + lane] -= 1;
+        else lh16[LH_BINS * 32 + lane] -= 1;
+        if (ox < LH_BINS) lh16[ox * 32 + lane] += 1;
+        else acc.outwin = 1;
     }
 }
 
@@ -225,11 +244,11 @@ __global__ void __launch_bounds__(384, 1) k_quant_reg(const __grid_constant__ Co
     double* abt2 = abt + A.rmax;
     double* ctab = abt2 + A.rmax;
     u16* lh16 = (u16*)(ctab + 64);
-    ws.bar = (u64*)(lh16 + LH_BINS * 32);
+    ws.bar = (u64*)(lh16 + (LH_BINS + 1) * 32);
     u32* hwin = (u32*)(smem + (size_t)nw * A.qr_slot);
     const int wlo = A.center - HWIN_REG / 2, lhlo = A.center - LH_BINS / 2;
     for (int t = threadIdx.x; t < HWIN_REG; t += blockDim.x) hwin[t] = 0;
-    for (int t = lane; t < LH_BINS * 16; t += 32) ((u32*)lh16)[t] = 0;
+    for (int t = lane; t < (LH_BINS + 1) * 16; t += 32) ((u32*)lh16)[t] = 0;
     ws.init(lane);
     __syncthreads();
 
@@ -243,14 +262,18 @@ __global__ void __launch_bounds__(384, 1) k_quant_reg(const __grid_constant__ Co
     };
     u32 lh_load = 0;   // max per-lane count added since the last flush
     long long b = next_reg((long long)blockIdx.x * nw + warp);
-    if (b < g.nb) ws.issue(A.x, g, S, &tmap, block_info(g, b), 0, lane);
+    BlockInfo Bnext = block_info(g, b);
+    if (b < g.nb) ws.issue(A.x, g, S, &tmap, Bnext, 0, lane);
     int buf = 0;
     while (b < g.nb) {
+        const BlockInfo B = Bnext;
         const long long bn = next_reg(b + NW);
-        if (bn < g.nb) ws.issue(A.x, g, S, &tmap, block_info(g, bn), buf ^ 1, lane);
+        if (bn < g.nb) {
+            Bnext = block_info(g, bn);
+            ws.issue(A.x, g, S, &tmap, Bnext, buf ^ 1, lane);
+        }
         ws.wait(S, buf, bn < g.nb);
         float* tile = (float*)(slot + buf * S.tile_bytes);
-        const BlockInfo B = block_info(g, b);
         const int bx = B.bx, by = B.by, bz = B.bz, vol = B.vol, rows = bx * by;
         TileWalk w0;
         w0.bx = bx; w0.by = by; w0.bz = bz; w0.stride = S.tz; w0.zoff = zshift(g, B); w0.bye = S.tye;
@@ -307,6 +330,8 @@ __global__ void __launch_bounds__(384, 1) k_quant_reg(const __grid_constant__ Co
                     else reg_fixup<false>(Q, K, cf, p0, pend, w0.zoff, S.tz, S.tye, lane, lh16, hwin, A.hist, lhlo, wlo, acc, mism);
                 }
             }
+            if (__any_sync(0xffffffffu, acc.outwin != 0) && acc.outwin)
+                reg_hist_outwin(bins16, p0, pend, hwin, A.hist, lhlo, wlo);
             if (!pin || pass == 1) break;
             // stage (c) verification of the re-read input against the stage (a) pair
             const u64 cs = warp_sum_u64(acc.cs), csi = warp_sum_u64(acc.csi);
