@@ -19,6 +19,7 @@
 #include "blocks.cu"
 #include "quant_block.cu"
 #include "prep_block.cu"
+#include "encode.cu"
 #include "decompress.cu"
 
 using namespace ftlz;
@@ -353,6 +354,8 @@ static int kernel_attrs_once() {
         setmax((const void*)k_quant_reg);
         setmax((const void*)k_quant_lor);
         setmax((const void*)k_codebook);
+        setmax((const void*)k_enc_len);
+        setmax((const void*)k_enc_pack);
         setmax((const void*)k_parse_tail);
         setmax((const void*)k_decode);
         setmax((const void*)k_recon_warp);
@@ -378,7 +381,7 @@ struct CompLayout {
     size_t result;       // DevStatus | minmax[4] | counters[16] | layout[16]  (zeroed)
     size_t zero_end;
     size_t hist, lbflag, events, fixed;
-    size_t coef, insum, inisum, ind, unpc, bsum, bisum, dcs, bitlen, regpre, unppre;
+    size_t coef, insum, inisum, ind, unpc, bsum, bisum, dcs, bitlen, lanepre, bitoff, regpre, unppre;
     size_t enc, qp, lbbits, lbreg, lbunp;
     size_t cb_keys, cb_syms, cb_w, cb_parent, cb_lens;
     size_t bins, unp, fix, faults, ffirst, ovr, plan, lor;
@@ -390,7 +393,7 @@ static const size_t RESULT_BYTES = 512;
 static CompLayout comp_layout(const HostPlan& P, int cap, int64_t n_faults) {
     const Geom& g = P.g;
     size_t nb = (size_t)g.nb, c = (size_t)cap;
-    size_t ntiles = (nb + ENC_BLOCKS - 1) / ENC_BLOCKS + 1;
+    size_t ntiles = (nb + SCAN_TILE - 1) / SCAN_TILE + 1;
     CompLayout L;
     size_t o = 0;
     auto take = [&](size_t n) { size_t r = o; o = al256(o + n); return r; };
@@ -409,6 +412,8 @@ static CompLayout comp_layout(const HostPlan& P, int cap, int64_t n_faults) {
     L.bisum = take(8 * nb);
     L.dcs = take(8 * nb);
     L.bitlen = take(4 * nb);
+    L.lanepre = take(4 * 32 * nb);
+    L.bitoff = take(8 * nb);
     L.regpre = take(4 * nb);
     L.unppre = take(8 * nb);
     L.enc = take(8 * c);
@@ -421,8 +426,7 @@ static CompLayout comp_layout(const HostPlan& P, int cap, int64_t n_faults) {
     L.cb_w = take(16 * c);
     L.cb_parent = take(8 * c);
     L.cb_lens = take(c);
-    size_t ngroups = (nb + 31) / 32;
-    L.bins = take(2 * ngroups * 32 * (size_t)g.nvmax8 + 64);
+    L.bins = take(2 * nb * (size_t)g.nvmax8 + 64);
     L.unp = take(4 * nb * (size_t)g.vmax);
     L.fix = take(n_faults ? 4 * nb * (size_t)g.vmax : 0);
     L.faults = take(sizeof(ftlz_fault) * (size_t)std::max<int64_t>(1, n_faults));
@@ -571,6 +575,7 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     A.ind = ws + L.ind; A.unpc = (u32*)(ws + L.unpc); A.bsum = (u64*)(ws + L.bsum); A.bisum = (u64*)(ws + L.bisum);
     A.dcs = (u64*)(ws + L.dcs); A.bitlen = (u32*)(ws + L.bitlen); A.regpre = (u32*)(ws + L.regpre);
     A.unppre = (u64*)(ws + L.unppre); A.events = ws + L.events;
+    A.lanepre = (u32*)(ws + L.lanepre); A.bitoff = (u64*)(ws + L.bitoff);
     A.st = (DevStatus*)(ws + L.result);
     A.minmax = (u32*)(ws + L.result + 64);
     A.counters = (u32*)(ws + L.result + 80);
@@ -609,11 +614,21 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     PF.mark("k_zero", s);
     k_zero<<<num_sms() * 4, 256, 0, s>>>(A);
     LCHK("k_zero");
-    unsigned ntiles = (unsigned)((g.nb + ENC_BLOCKS - 1) / ENC_BLOCKS);
-    PF.mark("k_encode", s);
-    k_encode<<<ntiles, ENC_BLOCKS, 0, s>>>(A, (u32*)(ws + L.fix), (const u8*)(ws + L.fixed), (u32*)(ws + L.lbflag), (u64*)(ws + L.lbbits),
-                                           (u64*)(ws + L.lbreg), (u64*)(ws + L.lbunp));
-    LCHK("k_encode");
+    {
+        const int ew = (int)std::max<size_t>(1, std::min<size_t>(16, (227 * 1024 - 8 * ENC_WIN) / (4 * (size_t)g.nvmax8)));
+        const size_t esm = 8 * ENC_WIN + (size_t)ew * 4 * (size_t)g.nvmax8;
+        PF.mark("k_enc_len", s);
+        k_enc_len<<<num_sms() * 2, 32 * ew, esm, s>>>(A, (const u32*)(ws + L.fix), (const u8*)(ws + L.fixed));
+        LCHK("k_enc_len");
+        unsigned ntiles = (unsigned)((g.nb + SCAN_TILE - 1) / SCAN_TILE);
+        PF.mark("k_enc_scan", s);
+        k_enc_scan<<<ntiles, SCAN_TILE, 0, s>>>(A, (u32*)(ws + L.lbflag), (u64*)(ws + L.lbbits), (u64*)(ws + L.lbreg),
+                                                (u64*)(ws + L.lbunp));
+        LCHK("k_enc_scan");
+        PF.mark("k_enc_pack", s);
+        k_enc_pack<<<num_sms() * 2, 32 * ew, esm, s>>>(A, (const u32*)(ws + L.fix), (const u8*)(ws + L.fixed));
+        LCHK("k_enc_pack");
+    }
     ftlz_header H;
     memset(&H, 0, sizeof H);
     H.nx = g.nx; H.ny = g.ny; H.nz = g.nz; H.block_edge = g.e; H.eb_mode = eb_mode ? 1 : 0;

@@ -128,7 +128,7 @@ FTLZ_DEV void emit_block(const CompArgs& A, long long b, int vol, const u16* bin
             bs += (u64)bin;
             bis += (u64)p * (u64)bin;
             // [group][chunk][lane][8]: chunk p/8 advances 256 elements per 8 points
-            A.bins[bidx0 + (size_t)(p >> 3) * 256 + (p & 7)] = (u16)bin;
+            A.bins[bidx0 + (size_t)p] = (u16)bin;
         }
         unsigned peers = __match_any_sync(0xffffffffu, bin);
         if (act && lane == __ffs(peers) - 1) hist_add(hwin, A.hist, wlo, bin, (u32)__popc(peers));

@@ -237,14 +237,9 @@ FTLZ_DEV void extent_of(const Geom& g, int xid, int* bx, int* by, int* bz) {
     *bz = (xid & 1) ? g.rz : g.e;
 }
 
-// bins layout shared by the quantizer (writer) and the encoder (reader):
-//   [group = b/32][chunk = p/8][lane = b%32][8 x u16]
-FTLZ_DEV size_t bins_index(const Geom& g, long long b, int p) {
-    long long grp = b >> 5;
-    int lane = (int)(b & 31);
-    return (((size_t)grp * (size_t)(g.nvmax8 >> 3) + (size_t)(p >> 3)) * 32u + (size_t)lane) * 8u +
-           (size_t)(p & 7);
-}
+// bins layout shared by the quantizer (writer) and the encoder (reader): block-contiguous,
+// nvmax8 u16 per block (16-byte aligned rows)
+FTLZ_DEV size_t bins_index(const Geom& g, long long b, int p) { return (size_t)b * (size_t)g.nvmax8 + (size_t)p; }
 
 struct BlockInfo {
     long long b, bi, bj, bk;

@@ -10,7 +10,7 @@
 //   k_fault_bins  bins-stage faults: verify/correct (protect_bins) and histogram fix-up
 //   k_codebook  canonical Huffman codebook from the global histogram (K3), archive layout
 //   k_zero      zero the payload words
-//   k_encode    verify bins, per-block bit lengths, decoupled look-back scan, MSB-first packing (K4)
+//   k_enc_*     (encode.cu) per-block bit lengths, block offsets, MSB-first packing (K4)
 //   k_assemble  header, block table, unpredictable words, sum_dc section (K5)
 #include <cstdio>
 
@@ -55,6 +55,8 @@ struct CompArgs {
     u64* bisum;
     u64* dcs;
     u32* bitlen;
+    u32* lanepre;        // nb x 32: bit offset of each lane's symbol range inside its block
+    u64* bitoff;         // nb: payload bit offset of each block
     u32* regpre;
     u64* unppre;
     u8* events;          // bit0 input corrected, bit1 bins corrected, bit2 input uncorrectable, bit3 bins uncorrectable
@@ -468,176 +470,6 @@ __global__ void k_fault_bins(CompArgs A, u32* fix_scratch, u8* fixed) {
         }
         fixed[b] = 1;
     }
-}
-
-// ==========================================================================================
-// K4: encode.  Lane = block; a CTA of ENC_WARPS warps covers 32*ENC_WARPS consecutive blocks.
-// Pass 1: verify/correct the bin array (stage d, pipeline.py:473-495) and sum code lengths.
-// Decoupled look-back over CTAs (tickets in launch order) gives global bit offsets and the
-// block-table / unpredictable-section prefixes.
-// Pass 2: MSB-first packing (encode.py:117-140) into 32-bit big-endian words of the archive.
-#define ENC_WARPS 4
-#define ENC_BLOCKS (ENC_WARPS * 32)
-
-FTLZ_DEV u32 bswap32(u32 v) { return __byte_perm(v, 0, 0x0123); }
-
-FTLZ_DEV void put_word(u32* words, u64 widx, u32 bits_be, bool partial) {
-    u32 v = bswap32(bits_be);
-    if (partial) atomicOr(words + widx, v);
-    else words[widx] = v;
-}
-
-// iterate the bin symbols of block b in order; 8 bins per 16-byte load.  Blocks touched by
-// bins-stage faults read their verified 32-bit words from fix_scratch (k_fault_bins).
-template <typename F>
-FTLZ_DEV void for_each_bin(const CompArgs& A, long long b, int vol, const u32* fixed, F fn) {
-    if (fixed) {
-        for (int p = 0; p < vol; p++) fn(p, fixed[p]);
-        return;
-    }
-    for (int p8 = 0; p8 < vol; p8 += 8) {
-        uint4 v = __ldg((const uint4*)(A.bins + bins_index(A.g, b, p8)));
-        u32 w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int t = 0; t < 8; t++) {
-            int p = p8 + t;
-            if (p < vol) fn(p, (w[t >> 1] >> ((t & 1) * 16)) & 0xffffu);
-        }
-    }
-}
-
-__global__ void __launch_bounds__(ENC_BLOCKS) k_encode(CompArgs A, u32* fix_scratch, const u8* fixed_flag, u32* lb_flag,
-                                                       u64* lb_bits, u64* lb_reg, u64* lb_unp) {
-    if (dev_failed(A.st)) return;
-    const Geom& g = A.g;
-    __shared__ u64 s_enc[4096];    // symbols in [center-2048, center+2048)
-    __shared__ u64 s_w[3][ENC_WARPS];
-    __shared__ u64 s_pre[3];
-    __shared__ unsigned s_tile;
-    int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    int wlo = A.center - 2048;
-    for (int t = tid; t < 4096; t += blockDim.x) {
-        int s = wlo + t;
-        s_enc[t] = (s >= 0 && s < A.cap) ? A.enc[s] : 0ull;
-    }
-    if (tid == 0) s_tile = atomicAdd(&A.counters[2], 1u);
-    __syncthreads();
-    unsigned tile = s_tile;
-    long long b = (long long)tile * ENC_BLOCKS + tid;
-    bool valid = b < g.nb;
-    int vol = 0, f0 = -1;
-    if (valid) {
-        BlockInfo B = block_info(g, b);
-        vol = B.vol;
-        if (A.n_faults) f0 = A.fault_first[b];
-    }
-    auto lookup = [&](u32 sym) -> u64 {
-        return (sym - (u32)wlo) < 4096u ? s_enc[sym - wlo] : (sym < (u32)A.cap ? A.enc[sym] : 0ull);
-    };
-    // pass 1: bit length (bins verification of faulted blocks already ran in k_fault_bins)
-    u64 bits = 0;
-    const u32* fixed = nullptr;
-    bool bad = false;
-    if (valid) {
-        if (f0 >= 0 && fixed_flag[b]) fixed = fix_scratch + (size_t)b * g.vmax;
-        if (A.events[b] & 8) bad = true;
-        if (!bad)
-            for_each_bin(A, b, vol, fixed, [&](int p, u32 sym) {
-                u32 l = (u32)(lookup(sym) & 63);
-                if (l == 0) {
-                    dev_fail(A.st, FTLZ_ERR_INVARIANT, FTLZ_K_BIN_RANGE, -1, b, 0, 0, 0);
-                    l = 1;
-                }
-                bits += l;
-            });
-    }
-    // CTA-wide inclusive scans of (bits, regression records, unpredictable words)
-    u64 v3[3] = {bits, valid ? (u64)A.ind[b] : 0ull, valid ? (u64)A.unpc[b] : 0ull};
-    u64 inc[3];
-#pragma unroll
-    for (int q = 0; q < 3; q++) {
-        inc[q] = v3[q];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            u64 t = __shfl_up_sync(0xffffffffu, inc[q], o);
-            if (lane >= o) inc[q] += t;
-        }
-        if (lane == 31) s_w[q][warp] = inc[q];
-    }
-    __syncthreads();
-    u64 woff[3] = {0, 0, 0}, tsum[3] = {0, 0, 0};
-#pragma unroll
-    for (int q = 0; q < 3; q++)
-        for (int w = 0; w < ENC_WARPS; w++) {
-            if (w < warp) woff[q] += s_w[q][w];
-            tsum[q] += s_w[q][w];
-        }
-    if (tid == 0) {
-        // flag: 0 = empty, 1 = aggregate published, 2 = inclusive prefix published
-        volatile u64* vb = lb_bits; volatile u64* vr = lb_reg; volatile u64* vu = lb_unp;
-        volatile u32* vf = lb_flag;
-        u64 pre[3] = {0, 0, 0};
-        if (tile > 0) {
-            vb[2 * tile] = tsum[0]; vr[2 * tile] = tsum[1]; vu[2 * tile] = tsum[2];
-            __threadfence();
-            vf[tile] = 1;
-            long long t = (long long)tile - 1;
-            while (t >= 0) {
-                u32 f = vf[t];
-                if (f == 0) continue;
-                __threadfence();
-                int sl = f == 2 ? 1 : 0;
-                pre[0] += vb[2 * t + sl]; pre[1] += vr[2 * t + sl]; pre[2] += vu[2 * t + sl];
-                if (f == 2) break;
-                t--;
-            }
-        }
-        vb[2 * tile + 1] = pre[0] + tsum[0]; vr[2 * tile + 1] = pre[1] + tsum[1]; vu[2 * tile + 1] = pre[2] + tsum[2];
-        __threadfence();
-        vf[tile] = 2;
-        s_pre[0] = pre[0]; s_pre[1] = pre[1]; s_pre[2] = pre[2];
-    }
-    __syncthreads();
-    if (!valid || bad) return;
-    u64 start = s_pre[0] + woff[0] + inc[0] - bits;   // bit offset of this block in the payload
-    A.bitlen[b] = (u32)bits;
-    A.regpre[b] = (u32)(s_pre[1] + woff[1] + inc[1] - v3[1]);
-    A.unppre[b] = s_pre[2] + woff[2] + inc[2] - v3[2];
-    if (dev_failed(A.st)) return;
-    // pass 2: pack
-    u64 gpos = A.layout[LAYOUT_PAY_OFF] * 8 + start;  // absolute bit in the archive
-    u32* words = (u32*)A.out;
-    u64 widx = gpos >> 5;
-    u64 acc = 0;                          // pending bits, left-aligned at bit 63
-    int nacc = (int)(gpos & 31);          // the first bits of the word belong to the previous block
-    bool first = true;
-    for_each_bin(A, b, vol, fixed, [&](int p, u32 sym) {
-        u64 e = lookup(sym);
-        int l = (int)(e & 63);
-        u64 code = e >> 6;
-        if (l > 32) {
-            int hl = l - 32;
-            acc |= (code >> 32) << (64 - nacc - hl);
-            nacc += hl;
-            if (nacc >= 32) {
-                put_word(words, widx++, (u32)(acc >> 32), first);
-                first = false;
-                acc <<= 32;
-                nacc -= 32;
-            }
-            code &= 0xffffffffull;
-            l = 32;
-        }
-        acc |= code << (64 - nacc - l);
-        nacc += l;
-        if (nacc >= 32) {
-            put_word(words, widx++, (u32)(acc >> 32), first);
-            first = false;
-            acc <<= 32;
-            nacc -= 32;
-        }
-    });
-    if (nacc > 0) put_word(words, widx, (u32)(acc >> 32), true);
 }
 
 // ==========================================================================================

@@ -1,0 +1,240 @@
+// encode.cu -- K4 of pipeline.compress: per-block bit lengths, block offsets, MSB-first packing
+// (encode.py:117-151 symbol_bit_lengths / encode_symbols; pipeline.py:498-509).
+//
+//   k_enc_len   warp per block: bins staged in shared memory (coalesced 16-byte loads), lane l
+//               owns the contiguous symbol range [l*c, l*c + c); per-lane bit counts, their
+//               exclusive warp scan (kept for k_enc_pack) and the block total
+//   k_enc_scan  decoupled look-back scan over blocks of (bits, regression records,
+//               unpredictable words) -> payload bit offset, record offset, unpredictable offset
+//   k_enc_pack  warp per block: each lane packs its range at its absolute bit offset into
+//               big-endian 32-bit words; words shared with a neighbouring lane or block are
+//               merged with atomicOr (the payload is zeroed by k_zero), the rest are stored
+//
+// Codes come from a 4096-symbol shared window around the quantizer centre (code << 6 | len),
+// global memory outside it.  Blocks touched by bins-stage faults read their verified 32-bit
+// words from fix_scratch (k_fault_bins).
+namespace ftlz {
+
+#define ENC_WIN 4096
+#define SCAN_TILE 1024
+
+struct EncWin {
+    const u64* s_enc;
+    const u64* g_enc;
+    int wlo, cap;
+    FTLZ_DEV u64 get(u32 sym) const {
+        const u32 o = sym - (u32)wlo;
+        return o < (u32)ENC_WIN ? s_enc[o] : (sym < (u32)cap ? __ldg(g_enc + sym) : 0ull);
+    }
+};
+
+FTLZ_DEV void enc_fill_window(const CompArgs& A, u64* s_enc) {
+    const int wlo = A.center - ENC_WIN / 2;
+    for (int t = threadIdx.x; t < ENC_WIN; t += blockDim.x) {
+        const int s = wlo + t;
+        s_enc[t] = (s >= 0 && s < A.cap) ? A.enc[s] : 0ull;
+    }
+}
+
+// stage block b's symbols in shared memory (u16 when read from the bins array, u32 words
+// from fix_scratch for bins-faulted blocks); returns true when `sym32` holds them
+FTLZ_DEV bool enc_stage(const CompArgs& A, long long b, int vol, const u32* fix, const u8* fixed_flag, u16* sym16,
+                        u32* sym32, int lane) {
+    const Geom& g = A.g;
+    const bool fixed = A.n_faults && A.fault_first[b] >= 0 && fixed_flag[b];
+    if (fixed) {
+        const u32* w = fix + (size_t)b * g.vmax;
+        for (int p = lane; p < vol; p += 32) sym32[p] = w[p];
+    } else {
+        const int nch = (vol + 7) >> 3;
+        const uint4* src = (const uint4*)(A.bins + bins_index(g, b, 0));
+        for (int c = lane; c < nch; c += 32) ((uint4*)sym16)[c] = __ldg(src + c);
+    }
+    __syncwarp();
+    return fixed;
+}
+
+__global__ void __launch_bounds__(512) k_enc_len(CompArgs A, const u32* fix, const u8* fixed_flag) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    if (dev_failed(A.st)) return;
+    const Geom& g = A.g;
+    u64* s_enc = (u64*)smem;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    u16* sym16 = (u16*)(smem + 8 * ENC_WIN + (size_t)warp * 4 * g.nvmax8);
+    u32* sym32 = (u32*)sym16;
+    enc_fill_window(A, s_enc);
+    __syncthreads();
+    const EncWin W = {s_enc, A.enc, A.center - ENC_WIN / 2, A.cap};
+    for (long long b = (long long)blockIdx.x * nw + warp; b < g.nb; b += (long long)gridDim.x * nw) {
+        const BlockInfo B = block_info(g, b);
+        const int vol = B.vol;
+        u32 bits = 0;
+        bool range_err = false;
+        if (!(A.events[b] & 8)) {
+            const bool fixed = enc_stage(A, b, vol, fix, fixed_flag, sym16, sym32, lane);
+            const int chunk = ((vol + 31) >> 5) | 1;
+            const int p0 = lane * chunk, pend = min(p0 + chunk, vol);
+            for (int p = p0; p < pend; p++) {
+                const u32 sym = fixed ? sym32[p] : (u32)sym16[p];
+                u32 l = (u32)(W.get(sym) & 63);
+                if (l == 0) {
+                    range_err = true;
+                    l = 1;
+                }
+                bits += l;
+            }
+            __syncwarp();
+        }
+        u32 pre = bits;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 v = __shfl_up_sync(0xffffffffu, pre, o);
+            if (lane >= o) pre += v;
+        }
+        A.lanepre[(size_t)b * 32 + lane] = pre - bits;
+        if (lane == 31) A.bitlen[b] = pre;
+        if (__any_sync(0xffffffffu, range_err) && lane == 0)
+            dev_fail(A.st, FTLZ_ERR_INVARIANT, FTLZ_K_BIN_RANGE, -1, b, 0, 0, 0);
+    }
+}
+
+// exclusive scans over blocks: payload bits (u64), regression records, unpredictable words
+__global__ void __launch_bounds__(SCAN_TILE) k_enc_scan(CompArgs A, u32* lb_flag, u64* lb_bits, u64* lb_reg, u64* lb_unp) {
+    if (dev_failed(A.st)) return;
+    const Geom& g = A.g;
+    __shared__ u64 s_w[3][SCAN_TILE / 32];
+    __shared__ u64 s_pre[3];
+    __shared__ unsigned s_tile;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+    if (tid == 0) s_tile = atomicAdd(&A.counters[2], 1u);
+    __syncthreads();
+    const unsigned tile = s_tile;
+    const long long b = (long long)tile * SCAN_TILE + tid;
+    const bool valid = b < g.nb;
+    u64 v3[3] = {valid ? (u64)A.bitlen[b] : 0ull, valid ? (u64)A.ind[b] : 0ull, valid ? (u64)A.unpc[b] : 0ull};
+    u64 inc[3];
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        inc[q] = v3[q];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u64 t = __shfl_up_sync(0xffffffffu, inc[q], o);
+            if (lane >= o) inc[q] += t;
+        }
+        if (lane == 31) s_w[q][warp] = inc[q];
+    }
+    __syncthreads();
+    u64 woff[3] = {0, 0, 0}, tsum[3] = {0, 0, 0};
+#pragma unroll
+    for (int q = 0; q < 3; q++)
+        for (int w = 0; w < nwarp; w++) {
+            if (w < warp) woff[q] += s_w[q][w];
+            tsum[q] += s_w[q][w];
+        }
+    if (tid == 0) {
+        // flag: 0 = empty, 1 = aggregate published, 2 = inclusive prefix published
+        volatile u64* vb = lb_bits;
+        volatile u64* vr = lb_reg;
+        volatile u64* vu = lb_unp;
+        volatile u32* vf = lb_flag;
+        u64 pre[3] = {0, 0, 0};
+        if (tile > 0) {
+            vb[2 * tile] = tsum[0];
+            vr[2 * tile] = tsum[1];
+            vu[2 * tile] = tsum[2];
+            __threadfence();
+            vf[tile] = 1;
+            long long t = (long long)tile - 1;
+            while (t >= 0) {
+                const u32 f = vf[t];
+                if (f == 0) continue;
+                __threadfence();
+                const int sl = f == 2 ? 1 : 0;
+                pre[0] += vb[2 * t + sl];
+                pre[1] += vr[2 * t + sl];
+                pre[2] += vu[2 * t + sl];
+                if (f == 2) break;
+                t--;
+            }
+        }
+        vb[2 * tile + 1] = pre[0] + tsum[0];
+        vr[2 * tile + 1] = pre[1] + tsum[1];
+        vu[2 * tile + 1] = pre[2] + tsum[2];
+        __threadfence();
+        vf[tile] = 2;
+        s_pre[0] = pre[0];
+        s_pre[1] = pre[1];
+        s_pre[2] = pre[2];
+    }
+    __syncthreads();
+    if (!valid) return;
+    A.bitoff[b] = s_pre[0] + woff[0] + inc[0] - v3[0];
+    A.regpre[b] = (u32)(s_pre[1] + woff[1] + inc[1] - v3[1]);
+    A.unppre[b] = s_pre[2] + woff[2] + inc[2] - v3[2];
+}
+
+// one big-endian word of the payload (u32 index into the archive): atomicOr when shared
+FTLZ_DEV void enc_put(u32* words, u64 widx, u32 bits_be, bool shared_word) {
+    const u32 v = __byte_perm(bits_be, 0, 0x0123);
+    if (shared_word) atomicOr(words + widx, v);
+    else words[widx] = v;
+}
+
+__global__ void __launch_bounds__(512) k_enc_pack(CompArgs A, const u32* fix, const u8* fixed_flag) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    if (dev_failed(A.st)) return;
+    const Geom& g = A.g;
+    u64* s_enc = (u64*)smem;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    u16* sym16 = (u16*)(smem + 8 * ENC_WIN + (size_t)warp * 4 * g.nvmax8);
+    u32* sym32 = (u32*)sym16;
+    enc_fill_window(A, s_enc);
+    __syncthreads();
+    const EncWin W = {s_enc, A.enc, A.center - ENC_WIN / 2, A.cap};
+    u32* words = (u32*)A.out;
+    const u64 pay0 = A.layout[LAYOUT_PAY_OFF] * 8;
+    for (long long b = (long long)blockIdx.x * nw + warp; b < g.nb; b += (long long)gridDim.x * nw) {
+        if (A.events[b] & 8) continue;
+        const BlockInfo B = block_info(g, b);
+        const int vol = B.vol;
+        const bool fixed = enc_stage(A, b, vol, fix, fixed_flag, sym16, sym32, lane);
+        const int chunk = ((vol + 31) >> 5) | 1;
+        const int p0 = lane * chunk, pend = min(p0 + chunk, vol);
+        const u64 gpos = pay0 + A.bitoff[b] + A.lanepre[(size_t)b * 32 + lane];
+        u64 widx = gpos >> 5;
+        u64 acc = 0;                          // pending bits, left-aligned at bit 63
+        int nacc = (int)(gpos & 31);          // leading bits of the first word belong to others
+        bool first = true;
+        for (int p = p0; p < pend; p++) {
+            const u32 sym = fixed ? sym32[p] : (u32)sym16[p];
+            const u64 e = W.get(sym);
+            int l = (int)(e & 63);
+            u64 code = e >> 6;
+            if (l > 32) {
+                const int hl = l - 32;
+                acc |= (code >> 32) << (64 - nacc - hl);
+                nacc += hl;
+                if (nacc >= 32) {
+                    enc_put(words, widx++, (u32)(acc >> 32), first);
+                    first = false;
+                    acc <<= 32;
+                    nacc -= 32;
+                }
+                code &= 0xffffffffull;
+                l = 32;
+            }
+            acc |= code << (64 - nacc - l);
+            nacc += l;
+            if (nacc >= 32) {
+                enc_put(words, widx++, (u32)(acc >> 32), first);
+                first = false;
+                acc <<= 32;
+                nacc -= 32;
+            }
+        }
+        if (nacc > 0 && p0 < pend) enc_put(words, widx, (u32)(acc >> 32), true);
+        __syncwarp();
+    }
+}
+
+}  // namespace ftlz
