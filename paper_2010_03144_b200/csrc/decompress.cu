@@ -445,16 +445,19 @@ struct BitReader {
     u64 end;
     u64 win;
     int have;
-    u64 nextw;
+    u64 nextw;   // index of the word held (raw, not yet byte-swapped) in `raw`
+    u32 raw;     // loaded one refill ahead so the load latency overlaps decoding
 };
 
-FTLZ_DEV u32 load_be(const u8* a, u64 wi, u64 end) {
+FTLZ_DEV u32 load_raw(const u8* a, u64 wi, u64 end) { return wi * 32 < end ? __ldg((const u32*)a + wi) : 0u; }
+FTLZ_DEV u32 raw_be(u32 raw, u64 wi, u64 end) {
     u64 bit0 = wi * 32;
     if (bit0 >= end) return 0;
-    u32 v = __byte_perm(__ldg((const u32*)a + wi), 0, 0x0123);
+    u32 v = __byte_perm(raw, 0, 0x0123);
     if (bit0 + 32 > end) v &= 0xffffffffu << (u32)(bit0 + 32 - end);
     return v;
 }
+FTLZ_DEV u32 load_be(const u8* a, u64 wi, u64 end) { return raw_be(load_raw(a, wi, end), wi, end); }
 
 FTLZ_DEV void br_init(BitReader& R, const u8* a, u64 pos, u64 end) {
     R.a = a;
@@ -463,20 +466,20 @@ FTLZ_DEV void br_init(BitReader& R, const u8* a, u64 pos, u64 end) {
     R.win = ((u64)load_be(a, wi, end) << 32) << (pos & 31);
     R.have = 32 - (int)(pos & 31);
     R.nextw = wi + 1;
-    while (R.have <= 32) {
-        R.win |= (u64)load_be(a, R.nextw, end) << (32 - R.have);
-        R.have += 32;
-        R.nextw++;
-    }
+    R.win |= (u64)load_be(a, R.nextw, end) << (32 - R.have);
+    R.have += 32;
+    R.nextw++;
+    R.raw = load_raw(a, R.nextw, end);
 }
 
 FTLZ_DEV void br_consume(BitReader& R, int l) {
     R.win <<= l;
     R.have -= l;
     if (R.have <= 32) {
-        R.win |= (u64)load_be(R.a, R.nextw, R.end) << (32 - R.have);
+        R.win |= (u64)raw_be(R.raw, R.nextw, R.end) << (32 - R.have);
         R.have += 32;
         R.nextw++;
+        R.raw = load_raw(R.a, R.nextw, R.end);
     }
 }
 
@@ -549,24 +552,34 @@ FTLZ_DEV void fail_block(const DecArgs& A, long long b, int kind, long long x, l
 #define DEC_WARPS 4
 #define MAXE 64
 
+FTLZ_DEV u32 lds_u32(u32 addr) {
+    u32 v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
 __global__ void __launch_bounds__(DEC_WARPS * 32) k_decode(DecArgs A, const u32* list, int nlist) {
     if (dev_failed(A.st)) return;
     extern __shared__ __align__(16) unsigned char dsm[];
     const Geom& g = A.g;
-    int T = (int)A.info[DI_T];
+    const int T = (int)A.info[DI_T];
     u32* s_lut = (u32*)dsm;
     float* stage_all = (float*)(dsm + ((size_t)4 << DEC_TBITS));
     __shared__ u64 s_first[64];
     __shared__ u32 s_count[64], s_base[64];
-    int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ long long s_rbase[DEC_WARPS][32];
+    __shared__ int s_rlen[DEC_WARPS][32], s_rbx[DEC_WARPS][32], s_rby[DEC_WARPS][32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int x = tid; x < (1 << T); x += blockDim.x) s_lut[x] = A.lut[x];
     if (tid < 64) { s_first[tid] = A.first_code[tid]; s_count[tid] = A.lcount[tid]; s_base[tid] = A.lbase[tid]; }
     __syncthreads();
-    DecTables D = {s_lut, T, (int)A.info[DI_MAXLEN], s_first, s_count, s_base, A.dsym};
+    const DecTables D = {s_lut, T, (int)A.info[DI_MAXLEN], s_first, s_count, s_base, A.dsym};
+    const u32 lut_sa = smem_u32(s_lut);
+    const int lsh = 64 - T;
     float* stage = stage_all + (size_t)warp * 32 * g.e;
     long long b;
     bool valid;
-    bool mode_list = list != nullptr;
+    const bool mode_list = list != nullptr;
     if (mode_list) {
         // re-execution: lane over the given block list, decode only (bins to scratch)
         long long idx = ((long long)blockIdx.x * DEC_WARPS + warp) * 32 + lane;
@@ -576,62 +589,98 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) k_decode(DecArgs A, const u32*
         b = ((long long)blockIdx.x * DEC_WARPS + warp) * 32 + lane;
         valid = b < g.nb;
     }
-    BlockInfo B = block_info(g, valid ? b : 0);
-    int kind = valid ? A.ind[b] : 0;
-    bool recon_here = valid && kind == 1 && !mode_list;
-    u64 pay_off = A.info[DI_PAY_OFF], pay_len = A.info[DI_PAY_LEN];
-    u64 bl = valid ? A.bitlen[b] : 0;
-    u64 rel = valid ? A.bofs[b] : 0;
+    const BlockInfo B = block_info(g, valid ? b : 0);
+    const int kind = valid ? A.ind[b] : 0;
+    const bool recon_here = valid && kind == 1 && !mode_list;
+    const u64 pay_off = A.info[DI_PAY_OFF], pay_len = A.info[DI_PAY_LEN];
+    const u32 bl = valid ? A.bitlen[b] : 0;
+    const u64 rel = valid ? A.bofs[b] : 0;
     int err = 0;
     long long ea = 0, eb2 = 0;
-    u64 last_byte = (rel + bl + 7) >> 3;
+    const u64 last_byte = (rel + bl + 7) >> 3;
     if (valid && last_byte > pay_len) err = FTLZ_K_D_PAST_END;
     BitReader R;
-    u64 start = pay_off * 8 + rel;
+    const u64 start = pay_off * 8 + rel;
     br_init(R, A.a, valid && !err ? start : 0, valid && !err ? (pay_off + last_byte) * 8 : 0);
-    u64 consumed = 0;
+    u32 consumed = 0;
     u32 zeros = 0;
-    u32 nunp = valid ? A.unpc[b] : 0;
-    u64 unp_base = A.info[DI_UNP_OFF] + 4 * (valid ? A.uofs[b] : 0);
-    float4 cf = recon_here ? load_coef(A.a, A.rec_off[b]) : make_float4(0, 0, 0, 0);
-    double c0 = (double)cf.x, c1 = (double)cf.y, c2 = (double)cf.z, c3 = (double)cf.w;
-    int f0 = (A.n_faults && valid) ? A.fault_first[b] : -1;
+    const u32 nunp = valid ? A.unpc[b] : 0;
+    const u64 unp_base = A.info[DI_UNP_OFF] + 4 * (valid ? A.uofs[b] : 0);
+    const float4 cf = recon_here ? load_coef(A.a, A.rec_off[b]) : make_float4(0, 0, 0, 0);
+    const double c0 = (double)cf.x, c1 = (double)cf.y, c2 = (double)cf.z, c3 = (double)cf.w;
+    const double twoeb = A.twoeb;
+    const int center = A.center;
+    const int f0 = (A.n_faults && valid) ? A.fault_first[b] : -1;
     u64 dsum = 0;
-    // run structure (lanes of one block-row with consecutive bk are contiguous in memory)
-    bool prev_same = false;
-    {
-        long long pbi = __shfl_up_sync(0xffffffffu, B.bi, 1), pbj = __shfl_up_sync(0xffffffffu, B.bj, 1);
-        long long pbk = __shfl_up_sync(0xffffffffu, B.bk, 1);
-        bool pv = __shfl_up_sync(0xffffffffu, valid, 1);
-        prev_same = lane > 0 && pv && valid && pbi == B.bi && pbj == B.bj && pbk + 1 == B.bk && !mode_list;
+    // runs: lanes of one block row with consecutive bk are contiguous in memory; each run is
+    // written back row by row with coalesced stores (structure computed once)
+    unsigned heads = 0;
+    const int e = g.e;
+    if (!mode_list) {
+        const long long pbi = __shfl_up_sync(0xffffffffu, B.bi, 1), pbj = __shfl_up_sync(0xffffffffu, B.bj, 1);
+        const long long pbk = __shfl_up_sync(0xffffffffu, B.bk, 1);
+        const bool pv = __shfl_up_sync(0xffffffffu, valid, 1);
+        const bool prev_same = lane > 0 && pv && valid && pbi == B.bi && pbj == B.bj && pbk + 1 == B.bk;
+        heads = __ballot_sync(0xffffffffu, valid && !prev_same);
+        const unsigned vm = __ballot_sync(0xffffffffu, valid);
+        // last lane of my run: the lane before the next head (or the last valid lane)
+        const unsigned later = heads & (lane == 31 ? 0u : (~0u << (lane + 1)));
+        const int hn = later ? __ffs(later) - 1 : 32;
+        const unsigned runm = vm & (hn == 32 ? ~0u : ((1u << hn) - 1u)) & ~((1u << lane) - 1u);
+        const int last = runm ? 31 - __clz(runm) : lane;
+        const int lbz = __shfl_sync(0xffffffffu, B.bz, last);
+        if ((heads >> lane) & 1u) {
+            s_rbase[warp][lane] = ((B.bi * e) * g.ny + B.bj * e) * g.nz + B.bk * e;
+            s_rlen[warp][lane] = (last - lane) * e + lbz;
+            s_rbx[warp][lane] = B.bx;
+            s_rby[warp][lane] = B.by;
+        }
+        __syncwarp();
     }
-    unsigned heads = __ballot_sync(0xffffffffu, valid && !prev_same);
-    int e = g.e;
+    const u32 st_sa = smem_u32(stage + lane * e);
+    int i = 0, j = 0;
     for (int r = 0; r < e * e; r++) {
-        int i = r / e, j = r - (r / e) * e;
-        bool act = valid && !err && i < B.bx && j < B.by;
+        const bool act = valid && !err && i < B.bx && j < B.by;
         if (act) {
             double ab = 0.0;
             if (recon_here) ab = __dadd_rn(__dadd_rn(c0, __dmul_rn(c1, int_to_f64(i))), __dmul_rn(c2, int_to_f64(j)));
-            int pbase = (i * B.by + j) * B.bz;
+            const int pbase = (i * B.by + j) * B.bz;
             for (int k = 0; k < B.bz; k++) {
                 if (consumed > bl) { err = FTLZ_K_D_RAN_PAST; break; }
+                u32 ent = lds_u32(lut_sa + 4u * (u32)(R.win >> lsh));
                 u32 sym;
-                int l = decode_sym(R, D, start + consumed, &sym);
-                if (l == 0) { err = FTLZ_K_D_OUTSIDE; break; }
-                consumed += (u64)l;
-                int p = pbase + k;
+                int l;
+                if (ent) {
+                    l = (int)(ent & 63);
+                    sym = ent >> 8;
+                    R.win <<= l;
+                    R.have -= l;
+                    // refill without a divergent branch: the next word was loaded one refill ago
+                    const bool need = R.have <= 32;
+                    const u32 v = raw_be(R.raw, R.nextw, R.end);
+                    R.win |= need ? ((u64)v << (32 - R.have)) : 0ull;
+                    R.have += need ? 32 : 0;
+                    if (need) {
+                        R.nextw++;
+                        R.raw = load_raw(R.a, R.nextw, R.end);
+                    }
+                } else {
+                    l = decode_sym(R, D, start + consumed, &sym);
+                    if (l == 0) { err = FTLZ_K_D_OUTSIDE; break; }
+                }
+                consumed += (u32)l;
+                const int p = pbase + k;
                 if (recon_here) {
                     float v;
                     if (sym) {
-                        double pred = __dadd_rn(ab, __dmul_rn(c3, int_to_f64(k)));
-                        v = __double2float_rn(__dadd_rn(pred, __dmul_rn(A.twoeb, int_to_f64((int)sym - A.center))));
+                        const double pred = __dadd_rn(ab, __dmul_rn(c3, int_to_f64(k)));
+                        v = __double2float_rn(__dadd_rn(pred, __dmul_rn(twoeb, int_to_f64((int)sym - center))));
                     } else {
                         v = zeros < nunp ? __uint_as_float((u32)ld_le(A.a + unp_base + 4ull * zeros, 4)) : 0.0f;
                     }
                     if (f0 >= 0) v = apply_decomp_faults(A, b, p, f0, v);
                     dsum += __float_as_uint(v);
-                    stage[lane * e + k] = v;
+                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(st_sa + 4u * (u32)k), "f"(v) : "memory");
                 } else {
                     A.bins[bins_index(g, b, p)] = (u16)sym;
                 }
@@ -640,27 +689,21 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) k_decode(DecArgs A, const u32*
         }
         if (!mode_list) {
             __syncwarp();
-            // coalesced write of this row for every run of lanes
             unsigned hm = heads;
             while (hm) {
-                int h = __ffs(hm) - 1;
+                const int h = __ffs(hm) - 1;
                 hm &= hm - 1;
-                int hn = hm ? __ffs(hm) - 1 : 32;   // next head (runs end at the next head)
-                long long hbi = __shfl_sync(0xffffffffu, B.bi, h), hbj = __shfl_sync(0xffffffffu, B.bj, h);
-                long long hbk = __shfl_sync(0xffffffffu, B.bk, h);
-                int hbx = __shfl_sync(0xffffffffu, B.bx, h), hby = __shfl_sync(0xffffffffu, B.by, h);
-                // run = lanes [h, last] where last = max valid lane < hn
-                unsigned vm = __ballot_sync(0xffffffffu, valid);
-                unsigned runm = vm & (hn == 32 ? ~0u : ((1u << hn) - 1u)) & ~((1u << h) - 1u);
-                int last = 31 - __clz(runm);
-                int lbz = __shfl_sync(0xffffffffu, B.bz, last);
-                if (i < hbx && j < hby) {
-                    int L = (last - h) * e + lbz;
-                    long long base = ((hbi * e + i) * g.ny + (hbj * e + j)) * g.nz + hbk * e;
+                if (i < s_rbx[warp][h] && j < s_rby[warp][h]) {
+                    const int L = s_rlen[warp][h];
+                    const long long base = s_rbase[warp][h] + ((long long)i * g.ny + j) * g.nz;
                     for (int o = lane; o < L; o += 32) A.out[base + o] = stage[h * e + o];
                 }
             }
             __syncwarp();
+        }
+        if (++j == e) {
+            j = 0;
+            i++;
         }
     }
     if (valid && !err && consumed != bl) { err = FTLZ_K_D_CONSUMED; ea = (long long)consumed; eb2 = (long long)bl; }
@@ -671,7 +714,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) k_decode(DecArgs A, const u32*
         return;
     }
     if (recon_here && A.info[DI_HAS_SDC]) {
-        u64 stored = ld_le(A.a + A.info[DI_SDC_OFF] + 8ull * (u64)b, 8);
+        const u64 stored = ld_le(A.a + A.info[DI_SDC_OFF] + 8ull * (u64)b, 8);
         if (stored != dsum) {
             A.mflag[b] = 1;
             A.mis_list[atomicAdd(&A.counters[DC_NMIS], 1u)] = (u32)b;
