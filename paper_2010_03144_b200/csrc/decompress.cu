@@ -437,57 +437,72 @@ __global__ void __launch_bounds__(PT_THREADS) k_parse_tail(DecArgs A) {
 }
 
 // ------------------------------------------------------------------------------------------
-// Huffman bit reader: MSB-first 64-bit window over big-endian 32-bit words of the archive;
-// bits at or beyond `end` read as zero (the reference pads the slice with zero bytes,
-// encode.py:214).
+// Huffman bit reader: MSB-first 64-bit window over the big-endian 32-bit words of one block's
+// bit slice; positions are relative to the word holding the block's first bit (32-bit
+// arithmetic).  Bits at or beyond `end` read as zero (the reference pads the slice with zero
+// bytes, encode.py:214).  The next word is loaded one refill ahead so its latency overlaps
+// decoding.
 struct BitReader {
-    const u8* a;
-    u64 end;
+    const u32* w;     // word 0: the word holding the block's first bit
+    u32 endw;         // words [0, endw) are fully inside the slice
+    u32 emask;        // valid-bit mask of word endw (0: none)
     u64 win;
     int have;
-    u64 nextw;   // index of the word held (raw, not yet byte-swapped) in `raw`
-    u32 raw;     // loaded one refill ahead so the load latency overlaps decoding
+    u32 nw;           // index of the word held in `raw`
+    u32 raw;          // raw (little-endian) word nw
 };
 
-FTLZ_DEV u32 load_raw(const u8* a, u64 wi, u64 end) { return wi * 32 < end ? __ldg((const u32*)a + wi) : 0u; }
-FTLZ_DEV u32 raw_be(u32 raw, u64 wi, u64 end) {
-    u64 bit0 = wi * 32;
-    if (bit0 >= end) return 0;
-    u32 v = __byte_perm(raw, 0, 0x0123);
-    if (bit0 + 32 > end) v &= 0xffffffffu << (u32)(bit0 + 32 - end);
-    return v;
+FTLZ_DEV u32 br_word(const BitReader& R, u32 n, u32 raw) {
+    const u32 v = __byte_perm(raw, 0, 0x0123);
+    return n < R.endw ? v : (n == R.endw ? (v & R.emask) : 0u);
 }
-FTLZ_DEV u32 load_be(const u8* a, u64 wi, u64 end) { return raw_be(load_raw(a, wi, end), wi, end); }
+FTLZ_DEV u32 br_load(const BitReader& R, u32 n) { return n <= R.endw && (n < R.endw || R.emask) ? __ldg(R.w + n) : 0u; }
 
-FTLZ_DEV void br_init(BitReader& R, const u8* a, u64 pos, u64 end) {
-    R.a = a;
-    R.end = end;
-    u64 wi = pos >> 5;
-    R.win = ((u64)load_be(a, wi, end) << 32) << (pos & 31);
-    R.have = 32 - (int)(pos & 31);
-    R.nextw = wi + 1;
-    R.win |= (u64)load_be(a, R.nextw, end) << (32 - R.have);
-    R.have += 32;
-    R.nextw++;
-    R.raw = load_raw(a, R.nextw, end);
+// position the window at relative bit `pos`
+FTLZ_DEV void br_seek(BitReader& R, u32 pos) {
+    const u32 n = pos >> 5;
+    R.win = ((u64)br_word(R, n, br_load(R, n)) << 32 | (u64)br_word(R, n + 1, br_load(R, n + 1))) << (pos & 31);
+    R.have = 64 - (int)(pos & 31);
+    R.nw = n + 2;
+    if (R.have <= 32) {
+        R.win |= (u64)br_word(R, R.nw, br_load(R, R.nw)) << (32 - R.have);
+        R.have += 32;
+        R.nw++;
+    }
+    R.raw = br_load(R, R.nw);
+}
+
+// slice [start, end) in absolute archive bits; returns the relative position of `start`
+FTLZ_DEV u32 br_init(BitReader& R, const u8* a, u64 start, u64 end) {
+    const u64 w0 = start >> 5;
+    R.w = (const u32*)a + w0;
+    const u64 rend = end > w0 * 32 ? end - w0 * 32 : 0;
+    R.endw = (u32)(rend >> 5);
+    R.emask = (rend & 31) ? (0xffffffffu << (32 - (u32)(rend & 31))) : 0u;
+    const u32 pos = (u32)(start & 31);
+    br_seek(R, pos);
+    return pos;
 }
 
 FTLZ_DEV void br_consume(BitReader& R, int l) {
     R.win <<= l;
     R.have -= l;
-    if (R.have <= 32) {
-        R.win |= (u64)raw_be(R.raw, R.nextw, R.end) << (32 - R.have);
-        R.have += 32;
-        R.nextw++;
-        R.raw = load_raw(R.a, R.nextw, R.end);
+    const bool need = R.have <= 32;
+    const u32 v = br_word(R, R.nw, R.raw);
+    R.win |= need ? ((u64)v << (32 - R.have)) : 0ull;
+    R.have += need ? 32 : 0;
+    if (need) {
+        R.nw++;
+        R.raw = br_load(R, R.nw);
     }
 }
 
-FTLZ_DEV u64 peek64(const u8* a, u64 pos, u64 end) {
-    u64 wi = pos >> 5;
-    u64 hi = ((u64)load_be(a, wi, end) << 32) | load_be(a, wi + 1, end);
-    u32 w2 = load_be(a, wi + 2, end);
-    int sh = (int)(pos & 31);
+// 64 bits at relative position pos (slow path)
+FTLZ_DEV u64 br_peek64(const BitReader& R, u32 pos) {
+    const u32 n = pos >> 5;
+    const u64 hi = ((u64)br_word(R, n, br_load(R, n)) << 32) | br_word(R, n + 1, br_load(R, n + 1));
+    const u32 w2 = br_word(R, n + 2, br_load(R, n + 2));
+    const int sh = (int)(pos & 31);
     return sh ? ((hi << sh) | ((u64)w2 >> (32 - sh))) : hi;
 }
 
@@ -500,8 +515,9 @@ struct DecTables {
     const u32* dsym;
 };
 
-// decode one symbol at absolute bit position `cur`; returns length (0 = outside code space)
-FTLZ_DEV int decode_sym(BitReader& R, const DecTables& D, u64 cur, u32* sym) {
+// decode one symbol whose code starts at relative bit `cur` (the window is positioned there);
+// returns its length (0 = outside the code space)
+FTLZ_DEV int decode_sym(BitReader& R, const DecTables& D, u32 cur, u32* sym) {
     u32 e = D.lut[R.win >> (64 - D.T)];
     if (e) {
         int l = (int)(e & 63);
@@ -509,13 +525,13 @@ FTLZ_DEV int decode_sym(BitReader& R, const DecTables& D, u64 cur, u32* sym) {
         br_consume(R, l);
         return l;
     }
-    u64 bits = peek64(R.a, cur, R.end);
+    u64 bits = br_peek64(R, cur);
     for (int l = D.T + 1; l <= D.maxlen; l++) {
         u64 code = bits >> (64 - l);
         u64 d = code - D.first[l];
         if (d < (u64)D.count[l]) {
             *sym = D.dsym[D.base[l] + d];
-            br_init(R, R.a, cur + l, R.end);
+            br_seek(R, cur + l);
             return l;
         }
     }
@@ -558,7 +574,7 @@ FTLZ_DEV u32 lds_u32(u32 addr) {
     return v;
 }
 
-__global__ void __launch_bounds__(DEC_WARPS * 32) k_decode(DecArgs A, const u32* list, int nlist) {
+__global__ void __launch_bounds__(DEC_WARPS * 32, 6) k_decode(DecArgs A, const u32* list, int nlist) {
     if (dev_failed(A.st)) return;
     extern __shared__ __align__(16) unsigned char dsm[];
     const Geom& g = A.g;
@@ -574,7 +590,8 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) k_decode(DecArgs A, const u32*
     if (tid < 64) { s_first[tid] = A.first_code[tid]; s_count[tid] = A.lcount[tid]; s_base[tid] = A.lbase[tid]; }
     __syncthreads();
     const DecTables D = {s_lut, T, (int)A.info[DI_MAXLEN], s_first, s_count, s_base, A.dsym};
-    const u32 lut_sa = smem_u32(s_lut);
+    u32 lut_sa;
+    asm volatile("mov.u32 %0, %1;" : "=r"(lut_sa) : "r"(smem_u32(s_lut)));   // keep in a register
     const int lsh = 64 - T;
     float* stage = stage_all + (size_t)warp * 32 * g.e;
     long long b;
@@ -601,7 +618,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) k_decode(DecArgs A, const u32*
     if (valid && last_byte > pay_len) err = FTLZ_K_D_PAST_END;
     BitReader R;
     const u64 start = pay_off * 8 + rel;
-    br_init(R, A.a, valid && !err ? start : 0, valid && !err ? (pay_off + last_byte) * 8 : 0);
+    const u32 pos0 = br_init(R, A.a, valid && !err ? start : 0, valid && !err ? (pay_off + last_byte) * 8 : 0);
     u32 consumed = 0;
     u32 zeros = 0;
     const u32 nunp = valid ? A.unpc[b] : 0;
@@ -653,19 +670,9 @@ __global__ void __launch_bounds__(DEC_WARPS * 32) k_decode(DecArgs A, const u32*
                 if (ent) {
                     l = (int)(ent & 63);
                     sym = ent >> 8;
-                    R.win <<= l;
-                    R.have -= l;
-                    // refill without a divergent branch: the next word was loaded one refill ago
-                    const bool need = R.have <= 32;
-                    const u32 v = raw_be(R.raw, R.nextw, R.end);
-                    R.win |= need ? ((u64)v << (32 - R.have)) : 0ull;
-                    R.have += need ? 32 : 0;
-                    if (need) {
-                        R.nextw++;
-                        R.raw = load_raw(R.a, R.nextw, R.end);
-                    }
+                    br_consume(R, l);
                 } else {
-                    l = decode_sym(R, D, start + consumed, &sym);
+                    l = decode_sym(R, D, pos0 + consumed, &sym);
                     if (l == 0) { err = FTLZ_K_D_OUTSIDE; break; }
                 }
                 consumed += (u32)l;
