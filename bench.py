@@ -210,9 +210,14 @@ def run_ours(args, world, rank, local):
     cfg_off = F.FtConfig.unprotected()
     mcode = {"absolute": 0, "value_range_relative": 1}[mode]
 
+    rb_cache = {}
+
     def rep_new(cap):
-        rb = F.pipeline._ReportBuf(cap)
-        return rb
+        # report buffers are allocated once and reused (a caller in a loop does the same); the
+        # library resets them on every call
+        if cap not in rb_cache:
+            rb_cache[cap] = F.pipeline._ReportBuf(cap)
+        return rb_cache[cap]
 
     nb = F.partition(x.shape, 10).n_blocks
     fa0, _ = F.pipeline._faults_c([])

@@ -1093,6 +1093,7 @@ extern "C" void* ftlz_ctx_stream(ftlz_ctx* c) { return c ? (void*)c->stream : nu
 static int ctx_compress(ftlz_ctx* c, const float* d_in, int64_t nx, int64_t ny, int64_t nz, int32_t eb_mode,
                         double eb_value, const ftlz_config* cfg, const ftlz_fault* faults, int64_t nf,
                         const int8_t* ovr, ftlz_report* rep) {
+    c->prof.mark("c_host_prelude", c->stream);
     int rc = ctx_plan(c, nx, ny, nz, cfg->block_edge);
     if (rc) {
         report_reset(rep);
@@ -1185,6 +1186,7 @@ static int ctx_upload_archive(ftlz_ctx* c, const uint8_t* h, size_t len, ftlz_he
 
 static int ctx_decompress(ftlz_ctx* c, const uint8_t* d_a, size_t len, const ftlz_header* hdr, float* d_out,
                           const ftlz_fault* faults, int64_t nf, ftlz_report* rep, ftlz_stream_info* si, bool decode) {
+    c->prof.mark("d_host_prelude", c->stream);
     int rc = ctx_plan(c, hdr->nx, hdr->ny, hdr->nz, hdr->block_edge);
     if (rc) return rc;
     DecLayout L = dec_layout(c->hp, len, (int)std::min<uint32_t>(hdr->bin_capacity, 65536u), nf);

@@ -574,7 +574,7 @@ FTLZ_DEV u32 lds_u32(u32 addr) {
     return v;
 }
 
-__global__ void __launch_bounds__(DEC_WARPS * 32, 6) k_decode(DecArgs A, const u32* list, int nlist) {
+__global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u32* list, int nlist) {
     if (dev_failed(A.st)) return;
     extern __shared__ __align__(16) unsigned char dsm[];
     const Geom& g = A.g;

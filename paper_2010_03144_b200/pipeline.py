@@ -11,6 +11,7 @@ faults.py:157-189 ("input", "bins", "decomp", "regression", "sampling").
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from dataclasses import dataclass, field
 from typing import Optional
 
@@ -105,6 +106,20 @@ def _faults_c(faults):
     return arr, len(faults)
 
 
+_tls = threading.local()
+
+
+def _report_buf(capacity: int) -> "_ReportBuf":
+    """Per-thread report buffers, reused across calls (results are copied out by lists())."""
+    cache = getattr(_tls, "reports", None)
+    if cache is None:
+        cache = _tls.reports = {}
+    rb = cache.get(capacity)
+    if rb is None:
+        rb = cache[capacity] = _ReportBuf(capacity)
+    return rb
+
+
 class _ReportBuf:
     def __init__(self, capacity: int):
         self.bufs = [np.zeros(max(1, capacity), np.int64) for _ in range(4)]
@@ -159,7 +174,7 @@ def _compress_array(values, eb_spec, cfg, predictor_override, faults, grid, out=
         ov = np.full(nb, -1, np.int8)
         for b, k in predictor_override.items():
             ov[int(b)] = int(k)
-    rep = _ReportBuf(nb)
+    rep = _report_buf(nb)
     st = L.ftlz_ctx_compress_host(ctx, x.ctypes.data, nx, ny, nz, EB_MODE_CODES[eb_spec.mode],
                                   float(eb_spec.value), C.byref(cfg._c()), fa, nf,
                                   ov.ctypes.data if ov is not None else None, C.byref(rep.r))
@@ -213,7 +228,7 @@ def _decompress_bytes(data, faults=None, out=None, reuse=None):
     if out is None:
         out = np.empty((hdr.nx, hdr.ny, hdr.nz), np.float32)
     fa, nf = _faults_c(faults)
-    rb = _ReportBuf(int(hdr.block_count))
+    rb = _report_buf(int(hdr.block_count))
     st = L.ftlz_ctx_decompress_host(ctx, buf, len(data), out.ctypes.data, fa, nf,
                                     1 if reuse is not None and reuse is _lib.last_parse[0] else 0,
                                     C.byref(rb.r))
