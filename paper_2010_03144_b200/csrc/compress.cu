@@ -236,66 +236,114 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
     __shared__ u64 s_total;
     int cap = A.cap;
     int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // bins verification failures (stage d) happen in k_encode; histogram of clean bins here.
-    // 1) compact alphabet in symbol order: {0} U {s : hist[s] > 0}
-    int per = (cap + CB_THREADS - 1) / CB_THREADS;
-    int s0 = tid * per, s1 = min(cap, s0 + per);
-    int cnt = 0;
-    for (int s = s0; s < s1; s++) cnt += (A.hist[s] > 0 || s == 0);
-    int inc = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int t = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += t;
-    }
-    if (lane == 31) wcount[warp] = inc;
-    __syncthreads();
-    if (warp == 0) {
-        int v = wcount[lane];
+    // 1) alphabet {0} U {s : hist[s] > 0} in symbol order: a bitmap built from warp ballots
+    //    over coalesced histogram reads, then word-popcount prefixes give every symbol its rank
+    // (bitmap and prefixes live in the parent region, which is free before the merge and
+    //  after the depth walk; they are rebuilt for the codebook section)
+    u32* s_bm = (u32*)(cb_dyn + 3 * CB_SMEM_KEYS);
+    u32* s_wpre = s_bm + 2048;
+    const int nwords = (cap + 31) >> 5;
+    auto build_ranks = [&]() {
+#pragma unroll 4
+        for (int s0 = warp * 32; s0 < nwords * 32; s0 += CB_THREADS) {
+            const int sy = s0 + lane;
+            const bool nz = sy < cap && (sy == 0 || A.hist[sy] > 0);
+            const u32 m = __ballot_sync(0xffffffffu, nz);
+            if (lane == 0) s_bm[s0 >> 5] = m;
+        }
+        __syncthreads();
+        const u32 c0 = 2 * tid < nwords ? __popc(s_bm[2 * tid]) : 0u;
+        const u32 c1 = 2 * tid + 1 < nwords ? __popc(s_bm[2 * tid + 1]) : 0u;
+        u32 inc = c0 + c1;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            int t = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o) v += t;
+            const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
         }
-        wcount[lane] = v;
-        if (lane == 31) s_n = v;
-    }
-    __syncthreads();
+        if (lane == 31) wcount[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {
+            u32 v = wcount[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 t = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += t;
+            }
+            wcount[lane] = v;
+            if (lane == 31) s_n = (int)v;
+        }
+        __syncthreads();
+        const u32 ex = (warp ? wcount[warp - 1] : 0u) + inc - (c0 + c1);
+        if (2 * tid < nwords) s_wpre[2 * tid] = ex;
+        if (2 * tid + 1 < nwords) s_wpre[2 * tid + 1] = ex + c0;
+        __syncthreads();
+    };
+    build_ranks();
     int n = s_n;
-    int pos = (warp ? wcount[warp - 1] : 0) + inc - cnt;
     int np2 = 1;
     while (np2 < n) np2 <<= 1;
     u64* keys = np2 <= CB_SMEM_KEYS ? skeys : S.keys;
-    for (int s = s0; s < s1; s++) {
-        u32 h = A.hist[s];
-        if (h > 0 || s == 0) keys[pos++] = ((u64)h << 16) | (u64)s;   // (weight, symbol)
+    for (int w = tid; w < nwords; w += CB_THREADS) {
+        u32 m = s_bm[w];
+        u32 pos = s_wpre[w];
+        while (m) {
+            const int bit = __ffs(m) - 1;
+            m &= m - 1;
+            const int sy = w * 32 + bit;
+            keys[pos++] = ((u64)A.hist[sy] << 16) | (u64)sy;   // (weight, symbol)
+        }
     }
     for (int i = n + tid; i < np2; i += CB_THREADS) keys[i] = ~0ull;
     __syncthreads();
     bitonic_sort_u64(keys, np2);
-    // 2) two-queue merge (sequential, one thread); node ids: leaves 0..n-1 in sorted order,
-    //    merged nodes n..2n-2
+    // 2) two-queue merge (sequential, one thread; the reference heap with its (weight, tie)
+    //    order, encode.py:26-71): node ids: leaves 0..n-1 in sorted order, merged n..2n-2.
+    //    Queue heads are kept in registers; weights and parents live in shared memory when the
+    //    alphabet fits (u16 parents), else in global scratch.
+    const bool small = np2 <= CB_SMEM_KEYS;
+    u16* par16 = (u16*)(cb_dyn + 3 * CB_SMEM_KEYS);
     if (tid == 0) {
         s_maxlen = 0;
         if (n == 1) {
-            S.parent[0] = 0xffffffffu;
+            if (small) par16[0] = 0xffffu;
+            else S.parent[0] = 0xffffffffu;
         } else {
-            u64* W = np2 <= CB_SMEM_KEYS ? cb_dyn + CB_SMEM_KEYS : S.w;
+            u64* W = small ? cb_dyn + CB_SMEM_KEYS : S.w;
             for (int i = 0; i < n; i++) W[i] = keys[i] >> 16;
             int li = 0, mi = n, mk = n;  // next leaf, next merged to consume, next merged to create
+            u64 wl = W[0], wm = 0;
             for (int t = 0; t < n - 1; t++) {
-                int pick[2];
+                int pk[2];
+                u64 pw[2];
 #pragma unroll
                 for (int r = 0; r < 2; r++) {
-                    if (li < n && (mi >= mk || W[li] <= W[mi])) pick[r] = li++;
-                    else pick[r] = mi++;
+                    // leaf wins ties (heap order of the reference)
+                    if (li < n && (mi >= mk || wl <= wm)) {
+                        pk[r] = li;
+                        pw[r] = wl;
+                        li++;
+                        wl = li < n ? W[li] : 0;
+                    } else {
+                        pk[r] = mi;
+                        pw[r] = wm;
+                        mi++;
+                        wm = mi < mk ? W[mi] : 0;
+                    }
                 }
-                W[mk] = W[pick[0]] + W[pick[1]];
-                S.parent[pick[0]] = (u32)mk;
-                S.parent[pick[1]] = (u32)mk;
+                const u64 sum = pw[0] + pw[1];
+                W[mk] = sum;
+                if (mi == mk) wm = sum;   // the merged queue was empty: its head is the new node
+                if (small) {
+                    par16[pk[0]] = (u16)mk;
+                    par16[pk[1]] = (u16)mk;
+                } else {
+                    S.parent[pk[0]] = (u32)mk;
+                    S.parent[pk[1]] = (u32)mk;
+                }
                 mk++;
             }
-            S.parent[mk - 1] = 0xffffffffu;
+            if (small) par16[mk - 1] = 0xffffu;
+            else S.parent[mk - 1] = 0xffffffffu;
         }
     }
     __syncthreads();
@@ -307,7 +355,10 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
         if (n == 1) d = 1;
         else {
             u32 v = (u32)i;
-            while (v != (u32)root) { v = S.parent[v]; d++; }
+            if (small)
+                while (v != (u32)root) { v = par16[v]; d++; }
+            else
+                while (v != (u32)root) { v = S.parent[v]; d++; }
         }
         u32 sym = (u32)(keys[i] & 0xffff);
         S.lens[sym] = (u8)min(d, 255);
@@ -388,13 +439,20 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
     // 6) codebook section: u32 count, then (u32 symbol, u8 length) in ascending symbol order
     u8* o = A.out + book_off;
     if (tid < 4) o[tid] = (u8)(n >> (8 * tid));
-    // symbols in ascending order: re-derive rank by scanning the histogram chunk again
-    pos = (warp ? wcount[warp - 1] : 0) + inc - cnt;
-    for (int s = s0; s < s1; s++) {
-        if (A.hist[s] > 0 || s == 0) {
+    // symbols in ascending order: ranks from the bitmap prefixes (rebuilt: the region held
+    // the parent pointers)
+    __syncthreads();
+    build_ranks();
+    for (int w = tid; w < nwords; w += CB_THREADS) {
+        u32 m = s_bm[w];
+        u32 pos = s_wpre[w];
+        while (m) {
+            const int bit = __ffs(m) - 1;
+            m &= m - 1;
+            const u32 sy = (u32)(w * 32 + bit);
             u8* e = o + 4 + 5ull * (u64)pos;
-            e[0] = (u8)s; e[1] = (u8)(s >> 8); e[2] = (u8)(s >> 16); e[3] = (u8)(s >> 24);
-            e[4] = S.lens[s];
+            e[0] = (u8)sy; e[1] = (u8)(sy >> 8); e[2] = (u8)(sy >> 16); e[3] = (u8)(sy >> 24);
+            e[4] = S.lens[sy];
             pos++;
         }
     }
