@@ -12,6 +12,6 @@ print("C", {k: round(v["ms_per_step"], 3) for k, v in d["compress"]["kernels"].i
 print("D", {k: round(v["ms_per_step"], 3) for k, v in d["decompress"]["kernels"].items()})
 PY
 if [ -n "$1" ]; then
-  ncu --set full --clock-control none --import-source on -k regex:"$1" -s ${2:-3} -c 1 -o gpurun_out/prof_cycle python bench.py --steps 1 --warmup 3 --quick --no-c5 > gpurun_out/ncu_cycle.log 2>&1
+  ncu --set full --clock-control none --import-source on -k regex:"$1" -s ${2:-3} -c ${3:-1} -o gpurun_out/prof_cycle python bench.py --steps 1 --warmup 3 --quick --no-c5 > gpurun_out/ncu_cycle.log 2>&1
   tail -1 gpurun_out/ncu_cycle.log
 fi
