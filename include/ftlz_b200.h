@@ -43,7 +43,8 @@ enum ftlz_status {
     FTLZ_ERR_UNSUPPORTED_CODEC = 6, /* UnsupportedCodec           */
     FTLZ_ERR_INVALID_ARGUMENT = 7,  /* InvalidArgument            */
     FTLZ_ERR_CUDA = 8,              /* CUDA runtime failure (no reference counterpart) */
-    FTLZ_ERR_CAPACITY = 9           /* caller buffer too small    */
+    FTLZ_ERR_CAPACITY = 9,          /* caller buffer too small    */
+    FTLZ_ERR_INVALID_REGION = 10    /* InvalidRegion              */
 };
 
 /* ---- detail kinds: select the reference message text ------------------------------------ */
@@ -237,6 +238,14 @@ int ftlz_ctx_parse_host(ftlz_ctx* ctx, const uint8_t* h_archive, size_t len,
 int ftlz_ctx_decompress_host(ftlz_ctx* ctx, const uint8_t* h_archive, size_t len, float* h_out,
                              const ftlz_fault* faults, int64_t n_faults, int32_t reuse_parsed,
                              ftlz_report* report);
+/* region extraction (pipeline.py:726-795): only the blocks intersecting the half-open box
+ * region = {x0, y0, z0, x1, y1, z1} are decoded, reconstructed and verified (one re-execution);
+ * h_out receives (x1-x0)*(y1-y0)*(z1-z0) float32 values, bit-identical to the same slice of a
+ * full decompression.  FTLZ_ERR_INVALID_REGION when the box is empty or outside the dims. */
+int ftlz_ctx_decompress_region_host(ftlz_ctx* ctx, const uint8_t* h_archive, size_t len, const int64_t* region,
+                                    float* h_out, int32_t reuse_parsed, ftlz_report* report);
+/* blocks a region extraction decodes (pipeline.py:798-810) */
+int64_t ftlz_intersecting_block_count(int64_t nx, int64_t ny, int64_t nz, int32_t block_edge, const int64_t* region);
 /* device archive -> device output */
 int ftlz_ctx_decompress_device(ftlz_ctx* ctx, const uint8_t* d_archive, size_t len,
                                const ftlz_header* hdr, float* d_out,

@@ -41,6 +41,8 @@ from .pipeline import (
     cr_decrease_bound,
     decompress,
     decompress_bytes,
+    decompress_region,
+    intersecting_block_count,
 )
 from .predict import PredictorKind, RegressionCoeffs
 from .quantize import QuantConfig
@@ -54,6 +56,7 @@ __all__ = [
     "InternalInvariantViolation", "InvalidArgument", "InvalidGeometry", "InvalidInjection",
     "InvalidRegion", "IoError", "PredictorKind", "QuantConfig", "RegressionCoeffs",
     "ShapeMismatch", "UncorrectableCorruption", "UnsupportedCodec", "compress",
-    "compress_bytes", "cr_decrease_bound", "decompress", "decompress_bytes", "parse",
+    "compress_bytes", "cr_decrease_bound", "decompress", "decompress_bytes", "decompress_region",
+    "intersecting_block_count", "parse",
     "partition", "resolve_error_bound", "serialize",
 ]

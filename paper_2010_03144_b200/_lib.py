@@ -76,7 +76,8 @@ EXPORTS = [
     "ftlz_ctx_destroy", "ftlz_ctx_stream", "ftlz_ctx_compress_device", "ftlz_ctx_compress_host",
     "ftlz_ctx_archive_device", "ftlz_ctx_archive_host", "ftlz_ctx_copy_archive",
     "ftlz_ctx_parse_host", "ftlz_ctx_decompress_host", "ftlz_ctx_decompress_device",
-    "ftlz_ctx_profile", "ftlz_ctx_profile_read",
+    "ftlz_ctx_profile", "ftlz_ctx_profile_read", "ftlz_ctx_decompress_region_host",
+    "ftlz_intersecting_block_count",
 ]
 
 _lib = None
@@ -129,6 +130,9 @@ def load():
         L.ftlz_ctx_parse_host.argtypes = [vp, vp, sz, C.POINTER(StreamInfo), PR]
         L.ftlz_ctx_decompress_host.argtypes = [vp, vp, sz, vp, PF, i64, i32, PR]
         L.ftlz_ctx_decompress_device.argtypes = [vp, vp, sz, PH, vp, PF, i64, PR]
+        L.ftlz_ctx_decompress_region_host.argtypes = [vp, vp, sz, vp, vp, i32, PR]
+        L.ftlz_intersecting_block_count.argtypes = [i64, i64, i64, i32, vp]
+        L.ftlz_intersecting_block_count.restype = i64
         L.ftlz_ctx_profile.argtypes = [vp, i32]
         L.ftlz_ctx_profile_read.argtypes = [vp, C.c_char_p, sz, C.POINTER(dbl), C.POINTER(i64), i32]
         _lib = L

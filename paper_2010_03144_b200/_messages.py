@@ -92,10 +92,15 @@ def raise_for_info(status: int, info, data: bytes = b"", eb_request=None, resolv
         raise E.InvalidArgument(_lib.last_error())
     if status == 9:
         raise E.InvalidArgument("capacity: " + _lib.last_error())
+    if status == 10:
+        raise E.InvalidRegion(_lib.last_error())
     raise E.DeviceError(_lib.last_error())
 
 
-def sdc_detail(info) -> str:
+def sdc_detail(info, region: bool = False) -> str:
+    """The reference's SDC detail text.  decompress (pipeline.py:673-677) prefixes decoder
+    failures with "block {b} undecodable: "; decompress_region (pipeline.py:788-793) reports
+    the decoder's own message."""
     k, b = info.kind, info.block
     why = {
         60: "bit slice extends past payload end",
@@ -107,4 +112,6 @@ def sdc_detail(info) -> str:
     }
     if k == 66:
         return f"block {b} mismatches after re-execution"
+    if region:
+        return why.get(k, str(k))
     return f"block {b} undecodable: {why.get(k, str(k))}"

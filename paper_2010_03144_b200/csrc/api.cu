@@ -728,7 +728,7 @@ struct DecLayout {
     size_t maps, smaps, sentry;
     size_t ind, recoff, unpc, bitlen, bofs, uofs, da, db, lor, mis;
     size_t lut, first, lcount, lbase, dsym, sortkeys, lba, lbb;
-    size_t bins, faults, ffirst, plan;
+    size_t bins, faults, ffirst, plan, rlist;
     size_t total;
     long long nchunks, nsuper;
 };
@@ -773,6 +773,7 @@ static DecLayout dec_layout(const HostPlan& P, size_t len, int cap, int64_t nf) 
     L.faults = take(sizeof(ftlz_fault) * (size_t)std::max<int64_t>(1, nf));
     L.ffirst = take(nf ? 4 * nb : 0);
     L.plan = take(P.bytes());
+    L.rlist = take(4 * nb);
     L.total = o;
     return L;
 }
@@ -807,6 +808,40 @@ static void stream_info_fill(const ftlz_header* h, const u64* info, ftlz_stream_
 }
 
 // parse (+ optionally decode) on the device; d_a must have >= 64 readable bytes past len
+static DecArgs make_dec_args(const HostPlan& P, const DevPlan& D, const DecLayout& L, const uint8_t* d_a, size_t len,
+                             const ftlz_header* h, float* d_out, int64_t nf, unsigned char* ws) {
+    const Geom& g = P.g;
+    int cap = (int)h->bin_capacity;
+    DecArgs A;
+    memset(&A, 0, sizeof A);
+    A.g = g;
+    A.a = d_a;
+    A.len = len;
+    A.cap = cap; A.center = cap / 2;
+    A.eb = h->eb_value; A.twoeb = 2.0 * h->eb_value;
+    A.codec = h->codec_id;
+    A.n_faults = (int)nf;
+    A.faults = (const ftlz_fault*)(ws + L.faults);
+    A.fault_first = (const int*)(ws + L.ffirst);
+    A.plans = D.ep; A.coords = D.coords; A.wave = D.wave; A.planes = D.planes;
+    A.maps = (u32*)(ws + L.maps); A.smaps = (u32*)(ws + L.smaps); A.sentry = (u64*)(ws + L.sentry);
+    A.nchunks = L.nchunks; A.nsuper = L.nsuper;
+    A.ind = ws + L.ind; A.rec_off = (u64*)(ws + L.recoff); A.unpc = (u32*)(ws + L.unpc);
+    A.bitlen = (u32*)(ws + L.bitlen); A.bofs = (u64*)(ws + L.bofs); A.uofs = (u64*)(ws + L.uofs);
+    A.dflag = ws + L.dflag; A.da = (long long*)(ws + L.da); A.db = (long long*)(ws + L.db);
+    A.mflag = ws + L.mflag; A.lor_list = (u32*)(ws + L.lor); A.mis_list = (u32*)(ws + L.mis);
+    A.st = (DevStatus*)(ws + L.result);
+    A.counters = (u32*)(ws + L.result + 64);
+    A.info = (u64*)(ws + L.result + 128);
+    A.lut = (u32*)(ws + L.lut); A.first_code = (u64*)(ws + L.first); A.lcount = (u32*)(ws + L.lcount);
+    A.lbase = (u32*)(ws + L.lbase); A.dsym = (u32*)(ws + L.dsym); A.sortkeys = (u64*)(ws + L.sortkeys);
+    A.bins = (u16*)(ws + L.bins);
+    A.out = d_out;
+    A.lb_flag = (u32*)(ws + L.lbflag); A.lb_a = (u64*)(ws + L.lba); A.lb_b = (u64*)(ws + L.lbb);
+
+    return A;
+}
+
 static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8_t* d_a, size_t len,
                            const ftlz_header* h, float* d_out, const ftlz_fault* faults, int64_t nf,
                            unsigned char* ws, size_t ws_size, ftlz_report* rep, ftlz_stream_info* si_out,
@@ -835,33 +870,7 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         CK(cudaMemcpyAsync(ws + L.faults, fs.data(), sizeof(ftlz_fault) * nf, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(ws + L.ffirst, ff.data(), 4 * (size_t)g.nb, cudaMemcpyHostToDevice, s));
     }
-    DecArgs A;
-    memset(&A, 0, sizeof A);
-    A.g = g;
-    A.a = d_a;
-    A.len = len;
-    A.cap = cap; A.center = cap / 2;
-    A.eb = h->eb_value; A.twoeb = 2.0 * h->eb_value;
-    A.codec = h->codec_id;
-    A.n_faults = (int)nf;
-    A.faults = (const ftlz_fault*)(ws + L.faults);
-    A.fault_first = (const int*)(ws + L.ffirst);
-    A.plans = D.ep; A.coords = D.coords; A.wave = D.wave; A.planes = D.planes;
-    A.maps = (u32*)(ws + L.maps); A.smaps = (u32*)(ws + L.smaps); A.sentry = (u64*)(ws + L.sentry);
-    A.nchunks = L.nchunks; A.nsuper = L.nsuper;
-    A.ind = ws + L.ind; A.rec_off = (u64*)(ws + L.recoff); A.unpc = (u32*)(ws + L.unpc);
-    A.bitlen = (u32*)(ws + L.bitlen); A.bofs = (u64*)(ws + L.bofs); A.uofs = (u64*)(ws + L.uofs);
-    A.dflag = ws + L.dflag; A.da = (long long*)(ws + L.da); A.db = (long long*)(ws + L.db);
-    A.mflag = ws + L.mflag; A.lor_list = (u32*)(ws + L.lor); A.mis_list = (u32*)(ws + L.mis);
-    A.st = (DevStatus*)(ws + L.result);
-    A.counters = (u32*)(ws + L.result + 64);
-    A.info = (u64*)(ws + L.result + 128);
-    A.lut = (u32*)(ws + L.lut); A.first_code = (u64*)(ws + L.first); A.lcount = (u32*)(ws + L.lcount);
-    A.lbase = (u32*)(ws + L.lbase); A.dsym = (u32*)(ws + L.dsym); A.sortkeys = (u64*)(ws + L.sortkeys);
-    A.bins = (u16*)(ws + L.bins);
-    A.out = d_out;
-    A.lb_flag = (u32*)(ws + L.lbflag); A.lb_a = (u64*)(ws + L.lba); A.lb_b = (u64*)(ws + L.lbb);
-
+    DecArgs A = make_dec_args(P, D, L, d_a, len, h, d_out, nf, ws);
     int sms = num_sms();
     PF.mark("k_parse_maps", s);
     k_parse_maps<<<sms * 8, 256, 0, s>>>(A);
@@ -964,6 +973,125 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     }
     put_list(rep->reexecuted, rep->capacity, &rep->n_reexecuted, reexec);
     return FTLZ_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// region extraction (pipeline.py:726-795), after a successful parse of the same archive in the
+// same workspace: decode + reconstruct only the intersecting blocks into the region buffer,
+// verify each with one re-execution, and report in the reference's processing order (extent
+// groups in sorted order, block ids ascending; the first failing group stops the walk).
+static int region_core(const HostPlan& P, const DevPlan& D, const uint8_t* d_a, size_t len, const ftlz_header* h,
+                       const int64_t* region, float* d_out, unsigned char* ws, ftlz_report* rep, cudaStream_t s) {
+    const Geom& g = P.g;
+    const int cap = (int)h->bin_capacity;
+    DecLayout L = dec_layout(P, len, cap, 0);
+    DecArgs A = make_dec_args(P, D, L, d_a, len, h, d_out, 0, ws);
+    const int64_t e = g.e;
+    std::vector<u32> ids;
+    for (int64_t bi = region[0] / e; bi < (region[3] + e - 1) / e; bi++)
+        for (int64_t bj = region[1] / e; bj < (region[4] + e - 1) / e; bj++)
+            for (int64_t bk = region[2] / e; bk < (region[5] + e - 1) / e; bk++)
+                ids.push_back((u32)((bi * g.cy + bj) * g.cz + bk));
+    std::sort(ids.begin(), ids.end());
+    const u32 n = (u32)ids.size();
+    CK(cudaMemcpyAsync(ws + L.rlist, ids.data(), 4 * (size_t)n, cudaMemcpyHostToDevice, s));
+    A.region = 1;
+    A.rx0 = region[0]; A.ry0 = region[1]; A.rz0 = region[2];
+    A.rnx = region[3] - region[0]; A.rny = region[4] - region[1]; A.rnz = region[5] - region[2];
+    A.region_list = (const u32*)(ws + L.rlist);
+    A.n_region = n;
+    const int sms = num_sms();
+    const size_t dec_smem = ((size_t)4 << DEC_TBITS) + (size_t)DEC_WARPS * 32 * g.e * 4;
+    const size_t rslot = al16((size_t)g.vmax * 8) + al16((size_t)g.vmax * 4);
+    const int rw = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / rslot));
+    k_decode<<<(n + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32), DEC_WARPS * 32, dec_smem, s>>>(A, A.region_list, (int)n);
+    LCHK("k_decode");
+    k_recon_warp<<<std::min<u32>((n + rw - 1) / rw, (u32)sms * 4), rw * 32, rslot * rw, s>>>(A, 2);
+    LCHK("k_recon_warp");
+    std::vector<unsigned char> df((size_t)g.nb), mf((size_t)g.nb);
+    CK(cudaMemcpyAsync(df.data(), ws + L.dflag, (size_t)g.nb, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(mf.data(), ws + L.mflag, (size_t)g.nb, cudaMemcpyDeviceToHost, s));
+    unsigned char hres[RESULT_BYTES];
+    CK(cudaMemcpyAsync(hres, ws + L.result, RESULT_BYTES, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    DevStatus st;
+    memcpy(&st, hres, sizeof st);
+    if (st.code) {
+        info_set(&rep->info, st.code, st.kind, st.offset, st.block, st.a, st.b);
+        return set_err(st.code, "device failure during region extraction");
+    }
+    u32 nmis = 0;
+    memcpy(&nmis, hres + 64 + 4 * DC_NMIS, 4);
+    if (nmis) {
+        // one re-execution of every mismatching block (no fault replay)
+        std::vector<u32> mis(nmis);
+        CK(cudaMemcpy(mis.data(), ws + L.mis, 4 * (size_t)nmis, cudaMemcpyDeviceToHost));
+        std::sort(mis.begin(), mis.end());
+        CK(cudaMemcpy(ws + L.mis, mis.data(), 4 * (size_t)nmis, cudaMemcpyHostToDevice));
+        A.region = 0;   // re-decode failures mark mflag = 3
+        k_decode<<<(nmis + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32), DEC_WARPS * 32, dec_smem, s>>>(
+            A, (const u32*)(ws + L.mis), (int)nmis);
+        LCHK("k_decode");
+        k_recon_warp<<<std::min<u32>((nmis + rw - 1) / rw, (u32)sms * 4), rw * 32, rslot * rw, s>>>(A, 3);
+        LCHK("k_recon_warp");
+        CK(cudaMemcpyAsync(mf.data(), ws + L.mflag, (size_t)g.nb, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    // verdict in processing order
+    std::vector<std::pair<std::tuple<int, int, int>, int64_t>> order;
+    for (u32 b : ids) order.push_back({block_extent(P, b), (int64_t)b});
+    std::sort(order.begin(), order.end());
+    std::vector<int64_t> reexec;
+    size_t gi = 0;
+    while (gi < order.size()) {
+        size_t gj = gi;
+        while (gj < order.size() && order[gj].first == order[gi].first) gj++;
+        // undecodable blocks are raised while the group's bins are decoded, before any check
+        for (size_t q = gi; q < gj; q++) {
+            const int64_t b = order[q].second;
+            if (df[b]) {
+                long long a2[2];
+                CK(cudaMemcpy(&a2[0], ws + L.da + 8 * b, 8, cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(&a2[1], ws + L.db + 8 * b, 8, cudaMemcpyDeviceToHost));
+                rep->sdc = 1;
+                info_set(&rep->info, FTLZ_OK, df[b], -1, b, a2[0], a2[1]);
+                put_list(rep->reexecuted, rep->capacity, &rep->n_reexecuted, reexec);
+                return FTLZ_OK;
+            }
+        }
+        for (size_t q = gi; q < gj; q++) {
+            const int64_t b = order[q].second;
+            if (mf[b] == 0) continue;
+            if (mf[b] == 2) {
+                reexec.push_back(b);
+                continue;
+            }
+            rep->sdc = 1;
+            info_set(&rep->info, FTLZ_OK, FTLZ_K_D_MISMATCH, -1, b, 0, 0);
+            std::sort(reexec.begin(), reexec.end());
+            put_list(rep->reexecuted, rep->capacity, &rep->n_reexecuted, reexec);
+            return FTLZ_OK;
+        }
+        gi = gj;
+    }
+    std::sort(reexec.begin(), reexec.end());
+    put_list(rep->reexecuted, rep->capacity, &rep->n_reexecuted, reexec);
+    return FTLZ_OK;
+}
+
+static int region_check(const ftlz_header* h, const int64_t* r) {
+    if (!(0 <= r[0] && r[0] < r[3] && r[3] <= h->nx && 0 <= r[1] && r[1] < r[4] && r[4] <= h->ny && 0 <= r[2] &&
+          r[2] < r[5] && r[5] <= h->nz))
+        return set_err(FTLZ_ERR_INVALID_REGION, "region outside dims");
+    return FTLZ_OK;
+}
+
+extern "C" int64_t ftlz_intersecting_block_count(int64_t nx, int64_t ny, int64_t nz, int32_t block_edge,
+                                                 const int64_t* r) {
+    (void)nx; (void)ny; (void)nz;
+    if (block_edge < 1) return -1;
+    const int64_t e = block_edge;
+    return ((r[3] + e - 1) / e - r[0] / e) * ((r[4] + e - 1) / e - r[1] / e) * ((r[5] + e - 1) / e - r[2] / e);
 }
 
 extern "C" int ftlz_parse(const uint8_t* d_archive, size_t len, const ftlz_header* hdr, void* d_workspace,
@@ -1223,6 +1351,35 @@ extern "C" int ftlz_ctx_decompress_host(ftlz_ctx* c, const uint8_t* h, size_t le
     size_t n = (size_t)hdr.nx * hdr.ny * hdr.nz;
     if ((rc = c->dout.ensure(4 * n))) return rc;
     rc = ctx_decompress(c, (const uint8_t*)c->arch.p, len, &hdr, (float*)c->dout.p, faults, nf, rep, nullptr, true);
+    if (rc) return rc;
+    if (!rep->sdc) {
+        CK(cudaMemcpyAsync(h_out, c->dout.p, 4 * n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+    }
+    return FTLZ_OK;
+}
+
+extern "C" int ftlz_ctx_decompress_region_host(ftlz_ctx* c, const uint8_t* h, size_t len, const int64_t* region,
+                                               float* h_out, int32_t reuse_parsed, ftlz_report* rep) {
+    std::lock_guard<std::mutex> g(c->mu);
+    cudaSetDevice(c->device);
+    report_reset(rep);
+    ftlz_header hdr;
+    int rc;
+    if (reuse_parsed && c->parsed_src == h && c->parsed_len == len) {
+        hdr = c->parsed_hdr;
+    } else {
+        rc = ctx_upload_archive(c, h, len, &hdr, rep);
+        if (rc) return rc;
+    }
+    if ((rc = region_check(&hdr, region))) return rc;
+    // parse (validation + tables) in the context workspace, then the region pass
+    rc = ctx_decompress(c, (const uint8_t*)c->arch.p, len, &hdr, nullptr, nullptr, 0, rep, nullptr, false);
+    if (rc) return rc;
+    const size_t n = (size_t)(region[3] - region[0]) * (region[4] - region[1]) * (region[5] - region[2]);
+    if ((rc = c->dout.ensure(4 * n))) return rc;
+    rc = region_core(c->hp, c->dp, (const uint8_t*)c->arch.p, len, &hdr, region, (float*)c->dout.p,
+                     (unsigned char*)c->dws.p, rep, c->stream);
     if (rc) return rc;
     if (!rep->sdc) {
         CK(cudaMemcpyAsync(h_out, c->dout.p, 4 * n, cudaMemcpyDeviceToHost, c->stream));

@@ -73,6 +73,13 @@ struct DecArgs {
     u32* lb_flag;
     u64* lb_a;
     u64* lb_b;
+    // region extraction (pipeline.py:726-795): output window in field coordinates
+    int region;               // 1: k_decode list mode reports failures like the full path
+    int pad_r;
+    long long rx0, ry0, rz0, rnx, rny, rnz;
+    const u32* region_list;   // the intersecting blocks, ascending
+    u32 n_region;
+    u32 pad_r2;
 };
 
 FTLZ_DEV u64 ld_le(const u8* p, int n) {
@@ -716,7 +723,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
     if (valid && !err && consumed != bl) { err = FTLZ_K_D_CONSUMED; ea = (long long)consumed; eb2 = (long long)bl; }
     if (valid && !err && zeros != nunp) { err = FTLZ_K_D_ZEROS; ea = zeros; eb2 = nunp; }
     if (valid && err) {
-        if (mode_list) A.mflag[b] = 3;
+        if (mode_list && !A.region) A.mflag[b] = 3;
         else fail_block(A, b, err, ea, eb2);
         return;
     }
@@ -742,12 +749,14 @@ __global__ void __launch_bounds__(128) k_recon_warp(DecArgs A, int mode) {
     size_t slot_bytes = (((size_t)g.vmax * 8 + 15) & ~(size_t)15) + (((size_t)g.vmax * 4 + 15) & ~(size_t)15);
     double* xd = (double*)(rsm + (size_t)warp * slot_bytes);
     float* v32 = (float*)(xd + g.vmax);
-    u32 n = mode ? A.counters[DC_NMIS] : A.counters[DC_NLOR];
-    const u32* list = mode ? A.mis_list : A.lor_list;
+    // mode 0: Lorenzo list; 1: re-execution list; 2: region list; 3: region re-execution
+    const bool rgn = mode >= 2, reexec = mode & 1;
+    u32 n = reexec ? A.counters[DC_NMIS] : (rgn ? A.n_region : A.counters[DC_NLOR]);
+    const u32* list = reexec ? A.mis_list : (rgn ? A.region_list : A.lor_list);
     for (long long idx = (long long)blockIdx.x * nw + warp; idx < (long long)n; idx += (long long)gridDim.x * nw) {
         long long b = list[idx];
         if (A.dflag[b]) continue;                       // undecodable: reported separately
-        if (mode && A.mflag[b] == 3) continue;          // re-decode failed
+        if (reexec && A.mflag[b] == 3) continue;        // re-decode failed
         BlockInfo B = block_info(g, b);
         int kind = A.ind[b];
         const ExtPlan& PL = A.plans[B.xid];
@@ -820,13 +829,20 @@ __global__ void __launch_bounds__(128) k_recon_warp(DecArgs A, int mode) {
             s += __float_as_uint(v);
             int i = p / byz, rem = p - (p / byz) * byz;
             int j = rem / bz, k = rem - (rem / bz) * bz;
-            A.out[base + ((long long)i * g.ny + j) * g.nz + k] = v;
+            if (rgn) {
+                // the block's intersection with the region window
+                const long long x = B.bi * g.e + i - A.rx0, y = B.bj * g.e + j - A.ry0, z = B.bk * g.e + k - A.rz0;
+                if (x >= 0 && x < A.rnx && y >= 0 && y < A.rny && z >= 0 && z < A.rnz)
+                    A.out[(x * A.rny + y) * A.rnz + z] = v;
+            } else {
+                A.out[base + ((long long)i * g.ny + j) * g.nz + k] = v;
+            }
         }
         s = warp_sum_u64(s);
         if (lane == 0) {
             bool has = A.info[DI_HAS_SDC] != 0;
             u64 stored = has ? ld_le(A.a + A.info[DI_SDC_OFF] + 8ull * (u64)b, 8) : 0;
-            if (mode) A.mflag[b] = (has && stored != s) ? 3 : 2;
+            if (reexec) A.mflag[b] = (has && stored != s) ? 3 : 2;
             else if (has && stored != s) {
                 A.mflag[b] = 1;
                 A.mis_list[atomicAdd(&A.counters[DC_NMIS], 1u)] = (u32)b;

@@ -249,6 +249,53 @@ def decompress_bytes(data: bytes, out=None, faults=None):
     return arr
 
 
+def decompress_region(stream: CompressedStream, region, threads: int = 1) -> tuple:
+    """Decode only the blocks intersecting the half-open box ((x0,y0,z0),(x1,y1,z1))
+    (pipeline.py:726-795) -> (Field or None, FtReport).  Values are bit-identical to the same
+    slice of a full decompression; each block is verified against its sum_dc with one
+    re-execution.  InvalidRegion when the box is empty or leaves the field."""
+    from .errors import InvalidRegion
+
+    (x0, y0, z0), (x1, y1, z1) = region
+    nx, ny, nz = stream.dims
+    if not (0 <= x0 < x1 <= nx and 0 <= y0 < y1 <= ny and 0 <= z0 < z1 <= nz):
+        raise InvalidRegion(f"region {region} outside dims {stream.dims}")
+    data = serialize(stream)
+    L = _lib.load()
+    ctx = _lib.context()
+    r6 = np.array([x0, y0, z0, x1, y1, z1], np.int64)
+    out = np.empty((x1 - x0, y1 - y0, z1 - z0), np.float32)
+    hdr = _lib.Header()
+    info = _lib.Info()
+    head = bytes(data[:64])
+    st = L.ftlz_peek_header(head, len(data), C.byref(hdr), C.byref(info))
+    if st != 0:
+        raise_for_info(st, info, data)
+    rb = _report_buf(int(hdr.block_count))
+    reuse = stream.__dict__.get("_parse_token")
+    st = L.ftlz_ctx_decompress_region_host(ctx, data, len(data), r6.ctypes.data, out.ctypes.data,
+                                           1 if reuse is not None and reuse is _lib.last_parse[0] else 0,
+                                           C.byref(rb.r))
+    if st != 0:
+        raise_for_info(st, rb.r.info, data)
+    _, _, _, rx = rb.lists()
+    sdc = bool(rb.r.sdc)
+    report = FtReport(decomp_block_reexecuted=rx, sdc_in_compression=sdc,
+                      detail=sdc_detail(rb.r.info, region=True) if sdc else "")
+    return (None if sdc else Field._wrap(out)), report
+
+
+def intersecting_block_count(stream_or_grid, region) -> int:
+    """Number of blocks a region extraction decodes (pipeline.py:798-810)."""
+    from .core import BlockGrid
+
+    grid = stream_or_grid if isinstance(stream_or_grid, BlockGrid) else partition(
+        stream_or_grid.dims, stream_or_grid.block_edge)
+    (x0, y0, z0), (x1, y1, z1) = region
+    e = grid.block_edge
+    return (-(-x1 // e) - x0 // e) * (-(-y1 // e) - y0 // e) * (-(-z1 // e) - z0 // e)
+
+
 def cr_decrease_bound(r0: float, n_blocks: int) -> float:
     """(r0 - 1) / (r0 + n - 1) * 100 (pipeline.py:182-189)."""
     from .errors import InvalidArgument

@@ -168,3 +168,44 @@ def test_product_path_has_no_cpu_fallback():
     x = np.ones((4, 4, 4), np.float32)
     with pytest.raises(BackendUnavailable):
         F.compress_bytes(x, "absolute", 0.1)
+
+
+def test_intersecting_block_count_matches_brute_force():
+    L = _lib.load()
+    grid = F.partition((64, 64, 64), 8)
+    assert F.intersecting_block_count(grid, ((0, 0, 0), (64, 64, 64))) == 512
+    assert F.intersecting_block_count(grid, ((0, 0, 0), (64, 64, 32))) == 256
+    assert F.intersecting_block_count(grid, ((0, 0, 0), (64, 32, 32))) == 128
+    assert F.intersecting_block_count(grid, ((0, 0, 0), (32, 32, 32))) == 64
+    rng = np.random.default_rng(3)
+    for _ in range(30):
+        dims = tuple(int(v) for v in rng.integers(1, 40, 3))
+        e = int(rng.integers(2, 9))
+        g = F.partition(dims, e)
+        lo = [int(rng.integers(0, d)) for d in dims]
+        hi = [int(rng.integers(a + 1, d + 1)) for a, d in zip(lo, dims)]
+        reg = (tuple(lo), tuple(hi))
+        hits = 0
+        for b in range(g.n_blocks):
+            s = g.spec(b)
+            (i0, j0, k0), (bx, by, bz) = s.origin, s.extent
+            if (i0 < hi[0] and i0 + bx > lo[0] and j0 < hi[1] and j0 + by > lo[1]
+                    and k0 < hi[2] and k0 + bz > lo[2]):
+                hits += 1
+        assert F.intersecting_block_count(g, reg) == hits
+        r6 = np.array(lo + hi, np.int64)
+        assert L.ftlz_intersecting_block_count(*dims, e, r6.ctypes.data) == hits
+
+
+def test_region_validation_before_any_device_work():
+    from oracle import oracle as O
+
+    data = load("c1")["archive"].tobytes()
+    si = O.parse_check(data)
+    s = CompressedStream._from_archive(data, {
+        "payload_off": si.payload_off, "payload_len": si.payload_len, "unpred_off": si.unpred_off,
+        "n_unpred": si.n_unpred, "has_sum_dc": bool(si.has_sum_dc), "sumdc_off": si.sumdc_off})
+    for reg in (((0, 0, 0), (65, 64, 64)), ((-1, 0, 0), (5, 5, 5)), ((4, 4, 4), (4, 5, 5))):
+        with pytest.raises(F.InvalidRegion) as ei:
+            F.decompress_region(s, reg)
+        assert str(ei.value) == f"region {reg} outside dims (64, 64, 64)"

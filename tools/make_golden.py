@@ -274,12 +274,40 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--large", action="store_true")
     ap.add_argument("--only", default=None)
+    ap.add_argument("--region", action="store_true", help="region-extraction fixtures only")
     args = ap.parse_args()
     os.makedirs(OUT, exist_ok=True)
     mpath = os.path.join(OUT, "manifest.json")
     manifest = json.load(open(mpath)) if os.path.exists(mpath) else {"cases": {}, "corrupt": {}, "large": {}}
     manifest["generator"] = {"numpy": np.__version__, "ftlz": ftlz.__version__,
                              "script": "tools/make_golden.py"}
+    if args.region:
+        # decompress_region (pipeline.py:726-795) on clean and payload-damaged archives
+        res = {}
+        for src in ("payload_14x10x9_e4", "pipe_noise_13x11x10_e5", "mixed_33x17x70_e16"):
+            z = np.load(os.path.join(OUT, src + ".npz"))
+            arch = z["archive"].tobytes()
+            blobs = [("clean", arch)]
+            if src != "mixed_33x17x70_e16":
+                cz = np.load(os.path.join(OUT, f"corrupt_{src}.npz"))
+                blobs += [(k, cz[k].tobytes()) for k in sorted(cz.files) if k.startswith("payflip_")]
+            dims = ftlz.parse(arch).dims
+            regions = [((0, 0, 0), tuple(dims)),
+                       ((1, 2, 3), tuple(max(4, d - 2) for d in dims)),
+                       ((0, 0, 0), (min(5, dims[0]), min(4, dims[1]), min(3, dims[2]))),
+                       ((dims[0] - 1, dims[1] - 1, dims[2] - 1), tuple(dims))]
+            for bname, blob in blobs:
+                stream = ftlz.parse(blob)
+                for ri, reg in enumerate(regions):
+                    out, rep = ftlz.decompress_region(stream, reg)
+                    key = f"{src}|{bname}|{ri}"
+                    res[key] = {"region": [list(reg[0]), list(reg[1])], "status": rep.status,
+                                "detail": rep.detail, "reexecuted": list(rep.decomp_block_reexecuted),
+                                "output_sha256": None if out is None else sha(out.values)}
+        manifest["region"] = res
+        json.dump(manifest, open(mpath, "w"), indent=1, sort_keys=True)
+        print("region", len(res))
+        return
     if not args.large:
         for c in small_cases():
             if args.only and args.only not in c["name"]:
