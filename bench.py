@@ -135,6 +135,23 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml, 5 ms"}
 
 
+def reduce_max(vals, dist, device=None):
+    """Element-wise max over ranks (the contract's max-over-ranks device time); identity when
+    `dist` is None.  NCCL needs a CUDA tensor (device), gloo a CPU one (device None)."""
+    if dist is None:
+        return [float(v) for v in vals]
+    import torch
+
+    t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(v) for v in t.tolist()]
+
+
+def job_value(world: int, n_bytes: float, step_ms: float) -> float:
+    """Whole-job throughput: every rank processes its own replica (scaling weak)."""
+    return world * n_bytes / (step_ms * 1e-3) / 1e9
+
+
 def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -298,12 +315,9 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     tc_ms, td_ms = sum(tc) / len(tc), sum(td) / len(td)
     step_ms = tc_ms + td_ms
-    if dist is not None:
-        t = torch.tensor([step_ms, tc_ms, td_ms], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        step_ms, tc_ms, td_ms = (float(v) for v in t.tolist())
+    step_ms, tc_ms, td_ms = reduce_max([step_ms, tc_ms, td_ms], dist, f"cuda:{local}")
     n_bytes = 4.0 * N
-    value = world * n_bytes / (step_ms * 1e-3) / 1e9
+    value = job_value(world, n_bytes, step_ms)
 
     # ---- parity of the timed workload against the reference's own archive / output hashes
     parity = {}
