@@ -209,3 +209,21 @@ def test_region_validation_before_any_device_work():
         with pytest.raises(F.InvalidRegion) as ei:
             F.decompress_region(s, reg)
         assert str(ei.value) == f"region {reg} outside dims (64, 64, 64)"
+
+
+def test_fault_plan_helpers_mirror_reference():
+    from paper_2010_03144_b200 import faults as FT
+
+    assert FT.InjectionPlan("compressed_bytes").target == "bytes"
+    with pytest.raises(F.InvalidInjection):
+        FT.InjectionPlan("nowhere")
+    buf = np.arange(4, dtype=np.float32)
+    FT.inject_bitflip(buf, 2, 31)
+    assert buf[2] == -2.0
+    FT.inject_bitflip(buf, 2, 31)
+    assert buf[2] == 2.0
+    b = bytearray(b"\x00\x01")
+    FT.inject_bitflip(b, 1, 1)
+    assert b == bytearray(b"\x00\x03")
+    s1, s2 = FT.trial_seed(7, 0, 0), FT.trial_seed(7, 0, 1)
+    assert s1 != s2 and s1 == FT.trial_seed(7, 0, 0)

@@ -275,12 +275,46 @@ def main():
     ap.add_argument("--large", action="store_true")
     ap.add_argument("--only", default=None)
     ap.add_argument("--region", action="store_true", help="region-extraction fixtures only")
+    ap.add_argument("--campaign", action="store_true", help="fault-campaign fixtures only")
     args = ap.parse_args()
     os.makedirs(OUT, exist_ok=True)
     mpath = os.path.join(OUT, "manifest.json")
     manifest = json.load(open(mpath)) if os.path.exists(mpath) else {"cases": {}, "corrupt": {}, "large": {}}
     manifest["generator"] = {"numpy": np.__version__, "ftlz": ftlz.__version__,
                              "script": "tools/make_golden.py"}
+    if args.campaign:
+        # faults.run_trial / run_campaign (faults.py:143-367): every target, both protections
+        from ftlz import faults as FT
+
+        f = ftlz.synth_field("mixed", (16, 14, 12), seed=21)
+        np.savez_compressed(os.path.join(OUT, "campaign.npz"), input=f.values)
+        ebs = [ftlz.ErrorBound.absolute(1e-3), ftlz.ErrorBound.relative(1e-3)]
+        cfgs = {"protected": ftlz.FtConfig.protected(block_edge=5),
+                "unprotected": ftlz.FtConfig.unprotected(block_edge=5)}
+        seed, trials = 7, 4
+        rep = FT.run_campaign(f, ebs, cfgs, trials=trials, seed=seed, targets=FT.TARGETS, field_note="golden")
+        outcomes = []
+        ci = 0
+        for cname, cfg in cfgs.items():
+            for tgt in FT.TARGETS:
+                for eb in ebs:
+                    ref = FT.fault_free_reference(f, eb, cfg)
+                    for t in range(trials):
+                        plan = FT.InjectionPlan(target=tgt, seed=FT.trial_seed(seed, ci, t))
+                        o = FT.run_trial(f, eb, cfg, plan, ref)
+                        outcomes.append({"cfg": cname, "target": tgt, "eb": [eb.mode, eb.value], "trial": t,
+                                         "classification": o.classification, "corrected": o.corrected,
+                                         "max_abs_error": o.max_abs_error, "ratio": o.ratio,
+                                         "bit_identical_output": o.bit_identical_output,
+                                         "bit_identical_archive": o.bit_identical_archive,
+                                         "compress_events": o.compress_events,
+                                         "decompress_events": o.decompress_events, "detail": o.detail})
+                    ci += 1
+        manifest["campaign"] = {"seed": seed, "trials": trials, "rows": rep.rows(), "outcomes": outcomes,
+                                "input_sha256": sha(f.values)}
+        json.dump(manifest, open(mpath, "w"), indent=1, sort_keys=True)
+        print("campaign", len(outcomes))
+        return
     if args.region:
         # decompress_region (pipeline.py:726-795) on clean and payload-damaged archives
         res = {}
