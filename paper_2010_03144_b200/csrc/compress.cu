@@ -224,6 +224,45 @@ struct CodebookScratch {
     u8* lens;      // cap (by symbol)
 };
 
+// two-queue Huffman merge over leaves sorted by (weight, symbol) (the reference heap with its
+// (weight, tie) order, encode.py:26-71): leaves 0..n-1, merged nodes n..2n-2; queue heads in
+// registers.  W must point into one memory space (shared or global) so accesses stay typed.
+template <typename SetParent>
+FTLZ_DEV void cb_merge(u64* W, const u64* keys, int n, SetParent set_parent) {
+    for (int i = 0; i < n; i++) W[i] = keys[i] >> 16;
+    int li = 0, mi = n, mk = n;   // next leaf, next merged to consume, next merged to create
+    u64 wl = W[0], wm = 0;
+    for (int t = 0; t < n - 1; t++) {
+        int pk0, pk1;
+        u64 pw0, pw1;
+        // leaf wins ties
+        if (li < n && (mi >= mk || wl <= wm)) { pk0 = li; pw0 = wl; li++; wl = li < n ? W[li] : 0; }
+        else { pk0 = mi; pw0 = wm; mi++; wm = mi < mk ? W[mi] : 0; }
+        if (li < n && (mi >= mk || wl <= wm)) { pk1 = li; pw1 = wl; li++; wl = li < n ? W[li] : 0; }
+        else { pk1 = mi; pw1 = wm; mi++; wm = mi < mk ? W[mi] : 0; }
+        const u64 sum = pw0 + pw1;
+        W[mk] = sum;
+        if (mi == mk) wm = sum;   // the merged queue was empty: its head is the new node
+        set_parent(pk0, mk);
+        set_parent(pk1, mk);
+        mk++;
+    }
+}
+
+// symbol of alphabet rank i: the word holding it by binary search over the word prefixes,
+// then the (i - prefix)-th set bit of that word
+FTLZ_DEV int cb_select(const u32* bm, const u32* wpre, int nwords, u32 i) {
+    int lo = 0, hi = nwords - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (wpre[mid] <= i) lo = mid;
+        else hi = mid - 1;
+    }
+    u32 m = bm[lo];
+    for (u32 r = i - wpre[lo]; r; r--) m &= m - 1;
+    return lo * 32 + __ffs(m) - 1;
+}
+
 __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScratch S) {
     if (dev_failed(A.st)) return;
     extern __shared__ __align__(16) u64 cb_dyn[];   // keys[CB_SMEM_KEYS] | weights[2*CB_SMEM_KEYS]
@@ -283,15 +322,9 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
     int np2 = 1;
     while (np2 < n) np2 <<= 1;
     u64* keys = np2 <= CB_SMEM_KEYS ? skeys : S.keys;
-    for (int w = tid; w < nwords; w += CB_THREADS) {
-        u32 m = s_bm[w];
-        u32 pos = s_wpre[w];
-        while (m) {
-            const int bit = __ffs(m) - 1;
-            m &= m - 1;
-            const int sy = w * 32 + bit;
-            keys[pos++] = ((u64)A.hist[sy] << 16) | (u64)sy;   // (weight, symbol)
-        }
+    for (int i = tid; i < n; i += CB_THREADS) {
+        const int sy = cb_select(s_bm, s_wpre, nwords, (u32)i);
+        keys[i] = ((u64)A.hist[sy] << 16) | (u64)sy;   // (weight, symbol)
     }
     for (int i = n + tid; i < np2; i += CB_THREADS) keys[i] = ~0ull;
     __syncthreads();
@@ -307,43 +340,12 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
         if (n == 1) {
             if (small) par16[0] = 0xffffu;
             else S.parent[0] = 0xffffffffu;
+        } else if (small) {
+            cb_merge(cb_dyn + CB_SMEM_KEYS, keys, n, [&](int i, int mk) { par16[i] = (u16)mk; });
+            par16[2 * n - 2] = 0xffffu;
         } else {
-            u64* W = small ? cb_dyn + CB_SMEM_KEYS : S.w;
-            for (int i = 0; i < n; i++) W[i] = keys[i] >> 16;
-            int li = 0, mi = n, mk = n;  // next leaf, next merged to consume, next merged to create
-            u64 wl = W[0], wm = 0;
-            for (int t = 0; t < n - 1; t++) {
-                int pk[2];
-                u64 pw[2];
-#pragma unroll
-                for (int r = 0; r < 2; r++) {
-                    // leaf wins ties (heap order of the reference)
-                    if (li < n && (mi >= mk || wl <= wm)) {
-                        pk[r] = li;
-                        pw[r] = wl;
-                        li++;
-                        wl = li < n ? W[li] : 0;
-                    } else {
-                        pk[r] = mi;
-                        pw[r] = wm;
-                        mi++;
-                        wm = mi < mk ? W[mi] : 0;
-                    }
-                }
-                const u64 sum = pw[0] + pw[1];
-                W[mk] = sum;
-                if (mi == mk) wm = sum;   // the merged queue was empty: its head is the new node
-                if (small) {
-                    par16[pk[0]] = (u16)mk;
-                    par16[pk[1]] = (u16)mk;
-                } else {
-                    S.parent[pk[0]] = (u32)mk;
-                    S.parent[pk[1]] = (u32)mk;
-                }
-                mk++;
-            }
-            if (small) par16[mk - 1] = 0xffffu;
-            else S.parent[mk - 1] = 0xffffffffu;
+            cb_merge(S.w, keys, n, [&](int i, int mk) { S.parent[i] = (u32)mk; });
+            S.parent[2 * n - 2] = 0xffffffffu;
         }
     }
     __syncthreads();
@@ -443,18 +445,11 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
     // the parent pointers)
     __syncthreads();
     build_ranks();
-    for (int w = tid; w < nwords; w += CB_THREADS) {
-        u32 m = s_bm[w];
-        u32 pos = s_wpre[w];
-        while (m) {
-            const int bit = __ffs(m) - 1;
-            m &= m - 1;
-            const u32 sy = (u32)(w * 32 + bit);
-            u8* e = o + 4 + 5ull * (u64)pos;
-            e[0] = (u8)sy; e[1] = (u8)(sy >> 8); e[2] = (u8)(sy >> 16); e[3] = (u8)(sy >> 24);
-            e[4] = S.lens[sy];
-            pos++;
-        }
+    for (int i = tid; i < n; i += CB_THREADS) {
+        const u32 sy = (u32)cb_select(s_bm, s_wpre, nwords, (u32)i);
+        u8* e = o + 4 + 5ull * (u64)i;
+        e[0] = (u8)sy; e[1] = (u8)(sy >> 8); e[2] = (u8)(sy >> 16); e[3] = (u8)(sy >> 24);
+        e[4] = S.lens[sy];
     }
 }
 
