@@ -54,6 +54,33 @@ FTLZ_DEV bool enc_stage(const CompArgs& A, long long b, int vol, const u32* fix,
     return fixed;
 }
 
+// next block's bins held in registers while the current block is processed (blocks of at most
+// 1024 symbols, not bins-faulted): one latency per block instead of a stall before each
+struct BinsPrefetch {
+    uint4 r[4];
+    int nch;
+    FTLZ_DEV void load(const CompArgs& A, long long b, int vol, int lane) {
+        nch = (vol + 7) >> 3;
+        const uint4* src = (const uint4*)(A.bins + bins_index(A.g, b, 0));
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int c = lane + 32 * q;
+            if (c < nch) r[q] = __ldg(src + c);
+        }
+    }
+    FTLZ_DEV void store(u16* sym16, int lane) const {
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int c = lane + 32 * q;
+            if (c < nch) ((uint4*)sym16)[c] = r[q];
+        }
+    }
+};
+
+FTLZ_DEV bool enc_prefetchable(const CompArgs& A, long long b, int vol, const u8* fixed_flag) {
+    return vol <= 1024 && !(A.events[b] & 8) && !(A.n_faults && A.fault_first[b] >= 0 && fixed_flag[b]);
+}
+
 __global__ void __launch_bounds__(512) k_enc_len(CompArgs A, const u32* fix, const u8* fixed_flag) {
     extern __shared__ __align__(16) unsigned char smem[];
     if (dev_failed(A.st)) return;
@@ -65,15 +92,36 @@ __global__ void __launch_bounds__(512) k_enc_len(CompArgs A, const u32* fix, con
     enc_fill_window(A, s_enc);
     __syncthreads();
     const EncWin W = {s_enc, A.enc, A.center - ENC_WIN / 2, A.cap};
-    for (long long b = (long long)blockIdx.x * nw + warp; b < g.nb; b += (long long)gridDim.x * nw) {
-        const BlockInfo B = block_info(g, b);
-        const int vol = B.vol;
+    const long long NW = (long long)gridDim.x * nw;
+    long long b = (long long)blockIdx.x * nw + warp;
+    BinsPrefetch P;
+    bool pf = false;
+    int vol = 0;
+    if (b < g.nb) {
+        vol = block_info(g, b).vol;
+        pf = enc_prefetchable(A, b, vol, fixed_flag);
+        if (pf) P.load(A, b, vol, lane);
+    }
+    for (; b < g.nb; b += NW) {
         u32 bits = 0;
         bool range_err = false;
-        if (!(A.events[b] & 8)) {
-            const bool fixed = enc_stage(A, b, vol, fix, fixed_flag, sym16, sym32, lane);
-            const int chunk = ((vol + 31) >> 5) | 1;
-            const int p0 = lane * chunk, pend = min(p0 + chunk, vol);
+        const bool bad = (A.events[b] & 8) != 0;
+        bool fixed = false;
+        if (!bad) {
+            if (pf) P.store(sym16, lane);
+            else fixed = enc_stage(A, b, vol, fix, fixed_flag, sym16, sym32, lane);
+        }
+        __syncwarp();
+        const int cvol = vol;
+        const long long bn = b + NW;
+        if (bn < g.nb) {
+            vol = block_info(g, bn).vol;
+            pf = enc_prefetchable(A, bn, vol, fixed_flag);
+            if (pf) P.load(A, bn, vol, lane);
+        }
+        if (!bad) {
+            const int chunk = ((cvol + 31) >> 5) | 1;
+            const int p0 = lane * chunk, pend = min(p0 + chunk, cvol);
             for (int p = p0; p < pend; p++) {
                 const u32 sym = fixed ? sym32[p] : (u32)sym16[p];
                 u32 l = (u32)(W.get(sym) & 63);
@@ -83,8 +131,8 @@ __global__ void __launch_bounds__(512) k_enc_len(CompArgs A, const u32* fix, con
                 }
                 bits += l;
             }
-            __syncwarp();
         }
+        __syncwarp();
         u32 pre = bits;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -193,11 +241,32 @@ __global__ void __launch_bounds__(512) k_enc_pack(CompArgs A, const u32* fix, co
     const EncWin W = {s_enc, A.enc, A.center - ENC_WIN / 2, A.cap};
     u32* words = (u32*)A.out;
     const u64 pay0 = A.layout[LAYOUT_PAY_OFF] * 8;
-    for (long long b = (long long)blockIdx.x * nw + warp; b < g.nb; b += (long long)gridDim.x * nw) {
-        if (A.events[b] & 8) continue;
-        const BlockInfo B = block_info(g, b);
-        const int vol = B.vol;
-        const bool fixed = enc_stage(A, b, vol, fix, fixed_flag, sym16, sym32, lane);
+    const long long NW = (long long)gridDim.x * nw;
+    long long b = (long long)blockIdx.x * nw + warp;
+    BinsPrefetch P;
+    bool pf = false;
+    int nvol = 0;
+    if (b < g.nb) {
+        nvol = block_info(g, b).vol;
+        pf = enc_prefetchable(A, b, nvol, fixed_flag);
+        if (pf) P.load(A, b, nvol, lane);
+    }
+    for (; b < g.nb; b += NW) {
+        const int vol = nvol;
+        const bool bad = (A.events[b] & 8) != 0;
+        bool fixed = false;
+        if (!bad) {
+            if (pf) P.store(sym16, lane);
+            else fixed = enc_stage(A, b, vol, fix, fixed_flag, sym16, sym32, lane);
+        }
+        __syncwarp();
+        const long long bn = b + NW;
+        if (bn < g.nb) {
+            nvol = block_info(g, bn).vol;
+            pf = enc_prefetchable(A, bn, nvol, fixed_flag);
+            if (pf) P.load(A, bn, nvol, lane);
+        }
+        if (bad) continue;
         const int chunk = ((vol + 31) >> 5) | 1;
         const int p0 = lane * chunk, pend = min(p0 + chunk, vol);
         const u64 gpos = pay0 + A.bitoff[b] + A.lanepre[(size_t)b * 32 + lane];
