@@ -88,7 +88,11 @@ FTLZ_DEV void prep_visit(const float* tile, const PWalk& w, int p, const double*
     t4[3] = __dmul_rn(cv[128 + w.k], v);
 }
 
-__global__ void __launch_bounds__(512, 1) k_prep(const __grid_constant__ CompArgs A, const __grid_constant__ CUtensorMap tmap) {
+// one tile per warp: the next block's TMA is issued as soon as the current tile is last read,
+// and the freed shared memory buys more resident warps (latency hiding across warps)
+#define PREP_NBUF 1
+
+__global__ void __launch_bounds__(768, 1) k_prep(const __grid_constant__ CompArgs A, const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     const Geom& g = A.g;
@@ -98,7 +102,7 @@ __global__ void __launch_bounds__(512, 1) k_prep(const __grid_constant__ CompArg
     WarpStager ws;
     ws.base = slot;
     ws.tbytes = S.tile_bytes;
-    double* cv = (double*)(slot + 2 * S.tile_bytes);   // [0,64) i - hx, [64,128) j - hy, [128,192) k - hz
+    double* cv = (double*)(slot + PREP_NBUF * S.tile_bytes);   // [0,64) i - hx, [64,128) j - hy, [128,192) k - hz
     double* stk = cv + 192;                            // 32 x 4
     double* leafval = stk + 128;                       // nls x 4
     double* ar = leafval + 4 * A.pp_nls;               // samples
@@ -123,11 +127,12 @@ __global__ void __launch_bounds__(512, 1) k_prep(const __grid_constant__ CompArg
     while (b < g.nb) {
         const BlockInfo B = Bnext;
         const long long bn = b + NW;
-        if (bn < g.nb) {
+        if (PREP_NBUF == 2 && bn < g.nb) {
             Bnext = block_info(g, bn);
             ws.issue(A.x, g, S, &tmap, Bnext, buf ^ 1, lane);
         }
-        ws.wait(S, buf, bn < g.nb);
+        ws.wait(S, buf, PREP_NBUF == 2 && bn < g.nb);
+        bool issued = false;
         float* tile = (float*)(slot + buf * S.tile_bytes);
         const int bx = B.bx, by = B.by, bz = B.bz, vol = B.vol;
         const int zoff = zshift(g, B), tjump = S.tz - bz, ijump = (S.tye - by) * S.tz;
@@ -292,6 +297,11 @@ __global__ void __launch_bounds__(512, 1) k_prep(const __grid_constant__ CompArg
                 al[q] = fabs(__dadd_rn(v, -pl));
             }
             __syncwarp();
+            if (PREP_NBUF == 1 && bn < g.nb) {   // the tile is free: start the next block's copy
+                Bnext = block_info(g, bn);
+                ws.issue(A.x, g, S, &tmap, Bnext, 0, lane);
+                issued = true;
+            }
             double e2[2];
             if (ns < 8) {
                 double r0 = 0.0, r1 = 0.0;
@@ -368,7 +378,11 @@ __global__ void __launch_bounds__(512, 1) k_prep(const __grid_constant__ CompArg
             A.coef[bb] = cf;
         }
         __syncwarp();
-        buf ^= 1;
+        if (PREP_NBUF == 1 && !issued && bn < g.nb) {
+            Bnext = block_info(g, bn);
+            ws.issue(A.x, g, S, &tmap, Bnext, 0, lane);
+        }
+        if (PREP_NBUF == 2) buf ^= 1;
         b = bn;
     }
     // value range: warp -> CTA -> global (ordered-int encoding as k_resolve expects; NaN apart)
