@@ -81,6 +81,18 @@ FTLZ_DEV bool enc_prefetchable(const CompArgs& A, long long b, int vol, const u8
     return vol <= 1024 && !(A.events[b] & 8) && !(A.n_faults && A.fault_first[b] >= 0 && fixed_flag[b]);
 }
 
+template <bool FIXED>
+FTLZ_DEV u32 len_range(const EncWin& W, const u16* sym16, const u32* sym32, int p0, int pend, bool& range_err) {
+    u32 bits = 0;
+    for (int p = p0; p < pend; p++) {
+        const u32 sym = FIXED ? sym32[p] : (u32)sym16[p];
+        u32 l = (u32)(W.get(sym) & 63);
+        range_err |= l == 0;
+        bits += l ? l : 1u;
+    }
+    return bits;
+}
+
 __global__ void __launch_bounds__(512) k_enc_len(CompArgs A, const u32* fix, const u8* fixed_flag) {
     extern __shared__ __align__(16) unsigned char smem[];
     if (dev_failed(A.st)) return;
@@ -122,15 +134,8 @@ __global__ void __launch_bounds__(512) k_enc_len(CompArgs A, const u32* fix, con
         if (!bad) {
             const int chunk = ((cvol + 31) >> 5) | 1;
             const int p0 = lane * chunk, pend = min(p0 + chunk, cvol);
-            for (int p = p0; p < pend; p++) {
-                const u32 sym = fixed ? sym32[p] : (u32)sym16[p];
-                u32 l = (u32)(W.get(sym) & 63);
-                if (l == 0) {
-                    range_err = true;
-                    l = 1;
-                }
-                bits += l;
-            }
+            if (fixed) bits = len_range<true>(W, sym16, sym32, p0, pend, range_err);
+            else bits = len_range<false>(W, sym16, sym32, p0, pend, range_err);
         }
         __syncwarp();
         u32 pre = bits;
@@ -228,6 +233,44 @@ FTLZ_DEV void enc_put(u32* words, u64 widx, u32 bits_be, bool shared_word) {
     else words[widx] = v;
 }
 
+// MSB-first packing of symbols [p0, pend) starting at absolute bit gpos; FIXED: 32-bit symbols
+// of a bins-faulted block; LONG: some code is longer than 32 bits
+template <bool FIXED, bool LONG>
+FTLZ_DEV void pack_range(const EncWin& W, const u16* sym16, const u32* sym32, int p0, int pend, u64 gpos, u32* words) {
+    u64 widx = gpos >> 5;
+    u64 acc = 0;                          // pending bits, left-aligned at bit 63
+    int nacc = (int)(gpos & 31);          // leading bits of the first word belong to others
+    bool first = true;
+    for (int p = p0; p < pend; p++) {
+        const u32 sym = FIXED ? sym32[p] : (u32)sym16[p];
+        const u64 e = W.get(sym);
+        int l = (int)(e & 63);
+        u64 code = e >> 6;
+        if (LONG && l > 32) {
+            const int hl = l - 32;
+            acc |= (code >> 32) << (64 - nacc - hl);
+            nacc += hl;
+            if (nacc >= 32) {
+                enc_put(words, widx++, (u32)(acc >> 32), first);
+                first = false;
+                acc <<= 32;
+                nacc -= 32;
+            }
+            code &= 0xffffffffull;
+            l = 32;
+        }
+        acc |= code << (64 - nacc - l);
+        nacc += l;
+        if (nacc >= 32) {
+            enc_put(words, widx++, (u32)(acc >> 32), first);
+            first = false;
+            acc <<= 32;
+            nacc -= 32;
+        }
+    }
+    if (nacc > 0) enc_put(words, widx, (u32)(acc >> 32), true);
+}
+
 __global__ void __launch_bounds__(512) k_enc_pack(CompArgs A, const u32* fix, const u8* fixed_flag) {
     extern __shared__ __align__(16) unsigned char smem[];
     if (dev_failed(A.st)) return;
@@ -241,6 +284,7 @@ __global__ void __launch_bounds__(512) k_enc_pack(CompArgs A, const u32* fix, co
     const EncWin W = {s_enc, A.enc, A.center - ENC_WIN / 2, A.cap};
     u32* words = (u32*)A.out;
     const u64 pay0 = A.layout[LAYOUT_PAY_OFF] * 8;
+    const bool longc = A.layout[LAYOUT_MAXLEN] > 32;
     const long long NW = (long long)gridDim.x * nw;
     long long b = (long long)blockIdx.x * nw + warp;
     BinsPrefetch P;
@@ -270,38 +314,11 @@ __global__ void __launch_bounds__(512) k_enc_pack(CompArgs A, const u32* fix, co
         const int chunk = ((vol + 31) >> 5) | 1;
         const int p0 = lane * chunk, pend = min(p0 + chunk, vol);
         const u64 gpos = pay0 + A.bitoff[b] + A.lanepre[(size_t)b * 32 + lane];
-        u64 widx = gpos >> 5;
-        u64 acc = 0;                          // pending bits, left-aligned at bit 63
-        int nacc = (int)(gpos & 31);          // leading bits of the first word belong to others
-        bool first = true;
-        for (int p = p0; p < pend; p++) {
-            const u32 sym = fixed ? sym32[p] : (u32)sym16[p];
-            const u64 e = W.get(sym);
-            int l = (int)(e & 63);
-            u64 code = e >> 6;
-            if (l > 32) {
-                const int hl = l - 32;
-                acc |= (code >> 32) << (64 - nacc - hl);
-                nacc += hl;
-                if (nacc >= 32) {
-                    enc_put(words, widx++, (u32)(acc >> 32), first);
-                    first = false;
-                    acc <<= 32;
-                    nacc -= 32;
-                }
-                code &= 0xffffffffull;
-                l = 32;
-            }
-            acc |= code << (64 - nacc - l);
-            nacc += l;
-            if (nacc >= 32) {
-                enc_put(words, widx++, (u32)(acc >> 32), first);
-                first = false;
-                acc <<= 32;
-                nacc -= 32;
-            }
+        if (p0 < pend) {
+            if (fixed) pack_range<true, true>(W, sym16, sym32, p0, pend, gpos, words);
+            else if (longc) pack_range<false, true>(W, sym16, sym32, p0, pend, gpos, words);
+            else pack_range<false, false>(W, sym16, sym32, p0, pend, gpos, words);
         }
-        if (nacc > 0 && p0 < pend) enc_put(words, widx, (u32)(acc >> 32), true);
         __syncwarp();
     }
 }
