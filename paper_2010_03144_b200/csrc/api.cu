@@ -146,8 +146,10 @@ struct HostPlan {
     ExtPlan ep[8];
     std::vector<Leaf> leaves;
     std::vector<uint32_t> coords, wave, planes;
+    std::vector<uint32_t> wcrd;   // coordinates in wavefront order (same offsets as wave)
     size_t bytes() const {
         return al256(sizeof(ep)) + al256(leaves.size() * sizeof(Leaf) + 16) + al256(coords.size() * 4 + 16) +
+               al256(wcrd.size() * 4 + 16) +
                al256(wave.size() * 4 + 16) + al256(planes.size() * 4 + 16);
     }
 };
@@ -177,7 +179,7 @@ static bool build_plan(int64_t nx, int64_t ny, int64_t nz, int e, HostPlan& P) {
     g.nvmax8 = (g.vmax + 7) & ~7;
     g.fcz = make_fastdiv((u32)std::min<int64_t>(g.cz, 0xffffffffll));
     g.fcy = make_fastdiv((u32)std::min<int64_t>(g.cy, 0xffffffffll));
-    P.leaves.clear(); P.coords.clear(); P.wave.clear(); P.planes.clear();
+    P.leaves.clear(); P.coords.clear(); P.wave.clear(); P.planes.clear(); P.wcrd.clear();
     for (int xid = 0; xid < 8; xid++) {
         ExtPlan& E = P.ep[xid];
         memset(&E, 0, sizeof E);
@@ -214,7 +216,10 @@ static bool build_plan(int64_t nx, int64_t ny, int64_t nz, int e, HostPlan& P) {
         uint32_t acc = 0;
         for (int s = 0; s < E.nplanes; s++) {
             P.planes.push_back(acc);
-            for (uint32_t q : byplane[s]) P.wave.push_back(q);
+            for (uint32_t q : byplane[s]) {
+                P.wave.push_back(q);
+                P.wcrd.push_back(P.coords[E.coord_off + q]);
+            }
             acc += (uint32_t)byplane[s].size();
         }
         P.planes.push_back(acc);
@@ -228,6 +233,7 @@ struct DevPlan {
     const u32* coords;
     const u32* wave;
     const u32* planes;
+    const u32* wcrd;
 };
 
 // upload plan tables into `dst` (device), returns pointers
@@ -248,12 +254,14 @@ static int upload_plan(const HostPlan& P, unsigned char* dst, DevPlan& D, cudaSt
     size_t o_c = put(P.coords.data(), P.coords.size() * 4);
     size_t o_w = put(P.wave.data(), P.wave.size() * 4);
     size_t o_p = put(P.planes.data(), P.planes.size() * 4);
+    size_t o_wc = put(P.wcrd.data(), P.wcrd.size() * 4);
     CK(cudaMemcpyAsync(dst, staging.data(), off, cudaMemcpyHostToDevice, s));
     D.ep = (const ExtPlan*)(dst + o_ep);
     D.leaves = (const Leaf*)(dst + o_l);
     D.coords = (const u32*)(dst + o_c);
     D.wave = (const u32*)(dst + o_w);
     D.planes = (const u32*)(dst + o_p);
+    D.wcrd = (const u32*)(dst + o_wc);
     return FTLZ_OK;
 }
 
@@ -570,7 +578,7 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     A.faults = (const ftlz_fault*)(ws + L.faults);
     A.fault_first = (const int*)(ws + L.ffirst);
     A.override_ = ovr ? (const int8_t*)(ws + L.ovr) : nullptr;
-    A.plans = D.ep; A.leaves = D.leaves; A.coords = D.coords; A.wave = D.wave; A.planes = D.planes;
+    A.plans = D.ep; A.leaves = D.leaves; A.coords = D.coords; A.wave = D.wave; A.planes = D.planes; A.wcrd = D.wcrd;
     A.coef = (float4*)(ws + L.coef); A.insum = (u64*)(ws + L.insum); A.inisum = (u64*)(ws + L.inisum);
     A.ind = ws + L.ind; A.unpc = (u32*)(ws + L.unpc); A.bsum = (u64*)(ws + L.bsum); A.bisum = (u64*)(ws + L.bisum);
     A.dcs = (u64*)(ws + L.dcs); A.bitlen = (u32*)(ws + L.bitlen); A.regpre = (u32*)(ws + L.regpre);
@@ -823,7 +831,7 @@ static DecArgs make_dec_args(const HostPlan& P, const DevPlan& D, const DecLayou
     A.n_faults = (int)nf;
     A.faults = (const ftlz_fault*)(ws + L.faults);
     A.fault_first = (const int*)(ws + L.ffirst);
-    A.plans = D.ep; A.coords = D.coords; A.wave = D.wave; A.planes = D.planes;
+    A.plans = D.ep; A.coords = D.coords; A.wave = D.wave; A.planes = D.planes; A.wcrd = D.wcrd;
     A.maps = (u32*)(ws + L.maps); A.smaps = (u32*)(ws + L.smaps); A.sentry = (u64*)(ws + L.sentry);
     A.nchunks = L.nchunks; A.nsuper = L.nsuper;
     A.ind = ws + L.ind; A.rec_off = (u64*)(ws + L.recoff); A.unpc = (u32*)(ws + L.unpc);
@@ -891,7 +899,7 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     k_parse_tail<<<1, PT_THREADS, 8192 * 8, s>>>(A);
     LCHK("k_parse_tail");
     size_t dec_smem = ((size_t)4 << DEC_TBITS) + (size_t)DEC_WARPS * 32 * g.e * 4;
-    size_t rslot = al16((size_t)g.vmax * 8) + al16((size_t)g.vmax * 4);
+    size_t rslot = al16((size_t)g.vmax * 8) + al16((size_t)g.vmax * 4) + al16(2 * (size_t)g.nvmax8);
     int rw = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / rslot));
     if (decode) {
         PF.mark("k_decode", s);
@@ -1002,7 +1010,7 @@ static int region_core(const HostPlan& P, const DevPlan& D, const uint8_t* d_a, 
     A.n_region = n;
     const int sms = num_sms();
     const size_t dec_smem = ((size_t)4 << DEC_TBITS) + (size_t)DEC_WARPS * 32 * g.e * 4;
-    const size_t rslot = al16((size_t)g.vmax * 8) + al16((size_t)g.vmax * 4);
+    const size_t rslot = al16((size_t)g.vmax * 8) + al16((size_t)g.vmax * 4) + al16(2 * (size_t)g.nvmax8);
     const int rw = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / rslot));
     k_decode<<<(n + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32), DEC_WARPS * 32, dec_smem, s>>>(A, A.region_list, (int)n);
     LCHK("k_decode");

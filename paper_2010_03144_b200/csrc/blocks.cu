@@ -256,6 +256,7 @@ __global__ void __launch_bounds__(128) k_quant_lor(CompArgs A) {
         const ExtPlan& PL = A.plans[B.xid];
         const u32* crd = A.coords + PL.coord_off;
         const u32* wave = A.wave + PL.wave_off;
+        const u32* wcrd = A.wcrd + PL.wave_off;
         const u32* planes = A.planes + PL.plane_off;
         bool mism = false;
         u64 dcsum = 0;
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(128) k_quant_lor(CompArgs A) {
             int q0 = __ldg(planes + s), q1 = __ldg(planes + s + 1);
             for (int q = q0 + lane; q < q1; q += 32) {
                 int p = __ldg(wave + q);
-                u32 c = __ldg(crd + p);
+                u32 c = __ldg(wcrd + q);
                 int i = c & 0xff, j = (c >> 8) & 0xff, k = c >> 16;
                 double d100 = i > 0 ? xd[p - byz] : 0.0;
                 double d010 = j > 0 ? xd[p - bz] : 0.0;

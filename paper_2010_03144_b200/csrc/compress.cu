@@ -44,6 +44,7 @@ struct CompArgs {
     const Leaf* leaves;
     const u32* coords;
     const u32* wave;
+    const u32* wcrd;     // coordinates in wavefront order
     const u32* planes;
     // per-block
     float4* coef;

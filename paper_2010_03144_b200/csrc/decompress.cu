@@ -41,6 +41,7 @@ struct DecArgs {
     const ExtPlan* plans;
     const u32* coords;
     const u32* wave;
+    const u32* wcrd;     // coordinates in wavefront order
     const u32* planes;
     u32* maps;
     u32* smaps;
@@ -746,9 +747,12 @@ __global__ void __launch_bounds__(128) k_recon_warp(DecArgs A, int mode) {
     const Geom& g = A.g;
     int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int nw = blockDim.x >> 5;
-    size_t slot_bytes = (((size_t)g.vmax * 8 + 15) & ~(size_t)15) + (((size_t)g.vmax * 4 + 15) & ~(size_t)15);
+    size_t slot_bytes = (((size_t)g.vmax * 8 + 15) & ~(size_t)15) + (((size_t)g.vmax * 4 + 15) & ~(size_t)15) +
+                        (((size_t)g.nvmax8 * 2 + 15) & ~(size_t)15);
     double* xd = (double*)(rsm + (size_t)warp * slot_bytes);
     float* v32 = (float*)(xd + g.vmax);
+    u16* sb = (u16*)(rsm + (size_t)warp * slot_bytes + (((size_t)g.vmax * 8 + 15) & ~(size_t)15) +
+                     (((size_t)g.vmax * 4 + 15) & ~(size_t)15));
     // mode 0: Lorenzo list; 1: re-execution list; 2: region list; 3: region re-execution
     const bool rgn = mode >= 2, reexec = mode & 1;
     u32 n = reexec ? A.counters[DC_NMIS] : (rgn ? A.n_region : A.counters[DC_NLOR]);
@@ -791,14 +795,23 @@ __global__ void __launch_bounds__(128) k_recon_warp(DecArgs A, int mode) {
             }
         } else {
             const u32* wave = A.wave + PL.wave_off;
+            const u32* wcrd = A.wcrd + PL.wave_off;
             const u32* planes = A.planes + PL.plane_off;
+            // the block's bins in shared memory (one coalesced burst instead of a dependent
+            // global load per point and plane)
+            {
+                const uint4* src = (const uint4*)(A.bins + bins_index(g, b, 0));
+                const int nch = (vol + 7) >> 3;
+                for (int c = lane; c < nch; c += 32) ((uint4*)sb)[c] = __ldg(src + c);
+                __syncwarp();
+            }
             for (int s = 0; s < PL.nplanes; s++) {
                 int q0 = __ldg(planes + s), q1 = __ldg(planes + s + 1);
                 for (int q = q0 + lane; q < q1; q += 32) {
                     int p = __ldg(wave + q);
-                    u32 c = __ldg(crd + p);
+                    u32 c = __ldg(wcrd + q);
                     int i = c & 0xff, j = (c >> 8) & 0xff, k = c >> 16;
-                    u32 bin = A.bins[bins_index(g, b, p)];
+                    u32 bin = sb[p];
                     float v;
                     if (bin) {
                         double d100 = i > 0 ? xd[p - byz] : 0.0;
