@@ -366,7 +366,8 @@ static int kernel_attrs_once() {
         setmax((const void*)k_enc_pack);
         setmax((const void*)k_parse_tail);
         setmax((const void*)k_decode);
-        setmax((const void*)k_recon_warp);
+        setmax((const void*)k_recon_g<32>);
+        setmax((const void*)k_recon_g<128>);
         if (cudaGetLastError() != cudaSuccess) rc = FTLZ_ERR_CUDA;
     });
     return rc;
@@ -906,8 +907,8 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         k_decode<<<(unsigned)((g.nb + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32)), DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
         LCHK("k_decode");
         PF.mark("k_recon_warp", s);
-        k_recon_warp<<<sms * 4, rw * 32, rslot * rw, s>>>(A, 0);
-        LCHK("k_recon_warp");
+        k_recon_g<128><<<sms * 4, 128, rslot, s>>>(A, 0);
+        LCHK("k_recon");
     }
     CK(cudaGetLastError());
     PF.mark("", s);
@@ -958,8 +959,8 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         k_decode<<<(unsigned)((nmis + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32)), DEC_WARPS * 32, dec_smem, s>>>(
             A, (const u32*)(ws + L.mis), (int)nmis);
         LCHK("k_decode");
-        k_recon_warp<<<(unsigned)std::min<u32>((nmis + rw - 1) / rw, sms * 4), rw * 32, rslot * rw, s>>>(A, 1);
-        LCHK("k_recon_warp");
+        k_recon_g<32><<<(unsigned)std::min<u32>((nmis + rw - 1) / rw, sms * 4), rw * 32, rslot * rw, s>>>(A, 1);
+        LCHK("k_recon");
         CK(cudaGetLastError());
         std::vector<unsigned char> mf((size_t)g.nb);
         CK(cudaMemcpyAsync(mf.data(), ws + L.mflag, (size_t)g.nb, cudaMemcpyDeviceToHost, s));
@@ -1014,8 +1015,8 @@ static int region_core(const HostPlan& P, const DevPlan& D, const uint8_t* d_a, 
     const int rw = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / rslot));
     k_decode<<<(n + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32), DEC_WARPS * 32, dec_smem, s>>>(A, A.region_list, (int)n);
     LCHK("k_decode");
-    k_recon_warp<<<std::min<u32>((n + rw - 1) / rw, (u32)sms * 4), rw * 32, rslot * rw, s>>>(A, 2);
-    LCHK("k_recon_warp");
+    k_recon_g<32><<<std::min<u32>((n + rw - 1) / rw, (u32)sms * 4), rw * 32, rslot * rw, s>>>(A, 2);
+    LCHK("k_recon");
     std::vector<unsigned char> df((size_t)g.nb), mf((size_t)g.nb);
     CK(cudaMemcpyAsync(df.data(), ws + L.dflag, (size_t)g.nb, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(mf.data(), ws + L.mflag, (size_t)g.nb, cudaMemcpyDeviceToHost, s));
@@ -1040,8 +1041,8 @@ static int region_core(const HostPlan& P, const DevPlan& D, const uint8_t* d_a, 
         k_decode<<<(nmis + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32), DEC_WARPS * 32, dec_smem, s>>>(
             A, (const u32*)(ws + L.mis), (int)nmis);
         LCHK("k_decode");
-        k_recon_warp<<<std::min<u32>((nmis + rw - 1) / rw, (u32)sms * 4), rw * 32, rslot * rw, s>>>(A, 3);
-        LCHK("k_recon_warp");
+        k_recon_g<32><<<std::min<u32>((nmis + rw - 1) / rw, (u32)sms * 4), rw * 32, rslot * rw, s>>>(A, 3);
+        LCHK("k_recon");
         CK(cudaMemcpyAsync(mf.data(), ws + L.mflag, (size_t)g.nb, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
     }

@@ -741,12 +741,51 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
 // K6b / K7: warp = block reconstruction from scratch bins (both predictors), verification.
 // mode 0: Lorenzo list, faults applied, mismatch -> mis_list.
 // mode 1: re-execution of mis_list (no faults); verdict in mflag (2 ok, 3 still mismatching).
-__global__ void __launch_bounds__(128) k_recon_warp(DecArgs A, int mode) {
+// G = threads per block group: 32 (a warp per block) or 128 (a CTA per block: the plane
+// wavefront then covers a whole plane per step, which shortens the per-block latency chain)
+template <int G>
+__global__ void __launch_bounds__(128) k_recon_g(DecArgs A, int mode) {
     if (dev_failed(A.st)) return;
     extern __shared__ __align__(16) unsigned char rsm[];
     const Geom& g = A.g;
-    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int nw = blockDim.x >> 5;
+    const int warp = threadIdx.x / G, lane = threadIdx.x % G;   // group, rank in group
+    const int nw = blockDim.x / G;
+    const int wl = threadIdx.x & 31, wi = (threadIdx.x % G) >> 5;   // lane / warp in the group
+    __shared__ u64 s_red[4];
+    __shared__ u32 s_cnt[4];
+    auto gsync = [&]() {
+        if (G == 32) __syncwarp();
+        else __syncthreads();
+    };
+    // exclusive rank of `flag` among the group's ranks this step + the step's total
+    auto gscan = [&](bool flag, u32& before, u32& total) {
+        const unsigned m = __ballot_sync(0xffffffffu, flag);
+        if (G == 32) {
+            before = __popc(m & ((1u << wl) - 1u));
+            total = __popc(m);
+        } else {
+            if (wl == 0) s_cnt[wi] = __popc(m);
+            __syncthreads();
+            u32 pre = 0, tot = 0;
+            for (int q = 0; q < G / 32; q++) {
+                if (q < wi) pre += s_cnt[q];
+                tot += s_cnt[q];
+            }
+            __syncthreads();
+            before = pre + __popc(m & ((1u << wl) - 1u));
+            total = tot;
+        }
+    };
+    auto gsum = [&](u64 v) -> u64 {
+        v = warp_sum_u64(v);
+        if (G == 32) return v;
+        if (wl == 0) s_red[wi] = v;
+        __syncthreads();
+        u64 t = 0;
+        for (int q = 0; q < G / 32; q++) t += s_red[q];
+        __syncthreads();
+        return t;
+    };
     size_t slot_bytes = (((size_t)g.vmax * 8 + 15) & ~(size_t)15) + (((size_t)g.vmax * 4 + 15) & ~(size_t)15) +
                         (((size_t)g.nvmax8 * 2 + 15) & ~(size_t)15);
     double* xd = (double*)(rsm + (size_t)warp * slot_bytes);
@@ -769,21 +808,19 @@ __global__ void __launch_bounds__(128) k_recon_warp(DecArgs A, int mode) {
         u64 unp_base = A.info[DI_UNP_OFF] + 4 * A.uofs[b];
         // raw words of unpredictable points in row-major order
         u32 zc = 0;
-        for (int p0 = 0; p0 < vol; p0 += 32) {
+        for (int p0 = 0; p0 < vol; p0 += G) {
             int p = p0 + lane;
             u32 bin = p < vol ? A.bins[bins_index(g, b, p)] : 1u;
-            unsigned zm = __ballot_sync(0xffffffffu, bin == 0);
-            if (bin == 0) {
-                u32 r = zc + __popc(zm & ((1u << lane) - 1u));
-                v32[p] = __uint_as_float((u32)ld_le(A.a + unp_base + 4ull * r, 4));
-            }
-            zc += __popc(zm);
+            u32 before, total;
+            gscan(bin == 0, before, total);
+            if (bin == 0) v32[p] = __uint_as_float((u32)ld_le(A.a + unp_base + 4ull * (zc + before), 4));
+            zc += total;
         }
-        __syncwarp();
+        gsync();
         if (kind == 1) {
             float4 cf = load_coef(A.a, A.rec_off[b]);
             double c0 = (double)cf.x, c1 = (double)cf.y, c2 = (double)cf.z, c3 = (double)cf.w;
-            for (int p = lane; p < vol; p += 32) {
+            for (int p = lane; p < vol; p += G) {
                 u32 bin = A.bins[bins_index(g, b, p)];
                 if (bin) {
                     u32 c = __ldg(crd + p);
@@ -802,12 +839,12 @@ __global__ void __launch_bounds__(128) k_recon_warp(DecArgs A, int mode) {
             {
                 const uint4* src = (const uint4*)(A.bins + bins_index(g, b, 0));
                 const int nch = (vol + 7) >> 3;
-                for (int c = lane; c < nch; c += 32) ((uint4*)sb)[c] = __ldg(src + c);
-                __syncwarp();
+                for (int c = lane; c < nch; c += G) ((uint4*)sb)[c] = __ldg(src + c);
+                gsync();
             }
             for (int s = 0; s < PL.nplanes; s++) {
                 int q0 = __ldg(planes + s), q1 = __ldg(planes + s + 1);
-                for (int q = q0 + lane; q < q1; q += 32) {
+                for (int q = q0 + lane; q < q1; q += G) {
                     int p = __ldg(wave + q);
                     u32 c = __ldg(wcrd + q);
                     int i = c & 0xff, j = (c >> 8) & 0xff, k = c >> 16;
@@ -829,14 +866,14 @@ __global__ void __launch_bounds__(128) k_recon_warp(DecArgs A, int mode) {
                     }
                     xd[p] = f32_to_f64(v);
                 }
-                __syncwarp();
+                gsync();
             }
         }
-        __syncwarp();
+        gsync();
         int f0 = (!mode && A.n_faults) ? A.fault_first[b] : -1;
         u64 s = 0;
         long long base = ((B.bi * g.e) * g.ny + B.bj * g.e) * g.nz + B.bk * g.e;
-        for (int p = lane; p < vol; p += 32) {
+        for (int p = lane; p < vol; p += G) {
             float v = v32[p];
             if (f0 >= 0) v = apply_decomp_faults(A, b, p, f0, v);
             s += __float_as_uint(v);
@@ -851,7 +888,7 @@ __global__ void __launch_bounds__(128) k_recon_warp(DecArgs A, int mode) {
                 A.out[base + ((long long)i * g.ny + j) * g.nz + k] = v;
             }
         }
-        s = warp_sum_u64(s);
+        s = gsum(s);
         if (lane == 0) {
             bool has = A.info[DI_HAS_SDC] != 0;
             u64 stored = has ? ld_le(A.a + A.info[DI_SDC_OFF] + 8ull * (u64)b, 8) : 0;
@@ -861,7 +898,7 @@ __global__ void __launch_bounds__(128) k_recon_warp(DecArgs A, int mode) {
                 A.mis_list[atomicAdd(&A.counters[DC_NMIS], 1u)] = (u32)b;
             }
         }
-        __syncwarp();
+        gsync();
     }
 }
 
