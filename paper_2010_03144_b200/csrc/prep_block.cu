@@ -51,6 +51,19 @@ struct PWalk {
         j = rp - i * by;
         t = (i * tye + j) * tz + zoff + k;
     }
+    // d <= bz: at most one row carry (branch-free)
+    FTLZ_DEV void step1(int d, int by, int bz, int tjump, int ijump) {
+        k += d;
+        t += d;
+        const bool w = k >= bz;
+        k -= w ? bz : 0;
+        t += w ? tjump : 0;
+        j += (int)w;
+        const bool w2 = j == by;
+        j = w2 ? 0 : j;
+        i += (int)w2;
+        t += w2 ? ijump : 0;
+    }
     FTLZ_DEV void step(int d, int by, int bz, int tjump, int ijump) {
         k += d;
         t += d;
@@ -189,7 +202,8 @@ __global__ void __launch_bounds__(768, 1) k_prep(const __grid_constant__ CompArg
                     prep_visit(tile, w, start + j8, cv, acc, r);
 #pragma unroll 2
                     for (int p = start + j8 + 8; p < start + len8; p += 8) {
-                        w.step(8, by, bz, tjump, ijump);
+                        if (bz >= 8) w.step1(8, by, bz, tjump, ijump);
+                        else w.step(8, by, bz, tjump, ijump);
                         double t4[4];
                         prep_visit(tile, w, p, cv, acc, t4);
 #pragma unroll
