@@ -164,3 +164,21 @@ def test_thread_argument_is_deterministic():
     a, _ = F.compress(F.Field.from_array(x), F.ErrorBound.absolute(1e-3), threads=1)
     b, _ = F.compress(F.Field.from_array(x), F.ErrorBound.absolute(1e-3), threads=8)
     assert F.serialize(a) == F.serialize(b)
+
+
+# ---- BASELINE.json configurations at full size: archive and output hashes of the reference's
+#      own runs (tools/make_golden.py --large), generated from the same seeded fields
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c1", "c4", "c2", "c2_1e-4", "c3"])
+def test_full_size_configs_match_reference_hashes(name):
+    from tools import synth
+
+    ent = manifest()["large"][name]
+    x = synth.field(name)
+    assert sha(x) == ent["input_sha256"]
+    mode, value = synth.CONFIGS[name]["eb"]
+    data = F.compress_bytes(x, mode, value)
+    assert len(data) == ent["archive_len"]
+    assert sha(np.frombuffer(data, np.uint8)) == ent["archive_sha256"]
+    y = F.decompress_bytes(data)
+    assert sha(y) == ent["output_sha256"]
