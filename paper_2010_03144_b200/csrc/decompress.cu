@@ -466,6 +466,11 @@ FTLZ_DEV u32 br_word(const BitReader& R, u32 n, u32 raw) {
 }
 FTLZ_DEV u32 br_load(const BitReader& R, u32 n) { return n <= R.endw && (n < R.endw || R.emask) ? __ldg(R.w + n) : 0u; }
 
+// L2 prefetch of the 128-byte line holding word n of the slice (no register, no scoreboard)
+FTLZ_DEV void br_prefetch(const BitReader& R, u32 n) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(R.w + n));
+}
+
 // position the window at relative bit `pos`
 FTLZ_DEV void br_seek(BitReader& R, u32 pos) {
     const u32 n = pos >> 5;
@@ -488,8 +493,20 @@ FTLZ_DEV u32 br_init(BitReader& R, const u8* a, u64 start, u64 end) {
     R.endw = (u32)(rend >> 5);
     R.emask = (rend & 31) ? (0xffffffffu << (32 - (u32)(rend & 31))) : 0u;
     const u32 pos = (u32)(start & 31);
+    // the first lines of the slice go to L2 now; later lines are prefetched as the reader
+    // crosses line boundaries (br_consume)
+    for (u32 n = 32; n < 96u && n <= R.endw; n += 32) br_prefetch(R, n);
     br_seek(R, pos);
     return pos;
+}
+
+// predicated load: lanes with !p keep `v` (no divergent branch around the refill)
+FTLZ_DEV u32 ldg_pred(const u32* ptr, bool p, u32 v) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.u32 %0, [%1];\n\t}"
+        : "+r"(v)
+        : "l"(ptr), "r"((u32)p));
+    return v;
 }
 
 FTLZ_DEV void br_consume(BitReader& R, int l) {
@@ -499,10 +516,11 @@ FTLZ_DEV void br_consume(BitReader& R, int l) {
     const u32 v = br_word(R, R.nw, R.raw);
     R.win |= need ? ((u64)v << (32 - R.have)) : 0ull;
     R.have += need ? 32 : 0;
-    if (need) {
-        R.nw++;
-        R.raw = br_load(R, R.nw);
-    }
+    R.nw += need ? 1u : 0u;
+    // next word (zero past the slice); a lane entering a new line prefetches two lines ahead
+    const bool inside = R.nw <= R.endw && (R.nw < R.endw || R.emask);
+    R.raw = ldg_pred(R.w + R.nw, need && inside, need ? 0u : R.raw);
+    if (need && (R.nw & 31u) == 0u && R.nw + 64u <= R.endw) br_prefetch(R, R.nw + 64u);
 }
 
 // 64 bits at relative position pos (slow path)
@@ -662,7 +680,8 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
         }
         __syncwarp();
     }
-    const u32 st_sa = smem_u32(stage + lane * e);
+    u32 st_sa;
+    asm volatile("mov.u32 %0, %1;" : "=r"(st_sa) : "r"(smem_u32(stage + lane * e)));   // keep in a register
     int i = 0, j = 0;
     for (int r = 0; r < e * e; r++) {
         const bool act = valid && !err && i < B.bx && j < B.by;
@@ -685,15 +704,13 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
                 }
                 consumed += (u32)l;
                 const int p = pbase + k;
+                // reconstruction on every lane (branch-free; Lorenzo lanes discard it)
+                const double pred = __dadd_rn(ab, __dmul_rn(c3, int_to_f64(k)));
+                float v = __double2float_rn(__dadd_rn(pred, __dmul_rn(twoeb, int_to_f64((int)sym - center))));
+                if (sym == 0u && recon_here)
+                    v = zeros < nunp ? __uint_as_float((u32)ld_le(A.a + unp_base + 4ull * zeros, 4)) : 0.0f;
+                if (f0 >= 0 && recon_here) v = apply_decomp_faults(A, b, p, f0, v);
                 if (recon_here) {
-                    float v;
-                    if (sym) {
-                        const double pred = __dadd_rn(ab, __dmul_rn(c3, int_to_f64(k)));
-                        v = __double2float_rn(__dadd_rn(pred, __dmul_rn(twoeb, int_to_f64((int)sym - center))));
-                    } else {
-                        v = zeros < nunp ? __uint_as_float((u32)ld_le(A.a + unp_base + 4ull * zeros, 4)) : 0.0f;
-                    }
-                    if (f0 >= 0) v = apply_decomp_faults(A, b, p, f0, v);
                     dsum += __float_as_uint(v);
                     asm volatile("st.shared.f32 [%0], %1;" ::"r"(st_sa + 4u * (u32)k), "f"(v) : "memory");
                 } else {

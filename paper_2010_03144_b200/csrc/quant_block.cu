@@ -137,14 +137,70 @@ FTLZ_DEV u32 reg_point_fast(const QuantParams& Q, float x32, double ab, double a
     return keep ? (u32)bin : 0u;
 }
 
+// one step of the point walk (branch-free): k, then the row (j), then i
+template <bool FULLJ>
+FTLZ_DEV void reg_step(RegPos& P, const RegBlk& K) {
+    P.k++;
+    P.t++;
+    const bool w = P.k == K.bz;
+    P.k = w ? 0 : P.k;
+    P.t += w ? K.tjump : 0;
+    P.rp += (int)w;
+    if (!FULLJ) {
+        P.j += (int)w;
+        const bool w2 = P.j == K.by;
+        P.j = w2 ? 0 : P.j;
+        P.t += w2 ? K.ijump : 0;
+    }
+}
+
 // points [p0, pend) starting at position P; accumulates into acc.  FULLJ: the block spans the
 // tile's whole j extent (no i-step jump), true for all but the last block row of a ragged field.
+// Points go in groups of RB: all RB points' operands are loaded before any store of the group,
+// so the RB float64 dependency chains interleave (the bins / histogram stores would otherwise
+// order every point after the previous one's stores).
+#define RB 4
 template <bool DUP, bool PIN, bool FULLJ>
 FTLZ_DEV void reg_points(const QuantParams& Q, const RegBlk& K, RegPos P, int p0, int pend, int lane, u16* lh16,
                          u32* hwin, u32* ghist, int lhlo, int wlo, RegAcc& acc) {
     u32 flag = 0, outw = 0;
-#pragma unroll 4
-    for (int p = p0; p < pend; p++) {
+    int p = p0;
+    for (; p + RB <= pend; p += RB) {
+        float x[RB];
+        double ab[RB], ab2[RB], ck[RB];
+#pragma unroll
+        for (int u = 0; u < RB; u++) {
+            x[u] = K.tile[P.t];
+            ab[u] = K.abt[P.rp];
+            ab2[u] = DUP ? K.abt2[P.rp] : ab[u];
+            ck[u] = K.ctab[P.k];
+            reg_step<FULLJ>(P, K);
+        }
+        u32 fb[RB];
+        float r32[RB];
+#pragma unroll
+        for (int u = 0; u < RB; u++) {
+            u32 slow;
+            fb[u] = reg_point_fast<DUP>(Q, x[u], ab[u], ab2[u], ck[u], r32[u], slow);
+            flag |= slow;
+        }
+#pragma unroll
+        for (int u = 0; u < RB; u++) {
+            const u32 pu = (u32)(p + u);
+            if (PIN) {
+                const u32 xu = __float_as_uint(x[u]);
+                acc.cs += (u64)xu;
+                acc.csi += (u64)pu * (u64)xu;
+            }
+            K.bins16[p + u] = (u16)fb[u];
+            acc.bs += fb[u];
+            acc.bis += (u64)pu * (u64)fb[u];
+            acc.dc += (u64)__float_as_uint(r32[u]);
+            acc.nz += fb[u] == 0u;
+            lh_bump(lh16, lhlo, (int)fb[u], lane, outw);
+        }
+    }
+    for (; p < pend; p++) {
         const float x32 = K.tile[P.t];
         const double ab = K.abt[P.rp], ab2 = DUP ? K.abt2[P.rp] : ab;
         if (PIN) {
@@ -162,19 +218,7 @@ FTLZ_DEV void reg_points(const QuantParams& Q, const RegBlk& K, RegPos P, int p0
         acc.dc += (u64)__float_as_uint(r32);
         acc.nz += fb == 0u;
         lh_bump(lh16, lhlo, (int)fb, lane, outw);
-        // walk (branch-free): k, then the row (j), then i
-        P.k++;
-        P.t++;
-        const bool w = P.k == K.bz;
-        P.k = w ? 0 : P.k;
-        P.t += w ? K.tjump : 0;
-        P.rp += (int)w;
-        if (!FULLJ) {
-            P.j += (int)w;
-            const bool w2 = P.j == K.by;
-            P.j = w2 ? 0 : P.j;
-            P.t += w2 ? K.ijump : 0;
-        }
+        reg_step<FULLJ>(P, K);
     }
     acc.flagged = flag;
     acc.outwin = outw;
