@@ -200,14 +200,23 @@ __global__ void __launch_bounds__(768, 1) k_prep(const __grid_constant__ CompArg
                     PWalk w;
                     w.set_crd(__ldg(crd + start + j8), S.tye, S.tz, zoff);
                     prep_visit(tile, w, start + j8, cv, acc, r);
+                    if (bz >= 8) {   // at most one row carry per step (the loop-invariant test hoisted)
 #pragma unroll 2
-                    for (int p = start + j8 + 8; p < start + len8; p += 8) {
-                        if (bz >= 8) w.step1(8, by, bz, tjump, ijump);
-                        else w.step(8, by, bz, tjump, ijump);
-                        double t4[4];
-                        prep_visit(tile, w, p, cv, acc, t4);
+                        for (int p = start + j8 + 8; p < start + len8; p += 8) {
+                            w.step1(8, by, bz, tjump, ijump);
+                            double t4[4];
+                            prep_visit(tile, w, p, cv, acc, t4);
 #pragma unroll
-                        for (int q = 0; q < 4; q++) r[q] = __dadd_rn(r[q], t4[q]);
+                            for (int q = 0; q < 4; q++) r[q] = __dadd_rn(r[q], t4[q]);
+                        }
+                    } else {
+                        for (int p = start + j8 + 8; p < start + len8; p += 8) {
+                            w.step(8, by, bz, tjump, ijump);
+                            double t4[4];
+                            prep_visit(tile, w, p, cv, acc, t4);
+#pragma unroll
+                            for (int q = 0; q < 4; q++) r[q] = __dadd_rn(r[q], t4[q]);
+                        }
                     }
                 }
                 // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)): the lower lane is the left operand
