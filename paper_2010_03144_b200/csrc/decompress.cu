@@ -450,6 +450,12 @@ __global__ void __launch_bounds__(PT_THREADS) k_parse_tail(DecArgs A) {
 // arithmetic).  Bits at or beyond `end` read as zero (the reference pads the slice with zero
 // bytes, encode.py:214).  The next word is loaded one refill ahead so its latency overlaps
 // decoding.
+FTLZ_DEV u32 lds_u32(u32 addr) {
+    u32 v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
 struct BitReader {
     const u32* w;     // word 0: the word holding the block's first bit
     u32 endw;         // words [0, endw) are fully inside the slice
@@ -594,11 +600,6 @@ FTLZ_DEV void fail_block(const DecArgs& A, long long b, int kind, long long x, l
 #define DEC_WARPS 4
 #define MAXE 64
 
-FTLZ_DEV u32 lds_u32(u32 addr) {
-    u32 v;
-    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-    return v;
-}
 
 __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u32* list, int nlist) {
     if (dev_failed(A.st)) return;
@@ -682,13 +683,15 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
     }
     u32 st_sa;
     asm volatile("mov.u32 %0, %1;" : "=r"(st_sa) : "r"(smem_u32(stage + lane * e)));   // keep in a register
+    const bool anyf = A.n_faults != 0;
     int i = 0, j = 0;
     for (int r = 0; r < e * e; r++) {
         const bool act = valid && !err && i < B.bx && j < B.by;
         if (act) {
-            double ab = 0.0;
+            // every lane stages one word per point: the reconstructed float (regression blocks
+            // of the full path) or the bin (Lorenzo blocks, re-execution)
+            double ab = 0.0, dk = 0.0;
             if (recon_here) ab = __dadd_rn(__dadd_rn(c0, __dmul_rn(c1, int_to_f64(i))), __dmul_rn(c2, int_to_f64(j)));
-            const int pbase = (i * B.by + j) * B.bz;
             for (int k = 0; k < B.bz; k++) {
                 if (consumed > bl) { err = FTLZ_K_D_RAN_PAST; break; }
                 u32 ent = lds_u32(lut_sa + 4u * (u32)(R.win >> lsh));
@@ -703,24 +706,20 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
                     if (l == 0) { err = FTLZ_K_D_OUTSIDE; break; }
                 }
                 consumed += (u32)l;
-                const int p = pbase + k;
-                // reconstruction on every lane (branch-free; Lorenzo lanes discard it)
-                const double pred = __dadd_rn(ab, __dmul_rn(c3, int_to_f64(k)));
+                const double pred = __dadd_rn(ab, __dmul_rn(c3, dk));
+                dk = __dadd_rn(dk, 1.0);
                 float v = __double2float_rn(__dadd_rn(pred, __dmul_rn(twoeb, int_to_f64((int)sym - center))));
-                if (sym == 0u && recon_here)
-                    v = zeros < nunp ? __uint_as_float((u32)ld_le(A.a + unp_base + 4ull * zeros, 4)) : 0.0f;
-                if (f0 >= 0 && recon_here) v = apply_decomp_faults(A, b, p, f0, v);
-                if (recon_here) {
-                    dsum += __float_as_uint(v);
-                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(st_sa + 4u * (u32)k), "f"(v) : "memory");
-                } else {
-                    A.bins[bins_index(g, b, p)] = (u16)sym;
-                }
+                if (sym == 0u)
+                    v = (recon_here && zeros < nunp) ? __uint_as_float((u32)ld_le(A.a + unp_base + 4ull * zeros, 4)) : 0.0f;
+                if (anyf && f0 >= 0 && recon_here) v = apply_decomp_faults(A, b, (i * B.by + j) * B.bz + k, f0, v);
+                const u32 word = recon_here ? __float_as_uint(v) : sym;
+                dsum += recon_here ? (u64)word : 0ull;
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(st_sa + 4u * (u32)k), "r"(word) : "memory");
                 zeros += sym == 0;
             }
         }
+        __syncwarp();
         if (!mode_list) {
-            __syncwarp();
             unsigned hm = heads;
             while (hm) {
                 const int h = __ffs(hm) - 1;
@@ -731,8 +730,15 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
                     for (int o = lane; o < L; o += 32) A.out[base + o] = stage[h * e + o];
                 }
             }
-            __syncwarp();
         }
+        if (act && !recon_here) {
+            // bins of this row to scratch (Lorenzo blocks are reconstructed by k_recon_g, whose
+            // output overwrites the run copy above)
+            const u32* sw = (const u32*)stage + lane * e;
+            const int pbase = (i * B.by + j) * B.bz;
+            for (int k = 0; k < B.bz; k++) A.bins[bins_index(g, b, pbase + k)] = (u16)sw[k];
+        }
+        __syncwarp();
         if (++j == e) {
             j = 0;
             i++;
