@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define FTLZ_ABI_VERSION 1
+#define FTLZ_ABI_VERSION 2
 
 /* ---- status codes (errors.py:4-59) ------------------------------------------------------- */
 enum ftlz_status {
@@ -78,6 +78,8 @@ enum ftlz_kind {
     FTLZ_K_SUMDC_MISMATCH = 37,
     FTLZ_K_ORPHAN = 38,
     FTLZ_K_TRAILING = 39,          /* a = trailing byte count */
+    FTLZ_K_RLE_ODD = 40,           /* "run-length stream has odd length" (encode.py:302-303), no offset */
+    FTLZ_K_RLE_ZERO = 41,          /* "run-length stream has zero-length run" (encode.py:307-308) */
     /* decompression SDC detail (pipeline.py:565-577, encode.py:198-256) */
     FTLZ_K_D_PAST_END = 60,        /* "bit slice extends past payload end" */
     FTLZ_K_D_RAN_PAST = 61,        /* "code ran past block boundary" */
@@ -170,6 +172,9 @@ typedef struct ftlz_stream_info {
     int64_t sumdc_off;                 /* first of the 8 B sums, -1 if absent */
     int64_t n_regression, total_bits;
     int32_t max_code_len, has_sum_dc;
+    /* stored (backend-coded) lengths: == payload_len and 8*nb for codec 0; for codec 1 the
+     * run-length pair streams at payload_off / sumdc_off (payload_len is then the inverted length) */
+    int64_t payload_stored_len, sumdc_stored_len;
 } ftlz_stream_info;
 
 /* ---- library identity ---------------------------------------------------------------------- */
@@ -246,6 +251,13 @@ int ftlz_ctx_decompress_region_host(ftlz_ctx* ctx, const uint8_t* h_archive, siz
                                     float* h_out, int32_t reuse_parsed, ftlz_report* report);
 /* blocks a region extraction decodes (pipeline.py:798-810) */
 int64_t ftlz_intersecting_block_count(int64_t nx, int64_t ny, int64_t nz, int32_t block_edge, const int64_t* region);
+/* backend codec 1 (encode.py:287-312) on the device for host bytes: invert == 0 applies the
+ * run-length pairs, invert != 0 inverts them (FTLZ_ERR_CORRUPT_STREAM, kind FTLZ_K_RLE_ODD /
+ * FTLZ_K_RLE_ZERO, on a malformed stream).  *out_len receives the result length; when it
+ * exceeds `capacity` nothing usable is written and FTLZ_ERR_CAPACITY is returned (retry with
+ * a larger buffer).  serialize / stream materialisation use it for codec-1 streams. */
+int ftlz_ctx_rle_host(ftlz_ctx* ctx, const uint8_t* h_in, size_t n, int32_t invert, uint8_t* h_out,
+                      size_t capacity, size_t* out_len, ftlz_info* info);
 /* device archive -> device output */
 int ftlz_ctx_decompress_device(ftlz_ctx* ctx, const uint8_t* d_archive, size_t len,
                                const ftlz_header* hdr, float* d_out,

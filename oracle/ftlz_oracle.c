@@ -1003,3 +1003,29 @@ finish:
 }
 
 int oc_version(void) { return 1; }
+
+/* ---- backend codec 1 (encode.py:287-312): greedy (run <= 255, byte) pairs --------------- */
+int64_t oc_rle_apply(const uint8_t* in, int64_t n, uint8_t* out) {
+    int64_t o = 0, i = 0;
+    while (i < n) {
+        const uint8_t b = in[i];
+        int run = 1;
+        while (run < 255 && i + run < n && in[i + run] == b) run++;
+        out[o++] = (uint8_t)run;
+        out[o++] = b;
+        i += run;
+    }
+    return o;
+}
+
+/* decoded length; -1: odd length, -2: zero-length run (encode.py:300-311).  out may be NULL. */
+int64_t oc_rle_invert(const uint8_t* in, int64_t n, uint8_t* out) {
+    if (n % 2) return -1;
+    int64_t o = 0;
+    for (int64_t i = 0; i < n; i += 2) {
+        if (in[i] == 0) return -2;
+        if (out) memset(out + o, in[i + 1], in[i]);
+        o += in[i];
+    }
+    return o;
+}

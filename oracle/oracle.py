@@ -68,7 +68,8 @@ class StreamInfo(C.Structure):
                 ("payload_off", C.c_int64), ("payload_len", C.c_int64),
                 ("unpred_off", C.c_int64), ("n_unpred", C.c_int64), ("sumdc_off", C.c_int64),
                 ("n_regression", C.c_int64), ("total_bits", C.c_int64),
-                ("max_code_len", C.c_int32), ("has_sum_dc", C.c_int32)]
+                ("max_code_len", C.c_int32), ("has_sum_dc", C.c_int32),
+                ("payload_stored_len", C.c_int64), ("sumdc_stored_len", C.c_int64)]
 
 
 _lib = None
@@ -94,6 +95,10 @@ def lib():
                                   C.POINTER(C.c_size_t), C.POINTER(Report)]
         L.oc_compress.restype = C.c_int
         L.oc_free.argtypes = [C.c_void_p]
+        L.oc_rle_apply.argtypes = [C.c_void_p, C.c_int64, C.c_void_p]
+        L.oc_rle_apply.restype = C.c_int64
+        L.oc_rle_invert.argtypes = [C.c_void_p, C.c_int64, C.c_void_p]
+        L.oc_rle_invert.restype = C.c_int64
         L.oc_parse.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(StreamInfo), C.POINTER(Info)]
         L.oc_parse.restype = C.c_int
         L.oc_decompress.argtypes = [C.c_void_p, C.c_size_t, C.c_void_p, C.POINTER(Fault),
@@ -318,3 +323,24 @@ def decompress(data: bytes, faults=None, threads: int = 1):
     report = {"status": _status_of(lists, sdc), **lists,
               "detail": sdc_detail(rep.info) if sdc else ""}
     return (None if sdc else out), report
+
+
+def rle_apply(data: bytes) -> bytes:
+    """Backend codec 1 apply (encode.py:287-299)."""
+    data = bytes(data)
+    out = (C.c_uint8 * (2 * len(data) + 2))()
+    n = lib().oc_rle_apply(data or b"\x00", len(data), out)
+    return bytes(memoryview(out)[:n])
+
+
+def rle_invert(data: bytes) -> bytes:
+    """Backend codec 1 invert (encode.py:300-311); OracleError like the reference."""
+    data = bytes(data)
+    n = lib().oc_rle_invert(data or b"\x00", len(data), None)
+    if n == -1:
+        raise OracleError("CorruptStream", "run-length stream has odd length")
+    if n == -2:
+        raise OracleError("CorruptStream", "run-length stream has zero-length run")
+    out = (C.c_uint8 * max(1, n))()
+    lib().oc_rle_invert(data or b"\x00", len(data), out)
+    return bytes(memoryview(out)[:n])

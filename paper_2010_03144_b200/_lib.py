@@ -65,7 +65,8 @@ class StreamInfo(C.Structure):
                 ("payload_off", C.c_int64), ("payload_len", C.c_int64),
                 ("unpred_off", C.c_int64), ("n_unpred", C.c_int64), ("sumdc_off", C.c_int64),
                 ("n_regression", C.c_int64), ("total_bits", C.c_int64),
-                ("max_code_len", C.c_int32), ("has_sum_dc", C.c_int32)]
+                ("max_code_len", C.c_int32), ("has_sum_dc", C.c_int32),
+                ("payload_stored_len", C.c_int64), ("sumdc_stored_len", C.c_int64)]
 
 
 # every symbol the header declares; tests check the library exports all of them
@@ -77,7 +78,7 @@ EXPORTS = [
     "ftlz_ctx_archive_device", "ftlz_ctx_archive_host", "ftlz_ctx_copy_archive",
     "ftlz_ctx_parse_host", "ftlz_ctx_decompress_host", "ftlz_ctx_decompress_device",
     "ftlz_ctx_profile", "ftlz_ctx_profile_read", "ftlz_ctx_decompress_region_host",
-    "ftlz_intersecting_block_count",
+    "ftlz_intersecting_block_count", "ftlz_ctx_rle_host",
 ]
 
 _lib = None
@@ -133,6 +134,7 @@ def load():
         L.ftlz_ctx_decompress_region_host.argtypes = [vp, vp, sz, vp, vp, i32, PR]
         L.ftlz_intersecting_block_count.argtypes = [i64, i64, i64, i32, vp]
         L.ftlz_intersecting_block_count.restype = i64
+        L.ftlz_ctx_rle_host.argtypes = [vp, vp, sz, i32, vp, sz, C.POINTER(sz), C.POINTER(Info)]
         L.ftlz_ctx_profile.argtypes = [vp, i32]
         L.ftlz_ctx_profile_read.argtypes = [vp, C.c_char_p, sz, C.POINTER(dbl), C.POINTER(i64), i32]
         _lib = L

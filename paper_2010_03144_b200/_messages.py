@@ -1,6 +1,6 @@
 """Map ftlz_info (status, kind, offset, operands) to the reference exceptions and texts
 (errors.py:4-59; core.py:188-192; pipeline.py:343,477,490,565-577,673-707;
-encode.py:85-88,206-255; container.py:155-285)."""
+encode.py:85-88,206-255,297-312; container.py:155-285)."""
 
 from __future__ import annotations
 
@@ -56,6 +56,10 @@ def _corrupt(info, data: bytes) -> E.CorruptStream:
         msg = "orphan checksum payload"
     elif k == 39:
         msg = f"{info.a} trailing bytes"
+    elif k == 40:
+        return E.CorruptStream("run-length stream has odd length")
+    elif k == 41:
+        return E.CorruptStream("run-length stream has zero-length run")
     else:
         msg = f"malformed archive (kind {k})"
     return E.CorruptStream(msg, offset=off)

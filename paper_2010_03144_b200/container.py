@@ -93,13 +93,21 @@ class CompressedStream:
     def _materialize(self):
         data = object.__getattribute__(self, "_archive")
         sec = object.__getattribute__(self, "_sections")
+        if sec is None:   # codec 1 straight from compress: section map from a device parse
+            sec = _parse_sections(data)
+            object.__setattr__(self, "_sections", sec)
         nb = (-(-self.dims[0] // self.block_edge) * -(-self.dims[1] // self.block_edge)
               * -(-self.dims[2] // self.block_edge))
         mv = memoryview(data)
         pos = 55
         recs = []
         has = sec["has_sum_dc"]
-        sums = (np.frombuffer(data, "<u8", nb, sec["sumdc_off"]) if has else None)
+        c1 = object.__getattribute__(self, "codec_id") == 1
+        if has and c1:   # stored as run-length pairs
+            so = sec["sumdc_off"]
+            sums = np.frombuffer(rle_invert(mv[so:so + sec["sumdc_stored_len"]]), "<u8", nb)
+        else:
+            sums = (np.frombuffer(data, "<u8", nb, sec["sumdc_off"]) if has else None)
         unpack_tail = struct.Struct("<II").unpack_from
         for b in range(nb):
             ind = data[pos]
@@ -120,7 +128,10 @@ class CompressedStream:
         uo, nu = sec["unpred_off"], sec["n_unpred"]
         object.__setattr__(self, "records", tuple(recs))
         object.__setattr__(self, "code_lengths", code_lengths)
-        object.__setattr__(self, "payload", bytes(mv[po:po + pl]))
+        if c1:
+            object.__setattr__(self, "payload", rle_invert(mv[po:po + sec["payload_stored_len"]]))
+        else:
+            object.__setattr__(self, "payload", bytes(mv[po:po + pl]))
         object.__setattr__(self, "unpred_words", bytes(mv[uo:uo + 4 * nu]))
 
     # ---------------------------------------------------------------- reference helpers
@@ -146,7 +157,48 @@ class CompressedStream:
         return bool(self.records) and self.records[0].sum_dc is not None
 
 
-def _sections_from_report(rep, nb: int, store_sum_dc: bool) -> dict:
+def _rle(data, invert: bool) -> bytes:
+    """Backend codec 1 (encode.py:287-312) run on the device for host bytes."""
+    data = bytes(data)
+    L = _lib.load()
+    ctx = _lib.context()
+    cap = max(64, (4 if invert else 2) * len(data) + 64)
+    buf = data if data else b"\x00"
+    while True:
+        out = (C.c_uint8 * cap)()
+        n = C.c_size_t()
+        info = _lib.Info()
+        st = L.ftlz_ctx_rle_host(ctx, buf, len(data), int(invert), out, cap, C.byref(n), C.byref(info))
+        if st == 9 and n.value > cap:
+            cap = n.value + 64
+            continue
+        if st != 0:
+            raise_for_info(st, info, data)
+        return bytes(memoryview(out)[:n.value])
+
+
+def rle_apply(data) -> bytes:
+    return _rle(data, False)
+
+
+def rle_invert(data) -> bytes:
+    return _rle(data, True)
+
+
+def _parse_sections(data: bytes) -> dict:
+    L = _lib.load()
+    si = _lib.StreamInfo()
+    rep = _lib.Report()
+    rep.capacity = 0
+    st = L.ftlz_ctx_parse_host(_lib.context(), data, len(data), C.byref(si), C.byref(rep))
+    if st != 0:
+        raise_for_info(st, rep.info, data)
+    return _sections_from_info(si)
+
+
+def _sections_from_report(rep, nb: int, store_sum_dc: bool, codec_id: int = 0):
+    if codec_id == 1:
+        return None   # stored lengths are only in the archive: mapped on first access
     table = 9 * nb + 16 * rep.n_regression
     book = 55 + table
     pay_off = book + 4 + 5 * rep.n_symbols + 8
@@ -154,13 +206,15 @@ def _sections_from_report(rep, nb: int, store_sum_dc: bool) -> dict:
     unp_off = pay_off + pay_len
     return {"payload_off": pay_off, "payload_len": pay_len, "unpred_off": unp_off,
             "n_unpred": rep.n_unpredictable, "has_sum_dc": store_sum_dc,
-            "sumdc_off": unp_off + 4 * rep.n_unpredictable + 16}
+            "sumdc_off": unp_off + 4 * rep.n_unpredictable + 16,
+            "payload_stored_len": pay_len, "sumdc_stored_len": 8 * nb if store_sum_dc else 0}
 
 
 def _sections_from_info(si) -> dict:
     return {"payload_off": si.payload_off, "payload_len": si.payload_len,
             "unpred_off": si.unpred_off, "n_unpred": si.n_unpred,
-            "has_sum_dc": bool(si.has_sum_dc), "sumdc_off": si.sumdc_off}
+            "has_sum_dc": bool(si.has_sum_dc), "sumdc_off": si.sumdc_off,
+            "payload_stored_len": si.payload_stored_len, "sumdc_stored_len": si.sumdc_stored_len}
 
 
 def serialize(stream: CompressedStream) -> bytes:
@@ -168,8 +222,9 @@ def serialize(stream: CompressedStream) -> bytes:
     data = stream.__dict__.get("_archive")
     if data is not None:
         return data
-    if stream.codec_id != 0:
-        raise UnsupportedCodec(f"codec {stream.codec_id} is not on the B200 path")
+    if stream.codec_id not in (0, 1):
+        raise UnsupportedCodec(f"codec {stream.codec_id} is not registered")
+    code = rle_apply if stream.codec_id == 1 else bytes
     out = bytearray()
     out += _HEADER.pack(MAGIC, VERSION, stream.codec_id, stream.dims[0], stream.dims[1],
                         stream.dims[2], stream.block_edge, EB_MODE_CODES[stream.eb_mode],
@@ -184,13 +239,15 @@ def serialize(stream: CompressedStream) -> bytes:
     out += struct.pack("<I", len(stream.code_lengths))
     for sym in sorted(stream.code_lengths):
         out += struct.pack("<IB", sym, stream.code_lengths[sym])
-    out += struct.pack("<Q", len(stream.payload))
-    out += stream.payload
+    stored = code(stream.payload)
+    out += struct.pack("<Q", len(stored))
+    out += stored
     out += stream.unpred_words
     if stream.has_sum_dc():
         raw = b"".join(rec.sum_dc.to_bytes(8, "little") for rec in stream.records)
-        out += struct.pack("<QQ", len(raw), len(raw))
-        out += raw
+        stored = code(raw)
+        out += struct.pack("<QQ", len(raw), len(stored))
+        out += stored
     else:
         out += struct.pack("<QQ", 0, 0)
     return bytes(out)

@@ -20,6 +20,7 @@
 #include "quant_block.cu"
 #include "prep_block.cu"
 #include "encode.cu"
+#include "rle.cu"
 #include "decompress.cu"
 
 using namespace ftlz;
@@ -394,12 +395,20 @@ struct CompLayout {
     size_t enc, qp, lbbits, lbreg, lbunp;
     size_t cb_keys, cb_syms, cb_w, cb_parent, cb_lens;
     size_t bins, unp, fix, faults, ffirst, ovr, plan, lor;
+    size_t cjobs, tarc, tarc_cap, rle, rle_bound;   // codec 1
     size_t total;
 };
 
 static const size_t RESULT_BYTES = 512;
 
-static CompLayout comp_layout(const HostPlan& P, int cap, int64_t n_faults) {
+static size_t identity_bound(const HostPlan& P, int cap) {
+    const Geom& g = P.g;
+    const size_t N = (size_t)g.nx * (size_t)g.ny * (size_t)g.nz, nb = (size_t)g.nb;
+    const size_t nsym = std::min<size_t>((size_t)cap, N + 1);
+    return 55 + 25 * nb + 4 + 5 * nsym + 8 + (57 * N + 7) / 8 + 4 * N + 16 + 8 * nb + 64;
+}
+
+static CompLayout comp_layout(const HostPlan& P, int cap, int64_t n_faults, int codec) {
     const Geom& g = P.g;
     size_t nb = (size_t)g.nb, c = (size_t)cap;
     size_t ntiles = (nb + SCAN_TILE - 1) / SCAN_TILE + 1;
@@ -411,6 +420,7 @@ static CompLayout comp_layout(const HostPlan& P, int cap, int64_t n_faults) {
     L.lbflag = take(4 * ntiles);
     L.events = take(nb);
     L.fixed = take(nb);
+    L.cjobs = take(2 * sizeof(RleJob));
     L.zero_end = o;
     L.coef = take(16 * nb);
     L.insum = take(8 * nb);
@@ -443,6 +453,11 @@ static CompLayout comp_layout(const HostPlan& P, int cap, int64_t n_faults) {
     L.ovr = take(nb);
     L.lor = take(4 * nb);
     L.plan = take(P.bytes());
+    // codec 1: the identity archive is assembled here, then transcoded (rle.cu)
+    L.tarc_cap = codec == 1 ? identity_bound(P, cap) : 0;
+    L.tarc = take(L.tarc_cap);
+    L.rle_bound = codec == 1 ? std::max<size_t>((57 * (size_t)g.nx * g.ny * g.nz + 7) / 8, 8 * nb) : 0;
+    L.rle = take(codec == 1 ? rle_scratch_bytes(L.rle_bound) : 0);
     L.total = o;
     return L;
 }
@@ -451,7 +466,7 @@ extern "C" size_t ftlz_compress_workspace_size(int64_t nx, int64_t ny, int64_t n
     HostPlan P;
     if (!build_plan(nx, ny, nz, cfg->block_edge, P)) return 0;
     // faults enlarge the workspace (fix scratch); size for the faulted case
-    return comp_layout(P, (int)cfg->bin_capacity, 1).total;
+    return comp_layout(P, (int)cfg->bin_capacity, 1, cfg->codec_id).total;
 }
 
 extern "C" size_t ftlz_compress_bound(int64_t nx, int64_t ny, int64_t nz, const ftlz_config* cfg) {
@@ -459,7 +474,9 @@ extern "C" size_t ftlz_compress_bound(int64_t nx, int64_t ny, int64_t nz, const 
     if (nb < 0) return 0;
     size_t N = (size_t)nx * ny * nz;
     size_t nsym = std::min<size_t>(cfg->bin_capacity, N + 1);
-    return 55 + 25 * (size_t)nb + 4 + 5 * nsym + 8 + (57 * N + 7) / 8 + 4 * N + 16 + 8 * (size_t)nb + 64;
+    size_t b0 = 55 + 25 * (size_t)nb + 4 + 5 * nsym + 8 + (57 * N + 7) / 8 + 4 * N + 16 + 8 * (size_t)nb + 64;
+    // run-length pairs at most double the payload and the sum_dc section
+    return cfg->codec_id == 1 ? b0 + (57 * N + 7) / 8 + 8 * (size_t)nb : b0;
 }
 
 // faults sorted by block + per-block first index
@@ -528,13 +545,13 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     int cap = (int)cfg->bin_capacity;
     if (cap < 4 || (cap & (cap - 1))) return set_err(FTLZ_ERR_INVALID_ARGUMENT, "bin_capacity must be a power of two >= 4");
     if (cap > 65536) return set_err(FTLZ_ERR_INVALID_ARGUMENT, "bin_capacity > 65536 is not supported on the device path");
-    if (cfg->codec_id != 0) {
+    if (cfg->codec_id != 0 && cfg->codec_id != 1) {
         info_set(&rep->info, FTLZ_ERR_UNSUPPORTED_CODEC, 0, -1, -1, cfg->codec_id, 0);
-        return set_err(FTLZ_ERR_UNSUPPORTED_CODEC, "only codec 0 (identity) is on the device path");
+        return set_err(FTLZ_ERR_UNSUPPORTED_CODEC, "only codecs 0 (identity) and 1 (run-length) are on the device path");
     }
     int rc = validate_faults(P, faults, nf);
     if (rc) return rc;
-    CompLayout L = comp_layout(P, cap, nf);
+    CompLayout L = comp_layout(P, cap, nf, cfg->codec_id);
     if (ws_size < L.total) return set_err(FTLZ_ERR_CAPACITY, "workspace too small");
     KCfg K = kcfg_comp(g);
     if (std::max(K.pp_smem, std::max(K.qr_smem, K.lor_smem)) > 227 * 1024)
@@ -594,8 +611,9 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     A.enc = (u64*)(ws + L.enc);
     A.bins = (u16*)(ws + L.bins);
     A.unp_scratch = (u32*)(ws + L.unp);
-    A.out = d_out;
-    A.out_cap = out_cap;
+    const bool c1 = cfg->codec_id == 1;
+    A.out = c1 ? ws + L.tarc : d_out;   // codec 1: identity archive in scratch, transcoded below
+    A.out_cap = c1 ? L.tarc_cap : out_cap;
     CodebookScratch S;
     S.keys = (u64*)(ws + L.cb_keys); S.syms = (u32*)(ws + L.cb_syms); S.w = (u64*)(ws + L.cb_w);
     S.parent = (u32*)(ws + L.cb_parent); S.lens = ws + L.cb_lens;
@@ -644,6 +662,18 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     PF.mark("k_assemble", s);
     k_assemble<<<num_sms() * 2, 256, 0, s>>>(A, H);
     LCHK("k_assemble");
+    if (c1) {
+        RleJob* jp = (RleJob*)(ws + L.cjobs);
+        RleJob* js = jp + 1;
+        const RleScratch RS = rle_scratch(ws + L.rle, L.rle_bound);
+        PF.mark("k_rle", s);
+        k_c1_prefix<<<num_sms() * 2, 256, 0, s>>>(A, d_out, out_cap, jp);
+        rle_encode_launch(jp, L.rle_bound, RS, s);
+        k_c1_mid<<<num_sms() * 2, 256, 0, s>>>(A, d_out, out_cap, jp, js);
+        rle_encode_launch(js, L.rle_bound, RS, s);
+        k_c1_fin<<<1, 1, 0, s>>>(A, d_out, out_cap, jp, js);
+        LCHK("k_rle");
+    }
     CK(cudaGetLastError());
     PF.mark("", s);
     unsigned char hres_local[RESULT_BYTES];
@@ -738,11 +768,15 @@ struct DecLayout {
     size_t ind, recoff, unpc, bitlen, bofs, uofs, da, db, lor, mis;
     size_t lut, first, lcount, lbase, dsym, sortkeys, lba, lbb;
     size_t bins, faults, ffirst, plan, rlist;
+    size_t jobs, payscr, sdcscr, rle;   // codec 1
+    size_t pay_cap, sdc_cap, rle_bound;
     size_t total;
     long long nchunks, nsuper;
 };
 
-static DecLayout dec_layout(const HostPlan& P, size_t len, int cap, int64_t nf) {
+// codec 1 inverts the payload into a scratch of 8 bytes per point (a valid block never needs
+// more than 57 bits per point) and the sum_dc section into 8 bytes per block
+static DecLayout dec_layout(const HostPlan& P, size_t len, int cap, int64_t nf, int codec) {
     const Geom& g = P.g;
     size_t nb = (size_t)g.nb;
     DecLayout L;
@@ -756,6 +790,7 @@ static DecLayout dec_layout(const HostPlan& P, size_t len, int cap, int64_t nf) 
     L.lbflag = take(4 * ntiles);
     L.dflag = take(nb);
     L.mflag = take(nb);
+    L.jobs = take(2 * sizeof(RleJob));
     L.zero_end = o;
     L.maps = take(4 * 25 * (size_t)L.nchunks);
     L.smaps = take(4 * 25 * (size_t)L.nsuper);
@@ -783,6 +818,13 @@ static DecLayout dec_layout(const HostPlan& P, size_t len, int cap, int64_t nf) 
     L.ffirst = take(nf ? 4 * nb : 0);
     L.plan = take(P.bytes());
     L.rlist = take(4 * nb);
+    const size_t N = (size_t)g.nx * (size_t)g.ny * (size_t)g.nz;
+    L.pay_cap = codec == 1 ? 8 * N + 64 : 0;
+    L.sdc_cap = codec == 1 ? 8 * nb + 64 : 0;
+    L.rle_bound = codec == 1 ? len : 0;
+    L.payscr = take(L.pay_cap);
+    L.sdcscr = take(L.sdc_cap);
+    L.rle = take(codec == 1 ? rle_scratch_bytes(len) : 0);
     L.total = o;
     return L;
 }
@@ -790,7 +832,7 @@ static DecLayout dec_layout(const HostPlan& P, size_t len, int cap, int64_t nf) 
 extern "C" size_t ftlz_decompress_workspace_size(const ftlz_header* h, size_t len) {
     HostPlan P;
     if (!build_plan(h->nx, h->ny, h->nz, h->block_edge, P)) return 0;
-    return dec_layout(P, len, (int)std::min<uint32_t>(h->bin_capacity, 65536u), 1).total;
+    return dec_layout(P, len, (int)std::min<uint32_t>(h->bin_capacity, 65536u), 1, h->codec_id).total;
 }
 
 struct DecResult {
@@ -814,6 +856,8 @@ static void stream_info_fill(const ftlz_header* h, const u64* info, ftlz_stream_
     si->total_bits = (int64_t)info[DI_TOTAL_BITS];
     si->max_code_len = (int32_t)info[DI_MAXLEN];
     si->has_sum_dc = (int32_t)info[DI_HAS_SDC];
+    si->payload_stored_len = (int64_t)info[DI_PAY_STORED];
+    si->sumdc_stored_len = (int64_t)info[DI_SDC_STORED];
 }
 
 // parse (+ optionally decode) on the device; d_a must have >= 64 readable bytes past len
@@ -847,6 +891,9 @@ static DecArgs make_dec_args(const HostPlan& P, const DevPlan& D, const DecLayou
     A.bins = (u16*)(ws + L.bins);
     A.out = d_out;
     A.lb_flag = (u32*)(ws + L.lbflag); A.lb_a = (u64*)(ws + L.lba); A.lb_b = (u64*)(ws + L.lbb);
+    A.rle_pay = (RleJob*)(ws + L.jobs); A.rle_sdc = A.rle_pay + 1;
+    A.pay_scratch = ws + L.payscr; A.sdc_scratch = ws + L.sdcscr;
+    A.pay_cap = L.pay_cap; A.sdc_cap = L.sdc_cap;
 
     return A;
 }
@@ -863,7 +910,7 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     if (cap > 65536) return set_err(FTLZ_ERR_INVALID_ARGUMENT, "bin_capacity > 65536 is not supported on the device path");
     int rc = validate_faults(P, faults, nf);
     if (rc) return rc;
-    DecLayout L = dec_layout(P, len, cap, nf);
+    DecLayout L = dec_layout(P, len, cap, nf, h->codec_id);
     if (ws_size < L.total) return set_err(FTLZ_ERR_CAPACITY, "workspace too small");
     if ((rc = kernel_attrs_once())) return set_err(rc, "cudaFuncSetAttribute failed");
     DevPlan D;
@@ -897,7 +944,17 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     k_scan2<<<(unsigned)((g.nb + 1023) / 1024), 1024, 0, s>>>(A);
     LCHK("k_scan2");
     PF.mark("k_parse_tail", s);
-    k_parse_tail<<<1, PT_THREADS, 8192 * 8, s>>>(A);
+    if (h->codec_id == 1) {
+        // run-length backend: invert the payload, then the sum_dc section, between the phases
+        const RleScratch RS = rle_scratch(ws + L.rle, L.rle_bound);
+        k_parse_tail<<<1, PT_THREADS, 8192 * 8, s>>>(A, 1);
+        rle_decode_launch(A.rle_pay, L.rle_bound, RS, s);
+        k_parse_tail<<<1, PT_THREADS, 8192 * 8, s>>>(A, 2);
+        rle_decode_launch(A.rle_sdc, L.rle_bound, RS, s);
+        k_parse_tail<<<1, PT_THREADS, 8192 * 8, s>>>(A, 3);
+    } else {
+        k_parse_tail<<<1, PT_THREADS, 8192 * 8, s>>>(A, 0);
+    }
     LCHK("k_parse_tail");
     size_t dec_smem = ((size_t)4 << DEC_TBITS) + (size_t)DEC_WARPS * 32 * g.e * 4;
     size_t rslot = al16((size_t)g.vmax * 8) + al16((size_t)g.vmax * 4) + al16(2 * (size_t)g.nvmax8);
@@ -993,7 +1050,7 @@ static int region_core(const HostPlan& P, const DevPlan& D, const uint8_t* d_a, 
                        const int64_t* region, float* d_out, unsigned char* ws, ftlz_report* rep, cudaStream_t s) {
     const Geom& g = P.g;
     const int cap = (int)h->bin_capacity;
-    DecLayout L = dec_layout(P, len, cap, 0);
+    DecLayout L = dec_layout(P, len, cap, 0, h->codec_id);
     DecArgs A = make_dec_args(P, D, L, d_a, len, h, d_out, 0, ws);
     const int64_t e = g.e;
     std::vector<u32> ids;
@@ -1167,7 +1224,7 @@ struct HostBuf {
 struct ftlz_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
-    DevBuf ws, in, out, dws, arch, dout, plan;
+    DevBuf ws, in, out, dws, arch, dout, plan, rle;
     HostBuf h_arch, h_res;
     size_t arch_len = 0;
     bool arch_on_host = false;
@@ -1220,7 +1277,7 @@ extern "C" void ftlz_ctx_destroy(ftlz_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     c->ws.release(); c->in.release(); c->out.release(); c->dws.release(); c->arch.release();
-    c->dout.release(); c->plan.release(); c->h_arch.release(); c->h_res.release();
+    c->dout.release(); c->plan.release(); c->rle.release(); c->h_arch.release(); c->h_res.release();
     cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -1237,7 +1294,7 @@ static int ctx_compress(ftlz_ctx* c, const float* d_in, int64_t nx, int64_t ny, 
         info_set(&rep->info, rc, 0, -1, -1, 0, 0);
         return rc;
     }
-    CompLayout L = comp_layout(c->hp, (int)cfg->bin_capacity, nf);
+    CompLayout L = comp_layout(c->hp, (int)cfg->bin_capacity, nf, cfg->codec_id);
     if ((rc = c->ws.ensure(L.total))) return rc;
     size_t bound = ftlz_compress_bound(nx, ny, nz, cfg);
     if ((rc = c->out.ensure(bound))) return rc;
@@ -1326,7 +1383,7 @@ static int ctx_decompress(ftlz_ctx* c, const uint8_t* d_a, size_t len, const ftl
     c->prof.mark("d_host_prelude", c->stream);
     int rc = ctx_plan(c, hdr->nx, hdr->ny, hdr->nz, hdr->block_edge);
     if (rc) return rc;
-    DecLayout L = dec_layout(c->hp, len, (int)std::min<uint32_t>(hdr->bin_capacity, 65536u), nf);
+    DecLayout L = dec_layout(c->hp, len, (int)std::min<uint32_t>(hdr->bin_capacity, 65536u), nf, hdr->codec_id);
     if ((rc = c->dws.ensure(L.total))) return rc;
     return decompress_core(c->hp, &c->dp, d_a, len, hdr, d_out, faults, nf, (unsigned char*)c->dws.p, c->dws.n,
                            rep, si, decode, c->stream, (unsigned char*)c->h_res.p, &c->prof);
@@ -1406,6 +1463,38 @@ extern "C" int ftlz_ctx_decompress_device(ftlz_ctx* c, const uint8_t* d_archive,
 
 // ------------------------------------------------------------------------------------------
 // profiling (bench.py): per-kernel event timing accumulated across calls
+extern "C" int ftlz_ctx_rle_host(ftlz_ctx* c, const uint8_t* h_in, size_t n, int32_t invert, uint8_t* h_out,
+                                 size_t capacity, size_t* out_len, ftlz_info* info) {
+    if (!c || (!h_in && n) || !out_len) return set_err(FTLZ_ERR_INVALID_ARGUMENT, "null argument");
+    if (info) info_set(info, FTLZ_OK, 0, -1, -1, 0, 0);
+    cudaStream_t s = c->stream;
+    const size_t cap = capacity;
+    const size_t o_in = 0, o_out = al256(n + 64), o_job = o_out + al256(cap + 64), o_scr = o_job + 256;
+    int rc = c->rle.ensure(o_scr + rle_scratch_bytes(n));
+    if (rc) return rc;
+    unsigned char* base = (unsigned char*)c->rle.p;
+    RleJob* J = (RleJob*)(base + o_job);
+    if (n) CK(cudaMemcpyAsync(base + o_in, h_in, n, cudaMemcpyHostToDevice, s));
+    k_rle_setjob<<<1, 1, 0, s>>>(J, base + o_in, (u64)n, base + o_out, (u64)cap);
+    const RleScratch RS = rle_scratch(base + o_scr, n);
+    if (invert) rle_decode_launch(J, n, RS, s);
+    else rle_encode_launch(J, n, RS, s);
+    CK(cudaGetLastError());
+    RleJob hj;
+    CK(cudaMemcpyAsync(&hj, J, sizeof hj, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *out_len = (size_t)hj.out_len;
+    if (invert && (hj.flags & 3u)) {
+        const int k = (hj.flags & 1u) ? FTLZ_K_RLE_ODD : FTLZ_K_RLE_ZERO;
+        if (info) info_set(info, FTLZ_ERR_CORRUPT_STREAM, k, -1, -1, 0, 0);
+        return FTLZ_ERR_CORRUPT_STREAM;
+    }
+    if (hj.out_len > cap) return set_err(FTLZ_ERR_CAPACITY, "output buffer too small");
+    if (hj.out_len) CK(cudaMemcpyAsync(h_out, base + o_out, (size_t)hj.out_len, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return FTLZ_OK;
+}
+
 extern "C" int ftlz_ctx_profile(ftlz_ctx* c, int32_t enable) {
     std::lock_guard<std::mutex> g(c->mu);
     c->prof.on = enable != 0;

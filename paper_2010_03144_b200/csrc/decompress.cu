@@ -24,7 +24,7 @@ namespace ftlz {
 
 enum {
     DI_TABLE_END = 0, DI_BOOK_OFF, DI_NSYM, DI_MAXLEN, DI_PAY_OFF, DI_PAY_LEN, DI_UNP_OFF,
-    DI_NUNP, DI_SDC_OFF, DI_HAS_SDC, DI_TOTAL_BITS, DI_NREG, DI_T, DI_COUNT
+    DI_NUNP, DI_SDC_OFF, DI_HAS_SDC, DI_TOTAL_BITS, DI_NREG, DI_T, DI_PAY_STORED, DI_SDC_STORED, DI_COUNT
 };
 enum { DC_NLOR = 0, DC_NMIS, DC_TICKET, DC_MINFAIL, DC_COUNT };
 
@@ -74,6 +74,12 @@ struct DecArgs {
     u32* lb_flag;
     u64* lb_a;
     u64* lb_b;
+    // codec 1 (run-length): parse inverts the payload and the sum_dc section into these
+    RleJob* rle_pay;
+    RleJob* rle_sdc;
+    u8* pay_scratch;
+    u8* sdc_scratch;
+    u64 pay_cap, sdc_cap;
     // region extraction (pipeline.py:726-795): output window in field coordinates
     int region;               // 1: k_decode list mode reports failures like the full path
     int pad_r;
@@ -87,6 +93,14 @@ FTLZ_DEV u64 ld_le(const u8* p, int n) {
     u64 v = 0;
     for (int i = 0; i < n; i++) v |= (u64)p[i] << (8 * i);
     return v;
+}
+
+// the payload the decoder reads (codec 0: inside the archive; codec 1: the inverted copy) and
+// the byte offset of its first byte there; the raw sum_dc words likewise
+FTLZ_DEV const u8* pay_base(const DecArgs& A) { return A.codec ? A.pay_scratch : A.a; }
+FTLZ_DEV u64 pay_boff(const DecArgs& A) { return A.codec ? 0ull : A.info[DI_PAY_OFF]; }
+FTLZ_DEV u64 stored_sum_dc(const DecArgs& A, long long b) {
+    return ld_le((A.codec ? A.sdc_scratch : A.a + A.info[DI_SDC_OFF]) + 8ull * (u64)b, 8);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -296,7 +310,11 @@ __global__ void __launch_bounds__(1024) k_scan2(DecArgs A) {
 #define PT_THREADS 1024
 #define DEC_TBITS 12
 
-__global__ void __launch_bounds__(PT_THREADS) k_parse_tail(DecArgs A) {
+// phase 0: codec 0, everything.  Codec 1 runs three phases around the run-length inversions:
+// 1 stops after the stored payload was taken (its job is filled), 2 checks the inverted payload
+// and continues to the stored sum_dc section (its job is filled), 3 checks that inversion and
+// finishes.  Every phase re-validates the codebook (cheap) so the positions are recomputed.
+__global__ void __launch_bounds__(PT_THREADS) k_parse_tail(DecArgs A, int phase) {
     if (dev_failed(A.st)) return;
     extern __shared__ __align__(16) u64 pt_dyn[];  // 8192 keys
     __shared__ long long s_bad;
@@ -363,11 +381,29 @@ __global__ void __launch_bounds__(PT_THREADS) k_parse_tail(DecArgs A) {
         u64 plen = ld_le(a + pos, 8);
         pos += 8;
         if (plen > len - pos) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_TRUNCATED, pos, -1, FTLZ_F_PAYLOAD, 0, 0); return; }
-        if (A.codec != 0) { dev_fail(A.st, FTLZ_ERR_UNSUPPORTED_CODEC, 0, -1, -1, A.codec, 0, 0); return; }
+        if (A.codec != 0 && A.codec != 1) { dev_fail(A.st, FTLZ_ERR_UNSUPPORTED_CODEC, 0, -1, -1, A.codec, 0, 0); return; }
         u64 pay_off = pos;
         pos += plen;
+        u64 dlen = plen;   // payload length after the backend inversion
+        if (A.codec == 1) {
+            if (phase == 1) {
+                RleJob* J = A.rle_pay;
+                J->in = a + pay_off; J->n = plen; J->out = A.pay_scratch; J->cap = A.pay_cap; J->flags = 0; J->out_len = 0;
+                A.info[DI_PAY_OFF] = pay_off;
+                A.info[DI_PAY_STORED] = plen;
+                return;
+            }
+            const RleJob* J = A.rle_pay;
+            if (J->flags & 1u) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_RLE_ODD, -1, -1, 0, 0, 0); return; }
+            if (J->flags & 2u) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_RLE_ZERO, -1, -1, 0, 0, 0); return; }
+            dlen = J->out_len;
+        }
         u64 tb = A.info[DI_TOTAL_BITS];
-        if (tb / 8 > plen || (tb / 8 == plen && (tb & 7))) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_BITS_EXCEED, pos, -1, 0, 0, 0); return; }
+        if (tb / 8 > dlen || (tb / 8 == dlen && (tb & 7))) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_BITS_EXCEED, pos, -1, 0, 0, 0); return; }
+        if (A.codec == 1 && (tb + 7) / 8 + 8 > A.rle_pay->cap) {
+            dev_fail(A.st, FTLZ_ERR_CAPACITY, 0, -1, -1, (long long)tb, 0, 0);
+            return;
+        }
         u64 nunp = A.info[DI_NUNP];
         if (nunp > (len - pos) / 4) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_TRUNCATED, pos, -1, FTLZ_F_UNPRED, 0, 0); return; }
         u64 unp_off = pos;
@@ -382,24 +418,40 @@ __global__ void __launch_bounds__(PT_THREADS) k_parse_tail(DecArgs A) {
             if (stl > len - pos) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_TRUNCATED, pos, -1, FTLZ_F_SUMDC, 0, 0); return; }
             sdc_off = pos;
             pos += stl;
-            if (stl != raw) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_SUMDC_MISMATCH, pos, -1, 0, 0, 0); return; }
+            u64 rlen = stl;
+            if (A.codec == 1) {
+                if (phase == 2) {
+                    RleJob* J = A.rle_sdc;
+                    J->in = a + sdc_off; J->n = stl; J->out = A.sdc_scratch; J->cap = A.sdc_cap; J->flags = 0; J->out_len = 0;
+                    return;
+                }
+                const RleJob* J = A.rle_sdc;
+                if (J->flags & 1u) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_RLE_ODD, -1, -1, 0, 0, 0); return; }
+                if (J->flags & 2u) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_RLE_ZERO, -1, -1, 0, 0, 0); return; }
+                rlen = J->out_len;
+            }
+            if (rlen != raw) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_SUMDC_MISMATCH, pos, -1, 0, 0, 0); return; }
             has = 1;
         } else if (stl) {
             dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_ORPHAN, pos - 8, -1, 0, 0, 0);
             return;
         }
+        if (A.codec == 1 && phase == 2) return;   // no sum_dc section to invert
         if (pos != len) { dev_fail(A.st, FTLZ_ERR_CORRUPT_STREAM, FTLZ_K_TRAILING, pos, -1, (long long)(len - pos), 0, 0); return; }
+        A.info[DI_PAY_STORED] = plen;
+        A.info[DI_SDC_STORED] = raw ? stl : 0;
         A.info[DI_BOOK_OFF] = e0 - 4;
         A.info[DI_NSYM] = nsym;
         A.info[DI_MAXLEN] = (u64)s_maxlen;
         A.info[DI_PAY_OFF] = pay_off;
-        A.info[DI_PAY_LEN] = plen;
+        A.info[DI_PAY_LEN] = dlen;
         A.info[DI_UNP_OFF] = unp_off;
         A.info[DI_SDC_OFF] = sdc_off;
         A.info[DI_HAS_SDC] = has;
     }
     __syncthreads();
     if (dev_failed(A.st)) return;
+    if (A.codec == 1 && phase != 3) return;
     // canonical order (length, symbol); symbols are strictly increasing already
     int n = (int)nsym;
     int np2 = 1;
@@ -636,7 +688,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
     const BlockInfo B = block_info(g, valid ? b : 0);
     const int kind = valid ? A.ind[b] : 0;
     const bool recon_here = valid && kind == 1 && !mode_list;
-    const u64 pay_off = A.info[DI_PAY_OFF], pay_len = A.info[DI_PAY_LEN];
+    const u64 pay_off = pay_boff(A), pay_len = A.info[DI_PAY_LEN];
     const u32 bl = valid ? A.bitlen[b] : 0;
     const u64 rel = valid ? A.bofs[b] : 0;
     int err = 0;
@@ -645,7 +697,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
     if (valid && last_byte > pay_len) err = FTLZ_K_D_PAST_END;
     BitReader R;
     const u64 start = pay_off * 8 + rel;
-    const u32 pos0 = br_init(R, A.a, valid && !err ? start : 0, valid && !err ? (pay_off + last_byte) * 8 : 0);
+    const u32 pos0 = br_init(R, pay_base(A), valid && !err ? start : 0, valid && !err ? (pay_off + last_byte) * 8 : 0);
     u32 consumed = 0;
     u32 zeros = 0;
     const u32 nunp = valid ? A.unpc[b] : 0;
@@ -752,7 +804,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
         return;
     }
     if (recon_here && A.info[DI_HAS_SDC]) {
-        const u64 stored = ld_le(A.a + A.info[DI_SDC_OFF] + 8ull * (u64)b, 8);
+        const u64 stored = stored_sum_dc(A, b);
         if (stored != dsum) {
             A.mflag[b] = 1;
             A.mis_list[atomicAdd(&A.counters[DC_NMIS], 1u)] = (u32)b;
@@ -914,7 +966,7 @@ __global__ void __launch_bounds__(128) k_recon_g(DecArgs A, int mode) {
         s = gsum(s);
         if (lane == 0) {
             bool has = A.info[DI_HAS_SDC] != 0;
-            u64 stored = has ? ld_le(A.a + A.info[DI_SDC_OFF] + 8ull * (u64)b, 8) : 0;
+            u64 stored = has ? stored_sum_dc(A, b) : 0;
             if (reexec) A.mflag[b] = (has && stored != s) ? 3 : 2;
             else if (has && stored != s) {
                 A.mflag[b] = 1;

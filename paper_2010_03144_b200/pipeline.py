@@ -157,7 +157,7 @@ def compress(field: Field, eb_spec: ErrorBound, cfg: FtConfig = FtConfig(), thre
     data, rep = _compress_array(values, eb_spec, cfg, predictor_override, faults, grid)
     nb = grid.n_blocks
     r = rep.r
-    stream = CompressedStream._from_archive(data, _sections_from_report(r, nb, cfg.store_sum_dc))
+    stream = CompressedStream._from_archive(data, _sections_from_report(r, nb, cfg.store_sum_dc, cfg.codec_id))
     ic, bc, dm, _ = rep.lists()
     return stream, FtReport(input_corrected=ic, bins_corrected=bc, dup_mismatch_resolved=dm)
 

@@ -44,7 +44,7 @@ def test_library_loads_and_exports_every_symbol():
     L = _lib.load()
     for name in _header_functions():
         assert hasattr(L, name), name
-    assert L.ftlz_abi_version() == 1
+    assert L.ftlz_abi_version() == 2
 
 
 def test_default_config_matches_reference_defaults():

@@ -63,3 +63,23 @@ def test_oracle_parse_and_sdc_match_reference(src, name):
     for k in ("status", "decomp_block_reexecuted", "detail"):
         assert rep[k] == e["decompress_report"][k], k
     assert (None if out is None else sha(out)) == e["output_sha256"]
+
+
+def test_oracle_rle_matches_reference_vectors():
+    """Backend codec 1 restatement (oracle) against the reference's own _rle_apply output."""
+    z = load("rle_vectors")
+    names = sorted(k[3:] for k in z.files if k.startswith("in_"))
+    assert len(names) >= 9
+    for k in names:
+        src, want = z[f"in_{k}"].tobytes(), z[f"out_{k}"].tobytes()
+        assert O.rle_apply(src) == want, k
+        assert O.rle_invert(want) == src, k
+
+
+def test_oracle_rle_invert_errors():
+    with pytest.raises(O.OracleError) as ei:
+        O.rle_invert(b"\x01\x02\x03")
+    assert str(ei.value) == "run-length stream has odd length"
+    with pytest.raises(O.OracleError) as ei:
+        O.rle_invert(b"\x01\x02\x00\x05")
+    assert str(ei.value) == "run-length stream has zero-length run"

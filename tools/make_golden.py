@@ -276,12 +276,85 @@ def main():
     ap.add_argument("--only", default=None)
     ap.add_argument("--region", action="store_true", help="region-extraction fixtures only")
     ap.add_argument("--campaign", action="store_true", help="fault-campaign fixtures only")
+    ap.add_argument("--codec", action="store_true", help="backend codec 1 (run-length) fixtures only")
     args = ap.parse_args()
     os.makedirs(OUT, exist_ok=True)
     mpath = os.path.join(OUT, "manifest.json")
     manifest = json.load(open(mpath)) if os.path.exists(mpath) else {"cases": {}, "corrupt": {}, "large": {}}
     manifest["generator"] = {"numpy": np.__version__, "ftlz": ftlz.__version__,
                              "script": "tools/make_golden.py"}
+    if args.codec:
+        # backend codec 1 (encode.py:287-312) through serialize/parse (container.py:134-145,241-262)
+        from ftlz import encode as ENC
+
+        rng = np.random.default_rng(123)
+        vecs = {"empty": b"", "one": b"\x07", "run255": b"\x00" * 255, "run256": b"\x00" * 256,
+                "run510": b"\xab" * 510, "run1000": b"\x01" * 1000,
+                "mixed": bytes(rng.integers(0, 3, 5000, dtype=np.uint8)),
+                "random": bytes(rng.integers(0, 256, 20000, dtype=np.uint8)),
+                "blocks": b"".join(bytes([v]) * int(n) for v, n in zip(rng.integers(0, 256, 300),
+                                                                      rng.integers(1, 700, 300)))}
+        arrs = {}
+        for k, v in vecs.items():
+            arrs[f"in_{k}"] = np.frombuffer(v, np.uint8)
+            arrs[f"out_{k}"] = np.frombuffer(ENC.backend_apply(v, 1), np.uint8)
+        np.savez_compressed(os.path.join(OUT, "rle_vectors.npz"), **arrs)
+        cases = {}
+        S = ftlz.synth_field
+        A, R = "absolute", "value_range_relative"
+        specs = [("c1_constant_30", S("constant", (30, 30, 30), seed=1).values, A, 1e-3, {}),
+                 ("c1_mixed_24x20x22", S("mixed", (24, 20, 22), seed=3).values, A, 1e-2, {}),
+                 ("c1_noise_20_1e-6", S("noise", (20, 20, 20), seed=5).values, A, 1e-6, {}),
+                 ("c1_lognormal_32x32x48", np.exp(synth.grf((32, 32, 48), 2.5, 11)), R, 1e-3, {}),
+                 ("c1_unprot_13x11x10_e5", S("mixed", (13, 11, 10), seed=31).values, A, 1e-3,
+                  {"block_edge": 5, "protect_input": False, "protect_bins": False,
+                   "duplicate_eval": False, "store_sum_dc": False})]
+        for name, vals, mode, ebv, cfg in specs:
+            vals = np.ascontiguousarray(vals, np.float32)
+            cfg = dict(cfg, codec_id=1)
+            arch, crep, err = run_compress(vals, mode, ebv, cfg, [], None)
+            assert err is None, err
+            out, drep, derr = run_decompress(arch, [])
+            stream = ftlz.parse(arch)
+            # corrupt variants of the run-length sections
+            nb = len(stream.records)
+            table = sum(9 + (16 if r.predictor == 1 else 0) for r in stream.records)
+            poff = 55 + table + 4 + 5 * len(stream.code_lengths)      # u64 stored payload length
+            plen = int.from_bytes(arch[poff:poff + 8], "little")
+            corrupt = {}
+            b = bytearray(arch); b[poff:poff + 8] = (plen - 1).to_bytes(8, "little"); del b[poff + 8 + plen - 1]
+            corrupt["pay_odd"] = bytes(b)
+            b = bytearray(arch); b[poff + 8] = 0
+            corrupt["pay_zero"] = bytes(b)
+            b = bytearray(arch); b[poff:poff + 8] = (plen - 2).to_bytes(8, "little"); del b[poff + 8 + plen - 2:poff + 8 + plen]
+            corrupt["pay_short"] = bytes(b)
+            b = bytearray(arch); b[poff + 8] = 255
+            corrupt["pay_longrun"] = bytes(b)
+            if cfg.get("store_sum_dc", True):
+                soff = poff + 8 + plen + len(stream.unpred_words)   # (raw, stored) lengths
+                slen = int.from_bytes(arch[soff + 8:soff + 16], "little")
+                b = bytearray(arch); b[soff + 8:soff + 16] = (slen - 1).to_bytes(8, "little"); del b[soff + 16 + slen - 1]
+                corrupt["sdc_odd"] = bytes(b)
+                b = bytearray(arch); b[soff + 16] = 0
+                corrupt["sdc_zero"] = bytes(b)
+                b = bytearray(arch); b[soff + 16] = min(255, b[soff + 16] + 1)
+                corrupt["sdc_long"] = bytes(b)
+            cres = {}
+            for k, blob in corrupt.items():
+                o2, r2, e2 = run_decompress(blob, [])
+                cres[k] = {"error": e2, "report": r2, "output_sha256": None if o2 is None else sha(o2),
+                           "len": len(blob)}
+            np.savez_compressed(os.path.join(OUT, f"{name}.npz"), input=vals,
+                                archive=np.frombuffer(arch, np.uint8),
+                                output=np.zeros(0, np.float32) if out is None else out,
+                                **{f"corrupt_{k}": np.frombuffer(v, np.uint8) for k, v in corrupt.items()})
+            cases[name] = {"mode": mode, "value": ebv, "cfg": cfg, "archive_sha256": sha(np.frombuffer(arch, np.uint8)),
+                           "archive_len": len(arch), "output_sha256": None if out is None else sha(out),
+                           "compress_report": crep, "decompress_report": drep, "corrupt": cres}
+        manifest["codec1"] = cases
+        json.dump(manifest, open(mpath, "w"), indent=1, sort_keys=True)
+        print("codec1", list(cases))
+        return
     if args.campaign:
         # faults.run_trial / run_campaign (faults.py:143-367): every target, both protections
         from ftlz import faults as FT
