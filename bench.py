@@ -392,6 +392,17 @@ def run_ours(args, world, rank, local):
                               "overhead_decompress": (td_ms - to_d) / to_d,
                               "overhead_total": (step_ms - to_c - to_d) / (to_c + to_d)}
 
+    # ---- backend codec 1 (run-length pairs) on the same workload
+    if not args.quick and rank == 0:
+        c1 = F.FtConfig(codec_id=1)
+        a1, l1, _ = c_compress(c1)   # warm-up: the codec-1 workspace is allocated on first use
+        c_decompress(a1, l1)
+        torch.cuda.synchronize()
+        t1c, t1d, S1, _ = timed(c1, 3, profile=False)
+        line["codec1"] = {"compress_ms": sum(t1c) / len(t1c), "decompress_ms": sum(t1d) / len(t1d),
+                          "archive_bytes": int(S1), "note": "FtConfig(codec_id=1): payload and sum_dc "
+                          "stored as run-length pairs (encode.py:287-312), coded/inverted on the device"}
+
     # ---- e2e through the public API, pinned host buffers
     if rank == 0:
         xp = torch.from_numpy(x).pin_memory().numpy()

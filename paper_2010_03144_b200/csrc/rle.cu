@@ -76,28 +76,36 @@ FTLZ_DEV T cta_excl_suffix(T v, T init, Op op, T* s_w) {
     return ex;
 }
 
-// tile bytes [a - 1, a + RLE_TILE) into shared memory (coalesced), s[0] = byte a - 1
-FTLZ_DEV void rle_load_tile(const u8* in, u64 n, u64 a, u8* s) {
-    for (int k = threadIdx.x; k < RLE_TILE + 1; k += blockDim.x) {
-        const u64 i = a + (u64)k - 1;
-        s[k] = (k == 0 && a == 0) || i >= n ? 0 : in[i];
-    }
+// tile bytes [a - 1, a + RLE_TILE) into shared memory with aligned 16-byte loads; returns the
+// shift: byte a + k - 1 sits at s[shift + k].  The 16-byte chunks around the ends stay inside
+// the buffer's allocation (device buffers are 256-byte aligned and padded past their end).
+#define RLE_SBUF (RLE_TILE + 48)
+FTLZ_DEV int rle_load_tile(const u8* in, u64 n, u64 a, u8* s) {
+    const u8* lo = in + a - (a ? 1 : 0);
+    const u8* base = (const u8*)((uintptr_t)lo & ~(uintptr_t)15);
+    const u64 end = min(n, a + (u64)RLE_TILE);
+    const u64 nch = ((uintptr_t)(in + end) - (uintptr_t)base + 15) >> 4;
+    for (u64 c = threadIdx.x; c < nch; c += blockDim.x) ((uint4*)s)[c] = __ldg((const uint4*)base + c);
     __syncthreads();
+    return (int)((uintptr_t)lo - (uintptr_t)base) - (a ? 0 : 1);
 }
 
-FTLZ_DEV bool rle_start(const u8* s, u64 a, int k) { return (a == 0 && k == 0) || s[k + 1] != s[k]; }
+FTLZ_DEV bool rle_start(const u8* s, int sh, u64 a, int k) {
+    return (a == 0 && k == 0) || s[sh + k + 1] != s[sh + k];
+}
 
 // per tile: first and last run start (-1: none)
 __global__ void __launch_bounds__(RLE_TPB) k_rle_bounds(const RleJob* J, long long* tfirst, long long* tlast) {
-    __shared__ u8 s[RLE_TILE + 1];
+    __shared__ __align__(16) u8 s[RLE_SBUF];
     __shared__ long long s_w[8], s_t;
-    const u64 n = J->n, a = (u64)blockIdx.x * RLE_TILE;
-    if (a >= n) return;
-    rle_load_tile(J->in, n, a, s);
+    const u64 n = J->n;
+    for (u64 t = blockIdx.x; t * RLE_TILE < n; t += gridDim.x) {
+    const u64 a = t * RLE_TILE;
+    const int sh = rle_load_tile(J->in, n, a, s);
     long long f = RLE_LMAX, l = -1;
     const int k0 = threadIdx.x * RLE_BPT;
     for (int k = k0; k < k0 + RLE_BPT && a + k < n; k++)
-        if (rle_start(s, a, k)) {
+        if (rle_start(s, sh, a, k)) {
             if (f == RLE_LMAX) f = (long long)(a + k);
             l = (long long)(a + k);
         }
@@ -108,8 +116,10 @@ __global__ void __launch_bounds__(RLE_TPB) k_rle_bounds(const RleJob* J, long lo
     __syncthreads();
     cta_excl_scan<long long>(l, -1LL, mx, s_w, &s_t);
     if (threadIdx.x == 0) {
-        tfirst[blockIdx.x] = fmin;
-        tlast[blockIdx.x] = s_t;
+        tfirst[t] = fmin;
+        tlast[t] = s_t;
+    }
+    __syncthreads();
     }
 }
 
@@ -158,30 +168,32 @@ __global__ void __launch_bounds__(RLE_SCAN_T) k_rle_carry(const RleJob* J, const
 template <bool WRITE>
 __global__ void __launch_bounds__(RLE_TPB) k_rle_emit(RleJob* J, const long long* cs, const long long* ce, u64* tcount,
                                                       const u64* toff) {
-    __shared__ u8 s[RLE_TILE + 1];
+    __shared__ __align__(16) u8 s[RLE_SBUF];
+    __shared__ u8 st[WRITE ? 2 * RLE_TILE : 1];
     __shared__ long long s_w[8], s_t;
     __shared__ u64 s_wu[8], s_tu;
-    const u64 n = J->n, a = (u64)blockIdx.x * RLE_TILE;
-    if (a >= n) return;
-    rle_load_tile(J->in, n, a, s);
+    const u64 n = J->n;
+    for (u64 t = blockIdx.x; t * RLE_TILE < n; t += gridDim.x) {
+    const u64 a = t * RLE_TILE;
+    const int sh = rle_load_tile(J->in, n, a, s);
     const int k0 = threadIdx.x * RLE_BPT;
     const int k1 = (int)min((u64)(k0 + RLE_BPT), n - a > (u64)RLE_TILE ? (u64)RLE_TILE : n - a);
     long long f = RLE_LMAX, l = -1;
     for (int k = k0; k < k1; k++)
-        if (rle_start(s, a, k)) {
+        if (rle_start(s, sh, a, k)) {
             if (f == RLE_LMAX) f = (long long)(a + k);
             l = (long long)(a + k);
         }
     auto mn = [](long long x, long long y) { return x < y ? x : y; };
     auto mx = [](long long x, long long y) { return x > y ? x : y; };
-    const long long sb = cta_excl_scan<long long>(l, cs[blockIdx.x], mx, s_w, &s_t);   // run start before k0
-    const long long ea = cta_excl_suffix<long long>(f, ce[blockIdx.x], mn, s_w);        // next start at/after k1
+    const long long sb = cta_excl_scan<long long>(l, cs[t], mx, s_w, &s_t);   // run start before k0
+    const long long ea = cta_excl_suffix<long long>(f, ce[t], mn, s_w);        // next start at/after k1
     // ascending: emission mask (bit k - k0)
     u32 mask = 0;
     if (k0 < k1) {
         u32 m = (u32)(((long long)(a + k0) - sb) % 255);
         for (int k = k0; k < k1; k++) {
-            if (rle_start(s, a, k)) m = 0;
+            if (rle_start(s, sh, a, k)) m = 0;
             if (m == 0) mask |= 1u << (k - k0);
             m = m + 1 == 255 ? 0 : m + 1;
         }
@@ -190,25 +202,32 @@ __global__ void __launch_bounds__(RLE_TPB) k_rle_emit(RleJob* J, const long long
     auto add = [](u64 x, u64 y) { return x + y; };
     const u64 pre = cta_excl_scan<u64>(cnt, 0ull, add, s_wu, &s_tu);
     if (!WRITE) {
-        if (threadIdx.x == 0) tcount[blockIdx.x] = s_tu;
-        return;
+        if (threadIdx.x == 0) tcount[t] = s_tu;
+        __syncthreads();
+        continue;
     }
-    const u64 base = toff[blockIdx.x] + pre;
-    if (2 * (base + cnt) > J->cap) {
-        if (cnt) atomicOr(&J->flags, 4u);
-        return;
-    }
+    // pairs of the tile staged in shared memory (at most 2 bytes per input byte), then one
+    // coalesced copy to the tile's output range
+    const u64 tbase = toff[t], tpairs = s_tu;
+    u8* const out = J->out;
+    const bool fits = 2 * (tbase + tpairs) <= J->cap;
+    if (!fits && threadIdx.x == 0 && tpairs) atomicOr(&J->flags, 4u);
     long long nxt = ea;
     for (int k = k1 - 1; k >= k0; k--) {
         const long long i = (long long)(a + k);
         const long long e = nxt;
-        if (rle_start(s, a, k)) nxt = i;
+        if (rle_start(s, sh, a, k)) nxt = i;
         if ((mask >> (k - k0)) & 1u) {
-            const u64 r = base + (u64)__popc(mask & ((1u << (k - k0)) - 1u));
+            const u64 r = pre + (u64)__popc(mask & ((1u << (k - k0)) - 1u));
             const long long run = e - i < 255 ? e - i : 255;
-            J->out[2 * r] = (u8)run;
-            J->out[2 * r + 1] = s[k + 1];
+            st[2 * r] = (u8)run;
+            st[2 * r + 1] = s[sh + k + 1];
         }
+    }
+    __syncthreads();
+    if (fits)
+        for (u64 q = threadIdx.x; q < 2 * tpairs; q += blockDim.x) out[2 * tbase + q] = st[q];
+    __syncthreads();
     }
 }
 
@@ -242,8 +261,9 @@ __global__ void __launch_bounds__(RLE_SCAN_T) k_rle_offsets(RleJob* J, const u64
 // whether a zero run occurs
 __global__ void __launch_bounds__(RLE_TPB) k_rld_sums(RleJob* J, u64* tcount) {
     __shared__ u64 s_wu[8], s_tu;
-    const u64 n = J->n & ~1ull, a = (u64)blockIdx.x * RLE_TILE;
-    if (a >= n) return;
+    const u64 n = J->n & ~1ull;
+    for (u64 t = blockIdx.x; t * RLE_TILE < n; t += gridDim.x) {
+    const u64 a = t * RLE_TILE;
     u64 sum = 0;
     bool zero = false;
     for (u64 k = a + 2 * threadIdx.x; k < a + RLE_TILE && k < n; k += 2 * blockDim.x) {
@@ -254,25 +274,30 @@ __global__ void __launch_bounds__(RLE_TPB) k_rld_sums(RleJob* J, u64* tcount) {
     auto add = [](u64 x, u64 y) { return x + y; };
     cta_excl_scan<u64>(sum, 0ull, add, s_wu, &s_tu);
     if (__syncthreads_or(zero) && threadIdx.x == 0) atomicOr(&J->flags, 2u);
-    if (threadIdx.x == 0) tcount[blockIdx.x] = s_tu;
+    if (threadIdx.x == 0) tcount[t] = s_tu;
+    __syncthreads();
+    }
 }
 
 // decode: expand the pairs of each tile at their offsets (bytes past the capacity are dropped)
 __global__ void __launch_bounds__(RLE_TPB) k_rld_write(RleJob* J, const u64* toff) {
     __shared__ u64 s_wu[8], s_tu;
-    const u64 n = J->n & ~1ull, a = (u64)blockIdx.x * RLE_TILE;
-    if (a >= n) return;
+    const u64 n = J->n & ~1ull;
+    u8* const out = J->out;
+    const u64 cap = J->cap;
+    for (u64 t = blockIdx.x; t * RLE_TILE < n; t += gridDim.x) {
+    const u64 a = t * RLE_TILE;
     const u64 k0 = a + (u64)threadIdx.x * RLE_BPT;
     u64 sum = 0;
     for (u64 k = k0; k < k0 + RLE_BPT && k < n; k += 2) sum += J->in[k];
     auto add = [](u64 x, u64 y) { return x + y; };
-    u64 o = toff[blockIdx.x] + cta_excl_scan<u64>(sum, 0ull, add, s_wu, &s_tu);
-    const u64 cap = J->cap;
+    u64 o = toff[t] + cta_excl_scan<u64>(sum, 0ull, add, s_wu, &s_tu);
     for (u64 k = k0; k < k0 + RLE_BPT && k < n; k += 2) {
         const u32 r = J->in[k];
         const u8 v = J->in[k + 1];
-        for (u32 q = 0; q < r && o + q < cap; q++) J->out[o + q] = v;
+        for (u32 q = 0; q < r && o + q < cap; q++) out[o + q] = v;
         o += r;
+    }
     }
 }
 
@@ -296,8 +321,20 @@ static RleScratch rle_scratch(unsigned char* p, size_t n_bound) {
     return R;
 }
 
+// tile kernels loop over tiles (the job's length is only known on the device)
+static unsigned rle_grid(size_t n_bound) {
+    static int sms = 0;
+    if (!sms) {
+        int d = 0;
+        cudaGetDevice(&d);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
+        if (sms <= 0) sms = 148;
+    }
+    return (unsigned)std::min<size_t>(rle_tiles(n_bound), (size_t)sms * 8);
+}
+
 static void rle_encode_launch(RleJob* J, size_t n_bound, const RleScratch& R, cudaStream_t s) {
-    const unsigned nt = (unsigned)rle_tiles(n_bound);
+    const unsigned nt = rle_grid(n_bound);
     k_rle_bounds<<<nt, RLE_TPB, 0, s>>>(J, R.tfirst, R.tlast);
     k_rle_carry<<<1, RLE_SCAN_T, 0, s>>>(J, R.tfirst, R.tlast, R.cs, R.ce);
     k_rle_emit<false><<<nt, RLE_TPB, 0, s>>>(J, R.cs, R.ce, R.tcount, R.toff);
@@ -306,7 +343,7 @@ static void rle_encode_launch(RleJob* J, size_t n_bound, const RleScratch& R, cu
 }
 
 static void rle_decode_launch(RleJob* J, size_t n_bound, const RleScratch& R, cudaStream_t s) {
-    const unsigned nt = (unsigned)rle_tiles(n_bound);
+    const unsigned nt = rle_grid(n_bound);
     k_rld_sums<<<nt, RLE_TPB, 0, s>>>(J, R.tcount);
     k_rle_offsets<<<1, RLE_SCAN_T, 0, s>>>(J, R.tcount, R.toff, 1);
     k_rld_write<<<nt, RLE_TPB, 0, s>>>(J, R.toff);
