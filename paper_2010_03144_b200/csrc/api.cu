@@ -421,6 +421,7 @@ static CompLayout comp_layout(const HostPlan& P, int cap, int64_t n_faults, int 
     L.events = take(nb);
     L.fixed = take(nb);
     L.cjobs = take(2 * sizeof(RleJob));
+    L.cb_lens = take(c);   // code lengths (0: not in the alphabet), read whole by k_enc_len
     L.zero_end = o;
     L.coef = take(16 * nb);
     L.insum = take(8 * nb);
@@ -444,7 +445,6 @@ static CompLayout comp_layout(const HostPlan& P, int cap, int64_t n_faults, int 
     L.cb_syms = take(4 * c);
     L.cb_w = take(16 * c);
     L.cb_parent = take(8 * c);
-    L.cb_lens = take(c);
     L.bins = take(2 * nb * (size_t)g.nvmax8 + 64);
     L.unp = take(4 * nb * (size_t)g.vmax);
     L.fix = take(n_faults ? 4 * nb * (size_t)g.vmax : 0);
@@ -642,10 +642,11 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     k_zero<<<num_sms() * 4, 256, 0, s>>>(A);
     LCHK("k_zero");
     {
-        const int ew = (int)std::max<size_t>(1, std::min<size_t>(16, (227 * 1024 - 8 * ENC_WIN) / (4 * (size_t)g.nvmax8)));
-        const size_t esm = 8 * ENC_WIN + (size_t)ew * 4 * (size_t)g.nvmax8;
+        const size_t capal = ((size_t)cap + 15) & ~(size_t)15;
+        const int lw = (int)std::max<size_t>(1, std::min<size_t>(16, (227 * 1024 / 2 - capal) / (2 * (size_t)g.nvmax8)));
         PF.mark("k_enc_len", s);
-        k_enc_len<<<num_sms() * 2, 32 * ew, esm, s>>>(A, (const u32*)(ws + L.fix), (const u8*)(ws + L.fixed));
+        k_enc_len<<<num_sms() * 2, 32 * lw, capal + (size_t)lw * 2 * (size_t)g.nvmax8, s>>>(
+            A, (const u32*)(ws + L.fix), (const u8*)(ws + L.fixed), ws + L.cb_lens);
         LCHK("k_enc_len");
         unsigned ntiles = (unsigned)((g.nb + SCAN_TILE - 1) / SCAN_TILE);
         PF.mark("k_enc_scan", s);
@@ -653,7 +654,10 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
                                                 (u64*)(ws + L.lbunp));
         LCHK("k_enc_scan");
         PF.mark("k_enc_pack", s);
-        k_enc_pack<<<num_sms() * 2, 32 * ew, esm, s>>>(A, (const u32*)(ws + L.fix), (const u8*)(ws + L.fixed));
+        const int pw = (int)std::max<size_t>(1, std::min<size_t>(16, (227 * 1024 / 2 - 8 * ENC_WIN) /
+                                                                         (4 * (size_t)g.nvmax8 + 4 * ENC_STG)));
+        k_enc_pack<<<num_sms() * 2, 32 * pw, 8 * ENC_WIN + (size_t)pw * (4 * (size_t)g.nvmax8 + 4 * ENC_STG), s>>>(
+            A, (const u32*)(ws + L.fix), (const u8*)(ws + L.fixed));
         LCHK("k_enc_pack");
     }
     ftlz_header H;

@@ -26,6 +26,13 @@ struct EncWin {
         const u32 o = sym - (u32)wlo;
         return o < (u32)ENC_WIN ? s_enc[o] : (sym < (u32)cap ? __ldg(g_enc + sym) : 0ull);
     }
+    // window hit without a branch; symbols outside it (rare) take the global table
+    FTLZ_DEV u64 get_fast(u32 sym) const {
+        const u32 o = sym - (u32)wlo;
+        u64 e = s_enc[o < (u32)ENC_WIN ? o : 0u];
+        if (o >= (u32)ENC_WIN) e = sym < (u32)cap ? __ldg(g_enc + sym) : 0ull;
+        return e;
+    }
 };
 
 FTLZ_DEV void enc_fill_window(const CompArgs& A, u64* s_enc) {
@@ -81,29 +88,43 @@ FTLZ_DEV bool enc_prefetchable(const CompArgs& A, long long b, int vol, const u8
     return vol <= 1024 && !(A.events[b] & 8) && !(A.n_faults && A.fault_first[b] >= 0 && fixed_flag[b]);
 }
 
-template <bool FIXED>
-FTLZ_DEV u32 len_range(const EncWin& W, const u16* sym16, const u32* sym32, int p0, int pend, bool& range_err) {
+// code lengths of the symbols [p0, pend): a shared u8 table over the whole alphabet (no window
+// test); a length of 0 marks a symbol outside the codebook (pipeline.py:490)
+FTLZ_DEV u32 len_range(const u8* s_len, const u16* sym16, int p0, int pend, bool& range_err) {
+    u32 bits = 0, zero = 0;
+#pragma unroll 4
+    for (int p = p0; p < pend; p++) {
+        const u32 l = s_len[sym16[p]];
+        zero |= (u32)(l == 0u);
+        bits += l;
+    }
+    range_err |= zero != 0;
+    return bits;
+}
+// bins-faulted blocks: 32-bit words straight from fix_scratch (rare path)
+FTLZ_DEV u32 len_range_fixed(const u8* s_len, int cap, const u32* w, int p0, int pend, bool& range_err) {
     u32 bits = 0;
     for (int p = p0; p < pend; p++) {
-        const u32 sym = FIXED ? sym32[p] : (u32)sym16[p];
-        u32 l = (u32)(W.get(sym) & 63);
-        range_err |= l == 0;
+        const u32 sym = w[p];
+        const u32 l = sym < (u32)cap ? s_len[sym] : 0u;
+        range_err |= l == 0u;
         bits += l ? l : 1u;
     }
     return bits;
 }
 
-__global__ void __launch_bounds__(512) k_enc_len(CompArgs A, const u32* fix, const u8* fixed_flag) {
+__global__ void __launch_bounds__(512) k_enc_len(CompArgs A, const u32* fix, const u8* fixed_flag, const u8* lens) {
     extern __shared__ __align__(16) unsigned char smem[];
     if (dev_failed(A.st)) return;
     const Geom& g = A.g;
-    u64* s_enc = (u64*)smem;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    u16* sym16 = (u16*)(smem + 8 * ENC_WIN + (size_t)warp * 4 * g.nvmax8);
-    u32* sym32 = (u32*)sym16;
-    enc_fill_window(A, s_enc);
+    const int capal = (A.cap + 15) & ~15;
+    u8* s_len = smem;
+    u16* sym16 = (u16*)(smem + capal + (size_t)warp * 2 * g.nvmax8);
+    for (int t = threadIdx.x; t < capal / 16; t += blockDim.x)
+        ((uint4*)s_len)[t] = t * 16 + 16 <= A.cap ? __ldg((const uint4*)lens + t) : make_uint4(0, 0, 0, 0);
+    for (int t = (A.cap & ~15) + threadIdx.x; t < A.cap; t += blockDim.x) s_len[t] = lens[t];
     __syncthreads();
-    const EncWin W = {s_enc, A.enc, A.center - ENC_WIN / 2, A.cap};
     const long long NW = (long long)gridDim.x * nw;
     long long b = (long long)blockIdx.x * nw + warp;
     BinsPrefetch P;
@@ -118,10 +139,14 @@ __global__ void __launch_bounds__(512) k_enc_len(CompArgs A, const u32* fix, con
         u32 bits = 0;
         bool range_err = false;
         const bool bad = (A.events[b] & 8) != 0;
-        bool fixed = false;
-        if (!bad) {
+        const bool fixed = !bad && A.n_faults && A.fault_first[b] >= 0 && fixed_flag[b];
+        if (!bad && !fixed) {
             if (pf) P.store(sym16, lane);
-            else fixed = enc_stage(A, b, vol, fix, fixed_flag, sym16, sym32, lane);
+            else {
+                const int nch = (vol + 7) >> 3;
+                const uint4* src = (const uint4*)(A.bins + bins_index(g, b, 0));
+                for (int c = lane; c < nch; c += 32) ((uint4*)sym16)[c] = __ldg(src + c);
+            }
         }
         __syncwarp();
         const int cvol = vol;
@@ -134,8 +159,8 @@ __global__ void __launch_bounds__(512) k_enc_len(CompArgs A, const u32* fix, con
         if (!bad) {
             const int chunk = ((cvol + 31) >> 5) | 1;
             const int p0 = lane * chunk, pend = min(p0 + chunk, cvol);
-            if (fixed) bits = len_range<true>(W, sym16, sym32, p0, pend, range_err);
-            else bits = len_range<false>(W, sym16, sym32, p0, pend, range_err);
+            if (fixed) bits = len_range_fixed(s_len, A.cap, fix + (size_t)b * g.vmax, p0, pend, range_err);
+            else bits = len_range(s_len, sym16, p0, pend, range_err);
         }
         __syncwarp();
         u32 pre = bits;
@@ -233,6 +258,16 @@ FTLZ_DEV void enc_put(u32* words, u64 widx, u32 bits_be, bool shared_word) {
     else words[widx] = v;
 }
 
+// predicated form for the packing loop (no divergent branch): p_st plain store, p_or atomic OR
+FTLZ_DEV void enc_put_pred(u32* addr, u32 bits_be, bool p_st, bool p_or) {
+    const u32 v = __byte_perm(bits_be, 0, 0x0123);
+    asm volatile(
+        "{\n\t.reg .pred a, b;\n\tsetp.ne.u32 a, %2, 0;\n\tsetp.ne.u32 b, %3, 0;\n\t"
+        "@a st.global.u32 [%0], %1;\n\t@b red.global.or.b32 [%0], %1;\n\t}"
+        ::"l"(addr), "r"(v), "r"((u32)p_st), "r"((u32)p_or)
+        : "memory");
+}
+
 // MSB-first packing of symbols [p0, pend) starting at absolute bit gpos; FIXED: 32-bit symbols
 // of a bins-faulted block; LONG: some code is longer than 32 bits
 template <bool FIXED, bool LONG>
@@ -243,7 +278,7 @@ FTLZ_DEV void pack_range(const EncWin& W, const u16* sym16, const u32* sym32, in
     bool first = true;
     for (int p = p0; p < pend; p++) {
         const u32 sym = FIXED ? sym32[p] : (u32)sym16[p];
-        const u64 e = W.get(sym);
+        const u64 e = W.get_fast(sym);
         int l = (int)(e & 63);
         u64 code = e >> 6;
         if (LONG && l > 32) {
@@ -261,14 +296,64 @@ FTLZ_DEV void pack_range(const EncWin& W, const u16* sym16, const u32* sym32, in
         }
         acc |= code << (64 - nacc - l);
         nacc += l;
-        if (nacc >= 32) {
-            enc_put(words, widx++, (u32)(acc >> 32), first);
-            first = false;
-            acc <<= 32;
-            nacc -= 32;
-        }
+        // full word: store it (atomic OR for the lane's first word, shared with the lane or
+        // block before), predicated instead of branched
+        const bool full = nacc >= 32;
+        enc_put_pred(words + widx, (u32)(acc >> 32), full && !first, full && first);
+        first = first && !full;
+        widx += full ? 1 : 0;
+        acc = full ? acc << 32 : acc;
+        nacc -= full ? 32 : 0;
     }
     if (nacc > 0) enc_put(words, widx, (u32)(acc >> 32), true);
+}
+
+// the same packing into a warp's shared staging buffer (word 0 = the block's first payload
+// word); words shared between lanes are merged with shared-memory ORs
+#define ENC_STG 256
+FTLZ_DEV void put_s(u32 addr, u32 bits_be, bool p_st, bool p_or) {
+    const u32 v = __byte_perm(bits_be, 0, 0x0123);
+    asm volatile(
+        "{\n\t.reg .pred a, b;\n\tsetp.ne.u32 a, %2, 0;\n\tsetp.ne.u32 b, %3, 0;\n\t"
+        "@a st.shared.u32 [%0], %1;\n\t@b red.shared.or.b32 [%0], %1;\n\t}"
+        ::"r"(addr), "r"(v), "r"((u32)p_st), "r"((u32)p_or)
+        : "memory");
+}
+
+template <bool FIXED, bool LONG>
+FTLZ_DEV void pack_range_s(const EncWin& W, const u16* sym16, const u32* sym32, int p0, int pend, u32 pos, u32 sbase) {
+    u32 widx = pos >> 5;
+    u64 acc = 0;
+    int nacc = (int)(pos & 31);
+    bool first = true;
+    for (int p = p0; p < pend; p++) {
+        const u32 sym = FIXED ? sym32[p] : (u32)sym16[p];
+        const u64 e = W.get_fast(sym);
+        int l = (int)(e & 63);
+        u64 code = e >> 6;
+        if (LONG && l > 32) {
+            const int hl = l - 32;
+            acc |= (code >> 32) << (64 - nacc - hl);
+            nacc += hl;
+            const bool f1 = nacc >= 32;
+            put_s(sbase + 4u * widx, (u32)(acc >> 32), f1 && !first, f1 && first);
+            first = first && !f1;
+            widx += f1 ? 1u : 0u;
+            acc = f1 ? acc << 32 : acc;
+            nacc -= f1 ? 32 : 0;
+            code &= 0xffffffffull;
+            l = 32;
+        }
+        acc |= code << (64 - nacc - l);
+        nacc += l;
+        const bool full = nacc >= 32;
+        put_s(sbase + 4u * widx, (u32)(acc >> 32), full && !first, full && first);
+        first = first && !full;
+        widx += full ? 1u : 0u;
+        acc = full ? acc << 32 : acc;
+        nacc -= full ? 32 : 0;
+    }
+    if (nacc > 0) put_s(sbase + 4u * widx, (u32)(acc >> 32), false, true);
 }
 
 __global__ void __launch_bounds__(512) k_enc_pack(CompArgs A, const u32* fix, const u8* fixed_flag) {
@@ -279,6 +364,8 @@ __global__ void __launch_bounds__(512) k_enc_pack(CompArgs A, const u32* fix, co
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     u16* sym16 = (u16*)(smem + 8 * ENC_WIN + (size_t)warp * 4 * g.nvmax8);
     u32* sym32 = (u32*)sym16;
+    u32* stg = (u32*)(smem + 8 * ENC_WIN + (size_t)nw * 4 * g.nvmax8) + (size_t)warp * ENC_STG;
+    const u32 stg_sa = smem_u32(stg);
     enc_fill_window(A, s_enc);
     __syncthreads();
     const EncWin W = {s_enc, A.enc, A.center - ENC_WIN / 2, A.cap};
@@ -313,8 +400,27 @@ __global__ void __launch_bounds__(512) k_enc_pack(CompArgs A, const u32* fix, co
         if (bad) continue;
         const int chunk = ((vol + 31) >> 5) | 1;
         const int p0 = lane * chunk, pend = min(p0 + chunk, vol);
-        const u64 gpos = pay0 + A.bitoff[b] + A.lanepre[(size_t)b * 32 + lane];
-        if (p0 < pend) {
+        const u64 bpos = pay0 + A.bitoff[b];
+        const u64 gpos = bpos + A.lanepre[(size_t)b * 32 + lane];
+        const u64 w0 = bpos >> 5, nwords = ((bpos + A.bitlen[b] + 31) >> 5) - w0;
+        if (nwords <= ENC_STG) {
+            // staged: the block's words assembled in shared memory, then written coalesced
+            // (its first and last words are shared with the neighbouring blocks: atomic OR)
+            for (int i = lane; i < (int)nwords; i += 32) stg[i] = 0;
+            __syncwarp();
+            const u32 pos = (u32)(gpos - w0 * 32);
+            if (p0 < pend) {
+                if (fixed) pack_range_s<true, true>(W, sym16, sym32, p0, pend, pos, stg_sa);
+                else if (longc) pack_range_s<false, true>(W, sym16, sym32, p0, pend, pos, stg_sa);
+                else pack_range_s<false, false>(W, sym16, sym32, p0, pend, pos, stg_sa);
+            }
+            __syncwarp();
+            for (int i = lane; i < (int)nwords; i += 32) {
+                const u32 v = stg[i];
+                if (i == 0 || i == (int)nwords - 1) atomicOr(words + w0 + i, v);
+                else words[w0 + i] = v;
+            }
+        } else if (p0 < pend) {
             if (fixed) pack_range<true, true>(W, sym16, sym32, p0, pend, gpos, words);
             else if (longc) pack_range<false, true>(W, sym16, sym32, p0, pend, gpos, words);
             else pack_range<false, false>(W, sym16, sym32, p0, pend, gpos, words);
