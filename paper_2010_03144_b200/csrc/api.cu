@@ -366,7 +366,8 @@ static int kernel_attrs_once() {
         setmax((const void*)k_enc_len);
         setmax((const void*)k_enc_pack);
         setmax((const void*)k_parse_tail);
-        setmax((const void*)k_decode);
+        setmax((const void*)k_decode<false>);
+        setmax((const void*)k_decode<true>);
         setmax((const void*)k_recon_g<32>);
         setmax((const void*)k_recon_g<128>);
         if (cudaGetLastError() != cudaSuccess) rc = FTLZ_ERR_CUDA;
@@ -965,7 +966,9 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     int rw = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / rslot));
     if (decode) {
         PF.mark("k_decode", s);
-        k_decode<<<(unsigned)((g.nb + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32)), DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
+        const unsigned dgrid = (unsigned)((g.nb + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32));
+        if (A.n_faults) k_decode<true><<<dgrid, DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
+        else k_decode<false><<<dgrid, DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
         LCHK("k_decode");
         PF.mark("k_recon_warp", s);
         k_recon_g<128><<<sms * 4, 128, rslot, s>>>(A, 0);
@@ -1017,7 +1020,7 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         std::sort(mis.begin(), mis.end());
         CK(cudaMemcpy(ws + L.mis, mis.data(), 4 * (size_t)nmis, cudaMemcpyHostToDevice));
         A.n_faults = 0;
-        k_decode<<<(unsigned)((nmis + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32)), DEC_WARPS * 32, dec_smem, s>>>(
+        k_decode<false><<<(unsigned)((nmis + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32)), DEC_WARPS * 32, dec_smem, s>>>(
             A, (const u32*)(ws + L.mis), (int)nmis);
         LCHK("k_decode");
         k_recon_g<32><<<(unsigned)std::min<u32>((nmis + rw - 1) / rw, sms * 4), rw * 32, rslot * rw, s>>>(A, 1);
@@ -1074,7 +1077,7 @@ static int region_core(const HostPlan& P, const DevPlan& D, const uint8_t* d_a, 
     const size_t dec_smem = ((size_t)4 << DEC_TBITS) + (size_t)DEC_WARPS * 32 * g.e * 4;
     const size_t rslot = al16((size_t)g.vmax * 8) + al16((size_t)g.vmax * 4) + al16(2 * (size_t)g.nvmax8);
     const int rw = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / rslot));
-    k_decode<<<(n + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32), DEC_WARPS * 32, dec_smem, s>>>(A, A.region_list, (int)n);
+    k_decode<false><<<(n + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32), DEC_WARPS * 32, dec_smem, s>>>(A, A.region_list, (int)n);
     LCHK("k_decode");
     k_recon_g<32><<<std::min<u32>((n + rw - 1) / rw, (u32)sms * 4), rw * 32, rslot * rw, s>>>(A, 2);
     LCHK("k_recon");
@@ -1099,7 +1102,7 @@ static int region_core(const HostPlan& P, const DevPlan& D, const uint8_t* d_a, 
         std::sort(mis.begin(), mis.end());
         CK(cudaMemcpy(ws + L.mis, mis.data(), 4 * (size_t)nmis, cudaMemcpyHostToDevice));
         A.region = 0;   // re-decode failures mark mflag = 3
-        k_decode<<<(nmis + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32), DEC_WARPS * 32, dec_smem, s>>>(
+        k_decode<false><<<(nmis + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32), DEC_WARPS * 32, dec_smem, s>>>(
             A, (const u32*)(ws + L.mis), (int)nmis);
         LCHK("k_decode");
         k_recon_g<32><<<std::min<u32>((nmis + rw - 1) / rw, (u32)sms * 4), rw * 32, rslot * rw, s>>>(A, 3);
