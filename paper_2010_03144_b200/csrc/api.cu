@@ -332,10 +332,11 @@ static KCfg kcfg_comp(const Geom& g) {
         // k_prep: 2 tiles, centred-coordinate tables, fold stack, leaf partials, samples
         k.pp_nls = (int)(v / 64 + 8);
         k.pp_ns = (int)(v / 8 + 8);
-        size_t ps = PREP_NBUF * (size_t)k.stage.tile_bytes + 8 * (192 + 128 + 4 * (size_t)k.pp_nls + 2 * (size_t)k.pp_ns) + 16;
+        size_t ps = PREP_NBUF * (size_t)k.stage.tile_bytes +
+                    8 * (3 * (size_t)g.e + 4 * PREP_STK + 4 * (size_t)k.pp_nls + 2 * (size_t)k.pp_ns) + 16;
         ps = (ps + 127) & ~(size_t)127;
         k.pp_slot = (int)ps;
-        k.pp_warps = (int)std::max<size_t>(1, std::min<size_t>(24, (227 * 1024 - 256) / ps));
+        k.pp_warps = (int)std::max<size_t>(1, std::min<size_t>(20, (227 * 1024 - 256) / ps));
         k.pp_smem = ps * k.pp_warps + 128;
     }
     k.lor_slot = al16(4 * v) + 8 * v + al16(2 * v);

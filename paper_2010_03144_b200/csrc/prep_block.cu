@@ -86,7 +86,7 @@ struct PrepAcc {
     u32 nan;
 };
 
-FTLZ_DEV void prep_visit(const float* tile, const PWalk& w, int p, const double* cv, PrepAcc& a, double t4[4]) {
+FTLZ_DEV void prep_visit(const float* tile, const PWalk& w, int p, const double* cv, int cvn, PrepAcc& a, double t4[4]) {
     const float f = tile[w.t];
     const u32 u = __float_as_uint(f);
     a.cs += (u64)u;
@@ -97,15 +97,16 @@ FTLZ_DEV void prep_visit(const float* tile, const PWalk& w, int p, const double*
     const double v = (double)f;
     t4[0] = v;
     t4[1] = __dmul_rn(cv[w.i], v);
-    t4[2] = __dmul_rn(cv[64 + w.j], v);
-    t4[3] = __dmul_rn(cv[128 + w.k], v);
+    t4[2] = __dmul_rn(cv[cvn + w.j], v);
+    t4[3] = __dmul_rn(cv[2 * cvn + w.k], v);
 }
 
 // one tile per warp: the next block's TMA is issued as soon as the current tile is last read,
 // and the freed shared memory buys more resident warps (latency hiding across warps)
 #define PREP_NBUF 1
+#define PREP_STK 16   // post-order fold depth: log2(leaves) + 1 <= 13 for 64^3 blocks
 
-__global__ void __launch_bounds__(768, 1) k_prep(const __grid_constant__ CompArgs A, const __grid_constant__ CUtensorMap tmap) {
+__global__ void __launch_bounds__(640, 1) k_prep(const __grid_constant__ CompArgs A, const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     const Geom& g = A.g;
@@ -115,9 +116,10 @@ __global__ void __launch_bounds__(768, 1) k_prep(const __grid_constant__ CompArg
     WarpStager ws;
     ws.base = slot;
     ws.tbytes = S.tile_bytes;
-    double* cv = (double*)(slot + PREP_NBUF * S.tile_bytes);   // [0,64) i - hx, [64,128) j - hy, [128,192) k - hz
-    double* stk = cv + 192;                            // 32 x 4
-    double* leafval = stk + 128;                       // nls x 4
+    const int cvn = g.e;
+    double* cv = (double*)(slot + PREP_NBUF * S.tile_bytes);   // [0,e) i - hx, [e,2e) j - hy, [2e,3e) k - hz
+    double* stk = cv + 3 * cvn;                        // fold stack: depth <= PREP_STK, x 4
+    double* leafval = stk + 4 * PREP_STK;              // nls x 4
     double* ar = leafval + 4 * A.pp_nls;               // samples
     double* al = ar + A.pp_ns;
     ws.bar = (u64*)(al + A.pp_ns);
@@ -154,10 +156,10 @@ __global__ void __launch_bounds__(768, 1) k_prep(const __grid_constant__ CompArg
         if (B.xid != last_xid) {
             // centred coordinates c = idx - (n - 1) / 2 (predict.py:90-98)
             const double hx = (double)(bx - 1) / 2.0, hy = (double)(by - 1) / 2.0, hz = (double)(bz - 1) / 2.0;
-            for (int t = lane; t < 64; t += 32) {
+            for (int t = lane; t < cvn; t += 32) {
                 cv[t] = __dadd_rn(int_to_f64(t), -hx);
-                cv[64 + t] = __dadd_rn(int_to_f64(t), -hy);
-                cv[128 + t] = __dadd_rn(int_to_f64(t), -hz);
+                cv[cvn + t] = __dadd_rn(int_to_f64(t), -hy);
+                cv[2 * cvn + t] = __dadd_rn(int_to_f64(t), -hz);
             }
             last_xid = B.xid;
             __syncwarp();
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(768, 1) k_prep(const __grid_constant__ CompArg
                 w.set(0, by, bz, S.tye, S.tz, zoff);
                 for (int p = 0; p < vol; p++) {
                     double t4[4];
-                    prep_visit(tile, w, p, cv, acc, t4);
+                    prep_visit(tile, w, p, cv, cvn, acc, t4);
 #pragma unroll
                     for (int q = 0; q < 4; q++) r[q] = __dadd_rn(r[q], t4[q]);
                     w.step(1, by, bz, tjump, ijump);
@@ -199,13 +201,13 @@ __global__ void __launch_bounds__(768, 1) k_prep(const __grid_constant__ CompArg
                     const int len8 = len - (len & 7);
                     PWalk w;
                     w.set_crd(__ldg(crd + start + j8), S.tye, S.tz, zoff);
-                    prep_visit(tile, w, start + j8, cv, acc, r);
+                    prep_visit(tile, w, start + j8, cv, cvn, acc, r);
                     if (bz >= 8) {   // at most one row carry per step (the loop-invariant test hoisted)
 #pragma unroll 2
                         for (int p = start + j8 + 8; p < start + len8; p += 8) {
                             w.step1(8, by, bz, tjump, ijump);
                             double t4[4];
-                            prep_visit(tile, w, p, cv, acc, t4);
+                            prep_visit(tile, w, p, cv, cvn, acc, t4);
 #pragma unroll
                             for (int q = 0; q < 4; q++) r[q] = __dadd_rn(r[q], t4[q]);
                         }
@@ -213,7 +215,7 @@ __global__ void __launch_bounds__(768, 1) k_prep(const __grid_constant__ CompArg
                         for (int p = start + j8 + 8; p < start + len8; p += 8) {
                             w.step(8, by, bz, tjump, ijump);
                             double t4[4];
-                            prep_visit(tile, w, p, cv, acc, t4);
+                            prep_visit(tile, w, p, cv, cvn, acc, t4);
 #pragma unroll
                             for (int q = 0; q < 4; q++) r[q] = __dadd_rn(r[q], t4[q]);
                         }
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(768, 1) k_prep(const __grid_constant__ CompArg
                         w.set_crd(__ldg(crd + start + len8), S.tye, S.tz, zoff);
                         for (int p = start + len8; p < start + len; p++) {
                             double t4[4];
-                            prep_visit(tile, w, p, cv, acc, t4);
+                            prep_visit(tile, w, p, cv, cvn, acc, t4);
 #pragma unroll
                             for (int q = 0; q < 4; q++) r[q] = __dadd_rn(r[q], t4[q]);
                             w.step(1, by, bz, tjump, ijump);
