@@ -231,6 +231,13 @@ int ftlz_ctx_compress_host(ftlz_ctx* ctx, const float* h_in, int64_t nx, int64_t
                            int32_t eb_mode, double eb_value, const ftlz_config* cfg,
                            const ftlz_fault* faults, int64_t n_faults,
                            const int8_t* predictor_override, ftlz_report* report);
+/* as ftlz_ctx_compress_host, with the archive downloaded straight into h_out (e.g. pinned
+ * memory): no staging copy.  FTLZ_ERR_CAPACITY (report->archive_len set, archive kept on the
+ * device for ftlz_ctx_copy_archive) when out_capacity is too small. */
+int ftlz_ctx_compress_host_to(ftlz_ctx* ctx, const float* h_in, int64_t nx, int64_t ny, int64_t nz,
+                              int32_t eb_mode, double eb_value, const ftlz_config* cfg,
+                              const ftlz_fault* faults, int64_t n_faults, const int8_t* predictor_override,
+                              uint8_t* h_out, size_t out_capacity, ftlz_report* report);
 int ftlz_ctx_archive_device(ftlz_ctx* ctx, const uint8_t** d_ptr, size_t* len);
 int ftlz_ctx_archive_host(ftlz_ctx* ctx, const uint8_t** h_ptr, size_t* len);
 /* copy the last archive into caller memory (host) */

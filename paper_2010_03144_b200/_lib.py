@@ -12,7 +12,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libftlz_b200.so")
+# FTLZ_LIB_PATH points at another build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("FTLZ_LIB_PATH") or os.path.join(_HERE, "lib", "libftlz_b200.so")
 
 
 class BackendUnavailable(RuntimeError):
@@ -78,7 +79,7 @@ EXPORTS = [
     "ftlz_ctx_archive_device", "ftlz_ctx_archive_host", "ftlz_ctx_copy_archive",
     "ftlz_ctx_parse_host", "ftlz_ctx_decompress_host", "ftlz_ctx_decompress_device",
     "ftlz_ctx_profile", "ftlz_ctx_profile_read", "ftlz_ctx_decompress_region_host",
-    "ftlz_intersecting_block_count", "ftlz_ctx_rle_host",
+    "ftlz_intersecting_block_count", "ftlz_ctx_rle_host", "ftlz_ctx_compress_host_to",
 ]
 
 _lib = None
@@ -125,6 +126,7 @@ def load():
         L.ftlz_ctx_stream.restype = vp
         L.ftlz_ctx_compress_device.argtypes = [vp, vp, i64, i64, i64, i32, dbl, PC, PF, i64, vp, PR]
         L.ftlz_ctx_compress_host.argtypes = [vp, vp, i64, i64, i64, i32, dbl, PC, PF, i64, vp, PR]
+        L.ftlz_ctx_compress_host_to.argtypes = [vp, vp, i64, i64, i64, i32, dbl, PC, PF, i64, vp, vp, sz, PR]
         L.ftlz_ctx_archive_device.argtypes = [vp, C.POINTER(vp), C.POINTER(sz)]
         L.ftlz_ctx_archive_host.argtypes = [vp, C.POINTER(vp), C.POINTER(sz)]
         L.ftlz_ctx_copy_archive.argtypes = [vp, vp, sz]

@@ -327,7 +327,7 @@ static KCfg kcfg_comp(const Geom& g) {
         slot = (slot + 127) & ~(size_t)127;
         k.qr_slot = (int)slot;
         size_t avail = 227 * 1024 - 4 * HWIN_REG - 128;
-        k.qr_warps = (int)std::max<size_t>(1, std::min<size_t>(12, avail / slot));
+        k.qr_warps = (int)std::max<size_t>(1, std::min<size_t>(QR_WARPS, avail / slot));
         k.qr_smem = slot * k.qr_warps + 4 * HWIN_REG + 128;   // + alignment slack
         // k_prep: 2 tiles, centred-coordinate tables, fold stack, leaf partials, samples
         k.pp_nls = (int)(v / 64 + 8);
@@ -1341,6 +1341,30 @@ extern "C" int ftlz_ctx_compress_host(ftlz_ctx* c, const float* h_in, int64_t nx
     CK(cudaMemcpyAsync(c->h_arch.p, c->out.p, c->arch_len, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     c->arch_on_host = true;
+    return FTLZ_OK;
+}
+
+extern "C" int ftlz_ctx_compress_host_to(ftlz_ctx* c, const float* h_in, int64_t nx, int64_t ny, int64_t nz,
+                                         int32_t eb_mode, double eb_value, const ftlz_config* cfg,
+                                         const ftlz_fault* faults, int64_t nf, const int8_t* ovr, uint8_t* h_out,
+                                         size_t out_capacity, ftlz_report* rep) {
+    std::lock_guard<std::mutex> g(c->mu);
+    cudaSetDevice(c->device);
+    if (nx < 1 || ny < 1 || nz < 1) {
+        report_reset(rep);
+        info_set(&rep->info, FTLZ_ERR_INVALID_GEOMETRY, 0, -1, -1, 0, 0);
+        return set_err(FTLZ_ERR_INVALID_GEOMETRY, "invalid dims");
+    }
+    size_t nbytes = (size_t)nx * ny * nz * 4;
+    int rc = c->in.ensure(nbytes);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(c->in.p, h_in, nbytes, cudaMemcpyHostToDevice, c->stream));
+    rc = ctx_compress(c, (const float*)c->in.p, nx, ny, nz, eb_mode, eb_value, cfg, faults, nf, ovr, rep);
+    if (rc) return rc;
+    // the archive stays on the device for ftlz_ctx_copy_archive when it does not fit
+    if (c->arch_len > out_capacity) return set_err(FTLZ_ERR_CAPACITY, "destination too small");
+    CK(cudaMemcpyAsync(h_out, c->out.p, c->arch_len, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
     return FTLZ_OK;
 }
 

@@ -159,7 +159,9 @@ FTLZ_DEV void reg_step(RegPos& P, const RegBlk& K) {
 // Points go in groups of RB: all RB points' operands are loaded before any store of the group,
 // so the RB float64 dependency chains interleave (the bins / histogram stores would otherwise
 // order every point after the previous one's stores).
+#ifndef RB
 #define RB 4
+#endif
 template <bool DUP, bool PIN, bool FULLJ>
 FTLZ_DEV void reg_points(const QuantParams& Q, const RegBlk& K, RegPos P, int p0, int pend, int lane, u16* lh16,
                          u32* hwin, u32* ghist, int lhlo, int wlo, RegAcc& acc) {
@@ -270,7 +272,10 @@ FTLZ_DEV void reg_fixup(const QuantParams& Q, const RegBlk& K, const float4& cf,
     }
 }
 
-__global__ void __launch_bounds__(384, 1) k_quant_reg(const __grid_constant__ CompArgs A,
+#ifndef QR_WARPS
+#define QR_WARPS 12
+#endif
+__global__ void __launch_bounds__(QR_WARPS * 32, 1) k_quant_reg(const __grid_constant__ CompArgs A,
                                                        const __grid_constant__ CUtensorMap tmap) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // 128-byte aligned base for the TMA destinations

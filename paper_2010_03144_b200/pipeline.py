@@ -175,17 +175,20 @@ def _compress_array(values, eb_spec, cfg, predictor_override, faults, grid, out=
         for b, k in predictor_override.items():
             ov[int(b)] = int(k)
     rep = _report_buf(nb)
-    st = L.ftlz_ctx_compress_host(ctx, x.ctypes.data, nx, ny, nz, EB_MODE_CODES[eb_spec.mode],
-                                  float(eb_spec.value), C.byref(cfg._c()), fa, nf,
-                                  ov.ctypes.data if ov is not None else None, C.byref(rep.r))
+    args = (ctx, x.ctypes.data, nx, ny, nz, EB_MODE_CODES[eb_spec.mode], float(eb_spec.value),
+            C.byref(cfg._c()), fa, nf, ov.ctypes.data if ov is not None else None)
+    if out is not None:
+        # the archive goes straight from the device into the caller's buffer
+        ob = np.frombuffer(out, np.uint8)
+        st = L.ftlz_ctx_compress_host_to(*args, ob.ctypes.data, ob.size, C.byref(rep.r))
+        if st == 9 and rep.r.archive_len > ob.size:
+            raise ValueError(f"output buffer holds {ob.size} bytes, archive needs {rep.r.archive_len}")
+        if st != 0:
+            raise_for_info(st, rep.r.info, eb_request=(eb_spec.mode, eb_spec.value), resolved=rep.r.eb)
+        return rep.r.archive_len, rep
+    st = L.ftlz_ctx_compress_host(*args, C.byref(rep.r))
     if st != 0:
         raise_for_info(st, rep.r.info, eb_request=(eb_spec.mode, eb_spec.value), resolved=rep.r.eb)
-    n = rep.r.archive_len
-    if out is not None:
-        if len(out) < n:
-            raise ValueError(f"output buffer holds {len(out)} bytes, archive needs {n}")
-        L.ftlz_ctx_copy_archive(ctx, np.frombuffer(out, np.uint8).ctypes.data, len(out))
-        return n, rep
     ptr = C.c_void_p()
     ln = C.c_size_t()
     L.ftlz_ctx_archive_host(ctx, C.byref(ptr), C.byref(ln))
