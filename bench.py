@@ -511,7 +511,9 @@ def ncu_traffic() -> dict:
             continue
         for k, v in d.get("kernels", {}).items():
             if v.get("dram_bytes") is not None:
-                out[k] = {"dram_bytes": v["dram_bytes"], "source": os.path.relpath(f, ROOT)}
+                # template instances ("void k_decode<0>") are reported under the kernel's name
+                name = k.split()[-1].split("<")[0]
+                out[name] = {"dram_bytes": v["dram_bytes"], "source": os.path.relpath(f, ROOT)}
     return out
 
 
