@@ -323,7 +323,7 @@ static KCfg kcfg_comp(const Geom& g) {
         k.stage.pad = 0;
         k.rmax = txe * tye;
         k.qr_tab = (int)al16(2 * k.stage.tile_bytes + al16(2 * (size_t)g.nvmax8));
-        size_t slot = (size_t)k.qr_tab + 8 * (2 * (size_t)k.rmax + 64) + 2 * 32 * 65 + 16;
+        size_t slot = (size_t)k.qr_tab + 8 * (2 * (size_t)k.rmax + 64) + sizeof(LHT) * 32 * (LH_BINS + 1) + 16;
         slot = (slot + 127) & ~(size_t)127;
         k.qr_slot = (int)slot;
         size_t avail = 227 * 1024 - 4 * HWIN_REG - 128;

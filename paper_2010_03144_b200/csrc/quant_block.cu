@@ -49,9 +49,21 @@ FTLZ_DEV float4 ld_volatile_f4(const float4* p) {
     return v;
 }
 
-// ---- lane-private histogram window: 64 bins around the centre, u16 counter of bin o for
-//      lane l at lh16[o * 32 + l] (lanes never share a counter; no atomics)
+// ---- lane-private histogram window around the centre: counter of bin o for lane l at
+//      lh16[o * 32 + l] (lanes never share a counter; no atomics).  LH8: 128 bins of u8
+//      counters (flushed every few blocks), else 64 bins of u16 counters.
+#ifndef LH16
+#define LH8
+#endif
+#ifdef LH8
+#define LH_BINS 128
+typedef unsigned char LHT;
+#define LH_MAXC 255u
+#else
 #define LH_BINS 64
+typedef u16 LHT;
+#define LH_MAXC 65535u
+#endif
 #define HWIN_REG 2048
 
 FTLZ_DEV void reg_hist_out(u32* hwin, u32* ghist, int wlo, int bin, u32 delta) {
@@ -59,14 +71,36 @@ FTLZ_DEV void reg_hist_out(u32* hwin, u32* ghist, int wlo, int bin, u32 delta) {
     if (ow < HWIN_REG) atomicAdd(&hwin[ow], delta);
     else atomicAdd(&ghist[bin], delta);
 }
-FTLZ_DEV void reg_hist_add(u16* lh16, u32* hwin, u32* ghist, int lhlo, int wlo, int bin, int lane, int delta) {
+FTLZ_DEV void reg_hist_add(LHT* lh16, u32* hwin, u32* ghist, int lhlo, int wlo, int bin, int lane, int delta) {
     unsigned o = (unsigned)(bin - lhlo);
-    if (o < LH_BINS) lh16[o * 32 + lane] += (u16)delta;
+    if (o < LH_BINS) lh16[o * 32 + lane] += (LHT)delta;
     else reg_hist_out(hwin, ghist, wlo, bin, (u32)delta);
 }
 
+#ifdef LH8
+// lane l sums bins lhlo + 4l .. + 3 over the 32 lane counters (8 words of 4 bytes each) and
+// clears them
+FTLZ_DEV void reg_hist_flush_lanes(LHT* lh16, u32* ghist, int lhlo, int cap, int lane) {
+    __syncwarp();
+    u32* w32 = (u32*)lh16;   // bin o occupies words o*8 .. o*8+7
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        const int o = 4 * lane + q;
+        u32 sum = 0;
+#pragma unroll
+        for (int c = 0; c < 8; c++) {
+            const int cc = (c + lane) & 7;
+            sum = __dp4a(w32[o * 8 + cc], 0x01010101u, sum);
+            w32[o * 8 + cc] = 0;
+        }
+        const int bn = lhlo + o;
+        if (sum && bn >= 0 && bn < cap) atomicAdd(&ghist[bn], sum);
+    }
+    __syncwarp();
+}
+#else
 // lane l sums bins lhlo + 2l and lhlo + 2l + 1 over the 32 lane counters and clears them
-FTLZ_DEV void reg_hist_flush_lanes(u16* lh16, u32* ghist, int lhlo, int cap, int lane) {
+FTLZ_DEV void reg_hist_flush_lanes(LHT* lh16, u32* ghist, int lhlo, int cap, int lane) {
     __syncwarp();
     u32* w32 = (u32*)lh16;   // bin o occupies words o*16 .. o*16+15
     u32 lo = 0, hi = 0;
@@ -84,6 +118,7 @@ FTLZ_DEV void reg_hist_flush_lanes(u16* lh16, u32* ghist, int lhlo, int cap, int
     if (hi && b0 + 1 >= 0 && b0 + 1 < cap) atomicAdd(&ghist[b0 + 1], hi);
     __syncwarp();
 }
+#endif
 
 // per-lane partial sums of one block
 struct RegAcc {
@@ -94,7 +129,7 @@ struct RegAcc {
 };
 
 // lane-private counter of an in-window bin; out-of-window bins go to the sink row LH_BINS
-FTLZ_DEV void lh_bump(u16* lh16, int lhlo, int bin, int lane, u32& outwin) {
+FTLZ_DEV void lh_bump(LHT* lh16, int lhlo, int bin, int lane, u32& outwin) {
     unsigned o = (unsigned)(bin - lhlo);
     const bool in = o < LH_BINS;
     outwin |= (u32)!in;
@@ -163,7 +198,7 @@ FTLZ_DEV void reg_step(RegPos& P, const RegBlk& K) {
 #define RB 4
 #endif
 template <bool DUP, bool PIN, bool FULLJ>
-FTLZ_DEV void reg_points(const QuantParams& Q, const RegBlk& K, RegPos P, int p0, int pend, int lane, u16* lh16,
+FTLZ_DEV void reg_points(const QuantParams& Q, const RegBlk& K, RegPos P, int p0, int pend, int lane, LHT* lh16,
                          u32* hwin, u32* ghist, int lhlo, int wlo, RegAcc& acc) {
     u32 flag = 0, outw = 0;
     int p = p0;
@@ -238,7 +273,7 @@ FTLZ_DEV void reg_hist_outwin(const u16* bins16, int p0, int pend, u32* hwin, u3
 // fast path and replace every flagged point's results by the exact formulation's
 template <bool DUP>
 FTLZ_DEV void reg_fixup(const QuantParams& Q, const RegBlk& K, const float4& cf, int p0, int pend, int zoff, int tz,
-                        int tye, int lane, u16* lh16, u32* hwin, u32* ghist, int lhlo, int wlo, RegAcc& acc,
+                        int tye, int lane, LHT* lh16, u32* hwin, u32* ghist, int lhlo, int wlo, RegAcc& acc,
                         bool& mism) {
     for (int p = p0; p < pend; p++) {
         const int rp = p / K.bz, k = p - rp * K.bz, i = rp / K.by, j = rp - i * K.by;
@@ -292,12 +327,12 @@ __global__ void __launch_bounds__(QR_WARPS * 32, 1) k_quant_reg(const __grid_con
     double* abt = (double*)(slot + A.qr_tab);
     double* abt2 = abt + A.rmax;
     double* ctab = abt2 + A.rmax;
-    u16* lh16 = (u16*)(ctab + 64);
+    LHT* lh16 = (LHT*)(ctab + 64);
     ws.bar = (u64*)(lh16 + (LH_BINS + 1) * 32);
     u32* hwin = (u32*)(smem + (size_t)nw * A.qr_slot);
     const int wlo = A.center - HWIN_REG / 2, lhlo = A.center - LH_BINS / 2;
     for (int t = threadIdx.x; t < HWIN_REG; t += blockDim.x) hwin[t] = 0;
-    for (int t = lane; t < (LH_BINS + 1) * 16; t += 32) ((u32*)lh16)[t] = 0;
+    for (int t = lane; t < (LH_BINS + 1) * 32 * (int)sizeof(LHT) / 4; t += 32) ((u32*)lh16)[t] = 0;
     ws.init(lane);
     __syncthreads();
 
@@ -444,7 +479,7 @@ __global__ void __launch_bounds__(QR_WARPS * 32, 1) k_quant_reg(const __grid_con
                 }
             }
         }
-        if (lh_load > 65535u - 2u * (u32)g.vmax / 32u - 64u) {
+        if (lh_load > LH_MAXC - 2u * ((((u32)g.vmax + 31u) >> 5) | 1u)) {
             reg_hist_flush_lanes(lh16, A.hist, lhlo, A.cap, lane);
             lh_load = 0;
         }
