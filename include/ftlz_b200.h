@@ -246,7 +246,9 @@ int ftlz_ctx_copy_archive(ftlz_ctx* ctx, void* h_dst, size_t capacity);
 int ftlz_ctx_parse_host(ftlz_ctx* ctx, const uint8_t* h_archive, size_t len,
                         ftlz_stream_info* info_out, ftlz_report* report);
 /* host archive -> host float32 output (h_out: nx*ny*nz floats, pinned or pageable).
- * If `reuse_parsed` is nonzero and the same archive was just parsed, the upload is skipped. */
+ * If `reuse_parsed` is nonzero and the same archive was just parsed, the upload is skipped.
+ * Large fields are decoded in slabs whose output is downloaded while later slabs decode, so
+ * h_out is unspecified when report->sdc withholds the output. */
 int ftlz_ctx_decompress_host(ftlz_ctx* ctx, const uint8_t* h_archive, size_t len, float* h_out,
                              const ftlz_fault* faults, int64_t n_faults, int32_t reuse_parsed,
                              ftlz_report* report);

@@ -900,14 +900,27 @@ static DecArgs make_dec_args(const HostPlan& P, const DevPlan& D, const DecLayou
     A.rle_pay = (RleJob*)(ws + L.jobs); A.rle_sdc = A.rle_pay + 1;
     A.pay_scratch = ws + L.payscr; A.sdc_scratch = ws + L.sdcscr;
     A.pay_cap = L.pay_cap; A.sdc_cap = L.sdc_cap;
+    A.sb0 = 0; A.sb1 = g.nb;
 
     return A;
 }
 
+// Optional download overlap (DlOverlap): the output is decoded in slabs of block layers and
+// each finished slab is copied to h_out on a second stream while the next slab decodes.  The
+// copies run before the SDC verdict is known; h_out is unspecified when the verdict withholds
+// the output, and re-executed blocks are copied again afterwards.
+struct DlOverlap {
+    float* h_out = nullptr;
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev[8] = {};
+    int nslab = 0;
+};
+
 static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8_t* d_a, size_t len,
                            const ftlz_header* h, float* d_out, const ftlz_fault* faults, int64_t nf,
                            unsigned char* ws, size_t ws_size, ftlz_report* rep, ftlz_stream_info* si_out,
-                           bool decode, cudaStream_t s, unsigned char* h_result, Profiler* prof = nullptr) {
+                           bool decode, cudaStream_t s, unsigned char* h_result, Profiler* prof = nullptr,
+                           const DlOverlap* dl = nullptr) {
     Profiler noprof;
     Profiler& PF = prof ? *prof : noprof;
     report_reset(rep);
@@ -967,13 +980,32 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     int rw = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / rslot));
     if (decode) {
         PF.mark("k_decode", s);
-        const unsigned dgrid = (unsigned)((g.nb + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32));
-        if (A.n_faults) k_decode<true><<<dgrid, DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
-        else k_decode<false><<<dgrid, DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
-        LCHK("k_decode");
-        PF.mark("k_recon_warp", s);
-        k_recon_g<128><<<sms * 4, 128, rslot, s>>>(A, 0);
-        LCHK("k_recon");
+        // slabs: whole block layers (block ids are layer-major), so each slab's output is one
+        // contiguous range of x-planes
+        const int nslab = dl && dl->h_out ? std::max(1, std::min<int>(dl->nslab, (int)g.cx)) : 1;
+        const long long layer = g.cy * g.cz, plane = g.ny * g.nz;
+        for (int si = 0; si < nslab; si++) {
+            const long long l0 = g.cx * si / nslab, l1 = g.cx * (si + 1) / nslab;
+            A.sb0 = l0 * layer;
+            A.sb1 = l1 * layer;
+            const unsigned dgrid = (unsigned)((A.sb1 - A.sb0 + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32));
+            PF.mark("k_decode", s);
+            if (A.n_faults) k_decode<true><<<dgrid, DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
+            else k_decode<false><<<dgrid, DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
+            LCHK("k_decode");
+            PF.mark("k_recon_warp", s);
+            k_recon_g<128><<<sms * 4, 128, rslot, s>>>(A, 0);
+            LCHK("k_recon");
+            if (nslab > 1 || (dl && dl->h_out)) {
+                const long long x0 = l0 * g.e, x1 = std::min<long long>(l1 * g.e, g.nx);
+                CK(cudaEventRecord(dl->ev[si], s));
+                CK(cudaStreamWaitEvent(dl->cs, dl->ev[si], 0));
+                CK(cudaMemcpyAsync(dl->h_out + x0 * plane, d_out + x0 * plane, (size_t)(x1 - x0) * plane * 4,
+                                   cudaMemcpyDeviceToHost, dl->cs));
+            }
+        }
+        A.sb0 = 0;
+        A.sb1 = g.nb;
     }
     CK(cudaGetLastError());
     PF.mark("", s);
@@ -1044,6 +1076,12 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
             }
         }
         std::sort(reexec.begin(), reexec.end());
+        if (dl && dl->h_out && !rep->sdc) {
+            // re-executed blocks changed d_out after the slab copies: copy it again
+            CK(cudaStreamSynchronize(dl->cs));
+            CK(cudaMemcpyAsync(dl->h_out, d_out, (size_t)g.nx * g.ny * g.nz * 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+        }
     }
     put_list(rep->reexecuted, rep->capacity, &rep->n_reexecuted, reexec);
     return FTLZ_OK;
@@ -1232,6 +1270,8 @@ struct HostBuf {
 struct ftlz_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t cs = nullptr;   // download stream of the slab-overlapped decompress
+    cudaEvent_t ev[8] = {};
     DevBuf ws, in, out, dws, arch, dout, plan, rle;
     HostBuf h_arch, h_res;
     size_t arch_len = 0;
@@ -1287,6 +1327,11 @@ extern "C" void ftlz_ctx_destroy(ftlz_ctx* c) {
     c->ws.release(); c->in.release(); c->out.release(); c->dws.release(); c->arch.release();
     c->dout.release(); c->plan.release(); c->rle.release(); c->h_arch.release(); c->h_res.release();
     cudaStreamDestroy(c->stream);
+    if (c->cs) {
+        cudaStreamSynchronize(c->cs);
+        cudaStreamDestroy(c->cs);
+        for (auto& e : c->ev) cudaEventDestroy(e);
+    }
     delete c;
 }
 
@@ -1411,14 +1456,15 @@ static int ctx_upload_archive(ftlz_ctx* c, const uint8_t* h, size_t len, ftlz_he
 }
 
 static int ctx_decompress(ftlz_ctx* c, const uint8_t* d_a, size_t len, const ftlz_header* hdr, float* d_out,
-                          const ftlz_fault* faults, int64_t nf, ftlz_report* rep, ftlz_stream_info* si, bool decode) {
+                          const ftlz_fault* faults, int64_t nf, ftlz_report* rep, ftlz_stream_info* si, bool decode,
+                          const DlOverlap* dl = nullptr) {
     c->prof.mark("d_host_prelude", c->stream);
     int rc = ctx_plan(c, hdr->nx, hdr->ny, hdr->nz, hdr->block_edge);
     if (rc) return rc;
     DecLayout L = dec_layout(c->hp, len, (int)std::min<uint32_t>(hdr->bin_capacity, 65536u), nf, hdr->codec_id);
     if ((rc = c->dws.ensure(L.total))) return rc;
     return decompress_core(c->hp, &c->dp, d_a, len, hdr, d_out, faults, nf, (unsigned char*)c->dws.p, c->dws.n,
-                           rep, si, decode, c->stream, (unsigned char*)c->h_res.p, &c->prof);
+                           rep, si, decode, c->stream, (unsigned char*)c->h_res.p, &c->prof, dl);
 }
 
 extern "C" int ftlz_ctx_parse_host(ftlz_ctx* c, const uint8_t* h, size_t len, ftlz_stream_info* si, ftlz_report* rep) {
@@ -1448,12 +1494,20 @@ extern "C" int ftlz_ctx_decompress_host(ftlz_ctx* c, const uint8_t* h, size_t le
     }
     size_t n = (size_t)hdr.nx * hdr.ny * hdr.nz;
     if ((rc = c->dout.ensure(4 * n))) return rc;
-    rc = ctx_decompress(c, (const uint8_t*)c->arch.p, len, &hdr, (float*)c->dout.p, faults, nf, rep, nullptr, true);
-    if (rc) return rc;
-    if (!rep->sdc) {
-        CK(cudaMemcpyAsync(h_out, c->dout.p, 4 * n, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
+    // the output goes down slab by slab while later slabs decode (DlOverlap)
+    if (!c->cs) {
+        CK(cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking));
+        for (auto& e : c->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
+    DlOverlap dl;
+    dl.h_out = h_out;
+    dl.cs = c->cs;
+    for (int i = 0; i < 8; i++) dl.ev[i] = c->ev[i];
+    dl.nslab = n >= ((size_t)64 << 20) ? 4 : 1;   // small fields: one slab
+    rc = ctx_decompress(c, (const uint8_t*)c->arch.p, len, &hdr, (float*)c->dout.p, faults, nf, rep, nullptr, true, &dl);
+    cudaError_t ce = cudaStreamSynchronize(c->cs);
+    if (rc) return rc;
+    if (ce != cudaSuccess) return set_err(FTLZ_ERR_CUDA, cudaGetErrorString(ce));
     return FTLZ_OK;
 }
 

@@ -87,6 +87,9 @@ struct DecArgs {
     const u32* region_list;   // the intersecting blocks, ascending
     u32 n_region;
     u32 pad_r2;
+    // blocks [sb0, sb1) of the full path (k_decode, Lorenzo pass of k_recon_g): slabs of block
+    // layers let the host download each finished slab while the next one decodes
+    long long sb0, sb1;
 };
 
 FTLZ_DEV u64 ld_le(const u8* p, int n) {
@@ -683,8 +686,8 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
         valid = idx < (long long)nlist;
         b = valid ? (long long)list[idx] : 0;
     } else {
-        b = ((long long)blockIdx.x * DEC_WARPS + warp) * 32 + lane;
-        valid = b < g.nb;
+        b = A.sb0 + ((long long)blockIdx.x * DEC_WARPS + warp) * 32 + lane;
+        valid = b < A.sb1;
     }
     const BlockInfo B = block_info(g, valid ? b : 0);
     const int kind = valid ? A.ind[b] : 0;
@@ -879,6 +882,7 @@ __global__ void __launch_bounds__(128) k_recon_g(DecArgs A, int mode) {
     const u32* list = reexec ? A.mis_list : (rgn ? A.region_list : A.lor_list);
     for (long long idx = (long long)blockIdx.x * nw + warp; idx < (long long)n; idx += (long long)gridDim.x * nw) {
         long long b = list[idx];
+        if (mode == 0 && (b < A.sb0 || b >= A.sb1)) continue;   // another slab's block
         if (A.dflag[b]) continue;                       // undecodable: reported separately
         if (reexec && A.mflag[b] == 3) continue;        // re-decode failed
         BlockInfo B = block_info(g, b);
