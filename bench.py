@@ -366,6 +366,22 @@ def run_ours(args, world, rank, local):
                 "traffic_source": traffic["source"] if traffic else None,
                 "peak_source": peak_kind, "algorithmic_bytes_per_launch": a_bytes}
 
+    # issue roofline (the bound these kernels actually hit): warp instructions per
+    # launch from the committed ncu capture over the live CUDA-event time of the same kernel,
+    # against 4 warp instructions per cycle per SM at the sampled SM clock
+    issue = {}
+    ncu_k = ncu_kernels()
+    num_sms = torch.cuda.get_device_properties(local).multi_processor_count
+    for name, kd in kern.items():
+        nk = ncu_k.get(name)
+        if nk is None or not nk.get("warp_instructions") or kd["launches_per_step"] <= 0:
+            continue
+        t_launch = kd["ms_per_step"] / kd["launches_per_step"] * 1e-3
+        peak_ips = num_sms * 4 * (clocks.get("sm_mhz") or 1965.0) * 1e6
+        issue[name] = {"warp_instructions_per_launch": nk["warp_instructions"],
+                       "frac": nk["warp_instructions"] / t_launch / peak_ips,
+                       "ncu_ipc_per_sm": nk.get("ipc"), "source": nk["source"]}
+
     line = {
         "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
@@ -378,6 +394,7 @@ def run_ours(args, world, rank, local):
         "decompress": {"gbs_input": n_bytes / (td_ms * 1e-3) / 1e9, "ms": td_ms, "algorithmic_bytes": Bd,
                        "roofline_frac": ach_d / peak, "kernels": dec_k},
         "roofline": roof,
+        "issue_roofline": issue,
         "gpu_launches": launches,
         "clocks": clocks,
         "parity": parity,
@@ -496,6 +513,21 @@ def run_c5(F, L, _lib, torch, local):
             r["reference_archive_match"] = synth.sha256(np.frombuffer(data, np.uint8)) == man[tgt]["archive_sha256"]
         res[tgt] = r
     return res
+
+
+def ncu_kernels() -> dict:
+    """Per-kernel ncu metrics (warp instructions, IPC) of the newest committed capture."""
+    import glob
+
+    out = {}
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_kernels.json"))):
+        try:
+            d = json.load(open(f))
+        except Exception:
+            continue
+        for k, v in d.get("kernels", {}).items():
+            out[k.split()[-1].split("<")[0]] = dict(v, source=os.path.relpath(f, ROOT))
+    return out
 
 
 def ncu_traffic() -> dict:

@@ -979,7 +979,6 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     size_t rslot = al16((size_t)g.vmax * 8) + al16((size_t)g.vmax * 4) + al16(2 * (size_t)g.nvmax8);
     int rw = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / rslot));
     if (decode) {
-        PF.mark("k_decode", s);
         // slabs: whole block layers (block ids are layer-major), so each slab's output is one
         // contiguous range of x-planes
         const int nslab = dl && dl->h_out ? std::max(1, std::min<int>(dl->nslab, (int)g.cx)) : 1;
