@@ -56,7 +56,10 @@ FTLZ_DEV float4 ld_volatile_f4(const float4* p) {
 #define LH8
 #endif
 #ifdef LH8
-#define LH_BINS 128
+#ifndef LH8_BINS
+#define LH8_BINS 128
+#endif
+#define LH_BINS LH8_BINS
 typedef unsigned char LHT;
 #define LH_MAXC 255u
 #else
@@ -86,6 +89,7 @@ FTLZ_DEV void reg_hist_flush_lanes(LHT* lh16, u32* ghist, int lhlo, int cap, int
 #pragma unroll
     for (int q = 0; q < 4; q++) {
         const int o = 4 * lane + q;
+        if (o >= LH_BINS) break;
         u32 sum = 0;
 #pragma unroll
         for (int c = 0; c < 8; c++) {
