@@ -182,3 +182,20 @@ def test_full_size_configs_match_reference_hashes(name):
     assert sha(np.frombuffer(data, np.uint8)) == ent["archive_sha256"]
     y = F.decompress_bytes(data)
     assert sha(y) == ent["output_sha256"]
+
+
+@pytest.mark.gpu
+def test_slab_overlapped_decompress_with_reexecution_on_c3():
+    """Large fields decode in slabs whose output downloads overlap the decode; decompressed-data
+    faults force re-execution afterwards, and the result must still be the fault-free output
+    (pipeline.py:708-723)."""
+    from tools import synth
+    x = synth.field("c3")
+    data = F.compress_bytes(x, "value_range_relative", 1e-3)
+    clean = F.decompress_bytes(data)
+    stream = F.parse(data)
+    faults = [("decomp", 5, 17, 30), ("decomp", 70000, 999, 22), ("decomp", 140607, 3, 31)]
+    out, rep = F.decompress(stream, faults=faults)
+    rd = rep.to_dict()
+    assert rd["status"] == "corrected" and rd["decomp_block_reexecuted"] == [5, 70000, 140607]
+    np.testing.assert_array_equal(out.values.view(np.uint32), clean.view(np.uint32))
