@@ -13,7 +13,6 @@ from __future__ import annotations
 import ctypes as C
 import threading
 from dataclasses import dataclass, field
-from typing import Optional
 
 import numpy as np
 
