@@ -1413,6 +1413,7 @@ extern "C" int ftlz_ctx_compress_host_to(ftlz_ctx* c, const float* h_in, int64_t
 }
 
 extern "C" int ftlz_ctx_archive_device(ftlz_ctx* c, const uint8_t** d_ptr, size_t* len) {
+    std::lock_guard<std::mutex> g(c->mu);
     *d_ptr = (const uint8_t*)c->out.p;
     *len = c->arch_len;
     return FTLZ_OK;
@@ -1551,6 +1552,8 @@ extern "C" int ftlz_ctx_decompress_device(ftlz_ctx* c, const uint8_t* d_archive,
 extern "C" int ftlz_ctx_rle_host(ftlz_ctx* c, const uint8_t* h_in, size_t n, int32_t invert, uint8_t* h_out,
                                  size_t capacity, size_t* out_len, ftlz_info* info) {
     if (!c || (!h_in && n) || !out_len) return set_err(FTLZ_ERR_INVALID_ARGUMENT, "null argument");
+    std::lock_guard<std::mutex> g(c->mu);
+    cudaSetDevice(c->device);
     if (info) info_set(info, FTLZ_OK, 0, -1, -1, 0, 0);
     cudaStream_t s = c->stream;
     const size_t cap = capacity;
