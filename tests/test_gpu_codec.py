@@ -109,3 +109,39 @@ def test_codec2_is_unsupported():
     x = np.zeros((8, 8, 8), np.float32) + np.arange(8, dtype=np.float32)
     with pytest.raises(F.UnsupportedCodec):
         F.compress(F.Field.from_array(x), F.ErrorBound("absolute", 1e-3), F.FtConfig(codec_id=2))
+
+
+@pytest.mark.parametrize("name", sorted(C1))
+def test_codec1_region_extraction_matches_full_decompress(name):
+    """decompress_region (pipeline.py:726-795) on a codec-1 archive: the payload and sum_dc
+    are inverted on the device by the parse, then only the intersecting blocks decode."""
+    z = load(name)
+    data = z["archive"].tobytes()
+    full, _ = F.decompress(F.parse(data))
+    dims = full.values.shape
+    lo = tuple(d // 4 for d in dims)
+    hi = tuple(max(l + 1, (3 * d) // 4) for l, d in zip(lo, dims))
+    out, rep = F.decompress_region(F.parse(data), (lo, hi))
+    assert rep.to_dict()["status"] == "clean"
+    want = full.values[lo[0]:hi[0], lo[1]:hi[1], lo[2]:hi[2]]
+    np.testing.assert_array_equal(out.values.view(np.uint32), want.view(np.uint32))
+
+
+def test_codec1_fault_campaign_cell_matches_codec0():
+    """Injected input / bins / decompressed-data flips behave the same under codec 1: the
+    backend codec only changes how the payload is stored (faults.py:143-260)."""
+    from paper_2010_03144_b200 import faults as FT
+    f = F.synth_field("mixed", (16, 14, 12), seed=21) if hasattr(F, "synth_field") else None
+    if f is None:
+        x = np.random.default_rng(3).standard_normal((16, 14, 12)).astype(np.float32)
+        f = F.Field.from_array(x)
+    eb = F.ErrorBound.absolute(1e-3)
+    for tgt in ("input", "bins", "decomp"):
+        for seed in range(3):
+            plan = FT.InjectionPlan(target=tgt, seed=seed)
+            o0 = FT.run_trial(f, eb, F.FtConfig(block_edge=5), plan)
+            o1 = FT.run_trial(f, eb, F.FtConfig(block_edge=5, codec_id=1), plan)
+            assert o0.classification == o1.classification
+            assert o0.corrected == o1.corrected
+            assert o0.max_abs_error == o1.max_abs_error
+            assert o0.bit_identical_output == o1.bit_identical_output
