@@ -112,7 +112,7 @@ typedef struct ftlz_config {
     int32_t duplicate_eval;
     int32_t store_sum_dc;
     int32_t block_edge;     /* 2..64, default 10 (core.py:18-20) */
-    int32_t codec_id;       /* only 0 (identity) is on the device path */
+    int32_t codec_id;       /* 0 identity, 1 run-length pairs; 2 (zlib) -> FTLZ_ERR_UNSUPPORTED_CODEC */
     uint32_t bin_capacity;  /* power of two >= 4, default 65536 */
     int32_t reserved;
 } ftlz_config;
