@@ -593,31 +593,21 @@ FTLZ_DEV u64 br_peek64(const BitReader& R, u32 pos) {
     return sh ? ((hi << sh) | ((u64)w2 >> (32 - sh))) : hi;
 }
 
-struct DecTables {
-    const u32* lut;
-    int T, maxlen;
-    const u64* first;
-    const u32* count;
-    const u32* base;
-    const u32* dsym;
-};
+// canonical decode tables of k_decode's slow path, at namespace scope so the path needs no
+// registers for them across the symbol loop (k_decode fills them once per CTA)
+__shared__ u64 s_dec_first[64];
+__shared__ u32 s_dec_count[64], s_dec_base[64];
+__shared__ int s_dec_T, s_dec_maxlen;
 
-// decode one symbol whose code starts at relative bit `cur` (the window is positioned there);
-// returns its length (0 = outside the code space)
-FTLZ_DEV int decode_sym(BitReader& R, const DecTables& D, u32 cur, u32* sym) {
-    u32 e = D.lut[R.win >> (64 - D.T)];
-    if (e) {
-        int l = (int)(e & 63);
-        *sym = e >> 8;
-        br_consume(R, l);
-        return l;
-    }
-    u64 bits = br_peek64(R, cur);
-    for (int l = D.T + 1; l <= D.maxlen; l++) {
-        u64 code = bits >> (64 - l);
-        u64 d = code - D.first[l];
-        if (d < (u64)D.count[l]) {
-            *sym = D.dsym[D.base[l] + d];
+// a code longer than the table (or outside the code space: 0) at relative bit `cur`
+FTLZ_DEV int decode_sym_slow(BitReader& R, const u32* dsym, u32 cur, u32* sym) {
+    const u64 bits = br_peek64(R, cur);
+    const int T = s_dec_T, maxlen = s_dec_maxlen;
+    for (int l = T + 1; l <= maxlen; l++) {
+        const u64 code = bits >> (64 - l);
+        const u64 d = code - s_dec_first[l];
+        if (d < (u64)s_dec_count[l]) {
+            *sym = dsym[s_dec_base[l] + d];
             br_seek(R, cur + l);
             return l;
         }
@@ -664,15 +654,13 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
     const int T = (int)A.info[DI_T];
     u32* s_lut = (u32*)dsm;
     float* stage_all = (float*)(dsm + ((size_t)4 << DEC_TBITS));
-    __shared__ u64 s_first[64];
-    __shared__ u32 s_count[64], s_base[64];
     __shared__ long long s_rbase[DEC_WARPS][32];
     __shared__ int s_rlen[DEC_WARPS][32], s_rbx[DEC_WARPS][32], s_rby[DEC_WARPS][32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int x = tid; x < (1 << T); x += blockDim.x) s_lut[x] = A.lut[x];
-    if (tid < 64) { s_first[tid] = A.first_code[tid]; s_count[tid] = A.lcount[tid]; s_base[tid] = A.lbase[tid]; }
+    if (tid < 64) { s_dec_first[tid] = A.first_code[tid]; s_dec_count[tid] = A.lcount[tid]; s_dec_base[tid] = A.lbase[tid]; }
+    if (tid == 0) { s_dec_T = T; s_dec_maxlen = (int)A.info[DI_MAXLEN]; }
     __syncthreads();
-    const DecTables D = {s_lut, T, (int)A.info[DI_MAXLEN], s_first, s_count, s_base, A.dsym};
     u32 lut_sa;
     asm volatile("mov.u32 %0, %1;" : "=r"(lut_sa) : "r"(smem_u32(s_lut)));   // keep in a register
     const int lsh = 64 - T;
@@ -760,7 +748,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
                     br_consume(R, l);
                 } else {
                     if (consumed > bl) { err = FTLZ_K_D_RAN_PAST; break; }
-                    l = decode_sym(R, D, pos0 + consumed, &sym);
+                    l = decode_sym_slow(R, A.dsym, pos0 + consumed, &sym);
                     if (l == 0) { err = FTLZ_K_D_OUTSIDE; break; }
                 }
                 consumed += (u32)l;
