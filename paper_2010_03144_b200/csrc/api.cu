@@ -536,10 +536,20 @@ static void report_reset(ftlz_report* r) {
 // ------------------------------------------------------------------------------------------
 // core compress on a carved workspace.  `plan_dev` may point into the workspace (stateless
 // API) or into a context cache; if `upload` the plan is copied there first.
+// Optional upload overlap (UlOverlap): the host input is copied to d_in in slabs of block
+// layers on a second stream, and k_prep runs on each slab as soon as it has arrived.
+struct UlOverlap {
+    const float* h_in = nullptr;
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev[8] = {};
+    int nslab = 0;
+};
+
 static int compress_core(const HostPlan& P, const DevPlan* cached, const float* d_in, int32_t eb_mode,
                          double eb_value, const ftlz_config* cfg, const ftlz_fault* faults, int64_t nf,
                          const int8_t* ovr, unsigned char* ws, size_t ws_size, uint8_t* d_out, size_t out_cap,
-                         ftlz_report* rep, cudaStream_t s, unsigned char* h_result, Profiler* prof = nullptr) {
+                         ftlz_report* rep, cudaStream_t s, unsigned char* h_result, Profiler* prof = nullptr,
+                         const UlOverlap* ul = nullptr) {
     Profiler noprof;
     Profiler& PF = prof ? *prof : noprof;
     report_reset(rep);
@@ -620,9 +630,27 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     S.keys = (u64*)(ws + L.cb_keys); S.syms = (u32*)(ws + L.cb_syms); S.w = (u64*)(ws + L.cb_w);
     S.parent = (u32*)(ws + L.cb_parent); S.lens = ws + L.cb_lens;
 
-    PF.mark("k_prep", s);
-    k_prep<<<(unsigned)num_sms(), 32 * K.pp_warps, K.pp_smem, s>>>(A, tmap);
-    LCHK("k_prep");
+    {
+        const int nslab = ul && ul->h_in ? std::max(1, std::min<int>(ul->nslab, (int)g.cx)) : 1;
+        const long long layer = g.cy * g.cz, plane = g.ny * g.nz;
+        for (int si = 0; si < nslab; si++) {
+            const long long l0 = g.cx * si / nslab, l1 = g.cx * (si + 1) / nslab;
+            if (ul && ul->h_in) {
+                const long long x0 = l0 * g.e, x1 = std::min<long long>(l1 * g.e, g.nx);
+                CK(cudaMemcpyAsync((float*)d_in + x0 * plane, ul->h_in + x0 * plane, (size_t)(x1 - x0) * plane * 4,
+                                   cudaMemcpyHostToDevice, ul->cs));
+                CK(cudaEventRecord(ul->ev[si], ul->cs));
+                CK(cudaStreamWaitEvent(s, ul->ev[si], 0));
+            }
+            A.pb0 = l0 * layer;
+            A.pb1 = l1 * layer;
+            PF.mark("k_prep", s);
+            k_prep<<<(unsigned)num_sms(), 32 * K.pp_warps, K.pp_smem, s>>>(A, tmap);
+            LCHK("k_prep");
+        }
+        A.pb0 = 0;
+        A.pb1 = g.nb;
+    }
     PF.mark("k_resolve", s);
     k_resolve<<<1, 1, 0, s>>>(A);
     LCHK("k_resolve");
@@ -1338,7 +1366,7 @@ extern "C" void* ftlz_ctx_stream(ftlz_ctx* c) { return c ? (void*)c->stream : nu
 
 static int ctx_compress(ftlz_ctx* c, const float* d_in, int64_t nx, int64_t ny, int64_t nz, int32_t eb_mode,
                         double eb_value, const ftlz_config* cfg, const ftlz_fault* faults, int64_t nf,
-                        const int8_t* ovr, ftlz_report* rep) {
+                        const int8_t* ovr, ftlz_report* rep, const UlOverlap* ul = nullptr) {
     c->prof.mark("c_host_prelude", c->stream);
     int rc = ctx_plan(c, nx, ny, nz, cfg->block_edge);
     if (rc) {
@@ -1351,7 +1379,7 @@ static int ctx_compress(ftlz_ctx* c, const float* d_in, int64_t nx, int64_t ny, 
     size_t bound = ftlz_compress_bound(nx, ny, nz, cfg);
     if ((rc = c->out.ensure(bound))) return rc;
     rc = compress_core(c->hp, &c->dp, d_in, eb_mode, eb_value, cfg, faults, nf, ovr, (unsigned char*)c->ws.p,
-                       c->ws.n, (uint8_t*)c->out.p, c->out.n, rep, c->stream, (unsigned char*)c->h_res.p, &c->prof);
+                       c->ws.n, (uint8_t*)c->out.p, c->out.n, rep, c->stream, (unsigned char*)c->h_res.p, &c->prof, ul);
     c->arch_len = rc == FTLZ_OK ? (size_t)rep->archive_len : 0;
     c->arch_on_host = false;
     return rc;
@@ -1363,6 +1391,18 @@ extern "C" int ftlz_ctx_compress_device(ftlz_ctx* c, const float* d_in, int64_t 
     std::lock_guard<std::mutex> g(c->mu);
     cudaSetDevice(c->device);
     return ctx_compress(c, d_in, nx, ny, nz, eb_mode, eb_value, cfg, faults, nf, ovr, rep);
+}
+
+// overlapped upload of a host field into c->in (UlOverlap), large fields only
+static void ctx_upload_plan(ftlz_ctx* c, const float* h_in, size_t n, UlOverlap& ul) {
+    if (!c->cs) {
+        cudaStreamCreateWithFlags(&c->cs, cudaStreamNonBlocking);
+        for (auto& e : c->ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    }
+    ul.h_in = h_in;
+    ul.cs = c->cs;
+    for (int i = 0; i < 8; i++) ul.ev[i] = c->ev[i];
+    ul.nslab = n >= ((size_t)64 << 20) ? 4 : 1;
 }
 
 extern "C" int ftlz_ctx_compress_host(ftlz_ctx* c, const float* h_in, int64_t nx, int64_t ny, int64_t nz,
@@ -1378,8 +1418,9 @@ extern "C" int ftlz_ctx_compress_host(ftlz_ctx* c, const float* h_in, int64_t nx
     size_t nbytes = (size_t)nx * ny * nz * 4;
     int rc = c->in.ensure(nbytes);
     if (rc) return rc;
-    CK(cudaMemcpyAsync(c->in.p, h_in, nbytes, cudaMemcpyHostToDevice, c->stream));
-    rc = ctx_compress(c, (const float*)c->in.p, nx, ny, nz, eb_mode, eb_value, cfg, faults, nf, ovr, rep);
+    UlOverlap ul;
+    ctx_upload_plan(c, h_in, nbytes / 4, ul);
+    rc = ctx_compress(c, (const float*)c->in.p, nx, ny, nz, eb_mode, eb_value, cfg, faults, nf, ovr, rep, &ul);
     if (rc) return rc;
     if ((rc = c->h_arch.ensure(c->arch_len))) return rc;
     CK(cudaMemcpyAsync(c->h_arch.p, c->out.p, c->arch_len, cudaMemcpyDeviceToHost, c->stream));
@@ -1402,8 +1443,9 @@ extern "C" int ftlz_ctx_compress_host_to(ftlz_ctx* c, const float* h_in, int64_t
     size_t nbytes = (size_t)nx * ny * nz * 4;
     int rc = c->in.ensure(nbytes);
     if (rc) return rc;
-    CK(cudaMemcpyAsync(c->in.p, h_in, nbytes, cudaMemcpyHostToDevice, c->stream));
-    rc = ctx_compress(c, (const float*)c->in.p, nx, ny, nz, eb_mode, eb_value, cfg, faults, nf, ovr, rep);
+    UlOverlap ul;
+    ctx_upload_plan(c, h_in, nbytes / 4, ul);
+    rc = ctx_compress(c, (const float*)c->in.p, nx, ny, nz, eb_mode, eb_value, cfg, faults, nf, ovr, rep, &ul);
     if (rc) return rc;
     // the archive stays on the device for ftlz_ctx_copy_archive when it does not fit
     if (c->arch_len > out_capacity) return set_err(FTLZ_ERR_CAPACITY, "destination too small");

@@ -69,6 +69,7 @@ struct CompArgs {
     u32* hist;           // cap entries
     u64* enc;            // cap entries: code << 6 | len (0 = absent)
     u64* layout;         // archive layout (see LAYOUT_*)
+    long long pb0, pb1;  // k_prep's blocks (slabs of block layers when the upload is overlapped)
     u64* lookback;       // encode tiles
     u16* bins;
     u32* unp_scratch;    // nb * vmax (sparse)

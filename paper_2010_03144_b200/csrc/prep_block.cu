@@ -135,18 +135,20 @@ __global__ void __launch_bounds__(640, 1) k_prep(const __grid_constant__ CompArg
     u32 nreg = 0;
     int last_xid = -1;
     const long long NW = (long long)gridDim.x * nw;
-    long long b = (long long)blockIdx.x * nw + warp;
+    // blocks [pb0, pb1): the whole field, or one slab of block layers whose input has arrived
+    const long long pb1 = A.pb1;
+    long long b = A.pb0 + (long long)blockIdx.x * nw + warp;
     BlockInfo Bnext = block_info(g, b);
-    if (b < g.nb) ws.issue(A.x, g, S, &tmap, Bnext, 0, lane);
+    if (b < pb1) ws.issue(A.x, g, S, &tmap, Bnext, 0, lane);
     int buf = 0;
-    while (b < g.nb) {
+    while (b < pb1) {
         const BlockInfo B = Bnext;
         const long long bn = b + NW;
-        if (PREP_NBUF == 2 && bn < g.nb) {
+        if (PREP_NBUF == 2 && bn < pb1) {
             Bnext = block_info(g, bn);
             ws.issue(A.x, g, S, &tmap, Bnext, buf ^ 1, lane);
         }
-        ws.wait(S, buf, PREP_NBUF == 2 && bn < g.nb);
+        ws.wait(S, buf, PREP_NBUF == 2 && bn < pb1);
         bool issued = false;
         float* tile = (float*)(slot + buf * S.tile_bytes);
         const int bx = B.bx, by = B.by, bz = B.bz, vol = B.vol;
@@ -322,7 +324,7 @@ __global__ void __launch_bounds__(640, 1) k_prep(const __grid_constant__ CompArg
                 al[q] = fabs(__dadd_rn(v, -pl));
             }
             __syncwarp();
-            if (PREP_NBUF == 1 && bn < g.nb) {   // the tile is free: start the next block's copy
+            if (PREP_NBUF == 1 && bn < pb1) {   // the tile is free: start the next block's copy
                 Bnext = block_info(g, bn);
                 ws.issue(A.x, g, S, &tmap, Bnext, 0, lane);
                 issued = true;
@@ -403,7 +405,7 @@ __global__ void __launch_bounds__(640, 1) k_prep(const __grid_constant__ CompArg
             A.coef[bb] = cf;
         }
         __syncwarp();
-        if (PREP_NBUF == 1 && !issued && bn < g.nb) {
+        if (PREP_NBUF == 1 && !issued && bn < pb1) {
             Bnext = block_info(g, bn);
             ws.issue(A.x, g, S, &tmap, Bnext, 0, lane);
         }
