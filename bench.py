@@ -493,12 +493,21 @@ def run_c5(F, L, _lib, torch, local):
         t2 = time.perf_counter()
         return data, out, rc, rd, t1 - t0, t2 - t1
 
-    clean = run(None)
+    run(None)  # warm-up: first-call workspace and plan setup stay out of the timed runs
+
+    def timed(target, reps=3):
+        rs = [run(target) for _ in range(reps)]
+        tc = statistics.median(r[4] for r in rs)
+        td = statistics.median(r[5] for r in rs)
+        return rs[-1][:4] + (tc, td)
+
+    clean = timed(None)
     res = {"field": "c2 GRF 100x500x500, rel eb 1e-3", "plan": "seed 12345, 1% of blocks, bits 0..31",
-           "n_injected": len(injected)}
+           "n_injected": len(injected),
+           "timing": "wall clock of compress+serialize+parse+decompress on host arrays, median of 3 after a warm-up"}
     man = json.load(open(os.path.join(ROOT, "tests", "golden", "manifest.json")))["large"].get("c5", {})
     for tgt in ("input", "bins", "decomp"):
-        data, out, rc, rd, tc, td = run(tgt)
+        data, out, rc, rd, tc, td = timed(tgt)
         rep = {"input": rc.input_corrected, "bins": rc.bins_corrected, "decomp": rd.decomp_block_reexecuted}[tgt]
         det = len(set(rep) & set(injected)) / len(injected)
         same_arch = data == clean[0]
@@ -507,7 +516,8 @@ def run_c5(F, L, _lib, torch, local):
         r = {"detected_corrected": det, "reported_equals_injected": sorted(rep) == injected,
              "archive_bit_identical": bool(same_arch), "output_bit_identical": bool(same_out),
              "max_abs_error": err, "eb": rc_eb(data),
-             "time_overhead": ((tc + td) - (clean[4] + clean[5])) / (clean[4] + clean[5])}
+             "time_overhead": ((tc + td) - (clean[4] + clean[5])) / (clean[4] + clean[5]),
+             "ms": 1e3 * (tc + td), "fault_free_ms": 1e3 * (clean[4] + clean[5])}
         if tgt in man:
             r["reference_archive_match"] = synth.sha256(np.frombuffer(data, np.uint8)) == man[tgt]["archive_sha256"]
         res[tgt] = r
