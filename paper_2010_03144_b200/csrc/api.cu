@@ -367,8 +367,9 @@ static int kernel_attrs_once() {
         setmax((const void*)k_enc_len);
         setmax((const void*)k_enc_pack);
         setmax((const void*)k_parse_tail);
-        setmax((const void*)k_decode<false>);
-        setmax((const void*)k_decode<true>);
+        setmax((const void*)k_decode<false, false>);
+        setmax((const void*)k_decode<false, true>);
+        setmax((const void*)k_decode<true, false>);
         setmax((const void*)k_recon_g<32>);
         setmax((const void*)k_recon_g<128>);
         if (cudaGetLastError() != cudaSuccess) rc = FTLZ_ERR_CUDA;
@@ -1017,8 +1018,8 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
             A.sb1 = l1 * layer;
             const unsigned dgrid = (unsigned)((A.sb1 - A.sb0 + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32));
             PF.mark("k_decode", s);
-            if (A.n_faults) k_decode<true><<<dgrid, DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
-            else k_decode<false><<<dgrid, DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
+            if (A.n_faults) k_decode<true, false><<<dgrid, DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
+            else k_decode<false, true><<<dgrid, DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
             LCHK("k_decode");
             PF.mark("k_recon_warp", s);
             k_recon_g<128><<<sms * 4, 128, rslot, s>>>(A, 0);
@@ -1065,6 +1066,19 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         unsigned char k;
         long long a2[2];
         CK(cudaMemcpy(&k, ws + L.dflag + b, 1, cudaMemcpyDeviceToHost));
+        if (k == DF_PENDING) {
+            // failed on the fast reader: the masked reader (which fails on exactly the same
+            // blocks) names the kind and its arguments
+            const u32 bb = (u32)b;
+            CK(cudaMemcpy(ws + L.mis, &bb, 4, cudaMemcpyHostToDevice));
+            A.region = 1;
+            A.n_faults = 0;
+            k_decode<false, false><<<1, DEC_WARPS * 32, dec_smem, s>>>(A, (const u32*)(ws + L.mis), 1);
+            LCHK("k_decode");
+            CK(cudaStreamSynchronize(s));
+            CK(cudaMemcpy(&k, ws + L.dflag + b, 1, cudaMemcpyDeviceToHost));
+            if (k == DF_PENDING) return set_err(FTLZ_ERR_INVARIANT, "fast and masked decoders disagree");
+        }
         CK(cudaMemcpy(&a2[0], ws + L.da + 8 * b, 8, cudaMemcpyDeviceToHost));
         CK(cudaMemcpy(&a2[1], ws + L.db + 8 * b, 8, cudaMemcpyDeviceToHost));
         rep->sdc = 1;
@@ -1080,7 +1094,7 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         std::sort(mis.begin(), mis.end());
         CK(cudaMemcpy(ws + L.mis, mis.data(), 4 * (size_t)nmis, cudaMemcpyHostToDevice));
         A.n_faults = 0;
-        k_decode<false><<<(unsigned)((nmis + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32)), DEC_WARPS * 32, dec_smem, s>>>(
+        k_decode<false, false><<<(unsigned)((nmis + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32)), DEC_WARPS * 32, dec_smem, s>>>(
             A, (const u32*)(ws + L.mis), (int)nmis);
         LCHK("k_decode");
         k_recon_g<32><<<(unsigned)std::min<u32>((nmis + rw - 1) / rw, sms * 4), rw * 32, rslot * rw, s>>>(A, 1);
@@ -1143,7 +1157,7 @@ static int region_core(const HostPlan& P, const DevPlan& D, const uint8_t* d_a, 
     const size_t dec_smem = ((size_t)4 << DEC_TBITS) + (size_t)DEC_WARPS * 32 * g.e * 4;
     const size_t rslot = al16((size_t)g.vmax * 8) + al16((size_t)g.vmax * 4) + al16(2 * (size_t)g.nvmax8);
     const int rw = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / rslot));
-    k_decode<false><<<(n + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32), DEC_WARPS * 32, dec_smem, s>>>(A, A.region_list, (int)n);
+    k_decode<false, false><<<(n + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32), DEC_WARPS * 32, dec_smem, s>>>(A, A.region_list, (int)n);
     LCHK("k_decode");
     k_recon_g<32><<<std::min<u32>((n + rw - 1) / rw, (u32)sms * 4), rw * 32, rslot * rw, s>>>(A, 2);
     LCHK("k_recon");
@@ -1168,7 +1182,7 @@ static int region_core(const HostPlan& P, const DevPlan& D, const uint8_t* d_a, 
         std::sort(mis.begin(), mis.end());
         CK(cudaMemcpy(ws + L.mis, mis.data(), 4 * (size_t)nmis, cudaMemcpyHostToDevice));
         A.region = 0;   // re-decode failures mark mflag = 3
-        k_decode<false><<<(nmis + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32), DEC_WARPS * 32, dec_smem, s>>>(
+        k_decode<false, false><<<(nmis + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32), DEC_WARPS * 32, dec_smem, s>>>(
             A, (const u32*)(ws + L.mis), (int)nmis);
         LCHK("k_decode");
         k_recon_g<32><<<std::min<u32>((nmis + rw - 1) / rw, (u32)sms * 4), rw * 32, rslot * rw, s>>>(A, 3);

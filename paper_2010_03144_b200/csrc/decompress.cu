@@ -527,6 +527,8 @@ FTLZ_DEV u32 br_word(const BitReader& R, u32 n, u32 raw) {
 }
 FTLZ_DEV u32 br_load(const BitReader& R, u32 n) { return n <= R.endw && (n < R.endw || R.emask) ? __ldg(R.w + n) : 0u; }
 
+FTLZ_DEV void br_prefetch_ptr(const u32* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 // L2 prefetch of the 128-byte line holding word n of the slice (no register, no scoreboard)
 FTLZ_DEV void br_prefetch(const BitReader& R, u32 n) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(R.w + n));
@@ -615,6 +617,84 @@ FTLZ_DEV int decode_sym_slow(BitReader& R, const u32* dsym, u32 cur, u32* sym) {
     return 0;
 }
 
+// ------------------------------------------------------------------------------------------
+// Fast bit reader of the fault-free full path.  Same MSB-first window, but with no masking at
+// the slice end: bits past the slice read as whatever the buffer holds (words past the buffer
+// read as zero).  A block that decodes with consumed == bit_length, every code found and the
+// right zero count had every code inside [start, start + bit_length), where both readers see
+// the same bits, so its symbols equal the masked reader's; any other outcome is a failure of
+// the masked reader too (contrapositive), and k_decode only marks such a block for the masked
+// reader to classify (DF_PENDING).  Invariant after every refill: have >= 33.
+struct FastReader {
+    const u32* w;     // word 0: the word holding the block's first bit
+    u32 lim;          // words [0, lim) may be loaded (the buffer's words, last one partial)
+    u64 win;
+    int have;
+    u32 nw;           // index of the word held in `raw`
+    u32 raw;          // raw (little-endian) word nw
+};
+
+FTLZ_DEV u32 fr_load(const FastReader& R, u32 n) { return n < R.lim ? __ldg(R.w + n) : 0u; }
+
+FTLZ_DEV void fr_seek(FastReader& R, u32 pos) {
+    const u32 n = pos >> 5;
+    R.win = ((u64)__byte_perm(fr_load(R, n), 0, 0x0123) << 32 | (u64)__byte_perm(fr_load(R, n + 1), 0, 0x0123))
+            << (pos & 31);
+    R.have = 64 - (int)(pos & 31);
+    R.nw = n + 2;
+    if (R.have <= 32) {
+        R.win |= (u64)__byte_perm(fr_load(R, R.nw), 0, 0x0123) << (32 - R.have);
+        R.have += 32;
+        R.nw++;
+    }
+    R.raw = fr_load(R, R.nw);
+}
+
+// relative bit position of the window's first bit
+FTLZ_DEV u32 fr_pos(const FastReader& R) { return R.nw * 32u - (u32)R.have; }
+
+// top up to >= 33 bits: one merge of the held word, one predicated load of the next
+FTLZ_DEV void fr_refill(FastReader& R) {
+    const bool need = R.have <= 32;
+    const u32 v = __byte_perm(R.raw, 0, 0x0123);
+    R.win |= need ? ((u64)v << (32 - R.have)) : 0ull;
+    R.have += need ? 32 : 0;
+    R.nw += need ? 1u : 0u;
+    R.raw = ldg_pred(R.w + R.nw, need && R.nw < R.lim, need ? 0u : R.raw);
+}
+
+// one symbol with at least 12 bits in the window; codes longer than the table re-seek from the
+// absolute position (leaving >= 33 bits); returns false outside the code space
+FTLZ_DEV bool fr_symbol(FastReader& R, u32 lut_sa, int lsh, const u32* dsym, u32& sym) {
+    const u32 ent = lds_u32(lut_sa + 4u * (u32)(R.win >> lsh));
+    if (ent) {
+        const int l = (int)(ent & 63);
+        sym = ent >> 8;
+        R.win <<= l;
+        R.have -= l;
+        return true;
+    }
+    const u32 cur = fr_pos(R);
+    const u32 n = cur >> 5;
+    const u64 hi = ((u64)__byte_perm(fr_load(R, n), 0, 0x0123) << 32) | __byte_perm(fr_load(R, n + 1), 0, 0x0123);
+    const u32 w2 = __byte_perm(fr_load(R, n + 2), 0, 0x0123);
+    const int sh = (int)(cur & 31);
+    const u64 bits = sh ? ((hi << sh) | ((u64)w2 >> (32 - sh))) : hi;
+    const int T = s_dec_T, maxlen = s_dec_maxlen;
+    for (int l = T + 1; l <= maxlen; l++) {
+        const u64 code = bits >> (64 - l);
+        const u64 d = code - s_dec_first[l];
+        if (d < (u64)s_dec_count[l]) {
+            sym = dsym[s_dec_base[l] + d];
+            fr_seek(R, cur + l);
+            return true;
+        }
+    }
+    return false;
+}
+
+#define DF_PENDING 0xffu   // dflag: failed on the fast path, kind not yet classified
+
 FTLZ_DEV float4 load_coef(const u8* a, u64 rec) {
     const u8* p = a + rec + 1;
     float4 c;
@@ -646,8 +726,9 @@ FTLZ_DEV void fail_block(const DecArgs& A, long long b, int kind, long long x, l
 #define MAXE 64
 
 
-template <bool FAULTS>
+template <bool FAULTS, bool FAST>
 __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u32* list, int nlist) {
+    static_assert(!(FAULTS && FAST), "the fast reader serves the fault-free full path only");
     if (dev_failed(A.st)) return;
     extern __shared__ __align__(16) unsigned char dsm[];
     const Geom& g = A.g;
@@ -688,8 +769,22 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
     const u64 last_byte = (rel + bl + 7) >> 3;
     if (valid && last_byte > pay_len) err = FTLZ_K_D_PAST_END;
     BitReader R;
+    FastReader FR;
     const u64 start = pay_off * 8 + rel;
-    const u32 pos0 = br_init(R, pay_base(A), valid && !err ? start : 0, valid && !err ? (pay_off + last_byte) * 8 : 0);
+    u32 pos0;
+    if constexpr (FAST) {
+        const u64 s0 = valid && !err ? start : 0;
+        const u64 w0 = s0 >> 5;
+        const u64 bufw = ((A.codec ? A.pay_cap : A.len) + 3) >> 2;
+        FR.w = (const u32*)pay_base(A) + w0;
+        FR.lim = (u32)(bufw > w0 ? (bufw - w0 < 0xffffffffull ? bufw - w0 : 0xffffffffull) : 0ull);
+        if (!(valid && !err)) FR.lim = 0;
+        pos0 = (u32)(s0 & 31);
+        for (u32 n = 32; n < 96u && n < FR.lim; n += 32) br_prefetch_ptr(FR.w + n);
+        fr_seek(FR, pos0);
+    } else {
+        pos0 = br_init(R, pay_base(A), valid && !err ? start : 0, valid && !err ? (pay_off + last_byte) * 8 : 0);
+    }
     u32 consumed = 0;
     u32 zeros = 0;
     const u32 nunp = valid ? A.unpc[b] : 0;
@@ -735,6 +830,32 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
             // of the full path) or the bin (Lorenzo blocks, re-execution)
             double ab = 0.0, dk = 0.0;
             if (recon_here) ab = __dadd_rn(__dadd_rn(c0, __dmul_rn(c1, int_to_f64(i))), __dmul_rn(c2, int_to_f64(j)));
+            auto emit = [&](u32 sym, int k) {
+                const double pred = __dadd_rn(ab, __dmul_rn(c3, dk));
+                dk = __dadd_rn(dk, 1.0);
+                float v = __double2float_rn(__dadd_rn(pred, __dmul_rn(twoeb, int_to_f64((int)sym - center))));
+                if (sym == 0u)
+                    v = (recon_here && zeros < nunp) ? __uint_as_float((u32)ld_le(A.a + unp_base + 4ull * zeros, 4)) : 0.0f;
+                if (FAULTS && f0 >= 0 && recon_here) v = apply_decomp_faults(A, b, (i * B.by + j) * B.bz + k, f0, v);
+                const u32 word = recon_here ? __float_as_uint(v) : sym;
+                dsum += recon_here ? (u64)word : 0ull;
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(st_sa + 4u * (u32)k), "r"(word) : "memory");
+                zeros += sym == 0;
+            };
+            if constexpr (FAST) {
+                // symbol pairs: one refill per pair (>= 33 bits before, <= 24 consumed)
+                if ((FR.nw & 31u) == 0u && FR.nw + 64u < FR.lim) br_prefetch_ptr(FR.w + FR.nw + 64u);
+                for (int k = 0; k < B.bz; k += 2) {
+                    u32 s0, s1 = 0;
+                    const bool two = k + 1 < B.bz;
+                    if (!fr_symbol(FR, lut_sa, lsh, A.dsym, s0)) { err = DF_PENDING; break; }
+                    if (two && !fr_symbol(FR, lut_sa, lsh, A.dsym, s1)) { err = DF_PENDING; break; }
+                    fr_refill(FR);
+                    emit(s0, k);
+                    if (two) emit(s1, k + 1);
+                }
+                consumed = fr_pos(FR) - pos0;
+            } else
             // The reference tests "ran past the slice" before every symbol.  Here it is tested
             // once per row (below) and before the slow path, the only place another error can
             // arise: symbols decoded past the slice are garbage of a block that fails anyway.
@@ -752,20 +873,11 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
                     if (l == 0) { err = FTLZ_K_D_OUTSIDE; break; }
                 }
                 consumed += (u32)l;
-                const double pred = __dadd_rn(ab, __dmul_rn(c3, dk));
-                dk = __dadd_rn(dk, 1.0);
-                float v = __double2float_rn(__dadd_rn(pred, __dmul_rn(twoeb, int_to_f64((int)sym - center))));
-                if (sym == 0u)
-                    v = (recon_here && zeros < nunp) ? __uint_as_float((u32)ld_le(A.a + unp_base + 4ull * zeros, 4)) : 0.0f;
-                if (FAULTS && f0 >= 0 && recon_here) v = apply_decomp_faults(A, b, (i * B.by + j) * B.bz + k, f0, v);
-                const u32 word = recon_here ? __float_as_uint(v) : sym;
-                dsum += recon_here ? (u64)word : 0ull;
-                asm volatile("st.shared.u32 [%0], %1;" ::"r"(st_sa + 4u * (u32)k), "r"(word) : "memory");
-                zeros += sym == 0;
+                emit(sym, k);
             }
             // past the slice with symbols left (the last symbol's overrun is the reference's
             // consumed != bit_length check at the end)
-            if (!err && consumed > bl && !(i == B.bx - 1 && j == B.by - 1)) err = FTLZ_K_D_RAN_PAST;
+            if (!err && consumed > bl && !(i == B.bx - 1 && j == B.by - 1)) err = FAST ? DF_PENDING : FTLZ_K_D_RAN_PAST;
         }
         __syncwarp();
         if (!mode_list) {
@@ -795,6 +907,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
     }
     if (valid && !err && consumed != bl) { err = FTLZ_K_D_CONSUMED; ea = (long long)consumed; eb2 = (long long)bl; }
     if (valid && !err && zeros != nunp) { err = FTLZ_K_D_ZEROS; ea = zeros; eb2 = nunp; }
+    if (FAST && valid && err && err != FTLZ_K_D_PAST_END) err = DF_PENDING;   // classified by the masked reader
     if (valid && err) {
         if (mode_list && !A.region) A.mflag[b] = 3;
         else fail_block(A, b, err, ea, eb2);
