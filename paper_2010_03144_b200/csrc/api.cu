@@ -1004,7 +1004,7 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         k_parse_tail<<<1, PT_THREADS, 8192 * 8, s>>>(A, 0);
     }
     LCHK("k_parse_tail");
-    size_t dec_smem = ((size_t)4 << DEC_TBITS) + (size_t)DEC_WARPS * 32 * g.e * 4;
+    size_t dec_smem = ((size_t)4 << DEC_TBITS) + (size_t)DEC_WARPS * dec_stage_words((int)g.e) * 4;
     size_t rslot = al16((size_t)g.vmax * 8) + al16((size_t)g.vmax * 4) + al16(2 * (size_t)g.nvmax8);
     int rw = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / rslot));
     if (decode) {
@@ -1154,7 +1154,7 @@ static int region_core(const HostPlan& P, const DevPlan& D, const uint8_t* d_a, 
     A.region_list = (const u32*)(ws + L.rlist);
     A.n_region = n;
     const int sms = num_sms();
-    const size_t dec_smem = ((size_t)4 << DEC_TBITS) + (size_t)DEC_WARPS * 32 * g.e * 4;
+    const size_t dec_smem = ((size_t)4 << DEC_TBITS) + (size_t)DEC_WARPS * dec_stage_words((int)g.e) * 4;
     const size_t rslot = al16((size_t)g.vmax * 8) + al16((size_t)g.vmax * 4) + al16(2 * (size_t)g.nvmax8);
     const int rw = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / rslot));
     k_decode<false, false><<<(n + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32), DEC_WARPS * 32, dec_smem, s>>>(A, A.region_list, (int)n);

@@ -663,8 +663,9 @@ FTLZ_DEV void fr_refill(FastReader& R) {
     R.raw = ldg_pred(R.w + R.nw, need && R.nw < R.lim, need ? 0u : R.raw);
 }
 
-// one symbol with at least 12 bits in the window; codes longer than the table re-seek from the
-// absolute position (leaving >= 33 bits); returns false outside the code space
+// one symbol with at least 12 bits in the window; a code longer than the table is searched in
+// the window when the window holds maxlen bits (then topped up to >= 32 bits), else after a
+// re-seek from the absolute position (>= 33 bits); returns false outside the code space
 FTLZ_DEV bool fr_symbol(FastReader& R, u32 lut_sa, int lsh, const u32* dsym, u32& sym) {
     const u32 ent = lds_u32(lut_sa + 4u * (u32)(R.win >> lsh));
     if (ent) {
@@ -674,13 +675,27 @@ FTLZ_DEV bool fr_symbol(FastReader& R, u32 lut_sa, int lsh, const u32* dsym, u32
         R.have -= l;
         return true;
     }
+    const int T = s_dec_T, maxlen = s_dec_maxlen;
+    if (R.have >= maxlen) {
+        // every code fits in the window's valid bits: search there, then top the window up
+        for (int l = T + 1; l <= maxlen; l++) {
+            const u64 d = (R.win >> (64 - l)) - s_dec_first[l];
+            if (d < (u64)s_dec_count[l]) {
+                sym = dsym[s_dec_base[l] + d];
+                R.win <<= l;
+                R.have -= l;
+                fr_refill(R);
+                return true;
+            }
+        }
+        return false;
+    }
     const u32 cur = fr_pos(R);
     const u32 n = cur >> 5;
     const u64 hi = ((u64)__byte_perm(fr_load(R, n), 0, 0x0123) << 32) | __byte_perm(fr_load(R, n + 1), 0, 0x0123);
     const u32 w2 = __byte_perm(fr_load(R, n + 2), 0, 0x0123);
     const int sh = (int)(cur & 31);
     const u64 bits = sh ? ((hi << sh) | ((u64)w2 >> (32 - sh))) : hi;
-    const int T = s_dec_T, maxlen = s_dec_maxlen;
     for (int l = T + 1; l <= maxlen; l++) {
         const u64 code = bits >> (64 - l);
         const u64 d = code - s_dec_first[l];
@@ -723,6 +738,9 @@ FTLZ_DEV void fail_block(const DecArgs& A, long long b, int kind, long long x, l
 // K6: lane = block.  Warp = 32 consecutive blocks, decoded row by row in lockstep so that the
 // warp's rows (contiguous along z for blocks of one block-row) are written coalesced.
 #define DEC_WARPS 4
+// stage words per warp: 32 rows of e plus up to 3 words of alignment shift per run, 16-byte
+// multiple
+__host__ __device__ inline size_t dec_stage_words(int e) { return ((size_t)32 * e + 96 + 3) & ~(size_t)3; }
 #define MAXE 64
 
 
@@ -736,7 +754,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
     u32* s_lut = (u32*)dsm;
     float* stage_all = (float*)(dsm + ((size_t)4 << DEC_TBITS));
     __shared__ long long s_rbase[DEC_WARPS][32];
-    __shared__ int s_rlen[DEC_WARPS][32], s_rbx[DEC_WARPS][32], s_rby[DEC_WARPS][32];
+    __shared__ int s_rlen[DEC_WARPS][32], s_rbx[DEC_WARPS][32], s_rby[DEC_WARPS][32], s_rpad[DEC_WARPS][32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int x = tid; x < (1 << T); x += blockDim.x) s_lut[x] = A.lut[x];
     if (tid < 64) { s_dec_first[tid] = A.first_code[tid]; s_dec_count[tid] = A.lcount[tid]; s_dec_base[tid] = A.lbase[tid]; }
@@ -745,7 +763,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
     u32 lut_sa;
     asm volatile("mov.u32 %0, %1;" : "=r"(lut_sa) : "r"(smem_u32(s_lut)));   // keep in a register
     const int lsh = 64 - T;
-    float* stage = stage_all + (size_t)warp * 32 * g.e;
+    float* stage = stage_all + (size_t)warp * dec_stage_words(g.e);
     long long b;
     bool valid;
     const bool mode_list = list != nullptr;
@@ -820,8 +838,28 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
         }
         __syncwarp();
     }
+    // 16-byte write-back: when every row start is congruent mod 4 floats to its block's first
+    // row (nz % 4 == 0) each run's stage rows are shifted by 0..3 floats so that stage and
+    // output share the alignment mod 16 bytes (P_h: cumulative shift up to run h)
+    const bool vec = !mode_list && (g.nz & 3) == 0 && ((size_t)A.out & 15) == 0;
+    int soff = lane * e;
+    if (vec) {
+        if (lane == 0) {
+            int P = 0;
+            unsigned hm = heads;
+            while (hm) {
+                const int h = __ffs(hm) - 1;
+                hm &= hm - 1;
+                P += (int)((s_rbase[warp][h] - (long long)(h * e + P)) & 3);
+                s_rpad[warp][h] = P;
+            }
+        }
+        __syncwarp();
+        const unsigned mine = heads & ((2u << lane) - 1u);
+        if (mine) soff += s_rpad[warp][31 - __clz(mine)];
+    }
     u32 st_sa;
-    asm volatile("mov.u32 %0, %1;" : "=r"(st_sa) : "r"(smem_u32(stage + lane * e)));   // keep in a register
+    asm volatile("mov.u32 %0, %1;" : "=r"(st_sa) : "r"(smem_u32(stage + soff)));   // keep in a register
     int i = 0, j = 0;
     for (int r = 0; r < e * e; r++) {
         const bool act = valid && !err && i < B.bx && j < B.by;
@@ -881,21 +919,34 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
         }
         __syncwarp();
         if (!mode_list) {
+            const long long rowoff = ((long long)i * g.ny + j) * g.nz;
             unsigned hm = heads;
             while (hm) {
                 const int h = __ffs(hm) - 1;
                 hm &= hm - 1;
                 if (i < s_rbx[warp][h] && j < s_rby[warp][h]) {
                     const int L = s_rlen[warp][h];
-                    const long long base = s_rbase[warp][h] + ((long long)i * g.ny + j) * g.nz;
-                    for (int o = lane; o < L; o += 32) A.out[base + o] = stage[h * e + o];
+                    const long long base = s_rbase[warp][h] + rowoff;
+                    if (vec) {
+                        const float* src = stage + h * e + s_rpad[warp][h];
+                        float* dst = A.out + base;
+                        const int a0 = min((int)((-base) & 3), L);
+                        const int n4 = (L - a0) >> 2, t0 = a0 + 4 * n4;
+                        if (lane < a0) dst[lane] = src[lane];
+                        if (lane < L - t0) dst[t0 + lane] = src[t0 + lane];
+                        const float4* s4 = (const float4*)(src + a0);
+                        float4* d4 = (float4*)(dst + a0);
+                        for (int o = lane; o < n4; o += 32) d4[o] = s4[o];
+                    } else {
+                        for (int o = lane; o < L; o += 32) A.out[base + o] = stage[h * e + o];
+                    }
                 }
             }
         }
         if (act && !recon_here) {
             // bins of this row to scratch (Lorenzo blocks are reconstructed by k_recon_g, whose
             // output overwrites the run copy above)
-            const u32* sw = (const u32*)stage + lane * e;
+            const u32* sw = (const u32*)stage + soff;
             const int pbase = (i * B.by + j) * B.bz;
             for (int k = 0; k < B.bz; k++) A.bins[bins_index(g, b, pbase + k)] = (u16)sw[k];
         }
