@@ -656,8 +656,8 @@ FTLZ_DEV u32 fr_pos(const FastReader& R) { return R.nw * 32u - (u32)R.have; }
 // top up to >= 33 bits: one merge of the held word, one predicated load of the next
 FTLZ_DEV void fr_refill(FastReader& R) {
     const bool need = R.have <= 32;
-    const u32 v = __byte_perm(R.raw, 0, 0x0123);
-    R.win |= need ? ((u64)v << (32 - R.have)) : 0ull;
+    const u32 v = need ? __byte_perm(R.raw, 0, 0x0123) : 0u;
+    R.win |= (u64)v << ((32 - R.have) & 63);
     R.have += need ? 32 : 0;
     R.nw += need ? 1u : 0u;
     R.raw = ldg_pred(R.w + R.nw, need && R.nw < R.lim, need ? 0u : R.raw);
@@ -860,6 +860,9 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
     }
     u32 st_sa;
     asm volatile("mov.u32 %0, %1;" : "=r"(st_sa) : "r"(smem_u32(stage + soff)));   // keep in a register
+    // warp-uniform row shapes of the fast path: all rows of 10 (unrolled pairs) or all even
+    const bool rows10 = FAST && __all_sync(0xffffffffu, !valid || B.bz == 10);
+    const bool rows_even = FAST && __all_sync(0xffffffffu, !valid || (B.bz & 1) == 0);
     int i = 0, j = 0;
     for (int r = 0; r < e * e; r++) {
         const bool act = valid && !err && i < B.bx && j < B.by;
@@ -881,16 +884,60 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
                 zeros += sym == 0;
             };
             if constexpr (FAST) {
-                // symbol pairs: one refill per pair (>= 33 bits before, <= 24 consumed)
-                if ((FR.nw & 31u) == 0u && FR.nw + 64u < FR.lim) br_prefetch_ptr(FR.w + FR.nw + 64u);
-                for (int k = 0; k < B.bz; k += 2) {
-                    u32 s0, s1 = 0;
-                    const bool two = k + 1 < B.bz;
-                    if (!fr_symbol(FR, lut_sa, lsh, A.dsym, s0)) { err = DF_PENDING; break; }
-                    if (two && !fr_symbol(FR, lut_sa, lsh, A.dsym, s1)) { err = DF_PENDING; break; }
+                // Unpredictable points (bin 0) are rare: the symbol loop only records them in
+                // zmask, and a fix-up after the row puts the stored words in place (and
+                // corrects dsum).  dsum and the word of Lorenzo lanes are left unselected: only
+                // regression lanes use them.
+                u32 zmask = 0;
+                auto femit = [&](u32 sym, int k, double dkv) {
+                    const double pred = __dadd_rn(ab, __dmul_rn(c3, dkv));
+                    const float v = __double2float_rn(__dadd_rn(pred, __dmul_rn(twoeb, int_to_f64((int)sym - center))));
+                    const u32 word = recon_here ? __float_as_uint(v) : sym;
+                    dsum += (u64)word;
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(st_sa + 4u * (u32)k), "r"(word) : "memory");
+                    zmask |= (u32)(sym == 0u) << k;
+                };
+                // symbol pairs: one refill per pair (>= 32 bits before, <= 24 consumed)
+                auto fpair = [&](int k, double dk0, double dk1) -> bool {
+                    u32 s0, s1;
+                    if (!fr_symbol(FR, lut_sa, lsh, A.dsym, s0)) return false;
+                    if (!fr_symbol(FR, lut_sa, lsh, A.dsym, s1)) return false;
                     fr_refill(FR);
-                    emit(s0, k);
-                    if (two) emit(s1, k + 1);
+                    femit(s0, k, dk0);
+                    femit(s1, k + 1, dk1);
+                    return true;
+                };
+                if ((FR.nw & 31u) == 0u && FR.nw + 64u < FR.lim) br_prefetch_ptr(FR.w + FR.nw + 64u);
+                if (rows10) {
+#pragma unroll
+                    for (int k = 0; k < 10; k += 2)
+                        if (!fpair(k, (double)k, (double)(k + 1))) { err = DF_PENDING; break; }
+                } else if (rows_even) {
+                    double dk2 = 0.0;
+                    for (int k = 0; k < B.bz; k += 2) {
+                        if (!fpair(k, dk2, __dadd_rn(dk2, 1.0))) { err = DF_PENDING; break; }
+                        dk2 = __dadd_rn(dk2, 2.0);
+                    }
+                } else {
+                    double dk1 = 0.0;
+                    for (int k = 0; k < B.bz; k++) {
+                        u32 s0;
+                        if (!fr_symbol(FR, lut_sa, lsh, A.dsym, s0)) { err = DF_PENDING; break; }
+                        fr_refill(FR);
+                        femit(s0, k, dk1);
+                        dk1 = __dadd_rn(dk1, 1.0);
+                    }
+                }
+                while (zmask) {
+                    const int k = __ffs(zmask) - 1;
+                    zmask &= zmask - 1;
+                    if (recon_here) {
+                        const u32 w = zeros < nunp ? (u32)ld_le(A.a + unp_base + 4ull * zeros, 4) : 0u;
+                        const u32 old = lds_u32(st_sa + 4u * (u32)k);
+                        asm volatile("st.shared.u32 [%0], %1;" ::"r"(st_sa + 4u * (u32)k), "r"(w) : "memory");
+                        dsum += (u64)w - (u64)old;
+                    }
+                    zeros++;
                 }
                 consumed = fr_pos(FR) - pos0;
             } else
