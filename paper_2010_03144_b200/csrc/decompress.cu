@@ -894,7 +894,9 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
                     const float v = __double2float_rn(__dadd_rn(pred, __dmul_rn(twoeb, int_to_f64((int)sym - center))));
                     const u32 word = recon_here ? __float_as_uint(v) : sym;
                     dsum += (u64)word;
-                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(st_sa + 4u * (u32)k), "r"(word) : "memory");
+                    // no memory clobber: the stores may move within the row (the row ends with
+                    // an explicit compiler barrier before the write-back reads)
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(st_sa + 4u * (u32)k), "r"(word));
                     zmask |= (u32)(sym == 0u) << k;
                 };
                 // symbol pairs: one refill per pair (>= 32 bits before, <= 24 consumed)
@@ -928,6 +930,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
                         dk1 = __dadd_rn(dk1, 1.0);
                     }
                 }
+                asm volatile("" ::: "memory");
                 while (zmask) {
                     const int k = __ffs(zmask) - 1;
                     zmask &= zmask - 1;
