@@ -356,17 +356,68 @@ FTLZ_DEV void pack_range_s(const EncWin& W, const u16* sym16, const u32* sym32, 
     if (nacc > 0) put_s(sbase + 4u * widx, (u32)(acc >> 32), false, true);
 }
 
+// symbol pairs around the centre: one shared lookup appends two codes.  Entry (a, c) of the
+// PAIR_W x PAIR_W table is (code_a code_c) << 5 | (len_a + len_c) when both symbols are in the
+// codebook and the pair fits in 27 bits, else 0 (the pair goes through the single-symbol table).
+#define PAIR_W 32
+#define PAIR_BYTES (4 * PAIR_W * PAIR_W)
+
+FTLZ_DEV void enc_fill_pairs(const CompArgs& A, u32* s_pair) {
+    const int plo = A.center - PAIR_W / 2;
+    for (int t = threadIdx.x; t < PAIR_W * PAIR_W; t += blockDim.x) {
+        const int a = plo + t / PAIR_W, c = plo + t % PAIR_W;
+        const u64 ea = (a >= 0 && a < A.cap) ? A.enc[a] : 0ull, ec = (c >= 0 && c < A.cap) ? A.enc[c] : 0ull;
+        const u32 la = (u32)(ea & 63), lc = (u32)(ec & 63);
+        s_pair[t] = (la && lc && la + lc <= 27u) ? (u32)((((ea >> 6) << lc) | (ec >> 6)) << 5) | (la + lc) : 0u;
+    }
+}
+
+// pack_range_s for codes of at most 32 bits.  Every step appends ONE table entry: the pair
+// (p, p + 1) when the pair table holds it (advance 2), else symbol p alone (advance 1), so the
+// lanes of a warp never diverge on a miss; they only run different step counts.
+FTLZ_DEV void pack_range_s2(const EncWin& W, u32 pair_sa, int plo, const u16* sym16, int p0, int pend, u32 pos,
+                            u32 sbase) {
+    u32 widx = pos >> 5;
+    u64 acc = 0;
+    int nacc = (int)(pos & 31);
+    bool first = true;
+    for (int p = p0; p < pend;) {
+        const u32 s0 = sym16[p], s1 = p + 1 < pend ? (u32)sym16[p + 1] : 0xffffffffu;
+        const u32 o0 = s0 - (u32)plo, o1 = s1 - (u32)plo;
+        const bool in = (o0 | o1) < (u32)PAIR_W;
+        u32 pe;
+        asm("ld.shared.u32 %0, [%1];" : "=r"(pe) : "r"(pair_sa + 4u * (in ? o0 * PAIR_W + o1 : 0u)));
+        const bool two = in && pe != 0u;
+        const u64 se = W.get_fast(s0);
+        const u64 code = two ? (u64)(pe >> 5) : se >> 6;
+        const int l = two ? (int)(pe & 31) : (int)(se & 63);
+        p += two ? 2 : 1;
+        acc |= code << (64 - nacc - l);   // l <= 32, nacc < 32
+        nacc += l;
+        const bool full = nacc >= 32;
+        put_s(sbase + 4u * widx, (u32)(acc >> 32), full && !first, full && first);
+        first = first && !full;
+        widx += full ? 1u : 0u;
+        acc = full ? acc << 32 : acc;
+        nacc -= full ? 32 : 0;
+    }
+    if (nacc > 0) put_s(sbase + 4u * widx, (u32)(acc >> 32), false, true);
+}
+
 __global__ void __launch_bounds__(512) k_enc_pack(CompArgs A, const u32* fix, const u8* fixed_flag) {
     extern __shared__ __align__(16) unsigned char smem[];
     if (dev_failed(A.st)) return;
     const Geom& g = A.g;
     u64* s_enc = (u64*)smem;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    u16* sym16 = (u16*)(smem + 8 * ENC_WIN + (size_t)warp * 4 * g.nvmax8);
+    u32* s_pair = (u32*)(smem + 8 * ENC_WIN);
+    u16* sym16 = (u16*)(smem + 8 * ENC_WIN + PAIR_BYTES + (size_t)warp * 4 * g.nvmax8);
     u32* sym32 = (u32*)sym16;
-    u32* stg = (u32*)(smem + 8 * ENC_WIN + (size_t)nw * 4 * g.nvmax8) + (size_t)warp * ENC_STG;
-    const u32 stg_sa = smem_u32(stg);
+    u32* stg = (u32*)(smem + 8 * ENC_WIN + PAIR_BYTES + (size_t)nw * 4 * g.nvmax8) + (size_t)warp * ENC_STG;
+    const u32 stg_sa = smem_u32(stg), pair_sa = smem_u32(s_pair);
+    const int plo = A.center - PAIR_W / 2;
     enc_fill_window(A, s_enc);
+    enc_fill_pairs(A, s_pair);
     __syncthreads();
     const EncWin W = {s_enc, A.enc, A.center - ENC_WIN / 2, A.cap};
     u32* words = (u32*)A.out;
@@ -412,7 +463,7 @@ __global__ void __launch_bounds__(512) k_enc_pack(CompArgs A, const u32* fix, co
             if (p0 < pend) {
                 if (fixed) pack_range_s<true, true>(W, sym16, sym32, p0, pend, pos, stg_sa);
                 else if (longc) pack_range_s<false, true>(W, sym16, sym32, p0, pend, pos, stg_sa);
-                else pack_range_s<false, false>(W, sym16, sym32, p0, pend, pos, stg_sa);
+                else pack_range_s2(W, pair_sa, plo, sym16, p0, pend, pos, stg_sa);
             }
             __syncwarp();
             for (int i = lane; i < (int)nwords; i += 32) {
