@@ -524,6 +524,14 @@ def run_c5(F, L, _lib, torch, local):
     return res
 
 
+def kernel_base(name: str) -> str:
+    """'void k_decode<0, 1>(DecArgs, ...)' -> 'k_decode' (template arguments and signature dropped)."""
+    import re
+
+    m = re.search(r"\b(k_\w+)", name)
+    return m.group(1) if m else name
+
+
 def ncu_kernels() -> dict:
     """Per-kernel ncu metrics (warp instructions, IPC) of the newest committed capture."""
     import glob
@@ -535,7 +543,7 @@ def ncu_kernels() -> dict:
         except Exception:
             continue
         for k, v in d.get("kernels", {}).items():
-            out[k.split()[-1].split("<")[0]] = dict(v, source=os.path.relpath(f, ROOT))
+            out[kernel_base(k)] = dict(v, source=os.path.relpath(f, ROOT))
     return out
 
 
@@ -553,7 +561,7 @@ def ncu_traffic() -> dict:
         for k, v in d.get("kernels", {}).items():
             if v.get("dram_bytes") is not None:
                 # template instances ("void k_decode<0>") are reported under the kernel's name
-                name = k.split()[-1].split("<")[0]
+                name = kernel_base(k)
                 out[name] = {"dram_bytes": v["dram_bytes"], "source": os.path.relpath(f, ROOT)}
     return out
 
