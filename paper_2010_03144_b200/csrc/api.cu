@@ -396,7 +396,7 @@ struct CompLayout {
     size_t hist, lbflag, events, fixed;
     size_t coef, insum, inisum, ind, unpc, bsum, bisum, dcs, bitlen, lanepre, bitoff, regpre, unppre;
     size_t enc, qp, lbbits, lbreg, lbunp;
-    size_t cb_keys, cb_syms, cb_w, cb_parent, cb_lens;
+    size_t cb_keys, cb_syms, cb_w, cb_parent, cb_lens, cb_bm;
     size_t bins, unp, fix, faults, ffirst, ovr, plan, lor;
     size_t cjobs, tarc, tarc_cap, rle, rle_bound;   // codec 1
     size_t total;
@@ -448,6 +448,7 @@ static CompLayout comp_layout(const HostPlan& P, int cap, int64_t n_faults, int 
     L.cb_syms = take(4 * c);
     L.cb_w = take(16 * c);
     L.cb_parent = take(8 * c);
+    L.cb_bm = take(4 * ((c + 31) / 32));
     L.bins = take(2 * nb * (size_t)g.nvmax8 + 64);
     L.unp = take(4 * nb * (size_t)g.vmax);
     L.fix = take(n_faults ? 4 * nb * (size_t)g.vmax : 0);
@@ -629,7 +630,7 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     A.out_cap = c1 ? L.tarc_cap : out_cap;
     CodebookScratch S;
     S.keys = (u64*)(ws + L.cb_keys); S.syms = (u32*)(ws + L.cb_syms); S.w = (u64*)(ws + L.cb_w);
-    S.parent = (u32*)(ws + L.cb_parent); S.lens = ws + L.cb_lens;
+    S.parent = (u32*)(ws + L.cb_parent); S.lens = ws + L.cb_lens; S.bm = (u32*)(ws + L.cb_bm);
 
     {
         const int nslab = ul && ul->h_in ? std::max(1, std::min<int>(ul->nslab, (int)g.cx)) : 1;
@@ -667,6 +668,7 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     if (nf) k_fault_bins<<<num_sms(), 256, 0, s>>>(A, (u32*)(ws + L.fix), (u8*)(ws + L.fixed));
     LCHK("k_fault_bins");
     PF.mark("k_codebook", s);
+    k_cb_bitmap<<<(unsigned)((cap + 255) / 256), 256, 0, s>>>(A, S.bm);
     k_codebook<<<1, CB_THREADS, (CB_SMEM_KEYS * 3) * 8 + CB_SMEM_KEYS * 2 * 2, s>>>(A, S);
     LCHK("k_codebook");
     PF.mark("k_zero", s);

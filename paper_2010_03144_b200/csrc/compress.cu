@@ -224,29 +224,48 @@ struct CodebookScratch {
     u64* w;        // 2 * cap node weights (leaves then internal)
     u32* parent;   // 2 * cap
     u8* lens;      // cap (by symbol)
+    u32* bm;       // (cap + 31) / 32 words: alphabet bitmap (k_cb_bitmap)
 };
 
 // two-queue Huffman merge over leaves sorted by (weight, symbol) (the reference heap with its
 // (weight, tie) order, encode.py:26-71): leaves 0..n-1, merged nodes n..2n-2; queue heads in
 // registers.  W must point into one memory space (shared or global) so accesses stay typed.
 template <typename SetParent>
-FTLZ_DEV void cb_merge(u64* W, const u64* keys, int n, SetParent set_parent) {
-    for (int i = 0; i < n; i++) W[i] = keys[i] >> 16;
+FTLZ_DEV void cb_merge(u64* W, int n, SetParent set_parent) {
+    // W[0, n) holds the sorted leaf weights.  Queue heads live in registers three deep
+    // (L0..L2 = W[li..li+2], M0..M2 = W[mi..mi+2]; ~0 = none), refilled by selects and loads
+    // issued two pops before their use: a pop is a compare and a rank of selects, no branch
+    // and no wait on shared memory.
+    const u64 INF = ~0ull;
     int li = 0, mi = n, mk = n;   // next leaf, next merged to consume, next merged to create
-    u64 wl = W[0], wm = 0;
+    u64 L0 = W[0], L1 = n > 1 ? W[1] : INF, L2 = n > 2 ? W[2] : INF, M0 = INF, M1 = INF, M2 = INF;
     for (int t = 0; t < n - 1; t++) {
-        int pk0, pk1;
-        u64 pw0, pw1;
-        // leaf wins ties
-        if (li < n && (mi >= mk || wl <= wm)) { pk0 = li; pw0 = wl; li++; wl = li < n ? W[li] : 0; }
-        else { pk0 = mi; pw0 = wm; mi++; wm = mi < mk ? W[mi] : 0; }
-        if (li < n && (mi >= mk || wl <= wm)) { pk1 = li; pw1 = wl; li++; wl = li < n ? W[li] : 0; }
-        else { pk1 = mi; pw1 = wm; mi++; wm = mi < mk ? W[mi] : 0; }
-        const u64 sum = pw0 + pw1;
+        int pk[2];
+        u64 pw[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const bool tl = L0 <= M0;   // a leaf wins a tie
+            const u64 nL = li + 3 < n ? W[li + 3] : INF;
+            const u64 nM = mi + 3 < mk ? W[mi + 3] : INF;
+            pk[h] = tl ? li : mi;
+            pw[h] = tl ? L0 : M0;
+            L0 = tl ? L1 : L0;
+            L1 = tl ? L2 : L1;
+            L2 = tl ? nL : L2;
+            M0 = tl ? M0 : M1;
+            M1 = tl ? M1 : M2;
+            M2 = tl ? M2 : nM;
+            li += tl ? 1 : 0;
+            mi += tl ? 0 : 1;
+        }
+        const u64 sum = pw[0] + pw[1];
         W[mk] = sum;
-        if (mi == mk) wm = sum;   // the merged queue was empty: its head is the new node
-        set_parent(pk0, mk);
-        set_parent(pk1, mk);
+        const int q = mk - mi;   // merged nodes waiting before this one
+        M0 = q == 0 ? sum : M0;
+        M1 = q == 1 ? sum : M1;
+        M2 = q == 2 ? sum : M2;
+        set_parent(pk[0], mk);
+        set_parent(pk[1], mk);
         mk++;
     }
 }
@@ -265,6 +284,18 @@ FTLZ_DEV int cb_select(const u32* bm, const u32* wpre, int nwords, u32 i) {
     return lo * 32 + __ffs(m) - 1;
 }
 
+// alphabet bitmap {0} U {s : hist[s] > 0} over the whole grid: the histogram is read once by
+// all SMs instead of by k_codebook's single CTA (a warp per 32-symbol word, coalesced)
+__global__ void __launch_bounds__(256) k_cb_bitmap(CompArgs A, u32* bm) {
+    if (dev_failed(A.st)) return;
+    const int lane = threadIdx.x & 31;
+    const int w = (int)(blockIdx.x * 8 + (threadIdx.x >> 5));
+    const int sy = w * 32 + lane;
+    if (w * 32 >= A.cap) return;
+    const u32 m = __ballot_sync(0xffffffffu, sy < A.cap && (sy == 0 || A.hist[sy] != 0u));
+    if (lane == 0) bm[w] = m;
+}
+
 __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScratch S) {
     if (dev_failed(A.st)) return;
     extern __shared__ __align__(16) u64 cb_dyn[];   // keys[CB_SMEM_KEYS] | weights[2*CB_SMEM_KEYS]
@@ -277,21 +308,15 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
     __shared__ u64 s_total;
     int cap = A.cap;
     int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // 1) alphabet {0} U {s : hist[s] > 0} in symbol order: a bitmap built from warp ballots
-    //    over coalesced histogram reads, then word-popcount prefixes give every symbol its rank
+    // 1) alphabet {0} U {s : hist[s] > 0} in symbol order: the bitmap of k_cb_bitmap, then
+    //    word-popcount prefixes give every symbol its rank
     // (bitmap and prefixes live in the parent region, which is free before the merge and
     //  after the depth walk; they are rebuilt for the codebook section)
     u32* s_bm = (u32*)(cb_dyn + 3 * CB_SMEM_KEYS);
     u32* s_wpre = s_bm + 2048;
     const int nwords = (cap + 31) >> 5;
     auto build_ranks = [&]() {
-#pragma unroll 4
-        for (int s0 = warp * 32; s0 < nwords * 32; s0 += CB_THREADS) {
-            const int sy = s0 + lane;
-            const bool nz = sy < cap && (sy == 0 || A.hist[sy] > 0);
-            const u32 m = __ballot_sync(0xffffffffu, nz);
-            if (lane == 0) s_bm[s0 >> 5] = m;
-        }
+        for (int w = tid; w < nwords; w += CB_THREADS) s_bm[w] = S.bm[w];
         __syncthreads();
         const u32 c0 = 2 * tid < nwords ? __popc(s_bm[2 * tid]) : 0u;
         const u32 c1 = 2 * tid + 1 < nwords ? __popc(s_bm[2 * tid + 1]) : 0u;
@@ -337,16 +362,21 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
     //    alphabet fits (u16 parents), else in global scratch.
     const bool small = np2 <= CB_SMEM_KEYS;
     u16* par16 = (u16*)(cb_dyn + 3 * CB_SMEM_KEYS);
+    {
+        u64* W = small ? cb_dyn + CB_SMEM_KEYS : S.w;
+        for (int i = tid; i < n; i += CB_THREADS) W[i] = keys[i] >> 16;
+        __syncthreads();
+    }
     if (tid == 0) {
         s_maxlen = 0;
         if (n == 1) {
             if (small) par16[0] = 0xffffu;
             else S.parent[0] = 0xffffffffu;
         } else if (small) {
-            cb_merge(cb_dyn + CB_SMEM_KEYS, keys, n, [&](int i, int mk) { par16[i] = (u16)mk; });
+            cb_merge(cb_dyn + CB_SMEM_KEYS, n, [&](int i, int mk) { par16[i] = (u16)mk; });
             par16[2 * n - 2] = 0xffffu;
         } else {
-            cb_merge(S.w, keys, n, [&](int i, int mk) { S.parent[i] = (u32)mk; });
+            cb_merge(S.w, n, [&](int i, int mk) { S.parent[i] = (u32)mk; });
             S.parent[2 * n - 2] = 0xffffffffu;
         }
     }
