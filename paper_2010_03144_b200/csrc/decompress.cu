@@ -129,19 +129,72 @@ __global__ void k_parse_maps(DecArgs A) {
     }
 }
 
-// map value: exit phase (8 bits) | record count (24 bits); STUCK = error on this path
-FTLZ_DEV u32 compose_walk(const u32* m, int n, u32 state, u32* cnt) {
-    u32 c = 0;
-    for (int i = 0; i < n; i++) {
-        u32 v = m[i * 25 + state];
-        if (v == STUCK) { *cnt = c; return STUCK; }
-        c += v >> 8;
-        state = v & 0xff;
-    }
-    *cnt = c;
-    return state;
+// map value: exit phase (8 bits) | record count (24 bits); STUCK = error on this path.
+// Walking chunk a then chunk b from entry phase s: map_apply(a, b, s).  Composition is
+// associative, so the chunk and super-chunk walks are tree reductions / scans over maps.
+FTLZ_DEV u32 map_apply(const u32* f, const u32* g, int s) {
+    const u32 v = f[s];
+    if (v == STUCK) return STUCK;
+    const u32 w = g[v & 0xff];
+    return w == STUCK ? STUCK : ((w & 0xff) | (((v >> 8) + (w >> 8)) << 8));
 }
 
+// entries of a walk from (st0, base0) through n <= 256 maps: entry[i] = (phase << 56 | record
+// index) before map i, ~0 once the walk is stuck.  Two levels of 16 maps shorten the chain of
+// dependent steps from n to <= 48: the 16-map group maps for all 25 phases, the walk over the
+// groups, then every group's walk from its entry.  Returns the exit (STUCK or phase) and sets
+// *base_out.  gm: 16 x 25 words, ge: 16 entries (shared).
+#define WG 16
+FTLZ_DEV u32 walk2(const u32* m, int n, u32 st0, u64 base0, u64* entry, u32* gm, u64* ge, u64* base_out) {
+    const int ng = (n + WG - 1) / WG;
+    for (int t = threadIdx.x; t < ng * 25; t += blockDim.x) {
+        const int gi = t / 25, s = t - gi * 25;
+        const int i1 = min(n, gi * WG + WG);
+        u32 st = (u32)s, c = 0;
+        for (int i = gi * WG; i < i1 && st != STUCK; i++) {
+            const u32 v = m[i * 25 + st];
+            st = v == STUCK ? STUCK : (v & 0xff);
+            c += v == STUCK ? 0u : (v >> 8);
+        }
+        gm[t] = st == STUCK ? STUCK : (st | (c << 8));
+    }
+    __syncthreads();
+    __shared__ u32 s_exit;
+    __shared__ u64 s_base;
+    if (threadIdx.x == 0) {
+        u32 st = st0;
+        u64 base = base0;
+        for (int gi = 0; gi < ng; gi++) {
+            ge[gi] = st == STUCK ? ~0ull : (((u64)st << 56) | base);
+            if (st == STUCK) continue;
+            const u32 v = gm[gi * 25 + st];
+            st = v == STUCK ? STUCK : (v & 0xff);
+            base += v == STUCK ? 0ull : (u64)(v >> 8);
+        }
+        s_exit = st;
+        s_base = base;
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < ng) {
+        const int gi = threadIdx.x;
+        const u64 g0 = ge[gi];
+        u32 st = g0 == ~0ull ? STUCK : (u32)(g0 >> 56);
+        u64 base = g0 & ((1ull << 56) - 1);
+        const int i1 = min(n, gi * WG + WG);
+        for (int i = gi * WG; i < i1; i++) {
+            entry[i] = st == STUCK ? ~0ull : (((u64)st << 56) | base);
+            if (st == STUCK) continue;
+            const u32 v = m[i * 25 + st];
+            st = v == STUCK ? STUCK : (v & 0xff);
+            base += v == STUCK ? 0ull : (u64)(v >> 8);
+        }
+    }
+    __syncthreads();
+    *base_out = s_base;
+    return s_exit;
+}
+
+// the super-chunk's map: in-place tree reduction of its chunk maps
 __global__ void __launch_bounds__(PSUPER) k_parse_compose(DecArgs A) {
     __shared__ u32 m[PSUPER * 25];
     long long sc = blockIdx.x;
@@ -149,43 +202,41 @@ __global__ void __launch_bounds__(PSUPER) k_parse_compose(DecArgs A) {
     int n = (int)min((long long)PSUPER, A.nchunks - c0);
     for (int t = threadIdx.x; t < n * 25; t += blockDim.x) m[t] = A.maps[c0 * 25 + t];
     __syncthreads();
-    if (threadIdx.x < 25) {
-        u32 cnt;
-        u32 st = compose_walk(m, n, threadIdx.x, &cnt);
-        A.smaps[sc * 25 + threadIdx.x] = st == STUCK ? STUCK : (st | (cnt << 8));
+    for (int d = 1; d < n; d <<= 1) {
+        const int np = (n - d + 2 * d - 1) / (2 * d);   // pairs (i, i + d), i = 0, 2d, ... with i + d < n
+        for (int t = threadIdx.x; t < np * 25; t += blockDim.x) {
+            const int pi = t / 25, s = t - pi * 25, i = pi * 2 * d;
+            m[i * 25 + s] = map_apply(m + i * 25, m + (i + d) * 25, s);
+        }
+        __syncthreads();
     }
+    if (threadIdx.x < 25) A.smaps[sc * 25 + threadIdx.x] = m[threadIdx.x];
 }
 
+// entry (phase, record index) of every super-chunk: the two-level walk over windows of 256
+// super-chunk maps, the state carried between windows
 __global__ void __launch_bounds__(256) k_parse_top(DecArgs A) {
     __shared__ u32 m[256 * 25];
-    __shared__ u32 s_state;
-    __shared__ u64 s_base;
-    if (threadIdx.x == 0) { s_state = 0; s_base = 0; }
+    __shared__ u32 gm[WG * 25];
+    __shared__ u64 ge[WG], ent[256];
+    u32 st = 0;
+    u64 base = 0;
     for (long long w0 = 0; w0 < A.nsuper; w0 += 256) {
         int n = (int)min(256ll, A.nsuper - w0);
         __syncthreads();
         for (int t = threadIdx.x; t < n * 25; t += blockDim.x) m[t] = A.smaps[w0 * 25 + t];
         __syncthreads();
-        if (threadIdx.x == 0) {
-            u32 state = s_state;
-            u64 base = s_base;
-            for (int i = 0; i < n; i++) {
-                A.sentry[w0 + i] = state == STUCK ? ~0ull : (((u64)state << 56) | base);
-                if (state == STUCK) continue;
-                u32 v = m[i * 25 + state];
-                if (v == STUCK) { state = STUCK; continue; }
-                base += v >> 8;
-                state = v & 0xff;
-            }
-            s_state = state;
-            s_base = base;
-        }
+        u64 nb;
+        st = walk2(m, n, st, base, ent, gm, ge, &nb);
+        base = nb;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) A.sentry[w0 + i] = ent[i];
     }
 }
 
 __global__ void __launch_bounds__(PSUPER) k_parse_records(DecArgs A) {
     __shared__ u32 m[PSUPER * 25];
-    __shared__ u64 entry[PSUPER];
+    __shared__ u32 gm[WG * 25];
+    __shared__ u64 ge[WG], entry[PSUPER];
     long long sc = blockIdx.x;
     long long c0 = sc * PSUPER;
     int n = (int)min((long long)PSUPER, A.nchunks - c0);
@@ -193,19 +244,8 @@ __global__ void __launch_bounds__(PSUPER) k_parse_records(DecArgs A) {
     if (se == ~0ull) return;
     for (int t = threadIdx.x; t < n * 25; t += blockDim.x) m[t] = A.maps[c0 * 25 + t];
     __syncthreads();
-    if (threadIdx.x == 0) {
-        u32 state = (u32)(se >> 56);
-        u64 base = se & ((1ull << 56) - 1);
-        for (int i = 0; i < n; i++) {
-            entry[i] = state == STUCK ? ~0ull : (((u64)state << 56) | base);
-            if (state == STUCK) continue;
-            u32 v = m[i * 25 + state];
-            if (v == STUCK) { state = STUCK; continue; }
-            base += v >> 8;
-            state = v & 0xff;
-        }
-    }
-    __syncthreads();
+    u64 nb_unused;
+    walk2(m, n, (u32)(se >> 56), se & ((1ull << 56) - 1), entry, gm, ge, &nb_unused);
     if ((int)threadIdx.x >= n) return;
     u64 en = entry[threadIdx.x];
     if (en == ~0ull) return;
@@ -273,32 +313,52 @@ __global__ void __launch_bounds__(1024) k_scan2(DecArgs A) {
         }
     }
     __syncthreads();
-    if (tid == 0) {
+    if (warp == 0) {
+        // look-back by the whole warp: lane l reads tile (t - l); the nearest tile holding an
+        // inclusive prefix ends the walk, the aggregates before it are summed in one reduction
         volatile u64* va = A.lb_a; volatile u64* vb = A.lb_b; volatile u32* vf = A.lb_flag;
-        u64 p0 = 0, p1 = 0, t0 = ws[0][31], t1 = ws[1][31];
+        u64 p0 = 0, p1 = 0;
+        const u64 t0 = ws[0][31], t1 = ws[1][31];
         if (tile > 0) {
-            va[2 * tile] = t0; vb[2 * tile] = t1;
-            __threadfence();
-            vf[tile] = 1;
+            if (lane == 0) {
+                va[2 * tile] = t0; vb[2 * tile] = t1;
+                __threadfence();
+                vf[tile] = 1;
+            }
             long long t = (long long)tile - 1;
             while (t >= 0) {
-                u32 f = vf[t];
-                if (f == 0) continue;
+                const long long ti = t - lane;
+                const u32 f = ti >= 0 ? vf[ti] : 3u;   // 3: before tile 0 (an empty inclusive prefix)
+                const unsigned incl = __ballot_sync(0xffffffffu, f >= 2u);
+                const unsigned zero = __ballot_sync(0xffffffffu, f == 0u);
+                const int fi = incl ? __ffs(incl) - 1 : 32;
+                const unsigned need = fi == 32 ? 0xffffffffu : ((2u << fi) - 1u);
+                if (zero & need) continue;   // a tile up to the stop has published nothing yet
                 __threadfence();
-                int sl = f == 2 ? 1 : 0;
-                p0 += va[2 * t + sl]; p1 += vb[2 * t + sl];
-                if (f == 2) break;
-                t--;
+                u64 a0 = 0, a1 = 0;
+                if (lane < fi) { a0 = va[2 * ti]; a1 = vb[2 * ti]; }
+                else if (lane == fi && f == 2u) { a0 = va[2 * ti + 1]; a1 = vb[2 * ti + 1]; }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+                    a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+                }
+                p0 += a0;
+                p1 += a1;
+                if (fi < 32) break;
+                t -= 32;
             }
         }
-        va[2 * tile + 1] = p0 + t0; vb[2 * tile + 1] = p1 + t1;
-        __threadfence();
-        vf[tile] = 2;
-        pre[0] = p0; pre[1] = p1;
-        long long ntile = (A.g.nb + 1023) / 1024;
-        if ((long long)tile == ntile - 1) {
-            A.info[DI_TOTAL_BITS] = p0 + t0;
-            A.info[DI_NUNP] = p1 + t1;
+        if (lane == 0) {
+            va[2 * tile + 1] = p0 + t0; vb[2 * tile + 1] = p1 + t1;
+            __threadfence();
+            vf[tile] = 2;
+            pre[0] = p0; pre[1] = p1;
+            long long ntile = (A.g.nb + 1023) / 1024;
+            if ((long long)tile == ntile - 1) {
+                A.info[DI_TOTAL_BITS] = p0 + t0;
+                A.info[DI_NUNP] = p1 + t1;
+            }
         }
     }
     __syncthreads();
