@@ -209,40 +209,59 @@ __global__ void __launch_bounds__(SCAN_TILE) k_enc_scan(CompArgs A, u32* lb_flag
             if (w < warp) woff[q] += s_w[q][w];
             tsum[q] += s_w[q][w];
         }
-    if (tid == 0) {
-        // flag: 0 = empty, 1 = aggregate published, 2 = inclusive prefix published
+    if (warp == 0) {
+        // flag: 0 = empty, 1 = aggregate published, 2 = inclusive prefix published.  Look-back
+        // by the whole warp: lane l reads tile (t - l); the nearest inclusive prefix ends it.
         volatile u64* vb = lb_bits;
         volatile u64* vr = lb_reg;
         volatile u64* vu = lb_unp;
         volatile u32* vf = lb_flag;
         u64 pre[3] = {0, 0, 0};
         if (tile > 0) {
-            vb[2 * tile] = tsum[0];
-            vr[2 * tile] = tsum[1];
-            vu[2 * tile] = tsum[2];
-            __threadfence();
-            vf[tile] = 1;
+            if (lane == 0) {
+                vb[2 * tile] = tsum[0];
+                vr[2 * tile] = tsum[1];
+                vu[2 * tile] = tsum[2];
+                __threadfence();
+                vf[tile] = 1;
+            }
             long long t = (long long)tile - 1;
             while (t >= 0) {
-                const u32 f = vf[t];
-                if (f == 0) continue;
+                const long long ti = t - lane;
+                const u32 f = ti >= 0 ? vf[ti] : 3u;   // 3: before tile 0 (an empty inclusive prefix)
+                const unsigned incl = __ballot_sync(0xffffffffu, f >= 2u);
+                const unsigned zero = __ballot_sync(0xffffffffu, f == 0u);
+                const int fi = incl ? __ffs(incl) - 1 : 32;
+                const unsigned need = fi == 32 ? 0xffffffffu : ((2u << fi) - 1u);
+                if (zero & need) continue;
                 __threadfence();
-                const int sl = f == 2 ? 1 : 0;
-                pre[0] += vb[2 * t + sl];
-                pre[1] += vr[2 * t + sl];
-                pre[2] += vu[2 * t + sl];
-                if (f == 2) break;
-                t--;
+                u64 a[3] = {0, 0, 0};
+                const int sl = lane < fi ? 0 : 1;
+                if (lane < fi || (lane == fi && f == 2u)) {
+                    a[0] = vb[2 * ti + sl];
+                    a[1] = vr[2 * ti + sl];
+                    a[2] = vu[2 * ti + sl];
+                }
+#pragma unroll
+                for (int q = 0; q < 3; q++) {
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) a[q] += __shfl_xor_sync(0xffffffffu, a[q], o);
+                    pre[q] += a[q];
+                }
+                if (fi < 32) break;
+                t -= 32;
             }
         }
-        vb[2 * tile + 1] = pre[0] + tsum[0];
-        vr[2 * tile + 1] = pre[1] + tsum[1];
-        vu[2 * tile + 1] = pre[2] + tsum[2];
-        __threadfence();
-        vf[tile] = 2;
-        s_pre[0] = pre[0];
-        s_pre[1] = pre[1];
-        s_pre[2] = pre[2];
+        if (lane == 0) {
+            vb[2 * tile + 1] = pre[0] + tsum[0];
+            vr[2 * tile + 1] = pre[1] + tsum[1];
+            vu[2 * tile + 1] = pre[2] + tsum[2];
+            __threadfence();
+            vf[tile] = 2;
+            s_pre[0] = pre[0];
+            s_pre[1] = pre[1];
+            s_pre[2] = pre[2];
+        }
     }
     __syncthreads();
     if (!valid) return;
