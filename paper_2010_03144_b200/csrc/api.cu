@@ -671,9 +671,6 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     k_cb_bitmap<<<(unsigned)((cap + 255) / 256), 256, 0, s>>>(A, S.bm);
     k_codebook<<<1, CB_THREADS, (CB_SMEM_KEYS * 3) * 8 + CB_SMEM_KEYS * 2 * 2, s>>>(A, S);
     LCHK("k_codebook");
-    PF.mark("k_zero", s);
-    k_zero<<<num_sms() * 4, 256, 0, s>>>(A);
-    LCHK("k_zero");
     {
         const size_t capal = ((size_t)cap + 15) & ~(size_t)15;
         const int lw = (int)std::max<size_t>(1, std::min<size_t>(16, (227 * 1024 / 2 - capal) / (2 * (size_t)g.nvmax8)));

@@ -9,7 +9,6 @@
 //               (duplicated), double-check, bins/unpredictables/checksums/sum_dc/histogram (K2)
 //   k_fault_bins  bins-stage faults: verify/correct (protect_bins) and histogram fix-up
 //   k_codebook  canonical Huffman codebook from the global histogram (K3), archive layout
-//   k_zero      zero the payload words
 //   k_enc_*     (encode.cu) per-block bit lengths, block offsets, MSB-first packing (K4)
 //   k_assemble  header, block table, unpredictable words, sum_dc section (K5)
 #include <cstdio>
@@ -486,13 +485,6 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
 }
 
 // ==========================================================================================
-__global__ void k_zero(CompArgs A) {
-    if (dev_failed(A.st)) return;
-    u64 off = A.layout[LAYOUT_PAY_OFF], nbytes = A.layout[LAYOUT_PAY_BYTES];
-    u64 w0 = off >> 2, w1 = (off + nbytes + 3) >> 2;
-    u32* w = (u32*)A.out;
-    for (u64 i = w0 + (u64)blockIdx.x * blockDim.x + threadIdx.x; i < w1; i += (u64)gridDim.x * blockDim.x) w[i] = 0;
-}
 
 // ==========================================================================================
 // bins-stage faults (STAGE_BINS_FINALIZED, pipeline.py:468-496).  For every block a fault

@@ -8,7 +8,7 @@
 //               unpredictable words) -> payload bit offset, record offset, unpredictable offset
 //   k_enc_pack  warp per block: each lane packs its range at its absolute bit offset into
 //               big-endian 32-bit words; words shared with a neighbouring lane or block are
-//               merged with atomicOr (the payload is zeroed by k_zero), the rest are stored
+//               merged with atomicOr (k_enc_scan zeroes those words), the rest are stored
 //
 // Codes come from a 4096-symbol shared window around the quantizer centre (code << 6 | len),
 // global memory outside it.  Blocks touched by bins-stage faults read their verified 32-bit
@@ -17,6 +17,7 @@ namespace ftlz {
 
 #define ENC_WIN 4096
 #define SCAN_TILE 1024
+#define ENC_STG 256   // payload words of a block packed through the warp's shared-memory stage
 
 struct EncWin {
     const u64* s_enc;
@@ -265,7 +266,22 @@ __global__ void __launch_bounds__(SCAN_TILE) k_enc_scan(CompArgs A, u32* lb_flag
     }
     __syncthreads();
     if (!valid) return;
-    A.bitoff[b] = s_pre[0] + woff[0] + inc[0] - v3[0];
+    const u64 boff = s_pre[0] + woff[0] + inc[0] - v3[0];
+    // zero the payload words k_enc_pack merges with atomicOr (k_enc_pack runs after this
+    // kernel): the first and last word of every block (shared with its neighbours) and every
+    // word of a block packed without the shared-memory stage (lane boundaries)
+    {
+        u32* words = (u32*)A.out;
+        const u64 bpos = A.layout[LAYOUT_PAY_OFF] * 8 + boff;
+        const u64 w0 = bpos >> 5, w1 = (bpos + v3[0] + 31) >> 5;
+        if (w1 - w0 > ENC_STG) {
+            for (u64 w = w0; w < w1; w++) words[w] = 0u;
+        } else if (w1 > w0) {
+            words[w0] = 0u;
+            words[w1 - 1] = 0u;
+        }
+    }
+    A.bitoff[b] = boff;
     A.regpre[b] = (u32)(s_pre[1] + woff[1] + inc[1] - v3[1]);
     A.unppre[b] = s_pre[2] + woff[2] + inc[2] - v3[2];
 }
@@ -329,7 +345,6 @@ FTLZ_DEV void pack_range(const EncWin& W, const u16* sym16, const u32* sym32, in
 
 // the same packing into a warp's shared staging buffer (word 0 = the block's first payload
 // word); words shared between lanes are merged with shared-memory ORs
-#define ENC_STG 256
 FTLZ_DEV void put_s(u32 addr, u32 bits_be, bool p_st, bool p_or) {
     const u32 v = __byte_perm(bits_be, 0, 0x0123);
     asm volatile(
