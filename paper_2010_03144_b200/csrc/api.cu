@@ -369,7 +369,7 @@ static int kernel_attrs_once() {
         setmax((const void*)k_parse_tail);
         setmax((const void*)k_decode<false, false>);
         setmax((const void*)k_decode<false, true>);
-        setmax((const void*)k_decode<true, false>);
+        setmax((const void*)k_decode<true, true>);
         setmax((const void*)k_recon_g<32>);
         setmax((const void*)k_recon_g<128>);
         if (cudaGetLastError() != cudaSuccess) rc = FTLZ_ERR_CUDA;
@@ -665,7 +665,7 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     k_quant_lor<<<num_sms() * 4, 32 * K.lor_warps, K.lor_smem, s>>>(A);
     LCHK("k_quant_lor");
     if (nf) PF.mark("k_fault_bins", s);
-    if (nf) k_fault_bins<<<num_sms(), 256, 0, s>>>(A, (u32*)(ws + L.fix), (u8*)(ws + L.fixed));
+    if (nf) k_fault_bins<<<num_sms() * 4, 256, 0, s>>>(A, (u32*)(ws + L.fix), (u8*)(ws + L.fixed));
     LCHK("k_fault_bins");
     PF.mark("k_codebook", s);
     k_cb_bitmap<<<(unsigned)((cap + 255) / 256), 256, 0, s>>>(A, S.bm);
@@ -1017,7 +1017,7 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
             A.sb1 = l1 * layer;
             const unsigned dgrid = (unsigned)((A.sb1 - A.sb0 + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32));
             PF.mark("k_decode", s);
-            if (A.n_faults) k_decode<true, false><<<dgrid, DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
+            if (A.n_faults) k_decode<true, true><<<dgrid, DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
             else k_decode<false, true><<<dgrid, DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
             LCHK("k_decode");
             PF.mark("k_recon_warp", s);

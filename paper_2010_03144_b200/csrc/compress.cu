@@ -493,50 +493,77 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
 // counts of every word that differs from the clean bin (the reference builds its histogram
 // from the verified -- possibly mis-corrected -- bins, pipeline.py:484-492).  The encoder
 // then reads these words from fix_scratch.
+// warp per block with injected bins faults: verification, correction (checksum.py:109-142,
+// candidates tried in increasing j as the reference scans them), histogram fix-up
 __global__ void k_fault_bins(CompArgs A, u32* fix_scratch, u8* fixed) {
     if (dev_failed(A.st)) return;
     const Geom& g = A.g;
-    for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < g.nb; b += (long long)gridDim.x * blockDim.x) {
-        int f0 = A.fault_first[b];
+    const int lane = threadIdx.x & 31;
+    const long long nwarp = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long b = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < g.nb; b += nwarp) {
+        const int f0 = A.fault_first[b];
         if (f0 < 0) continue;
         bool any = false;
         for (int f = f0; f < A.n_faults && A.faults[f].block == b; f++) any |= A.faults[f].target == FTLZ_FAULT_BINS;
         if (!any) continue;
-        BlockInfo B = block_info(g, b);
-        int vol = B.vol;
+        const BlockInfo B = block_info(g, b);
+        const int vol = B.vol;
         u32* w = fix_scratch + (size_t)b * g.vmax;
-        for (int p = 0; p < vol; p++) w[p] = A.bins[bins_index(g, b, p)];
-        for (int f = f0; f < A.n_faults && A.faults[f].block == b; f++)
-            if (A.faults[f].target == FTLZ_FAULT_BINS) w[A.faults[f].element] ^= 1u << A.faults[f].bit;
+        for (int p = lane; p < vol; p += 32) w[p] = A.bins[bins_index(g, b, p)];
+        __syncwarp();
+        if (lane == 0)
+            for (int f = f0; f < A.n_faults && A.faults[f].block == b; f++)
+                if (A.faults[f].target == FTLZ_FAULT_BINS) w[A.faults[f].element] ^= 1u << A.faults[f].bit;
+        __syncwarp();
+        auto sums = [&](u64& s, u64& si) {
+            s = 0;
+            si = 0;
+            for (int p = lane; p < vol; p += 32) { s += w[p]; si += (u64)p * w[p]; }
+            s = warp_sum_u64(s);
+            si = warp_sum_u64(si);
+        };
         if (A.protect_bins) {
-            u64 s = 0, si = 0;
-            for (int p = 0; p < vol; p++) { s += w[p]; si += (u64)p * w[p]; }
+            u64 s, si;
+            sums(s, si);
             int status = 0;
             if (s != A.bsum[b] || si != A.bisum[b]) {
                 status = 2;
-                u64 ds = s - A.bsum[b], dsi = si - A.bisum[b];
+                const u64 ds = s - A.bsum[b], dsi = si - A.bisum[b];
                 if (ds != 0) {
-                    for (int j = 0; j < vol && status == 2; j++) {
-                        if ((u64)j * ds != dsi) continue;
-                        u64 old = w[j], rest = old - ds;
-                        if (rest >> 32) continue;
-                        w[j] = (u32)rest;
-                        u64 s2 = 0, si2 = 0;
-                        for (int p = 0; p < vol; p++) { s2 += w[p]; si2 += (u64)p * w[p]; }
-                        if (s2 == A.bsum[b] && si2 == A.bisum[b]) status = 1;
-                        else w[j] = (u32)old;
+                    for (int j0 = 0; j0 < vol && status == 2; j0 += 32) {
+                        const int j = j0 + lane;
+                        const bool cand = j < vol && (u64)j * ds == dsi && (((u64)w[j] - ds) >> 32) == 0;
+                        unsigned cm = __ballot_sync(0xffffffffu, cand);
+                        while (cm && status == 2) {
+                            const int jj = j0 + __ffs(cm) - 1;
+                            cm &= cm - 1;
+                            const u32 old = w[jj];
+                            __syncwarp();
+                            if (lane == 0) w[jj] = (u32)((u64)old - ds);
+                            __syncwarp();
+                            u64 s2, si2;
+                            sums(s2, si2);
+                            if (s2 == A.bsum[b] && si2 == A.bisum[b]) status = 1;
+                            else {
+                                __syncwarp();
+                                if (lane == 0) w[jj] = old;
+                                __syncwarp();
+                            }
+                        }
                     }
                 }
             }
-            if (status == 1) { A.events[b] |= 2; atomicAdd(&A.counters[3], 1u); }
+            if (status == 1 && lane == 0) { A.events[b] |= 2; atomicAdd(&A.counters[3], 1u); }
             if (status == 2) {
-                A.events[b] |= 8;
-                atomicAdd(&A.counters[3], 1u);
+                if (lane == 0) {
+                    A.events[b] |= 8;
+                    atomicAdd(&A.counters[3], 1u);
+                }
                 continue;
             }
         }
-        for (int p = 0; p < vol; p++) {
-            u32 orig = A.bins[bins_index(g, b, p)];
+        for (int p = lane; p < vol; p += 32) {
+            const u32 orig = A.bins[bins_index(g, b, p)];
             if (w[p] == orig) continue;
             if (w[p] >= (u32)A.cap) {
                 dev_fail(A.st, FTLZ_ERR_INVARIANT, FTLZ_K_BIN_RANGE, -1, -1, 0, 0, 0);
@@ -545,7 +572,7 @@ __global__ void k_fault_bins(CompArgs A, u32* fix_scratch, u8* fixed) {
             atomicSub(&A.hist[orig], 1u);
             atomicAdd(&A.hist[w[p]], 1u);
         }
-        fixed[b] = 1;
+        if (lane == 0) fixed[b] = 1;
     }
 }
 

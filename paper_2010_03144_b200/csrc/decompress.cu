@@ -684,7 +684,8 @@ FTLZ_DEV int decode_sym_slow(BitReader& R, const u32* dsym, u32 cur, u32* sym) {
 // right zero count had every code inside [start, start + bit_length), where both readers see
 // the same bits, so its symbols equal the masked reader's; any other outcome is a failure of
 // the masked reader too (contrapositive), and k_decode only marks such a block for the masked
-// reader to classify (DF_PENDING).  Invariant after every refill: have >= 33.
+// reader to classify (DF_PENDING).  Decompressed-data faults (FAULTS) change only the values
+// written, never the decode.  Invariant after every refill: have >= 33.
 struct FastReader {
     const u32* w;     // word 0: the word holding the block's first bit
     u32 lim;          // words [0, lim) may be loaded (the buffer's words, last one partial)
@@ -806,7 +807,6 @@ __host__ __device__ inline size_t dec_stage_words(int e) { return ((size_t)32 * 
 
 template <bool FAULTS, bool FAST>
 __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u32* list, int nlist) {
-    static_assert(!(FAULTS && FAST), "the fast reader serves the fault-free full path only");
     if (dev_failed(A.st)) return;
     extern __shared__ __align__(16) unsigned char dsm[];
     const Geom& g = A.g;
@@ -951,7 +951,8 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
                 u32 zmask = 0;
                 auto femit = [&](u32 sym, int k, double dkv) {
                     const double pred = __dadd_rn(ab, __dmul_rn(c3, dkv));
-                    const float v = __double2float_rn(__dadd_rn(pred, __dmul_rn(twoeb, int_to_f64((int)sym - center))));
+                    float v = __double2float_rn(__dadd_rn(pred, __dmul_rn(twoeb, int_to_f64((int)sym - center))));
+                    if (FAULTS && f0 >= 0 && recon_here) v = apply_decomp_faults(A, b, (i * B.by + j) * B.bz + k, f0, v);
                     const u32 word = recon_here ? __float_as_uint(v) : sym;
                     dsum += (u64)word;
                     // no memory clobber: the stores may move within the row (the row ends with
@@ -995,7 +996,9 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
                     const int k = __ffs(zmask) - 1;
                     zmask &= zmask - 1;
                     if (recon_here) {
-                        const u32 w = zeros < nunp ? (u32)ld_le(A.a + unp_base + 4ull * zeros, 4) : 0u;
+                        u32 w = zeros < nunp ? (u32)ld_le(A.a + unp_base + 4ull * zeros, 4) : 0u;
+                        if (FAULTS && f0 >= 0)
+                            w = __float_as_uint(apply_decomp_faults(A, b, (i * B.by + j) * B.bz + k, f0, __uint_as_float(w)));
                         const u32 old = lds_u32(st_sa + 4u * (u32)k);
                         asm volatile("st.shared.u32 [%0], %1;" ::"r"(st_sa + 4u * (u32)k), "r"(w) : "memory");
                         dsum += (u64)w - (u64)old;
