@@ -1093,7 +1093,7 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         std::sort(mis.begin(), mis.end());
         CK(cudaMemcpy(ws + L.mis, mis.data(), 4 * (size_t)nmis, cudaMemcpyHostToDevice));
         A.n_faults = 0;
-        k_decode<false, false><<<(unsigned)((nmis + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32)), DEC_WARPS * 32, dec_smem, s>>>(
+        k_decode<false, true><<<(unsigned)((nmis + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32)), DEC_WARPS * 32, dec_smem, s>>>(
             A, (const u32*)(ws + L.mis), (int)nmis);
         LCHK("k_decode");
         k_recon_g<32><<<(unsigned)std::min<u32>((nmis + rw - 1) / rw, sms * 4), rw * 32, rslot * rw, s>>>(A, 1);
@@ -1181,7 +1181,7 @@ static int region_core(const HostPlan& P, const DevPlan& D, const uint8_t* d_a, 
         std::sort(mis.begin(), mis.end());
         CK(cudaMemcpy(ws + L.mis, mis.data(), 4 * (size_t)nmis, cudaMemcpyHostToDevice));
         A.region = 0;   // re-decode failures mark mflag = 3
-        k_decode<false, false><<<(nmis + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32), DEC_WARPS * 32, dec_smem, s>>>(
+        k_decode<false, true><<<(nmis + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32), DEC_WARPS * 32, dec_smem, s>>>(
             A, (const u32*)(ws + L.mis), (int)nmis);
         LCHK("k_decode");
         k_recon_g<32><<<std::min<u32>((nmis + rw - 1) / rw, (u32)sms * 4), rw * 32, rslot * rw, s>>>(A, 3);
