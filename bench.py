@@ -464,6 +464,10 @@ def run_ours(args, world, rank, local):
                                 "compress_s": tcm, "decompress_s": tdm,
                                 "archive_identical_to_gpu": (data == parity_archive) if parity_archive else None}
 
+    # ---- the other BASELINE configs (c1, c2 at both bounds, c4) at full size
+    if rank == 0 and not args.quick and not args.no_c5:
+        line["configs"] = run_configs(F, L, _lib, torch, local)
+
     # ---- c5: seeded 1% single-bit flips on the c2 field at rel 1e-3
     if rank == 0 and not args.quick and not args.no_c5:
         line["c5"] = run_c5(F, L, _lib, torch, local)
@@ -561,6 +565,67 @@ def run_c5(F, L, _lib, torch, local):
             r["reference_archive_match"] = synth.sha256(np.frombuffer(data, np.uint8)) == man[tgt]["archive_sha256"]
         res[tgt] = r
     return res
+
+
+def run_configs(F, L, _lib, torch, local, names=("c1", "c2", "c2_1e-4", "c4")):
+    """The other BASELINE configs at full size: device time of compress and decompress through
+    the C ABI (inputs and archive in HBM, CUDA events, L2 flushed before each call, median of
+    5 after 3 warm-ups), with the archive and output checked against the reference's hashes."""
+    ctx = _lib.context(local)
+    stream = torch.cuda.ExternalStream(L.ftlz_ctx_stream(ctx), device=local)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+    man = json.load(open(os.path.join(ROOT, "tests", "golden", "manifest.json")))["large"]
+    fa0, _ = F.pipeline._faults_c([])
+    cfg = F.FtConfig()
+    out = {}
+    for name in names:
+        x = load_field(name)
+        mode, v = synth.CONFIGS[name]["eb"]
+        nx, ny, nz = x.shape
+        d_x = torch.from_numpy(x).to(f"cuda:{local}")
+        d_o = torch.empty(x.size, dtype=torch.float32, device=f"cuda:{local}")
+        mcode = {"absolute": 0, "value_range_relative": 1}[mode]
+        rb = F.pipeline._ReportBuf(F.partition(x.shape, 10).n_blocks)
+        tc, td = [], []
+        ptr, ln = C.c_void_p(), C.c_size_t()
+        for it in range(8):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            e0, e1, e2, e3 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+            stream.synchronize()
+            e0.record(stream)
+            if L.ftlz_ctx_compress_device(ctx, d_x.data_ptr(), nx, ny, nz, mcode, v, C.byref(cfg._c()), fa0, 0,
+                                          None, C.byref(rb.r)) != 0:
+                raise RuntimeError(f"{name} compress failed: {_lib.last_error()}")
+            e1.record(stream)
+            L.ftlz_ctx_archive_device(ctx, C.byref(ptr), C.byref(ln))
+            hbuf = np.zeros(64, np.uint8)
+            ctypes_cuda().cudaMemcpy(C.c_void_p(hbuf.ctypes.data), C.c_void_p(ptr.value), C.c_size_t(64), 2)
+            hdr, info = _lib.Header(), _lib.Info()
+            L.ftlz_peek_header(hbuf.tobytes(), 64, C.byref(hdr), C.byref(info))
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            e2.record(stream)
+            if L.ftlz_ctx_decompress_device(ctx, ptr.value, ln.value, C.byref(hdr), d_o.data_ptr(), fa0, 0,
+                                            C.byref(rb.r)) != 0:
+                raise RuntimeError(f"{name} decompress failed: {_lib.last_error()}")
+            e3.record(stream)
+            torch.cuda.synchronize()
+            if it >= 3:
+                tc.append(e0.elapsed_time(e1))
+                td.append(e2.elapsed_time(e3))
+        arch = np.empty(ln.value, np.uint8)
+        ctypes_cuda().cudaMemcpy(C.c_void_p(arch.ctypes.data), C.c_void_p(ptr.value), C.c_size_t(ln.value), 2)
+        y = d_o.cpu().numpy()
+        mc, md = statistics.median(tc), statistics.median(td)
+        nbytes = 4.0 * x.size
+        out[name] = {"dims": list(x.shape), "eb": [mode, v], "compress_ms": mc, "decompress_ms": md,
+                     "compress_gbs": nbytes / mc / 1e6, "decompress_gbs": nbytes / md / 1e6,
+                     "archive_bytes": int(ln.value), "ratio": nbytes / ln.value,
+                     "archive_sha256_match": synth.sha256(arch) == man[name]["archive_sha256"],
+                     "output_sha256_match": synth.sha256(y.reshape(x.shape)) == man[name]["output_sha256"]}
+        del d_x, d_o
+    return out
 
 
 def kernel_base(name: str) -> str:
