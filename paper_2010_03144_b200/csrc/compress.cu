@@ -229,42 +229,35 @@ struct CodebookScratch {
 // two-queue Huffman merge over leaves sorted by (weight, symbol) (the reference heap with its
 // (weight, tie) order, encode.py:26-71): leaves 0..n-1, merged nodes n..2n-2; queue heads in
 // registers.  W must point into one memory space (shared or global) so accesses stay typed.
-template <typename SetParent>
-FTLZ_DEV void cb_merge(u64* W, int n, SetParent set_parent) {
-    // W[0, n) holds the sorted leaf weights.  Queue heads live in registers three deep
-    // (L0..L2 = W[li..li+2], M0..M2 = W[mi..mi+2]; ~0 = none), refilled by selects and loads
-    // issued two pops before their use: a pop is a compare and a rank of selects, no branch
-    // and no wait on shared memory.
-    const u64 INF = ~0ull;
-    int li = 0, mi = n, mk = n;   // next leaf, next merged to consume, next merged to create
-    u64 L0 = W[0], L1 = n > 1 ? W[1] : INF, L2 = n > 2 ? W[2] : INF, M0 = INF, M1 = INF, M2 = INF;
+template <typename WT, typename SetParent>
+FTLZ_DEV void cb_merge3(WT* W, int n, SetParent set_parent) {
+    const WT INF = (WT)~(WT)0;
+    int li = 0, mi = n, mk = n;
+    WT L0 = W[0], L1 = n > 1 ? W[1] : INF, L2 = n > 2 ? W[2] : INF, L3 = n > 3 ? W[3] : INF;
+    WT M0 = INF, M1 = INF, M2 = INF, M3 = INF;
     for (int t = 0; t < n - 1; t++) {
-        int pk[2];
-        u64 pw[2];
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const bool tl = L0 <= M0;   // a leaf wins a tie
-            const u64 nL = li + 3 < n ? W[li + 3] : INF;
-            const u64 nM = mi + 3 < mk ? W[mi + 3] : INF;
-            pk[h] = tl ? li : mi;
-            pw[h] = tl ? L0 : M0;
-            L0 = tl ? L1 : L0;
-            L1 = tl ? L2 : L1;
-            L2 = tl ? nL : L2;
-            M0 = tl ? M0 : M1;
-            M1 = tl ? M1 : M2;
-            M2 = tl ? M2 : nM;
-            li += tl ? 1 : 0;
-            mi += tl ? 0 : 1;
-        }
-        const u64 sum = pw[0] + pw[1];
+        const bool c1 = L0 <= M0, c2 = L1 <= M0, c3 = L0 <= M1;
+        const bool LL = c1 && c2, MM = !c1 && !c3;
+        const int ca = MM ? mi : li, cb = LL ? li + 1 : (MM ? mi + 1 : mi);
+        const WT sum = LL ? L0 + L1 : (MM ? M0 + M1 : L0 + M0);
+        const int dl = LL ? 2 : (MM ? 0 : 1), dm = 2 - dl;
+        const WT nl0 = li + 4 < n ? W[li + 4] : INF, nl1 = li + 5 < n ? W[li + 5] : INF;
+        const WT nm0 = mi + 4 < mk ? W[mi + 4] : INF, nm1 = mi + 5 < mk ? W[mi + 5] : INF;
+        const WT a0 = dl == 0 ? L0 : (dl == 1 ? L1 : L2), a1 = dl == 0 ? L1 : (dl == 1 ? L2 : L3);
+        const WT a2 = dl == 0 ? L2 : (dl == 1 ? L3 : nl0), a3 = dl == 0 ? L3 : (dl == 1 ? nl0 : nl1);
+        L0 = a0; L1 = a1; L2 = a2; L3 = a3;
+        const WT b0 = dm == 0 ? M0 : (dm == 1 ? M1 : M2), b1 = dm == 0 ? M1 : (dm == 1 ? M2 : M3);
+        const WT b2 = dm == 0 ? M2 : (dm == 1 ? M3 : nm0), b3 = dm == 0 ? M3 : (dm == 1 ? nm0 : nm1);
+        li += dl;
+        mi += dm;
         W[mk] = sum;
-        const int q = mk - mi;   // merged nodes waiting before this one
-        M0 = q == 0 ? sum : M0;
-        M1 = q == 1 ? sum : M1;
-        M2 = q == 2 ? sum : M2;
-        set_parent(pk[0], mk);
-        set_parent(pk[1], mk);
+        const int q = mk - mi;   // merged nodes waiting before the new one
+        M0 = q == 0 ? sum : b0;
+        M1 = q == 1 ? sum : b1;
+        M2 = q == 2 ? sum : b2;
+        M3 = q == 3 ? sum : b3;
+        set_parent(ca, mk);
+        set_parent(cb, mk);
         mk++;
     }
 }
@@ -301,6 +294,7 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
     u64* skeys = cb_dyn;
     __shared__ u32 wcount[33];
     __shared__ u64 lencount[64];
+    __shared__ u32 s_lfirst[64], s_llast[64];
     __shared__ u64 firstcode[64];
     __shared__ u32 firstidx[64];
     __shared__ int s_n, s_maxlen, s_np2;
@@ -361,9 +355,14 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
     //    alphabet fits (u16 parents), else in global scratch.
     const bool small = np2 <= CB_SMEM_KEYS;
     u16* par16 = (u16*)(cb_dyn + 3 * CB_SMEM_KEYS);
+    const bool w32 = (u64)A.g.nx * (u64)A.g.ny * (u64)A.g.nz < 0xffffffffull;   // total weight fits u32
     {
         u64* W = small ? cb_dyn + CB_SMEM_KEYS : S.w;
-        for (int i = tid; i < n; i += CB_THREADS) W[i] = keys[i] >> 16;
+        u32* W32 = (u32*)W;
+        for (int i = tid; i < n; i += CB_THREADS) {
+            if (w32) W32[i] = (u32)(keys[i] >> 16);
+            else W[i] = keys[i] >> 16;
+        }
         __syncthreads();
     }
     if (tid == 0) {
@@ -372,10 +371,14 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
             if (small) par16[0] = 0xffffu;
             else S.parent[0] = 0xffffffffu;
         } else if (small) {
-            cb_merge(cb_dyn + CB_SMEM_KEYS, n, [&](int i, int mk) { par16[i] = (u16)mk; });
+            auto sp = [&](int i, int mk) { par16[i] = (u16)mk; };
+            if (w32) cb_merge3((u32*)(cb_dyn + CB_SMEM_KEYS), n, sp);
+            else cb_merge3(cb_dyn + CB_SMEM_KEYS, n, sp);
             par16[2 * n - 2] = 0xffffu;
         } else {
-            cb_merge(S.w, n, [&](int i, int mk) { S.parent[i] = (u32)mk; });
+            auto sp = [&](int i, int mk) { S.parent[i] = (u32)mk; };
+            if (w32) cb_merge3((u32*)S.w, n, sp);
+            else cb_merge3(S.w, n, sp);
             S.parent[2 * n - 2] = 0xffffffffu;
         }
     }
@@ -412,10 +415,17 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
             keys[i] = ((u64)S.lens[sym] << 16) | sym;
         } else keys[i] = ~0ull;
     }
-    if (tid < 64) lencount[tid] = 0;
+    if (tid < 64) { lencount[tid] = 0; s_lfirst[tid] = 0; s_llast[tid] = 0; }
     __syncthreads();
     bitonic_sort_u64(keys, np2);
-    for (int i = tid; i < n; i += CB_THREADS) atomicAdd(&lencount[keys[i] >> 16], 1ull);
+    // keys are sorted by length: each length's count is the span between its boundaries
+    for (int i = tid; i < n; i += CB_THREADS) {
+        const u32 l = (u32)(keys[i] >> 16);
+        if (i == 0 || (u32)(keys[i - 1] >> 16) != l) s_lfirst[l] = (u32)i;
+        if (i == n - 1 || (u32)(keys[i + 1] >> 16) != l) s_llast[l] = (u32)(i + 1);
+    }
+    __syncthreads();
+    if (tid < 64) lencount[tid] = (u64)(s_llast[tid] - s_lfirst[tid]);
     __syncthreads();
     if (tid == 0) {
         u64 code = 0;

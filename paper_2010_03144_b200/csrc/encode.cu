@@ -268,15 +268,12 @@ __global__ void __launch_bounds__(SCAN_TILE) k_enc_scan(CompArgs A, u32* lb_flag
     if (!valid) return;
     const u64 boff = s_pre[0] + woff[0] + inc[0] - v3[0];
     // zero the payload words k_enc_pack merges with atomicOr (k_enc_pack runs after this
-    // kernel): the first and last word of every block (shared with its neighbours) and every
-    // word of a block packed without the shared-memory stage (lane boundaries)
+    // kernel): the first and last word of every block (shared with its neighbours)
     {
         u32* words = (u32*)A.out;
         const u64 bpos = A.layout[LAYOUT_PAY_OFF] * 8 + boff;
         const u64 w0 = bpos >> 5, w1 = (bpos + v3[0] + 31) >> 5;
-        if (w1 - w0 > ENC_STG) {
-            for (u64 w = w0; w < w1; w++) words[w] = 0u;
-        } else if (w1 > w0) {
+        if (w1 > w0) {   // (the interior of an unstaged block is zeroed by its own warp in k_enc_pack)
             words[w0] = 0u;
             words[w1 - 1] = 0u;
         }
@@ -505,7 +502,14 @@ __global__ void __launch_bounds__(512) k_enc_pack(CompArgs A, const u32* fix, co
                 if (i == 0 || i == (int)nwords - 1) atomicOr(words + w0 + i, v);
                 else words[w0 + i] = v;
             }
-        } else if (p0 < pend) {
+        } else {
+            // unstaged: this warp zeroes the block's interior words (lanes merge at their range
+            // boundaries), coalesced, before packing in place
+            for (u64 i = w0 + 1 + lane; i + 1 < w0 + nwords; i += 32) words[i] = 0u;
+            __threadfence();   // the zeros reach L2 before any lane's atomicOr on them
+            __syncwarp();
+        }
+        if (nwords > ENC_STG && p0 < pend) {
             if (fixed) pack_range<true, true>(W, sym16, sym32, p0, pend, gpos, words);
             else if (longc) pack_range<false, true>(W, sym16, sym32, p0, pend, gpos, words);
             else pack_range<false, false>(W, sym16, sym32, p0, pend, gpos, words);
