@@ -944,6 +944,23 @@ struct DlOverlap {
     int nslab = 0;
 };
 
+// largest wavefront plane (points with i + j + k = const) of the largest block extent
+static int lor_wave_max(const Geom& g) {
+    const int bx = (int)std::min<int64_t>(g.e, g.nx), by = (int)std::min<int64_t>(g.e, g.ny),
+              bz = (int)std::min<int64_t>(g.e, g.nz);
+    int best = 0;
+    for (int d = 0; d <= bx + by + bz - 3; d++) {
+        int c = 0;
+        for (int i = 0; i < bx; i++)
+            for (int j = 0; j < by; j++) {
+                const int k = d - i - j;
+                c += k >= 0 && k < bz;
+            }
+        best = std::max(best, c);
+    }
+    return best;
+}
+
 static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8_t* d_a, size_t len,
                            const ftlz_header* h, float* d_out, const ftlz_fault* faults, int64_t nf,
                            unsigned char* ws, size_t ws_size, ftlz_report* rep, ftlz_stream_info* si_out,
@@ -1021,7 +1038,10 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
             else k_decode<false, true><<<dgrid, DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
             LCHK("k_decode");
             PF.mark("k_recon_warp", s);
-            k_recon_g<128><<<sms * 4, 128, rslot, s>>>(A, 0);
+            // a CTA per Lorenzo block when a wavefront plane exceeds a warp (10^3 blocks: up to
+            // 75 points), else a warp per block (1 x e x e planes: e points) without CTA barriers
+            if (lor_wave_max(g) > 32) k_recon_g<128><<<sms * 4, 128, rslot, s>>>(A, 0);
+            else k_recon_g<32><<<sms * 8, rw * 32, rslot * rw, s>>>(A, 0);
             LCHK("k_recon");
             if (nslab > 1 || (dl && dl->h_out)) {
                 const long long x0 = l0 * g.e, x1 = std::min<long long>(l1 * g.e, g.nx);
