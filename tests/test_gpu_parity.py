@@ -199,3 +199,25 @@ def test_slab_overlapped_decompress_with_reexecution_on_c3():
     rd = rep.to_dict()
     assert rd["status"] == "corrected" and rd["decomp_block_reexecuted"] == [5, 70000, 140607]
     np.testing.assert_array_equal(out.values.view(np.uint32), clean.view(np.uint32))
+
+
+def test_reused_context_buffers_do_not_leak_into_archives():
+    """The device archive and workspace are reused across calls, and k_enc_pack merges the
+    words it shares with neighbouring blocks (or lanes) with atomicOr into words k_enc_scan /
+    k_enc_pack zeroed first.  Alternate unlike fields of one shape (noise with unstaged blocks,
+    a smooth field, constant) through the same context: every archive must equal the oracle's,
+    whatever the previous call left in the buffers."""
+    dims = (48, 40, 36)
+    rng = np.random.default_rng(17)
+    noise = rng.standard_normal(dims).astype(np.float32)
+    smooth = _seeded("smooth", dims, seed=3)
+    const = np.full(dims, 2.5, np.float32)
+    cases = [(noise, "absolute", 1e-5), (smooth, "value_range_relative", 1e-3), (noise, "absolute", 1e-2),
+             (const, "absolute", 1e-3), (noise, "absolute", 1e-5), (smooth, "absolute", 1e-6)]
+    for x, mode, v in cases + cases[::-1]:
+        want, _ = O.compress(x, mode, v, threads=4)
+        got = F.compress_bytes(x, mode, v)
+        assert got == want
+        out = F.decompress_bytes(got)
+        ref, _ = O.decompress(want, threads=4)
+        np.testing.assert_array_equal(out.view(np.uint32), ref.view(np.uint32))
