@@ -7,6 +7,7 @@
 // F2F / F2I / I2F at ~1/4 of that and DDIV at 1/14, so conversions and divisions are replaced
 // by exact integer bit manipulations wherever the result is provably identical.
 #pragma once
+#include <type_traits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -281,7 +282,95 @@ struct Leaf {
 };
 
 // block-wide bitonic sort of n_pow2 u64 keys (ascending); all threads of the CTA participate
+// Bitonic sort of n_pow2 keys in shared memory by the whole CTA (blockDim a multiple of 32).
+// Element e = tid + r * blockDim lives in register r of thread tid while in registers: the
+// stages with j < 32 run as warp shuffles and those with j >= blockDim inside one thread, so
+// only 32 <= j < blockDim need shared memory and a barrier (42 barriers at 8192 keys and
+// 1024 threads instead of 91).  Same comparisons and result as the plain network.
+#define BS_MAXR 8
+FTLZ_DEV void bitonic_sort_u64_plain(u64* keys, int n_pow2);
 FTLZ_DEV void bitonic_sort_u64(u64* keys, int n_pow2) {
+    const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31;
+    const int R = (n_pow2 + T - 1) / T;
+    if (R > BS_MAXR || (T & 31) || (T & (T - 1)) || n_pow2 < 64) {
+        bitonic_sort_u64_plain(keys, n_pow2);
+        return;
+    }
+    u64 v[BS_MAXR];
+    auto load = [&]() {
+#pragma unroll
+        for (int r = 0; r < BS_MAXR; r++)
+            if (r < R && tid + r * T < n_pow2) v[r] = keys[tid + r * T];
+    };
+    auto store = [&]() {
+#pragma unroll
+        for (int r = 0; r < BS_MAXR; r++)
+            if (r < R && tid + r * T < n_pow2) keys[tid + r * T] = v[r];
+        __syncthreads();
+    };
+    // stages j < 32 of merge size k (k >= 2): partner e ^ j is lane ^ j of the same register
+    auto warp_stages = [&](int k) {
+        for (int j = min(k >> 1, 16); j > 0; j >>= 1) {
+#pragma unroll
+            for (int r = 0; r < BS_MAXR; r++) {
+                if (r >= R) break;
+                const int e = tid + r * T;
+                const u64 o = __shfl_xor_sync(0xffffffffu, v[r], j);
+                const bool up = (e & k) == 0, lower = (e & j) == 0;
+                const u64 mn = v[r] < o ? v[r] : o, mx = v[r] < o ? o : v[r];
+                v[r] = (lower == up) ? mn : mx;
+            }
+        }
+    };
+    load();
+    for (int k = 2; k <= 32 && k <= n_pow2; k <<= 1) warp_stages(k);
+    store();
+    for (int k = 64; k <= n_pow2; k <<= 1) {
+        int j = k >> 1;
+        if (j >= T) {
+            // partner in another register of the same thread
+            load();
+            // register distance rj = j / T in {4, 2, 1}: compile-time indices keep v in registers
+            auto reg_stage = [&](auto rjc) {
+                constexpr int RJ = decltype(rjc)::value;
+#pragma unroll
+                for (int r = 0; r < BS_MAXR; r++) {
+                    if ((r & RJ) || r + RJ >= BS_MAXR) continue;
+                    if (r + RJ >= R) continue;
+                    const int e = tid + r * T;
+                    const bool up = (e & k) == 0;
+                    const u64 a = v[r], c = v[r + RJ];
+                    const bool sw = (a > c) == up;
+                    v[r] = sw ? c : a;
+                    v[r + RJ] = sw ? a : c;
+                }
+            };
+            for (; j >= T; j >>= 1) {
+                const int rj = j / T;
+                if (rj == 4) reg_stage(std::integral_constant<int, 4>());
+                else if (rj == 2) reg_stage(std::integral_constant<int, 2>());
+                else reg_stage(std::integral_constant<int, 1>());
+            }
+            store();
+        }
+        for (; j >= 32; j >>= 1) {
+            for (int i = tid; i < n_pow2; i += T) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const u64 a = keys[i], c = keys[ixj];
+                    const bool up = (i & k) == 0;
+                    if ((a > c) == up) { keys[i] = c; keys[ixj] = a; }
+                }
+            }
+            __syncthreads();
+        }
+        load();
+        warp_stages(k);
+        store();
+    }
+}
+
+FTLZ_DEV void bitonic_sort_u64_plain(u64* keys, int n_pow2) {
     for (int k = 2; k <= n_pow2; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
             for (int i = threadIdx.x; i < n_pow2; i += blockDim.x) {
