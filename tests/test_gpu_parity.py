@@ -221,3 +221,18 @@ def test_reused_context_buffers_do_not_leak_into_archives():
         out = F.decompress_bytes(got)
         ref, _ = O.decompress(want, threads=4)
         np.testing.assert_array_equal(out.view(np.uint32), ref.view(np.uint32))
+
+
+@pytest.mark.parametrize("ebv", [3e-3, 1e-3, 4e-4, 1.5e-4, 6e-5, 2.5e-5])
+def test_alphabet_sizes_sort_and_merge_paths(ebv):
+    """Noise at falling bounds grows the alphabet from hundreds to tens of thousands of symbols:
+    the codebook's bitonic sorts cross every register / shared-memory stage split (and the
+    plain network past 8,192 keys), the two-queue merge runs in shared and in global memory,
+    and the decoder's long-code path is taken.  Archives and outputs equal the oracle's."""
+    x = _seeded("noise", (64, 60, 56), seed=23)
+    want, wrep = O.compress(x, "absolute", ebv, threads=4)
+    got = F.compress_bytes(x, "absolute", ebv)
+    assert got == want
+    out = F.decompress_bytes(got)
+    ref, _ = O.decompress(want, threads=4)
+    np.testing.assert_array_equal(out.view(np.uint32), ref.view(np.uint32))
