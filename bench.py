@@ -345,7 +345,8 @@ def run_ours(args, world, rank, local):
     ach_d = Bd / (td_ms * 1e-3) / 1e9
     kern = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
             for k, v in prof.items()}
-    launches = int(round(sum(v[1] for v in prof.values()) / max(1, args.steps)))
+    # kernels only (the profiler's host-prelude marks are not launches)
+    launches = int(round(sum(v[1] for k, v in prof.items() if k.startswith("k_")) / max(1, args.steps)))
     dec_names = ("k_parse_maps", "k_parse_compose", "k_parse_top", "k_parse_records", "k_scan2", "k_parse_tail",
                  "k_decode", "k_recon_warp")
     comp_k = {k: v for k, v in kern.items() if k not in dec_names}

@@ -667,8 +667,9 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     if (nf) PF.mark("k_fault_bins", s);
     if (nf) k_fault_bins<<<num_sms() * 4, 256, 0, s>>>(A, (u32*)(ws + L.fix), (u8*)(ws + L.fixed));
     LCHK("k_fault_bins");
-    PF.mark("k_codebook", s);
+    PF.mark("k_cb_bitmap", s);
     k_cb_bitmap<<<(unsigned)((cap + 255) / 256), 256, 0, s>>>(A, S.bm);
+    PF.mark("k_codebook", s);
     k_codebook<<<1, CB_THREADS, (CB_SMEM_KEYS * 3) * 8 + CB_SMEM_KEYS * 2 * 2, s>>>(A, S);
     LCHK("k_codebook");
     {
