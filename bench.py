@@ -430,7 +430,7 @@ def run_ours(args, world, rank, local):
             n = F.compress_bytes(xp, mode, ebv, cfg, out=arch_p)
             F.decompress_bytes(arch_p[:n], out=out_p)
         te = []
-        for _ in range(max(2, min(args.steps, 5))):
+        for _ in range(max(3, args.steps)):
             t0 = time.perf_counter()
             n = F.compress_bytes(xp, mode, ebv, cfg, out=arch_p)
             F.decompress_bytes(arch_p[:n], out=out_p)
