@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define FTLZ_ABI_VERSION 2
+#define FTLZ_ABI_VERSION 3
 
 /* ---- status codes (errors.py:4-59) ------------------------------------------------------- */
 enum ftlz_status {
@@ -124,7 +124,13 @@ enum ftlz_fault_target {
     FTLZ_FAULT_BINS = 1,     /* u32 bin word after stage (c)              (STAGE_BINS_FINALIZED)       */
     FTLZ_FAULT_DECOMP = 2,   /* decompressed word before verification, once (STAGE_DECOMP_BEFORE_VERIFY) */
     FTLZ_FAULT_COEFF = 3,    /* float32 regression coefficient `element` (STAGE_COEFFS_FITTED)        */
-    FTLZ_FAULT_ESTIMATE = 4  /* float64 estimate: element 0 = e_reg, 1 = e_lor; bit 0..63 (STAGE_ESTIMATES) */
+    FTLZ_FAULT_ESTIMATE = 4, /* float64 estimate: element 0 = e_reg, 1 = e_lor; bit 0..63 (STAGE_ESTIMATES) */
+    /* duplicated evaluation (STAGE_DUP_EVAL, hooks.py:19, fired at pipeline.py:166-173): XOR one
+     * bit of the float64 prediction / reconstruction of point `element` of `block` as evaluation
+     * round r (1..3) returns it; `bit` = 64 * (r - 1) + b, b in 0..63.  Round 2 exists only with
+     * duplicate_eval, round 3 only where rounds 1 and 2 disagree (2-of-3 vote). */
+    FTLZ_FAULT_DUP_PREDICT = 5,
+    FTLZ_FAULT_DUP_RECON = 6
 };
 
 typedef struct ftlz_fault {

@@ -213,24 +213,70 @@ static inline uint32_t quantize(const quant_t* q, double diff, int* ok) {
 /* stage (c) for one block, sequential per point in row-major order (a valid topological
  * order of the Lorenzo wavefront, pipeline.py:196-213; == test_pipeline.py reference_block).
  * Outputs bins[vol], recon words, unpredictable words (count returned). */
+/* duplicated_eval (pipeline.py:157-179) of one element: evaluation r (1..3) returns the clean
+ * value with mask m[r-1] XORed in (the STAGE_DUP_EVAL hook seam, hooks.py:19, restated as
+ * per-element bit flips).  Round 2 runs only when `dup`; round 3 only on a mismatch.  The
+ * vote keeps a where a == b or a == c, else b; all three distinct -> *dis = 1. */
+static double dup_vote(double v, const uint64_t m[3], int dup, int* mism, int* dis) {
+    uint64_t a = d2w(v) ^ m[0];
+    if (!dup) return w2d(a);
+    uint64_t b = d2w(v) ^ m[1];
+    if (a == b) return w2d(a);
+    uint64_t c = d2w(v) ^ m[2];
+    *mism = 1;
+    if (!(b == c || a == c)) *dis = 1;
+    return w2d(a == c ? a : b);
+}
+
+/* STAGE_DUP_EVAL masks of element p of block b: mp = predict rounds, mr = reconstruct rounds
+ * (ftlz_fault.bit = 64 * (round - 1) + bit) */
+static int dup_masks(const ftlz_fault* faults, int64_t nf, int64_t b, int64_t p, uint64_t mp[3], uint64_t mr[3]) {
+    int any = 0;
+    mp[0] = mp[1] = mp[2] = mr[0] = mr[1] = mr[2] = 0;
+    for (int64_t f = 0; f < nf; f++) {
+        if (faults[f].block != b || faults[f].element != p) continue;
+        if (faults[f].target != FTLZ_FAULT_DUP_PREDICT && faults[f].target != FTLZ_FAULT_DUP_RECON) continue;
+        uint64_t* m = faults[f].target == FTLZ_FAULT_DUP_PREDICT ? mp : mr;
+        m[faults[f].bit >> 6] ^= 1ull << (faults[f].bit & 63);
+        any = 1;
+    }
+    return any;
+}
+
+/* stage (c) of one block (pipeline.py:382-453): predict (duplicated), quantize, reconstruct
+ * (duplicated), check; returns the unpredictable count, *mism = a duplicated evaluation of
+ * this block mismatched */
 static int64_t compress_block(const quant_t* q, const float* x, const int ext[3], int kind,
                               const float coef[4], uint32_t* bins, uint32_t* unp, uint64_t* dc_sum,
-                              double* P) {
+                              double* P, int dup, const ftlz_fault* faults, int64_t nf, int64_t blk_id,
+                              int* mism) {
     int bx = ext[0], by = ext[1], bz = ext[2];
     int py = by + 1, pz = bz + 1;
     if (kind == 0) memset(P, 0, sizeof(double) * (size_t)(bx + 1) * py * pz);
     int64_t p = 0, nu = 0;
     uint64_t dc = 0;
+    int has_dup = 0;
+    for (int64_t f = 0; f < nf; f++)
+        if (faults[f].block == blk_id &&
+            (faults[f].target == FTLZ_FAULT_DUP_PREDICT || faults[f].target == FTLZ_FAULT_DUP_RECON))
+            has_dup = 1;
+    *mism = 0;
     for (int i = 0; i < bx; i++)
         for (int j = 0; j < by; j++)
             for (int k = 0; k < bz; k++, p++) {
+                uint64_t mp[3] = {0, 0, 0}, mr[3] = {0, 0, 0};
+                if (has_dup) dup_masks(faults, nf, blk_id, p, mp, mr);
+                int pdis = 0, ddis = 0;
                 double pred = kind == 1 ? reg_pred(coef, i, j, k) : lor_pred(P, py, pz, i, j, k);
+                pred = dup_vote(pred, mp, dup, mism, &pdis);
                 double x64 = (double)x[p];
                 double diff = x64 - pred;
                 int ok;
                 uint32_t bin = quantize(q, diff, &ok);
+                if (pdis) ok = 0;
                 double offs = (double)bin - (double)q->center;
-                double dcmp = pred + q->twoeb * offs;
+                double dcmp = dup_vote(pred + q->twoeb * offs, mr, dup, mism, &ddis);
+                if (ddis) ok = 0;
                 float d32 = (float)dcmp;
                 int keep = ok && fabs(x64 - (double)d32) <= q->eb;
                 float r32 = keep ? d32 : x[p];
@@ -430,6 +476,7 @@ int oc_compress(const float* x, int64_t nx, int64_t ny, int64_t nz, int32_t eb_m
     uint8_t* in_bad = (uint8_t*)calloc((size_t)nb, 1);
     uint8_t* bin_fix = (uint8_t*)calloc((size_t)nb, 1);
     uint8_t* bin_bad = (uint8_t*)calloc((size_t)nb, 1);
+    uint8_t* dup_mm = (uint8_t*)calloc((size_t)nb, 1);
     int64_t* unp_cnt = (int64_t*)malloc(sizeof(int64_t) * (size_t)nb);
     uint64_t* bsum = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)nb);
     uint64_t* bisum = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)nb);
@@ -499,7 +546,10 @@ int oc_compress(const float* x, int64_t nx, int64_t ny, int64_t nz, int32_t eb_m
             /* stage (c) (pipeline.py:455-467); stage-(c) verification is a no-op after (b) */
             uint32_t* bb = bins + boff[b];
             uint64_t dc;
-            unp_cnt[b] = compress_block(&q, blk, ext, kind, c, bb, unpw + boff[b], &dc, tmp);
+            int mism = 0;
+            unp_cnt[b] = compress_block(&q, blk, ext, kind, c, bb, unpw + boff[b], &dc, tmp, cfg->duplicate_eval,
+                                        faults, nf, b, &mism);
+            dup_mm[b] = (uint8_t)mism;
             checksum_words(bb, vol, &bsum[b], &bisum[b]);
             dcs[b] = dc;
             /* hook STAGE_BINS_FINALIZED (pipeline.py:468) */
@@ -629,7 +679,28 @@ int oc_compress(const float* x, int64_t nx, int64_t ny, int64_t nz, int32_t eb_m
     }
     emit_list(rep->input_corrected, rep->capacity, &rep->n_input_corrected, in_fix, nb);
     emit_list(rep->bins_corrected, rep->capacity, &rep->n_bins_corrected, bin_fix, nb);
+    {
+        /* dup_mismatch_resolved lists every block of a (extent group, predictor) batch in which a
+         * duplicated evaluation mismatched (pipeline.py:440-441) */
+        int gx[64], gy[64], gz[64], gk[64], ng = 0;
+        for (int64_t b = 0; b < nb; b++) {
+            if (!dup_mm[b]) continue;
+            int64_t org[3]; int ext[3];
+            block_geom(&g, b, org, ext);
+            int t = 0;
+            while (t < ng && !(gx[t] == ext[0] && gy[t] == ext[1] && gz[t] == ext[2] && gk[t] == ind[b])) t++;
+            if (t == ng && ng < 64) { gx[ng] = ext[0]; gy[ng] = ext[1]; gz[ng] = ext[2]; gk[ng] = ind[b]; ng++; }
+        }
+        for (int64_t b = 0; b < nb && ng; b++) {
+            int64_t org[3]; int ext[3];
+            block_geom(&g, b, org, ext);
+            for (int t = 0; t < ng; t++)
+                if (gx[t] == ext[0] && gy[t] == ext[1] && gz[t] == ext[2] && gk[t] == ind[b]) dup_mm[b] = 1;
+        }
+        emit_list(rep->dup_mismatch, rep->capacity, &rep->n_dup_mismatch, dup_mm, nb);
+    }
 done:
+    free(dup_mm);
     free(coefs); free(ind); free(in_fix); free(in_bad); free(bin_fix); free(bin_bad); free(unp_cnt);
     free(bsum); free(bisum); free(dcs); free(bins); free(unpw); free(boff);
     rep->info.code = status;

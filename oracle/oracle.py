@@ -108,7 +108,8 @@ def lib():
     return _lib
 
 
-TARGETS = {"input": 0, "bins": 1, "decomp": 2, "regression": 3, "sampling": 4}
+TARGETS = {"input": 0, "bins": 1, "decomp": 2, "regression": 3, "sampling": 4, "dup_predict": 5,
+           "dup_reconstruct": 6}
 
 _FIELD_NAMES = ["header", "block indicator", "regression coefficients", "block record",
                 "codebook size", "codebook entry", "payload length", "payload",
@@ -285,7 +286,6 @@ def compress(values: np.ndarray, mode: str, value: float, cfg: dict | None = Non
     data = C.string_at(out, n.value)
     lib().oc_free(out)
     lists = _lists(rep, bufs)
-    lists["dup_mismatch_resolved"] = []
     lists["decomp_block_reexecuted"] = []
     report = {"status": _status_of(lists, False), **lists, "detail": "",
               "eb": rep.eb, "n_regression": rep.n_regression,

@@ -46,11 +46,13 @@ from .pipeline import (
 )
 from .predict import PredictorKind, RegressionCoeffs
 from .quantize import QuantConfig
+from .faults import CampaignReport, InjectionPlan, inject_bitflip, run_campaign, run_trial
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "BackendUnavailable", "BlockGrid", "BlockRecord", "BlockSpec", "BlockTooLarge",
+    "BackendUnavailable", "BlockGrid", "CampaignReport", "InjectionPlan", "inject_bitflip",
+    "run_campaign", "run_trial", "BlockRecord", "BlockSpec", "BlockTooLarge",
     "CompressedStream", "CorruptStream", "DegenerateBound", "DeviceError", "EB_ABSOLUTE",
     "EB_RELATIVE", "ErrorBound", "Field", "FtConfig", "FtReport", "FtlzError",
     "InternalInvariantViolation", "InvalidArgument", "InvalidGeometry", "InvalidInjection",

@@ -128,6 +128,24 @@ extern "C" int ftlz_peek_header(const uint8_t* d, size_t len, ftlz_header* h, ft
         if (expect >> 64) over = true;
     }
     if (over || (uint64_t)expect != nb) return fail(FTLZ_K_BLOCK_COUNT, 47, (int64_t)nb);
+    if ((len - 55) / 9 < nb) {
+        // the record table cannot fit (every record takes >= 9 bytes): the archive is truncated
+        // inside it.  Walk the records as container.py:212-218 reads them, so the error (and its
+        // offset) is the reference's, without sizing any buffer by the claimed dims.
+        size_t pos = 55;
+        for (uint64_t b = 0; b < nb; b++) {
+            if (pos + 1 > len) return fail(FTLZ_K_TRUNCATED, (int64_t)pos, FTLZ_F_INDICATOR);
+            const uint8_t ib = d[pos];
+            if (ib > 1) return fail(FTLZ_K_BAD_INDICATOR, (int64_t)pos, ib);
+            pos += 1;
+            if (ib) {
+                if (pos + 16 > len) return fail(FTLZ_K_TRUNCATED, (int64_t)pos, FTLZ_F_COEFFS);
+                pos += 16;
+            }
+            if (pos + 8 > len) return fail(FTLZ_K_TRUNCATED, (int64_t)pos, FTLZ_F_RECORD);
+            pos += 8;
+        }
+    }
     h->version = d[4];
     h->codec_id = d[5];
     h->nx = (int64_t)nx; h->ny = (int64_t)ny; h->nz = (int64_t)nz;
@@ -323,7 +341,7 @@ static KCfg kcfg_comp(const Geom& g) {
         k.stage.pad = 0;
         k.rmax = txe * tye;
         k.qr_tab = (int)al16(2 * k.stage.tile_bytes + al16(2 * (size_t)g.nvmax8));
-        size_t slot = (size_t)k.qr_tab + 8 * (2 * (size_t)k.rmax + 64) + sizeof(LHT) * 32 * (LH_BINS + 1) + 16;
+        size_t slot = (size_t)k.qr_tab + 8 * (2 * (size_t)k.rmax + 128) + sizeof(LHT) * 32 * (LH_BINS + 1) + 16;
         slot = (slot + 127) & ~(size_t)127;
         k.qr_slot = (int)slot;
         size_t avail = 227 * 1024 - 4 * HWIN_REG - 128;
@@ -419,7 +437,7 @@ static CompLayout comp_layout(const HostPlan& P, int cap, int64_t n_faults, int 
     size_t o = 0;
     auto take = [&](size_t n) { size_t r = o; o = al256(o + n); return r; };
     L.result = take(RESULT_BYTES);
-    L.hist = take(4 * c);
+    L.hist = take(8 * c);
     L.lbflag = take(4 * ntiles);
     L.events = take(nb);
     L.fixed = take(nb);
@@ -502,8 +520,9 @@ static int validate_faults(const HostPlan& P, const ftlz_fault* f, int64_t nf) {
                   ((bk == P.g.cz - 1 && P.g.rz != P.g.e) ? 1 : 0);
         int vol = P.ep[xid].vol;
         int lim = f[i].target == FTLZ_FAULT_COEFF ? 4 : f[i].target == FTLZ_FAULT_ESTIMATE ? 2 : vol;
-        int blim = f[i].target == FTLZ_FAULT_ESTIMATE ? 64 : 32;
-        if (f[i].element < 0 || f[i].element >= lim || f[i].bit < 0 || f[i].bit >= blim || f[i].target < 0 || f[i].target > 4)
+        const bool dupf = f[i].target == FTLZ_FAULT_DUP_PREDICT || f[i].target == FTLZ_FAULT_DUP_RECON;
+        int blim = f[i].target == FTLZ_FAULT_ESTIMATE ? 64 : dupf ? 192 : 32;   // dup: 64 * (round - 1) + bit
+        if (f[i].element < 0 || f[i].element >= lim || f[i].bit < 0 || f[i].bit >= blim || f[i].target < 0 || f[i].target > 6)
             return set_err(FTLZ_ERR_INVALID_ARGUMENT, "fault element/bit/target out of range");
     }
     return FTLZ_OK;
@@ -621,7 +640,7 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     A.counters = (u32*)(ws + L.result + 80);
     A.layout = (u64*)(ws + L.result + 144);
     A.qp = (QuantParams*)(ws + L.qp);
-    A.hist = (u32*)(ws + L.hist);
+    A.hist = (u64*)(ws + L.hist);
     A.enc = (u64*)(ws + L.enc);
     A.bins = (u16*)(ws + L.bins);
     A.unp_scratch = (u32*)(ws + L.unp);
@@ -731,7 +750,8 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     int64_t bad_in = -1, bad_bin = -1;
     if (counters[3]) {
         std::vector<unsigned char> ev((size_t)g.nb);
-        CK(cudaMemcpy(ev.data(), ws + L.events, (size_t)g.nb, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(ev.data(), ws + L.events, (size_t)g.nb, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
         std::tuple<int, int, int> best;
         for (int64_t b = 0; b < g.nb; b++) {
             if (ev[b] & 1) in_fix.push_back(b);
@@ -762,7 +782,8 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     std::vector<int64_t> dup;
     if (counters[1]) {
         std::vector<unsigned char> ind((size_t)g.nb);
-        CK(cudaMemcpy(ind.data(), ws + L.ind, (size_t)g.nb, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(ind.data(), ws + L.ind, (size_t)g.nb, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
         for (int64_t b = 0; b < g.nb; b++)
             if (counters[1] & (1u << (block_xid(g, b) * 2 + ind[b]))) dup.push_back(b);
     }
@@ -1085,22 +1106,26 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         int64_t b = R.counters[DC_MINFAIL];
         unsigned char k;
         long long a2[2];
-        CK(cudaMemcpy(&k, ws + L.dflag + b, 1, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(&k, ws + L.dflag + b, 1, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
         if (k == DF_PENDING) {
             // failed on the fast reader: the masked reader (which fails on exactly the same
             // blocks) names the kind and its arguments
             const u32 bb = (u32)b;
-            CK(cudaMemcpy(ws + L.mis, &bb, 4, cudaMemcpyHostToDevice));
+            CK(cudaMemcpyAsync(ws + L.mis, &bb, 4, cudaMemcpyHostToDevice, s));
             A.region = 1;
             A.n_faults = 0;
             k_decode<false, false><<<1, DEC_WARPS * 32, dec_smem, s>>>(A, (const u32*)(ws + L.mis), 1);
             LCHK("k_decode");
             CK(cudaStreamSynchronize(s));
-            CK(cudaMemcpy(&k, ws + L.dflag + b, 1, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpyAsync(&k, ws + L.dflag + b, 1, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
             if (k == DF_PENDING) return set_err(FTLZ_ERR_INVARIANT, "fast and masked decoders disagree");
         }
-        CK(cudaMemcpy(&a2[0], ws + L.da + 8 * b, 8, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(&a2[1], ws + L.db + 8 * b, 8, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(&a2[0], ws + L.da + 8 * b, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        CK(cudaMemcpyAsync(&a2[1], ws + L.db + 8 * b, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
         rep->sdc = 1;
         info_set(&rep->info, FTLZ_OK, k, -1, b, a2[0], a2[1]);
         return FTLZ_OK;
@@ -1110,9 +1135,10 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     if (nmis) {
         // re-execution of every mismatching block (pipeline.py:713-723), no fault replay
         std::vector<u32> mis(nmis);
-        CK(cudaMemcpy(mis.data(), ws + L.mis, 4 * (size_t)nmis, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(mis.data(), ws + L.mis, 4 * (size_t)nmis, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
         std::sort(mis.begin(), mis.end());
-        CK(cudaMemcpy(ws + L.mis, mis.data(), 4 * (size_t)nmis, cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(ws + L.mis, mis.data(), 4 * (size_t)nmis, cudaMemcpyHostToDevice, s));
         A.n_faults = 0;
         k_decode<false, true><<<(unsigned)((nmis + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32)), DEC_WARPS * 32, dec_smem, s>>>(
             A, (const u32*)(ws + L.mis), (int)nmis);
@@ -1198,9 +1224,10 @@ static int region_core(const HostPlan& P, const DevPlan& D, const uint8_t* d_a, 
     if (nmis) {
         // one re-execution of every mismatching block (no fault replay)
         std::vector<u32> mis(nmis);
-        CK(cudaMemcpy(mis.data(), ws + L.mis, 4 * (size_t)nmis, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(mis.data(), ws + L.mis, 4 * (size_t)nmis, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
         std::sort(mis.begin(), mis.end());
-        CK(cudaMemcpy(ws + L.mis, mis.data(), 4 * (size_t)nmis, cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(ws + L.mis, mis.data(), 4 * (size_t)nmis, cudaMemcpyHostToDevice, s));
         A.region = 0;   // re-decode failures mark mflag = 3
         k_decode<false, true><<<(nmis + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32), DEC_WARPS * 32, dec_smem, s>>>(
             A, (const u32*)(ws + L.mis), (int)nmis);
@@ -1224,8 +1251,10 @@ static int region_core(const HostPlan& P, const DevPlan& D, const uint8_t* d_a, 
             const int64_t b = order[q].second;
             if (df[b]) {
                 long long a2[2];
-                CK(cudaMemcpy(&a2[0], ws + L.da + 8 * b, 8, cudaMemcpyDeviceToHost));
-                CK(cudaMemcpy(&a2[1], ws + L.db + 8 * b, 8, cudaMemcpyDeviceToHost));
+                CK(cudaMemcpyAsync(&a2[0], ws + L.da + 8 * b, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+                CK(cudaMemcpyAsync(&a2[1], ws + L.db + 8 * b, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
                 rep->sdc = 1;
                 info_set(&rep->info, FTLZ_OK, df[b], -1, b, a2[0], a2[1]);
                 put_list(rep->reexecuted, rep->capacity, &rep->n_reexecuted, reexec);
@@ -1523,6 +1552,8 @@ extern "C" int ftlz_ctx_copy_archive(ftlz_ctx* c, void* h_dst, size_t capacity) 
 
 static int ctx_upload_archive(ftlz_ctx* c, const uint8_t* h, size_t len, ftlz_header* hdr, ftlz_report* rep) {
     report_reset(rep);
+    c->parsed_src = nullptr;   // c->arch no longer holds the parsed archive (reuse is keyed on it)
+    c->parsed_len = 0;
     int rc = ftlz_peek_header(h, len, hdr, &rep->info);
     if (rc) return set_err(rc, "bad header");
     if ((rc = c->arch.ensure(len + 64))) return rc;

@@ -146,54 +146,74 @@ FTLZ_DEV void emit_block(const CompArgs& A, long long b, int vol, const u16* bin
     }
 }
 
-// 2-of-3 voting on scalars (pipeline.py:157-179); eval3 only on mismatch
-struct DupPred {
-    double v;
-    bool mismatch, disagree;
+// STAGE_DUP_EVAL fault masks of one point (ftlz_fault FTLZ_FAULT_DUP_*): XORed into the float64
+// value evaluation round r returns (p = prediction, r = reconstruction)
+struct DupMask {
+    u64 p[3], r[3];
 };
-template <typename F3>
-FTLZ_DEV DupPred vote(double a, double b, F3 eval3) {
-    DupPred r;
-    r.v = a;
-    r.mismatch = false;
-    r.disagree = false;
-    if (dbits(a) == dbits(b)) return r;
-    double c = eval3();
-    r.mismatch = true;
-    bool ac = dbits(a) == dbits(c), bc = dbits(b) == dbits(c);
-    r.v = ac ? a : b;
-    r.disagree = !(bc || ac);
-    return r;
+
+// does block b carry duplicated-evaluation faults?
+FTLZ_DEV bool block_has_dup(const CompArgs& A, long long b) {
+    if (!A.n_faults) return false;
+    const int f0 = A.fault_first[b];
+    if (f0 < 0) return false;
+    for (int f = f0; f < A.n_faults && A.faults[f].block == b; f++)
+        if (A.faults[f].target == FTLZ_FAULT_DUP_PREDICT || A.faults[f].target == FTLZ_FAULT_DUP_RECON) return true;
+    return false;
 }
 
-// one point of stage (c) given its prediction(s): returns bin, writes reconstructed value
-// (pipeline.py:390-409 / 416-438; quantize.py:37-100)
-template <typename F3P>
-FTLZ_DEV int quant_point(const QuantParams& Q, float x32, double p1, double p2, bool dup, F3P pred3,
+// masks of point p of block b (bit = 64 * (round - 1) + b); true if any
+FTLZ_DEV bool dup_masks(const CompArgs& A, long long b, int p, DupMask& m) {
+    bool any = false;
+#pragma unroll
+    for (int r = 0; r < 3; r++) m.p[r] = m.r[r] = 0ull;
+    const int f0 = A.fault_first[b];
+    for (int f = f0; f >= 0 && f < A.n_faults && A.faults[f].block == b; f++) {
+        const ftlz_fault F = A.faults[f];
+        if (F.element != p || (F.target != FTLZ_FAULT_DUP_PREDICT && F.target != FTLZ_FAULT_DUP_RECON)) continue;
+        const u64 bit = 1ull << (F.bit & 63);
+        if (F.target == FTLZ_FAULT_DUP_PREDICT) m.p[F.bit >> 6] ^= bit;
+        else m.r[F.bit >> 6] ^= bit;
+        any = true;
+    }
+    return any;
+}
+
+// duplicated_eval of one element (pipeline.py:157-179): a = eval 1, b = eval 2 (dup only),
+// c = eval 3 only when a != b (bitwise); the vote keeps a where a == b or a == c, else b;
+// all three distinct -> *dis.  Masks model the STAGE_DUP_EVAL hook.
+template <typename F2, typename F3>
+FTLZ_DEV double dup_eval(double a, bool dup, F2 eval2, F3 eval3, const u64 m[3], bool* mism, bool* dis) {
+    const u64 ab = dbits(a) ^ m[0];
+    if (!dup) return __longlong_as_double((long long)ab);
+    const u64 bb = dbits(eval2()) ^ m[1];
+    if (ab == bb) return __longlong_as_double((long long)ab);
+    const u64 cb = dbits(eval3()) ^ m[2];
+    *mism = true;
+    if (!(bb == cb || ab == cb)) *dis = true;
+    return __longlong_as_double((long long)(ab == cb ? ab : bb));
+}
+
+// one point of stage (c) by the reference formulation (pipeline.py:390-409 / 416-438;
+// quantize.py:37-100): pred1 / pred2 / pred3 are the three independent evaluations of the
+// prediction; the reconstruction is evaluated as pred + (2 eb) * offs from independently
+// loaded operands each round.  Returns the bin, writes the reconstructed value.
+template <typename F2P, typename F3P>
+FTLZ_DEV int quant_point(const QuantParams& Q, float x32, double p1, bool dup, F2P pred2, F3P pred3, const DupMask& M,
                          float* r32, bool* mism, double* back_out) {
     double x64 = (double)x32;
-    double pred = p1;
-    bool pdis = false;
-    if (dup && dbits(p1) != dbits(p2)) {
-        DupPred pr = vote(p1, p2, pred3);
-        pred = pr.v;
-        pdis = pr.disagree;
-        *mism = true;
-    }
+    bool pdis = false, ddis = false;
+    const double pred = dup_eval(p1, dup, pred2, pred3, M.p, mism, &pdis);
     bool ok;
     int bin = quantize(Q, __dadd_rn(x64, -pred), &ok);
     if (pdis) ok = false;
-    double offs = int_to_f64(bin - Q.center);
-    double d1 = __dadd_rn(pred, __dmul_rn(Q.twoeb, offs));
-    if (dup) {
-        double d2 = __dadd_rn(opaque(pred), __dmul_rn(Q.twoeb, opaque(offs)));
-        if (dbits(d1) != dbits(d2)) {
-            DupPred dr = vote(d1, d2, [&] { return __dadd_rn(pred, __dmul_rn(Q.twoeb, opaque(opaque(offs)))); });
-            d1 = dr.v;
-            if (dr.disagree) ok = false;
-            *mism = true;
-        }
-    }
+    const double offs = int_to_f64(bin - Q.center);
+    const double d1 = dup_eval(
+        __dadd_rn(pred, __dmul_rn(Q.twoeb, offs)), dup,
+        [&] { return __dadd_rn(opaque(pred), __dmul_rn(Q.twoeb_dup, opaque(offs))); },
+        [&] { return __dadd_rn(opaque(opaque(pred)), __dmul_rn(opaque(Q.twoeb), opaque(opaque(offs)))); }, M.r, mism,
+        &ddis);
+    if (ddis) ok = false;
     float d32 = __double2float_rn(d1);
     double back = (double)d32;
     bool keep = ok && fabs(__dadd_rn(x64, -back)) <= Q.eb;
@@ -260,27 +280,45 @@ __global__ void __launch_bounds__(128) k_quant_lor(CompArgs A) {
         const u32* planes = A.planes + PL.plane_off;
         bool mism = false;
         u64 dcsum = 0;
+        const bool hasdup = block_has_dup(A, b);
+        const volatile double* vxd = xd;
         for (int s = 0; s < PL.nplanes; s++) {
             int q0 = __ldg(planes + s), q1 = __ldg(planes + s + 1);
             for (int q = q0 + lane; q < q1; q += 32) {
                 int p = __ldg(wave + q);
                 u32 c = __ldg(wcrd + q);
                 int i = c & 0xff, j = (c >> 8) & 0xff, k = c >> 16;
-                double d100 = i > 0 ? xd[p - byz] : 0.0;
-                double d010 = j > 0 ? xd[p - bz] : 0.0;
-                double d001 = k > 0 ? xd[p - 1] : 0.0;
-                double d110 = (i > 0 && j > 0) ? xd[p - byz - bz] : 0.0;
-                double d101 = (i > 0 && k > 0) ? xd[p - byz - 1] : 0.0;
-                double d011 = (j > 0 && k > 0) ? xd[p - bz - 1] : 0.0;
-                double d111 = (i > 0 && j > 0 && k > 0) ? xd[p - byz - bz - 1] : 0.0;
-                auto lor = [&](double first) {
-                    return __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(first, d010), d001), -d110), -d101), -d011), d111);
+                // the 7-term Lorenzo sum (pipeline.py:246-256); evaluations 2 and 3 re-load
+                // every neighbour from the reconstruction buffer (volatile: no reuse)
+                auto lor = [&](const double* buf) {
+                    const double d100 = i > 0 ? buf[p - byz] : 0.0;
+                    const double d010 = j > 0 ? buf[p - bz] : 0.0;
+                    const double d001 = k > 0 ? buf[p - 1] : 0.0;
+                    const double d110 = (i > 0 && j > 0) ? buf[p - byz - bz] : 0.0;
+                    const double d101 = (i > 0 && k > 0) ? buf[p - byz - 1] : 0.0;
+                    const double d011 = (j > 0 && k > 0) ? buf[p - bz - 1] : 0.0;
+                    const double d111 = (i > 0 && j > 0 && k > 0) ? buf[p - byz - bz - 1] : 0.0;
+                    return __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(d100, d010), d001), -d110), -d101), -d011), d111);
                 };
-                double p1 = lor(d100);
-                double p2 = dup ? lor(opaque(d100)) : p1;
+                auto lorv = [&]() {
+                    const double d100 = i > 0 ? vxd[p - byz] : 0.0;
+                    const double d010 = j > 0 ? vxd[p - bz] : 0.0;
+                    const double d001 = k > 0 ? vxd[p - 1] : 0.0;
+                    const double d110 = (i > 0 && j > 0) ? vxd[p - byz - bz] : 0.0;
+                    const double d101 = (i > 0 && k > 0) ? vxd[p - byz - 1] : 0.0;
+                    const double d011 = (j > 0 && k > 0) ? vxd[p - bz - 1] : 0.0;
+                    const double d111 = (i > 0 && j > 0 && k > 0) ? vxd[p - byz - bz - 1] : 0.0;
+                    return __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(d100, d010), d001), -d110), -d101), -d011), d111);
+                };
+                DupMask M;
+                if (hasdup) dup_masks(A, b, p, M);
+                else {
+#pragma unroll
+                    for (int r = 0; r < 3; r++) M.p[r] = M.r[r] = 0ull;
+                }
                 float r32;
                 double back;
-                int bin = quant_point<>(Q, xf[p], p1, p2, dup, [&] { return lor(opaque(opaque(d100))); }, &r32, &mism, &back);
+                int bin = quant_point(Q, xf[p], lor(xd), dup, lorv, lorv, M, &r32, &mism, &back);
                 xd[p] = back;
                 bins16[p] = (u16)bin;
                 dcsum += __float_as_uint(r32);

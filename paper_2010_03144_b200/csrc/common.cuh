@@ -391,17 +391,17 @@ FTLZ_DEV void bitonic_sort_u64_plain(u64* keys, int n_pow2) {
 #define HWIN 4096   // shared-memory histogram window around the quantizer center
 
 // histogram increment: shared window (flushed once per CTA) or global for outliers
-FTLZ_DEV void hist_add(u32* hwin, u32* ghist, int wlo, int bin, u32 cnt) {
+FTLZ_DEV void hist_add(u32* hwin, u64* ghist, int wlo, int bin, u32 cnt) {
     unsigned o = (unsigned)(bin - wlo);
     if (o < HWIN) atomicAdd(&hwin[o], cnt);
-    else atomicAdd(&ghist[bin], cnt);
+    else atomicAdd(&ghist[bin], (u64)cnt);
 }
 
-FTLZ_DEV void hist_flush(u32* hwin, u32* ghist, int wlo, int cap) {
+FTLZ_DEV void hist_flush(u32* hwin, u64* ghist, int wlo, int cap) {
     for (int t = threadIdx.x; t < HWIN; t += blockDim.x) {
         u32 v = hwin[t];
         int s = wlo + t;
-        if (v && s >= 0 && s < cap) atomicAdd(&ghist[s], v);
+        if (v && s >= 0 && s < cap) atomicAdd(&ghist[s], (u64)v);
     }
 }
 

@@ -65,7 +65,7 @@ struct CompArgs {
     u32* minmax;         // [0] ordered max, [1] ordered min, [2] nan flag
     u32* counters;       // [0] n_reg, [1] dup group flags, [2] encode ticket, [3] events, [4] n_lor
     QuantParams* qp;
-    u32* hist;           // cap entries
+    u64* hist;           // cap entries (u64: a field may hold more than 2^32 points)
     u64* enc;            // cap entries: code << 6 | len (0 = absent)
     u64* layout;         // archive layout (see LAYOUT_*)
     long long pb0, pb1;  // k_prep's blocks (slabs of block layers when the upload is overlapped)
@@ -579,8 +579,8 @@ __global__ void k_fault_bins(CompArgs A, u32* fix_scratch, u8* fixed) {
                 dev_fail(A.st, FTLZ_ERR_INVARIANT, FTLZ_K_BIN_RANGE, -1, -1, 0, 0, 0);
                 continue;
             }
-            atomicSub(&A.hist[orig], 1u);
-            atomicAdd(&A.hist[w[p]], 1u);
+            atomicAdd(&A.hist[orig], ~0ull);   // -1
+            atomicAdd(&A.hist[w[p]], 1ull);
         }
         if (lane == 0) fixed[b] = 1;
     }

@@ -69,21 +69,21 @@ typedef u16 LHT;
 #endif
 #define HWIN_REG 2048
 
-FTLZ_DEV void reg_hist_out(u32* hwin, u32* ghist, int wlo, int bin, u32 delta) {
+FTLZ_DEV void reg_hist_out(u32* hwin, u64* ghist, int wlo, int bin, int delta) {
     unsigned ow = (unsigned)(bin - wlo);
-    if (ow < HWIN_REG) atomicAdd(&hwin[ow], delta);
-    else atomicAdd(&ghist[bin], delta);
+    if (ow < HWIN_REG) atomicAdd(&hwin[ow], (u32)delta);
+    else atomicAdd(&ghist[bin], (u64)(long long)delta);
 }
-FTLZ_DEV void reg_hist_add(LHT* lh16, u32* hwin, u32* ghist, int lhlo, int wlo, int bin, int lane, int delta) {
+FTLZ_DEV void reg_hist_add(LHT* lh16, u32* hwin, u64* ghist, int lhlo, int wlo, int bin, int lane, int delta) {
     unsigned o = (unsigned)(bin - lhlo);
     if (o < LH_BINS) lh16[o * 32 + lane] += (LHT)delta;
-    else reg_hist_out(hwin, ghist, wlo, bin, (u32)delta);
+    else reg_hist_out(hwin, ghist, wlo, bin, delta);
 }
 
 #ifdef LH8
 // lane l sums bins lhlo + 4l .. + 3 over the 32 lane counters (8 words of 4 bytes each) and
 // clears them
-FTLZ_DEV void reg_hist_flush_lanes(LHT* lh16, u32* ghist, int lhlo, int cap, int lane) {
+FTLZ_DEV void reg_hist_flush_lanes(LHT* lh16, u64* ghist, int lhlo, int cap, int lane) {
     __syncwarp();
     u32* w32 = (u32*)lh16;   // bin o occupies words o*8 .. o*8+7
 #pragma unroll
@@ -98,13 +98,13 @@ FTLZ_DEV void reg_hist_flush_lanes(LHT* lh16, u32* ghist, int lhlo, int cap, int
             w32[o * 8 + cc] = 0;
         }
         const int bn = lhlo + o;
-        if (sum && bn >= 0 && bn < cap) atomicAdd(&ghist[bn], sum);
+        if (sum && bn >= 0 && bn < cap) atomicAdd(&ghist[bn], (u64)sum);
     }
     __syncwarp();
 }
 #else
 // lane l sums bins lhlo + 2l and lhlo + 2l + 1 over the 32 lane counters and clears them
-FTLZ_DEV void reg_hist_flush_lanes(LHT* lh16, u32* ghist, int lhlo, int cap, int lane) {
+FTLZ_DEV void reg_hist_flush_lanes(LHT* lh16, u64* ghist, int lhlo, int cap, int lane) {
     __syncwarp();
     u32* w32 = (u32*)lh16;   // bin o occupies words o*16 .. o*16+15
     u32 lo = 0, hi = 0;
@@ -118,8 +118,8 @@ FTLZ_DEV void reg_hist_flush_lanes(LHT* lh16, u32* ghist, int lhlo, int cap, int
         hi += (b & 0xffffu) + (b >> 16);
     }
     int b0 = lhlo + 2 * lane;
-    if (lo && b0 >= 0 && b0 < cap) atomicAdd(&ghist[b0], lo);
-    if (hi && b0 + 1 >= 0 && b0 + 1 < cap) atomicAdd(&ghist[b0 + 1], hi);
+    if (lo && b0 >= 0 && b0 < cap) atomicAdd(&ghist[b0], (u64)lo);
+    if (hi && b0 + 1 >= 0 && b0 + 1 < cap) atomicAdd(&ghist[b0 + 1], (u64)hi);
     __syncwarp();
 }
 #endif
@@ -148,14 +148,15 @@ struct RegPos {
 
 struct RegBlk {
     const float* tile;
-    const double *abt, *abt2, *ctab;
+    const double *abt, *abt2, *ctab, *ctab2;
     u16* bins16;
     int by, bz, tjump, ijump;
 };
 
 // fast path for one point: bin, reconstructed value, ambiguity flag
 template <bool DUP>
-FTLZ_DEV u32 reg_point_fast(const QuantParams& Q, float x32, double ab, double ab2, double ck, float& r32, u32& slow) {
+FTLZ_DEV u32 reg_point_fast(const QuantParams& Q, float x32, double ab, double ab2, double ck, double ck2, float& r32,
+                            u32& slow) {
     const double x64 = (double)x32;
     const double p1 = __dadd_rn(ab, ck);
     bool ok;
@@ -165,7 +166,7 @@ FTLZ_DEV u32 reg_point_fast(const QuantParams& Q, float x32, double ab, double a
     const double d1 = __dadd_rn(p1, __dmul_rn(Q.twoeb, offs));
     if (DUP) {
         // second evaluation from independently loaded operands (ab2, twoeb_dup)
-        const double p2 = __dadd_rn(ab2, ck);
+        const double p2 = __dadd_rn(ab2, ck2);
         const double d2 = __dadd_rn(p2, __dmul_rn(Q.twoeb_dup, offs));
         const u64 xx = (dbits(p1) ^ dbits(p2)) | (dbits(d1) ^ dbits(d2));
         slow |= (u32)xx | (u32)(xx >> 32);
@@ -203,18 +204,19 @@ FTLZ_DEV void reg_step(RegPos& P, const RegBlk& K) {
 #endif
 template <bool DUP, bool PIN, bool FULLJ>
 FTLZ_DEV void reg_points(const QuantParams& Q, const RegBlk& K, RegPos P, int p0, int pend, int lane, LHT* lh16,
-                         u32* hwin, u32* ghist, int lhlo, int wlo, RegAcc& acc) {
+                         u32* hwin, u64* ghist, int lhlo, int wlo, RegAcc& acc) {
     u32 flag = 0, outw = 0;
     int p = p0;
     for (; p + RB <= pend; p += RB) {
         float x[RB];
-        double ab[RB], ab2[RB], ck[RB];
+        double ab[RB], ab2[RB], ck[RB], ck2[RB];
 #pragma unroll
         for (int u = 0; u < RB; u++) {
             x[u] = K.tile[P.t];
             ab[u] = K.abt[P.rp];
             ab2[u] = DUP ? K.abt2[P.rp] : ab[u];
             ck[u] = K.ctab[P.k];
+            ck2[u] = DUP ? K.ctab2[P.k] : ck[u];
             reg_step<FULLJ>(P, K);
         }
         u32 fb[RB];
@@ -222,7 +224,7 @@ FTLZ_DEV void reg_points(const QuantParams& Q, const RegBlk& K, RegPos P, int p0
 #pragma unroll
         for (int u = 0; u < RB; u++) {
             u32 slow;
-            fb[u] = reg_point_fast<DUP>(Q, x[u], ab[u], ab2[u], ck[u], r32[u], slow);
+            fb[u] = reg_point_fast<DUP>(Q, x[u], ab[u], ab2[u], ck[u], ck2[u], r32[u], slow);
             flag |= slow;
         }
 #pragma unroll
@@ -251,7 +253,7 @@ FTLZ_DEV void reg_points(const QuantParams& Q, const RegBlk& K, RegPos P, int p0
         }
         float r32;
         u32 slow;
-        const u32 fb = reg_point_fast<DUP>(Q, x32, ab, ab2, K.ctab[P.k], r32, slow);
+        const u32 fb = reg_point_fast<DUP>(Q, x32, ab, ab2, K.ctab[P.k], DUP ? K.ctab2[P.k] : K.ctab[P.k], r32, slow);
         flag |= slow;
         K.bins16[p] = (u16)fb;
         acc.bs += fb;
@@ -266,37 +268,46 @@ FTLZ_DEV void reg_points(const QuantParams& Q, const RegBlk& K, RegPos P, int p0
 }
 
 // out-of-window bins of this lane's range (after any fixup): CTA window / global atomics
-FTLZ_DEV void reg_hist_outwin(const u16* bins16, int p0, int pend, u32* hwin, u32* ghist, int lhlo, int wlo) {
+FTLZ_DEV void reg_hist_outwin(const u16* bins16, int p0, int pend, u32* hwin, u64* ghist, int lhlo, int wlo) {
     for (int p = p0; p < pend; p++) {
         const int bin = bins16[p];
-        if ((unsigned)(bin - lhlo) >= LH_BINS) reg_hist_out(hwin, ghist, wlo, bin, 1u);
+        if ((unsigned)(bin - lhlo) >= LH_BINS) reg_hist_out(hwin, ghist, wlo, bin, 1);
     }
 }
 
 // exact recomputation of the ambiguous points of this lane (rare): rescan the range with the
-// fast path and replace every flagged point's results by the exact formulation's
+// fast path and replace every flagged point's results by the exact formulation's; points with
+// injected duplicated-evaluation faults (hasdup) always take the exact formulation
 template <bool DUP>
-FTLZ_DEV void reg_fixup(const QuantParams& Q, const RegBlk& K, const float4& cf, int p0, int pend, int zoff, int tz,
-                        int tye, int lane, LHT* lh16, u32* hwin, u32* ghist, int lhlo, int wlo, RegAcc& acc,
-                        bool& mism) {
+FTLZ_DEV void reg_fixup(const CompArgs& A, long long b, bool hasdup, const QuantParams& Q, const RegBlk& K,
+                        const float4& cf, int p0, int pend, int zoff, int tz, int tye, int lane, LHT* lh16, u32* hwin,
+                        u64* ghist, int lhlo, int wlo, RegAcc& acc, bool& mism) {
     for (int p = p0; p < pend; p++) {
         const int rp = p / K.bz, k = p - rp * K.bz, i = rp / K.by, j = rp - i * K.by;
         const float x32 = K.tile[(i * tye + j) * tz + zoff + k];
-        const double ab = K.abt[rp], ab2 = DUP ? K.abt2[rp] : ab, ck = K.ctab[k];
+        const double ab = K.abt[rp], ab2 = DUP ? K.abt2[rp] : ab, ck = K.ctab[k], ck2 = DUP ? K.ctab2[k] : ck;
         float rf;
         u32 slow;
-        const u32 fb_fast = reg_point_fast<DUP>(Q, x32, ab, ab2, ck, rf, slow);
-        if (!slow) continue;
+        const u32 fb_fast = reg_point_fast<DUP>(Q, x32, ab, ab2, ck, ck2, rf, slow);
+        DupMask M;
+        const bool fp = hasdup && dup_masks(A, b, p, M);
+        if (!slow && !fp) continue;
+        if (!fp) {
+#pragma unroll
+            for (int r = 0; r < 3; r++) M.p[r] = M.r[r] = 0ull;
+        }
         float rx;
         double back;
-        const u32 fb = (u32)quant_point<>(
-            Q, x32, __dadd_rn(ab, ck), __dadd_rn(ab2, ck), DUP,
+        // evaluation 1 from the row / k tables, 2 from their independently built copies, 3 from
+        // the float32 coefficients (pipeline.py:392-394 re-evaluates _regression_grid_batch)
+        const u32 fb = (u32)quant_point(
+            Q, x32, __dadd_rn(ab, ck), DUP, [&] { return __dadd_rn(opaque(ab2), opaque(ck2)); },
             [&] {
                 return __dadd_rn(__dadd_rn(__dadd_rn((double)cf.x, __dmul_rn((double)cf.y, int_to_f64(i))),
                                            __dmul_rn((double)cf.z, int_to_f64(j))),
-                                 __dmul_rn((double)cf.w, int_to_f64(k)));
+                                 __dmul_rn(opaque((double)cf.w), int_to_f64(k)));
             },
-            &rx, &mism, &back);
+            M, &rx, &mism, &back);
         K.bins16[p] = (u16)fb;
         acc.bs += fb - fb_fast;
         acc.bis += (u64)(u32)p * (u64)fb - (u64)(u32)p * (u64)fb_fast;
@@ -331,7 +342,8 @@ __global__ void __launch_bounds__(QR_WARPS * 32, 1) k_quant_reg(const __grid_con
     double* abt = (double*)(slot + A.qr_tab);
     double* abt2 = abt + A.rmax;
     double* ctab = abt2 + A.rmax;
-    LHT* lh16 = (LHT*)(ctab + 64);
+    double* ctab2 = ctab + 64;
+    LHT* lh16 = (LHT*)(ctab2 + 64);
     ws.bar = (u64*)(lh16 + (LH_BINS + 1) * 32);
     u32* hwin = (u32*)(smem + (size_t)nw * A.qr_slot);
     const int wlo = A.center - HWIN_REG / 2, lhlo = A.center - LH_BINS / 2;
@@ -379,7 +391,10 @@ __global__ void __launch_bounds__(QR_WARPS * 32, 1) k_quant_reg(const __grid_con
             if (dup)
                 abt2[r] = __dadd_rn(__dadd_rn((double)cg.x, __dmul_rn((double)cg.y, di)), __dmul_rn((double)cg.z, dj));
         }
-        for (int k = lane; k < bz; k += 32) ctab[k] = __dmul_rn((double)cf.w, int_to_f64(k));
+        for (int k = lane; k < bz; k += 32) {
+            ctab[k] = __dmul_rn((double)cf.w, int_to_f64(k));
+            if (dup) ctab2[k] = __dmul_rn((double)cg.w, int_to_f64(k));
+        }
         __syncwarp();
 
         const int chunk = ((vol + 31) >> 5) | 1;
@@ -393,7 +408,8 @@ __global__ void __launch_bounds__(QR_WARPS * 32, 1) k_quant_reg(const __grid_con
         }
         P0.t = (P0.i * S.tye + P0.j) * S.tz + w0.zoff + P0.k;
         RegBlk K;
-        K.tile = tile; K.abt = abt; K.abt2 = abt2; K.ctab = ctab; K.bins16 = bins16;
+        K.tile = tile; K.abt = abt; K.abt2 = abt2; K.ctab = ctab; K.ctab2 = ctab2; K.bins16 = bins16;
+        const bool hasdup = block_has_dup(A, b);
         K.by = by; K.bz = bz; K.tjump = S.tz - bz; K.ijump = (S.tye - by) * S.tz;
         RegAcc acc;
         bool mism = false, skip = false;
@@ -412,10 +428,11 @@ __global__ void __launch_bounds__(QR_WARPS * 32, 1) k_quant_reg(const __grid_con
                 if (pin) reg_points<false, true, false>(Q, K, P0, p0, pend, lane, lh16, hwin, A.hist, lhlo, wlo, acc);
                 else reg_points<false, false, false>(Q, K, P0, p0, pend, lane, lh16, hwin, A.hist, lhlo, wlo, acc);
             }
+            if (hasdup) acc.flagged = 1;
             if (__any_sync(0xffffffffu, acc.flagged != 0)) {
                 if (acc.flagged) {
-                    if (dup) reg_fixup<true>(Q, K, cf, p0, pend, w0.zoff, S.tz, S.tye, lane, lh16, hwin, A.hist, lhlo, wlo, acc, mism);
-                    else reg_fixup<false>(Q, K, cf, p0, pend, w0.zoff, S.tz, S.tye, lane, lh16, hwin, A.hist, lhlo, wlo, acc, mism);
+                    if (dup) reg_fixup<true>(A, b, hasdup, Q, K, cf, p0, pend, w0.zoff, S.tz, S.tye, lane, lh16, hwin, A.hist, lhlo, wlo, acc, mism);
+                    else reg_fixup<false>(A, b, hasdup, Q, K, cf, p0, pend, w0.zoff, S.tz, S.tye, lane, lh16, hwin, A.hist, lhlo, wlo, acc, mism);
                 }
             }
             if (__any_sync(0xffffffffu, acc.outwin != 0) && acc.outwin)
@@ -495,7 +512,7 @@ __global__ void __launch_bounds__(QR_WARPS * 32, 1) k_quant_reg(const __grid_con
     for (int t = threadIdx.x; t < HWIN_REG; t += blockDim.x) {
         u32 v = hwin[t];
         int s = wlo + t;
-        if (v && s >= 0 && s < A.cap) atomicAdd(&A.hist[s], v);
+        if (v && s >= 0 && s < A.cap) atomicAdd(&A.hist[s], (u64)v);
     }
 }
 

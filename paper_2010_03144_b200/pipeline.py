@@ -5,7 +5,8 @@ duplicated prediction/reconstruction, quantization, ABFT checksums, Huffman codi
 assembly) and Algorithm 2 (device parse, decode, reconstruction, checksum verification,
 re-execution).  Fault injection uses per-call descriptors instead of the reference's global
 hook registry: ``faults=[(target, block, element, bit), ...]`` with the targets of
-faults.py:157-189 ("input", "bins", "decomp", "regression", "sampling").
+faults.py:157-189 ("input", "bins", "decomp", "regression", "sampling") plus the duplicated-
+evaluation seam ("dup_predict", "dup_reconstruct"; hooks.STAGE_DUP_EVAL).
 """
 
 from __future__ import annotations
@@ -30,7 +31,10 @@ STATUS_SDC = "sdc_in_compression"
 CODEC_IDENTITY = 0
 
 TARGETS = {"input": 0, "input_after_checksum": 0, "bins": 1, "bin_array": 1, "decomp": 2,
-           "decompressed_buffer": 2, "regression": 3, "regression_fit": 3, "sampling": 4}
+           "decompressed_buffer": 2, "regression": 3, "regression_fit": 3, "sampling": 4,
+           "dup_predict": 5, "dup_reconstruct": 6}
+# dup_* faults (STAGE_DUP_EVAL, pipeline.py:157-179): bit = 64 * (round - 1) + b flips bit b of
+# the float64 value evaluation `round` (1..3) of the prediction / reconstruction returns
 
 
 @dataclass(frozen=True)
@@ -113,9 +117,12 @@ def _report_buf(capacity: int) -> "_ReportBuf":
     cache = getattr(_tls, "reports", None)
     if cache is None:
         cache = _tls.reports = {}
-    rb = cache.get(capacity)
+    rb = cache.pop(capacity, None)
     if rb is None:
-        rb = cache[capacity] = _ReportBuf(capacity)
+        rb = _ReportBuf(capacity)
+        while len(cache) >= 4:   # bounded: keep the most recently used block counts
+            cache.pop(next(iter(cache)))
+    cache[capacity] = rb
     return rb
 
 
@@ -134,14 +141,16 @@ class _ReportBuf:
         return [b[:n].tolist() for b, n in zip(self.bufs, ns)]
 
 
-def _check_faults(faults, grid, targets):
-    for f in faults or []:
-        t = f[0]
-        if (TARGETS.get(t, t) if isinstance(t, str) else t) not in targets:
-            continue
-        b = int(f[1])
-        if not 0 <= b < grid.n_blocks:
-            raise InvalidInjection(f"block {b} out of range [0, {grid.n_blocks})")
+def _check_out(out, shape):
+    """A caller-supplied output array receives 4 * prod(shape) bytes straight from the device:
+    it must be a writable, C-contiguous float32 array of exactly that size."""
+    if not isinstance(out, np.ndarray):
+        raise ValueError("out must be a numpy float32 array")
+    n = int(np.prod(shape, dtype=np.int64))
+    if out.dtype != np.float32 or not out.flags.c_contiguous or not out.flags.writeable or out.size != n:
+        raise ValueError(f"out must be a writable C-contiguous float32 array of {n} elements "
+                         f"(got {out.dtype}, {out.size} elements, contiguous={out.flags.c_contiguous}, "
+                         f"writeable={out.flags.writeable})")
 
 
 def compress(field: Field, eb_spec: ErrorBound, cfg: FtConfig = FtConfig(), threads: int = 1,
@@ -223,12 +232,16 @@ def _decompress_bytes(data, faults=None, out=None, reuse=None):
         # any contiguous byte buffer (e.g. pinned numpy memory) is read in place
         data = np.frombuffer(data, np.uint8)
     buf = data if isinstance(data, bytes) else data.ctypes.data
-    head = bytes(data[:64])
-    st = L.ftlz_peek_header(head, len(data), C.byref(hdr), C.byref(info))
+    # the header checks see the whole buffer: an archive too short for its record table is
+    # rejected here (reference message and offset) before anything is sized by its dims
+    st = L.ftlz_peek_header(buf, len(data), C.byref(hdr), C.byref(info))
     if st != 0:
         raise_for_info(st, info, data)
+    shape = (hdr.nx, hdr.ny, hdr.nz)
     if out is None:
-        out = np.empty((hdr.nx, hdr.ny, hdr.nz), np.float32)
+        out = np.empty(shape, np.float32)
+    else:
+        _check_out(out, shape)
     fa, nf = _faults_c(faults)
     rb = _report_buf(int(hdr.block_count))
     st = L.ftlz_ctx_decompress_host(ctx, buf, len(data), out.ctypes.data, fa, nf,
@@ -269,8 +282,7 @@ def decompress_region(stream: CompressedStream, region, threads: int = 1) -> tup
     out = np.empty((x1 - x0, y1 - y0, z1 - z0), np.float32)
     hdr = _lib.Header()
     info = _lib.Info()
-    head = bytes(data[:64])
-    st = L.ftlz_peek_header(head, len(data), C.byref(hdr), C.byref(info))
+    st = L.ftlz_peek_header(data, len(data), C.byref(hdr), C.byref(info))
     if st != 0:
         raise_for_info(st, info, data)
     rb = _report_buf(int(hdr.block_count))

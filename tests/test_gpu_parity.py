@@ -236,3 +236,41 @@ def test_alphabet_sizes_sort_and_merge_paths(ebv):
     out = F.decompress_bytes(got)
     ref, _ = O.decompress(want, threads=4)
     np.testing.assert_array_equal(out.view(np.uint32), ref.view(np.uint32))
+
+
+def test_parse_reuse_is_invalidated_by_another_upload():
+    """parse(a) leaves a's device copy for decompress(s_a) to reuse; any other archive uploaded
+    in between (decompress_bytes(b), decompress of another stream) must invalidate that, so
+    decompress(s_a) still returns a's data (stale-archive reuse)."""
+    xa = _seeded("smooth", (30, 20, 25), seed=1)
+    xb = _seeded("smooth", (30, 20, 25), seed=2)
+    a = F.compress_bytes(xa, "absolute", 1e-3)
+    b = F.compress_bytes(xb, "absolute", 1e-3)
+    ya = F.decompress_bytes(a)
+    yb = F.decompress_bytes(b)
+    sa = F.parse(a)
+    F.decompress_bytes(b)
+    out, _ = F.decompress(sa)
+    np.testing.assert_array_equal(out.values.view(np.uint32), ya.view(np.uint32))
+    sb = F.parse(b)
+    out, _ = F.decompress(F.parse(a))
+    np.testing.assert_array_equal(out.values.view(np.uint32), ya.view(np.uint32))
+    out, _ = F.decompress(sb)
+    np.testing.assert_array_equal(out.values.view(np.uint32), yb.view(np.uint32))
+    reg, _ = F.decompress_region(sa, ((1, 2, 3), (20, 15, 22)))
+    np.testing.assert_array_equal(reg.values.view(np.uint32), ya[1:20, 2:15, 3:22].view(np.uint32))
+
+
+def test_decompress_bytes_validates_caller_output_buffer():
+    x = _seeded("smooth", (12, 10, 9), seed=4)
+    data = F.compress_bytes(x, "absolute", 1e-3)
+    good = np.empty(x.size, np.float32)
+    assert F.decompress_bytes(data, out=good) is good
+    for bad in (np.empty(x.size - 1, np.float32), np.empty(x.size, np.float64),
+                np.empty((x.size * 2,), np.float32)[::2]):
+        with pytest.raises(ValueError):
+            F.decompress_bytes(data, out=bad)
+    ro = np.empty(x.size, np.float32)
+    ro.flags.writeable = False
+    with pytest.raises(ValueError):
+        F.decompress_bytes(data, out=ro)

@@ -44,7 +44,7 @@ def test_library_loads_and_exports_every_symbol():
     L = _lib.load()
     for name in _header_functions():
         assert hasattr(L, name), name
-    assert L.ftlz_abi_version() == 2
+    assert L.ftlz_abi_version() == 3
 
 
 def test_default_config_matches_reference_defaults():
@@ -227,3 +227,34 @@ def test_fault_plan_helpers_mirror_reference():
     assert b == bytearray(b"\x00\x03")
     s1, s2 = FT.trial_seed(7, 0, 0), FT.trial_seed(7, 0, 1)
     assert s1 != s2 and s1 == FT.trial_seed(7, 0, 0)
+
+
+@pytest.mark.parametrize("dims,cut,flip", [((4096, 4096, 4096), 200, None), ((1000, 1000, 1000), 55, None),
+                                           ((64, 64, 64), 70, None), ((300, 300, 300), 90, 2)])
+def test_peek_header_rejects_short_record_tables_like_reference(dims, cut, flip):
+    """An archive too short for the record table its dims imply is rejected by the host header
+    check with the reference parse's own message and offset (container.py:212-218), before
+    any buffer is sized by the claimed dims (the oracle restates the reference parse)."""
+    from oracle import oracle as O
+
+    nb = 1
+    for d in dims:
+        nb *= -(-d // 10)
+    hdr = (b"FTLZ" + bytes([1, 0]) + b"".join(int(d).to_bytes(8, "little") for d in dims)
+           + (10).to_bytes(4, "little") + bytes([1]) + np.float64(0.5).tobytes()
+           + (65536).to_bytes(4, "little") + nb.to_bytes(8, "little"))
+    body = bytearray((np.arange(cut, dtype=np.int64) % 7 == 0).astype(np.uint8).tobytes())
+    if flip is not None and flip < len(body):
+        body[flip] = 5   # a bad indicator byte inside the table
+    blob = hdr + bytes(body)
+    L = _lib.load()
+    h, info = _lib.Header(), _lib.Info()
+    assert L.ftlz_peek_header(blob, len(blob), h, info) == 5
+    with pytest.raises(O.OracleError) as ei:
+        O.parse_check(blob)
+    assert ei.value.offset == info.offset
+    from paper_2010_03144_b200._messages import raise_for_info
+
+    with pytest.raises(F.FtlzError) as e2:
+        raise_for_info(5, info, blob)
+    assert (type(e2.value).__name__, str(e2.value)) == (ei.value.cls, str(ei.value))

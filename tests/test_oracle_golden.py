@@ -83,3 +83,27 @@ def test_oracle_rle_invert_errors():
     with pytest.raises(O.OracleError) as ei:
         O.rle_invert(b"\x01\x02\x00\x05")
     assert str(ei.value) == "run-length stream has zero-length run"
+
+
+def _truncation():
+    import json
+    import os
+
+    from tests.golden_util import GOLDEN
+
+    with open(os.path.join(GOLDEN, "truncation.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("src", sorted(_truncation()))
+def test_oracle_truncation_sweep_every_byte(src):
+    """test_container.py:59-63: every proper prefix of an archive is a CorruptStream, with the
+    reference's own message and offset for each cut."""
+    t = _truncation()[src]
+    arch = load(src)["archive"].tobytes()
+    assert len(arch) == t["len"]
+    for cut, ix in enumerate(t["index"]):
+        cls, msg = t["messages"][ix]
+        with pytest.raises(O.OracleError) as ei:
+            O.parse_check(arch[:cut])
+        assert (ei.value.cls, str(ei.value)) == (cls, msg), cut

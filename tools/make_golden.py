@@ -75,6 +75,42 @@ def run_compress(values, mode, value, cfg, faults, override):
             arr = est_reg if e == 0 else est_lor
             arr[b: b + 1].view(np.uint64)[0] ^= np.uint64(1 << bit)
 
+    dups = [(t, b, e, bit // 64 + 1, bit % 64) for t, b, e, bit in faults if t.startswith("dup_")]
+
+    def h_dup(tag, rnd, arr):
+        # STAGE_DUP_EVAL fires inside duplicated_eval with the whole batch of one (extent group,
+        # predictor) subset: (n, bx, by, bz) for regression, (n, m) per Lorenzo wavefront.  The
+        # calling _compress_rows frame names the batch's blocks and the current wavefront.
+        fr = sys._getframe(1)
+        while fr is not None and fr.f_code.co_name != "_compress_rows":
+            fr = fr.f_back
+        loc = fr.f_locals
+        blocks = loc["ids"][loc["rows"]]
+        out = None
+        for t, b, e, r, bit in dups:
+            if r != rnd or t != "dup_" + tag:
+                continue
+            hit = np.flatnonzero(blocks == b)
+            if not hit.size:
+                continue
+            if arr.ndim == 4:
+                q = e
+            else:
+                _, by, bz = loc["extent"]
+                li, rem = divmod(e, by * bz)
+                lj, lk = divmod(rem, bz)
+                qq = np.flatnonzero((loc["ii"] == li) & (loc["jj"] == lj) & (loc["kk"] == lk))
+                if not qq.size:
+                    continue
+                q = int(qq[0])
+            if out is None:
+                out = np.array(arr, dtype=np.float64, copy=True)
+            v = out.reshape(len(blocks), -1)
+            v[hit[0]: hit[0] + 1, q: q + 1].view(np.uint64)[0, 0] ^= np.uint64(1 << bit)
+        return arr if out is None else out
+
+    if dups:
+        hooks.arm(hooks.STAGE_DUP_EVAL, h_dup)
     if "input" in byt:
         hooks.arm(hooks.STAGE_INPUT_AFTER_CHECKSUM, h_input)
     if "bins" in byt:
@@ -193,6 +229,30 @@ def small_cases():
         {"block_edge": 5, "protect_input": False, "protect_bins": False,
          "duplicate_eval": False, "store_sum_dc": False},
         [("decomp", 3, 10, 30)])
+    # duplicated evaluation (STAGE_DUP_EVAL, pipeline.py:157-179): bit = 64 * (round - 1) + b.
+    # Regression blocks of `base` (edge 5): 4, 6, 8, 15, 17, 26-31, 34; the rest are Lorenzo.
+    R1, R2, R3 = 0, 64, 128
+    add("dup_majority", base, A, 1e-3, {"block_edge": 5},
+        [("dup_reconstruct", 4, 7, R1 + 52), ("dup_predict", 4, 20, R2 + 40),
+         ("dup_predict", 0, 3, R1 + 45), ("dup_reconstruct", 2, 30, R2 + 10),
+         ("dup_predict", 30, 11, R1 + 63), ("dup_reconstruct", 8, 6, R1 + 62)])
+    add("dup_triple_disagreement", base, A, 1e-3, {"block_edge": 5},
+        [("dup_reconstruct", 4, 7, R1 + 51), ("dup_reconstruct", 4, 7, R3 + 30),
+         ("dup_predict", 0, 12, R1 + 45), ("dup_predict", 0, 12, R2 + 20),
+         ("dup_predict", 15, 40, R1 + 33), ("dup_predict", 15, 40, R2 + 34), ("dup_predict", 15, 40, R3 + 35),
+         ("dup_reconstruct", 5, 0, R1 + 1), ("dup_reconstruct", 5, 0, R3 + 2)])
+    add("dup_same_flip_rounds_1_2", base, A, 1e-3, {"block_edge": 5},
+        [("dup_predict", 6, 9, R1 + 48), ("dup_predict", 6, 9, R2 + 48),
+         ("dup_reconstruct", 3, 14, R1 + 40), ("dup_reconstruct", 3, 14, R2 + 40)])
+    add("dup_round3_only", base, A, 1e-3, {"block_edge": 5},
+        [("dup_predict", 4, 5, R3 + 60), ("dup_reconstruct", 1, 9, R3 + 61)])
+    add("dup_unprotected", base, A, 1e-3, {"block_edge": 5, "duplicate_eval": False},
+        [("dup_predict", 4, 3, R1 + 50), ("dup_reconstruct", 1, 4, R1 + 33), ("dup_predict", 6, 2, R2 + 50),
+         ("dup_predict", 7, 8, R1 + 45)])
+    dplan = synth.fault_plan(len(synth.block_volumes((30, 30, 30), 10)), synth.block_volumes((30, 30, 30), 10),
+                             seed=99, frac=0.3)
+    add("dup_plan_30", S("mixed", (30, 30, 30), seed=5).values, R, 1e-3, {},
+        [("dup_predict" if t % 2 else "dup_reconstruct", b, e, (t % 2) * 64 + 20 + t) for b, e, t in dplan])
     add("override_mix", S("mixed", (20, 15, 10), seed=14).values, A, 1e-3, {"block_edge": 5},
         override={0: 1, 3: 0, 7: 1, 11: 0, 23: 1})
     # c5-style plan at reduced size: 10% of blocks, bits 0..31, three targets
@@ -277,12 +337,33 @@ def main():
     ap.add_argument("--region", action="store_true", help="region-extraction fixtures only")
     ap.add_argument("--campaign", action="store_true", help="fault-campaign fixtures only")
     ap.add_argument("--codec", action="store_true", help="backend codec 1 (run-length) fixtures only")
+    ap.add_argument("--truncation", action="store_true", help="every-byte truncation sweep only")
     args = ap.parse_args()
     os.makedirs(OUT, exist_ok=True)
     mpath = os.path.join(OUT, "manifest.json")
     manifest = json.load(open(mpath)) if os.path.exists(mpath) else {"cases": {}, "corrupt": {}, "large": {}}
     manifest["generator"] = {"numpy": np.__version__, "ftlz": ftlz.__version__,
                              "script": "tools/make_golden.py"}
+    if args.truncation:
+        # test_container.py:59-63: every proper prefix of an archive fails parse with CorruptStream;
+        # the class and message (with its offset) of each cut, for three small archives
+        res = {}
+        for src in ("pipe_sine_13x11x10_e5", "relative_sine_16", "mixed_12x9x7_e4_unprot"):
+            arch = np.load(os.path.join(OUT, src + ".npz"))["archive"].tobytes()
+            errs = []
+            for cut in range(len(arch)):
+                try:
+                    ftlz.parse(arch[:cut])
+                    errs.append(None)
+                except FtlzError as exc:
+                    errs.append([type(exc).__name__, str(exc)])
+            msgs = sorted({tuple(e) for e in errs if e})
+            pos = {m: i for i, m in enumerate(msgs)}
+            res[src] = {"len": len(arch), "messages": [list(m) for m in msgs],
+                        "index": [-1 if e is None else pos[tuple(e)] for e in errs]}
+        json.dump(res, open(os.path.join(OUT, "truncation.json"), "w"), separators=(",", ":"))
+        print("truncation", {k: v["len"] for k, v in res.items()})
+        return
     if args.codec:
         # backend codec 1 (encode.py:287-312) through serialize/parse (container.py:134-145,241-262)
         from ftlz import encode as ENC
