@@ -192,6 +192,10 @@ void ftlz_default_config(ftlz_config* cfg);
 /* Header validation in the reference order (container.py:189-210). Returns FTLZ_OK or
  * FTLZ_ERR_CORRUPT_STREAM with `info` filled. */
 int ftlz_peek_header(const uint8_t* h_data, size_t len, ftlz_header* hdr, ftlz_info* info);
+/* ftlz_peek_header on a whole host archive of `len` bytes, plus the record-table bound: an
+ * archive too short for the block records its header implies fails here with the reference's
+ * CorruptStream kind and offset (container.py:212-218), before anything is sized by its dims. */
+int ftlz_peek_archive(const uint8_t* h_data, size_t len, ftlz_header* hdr, ftlz_info* info);
 /* Number of blocks of the partition (core.py:133-157), or -1 on invalid geometry. */
 int64_t ftlz_block_count(int64_t nx, int64_t ny, int64_t nz, int32_t block_edge);
 

@@ -72,7 +72,7 @@ class StreamInfo(C.Structure):
 
 # every symbol the header declares; tests check the library exports all of them
 EXPORTS = [
-    "ftlz_abi_version", "ftlz_last_error", "ftlz_default_config", "ftlz_peek_header",
+    "ftlz_abi_version", "ftlz_last_error", "ftlz_default_config", "ftlz_peek_header", "ftlz_peek_archive",
     "ftlz_block_count", "ftlz_compress_workspace_size", "ftlz_compress_bound", "ftlz_compress",
     "ftlz_decompress_workspace_size", "ftlz_parse", "ftlz_decompress", "ftlz_ctx_create",
     "ftlz_ctx_destroy", "ftlz_ctx_stream", "ftlz_ctx_compress_device", "ftlz_ctx_compress_host",
@@ -108,6 +108,7 @@ def load():
         L.ftlz_last_error.restype = C.c_char_p
         L.ftlz_default_config.argtypes = [PC]
         L.ftlz_peek_header.argtypes = [vp, sz, PH, C.POINTER(Info)]
+        L.ftlz_peek_archive.argtypes = [vp, sz, PH, C.POINTER(Info)]
         L.ftlz_block_count.argtypes = [i64, i64, i64, i32]
         L.ftlz_block_count.restype = i64
         L.ftlz_compress_workspace_size.argtypes = [i64, i64, i64, PC]

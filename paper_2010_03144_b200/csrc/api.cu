@@ -128,24 +128,6 @@ extern "C" int ftlz_peek_header(const uint8_t* d, size_t len, ftlz_header* h, ft
         if (expect >> 64) over = true;
     }
     if (over || (uint64_t)expect != nb) return fail(FTLZ_K_BLOCK_COUNT, 47, (int64_t)nb);
-    if ((len - 55) / 9 < nb) {
-        // the record table cannot fit (every record takes >= 9 bytes): the archive is truncated
-        // inside it.  Walk the records as container.py:212-218 reads them, so the error (and its
-        // offset) is the reference's, without sizing any buffer by the claimed dims.
-        size_t pos = 55;
-        for (uint64_t b = 0; b < nb; b++) {
-            if (pos + 1 > len) return fail(FTLZ_K_TRUNCATED, (int64_t)pos, FTLZ_F_INDICATOR);
-            const uint8_t ib = d[pos];
-            if (ib > 1) return fail(FTLZ_K_BAD_INDICATOR, (int64_t)pos, ib);
-            pos += 1;
-            if (ib) {
-                if (pos + 16 > len) return fail(FTLZ_K_TRUNCATED, (int64_t)pos, FTLZ_F_COEFFS);
-                pos += 16;
-            }
-            if (pos + 8 > len) return fail(FTLZ_K_TRUNCATED, (int64_t)pos, FTLZ_F_RECORD);
-            pos += 8;
-        }
-    }
     h->version = d[4];
     h->codec_id = d[5];
     h->nx = (int64_t)nx; h->ny = (int64_t)ny; h->nz = (int64_t)nz;
@@ -156,6 +138,35 @@ extern "C" int ftlz_peek_header(const uint8_t* d, size_t len, ftlz_header* h, ft
     h->reserved = 0;
     h->block_count = (int64_t)nb;
     return FTLZ_OK;
+}
+
+// whole archive in host memory: header checks plus the record-table bound.  An archive too short
+// for the record table its dims imply (every record takes >= 9 bytes) is truncated inside the
+// table; the records are walked as container.py:212-218 reads them, so the error and its offset
+// are the reference's, and no buffer is ever sized by the claimed dims of such an archive.
+extern "C" int ftlz_peek_archive(const uint8_t* d, size_t len, ftlz_header* h, ftlz_info* info) {
+    int rc = ftlz_peek_header(d, len, h, info);
+    if (rc) return rc;
+    const uint64_t nb = (uint64_t)h->block_count;
+    if ((len - 55) / 9 >= nb) return FTLZ_OK;
+    auto fail = [&](int kind, size_t off, int64_t a) {
+        info_set(info, FTLZ_ERR_CORRUPT_STREAM, kind, (int64_t)off, -1, a, 0);
+        return FTLZ_ERR_CORRUPT_STREAM;
+    };
+    size_t pos = 55;
+    for (uint64_t b = 0; b < nb; b++) {
+        if (pos + 1 > len) return fail(FTLZ_K_TRUNCATED, pos, FTLZ_F_INDICATOR);
+        const uint8_t ib = d[pos];
+        if (ib > 1) return fail(FTLZ_K_BAD_INDICATOR, pos, ib);
+        pos += 1;
+        if (ib) {
+            if (pos + 16 > len) return fail(FTLZ_K_TRUNCATED, pos, FTLZ_F_COEFFS);
+            pos += 16;
+        }
+        if (pos + 8 > len) return fail(FTLZ_K_TRUNCATED, pos, FTLZ_F_RECORD);
+        pos += 8;
+    }
+    return FTLZ_OK;   // unreachable: the table cannot fit
 }
 
 // ------------------------------------------------------------------------------------------
@@ -217,6 +228,9 @@ static bool build_plan(int64_t nx, int64_t ny, int64_t nz, int e, HostPlan& P) {
         E.nsleaf = (int)P.leaves.size() - E.sleaf_off;
         {
             const int ext[3] = {E.bx, E.by, E.bz};
+            const long long m = 2ll * (std::max(E.bx, std::max(E.by, E.bz)) - 1) * vol;
+            E.exl = 0;
+            while ((1ll << E.exl) < m) E.exl++;
             for (int ax = 0; ax < 3; ax++)
                 E.den[ax] = (double)((long long)vol * ((long long)ext[ax] * ext[ax] - 1)) / 12.0;
         }
@@ -1554,7 +1568,7 @@ static int ctx_upload_archive(ftlz_ctx* c, const uint8_t* h, size_t len, ftlz_he
     report_reset(rep);
     c->parsed_src = nullptr;   // c->arch no longer holds the parsed archive (reuse is keyed on it)
     c->parsed_len = 0;
-    int rc = ftlz_peek_header(h, len, hdr, &rep->info);
+    int rc = ftlz_peek_archive(h, len, hdr, &rep->info);
     if (rc) return set_err(rc, "bad header");
     if ((rc = c->arch.ensure(len + 64))) return rc;
     CK(cudaMemcpyAsync(c->arch.p, h, len, cudaMemcpyHostToDevice, c->stream));

@@ -269,7 +269,7 @@ struct ExtPlan {
     int wave_off;            // vol u16-in-u32 entries: p ordered by plane i+j+k
     int plane_off;           // (bx+by+bz-1) u32 plane start offsets (+1 sentinel)
     int nplanes;
-    int pad;
+    int exl;                 // ceil(log2(2 (max edge - 1) vol)): exact-sum condition of k_prep
     double den[3];           // regression denominators vol * (n^2 - 1) / 12.0 per axis (predict.py:98)
 };
 

@@ -101,6 +101,127 @@ FTLZ_DEV void prep_visit(const float* tile, const PWalk& w, int p, const double*
     t4[3] = __dmul_rn(cv[2 * cvn + w.k], v);
 }
 
+// ---- exact-sum path of the fit ------------------------------------------------------------
+// numpy's pairwise order (predict.py:81-104) only matters when some partial sum rounds.  Every
+// summand c * v (c = idx - (n - 1) / 2, v = float64(x)) is a multiple of G / 2, G = the ulp of
+// the block's smallest nonzero |x|, and every partial sum of any order is bounded by
+// 2 (e - 1) vol max|x|.  When that bound is below 2^52 G (ExtPlan::exl, tested per block on the
+// exponents of max |x| and min nonzero |x|), every partial sum -- numpy's and ours -- is exact,
+// so the four sums can be formed in any order.  Here: lane = row (i, j); per row R = sum_k v,
+// T = sum_k sum_{k' < k} v_k' (so sum_k (k - hz) v = hz R - T), then S(ci v) = sum (i - hx) R,
+// S(cj v) = sum (j - hy) R, S(ck v) = sum (hz R - T); any failing block takes the pairwise path.
+
+FTLZ_DEV void madw(u64& acc, u32 a, u32 b) {   // acc += a * b (one IMAD.WIDE.U32)
+    asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(acc) : "r"(a), "r"(b));
+}
+
+struct ExactAcc {
+    double R, T;
+    u64 W, K;
+    u32 amax, amin;
+};
+
+FTLZ_DEV void exact_point(float x, u32 k, ExactAcc& e, PrepAcc& acc) {
+    const u32 u = __float_as_uint(x);
+    madw(e.W, u, 1u);
+    madw(e.K, u, k);
+    acc.mx = fmaxf(acc.mx, x);
+    acc.mn = fminf(acc.mn, x);
+    const u32 a = u & 0x7fffffffu;
+    e.amax = max(e.amax, a);
+    e.amin = min(e.amin, a - 1u);   // zero -> 0xffffffff: ignored
+    e.T = __dadd_rn(e.T, e.R);
+    e.R = __dadd_rn(e.R, (double)x);
+}
+
+// one 10-float row of a TMA tile whose rows start at z shift ZO (0 or 2): three vector loads
+// (16-byte rows groups of 12-float tile rows fall in distinct bank quads: conflict-free)
+template <int ZO>
+FTLZ_DEV void load_row10(const float* row, float v[10]) {
+    if (ZO == 0) {
+        const float4 a = *(const float4*)row, b = *(const float4*)(row + 4);
+        const float2 c = *(const float2*)(row + 8);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+        v[8] = c.x; v[9] = c.y;
+    } else {
+        const float2 a = *(const float2*)row;
+        const float4 b = *(const float4*)(row + 2), c = *(const float4*)(row + 6);
+        v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = b.z; v[5] = b.w; v[6] = c.x; v[7] = c.y;
+        v[8] = c.z; v[9] = c.w;
+    }
+}
+
+// rows of the block: ZO = 0 / 2 for 10-float rows, -1 generic
+template <int ZO>
+FTLZ_DEV void exact_rows(const float* tile, int rows, int by, int bz, int tye, int tz, int zoff, const FastDiv& fby,
+                         double hx, double hy, double hz, int lane, PrepAcc& acc, double s4[4], u64& cs, u64& csi,
+                         u32& amax, u32& amin) {
+    ExactAcc e;
+    e.amax = 0u;
+    e.amin = 0xffffffffu;
+    for (int r = lane; r < rows; r += 32) {
+        const int i = (int)fdiv((u32)r, fby), j = r - i * by;
+        const float* row = tile + (i * tye + j) * tz + zoff;
+        e.R = 0.0;
+        e.T = 0.0;
+        e.W = 0ull;
+        e.K = 0ull;
+        if (ZO >= 0) {
+            float v[10];
+            load_row10<ZO>(row, v);
+#pragma unroll
+            for (int k = 0; k < 10; k++) exact_point(v[k], (u32)k, e, acc);
+        } else {
+            for (int k = 0; k < bz; k++) exact_point(row[k], (u32)k, e, acc);
+        }
+        s4[0] = __dadd_rn(s4[0], e.R);
+        s4[1] = __dadd_rn(s4[1], __dmul_rn(__dadd_rn(int_to_f64(i), -hx), e.R));
+        s4[2] = __dadd_rn(s4[2], __dmul_rn(__dadd_rn(int_to_f64(j), -hy), e.R));
+        s4[3] = __dadd_rn(s4[3], __dadd_rn(__dmul_rn(hz, e.R), -e.T));
+        cs += e.W;
+        csi += (u64)(u32)(r * bz) * e.W + e.K;
+    }
+    amax = e.amax;
+    amin = e.amin;
+}
+
+// returns true (warp-uniform) when the exact path applies; then sums, cs, csi are final
+FTLZ_DEV bool prep_exact(const float* tile, const ExtPlan& PL, int by, int bz, int tye, int tz, int zoff,
+                         const FastDiv& fby, int lane, PrepAcc& acc, double sums[4], u64& cs, u64& csi) {
+    const int rows = PL.bx * by;
+    const double hx = 0.5 * (double)(PL.bx - 1), hy = 0.5 * (double)(by - 1), hz = 0.5 * (double)(bz - 1);
+    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+    u64 c0 = 0, c1 = 0;
+    u32 amax, amin;
+    if (bz == 10 && (tz & 3) == 0 && zoff == 0)
+        exact_rows<0>(tile, rows, by, bz, tye, tz, zoff, fby, hx, hy, hz, lane, acc, s4, c0, c1, amax, amin);
+    else if (bz == 10 && (tz & 3) == 0 && zoff == 2)
+        exact_rows<2>(tile, rows, by, bz, tye, tz, zoff, fby, hx, hy, hz, lane, acc, s4, c0, c1, amax, amin);
+    else
+        exact_rows<-1>(tile, rows, by, bz, tye, tz, zoff, fby, hx, hy, hz, lane, acc, s4, c0, c1, amax, amin);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        amax = max(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        amin = min(amin, __shfl_xor_sync(0xffffffffu, amin, o));
+    }
+    acc.nan |= (u32)(amax > 0x7f800000u);
+    cs = warp_sum_u64(c0);
+    csi = warp_sum_u64(c1);
+    if (amax >= 0x7f800000u) return false;   // inf / NaN: the pairwise path
+    if (amin != 0xffffffffu) {
+        const int emax = (int)(amax >> 23), emin = max((int)((amin + 1u) >> 23), 1);
+        if (emax - emin + PL.exl > 28) return false;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+        double v = s4[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+        sums[q] = __dadd_rn(0.0, v);   // exact; +0.0 for a zero sum, as numpy's 0.0 + S
+    }
+    return true;
+}
+
 // one tile per warp: the next block's TMA is issued as soon as the current tile is last read,
 // and the freed shared memory buys more resident warps (latency hiding across warps)
 #define PREP_NBUF 1
@@ -171,7 +292,12 @@ __global__ void __launch_bounds__(640, 1) k_prep(const __grid_constant__ CompArg
         acc.cs = 0;
         acc.csi = 0;
         double sums[4];
-        if (vol < 8) {
+        u64 cs, csi;
+        const FastDiv& fby = by == g.e ? A.fd_e : A.fd_ry;
+        const bool exact = prep_exact(tile, PL, by, bz, S.tye, S.tz, zoff, fby, lane, acc, sums, cs, csi);
+        if (exact) {
+            // exact sums, checksum pair and range from the row pass
+        } else if (vol < 8) {
             double r[4] = {0.0, 0.0, 0.0, 0.0};
             if (lane == 0) {
                 PWalk w;
@@ -252,7 +378,10 @@ __global__ void __launch_bounds__(640, 1) k_prep(const __grid_constant__ CompArg
             __syncwarp();
             fold_leaves<4>(leaves, PL.nleaf, leafval, stk, sums, lane);
         }
-        const u64 cs = warp_sum_u64(acc.cs), csi = warp_sum_u64(acc.csi);
+        if (!exact) {   // the pairwise path's visits recomputed the checksum pair
+            cs = warp_sum_u64(acc.cs);
+            csi = warp_sum_u64(acc.csi);
+        }
         // ---- coefficients (batch form, predict.py:90-104): slopes on lanes 1..3, mean on lane 0
         float4 cf;
         {

@@ -234,7 +234,7 @@ def _decompress_bytes(data, faults=None, out=None, reuse=None):
     buf = data if isinstance(data, bytes) else data.ctypes.data
     # the header checks see the whole buffer: an archive too short for its record table is
     # rejected here (reference message and offset) before anything is sized by its dims
-    st = L.ftlz_peek_header(buf, len(data), C.byref(hdr), C.byref(info))
+    st = L.ftlz_peek_archive(buf, len(data), C.byref(hdr), C.byref(info))
     if st != 0:
         raise_for_info(st, info, data)
     shape = (hdr.nx, hdr.ny, hdr.nz)
@@ -282,7 +282,7 @@ def decompress_region(stream: CompressedStream, region, threads: int = 1) -> tup
     out = np.empty((x1 - x0, y1 - y0, z1 - z0), np.float32)
     hdr = _lib.Header()
     info = _lib.Info()
-    st = L.ftlz_peek_header(data, len(data), C.byref(hdr), C.byref(info))
+    st = L.ftlz_peek_archive(data, len(data), C.byref(hdr), C.byref(info))
     if st != 0:
         raise_for_info(st, info, data)
     rb = _report_buf(int(hdr.block_count))
