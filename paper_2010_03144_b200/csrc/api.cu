@@ -19,6 +19,7 @@
 #include "blocks.cu"
 #include "quant_block.cu"
 #include "prep_block.cu"
+#include "quant_reg10.cu"
 #include "encode.cu"
 #include "rle.cu"
 #include "decompress.cu"
@@ -310,6 +311,8 @@ struct KCfg {
     size_t qr_smem;
     int pp_warps, pp_slot, pp_nls, pp_ns;
     size_t pp_smem;
+    int r10_slot, r10_warps;
+    size_t r10_smem;
 };
 
 // TMA tensor map of the input field (dims nz, ny, nx innermost first) with a box of one block
@@ -371,6 +374,10 @@ static KCfg kcfg_comp(const Geom& g) {
         k.pp_warps = (int)std::max<size_t>(1, std::min<size_t>(20, (227 * 1024 - 256) / ps));
         k.pp_smem = ps * k.pp_warps + 128;
     }
+    // k_quant_reg10: 2 TMA tiles, lane histogram (R10_LH + sink rows of 32 u8), mbarriers
+    k.r10_slot = (int)(((size_t)2 * k.stage.tile_bytes + (R10_LH + 1) * 32 + 16 + 127) & ~(size_t)127);
+    k.r10_warps = (int)std::max<size_t>(1, std::min<size_t>(R10_WARPS, (227 * 1024 - 256) / k.r10_slot));
+    k.r10_smem = (size_t)k.r10_slot * k.r10_warps + 128;
     k.lor_slot = al16(4 * v) + 8 * v + al16(2 * v);
     k.lor_warps = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / k.lor_slot));
     k.lor_smem = k.lor_slot * k.lor_warps + 4 * HWIN;
@@ -394,6 +401,10 @@ static int kernel_attrs_once() {
         };
         setmax((const void*)k_prep);
         setmax((const void*)k_quant_reg);
+        setmax((const void*)k_quant_reg10<false, false>);
+        setmax((const void*)k_quant_reg10<false, true>);
+        setmax((const void*)k_quant_reg10<true, false>);
+        setmax((const void*)k_quant_reg10<true, true>);
         setmax((const void*)k_quant_lor);
         setmax((const void*)k_codebook);
         setmax((const void*)k_enc_len);
@@ -429,7 +440,7 @@ struct CompLayout {
     size_t coef, insum, inisum, ind, unpc, bsum, bisum, dcs, bitlen, lanepre, bitoff, regpre, unppre;
     size_t enc, qp, lbbits, lbreg, lbunp;
     size_t cb_keys, cb_syms, cb_w, cb_parent, cb_lens, cb_bm;
-    size_t bins, unp, fix, faults, ffirst, ovr, plan, lor;
+    size_t bins, unp, fix, faults, ffirst, ovr, plan, lor, r10l, regxl;
     size_t cjobs, tarc, tarc_cap, rle, rle_bound;   // codec 1
     size_t total;
 };
@@ -488,6 +499,8 @@ static CompLayout comp_layout(const HostPlan& P, int cap, int64_t n_faults, int 
     L.ffirst = take(n_faults ? 4 * nb : 0);
     L.ovr = take(nb);
     L.lor = take(4 * nb);
+    L.r10l = take(4 * nb);
+    L.regxl = take(4 * nb);
     L.plan = take(P.bytes());
     // codec 1: the identity archive is assembled here, then transcoded (rle.cu)
     L.tarc_cap = codec == 1 ? identity_bound(P, cap) : 0;
@@ -637,8 +650,13 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     CUtensorMap tmap;
     memset(&tmap, 0, sizeof tmap);
     A.stage.use_tma = make_input_map(&tmap, d_in, g, K.stage);
+    // regression blocks with 10-point z rows go to k_quant_reg10 (TMA tiles of 12-float rows)
+    A.r10 = (g.e == 10 && A.stage.use_tma && A.stage.tz == 12) ? 1 : 0;
+    A.r10_slot = K.r10_slot;
     A.lor_slot = (int)K.lor_slot;
     A.lor_list = (u32*)(ws + L.lor);
+    A.r10_list = (u32*)(ws + L.r10l);
+    A.regx_list = (u32*)(ws + L.regxl);
     A.n_faults = (int)nf;
     A.faults = (const ftlz_fault*)(ws + L.faults);
     A.fault_first = (const int*)(ws + L.ffirst);
@@ -689,6 +707,19 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     PF.mark("k_resolve", s);
     k_resolve<<<1, 1, 0, s>>>(A);
     LCHK("k_resolve");
+    PF.mark("k_reglist", s);
+    k_reglist<<<(unsigned)((g.nb + 1023) / 1024), 1024, 0, s>>>(A);
+    LCHK("k_reglist");
+    if (A.r10) {
+        PF.mark("k_quant_reg10", s);
+        const dim3 gr((unsigned)num_sms()), bl(32 * K.r10_warps);
+        const bool dp = A.dup_eval != 0, pn = A.protect_input != 0;
+        if (dp && pn) k_quant_reg10<true, true><<<gr, bl, K.r10_smem, s>>>(A, tmap);
+        else if (dp) k_quant_reg10<true, false><<<gr, bl, K.r10_smem, s>>>(A, tmap);
+        else if (pn) k_quant_reg10<false, true><<<gr, bl, K.r10_smem, s>>>(A, tmap);
+        else k_quant_reg10<false, false><<<gr, bl, K.r10_smem, s>>>(A, tmap);
+        LCHK("k_quant_reg10");
+    }
     PF.mark("k_quant_reg", s);
     {
         k_quant_reg<<<(unsigned)num_sms(), 32 * K.qr_warps, K.qr_smem, s>>>(A, tmap);

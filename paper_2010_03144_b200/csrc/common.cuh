@@ -121,6 +121,11 @@ struct QuantParams {
     int exact_div;
     int pad;
     double twoeb_dup;       // second copy of 2*eb: the duplicated evaluation loads its own operand
+    // float32 decision path (quant_reg10.cu)
+    float rcp32, eb32;      // RN32(1 / (2 eb)), RN32(eb)
+    float band32, sbig;     // guard band around eb (eb32 * 2^-20); |s| >= sbig -> unpredictable
+    int fast32;             // 0: every point takes the reference formulation
+    int pad2;
 };
 
 // floor(t) for t in [0, 2^31): integer extraction from the bit pattern

@@ -34,7 +34,10 @@ struct CompArgs {
     int pp_slot, pp_nls, pp_ns;   // k_prep: smem bytes per warp, leaf / sample slots
     int dbg;                  // debugging switches (FTLZ_DBG)
     int lor_slot;             // smem bytes per warp in k_quant_lor
+    int r10, r10_slot;        // k_quant_reg10 active (edge 10, TMA tiles of 12-float rows); smem per warp
     u32* lor_list;            // Lorenzo blocks (appended by k_prep)
+    u32* r10_list;            // regression blocks for k_quant_reg10 (k_reglist; counters[5] entries)
+    u32* regx_list;           // the other regression blocks, for k_quant_reg (counters[6] entries)
     int n_faults;
     const ftlz_fault* faults;    // device copy
     const int* fault_first;      // nb: first fault index of this block or -1 (faults sorted by block)
@@ -198,6 +201,16 @@ __global__ void k_resolve(CompArgs A) {
     bool normal = tb >= 0x0010000000000000ull && tb < 0x7ff0000000000000ull &&
                   rb >= 0x0010000000000000ull && rb < 0x7ff0000000000000ull;
     Q.exact_div = normal ? 0 : 1;
+    Q.rcp32 = __double2float_rn(Q.rcp);
+    Q.eb32 = __double2float_rn(eb);
+    Q.band32 = Q.eb32 * 9.5367431640625e-07f;   // 2^-20
+    Q.sbig = A.cap > 65536 ? (float)A.cap : 65536.0f;
+    {
+        // both float32 operands well inside the normal range (the error bounds assume it)
+        const float ar = fabsf(Q.rcp32), ae = fabsf(Q.eb32);
+        Q.fast32 = normal && ar >= 7.9e-31f && ar <= 1.2e30f && ae >= 7.9e-31f && ae <= 1.2e30f ? 1 : 0;
+    }
+    Q.pad2 = 0;
     *A.qp = Q;
     A.layout[LAYOUT_EB_BITS] = dbits(eb);
     if (!(eb > 0.0) || !(dbits(eb) < 0x7ff0000000000000ull)) {

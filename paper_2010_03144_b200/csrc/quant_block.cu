@@ -355,13 +355,16 @@ __global__ void __launch_bounds__(QR_WARPS * 32, 1) k_quant_reg(const __grid_con
     const QuantParams Q = *A.qp;
     const bool dup = A.dup_eval != 0, pin = A.protect_input != 0;
     const long long NW = (long long)gridDim.x * nw;
-    auto next_reg = [&](long long b) {
-        for (; b < g.nb; b += NW)
-            if (A.ind[b] == 1 && !(A.events[b] & 4)) return b;
-        return (long long)g.nb;
+    // the regression blocks k_quant_reg10 does not take (regx_list, built by k_reglist)
+    const u32 nlist = A.counters[6];
+    u32 idx = blockIdx.x * nw + warp;
+    auto next_reg = [&](long long) {
+        const long long r = idx < nlist ? (long long)A.regx_list[idx] : (long long)g.nb;
+        idx += (u32)NW;
+        return r;
     };
     u32 lh_load = 0;   // max per-lane count added since the last flush
-    long long b = next_reg((long long)blockIdx.x * nw + warp);
+    long long b = next_reg(0);
     BlockInfo Bnext = block_info(g, b);
     if (b < g.nb) ws.issue(A.x, g, S, &tmap, Bnext, 0, lane);
     int buf = 0;

@@ -75,6 +75,7 @@ def main():
     ap.add_argument("--per", type=float, default=0)
     ap.add_argument("--top", type=int, default=40)
     ap.add_argument("--ops", action="store_true")
+    ap.add_argument("--dump", default=None, help="file:line[-line] -> print its SASS with counts")
     a = ap.parse_args()
     counts = ncu_counts(a.rep, a.kernel)
     base = counts[0][0]
@@ -100,6 +101,13 @@ def main():
           f", {st} stall samples (match {bscore}/200)")
     for line, n in per_line.most_common(a.top):
         print(f"  {line:28s} {n / scale:10.2f} {100.0 * n / tot:5.1f}%  stall {100.0 * per_line_st[line] / max(1, st):5.1f}%")
+    if a.dump:
+        f, rng = a.dump.split(":")
+        lo, hi = (int(x) for x in (rng.split("-") if "-" in rng else (rng, rng)))
+        for addr, op, n, st in counts:
+            line = t.get(addr - base, ("?", op))[0] or "?"
+            if line.startswith(f + ":") and lo <= int(line.split(":")[1]) <= hi:
+                print(f"  {addr - base:6x} {line:22s} {n / scale:8.3f}  {t.get(addr - base, (0, op))[1]}")
     if a.ops:
         print("opcode mix:")
         for op, n in ops.most_common(30):
