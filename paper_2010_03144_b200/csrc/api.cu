@@ -749,9 +749,9 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
                                                 (u64*)(ws + L.lbunp));
         LCHK("k_enc_scan");
         PF.mark("k_enc_pack", s);
-        const int pw = (int)std::max<size_t>(1, std::min<size_t>(16, (227 * 1024 / 2 - 8 * ENC_WIN - PAIR_BYTES) /
-                                                                         (4 * (size_t)g.nvmax8 + 4 * ENC_STG)));
-        k_enc_pack<<<num_sms() * 2, 32 * pw, 8 * ENC_WIN + PAIR_BYTES + (size_t)pw * (4 * (size_t)g.nvmax8 + 4 * ENC_STG), s>>>(
+        const int pw = (int)std::max<size_t>(1, std::min<size_t>(32, (227 * 1024 - 8 * ENC_WIN - C32_BYTES) /
+                                                                         (2 * (size_t)g.nvmax8 + 4 * ENC_STG)));
+        k_enc_pack<<<num_sms(), 32 * pw, 8 * ENC_WIN + C32_BYTES + (size_t)pw * (2 * (size_t)g.nvmax8 + 4 * ENC_STG), s>>>(
             A, (const u32*)(ws + L.fix), (const u8*)(ws + L.fixed));
         LCHK("k_enc_pack");
     }

@@ -83,7 +83,7 @@ struct CompArgs {
 enum {
     LAYOUT_TABLE_LEN = 0, LAYOUT_BOOK_OFF, LAYOUT_NSYM, LAYOUT_PAYLEN_OFF, LAYOUT_PAY_OFF,
     LAYOUT_PAY_BYTES, LAYOUT_UNP_OFF, LAYOUT_NUNP, LAYOUT_SDC_OFF, LAYOUT_TOTAL, LAYOUT_TOTAL_BITS,
-    LAYOUT_MAXLEN, LAYOUT_NREG, LAYOUT_EB_BITS, LAYOUT_COUNT
+    LAYOUT_MAXLEN, LAYOUT_NREG, LAYOUT_EB_BITS, LAYOUT_SYMLO, LAYOUT_SYMHI, LAYOUT_COUNT
 };
 
 // ------------------------------------------------------------------------------------------
@@ -450,15 +450,22 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
             idx += (u32)lencount[l];
         }
     }
+    __shared__ u32 s_symlo, s_symhi;
+    if (tid == 0) { s_symlo = 0xffffffffu; s_symhi = 0u; }
     __syncthreads();
     u64 tot = 0;
+    u32 slo = 0xffffffffu, shi = 0u;
     for (int i = tid; i < n; i += CB_THREADS) {
         int l = (int)(keys[i] >> 16);
         u32 sym = (u32)(keys[i] & 0xffff);
         u64 code = firstcode[l] + (u64)(i - firstidx[l]);
         A.enc[sym] = (code << 6) | (u64)l;
         tot += (u64)A.hist[sym] * (u64)l;
+        if (sym) { slo = min(slo, sym); shi = max(shi, sym); }
     }
+    // range of the nonzero symbols (k_enc_pack's window test)
+    atomicMin(&s_symlo, slo);
+    atomicMax(&s_symhi, shi);
     tot = warp_sum_u64(tot);
     if (tid == 0) s_total = 0;
     __syncthreads();
@@ -488,6 +495,8 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
         A.layout[LAYOUT_TOTAL_BITS] = s_total;
         A.layout[LAYOUT_MAXLEN] = (u64)maxlen;
         A.layout[LAYOUT_NREG] = nreg;
+        A.layout[LAYOUT_SYMLO] = s_symlo;
+        A.layout[LAYOUT_SYMHI] = s_symhi;
         if (total > A.out_cap) dev_fail(A.st, FTLZ_ERR_CAPACITY, 0, -1, -1, (long long)total, 0, 0);
     }
     __syncthreads();

@@ -6,12 +6,15 @@
 //               exclusive warp scan (kept for k_enc_pack) and the block total
 //   k_enc_scan  decoupled look-back scan over blocks of (bits, regression records,
 //               unpredictable words) -> payload bit offset, record offset, unpredictable offset
-//   k_enc_pack  warp per block: each lane packs its range at its absolute bit offset into
-//               big-endian 32-bit words; words shared with a neighbouring lane or block are
-//               merged with atomicOr (k_enc_scan zeroes those words), the rest are stored
+//   k_enc_pack  warp per block, 32 warps per SM: each lane packs its range at its absolute bit
+//               offset into a shared-memory image of the block's big-endian 32-bit words (one
+//               table load, one 64-bit shift-or per symbol, a word store every 32 bits), merged
+//               with its neighbours by shared-memory ORs, then written out coalesced; words shared
+//               with a neighbouring block are merged with atomicOr (k_enc_scan zeroes them)
 //
-// Codes come from a 4096-symbol shared window around the quantizer centre (code << 6 | len),
-// global memory outside it.  Blocks touched by bins-stage faults read their verified 32-bit
+// Codes come from a 4096-symbol shared window around the quantizer centre (code << 6 | len;
+// code << 5 | len for the sequential packer, whose last entry is symbol 0), global memory
+// outside it.  Blocks touched by bins-stage faults read their verified 32-bit
 // words from fix_scratch (k_fault_bins).
 namespace ftlz {
 
@@ -387,68 +390,53 @@ FTLZ_DEV void pack_range_s(const EncWin& W, const u16* sym16, const u32* sym32, 
     if (nacc > 0) put_s(sbase + 4u * widx, (u32)(acc >> 32), false, true);
 }
 
-// symbol pairs around the centre: one shared lookup appends two codes.  Entry (a, c) of the
-// PAIR_W x PAIR_W table is (code_a code_c) << 5 | (len_a + len_c) when both symbols are in the
-// codebook and the pair fits in 27 bits, else 0 (the pair goes through the single-symbol table).
-#define PAIR_W 32
-#define PAIR_BYTES (4 * PAIR_W * PAIR_W)
+#define C32_BYTES ((4 * (ENC_WIN + 1) + 15) & ~15)   // k_enc_pack's code << 5 | len window
 
-FTLZ_DEV void enc_fill_pairs(const CompArgs& A, u32* s_pair) {
-    const int plo = A.center - PAIR_W / 2;
-    for (int t = threadIdx.x; t < PAIR_W * PAIR_W; t += blockDim.x) {
-        const int a = plo + t / PAIR_W, c = plo + t % PAIR_W;
-        const u64 ea = (a >= 0 && a < A.cap) ? A.enc[a] : 0ull, ec = (c >= 0 && c < A.cap) ? A.enc[c] : 0ull;
-        const u32 la = (u32)(ea & 63), lc = (u32)(ec & 63);
-        s_pair[t] = (la && lc && la + lc <= 27u) ? (u32)((((ea >> 6) << lc) | (ec >> 6)) << 5) | (la + lc) : 0u;
-    }
-}
-
-// pack_range_s for codes of at most 32 bits.  Every step appends ONE table entry: the pair
-// (p, p + 1) when the pair table holds it (advance 2), else symbol p alone (advance 1), so the
-// lanes of a warp never diverge on a miss; they only run different step counts.
-FTLZ_DEV void pack_range_s2(const EncWin& W, u32 pair_sa, int plo, const u16* sym16, int p0, int pend, u32 pos,
-                            u32 sbase) {
+// sequential MSB-first packing of symbols [p0, pend) into the warp's staged words, for
+// alphabets whose nonzero symbols all lie in the window (code << 5 | len entries, codes of at
+// most 27 bits; entry ENC_WIN is symbol 0, every other symbol maps into the window): per
+// symbol one table load, a 64-bit shift-or and, every 32 bits, one predicated word store
+// (the lane's first word, shared with the lane before, is merged with a shared-memory OR)
+FTLZ_DEV void pack_range_seq(const u32* s_c32, int wlo, const u16* sym16, int p0, int pend, u32 pos, u32 sbase) {
     u32 widx = pos >> 5;
-    u64 acc = 0;
-    int nacc = (int)(pos & 31);
+    u32 nacc = pos & 31;   // bits of the first word that belong to the lanes before (zero in acc)
+    u64 acc = 0;           // pending bits, right-aligned
     bool first = true;
-    for (int p = p0; p < pend;) {
-        const u32 s0 = sym16[p], s1 = p + 1 < pend ? (u32)sym16[p + 1] : 0xffffffffu;
-        const u32 o0 = s0 - (u32)plo, o1 = s1 - (u32)plo;
-        const bool in = (o0 | o1) < (u32)PAIR_W;
-        u32 pe;
-        asm("ld.shared.u32 %0, [%1];" : "=r"(pe) : "r"(pair_sa + 4u * (in ? o0 * PAIR_W + o1 : 0u)));
-        const bool two = in && pe != 0u;
-        const u64 se = W.get_fast(s0);
-        const u64 code = two ? (u64)(pe >> 5) : se >> 6;
-        const int l = two ? (int)(pe & 31) : (int)(se & 63);
-        p += two ? 2 : 1;
-        acc |= code << (64 - nacc - l);   // l <= 32, nacc < 32
+#pragma unroll 2
+    for (int p = p0; p < pend; p++) {
+        const u32 e = s_c32[min((u32)sym16[p] - (u32)wlo, (u32)ENC_WIN)];
+        const u32 l = e & 31u;
+        acc = (acc << l) | (u64)(e >> 5);
         nacc += l;
-        const bool full = nacc >= 32;
-        put_s(sbase + 4u * widx, (u32)(acc >> 32), full && !first, full && first);
+        const bool full = nacc >= 32u;
+        nacc -= full ? 32u : 0u;
+        put_s(sbase + 4u * widx, (u32)(acc >> nacc), full && !first, full && first);
         first = first && !full;
         widx += full ? 1u : 0u;
-        acc = full ? acc << 32 : acc;
-        nacc -= full ? 32 : 0;
     }
-    if (nacc > 0) put_s(sbase + 4u * widx, (u32)(acc >> 32), false, true);
+    if (nacc > 0u) put_s(sbase + 4u * widx, (u32)(acc << (32u - nacc)), false, true);
 }
 
-__global__ void __launch_bounds__(512) k_enc_pack(CompArgs A, const u32* fix, const u8* fixed_flag) {
+__global__ void __launch_bounds__(1024) k_enc_pack(CompArgs A, const u32* fix, const u8* fixed_flag) {
     extern __shared__ __align__(16) unsigned char smem[];
     if (dev_failed(A.st)) return;
     const Geom& g = A.g;
     u64* s_enc = (u64*)smem;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    u32* s_pair = (u32*)(smem + 8 * ENC_WIN);
-    u16* sym16 = (u16*)(smem + 8 * ENC_WIN + PAIR_BYTES + (size_t)warp * 4 * g.nvmax8);
-    u32* sym32 = (u32*)sym16;
-    u32* stg = (u32*)(smem + 8 * ENC_WIN + PAIR_BYTES + (size_t)nw * 4 * g.nvmax8) + (size_t)warp * ENC_STG;
-    const u32 stg_sa = smem_u32(stg), pair_sa = smem_u32(s_pair);
-    const int plo = A.center - PAIR_W / 2;
+    u32* s_c32 = (u32*)(smem + 8 * ENC_WIN);   // ENC_WIN + 1 entries (code << 5 | len; last: symbol 0)
+    u16* sym16 = (u16*)(smem + 8 * ENC_WIN + C32_BYTES + (size_t)warp * 2 * g.nvmax8);
+    u32* stg = (u32*)(smem + 8 * ENC_WIN + C32_BYTES + (size_t)nw * 2 * g.nvmax8) + (size_t)warp * ENC_STG;
+    const u32 stg_sa = smem_u32(stg);
+    const int wlo = A.center - ENC_WIN / 2;
     enc_fill_window(A, s_enc);
-    enc_fill_pairs(A, s_pair);
+    for (int t = threadIdx.x; t <= ENC_WIN; t += blockDim.x) {
+        const int sy = t == ENC_WIN ? 0 : wlo + t;
+        const u64 e = (sy >= 0 && sy < A.cap) ? A.enc[sy] : 0ull;
+        s_c32[t] = (u32)((e >> 6) << 5) | (u32)(e & 31);
+    }
+    // every nonzero symbol inside the window and codes of at most 26 bits: sequential packer
+    const bool seq = A.layout[LAYOUT_MAXLEN] <= 27 && A.layout[LAYOUT_SYMLO] >= (u64)(wlo > 0 ? wlo : 0) &&
+                     A.layout[LAYOUT_SYMHI] < (u64)(wlo + ENC_WIN) && wlo > 0;
     __syncthreads();
     const EncWin W = {s_enc, A.enc, A.center - ENC_WIN / 2, A.cap};
     u32* words = (u32*)A.out;
@@ -467,10 +455,16 @@ __global__ void __launch_bounds__(512) k_enc_pack(CompArgs A, const u32* fix, co
     for (; b < g.nb; b += NW) {
         const int vol = nvol;
         const bool bad = (A.events[b] & 8) != 0;
-        bool fixed = false;
-        if (!bad) {
+        const bool fixed = !bad && A.n_faults && A.fault_first[b] >= 0 && fixed_flag[b];
+        // bins-faulted blocks pack their verified 32-bit words straight from fix_scratch
+        const u32* sym32 = fix + (size_t)b * g.vmax;
+        if (!bad && !fixed) {
             if (pf) P.store(sym16, lane);
-            else fixed = enc_stage(A, b, vol, fix, fixed_flag, sym16, sym32, lane);
+            else {
+                const int nch = (vol + 7) >> 3;
+                const uint4* src = (const uint4*)(A.bins + bins_index(g, b, 0));
+                for (int c = lane; c < nch; c += 32) ((uint4*)sym16)[c] = __ldg(src + c);
+            }
         }
         __syncwarp();
         const long long bn = b + NW;
@@ -493,8 +487,9 @@ __global__ void __launch_bounds__(512) k_enc_pack(CompArgs A, const u32* fix, co
             const u32 pos = (u32)(gpos - w0 * 32);
             if (p0 < pend) {
                 if (fixed) pack_range_s<true, true>(W, sym16, sym32, p0, pend, pos, stg_sa);
+                else if (seq) pack_range_seq(s_c32, wlo, sym16, p0, pend, pos, stg_sa);
                 else if (longc) pack_range_s<false, true>(W, sym16, sym32, p0, pend, pos, stg_sa);
-                else pack_range_s2(W, pair_sa, plo, sym16, p0, pend, pos, stg_sa);
+                else pack_range_s<false, false>(W, sym16, sym32, p0, pend, pos, stg_sa);
             }
             __syncwarp();
             for (int i = lane; i < (int)nwords; i += 32) {
