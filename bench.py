@@ -286,21 +286,26 @@ def run_ours(args, world, rank, local):
         for _ in range(steps):
             with torch.cuda.stream(stream):
                 flush.zero_()
-            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0, e1, e1b, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(4))
             stream.synchronize()
             e0.record(stream)
             aptr, alen, rb = c_compress(c)
             e1.record(stream)
+            # L2 flushed between the legs too: decompress reads its archive from HBM (the flush
+            # itself is outside both timed legs)
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            e1b.record(stream)
             c_decompress(aptr, alen)
             e2.record(stream)
-            ev.append((e0, e1, e2, alen))
+            ev.append((e0, e1, e1b, e2, alen))
         torch.cuda.synchronize()
         prof = _lib.profile_read(local) if profile else {}
         if profile:
             _lib.profile(False, local)
-        tc = [a.elapsed_time(b) for a, b, _, _ in ev]
-        td = [b.elapsed_time(c2) for _, b, c2, _ in ev]
-        return tc, td, ev[-1][3], prof
+        tc = [a.elapsed_time(b) for a, b, _, _, _ in ev]
+        td = [b2.elapsed_time(c2) for _, _, b2, c2, _ in ev]
+        return tc, td, ev[-1][4], prof
 
     sampler = ClockSampler(local)
     if dist is not None:
@@ -353,8 +358,8 @@ def run_ours(args, world, rank, local):
     dec_k = {k: v for k, v in kern.items() if k not in comp_k}
     dom = max(kern.items(), key=lambda kv: kv[1]["ms_per_step"])[0] if kern else None
     # algorithmic bytes per launch of each kernel: input/archive reads + output writes
-    alg = {"k_prep": 4.0 * N, "k_quant_reg": 4.0 * N, "k_encode": float(S), "k_decode": float(S) + 4.0 * N,
-           "k_recon_warp": 0.0}
+    alg = {"k_prep": 4.0 * N, "k_quant_reg10": 4.0 * N, "k_quant_reg": 4.0 * N, "k_enc_pack": float(S),
+           "k_decode": float(S) + 4.0 * N, "k_recon_warp": 0.0}
     roof = None
     if dom:
         dms = kern[dom]["ms_per_step"]
@@ -473,6 +478,24 @@ def run_ours(args, world, rank, local):
     if rank == 0 and not args.quick and not args.no_c5:
         line["c5"] = run_c5(F, L, _lib, torch, local)
 
+    # the whole-step numbers the verdict is judged on travel inside `roofline` too (the driver
+    # keeps that object): both legs' fractions, the ABFT overheads, the c5 overheads
+    if rank == 0 and line.get("roofline") is not None:
+        rf = line["roofline"]
+        rf.update({"compress_ms": tc_ms, "decompress_ms": td_ms,
+                   "compress_frac": line["compress"]["roofline_frac"],
+                   "decompress_frac": line["decompress"]["roofline_frac"],
+                   "compress_target_ms_at_50pct": Bc / (0.5 * peak * 1e9) * 1e3,
+                   "decompress_target_ms_at_50pct": Bd / (0.5 * peak * 1e9) * 1e3})
+        if "resilience" in line:
+            r = line["resilience"]
+            rf.update({"abft_overhead_compress": r["overhead_compress"],
+                       "abft_overhead_decompress": r["overhead_decompress"],
+                       "abft_overhead_total": r["overhead_total"]})
+        c5 = line.get("c5") or {}
+        if c5:
+            rf["c5_time_overhead"] = {t: c5[t]["time_overhead"] for t in ("input", "bins", "decomp") if t in c5}
+            rf["c5_corrected"] = {t: c5[t]["detected_corrected"] for t in ("input", "bins", "decomp") if t in c5}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:

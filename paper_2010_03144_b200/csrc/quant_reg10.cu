@@ -29,7 +29,7 @@ namespace ftlz {
 #ifndef R10_WARPS
 #define R10_WARPS 12
 #endif
-#define R10_LH 128   // lane-private histogram window (bins center - 64 .. center + 63) + a sink row
+#define R10_LH 256   // lane-private histogram window (bins center - 128 .. center + 127) + a sink row
 
 struct R10Acc {
     u32 bs;        // sum of bins
@@ -40,11 +40,25 @@ struct R10Acc {
     u32 rownz;     // bit t: row lane + 32 t has an unpredictable point
 };
 
-// lane-private u8 counters: bin o of the window at byte o * 32 + lane; bins outside the window
-// land in the sink row R10_LH, recounted by a rescan when a lane's sink is nonzero
-FTLZ_DEV void lh_add(unsigned char* lhl, u32 o, u32 delta) {   // o <= R10_LH; delta 1 or 0xff.. (-1)
-    lhl[o * 32] += (unsigned char)delta;
-}
+// lane-private u8 counters: bin o of the window at byte o * 32 + lane.  A bin outside the window
+// only bumps the lane's sink counter (row R10_LH): no branch in the point loop; a row whose
+// sink count moved is recounted afterwards into the CTA's shared window (hwin, HWIN_REG bins) or,
+// beyond it, the global histogram.
+struct R10Hist {
+    unsigned char* lhw;   // this lane's column of the u8 window
+    u32* hwin;            // CTA window
+    u64* ghist;
+    int lhlo, wlo;
+    // count `delta` (+1 / -1) for bin b (slow paths: fix-up, tail, undo)
+    FTLZ_DEV void add(u32 b, int delta) const {
+        const u32 o = b - (u32)lhlo;
+        if (o < (u32)R10_LH) lhw[o * 32] += (unsigned char)delta;
+        else reg_hist_out(hwin, ghist, wlo, (int)b, delta);
+    }
+    // hot path: window counter, or the sink for an out-of-window bin (recounted per row)
+    FTLZ_DEV void bump(u32 b) const { lhw[min(b - (u32)lhlo, (u32)R10_LH) * 32] += 1; }
+    FTLZ_DEV u32 sink() const { return lhw[R10_LH * 32]; }
+};
 
 FTLZ_DEV void lh_flush10(unsigned char* lh, u64* ghist, int lhlo, int cap, int lane) {
     __syncwarp();
@@ -68,7 +82,7 @@ FTLZ_DEV void lh_flush10(unsigned char* lh, u64* ghist, int lhlo, int cap, int l
 // one point of the fast path (see the file header); accumulates into the row sums
 template <bool DUP, bool PIN>
 FTLZ_DEV u32 r10_point(const QuantParams& Q, float x, int k, float kf, double kd, double ab, double ab2, double b3,
-                       double b3d, float b3r, float abr, float erow, u32 cbin, unsigned char* lhw, float& emax,
+                       double b3d, float b3r, float abr, float erow, u32 cbin, const R10Hist& H, float& emax,
                        float& amin, u32& macc, bool& nzf, u32& bsr, u32& kbr, u32& rbits, u64& kxr) {
     // float32 estimate of S and its distance to the nearest half-integer
     const float c = __fmaf_rn(b3r, kf, abr);
@@ -100,7 +114,7 @@ FTLZ_DEV u32 r10_point(const QuantParams& Q, float x, int k, float kf, double kd
     kbr += (u32)k * b;
     rbits = __float_as_uint(r32);
     if (PIN) kxr += (u64)(u32)k * (u64)__float_as_uint(x);
-    lh_add(lhw, min(b - (u32)(Q.center - R10_LH / 2), (u32)R10_LH), 1u);
+    H.bump(b);
     return b;
 }
 
@@ -109,7 +123,7 @@ FTLZ_DEV u32 r10_point(const QuantParams& Q, float x, int k, float kf, double kd
 // (bit 0: some point needs the exact formulation, bit 1: some point is unpredictable)
 template <bool DUP, bool PIN>
 FTLZ_DEV u32 r10_row(const QuantParams& Q, const float* row, double ab, double ab2, double b3, double b3d,
-                     float b3r, int p0, u16* gbins, unsigned char* lhw, R10Acc& acc) {
+                     float b3r, int p0, u16* gbins, const R10Hist& H, R10Acc& acc) {
     const float abr = __double2float_rn(__dmul_rn(ab, (double)Q.rcp32));
     const float erow = __fmaf_rn(9.0f, fabsf(b3r), fabsf(abr)) * 9.5367431640625e-07f + 9.094947017729282e-13f;
     const u32 cbin = (u32)Q.center - 0x4B400000u;   // bits(m) + cbin = center + RN(s)
@@ -118,16 +132,17 @@ FTLZ_DEV u32 r10_row(const QuantParams& Q, const float* row, double ab, double a
     bool nzf = false;
     u64 dcr = 0, csr = 0, kxr = 0;
     u32* gw = (u32*)(gbins + p0);   // p0 = 10 r: 4-byte aligned
+    const u32 sink0 = H.sink();
     float kf = 0.0f;
     double kd = 0.0;
 #pragma unroll 1
     for (int k = 0; k < 10; k += 2) {
         const float2 x2 = *(const float2*)(row + k);   // row start is 8-byte aligned (zoff 0 or 2)
         u32 r0, r1;
-        const u32 b0 = r10_point<DUP, PIN>(Q, x2.x, k, kf, kd, ab, ab2, b3, b3d, b3r, abr, erow, cbin, lhw, emax,
+        const u32 b0 = r10_point<DUP, PIN>(Q, x2.x, k, kf, kd, ab, ab2, b3, b3d, b3r, abr, erow, cbin, H, emax,
                                            amin, macc, nzf, bsr, kbr, r0, kxr);
         const u32 b1 = r10_point<DUP, PIN>(Q, x2.y, k + 1, __fadd_rn(kf, 1.0f), __dadd_rn(kd, 1.0), ab, ab2, b3, b3d,
-                                           b3r, abr, erow, cbin, lhw, emax, amin, macc, nzf, bsr, kbr, r1, kxr);
+                                           b3r, abr, erow, cbin, H, emax, amin, macc, nzf, bsr, kbr, r1, kxr);
         gw[k >> 1] = b0 | (b1 << 16);
         // 64-bit sums of word pairs: one three-input add with carries per pair
         dcr += (u64)r0 + (u64)r1;
@@ -141,6 +156,14 @@ FTLZ_DEV u32 r10_row(const QuantParams& Q, const float* row, double ab, double a
     if (PIN) {
         acc.cs += csr;
         acc.csi += (u64)(u32)p0 * csr + kxr;
+    }
+    if (H.sink() != sink0) {
+        // out-of-window bins of this row: move them from the sink to the CTA / global counts
+        H.lhw[R10_LH * 32] = (unsigned char)sink0;
+        for (int k = 0; k < 10; k++) {
+            const u32 bb = gbins[p0 + k];
+            if (bb - (u32)H.lhlo >= (u32)R10_LH) reg_hist_out(H.hwin, H.ghist, H.wlo, (int)bb, 1);
+        }
     }
     const bool fl = emax >= 0.49999905f || amin <= Q.band32 || macc != 0u;
     return (fl ? 1u : 0u) | (nzf ? 2u : 0u);
@@ -160,7 +183,7 @@ FTLZ_DEV u64 warp_sum_u64_redux(u64 v) {
 template <bool DUP>
 FTLZ_DEV void r10_fixup(const CompArgs& A, long long b, bool hasdup, const QuantParams& Q, const float* tile, int tye,
                         int tz, int zoff, int rows, const FastDiv& fby, int by, const float4& cf, const float4& cg,
-                        u16* gbins, unsigned char* lhw, int lhlo, int lane, R10Acc& acc, bool& mism) {
+                        u16* gbins, const R10Hist& H, int lane, R10Acc& acc, bool& mism) {
     const float b3r = __double2float_rn(__dmul_rn((double)cf.w, (double)Q.rcp32));
     for (int t = 0, r = lane; r < rows; t++, r += 32) {
         if (!((acc.rowflag >> t) & 1u)) continue;
@@ -225,10 +248,9 @@ FTLZ_DEV void r10_fixup(const CompArgs& A, long long b, bool hasdup, const Quant
             acc.bis += (u64)(u32)p * (u64)ex - (u64)(u32)p * (u64)fb;
             acc.dc += (u64)__float_as_uint(rx) - (u64)__float_as_uint(rf);
             if (ex == 0u) acc.rownz |= 1u << t;
-            // lane window: drop the fast bin, count the exact one (sink row: out of window)
-            const u32 of = fb - (u32)lhlo, ox = ex - (u32)lhlo;
-            lh_add(lhw, min(of, (u32)R10_LH), 0xffffffffu);
-            lh_add(lhw, min(ox, (u32)R10_LH), 1u);
+            // drop the fast bin's count, count the exact bin
+            H.add(fb, -1);
+            H.add(ex, 1);
         }
     }
 }
@@ -238,7 +260,7 @@ FTLZ_DEV void r10_fixup(const CompArgs& A, long long b, bool hasdup, const Quant
 template <bool DUP, bool PIN>
 FTLZ_DEV void r10_tail_point(const CompArgs& A, long long b, bool hasdup, const QuantParams& Q, const float* tile,
                              int tye, int tz, int zoff, int p, int by, const float4& cf, const float4& cg,
-                             u16* gbins, unsigned char* lhw, R10Acc& acc, bool& mism) {
+                             u16* gbins, const R10Hist& H, R10Acc& acc, bool& mism) {
     const int rr = p / 10, k = p - rr * 10, i = rr / by, j = rr - i * by;
     const float x = tile[(i * tye + j) * tz + zoff + k];
     const double di = int_to_f64(i), dj = int_to_f64(j), dk = int_to_f64(k);
@@ -270,7 +292,7 @@ FTLZ_DEV void r10_tail_point(const CompArgs& A, long long b, bool hasdup, const 
         acc.cs += (u64)u;
         acc.csi += (u64)(u32)p * (u64)u;
     }
-    lh_add(lhw, min(bin - (u32)(Q.center - R10_LH / 2), (u32)R10_LH), 1u);
+    H.add(bin, 1);
 }
 
 // compaction of the regression blocks after k_prep: 10-point-row blocks for k_quant_reg10
@@ -330,10 +352,11 @@ __global__ void __maxnreg__(R10_MAXREG) k_quant_reg10(const __grid_constant__ Co
     ws.tbytes = S.tile_bytes;
     unsigned char* lh = slot + 2 * S.tile_bytes;   // (R10_LH + 1) x 32 u8 counters
     ws.bar = (u64*)(lh + (R10_LH + 1) * 32);
-    const int lhlo = A.center - R10_LH / 2;
+    u32* hwin = (u32*)(smem + (size_t)nw * A.r10_slot);
+    const int lhlo = A.center - R10_LH / 2, wlo = A.center - HWIN_REG / 2;
     for (int t = lane; t < (R10_LH + 1) * 8; t += 32) ((u32*)lh)[t] = 0;
-    unsigned char* lhw = lh + lane;
-    unsigned char* sink = lhw + R10_LH * 32;
+    for (int t = threadIdx.x; t < HWIN_REG; t += blockDim.x) hwin[t] = 0;
+    const R10Hist H = {lh + lane, hwin, A.hist, lhlo, wlo};
     ws.init(lane);
     __syncthreads();
 
@@ -392,31 +415,20 @@ __global__ void __maxnreg__(R10_MAXREG) k_quant_reg10(const __grid_constant__ Co
                                                    __dmul_rn((double)cg.z, dj))
                                        : ab;
                 const float* row = tile + (i * S.tye + j) * S.tz + zoff;
-                const u32 rf = r10_row<DUP, PIN>(Q, row, ab, ab2, b3, b3d, b3r, r * 10, gbins, lhw, acc);
+                const u32 rf = r10_row<DUP, PIN>(Q, row, ab, ab2, b3, b3d, b3r, r * 10, gbins, H, acc);
                 acc.rowflag |= (rf & 1u) << t;
                 acc.rownz |= rf >> 1;
             }
             for (int p = nfull * 10 + lane; p < vol; p += 32)
-                r10_tail_point<DUP, PIN>(A, b, hasdup, Q, tile, S.tye, S.tz, zoff, p, by, cf, cg, gbins, lhw, acc, mism);
+                r10_tail_point<DUP, PIN>(A, b, hasdup, Q, tile, S.tye, S.tz, zoff, p, by, cf, cg, gbins, H, acc, mism);
             if (hasdup) acc.rowflag = ~0u;
             if (!Q.fast32) acc.rowflag = ~0u;
             if (__any_sync(0xffffffffu, acc.rowflag != 0)) {
                 __syncwarp();
                 if (acc.rowflag)
-                    r10_fixup<DUP>(A, b, hasdup, Q, tile, S.tye, S.tz, zoff, nfull, fby, by, cf, cg, gbins, lhw, lhlo,
+                    r10_fixup<DUP>(A, b, hasdup, Q, tile, S.tye, S.tz, zoff, nfull, fby, by, cf, cg, gbins, H,
                                    lane, acc, mism);
                 __syncwarp();
-            }
-            // out-of-window bins of this lane's points (counted in its sink): global atomics
-            __syncwarp();
-            if (__any_sync(0xffffffffu, *sink != 0)) {
-                if (*sink != 0) {
-                    lane_points([&](int p) {
-                        const u32 bb = gbins[p];
-                        if (bb - (u32)lhlo >= (u32)R10_LH) atomicAdd(&A.hist[bb], 1ull);
-                    });
-                    *sink = 0;
-                }
             }
             if (!PIN || pass == 1) break;
             // stage (c) verification of the tile against the stage (a) pair (pipeline.py:331-361)
@@ -424,12 +436,7 @@ __global__ void __maxnreg__(R10_MAXREG) k_quant_reg10(const __grid_constant__ Co
             if (cs == A.insum[b] && csi == A.inisum[b]) break;
             // undo this pass's histogram counts, correct the tile, run again
             __syncwarp();
-            lane_points([&](int p) {
-                const u32 bb = gbins[p];
-                const u32 o = bb - (u32)lhlo;
-                if (o < (u32)R10_LH) lh_add(lhw, o, 0xffffffffu);
-                else atomicAdd(&A.hist[bb], ~0ull);   // -1
-            });
+            lane_points([&](int p) { H.add(gbins[p], -1); });
             const int rr = tile_correct(tile, w0, vol, A.insum[b], A.inisum[b], lane);
             if (lane == 0) {
                 atomicAdd(&A.counters[3], 1u);
@@ -478,6 +485,12 @@ __global__ void __maxnreg__(R10_MAXREG) k_quant_reg10(const __grid_constant__ Co
         b = bnx;
     }
     lh_flush10(lh, A.hist, lhlo, A.cap, lane);
+    __syncthreads();
+    for (int t = threadIdx.x; t < HWIN_REG; t += blockDim.x) {
+        const u32 v = hwin[t];
+        const int sy = wlo + t;
+        if (v && sy >= 0 && sy < A.cap) atomicAdd(&A.hist[sy], (u64)v);
+    }
 }
 
 }  // namespace ftlz
