@@ -412,9 +412,9 @@ static int kernel_attrs_once() {
         setmax((const void*)k_parse_tail);
         setmax((const void*)k_decode<false, false>);
         setmax((const void*)k_decode<false, true>);
-        setmax((const void*)k_decode<true, true>);
         setmax((const void*)k_recon_g<32>);
         setmax((const void*)k_recon_g<128>);
+        setmax((const void*)k_redecode);
         if (cudaGetLastError() != cudaSuccess) rc = FTLZ_ERR_CUDA;
     });
     return rc;
@@ -868,7 +868,7 @@ struct DecLayout {
     size_t maps, smaps, sentry;
     size_t ind, recoff, unpc, bitlen, bofs, uofs, da, db, lor, mis;
     size_t lut, first, lcount, lbase, dsym, sortkeys, lba, lbb;
-    size_t bins, faults, ffirst, plan, rlist;
+    size_t bins, faults, ffirst, fblk, verdict, ckpt, plan, rlist;
     size_t jobs, payscr, sdcscr, rle;   // codec 1
     size_t pay_cap, sdc_cap, rle_bound;
     size_t total;
@@ -917,6 +917,9 @@ static DecLayout dec_layout(const HostPlan& P, size_t len, int cap, int64_t nf, 
     L.bins = take(2 * ((nb + 31) / 32) * 32 * (size_t)g.nvmax8 + 64);
     L.faults = take(sizeof(ftlz_fault) * (size_t)std::max<int64_t>(1, nf));
     L.ffirst = take(nf ? 4 * nb : 0);
+    L.fblk = take(4 * (size_t)std::max<int64_t>(1, nf));   // distinct faulted blocks
+    L.verdict = take(nb);                                   // re-execution verdicts, list order
+    L.ckpt = take(4 * RD_NCK * nb);                         // row checkpoints of the first decode
     L.plan = take(P.bytes());
     L.rlist = take(4 * nb);
     const size_t N = (size_t)g.nx * (size_t)g.ny * (size_t)g.nz;
@@ -977,6 +980,7 @@ static DecArgs make_dec_args(const HostPlan& P, const DevPlan& D, const DecLayou
     A.n_faults = (int)nf;
     A.faults = (const ftlz_fault*)(ws + L.faults);
     A.fault_first = (const int*)(ws + L.ffirst);
+    A.ckpt = (u32*)(ws + L.ckpt);
     A.plans = D.ep; A.coords = D.coords; A.wave = D.wave; A.planes = D.planes; A.wcrd = D.wcrd;
     A.maps = (u32*)(ws + L.maps); A.smaps = (u32*)(ws + L.smaps); A.sentry = (u64*)(ws + L.sentry);
     A.nchunks = L.nchunks; A.nsuper = L.nsuper;
@@ -1052,10 +1056,15 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     CK(cudaMemsetAsync(ws + L.result + 64 + 4 * DC_MINFAIL, 0xff, 4, s));
     std::vector<ftlz_fault> fs;
     std::vector<int> ff;
+    std::vector<u32> fblk;   // distinct blocks with decompressed-data faults
     if (nf) {
         prep_faults(faults, nf, g.nb, fs, ff);
+        for (const ftlz_fault& f : fs)
+            if (f.target == FTLZ_FAULT_DECOMP && (fblk.empty() || fblk.back() != (u32)f.block)) fblk.push_back((u32)f.block);
         CK(cudaMemcpyAsync(ws + L.faults, fs.data(), sizeof(ftlz_fault) * nf, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(ws + L.ffirst, ff.data(), 4 * (size_t)g.nb, cudaMemcpyHostToDevice, s));
+        if (!fblk.empty())
+            CK(cudaMemcpyAsync(ws + L.fblk, fblk.data(), 4 * fblk.size(), cudaMemcpyHostToDevice, s));
     }
     DecArgs A = make_dec_args(P, D, L, d_a, len, h, d_out, nf, ws);
     int sms = num_sms();
@@ -1093,7 +1102,8 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     if (decode) {
         // slabs: whole block layers (block ids are layer-major), so each slab's output is one
         // contiguous range of x-planes
-        const int nslab = dl && dl->h_out ? std::max(1, std::min<int>(dl->nslab, (int)g.cx)) : 1;
+        // faulted runs decode in one slab: k_decomp_faults edits the output before it goes down
+        const int nslab = dl && dl->h_out && fblk.empty() ? std::max(1, std::min<int>(dl->nslab, (int)g.cx)) : 1;
         const long long layer = g.cy * g.cz, plane = g.ny * g.nz;
         for (int si = 0; si < nslab; si++) {
             const long long l0 = g.cx * si / nslab, l1 = g.cx * (si + 1) / nslab;
@@ -1101,9 +1111,13 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
             A.sb1 = l1 * layer;
             const unsigned dgrid = (unsigned)((A.sb1 - A.sb0 + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32));
             PF.mark("k_decode", s);
-            if (A.n_faults) k_decode<true, true><<<dgrid, DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
-            else k_decode<false, true><<<dgrid, DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
+            k_decode<false, true><<<dgrid, DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
             LCHK("k_decode");
+            if (!fblk.empty()) {
+                k_decomp_faults<<<(unsigned)((fblk.size() + 7) / 8), 256, 0, s>>>(A, (const u32*)(ws + L.fblk),
+                                                                                   (int)fblk.size());
+                LCHK("k_decomp_faults");
+            }
             PF.mark("k_recon_warp", s);
             // a CTA per Lorenzo block when a wavefront plane exceeds a warp (10^3 blocks: up to
             // 75 points), else a warp per block (1 x e x e planes: e points) without CTA barriers
@@ -1178,29 +1192,38 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     u32 nmis = R.counters[DC_NMIS];
     std::vector<int64_t> reexec;
     if (nmis) {
-        // re-execution of every mismatching block (pipeline.py:713-723), no fault replay
-        std::vector<u32> mis(nmis);
-        CK(cudaMemcpyAsync(mis.data(), ws + L.mis, 4 * (size_t)nmis, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        std::sort(mis.begin(), mis.end());
-        CK(cudaMemcpyAsync(ws + L.mis, mis.data(), 4 * (size_t)nmis, cudaMemcpyHostToDevice, s));
+        // re-execution of every mismatching block (pipeline.py:713-723), no fault replay; the list
+        // stays on the device in arrival order (blocks are independent), only the verdicts and
+        // the ids come back
         A.n_faults = 0;
-        k_decode<false, true><<<(unsigned)((nmis + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32)), DEC_WARPS * 32, dec_smem, s>>>(
-            A, (const u32*)(ws + L.mis), (int)nmis);
+        PF.mark("k_reexec_decode", s);
+        {
+            const size_t rsm = ((size_t)4 << DEC_TBITS) + (size_t)RD_WARPS * RD_MAXW * 4;
+            k_redecode<<<(nmis + RD_WARPS - 1) / RD_WARPS, RD_WARPS * 32, rsm, s>>>(A, (const u32*)(ws + L.mis),
+                                                                                  (int)nmis);
+        }
+        A.list_spread = 0;
         LCHK("k_decode");
+        PF.mark("k_reexec_recon", s);
         k_recon_g<32><<<(unsigned)std::min<u32>((nmis + rw - 1) / rw, sms * 4), rw * 32, rslot * rw, s>>>(A, 1);
         LCHK("k_recon");
-        CK(cudaGetLastError());
-        std::vector<unsigned char> mf((size_t)g.nb);
-        CK(cudaMemcpyAsync(mf.data(), ws + L.mflag, (size_t)g.nb, cudaMemcpyDeviceToHost, s));
+        PF.mark("k_reexec_verdict", s);
+        k_reexec_verdict<<<(nmis + 255) / 256, 256, 0, s>>>(A, ws + L.verdict, nmis);
+        LCHK("k_reexec_verdict");
+        std::vector<u32> mis(nmis);
+        std::vector<unsigned char> vd(nmis);
+        CK(cudaMemcpyAsync(mis.data(), ws + L.mis, 4 * (size_t)nmis, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(vd.data(), ws + L.verdict, (size_t)nmis, cudaMemcpyDeviceToHost, s));
+        PF.mark("", s);
         CK(cudaStreamSynchronize(s));
+        PF.collect();
         // verification walks extent groups in sorted order, ids ascending (pipeline.py:692-708)
-        std::vector<std::pair<std::tuple<int, int, int>, int64_t>> order;
-        for (u32 b : mis) order.push_back({block_extent(P, b), (int64_t)b});
+        std::vector<std::tuple<std::tuple<int, int, int>, int64_t, unsigned char>> order;
+        for (u32 t = 0; t < nmis; t++) order.push_back({block_extent(P, mis[t]), (int64_t)mis[t], vd[t]});
         std::sort(order.begin(), order.end());
         for (auto& o : order) {
-            int64_t b = o.second;
-            if (mf[b] == 2) reexec.push_back(b);
+            const int64_t b = std::get<1>(o);
+            if (std::get<2>(o) == 2) reexec.push_back(b);
             else {
                 rep->sdc = 1;
                 info_set(&rep->info, FTLZ_OK, FTLZ_K_D_MISMATCH, -1, b, 0, 0);

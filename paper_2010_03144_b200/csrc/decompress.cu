@@ -82,7 +82,8 @@ struct DecArgs {
     u64 pay_cap, sdc_cap;
     // region extraction (pipeline.py:726-795): output window in field coordinates
     int region;               // 1: k_decode list mode reports failures like the full path
-    int pad_r;
+    int list_spread;          // list mode: one block per warp (short lists: latency over lane use)
+    u32* ckpt;                // full path: bit offset (in the block) of every RD_SEG-th row start, RD_NCK per block
     long long rx0, ry0, rz0, rnx, rny, rnz;
     const u32* region_list;   // the intersecting blocks, ascending
     u32 n_region;
@@ -770,6 +771,8 @@ FTLZ_DEV bool fr_symbol(FastReader& R, u32 lut_sa, int lsh, const u32* dsym, u32
 }
 
 #define DF_PENDING 0xffu   // dflag: failed on the fast path, kind not yet classified
+#define RD_SEG 10   // rows per re-decode segment
+#define RD_NCK 9    // row checkpoints kept per block (segments 1..9 of 10)
 
 FTLZ_DEV float4 load_coef(const u8* a, u64 rec) {
     const u8* p = a + rec + 1;
@@ -828,9 +831,12 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
     bool valid;
     const bool mode_list = list != nullptr;
     if (mode_list) {
-        // re-execution: lane over the given block list, decode only (bins to scratch)
-        long long idx = ((long long)blockIdx.x * DEC_WARPS + warp) * 32 + lane;
-        valid = idx < (long long)nlist;
+        // re-execution: lane over the given block list, decode only (bins to scratch); a short
+        // list spreads one block per warp (each block's decode is a serial chain: more warps,
+        // shorter wall time, and no other lane's rows to write back)
+        const long long wid = (long long)blockIdx.x * DEC_WARPS + warp;
+        long long idx = A.list_spread ? wid : wid * 32 + lane;
+        valid = idx < (long long)nlist && (!A.list_spread || lane == 0);
         b = valid ? (long long)list[idx] : 0;
     } else {
         b = A.sb0 + ((long long)blockIdx.x * DEC_WARPS + warp) * 32 + lane;
@@ -926,6 +932,11 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
     int i = 0, j = 0;
     for (int r = 0; r < e * e; r++) {
         const bool act = valid && !err && i < B.bx && j < B.by;
+        if (FAST && act && !mode_list && A.ckpt) {
+            // row checkpoints for a parallel re-decode (k_redecode): every RD_SEG-th row start
+            const int rr = i * B.by + j;
+            if (rr && rr % RD_SEG == 0 && rr / RD_SEG <= RD_NCK) A.ckpt[(size_t)b * RD_NCK + rr / RD_SEG - 1] = consumed;
+        }
         if (act) {
             // every lane stages one word per point: the reconstructed float (regression blocks
             // of the full path) or the bin (Lorenzo blocks, re-execution)
@@ -1250,6 +1261,135 @@ __global__ void __launch_bounds__(128) k_recon_g(DecArgs A, int mode) {
         }
         gsync();
     }
+}
+
+// ------------------------------------------------------------------------------------------
+// STAGE_DECOMP_BEFORE_VERIFY faults on regression blocks (pipeline.py:690, armed once): the
+// fault-free decoder has already written and verified the block; flip the injected bits in the
+// output, re-verify the block against its stored sum_dc (pipeline.py:692-707) and, on a
+// mismatch, queue it for re-execution like the decoder would have.  Lorenzo blocks receive their
+// faults inside k_recon_g (mode 0).  Warp per faulted block (fblk: distinct block ids).
+__global__ void k_decomp_faults(DecArgs A, const u32* fblk, int nfb) {
+    const Geom& g = A.g;
+    const int lane = threadIdx.x & 31;
+    const int w = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (w >= nfb) return;
+    const long long b = fblk[w];
+    if (A.ind[b] != 1 || A.dflag[b] != 0) return;
+    const BlockInfo B = block_info(g, b);
+    const long long base = ((B.bi * g.e) * g.ny + B.bj * g.e) * g.nz + B.bk * g.e;
+    const int byz = B.by * B.bz;
+    auto addr = [&](int p) {
+        const int i = p / byz, rem = p - i * byz, j = rem / B.bz, k = rem - j * B.bz;
+        return base + ((long long)i * g.ny + j) * g.nz + k;
+    };
+    if (lane == 0)
+        for (int f = A.fault_first[b]; f >= 0 && f < A.n_faults && A.faults[f].block == b; f++)
+            if (A.faults[f].target == FTLZ_FAULT_DECOMP) {
+                float* o = A.out + addr((int)A.faults[f].element);
+                *o = __uint_as_float(__float_as_uint(*o) ^ (1u << A.faults[f].bit));
+            }
+    __syncwarp();
+    if (!A.info[DI_HAS_SDC]) return;
+    u64 sum = 0;
+    for (int p = lane; p < B.vol; p += 32) sum += (u64)__float_as_uint(A.out[addr(p)]);
+    sum = warp_sum_u64(sum);
+    if (lane == 0 && sum != stored_sum_dc(A, b) && A.mflag[b] != 1) {
+        A.mflag[b] = 1;
+        A.mis_list[atomicAdd(&A.counters[DC_NMIS], 1u)] = (u32)b;
+    }
+}
+
+// Re-decode of one block per warp for re-execution (pipeline.py:713-723): the warp copies the
+// block's bit slice from the archive into shared memory with coalesced loads, then one lane
+// decodes it from there (the serial Huffman chain without global-memory latency) and writes
+// the bins to scratch for k_recon_g (mode 1).  The first pass decoded the same bytes without
+// error, so a failure here (impossible for an intact archive) is reported as a mismatch.
+#define RD_WARPS 4
+#define RD_MAXW 2048   // slice words staged per warp (a block of <= 1150 points at 57 bits)
+__global__ void __launch_bounds__(RD_WARPS * 32) k_redecode(DecArgs A, const u32* list, int n) {
+    extern __shared__ __align__(16) unsigned char rsm[];
+    u32* s_lut = (u32*)rsm;
+    u32* slice_all = s_lut + (1 << DEC_TBITS);
+    const Geom& g = A.g;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int T = (int)A.info[DI_T], maxlen = (int)A.info[DI_MAXLEN];
+    for (int x = tid; x < (1 << T); x += blockDim.x) s_lut[x] = A.lut[x];
+    if (tid < 64) { s_dec_first[tid] = A.first_code[tid]; s_dec_count[tid] = A.lcount[tid]; s_dec_base[tid] = A.lbase[tid]; }
+    __syncthreads();
+    const int w = blockIdx.x * RD_WARPS + warp;
+    if (w >= n) return;
+    const long long b = list[w];
+    const BlockInfo B = block_info(g, b);
+    const u32 bl = A.bitlen[b];
+    const u64 start = pay_boff(A) * 8 + A.bofs[b];
+    const u64 w0 = start >> 5;
+    const u32 nwords = (u32)(((start + bl + 31) >> 5) - w0) + 2;   // + 2: the 64-bit window's tail
+    u32* sl = slice_all + (size_t)warp * RD_MAXW;
+    if (nwords > RD_MAXW) {
+        if (lane == 0) A.mflag[b] = 3;
+        return;
+    }
+    const u64 bufw = ((A.codec ? A.pay_cap : A.len) + 3) >> 2;
+    const u32* src = (const u32*)pay_base(A);
+    for (u32 i = lane; i < nwords; i += 32) {
+        const u64 wi = w0 + i;
+        sl[i] = wi < bufw ? __byte_perm(__ldg(src + wi), 0, 0x0123) : 0u;   // big-endian words
+    }
+    __syncwarp();
+    // segments of RD_SEG rows decoded in parallel from the checkpoints of the first pass (lane
+    // s: rows [s RD_SEG, (s + 1) RD_SEG)); each must end exactly where the next begins
+    const int rows = B.bx * B.by;
+    int nseg = A.ckpt ? min((rows + RD_SEG - 1) / RD_SEG, RD_NCK + 1) : 1;
+    if (nseg > 1 && nseg * RD_SEG < rows) nseg = 1;   // more rows than checkpoints cover
+    const u32 base = (u32)(start & 31);
+    u32 sb = 0, se = bl;
+    if (lane < nseg) {
+        if (lane > 0) sb = A.ckpt[(size_t)b * RD_NCK + lane - 1];
+        if (lane < nseg - 1) se = A.ckpt[(size_t)b * RD_NCK + lane];
+    }
+    const int p_lo = lane * RD_SEG * B.bz, p_hi = nseg == 1 ? B.vol : min((lane + 1) * RD_SEG * B.bz, B.vol);
+    u32 pos = base + sb, zeros = 0;
+    const u32 end = base + se;
+    bool bad = sb > se || se > bl;
+    if (lane < nseg && !bad) {
+        for (int p = p_lo; p < p_hi; p++) {
+            const u32 wi = pos >> 5, sh = pos & 31;
+            const u64 hi = ((u64)sl[wi] << 32) | sl[wi + 1];
+            const u64 win = sh ? (hi << sh) | ((u64)sl[wi + 2] >> (32 - sh)) : hi;
+            const u32 ent = s_lut[(u32)(win >> (64 - T))];
+            u32 sym = 0, l;
+            if (ent) {
+                l = ent & 63;
+                sym = ent >> 8;
+            } else {
+                l = 0;
+                for (int t = T + 1; t <= maxlen; t++) {
+                    const u64 d = (win >> (64 - t)) - s_dec_first[t];
+                    if (d < (u64)s_dec_count[t]) {
+                        l = (u32)t;
+                        sym = A.dsym[s_dec_base[t] + d];
+                        break;
+                    }
+                }
+                if (!l) { bad = true; break; }
+            }
+            pos += l;
+            if (pos > end) { bad = true; break; }
+            zeros += sym == 0u;
+            A.bins[bins_index(g, b, p)] = (u16)sym;
+        }
+        bad |= pos != end;
+    }
+    const bool anybad = __any_sync(0xffffffffu, lane < nseg && bad);
+    const u32 ztot = __reduce_add_sync(0xffffffffu, lane < nseg ? zeros : 0u);
+    if (lane == 0 && (anybad || ztot != A.unpc[b])) A.mflag[b] = 3;
+}
+
+// verdicts of the re-executed blocks, in list order (2: matches after re-execution, else 3)
+__global__ void k_reexec_verdict(DecArgs A, u8* verdict, u32 n) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) verdict[i] = A.mflag[A.mis_list[i]];
 }
 
 }  // namespace ftlz
