@@ -368,7 +368,7 @@ static KCfg kcfg_comp(const Geom& g) {
         k.pp_nls = (int)(v / 64 + 8);
         k.pp_ns = (int)(v / 8 + 8);
         size_t ps = PREP_NBUF * (size_t)k.stage.tile_bytes +
-                    8 * (3 * (size_t)g.e + 4 * PREP_STK + 4 * (size_t)k.pp_nls + 2 * (size_t)k.pp_ns) + 16;
+                    8 * (6 * (size_t)g.e + 4 * PREP_STK + 4 * (size_t)k.pp_nls + 2 * (size_t)k.pp_ns) + 16;
         ps = (ps + 127) & ~(size_t)127;
         k.pp_slot = (int)ps;
         k.pp_warps = (int)std::max<size_t>(1, std::min<size_t>(20, (227 * 1024 - 256) / ps));

@@ -202,6 +202,14 @@ FTLZ_DEV unsigned warp_sum_u32(unsigned v) {
     return v;
 }
 
+// u64 warp sum through three 22-bit limbs and REDUX (each limb sum < 2^27)
+FTLZ_DEV u64 warp_sum_u64_redux(u64 v) {
+    const u32 l0 = (u32)v & 0x3fffffu, l1 = (u32)(v >> 22) & 0x3fffffu, l2 = (u32)(v >> 44);
+    const u64 s0 = __reduce_add_sync(0xffffffffu, l0), s1 = __reduce_add_sync(0xffffffffu, l1),
+              s2 = __reduce_add_sync(0xffffffffu, l2);
+    return s0 + (s1 << 22) + (s2 << 44);
+}
+
 // ------------------------------------------------------------------------------------------
 // geometry (core.py:113-157)
 struct Geom {

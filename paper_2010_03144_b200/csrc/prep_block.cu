@@ -199,26 +199,28 @@ FTLZ_DEV bool prep_exact(const float* tile, const ExtPlan& PL, int by, int bz, i
         exact_rows<2>(tile, rows, by, bz, tye, tz, zoff, fby, hx, hy, hz, lane, acc, s4, c0, c1, amax, amin);
     else
         exact_rows<-1>(tile, rows, by, bz, tye, tz, zoff, fby, hx, hy, hz, lane, acc, s4, c0, c1, amax, amin);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        amax = max(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-        amin = min(amin, __shfl_xor_sync(0xffffffffu, amin, o));
-    }
+    amax = __reduce_max_sync(0xffffffffu, amax);
+    amin = __reduce_min_sync(0xffffffffu, amin);
     acc.nan |= (u32)(amax > 0x7f800000u);
-    cs = warp_sum_u64(c0);
-    csi = warp_sum_u64(c1);
+    cs = warp_sum_u64_redux(c0);
+    csi = warp_sum_u64_redux(c1);
     if (amax >= 0x7f800000u) return false;   // inf / NaN: the pairwise path
     if (amin != 0xffffffffu) {
         const int emax = (int)(amax >> 23), emin = max((int)((amin + 1u) >> 23), 1);
         if (emax - emin + PL.exl > 28) return false;
     }
+    // butterfly: lane bits 4, 3 select which of the four sums a lane keeps (exact: any order)
+    const bool h4 = lane & 16, h3 = lane & 8;
+    double k0 = h4 ? s4[2] : s4[0], k1 = h4 ? s4[3] : s4[1];
+    k0 = __dadd_rn(k0, __shfl_xor_sync(0xffffffffu, h4 ? s4[0] : s4[2], 16));
+    k1 = __dadd_rn(k1, __shfl_xor_sync(0xffffffffu, h4 ? s4[1] : s4[3], 16));
+    double v = __dadd_rn(h3 ? k1 : k0, __shfl_xor_sync(0xffffffffu, h3 ? k0 : k1, 8));
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
-        double v = s4[q];
+    for (int o = 4; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    v = __dadd_rn(0.0, v);   // exact; +0.0 for a zero sum, as numpy's 0.0 + S
+    // sum q lives in lanes 8 q .. 8 q + 7 (q = 2 bit4 + bit3)
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
-        sums[q] = __dadd_rn(0.0, v);   // exact; +0.0 for a zero sum, as numpy's 0.0 + S
-    }
+    for (int q = 0; q < 4; q++) sums[q] = __shfl_sync(0xffffffffu, v, 8 * q);
     return true;
 }
 
@@ -243,7 +245,8 @@ __global__ void __launch_bounds__(640, 1) k_prep(const __grid_constant__ CompArg
     double* leafval = stk + 4 * PREP_STK;              // nls x 4
     double* ar = leafval + 4 * A.pp_nls;               // samples
     double* al = ar + A.pp_ns;
-    ws.bar = (u64*)(al + A.pp_ns);
+    double* ptab = al + A.pp_ns;                       // b1 i, b2 j, b3 k (3 e entries)
+    ws.bar = (u64*)(ptab + 3 * cvn);
     __shared__ u32 omx, omn, cta_nan, cta_nreg;
     if (threadIdx.x == 0) { omx = 0; omn = 0xffffffffu; cta_nan = 0; cta_nreg = 0; }
     ws.init(lane);
@@ -385,16 +388,22 @@ __global__ void __launch_bounds__(640, 1) k_prep(const __grid_constant__ CompArg
         // ---- coefficients (batch form, predict.py:90-104): slopes on lanes 1..3, mean on lane 0
         float4 cf;
         {
-            double sl = 0.0, corr = 0.0;
+            // lane 0: mean = S(v) / vol; lanes 1..3: slope = S(c v) / den, one division for all four
+            double sl = 0.0, corr = 0.0, out0 = 0.0;
             const int ax = lane - 1;
-            if (lane >= 1 && lane <= 3) {
-                const int e = ax == 0 ? bx : (ax == 1 ? by : bz);
-                if (e != 1) {
-                    sl = __ddiv_rn(sums[ax + 1], PL.den[ax]);
-                    corr = __dmul_rn(__dmul_rn(sl, (double)(e - 1)), 0.5);   // x / 2.0 == x * 0.5 exactly
+            if (lane <= 3) {
+                const double num = lane == 0 ? sums[0] : (lane == 1 ? sums[1] : (lane == 2 ? sums[2] : sums[3]));
+                const double den = lane == 0 ? (double)vol : PL.den[ax];
+                const double qd = __ddiv_rn(num, den);
+                if (lane == 0) out0 = qd;
+                else {
+                    const int e = ax == 0 ? bx : (ax == 1 ? by : bz);
+                    if (e != 1) {
+                        sl = qd;
+                        corr = __dmul_rn(__dmul_rn(sl, (double)(e - 1)), 0.5);   // x / 2.0 == x * 0.5 exactly
+                    }
                 }
             }
-            double out0 = lane == 0 ? __ddiv_rn(sums[0], (double)vol) : 0.0;
             const double s1 = __shfl_sync(0xffffffffu, sl, 1), s2 = __shfl_sync(0xffffffffu, sl, 2),
                          s3 = __shfl_sync(0xffffffffu, sl, 3);
             const double k1 = __shfl_sync(0xffffffffu, corr, 1), k2 = __shfl_sync(0xffffffffu, corr, 2),
@@ -432,15 +441,22 @@ __global__ void __launch_bounds__(640, 1) k_prep(const __grid_constant__ CompArg
         if (!bad) {
             // ---- sampled selection (predict.py:196-231): samples at p = 8, 16, ...
             const int ns = PL.ns;
-            const double c0 = (double)cf.x, c1 = (double)cf.y, c2 = (double)cf.z, c3 = (double)cf.w;
+            const double c0 = (double)cf.x;
+            // b1 i, b2 j, b3 k for the block's coordinates (predict.py:196-231 evaluates
+            // ((b0 + b1 i) + b2 j) + b3 k with these same float64 products)
+            for (int u = lane; u < 3 * cvn; u += 32) {
+                const int ax = u / cvn, t = u - ax * cvn;
+                const float cw = ax == 0 ? cf.y : (ax == 1 ? cf.z : cf.w);
+                ptab[u] = __dmul_rn((double)cw, int_to_f64(t));
+            }
+            __syncwarp();
             const int sr = S.tz, sp = S.tye * S.tz;   // tile offsets of (j-1) and (i-1)
             for (int q = lane; q < ns; q += 32) {
                 PWalk w;
                 w.set_crd(__ldg(crd + 8 * (q + 1)), S.tye, S.tz, zoff);
                 const int i = w.i, j = w.j, k = w.k, ad = w.t;
                 const double v = (double)tile[ad];
-                const double pr = __dadd_rn(__dadd_rn(__dadd_rn(c0, __dmul_rn(c1, int_to_f64(i))), __dmul_rn(c2, int_to_f64(j))),
-                                            __dmul_rn(c3, int_to_f64(k)));
+                const double pr = __dadd_rn(__dadd_rn(__dadd_rn(c0, ptab[i]), ptab[cvn + j]), ptab[2 * cvn + k]);
                 const double d100 = i > 0 ? (double)tile[ad - sp] : 0.0;
                 const double d010 = j > 0 ? (double)tile[ad - sr] : 0.0;
                 const double d001 = k > 0 ? (double)tile[ad - 1] : 0.0;
@@ -468,6 +484,29 @@ __global__ void __launch_bounds__(640, 1) k_prep(const __grid_constant__ CompArg
                 }
                 e2[0] = __shfl_sync(0xffffffffu, r0, 0);
                 e2[1] = __shfl_sync(0xffffffffu, r1, 0);
+            } else if (PL.nsleaf == 1) {
+                // one pairwise leaf (ns <= 128): lanes 0-7 carry the eight chains of e_reg, lanes
+                // 8-15 those of e_lor; ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7)) by
+                // shuffles, the tail in order, then 0.0 + S
+                const int j8 = lane & 7;
+                const double* src = lane < 8 ? ar : al;
+                const int len8 = ns - (ns & 7);
+                double r = 0.0;
+                if (lane < 16) {
+                    r = src[j8];
+                    for (int p = j8 + 8; p < len8; p += 8) r = __dadd_rn(r, src[p]);
+                }
+#pragma unroll
+                for (int o = 1; o < 8; o <<= 1) {
+                    const double other = __shfl_xor_sync(0xffffffffu, r, o);
+                    r = (j8 & o) ? __dadd_rn(other, r) : __dadd_rn(r, other);
+                }
+                if (lane == 0 || lane == 8) {
+                    for (int p = len8; p < ns; p++) r = __dadd_rn(r, src[p]);
+                    r = __dadd_rn(0.0, r);
+                }
+                e2[0] = __shfl_sync(0xffffffffu, r, 0);
+                e2[1] = __shfl_sync(0xffffffffu, r, 8);
             } else {
                 const Leaf* sl = A.leaves + PL.sleaf_off;
                 const int nchains = PL.nsleaf * 8;
