@@ -7,7 +7,7 @@
 set -e
 cd "$(dirname "$0")/.."
 TAG=${1:-r1}
-PAT=${2:-"k_quant_reg|k_prep|k_enc_pack|k_decode|k_codebook|k_enc_len"}
+PAT=${2:-"k_quant_reg10|k_prep|k_enc_pack|k_decode|k_codebook|k_enc_len"}
 CMD="python bench.py --steps 1 --warmup 3 --quick --no-c5"
 timeout 300 $CMD > gpurun_out/${TAG}_plain.json 2> gpurun_out/${TAG}_plain.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
