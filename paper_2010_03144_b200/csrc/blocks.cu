@@ -9,6 +9,14 @@ FTLZ_DEV void cp_async4(void* smem, const void* gmem) {
     unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem));
 }
+FTLZ_DEV void cp_async8(void* smem, const void* gmem) {
+    unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem));
+}
+FTLZ_DEV void cp_async16(void* smem, const void* gmem) {
+    unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem));
+}
 FTLZ_DEV void cp_async_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 FTLZ_DEV void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }

@@ -1,6 +1,6 @@
 // quant_reg10.cu -- stage (c) of pipeline.compress for regression blocks whose z rows hold 10
 // points (the default block edge; pipeline.py:390-453, quantize.py:37-52, duplicated
-// evaluation pipeline.py:157-179), one lane per (i, j) row.
+// evaluation pipeline.py:157-179), one lane per pair of consecutive points of a z row.
 //
 // Decision in float32, reconstruction in float64.  The bin of a point is RN(S) with
 // S = (x - p) / (2 eb) unless S lies at a half-integer (quantize.py: floor(|h| + 0.5) with the
@@ -19,25 +19,34 @@
 // also applies injected STAGE_DUP_EVAL faults.
 //
 // Layout: warp-autonomous persistent CTAs, each warp streams its regression blocks through
-// two TMA tiles (tma.cuh); lane l takes rows l, l + 32, ... of the block.  A row's ten floats
-// arrive in three vector loads (12-float tile rows: conflict-free), its bins leave as five
-// 32-bit stores straight into the encoder's bins array.  Histogram: lane-private u8 counters
-// for the 64 bins around the centre (flushed every few blocks), out-of-window bins counted by
-// a rescan of the lane's rows.
+// two TMA tiles (tma.cuh); row r's ten points form pairs 5 r .. 5 r + 4 and lane l
+// takes pairs l, l + 32, ... (500 pairs on a 10^3 block: 98% of the lane slots busy, against 78%
+// for one lane per row).  The per-row terms (row prediction, its float32 scaled copy) are built
+// once per block in shared memory (r10_rowtab).  A pair's two floats arrive in one 8-byte load,
+// its bins leave as one 32-bit store straight into the encoder's bins array.  Histogram:
+// lane-private u8 counters for the 128 bins around the centre (flushed every few blocks),
+// out-of-window bins counted by a rescan of the lane's pairs.
 namespace ftlz {
 
 #ifndef R10_WARPS
 #define R10_WARPS 12
 #endif
-#define R10_LH 256   // lane-private histogram window (bins center - 128 .. center + 127) + a sink row
+#define R10_LH 128   // lane-private histogram window (bins center - 64 .. center + 63) + a sink row
+#define R10_ROWS 100 // rows of a block (edge 10)
 
 struct R10Acc {
     u32 bs;        // sum of bins
-    u64 bis;       // sum of p * bin
+    u32 bis;       // sum of p * bin (a lane's <= 34 points of a block: < 2^32)
     u64 dc;        // sum of recon32 words
     u64 cs, csi;   // input checksum pair
-    u32 rowflag;   // bit t: row lane + 32 t has a flagged point
-    u32 rownz;     // bit t: row lane + 32 t has an unpredictable point
+    float emax;    // the lane's largest distance bound to a half-integer
+    float amin;    // the lane's smallest | |x - recon32| - eb |
+    u32 macc;      // OR of the duplicated evaluation's bit differences
+    bool nz;       // some point of the lane is unpredictable
+    FTLZ_DEV void reset() {
+        bs = 0; bis = 0; dc = 0; cs = 0; csi = 0;
+        emax = 0.0f; amin = INFINITY; macc = 0; nz = false;
+    }
 };
 
 // lane-private u8 counters: bin o of the window at byte o * 32 + lane.  A bin outside the window
@@ -49,13 +58,13 @@ struct R10Hist {
     u32* hwin;            // CTA window
     u64* ghist;
     int lhlo, wlo;
-    // count `delta` (+1 / -1) for bin b (slow paths: fix-up, tail, undo)
+    // count `delta` (+1 / -1) for bin b (slow paths: fix-up, recount, undo)
     FTLZ_DEV void add(u32 b, int delta) const {
         const u32 o = b - (u32)lhlo;
         if (o < (u32)R10_LH) lhw[o * 32] += (unsigned char)delta;
         else reg_hist_out(hwin, ghist, wlo, (int)b, delta);
     }
-    // hot path: window counter, or the sink for an out-of-window bin (recounted per row)
+    // hot path: window counter, or the sink for an out-of-window bin (recounted per block)
     FTLZ_DEV void bump(u32 b) const { lhw[min(b - (u32)lhlo, (u32)R10_LH) * 32] += 1; }
     FTLZ_DEV u32 sink() const { return lhw[R10_LH * 32]; }
 };
@@ -79,212 +88,139 @@ FTLZ_DEV void lh_flush10(unsigned char* lh, u64* ghist, int lhlo, int cap, int l
     __syncwarp();
 }
 
-// one point of the fast path (see the file header); accumulates into the row sums
-template <bool DUP, bool PIN>
-FTLZ_DEV u32 r10_point(const QuantParams& Q, float x, int k, float kf, double kd, double ab, double ab2, double b3,
-                       double b3d, float b3r, float abr, float erow, u32 cbin, const R10Hist& H, float& emax,
-                       float& amin, u32& macc, bool& nzf, u32& bsr, u32& kbr, u32& rbits, u64& kxr) {
+// per-row terms of a block, built once per block in the warp's shared-memory slot: the row
+// prediction ((b0 + b1 i) + b2 j) (and its duplicate from the independently loaded
+// coefficients), its float32 scaled copy and guard width, the row's tile offset
+struct R10Row {
+    double ab, ab2;
+    float abr, erow;
+    u32 toff;
+    int ij;   // i << 16 | j
+};
+
+// a block's global operands, staged one block ahead (k_quant_reg10)
+struct R10Pre {
+    float4 cf, cg;    // coefficients; the duplicate's own copy
+    u64 ins, inis;    // stage (a) checksum pair
+    u32 nxt, pad[3];  // list entry after the next block (~0: none)
+};
+
+// one point of the fast path (see the file header): k is the lane's constant z offset, so
+// ck = b3 k (and its duplicate ckd = b3' k) are per-lane constants; returns the bin (0:
+// unpredictable) and the recon32 word, folds the flag terms into the lane's accumulators
+template <bool DUP>
+FTLZ_DEV u32 r10_point(const QuantParams& Q, float x, float kf, double ck, double ckd, const R10Row& R, float b3r,
+                       u32 cbin, const R10Hist& H, R10Acc& acc, u32& rbits) {
     // float32 estimate of S and its distance to the nearest half-integer
-    const float c = __fmaf_rn(b3r, kf, abr);
+    const float c = __fmaf_rn(b3r, kf, R.abr);
     const float s = __fmaf_rn(x, Q.rcp32, -c);
     const float m = __fadd_rn(s, 12582912.0f);   // 1.5 * 2^23: low mantissa bits = RN(s)
     const float f = __fadd_rn(s, -__fadd_rn(m, -12582912.0f));
     const bool big = !(fabsf(s) < Q.sbig);
-    emax = fmaxf(emax, big ? 0.0f : __fadd_rn(fabsf(f), __fmaf_rn(fabsf(s), 4.76837158203125e-07f, erow)));
+    acc.emax = fmaxf(acc.emax, big ? 0.0f : __fadd_rn(fabsf(f), __fmaf_rn(fabsf(s), 4.76837158203125e-07f, R.erow)));
     const u32 bin = __float_as_uint(m) + cbin;
     const bool ok = !big && (bin - 1u) < (u32)(Q.cap - 1);
     // float64 reconstruction in the reference order
-    const double offs = __int2double_rn((int)(bin - (u32)Q.center));
-    const double p1 = __dadd_rn(ab, __dmul_rn(b3, kd));
+    const double offs = __int2double_rn((int)(__float_as_uint(m) - 0x4B400000u));
+    const double p1 = __dadd_rn(R.ab, ck);
     const double d1 = __dadd_rn(p1, __dmul_rn(Q.twoeb, offs));
     if (DUP) {
-        const double p2 = __dadd_rn(ab2, __dmul_rn(b3d, kd));
+        const double p2 = __dadd_rn(R.ab2, ckd);
         const double d2 = __dadd_rn(p2, __dmul_rn(Q.twoeb_dup, offs));
         const u64 xp = dbits(p1) ^ dbits(p2), xd = dbits(d1) ^ dbits(d2);
-        macc |= (u32)xp | (u32)(xp >> 32) | (u32)xd | (u32)(xd >> 32);
+        acc.macc |= (u32)xp | (u32)(xp >> 32) | (u32)xd | (u32)(xd >> 32);
     }
     const float d32 = __double2float_rn(d1);
     const float a = __fadd_rn(fabsf(__fadd_rn(x, -d32)), -Q.eb32);
-    amin = fminf(amin, ok ? fabsf(a) : INFINITY);
+    acc.amin = fminf(acc.amin, ok ? fabsf(a) : INFINITY);
     const bool keep = ok && a <= 0.0f;
+    acc.nz |= !keep;
+    rbits = __float_as_uint(keep ? d32 : x);
     const u32 b = keep ? bin : 0u;
-    const float r32 = keep ? d32 : x;
-    nzf |= !keep;
-    bsr += b;
-    kbr += (u32)k * b;
-    rbits = __float_as_uint(r32);
-    if (PIN) kxr += (u64)(u32)k * (u64)__float_as_uint(x);
     H.bump(b);
     return b;
 }
 
-// one row (i, j) of a regression block: 10 points as 5 pairs (two points in flight keep the
-// register footprint small enough for more resident warps); returns the row's flag bits
-// (bit 0: some point needs the exact formulation, bit 1: some point is unpredictable)
-template <bool DUP, bool PIN>
-FTLZ_DEV u32 r10_row(const QuantParams& Q, const float* row, double ab, double ab2, double b3, double b3d,
-                     float b3r, int p0, u16* gbins, const R10Hist& H, R10Acc& acc) {
-    const float abr = __double2float_rn(__dmul_rn(ab, (double)Q.rcp32));
-    const float erow = __fmaf_rn(9.0f, fabsf(b3r), fabsf(abr)) * 9.5367431640625e-07f + 9.094947017729282e-13f;
-    const u32 cbin = (u32)Q.center - 0x4B400000u;   // bits(m) + cbin = center + RN(s)
-    float emax = 0.0f, amin = INFINITY;
-    u32 macc = 0, bsr = 0, kbr = 0;
-    bool nzf = false;
-    u64 dcr = 0, csr = 0, kxr = 0;
-    u32* gw = (u32*)(gbins + p0);   // p0 = 10 r: 4-byte aligned
-    const u32 sink0 = H.sink();
-    float kf = 0.0f;
-    double kd = 0.0;
-#pragma unroll 1
-    for (int k = 0; k < 10; k += 2) {
-        const float2 x2 = *(const float2*)(row + k);   // row start is 8-byte aligned (zoff 0 or 2)
-        u32 r0, r1;
-        const u32 b0 = r10_point<DUP, PIN>(Q, x2.x, k, kf, kd, ab, ab2, b3, b3d, b3r, abr, erow, cbin, H, emax,
-                                           amin, macc, nzf, bsr, kbr, r0, kxr);
-        const u32 b1 = r10_point<DUP, PIN>(Q, x2.y, k + 1, __fadd_rn(kf, 1.0f), __dadd_rn(kd, 1.0), ab, ab2, b3, b3d,
-                                           b3r, abr, erow, cbin, H, emax, amin, macc, nzf, bsr, kbr, r1, kxr);
-        gw[k >> 1] = b0 | (b1 << 16);
-        // 64-bit sums of word pairs: one three-input add with carries per pair
-        dcr += (u64)r0 + (u64)r1;
-        if (PIN) csr += (u64)__float_as_uint(x2.x) + (u64)__float_as_uint(x2.y);
-        kf = __fadd_rn(kf, 2.0f);
-        kd = __dadd_rn(kd, 2.0);
-    }
-    acc.bs += bsr;
-    acc.bis += (u64)(u32)p0 * (u64)bsr + (u64)kbr;
-    acc.dc += dcr;
-    if (PIN) {
-        acc.cs += csr;
-        acc.csi += (u64)(u32)p0 * csr + kxr;
-    }
-    if (H.sink() != sink0) {
-        // out-of-window bins of this row: move them from the sink to the CTA / global counts
-        H.lhw[R10_LH * 32] = (unsigned char)sink0;
-        for (int k = 0; k < 10; k++) {
-            const u32 bb = gbins[p0 + k];
-            if (bb - (u32)H.lhlo >= (u32)R10_LH) reg_hist_out(H.hwin, H.ghist, H.wlo, (int)bb, 1);
-        }
-    }
-    const bool fl = emax >= 0.49999905f || amin <= Q.band32 || macc != 0u;
-    return (fl ? 1u : 0u) | (nzf ? 2u : 0u);
-}
-
-// exact recomputation of the flagged rows of this lane (reference formulation, blocks.cu
-// quant_point): replaces the fast results of every point whose fast evaluation was flagged,
-// or that carries an injected duplicated-evaluation fault
+// exact recomputation of one point (reference formulation, blocks.cu quant_point) when its fast
+// evaluation is flagged or it carries an injected duplicated-evaluation fault: replaces the
+// fast results (bin, sums, histogram)
 template <bool DUP>
-FTLZ_DEV void r10_fixup(const CompArgs& A, long long b, bool hasdup, const QuantParams& Q, const float* tile, int tye,
-                        int tz, int zoff, int rows, const FastDiv& fby, int by, const float4& cf, const float4& cg,
-                        u16* gbins, const R10Hist& H, int lane, R10Acc& acc, bool& mism) {
-    const float b3r = __double2float_rn(__dmul_rn((double)cf.w, (double)Q.rcp32));
-    for (int t = 0, r = lane; r < rows; t++, r += 32) {
-        if (!((acc.rowflag >> t) & 1u)) continue;
-        const int i = (int)fdiv((u32)r, fby), j = r - i * by;
-        const float* row = tile + (i * tye + j) * tz + zoff;
-        const double di = int_to_f64(i), dj = int_to_f64(j);
-        const double ab = __dadd_rn(__dadd_rn((double)cf.x, __dmul_rn((double)cf.y, di)), __dmul_rn((double)cf.z, dj));
-        const double ab2 = DUP ? __dadd_rn(__dadd_rn((double)cg.x, __dmul_rn((double)cg.y, di)), __dmul_rn((double)cg.z, dj)) : ab;
-        const float abr = __double2float_rn(__dmul_rn(ab, (double)Q.rcp32));
-        const float erow = __fmaf_rn(9.0f, fabsf(b3r), fabsf(abr)) * 9.5367431640625e-07f + 9.094947017729282e-13f;
-        for (int k = 0; k < 10; k++) {
-            const int p = r * 10 + k;
-            const float x = row[k];
-            const double kd = int_to_f64(k);
-            const double ckk = __dmul_rn((double)cf.w, kd), ck2k = DUP ? __dmul_rn((double)cg.w, kd) : ckk;
-            // the fast path's result for this point (recomputed: same operations)
-            const float c = __fmaf_rn(b3r, (float)k, abr);
-            const float s = __fmaf_rn(x, Q.rcp32, -c);
-            const float m = __fadd_rn(s, 12582912.0f);
-            const float rr = __fadd_rn(m, -12582912.0f);
-            const float f = __fadd_rn(s, -rr);
-            const float dl = __fmaf_rn(fabsf(s), 4.76837158203125e-07f, erow);
-            const bool big = !(fabsf(s) < Q.sbig);
-            const int qi = (int)__float_as_uint(m) - 0x4B400000;
-            const bool edge = !big && __fadd_rn(fabsf(f), dl) >= 0.49999905f;
-            const u32 bin = (u32)(Q.center + qi);
-            const bool ok = !big && (bin - 1u) < (u32)(Q.cap - 1);
-            const double offs = int_to_f64(qi);
-            const double p1 = __dadd_rn(ab, ckk);
-            const double d1 = __dadd_rn(p1, __dmul_rn(Q.twoeb, offs));
-            bool mis = false;
-            if (DUP) {
-                const double p2 = __dadd_rn(ab2, ck2k);
-                const double d2 = __dadd_rn(p2, __dmul_rn(Q.twoeb_dup, offs));
-                mis = dbits(p1) != dbits(p2) || dbits(d1) != dbits(d2);
-            }
-            const float d32 = __double2float_rn(d1);
-            const float a = __fadd_rn(fabsf(__fadd_rn(x, -d32)), -Q.eb32);
-            const bool unsure = ok && fabsf(a) <= Q.band32;
-            const bool keep = ok && a <= 0.0f;
-            const u32 fb = keep ? bin : 0u;
-            const float rf = keep ? d32 : x;
-            DupMask M;
-            const bool fp = hasdup && dup_masks(A, b, p, M);
-            if (!(edge || unsure || mis || fp)) continue;
-            if (!fp) {
-#pragma unroll
-                for (int q = 0; q < 3; q++) M.p[q] = M.r[q] = 0ull;
-            }
-            float rx;
-            double back;
-            const u32 ex = (u32)quant_point(
-                Q, x, p1, DUP, [&] { return __dadd_rn(opaque(ab2), opaque(ck2k)); },
-                [&] {
-                    return __dadd_rn(__dadd_rn(__dadd_rn((double)cf.x, __dmul_rn((double)cf.y, di)),
-                                               __dmul_rn((double)cf.z, dj)),
-                                     __dmul_rn(opaque((double)cf.w), int_to_f64(k)));
-                },
-                M, &rx, &mism, &back);
-            gbins[p] = (u16)ex;
-            acc.bs += ex - fb;
-            acc.bis += (u64)(u32)p * (u64)ex - (u64)(u32)p * (u64)fb;
-            acc.dc += (u64)__float_as_uint(rx) - (u64)__float_as_uint(rf);
-            if (ex == 0u) acc.rownz |= 1u << t;
-            // drop the fast bin's count, count the exact bin
-            H.add(fb, -1);
-            H.add(ex, 1);
-        }
+FTLZ_DEV void r10_fix_point(const CompArgs& A, long long b, bool hasdup, const QuantParams& Q, float x, int p, int k,
+                            double ab, double ab2, float abr, float erow, float b3r, double di, double dj,
+                            const float4& cf, const float4& cg, u16* gbins, const R10Hist& H, R10Acc& acc,
+                            bool& mism) {
+    const double kd = int_to_f64(k);
+    const double ckk = __dmul_rn((double)cf.w, kd), ck2k = DUP ? __dmul_rn((double)cg.w, kd) : ckk;
+    // the fast path's result for this point (recomputed: same operations)
+    const float c = __fmaf_rn(b3r, (float)k, abr);
+    const float s = __fmaf_rn(x, Q.rcp32, -c);
+    const float m = __fadd_rn(s, 12582912.0f);
+    const float rr = __fadd_rn(m, -12582912.0f);
+    const float f = __fadd_rn(s, -rr);
+    const float dl = __fmaf_rn(fabsf(s), 4.76837158203125e-07f, erow);
+    const bool big = !(fabsf(s) < Q.sbig);
+    const int qi = (int)__float_as_uint(m) - 0x4B400000;
+    const bool edge = !big && __fadd_rn(fabsf(f), dl) >= 0.49999905f;
+    const u32 bin = (u32)(Q.center + qi);
+    const bool ok = !big && (bin - 1u) < (u32)(Q.cap - 1);
+    const double offs = int_to_f64(qi);
+    const double p1 = __dadd_rn(ab, ckk);
+    const double d1 = __dadd_rn(p1, __dmul_rn(Q.twoeb, offs));
+    bool mis = false;
+    if (DUP) {
+        const double p2 = __dadd_rn(ab2, ck2k);
+        const double d2 = __dadd_rn(p2, __dmul_rn(Q.twoeb_dup, offs));
+        mis = dbits(p1) != dbits(p2) || dbits(d1) != dbits(d2);
     }
-}
-
-// tail points (rows past the last full 32-row iteration, at most 12 rows): one point per lane
-// per step, by the reference formulation directly (blocks.cu quant_point; no fix-up needed)
-template <bool DUP, bool PIN>
-FTLZ_DEV void r10_tail_point(const CompArgs& A, long long b, bool hasdup, const QuantParams& Q, const float* tile,
-                             int tye, int tz, int zoff, int p, int by, const float4& cf, const float4& cg,
-                             u16* gbins, const R10Hist& H, R10Acc& acc, bool& mism) {
-    const int rr = p / 10, k = p - rr * 10, i = rr / by, j = rr - i * by;
-    const float x = tile[(i * tye + j) * tz + zoff + k];
-    const double di = int_to_f64(i), dj = int_to_f64(j), dk = int_to_f64(k);
-    auto pred = [&](const float4& c) {
-        return __dadd_rn(__dadd_rn(__dadd_rn((double)c.x, __dmul_rn((double)c.y, di)), __dmul_rn((double)c.z, dj)),
-                         __dmul_rn((double)c.w, dk));
-    };
+    const float d32 = __double2float_rn(d1);
+    const float a = __fadd_rn(fabsf(__fadd_rn(x, -d32)), -Q.eb32);
+    const bool unsure = ok && fabsf(a) <= Q.band32;
+    const bool keep = ok && a <= 0.0f;
+    const u32 fb = keep ? bin : 0u;
+    const float rf = keep ? d32 : x;
     DupMask M;
-    if (!(hasdup && dup_masks(A, b, p, M))) {
+    const bool fp = hasdup && dup_masks(A, b, p, M);
+    if (!(edge || unsure || mis || fp || !Q.fast32)) return;
+    if (!fp) {
 #pragma unroll
         for (int q = 0; q < 3; q++) M.p[q] = M.r[q] = 0ull;
     }
-    float r32;
+    float rx;
     double back;
-    const u32 bin = (u32)quant_point(
-        Q, x, pred(cf), DUP, [&] { return pred(cg); },
+    const u32 ex = (u32)quant_point(
+        Q, x, p1, DUP, [&] { return __dadd_rn(opaque(ab2), opaque(ck2k)); },
         [&] {
             return __dadd_rn(__dadd_rn(__dadd_rn((double)cf.x, __dmul_rn((double)cf.y, di)), __dmul_rn((double)cf.z, dj)),
-                             __dmul_rn(opaque((double)cf.w), dk));
+                             __dmul_rn(opaque((double)cf.w), int_to_f64(k)));
         },
-        M, &r32, &mism, &back);
-    gbins[p] = (u16)bin;
-    acc.bs += bin;
-    acc.bis += (u64)(u32)p * (u64)bin;
-    acc.dc += (u64)__float_as_uint(r32);
-    if (bin == 0u) acc.rownz = 1u;
-    if (PIN) {
-        const u32 u = __float_as_uint(x);
-        acc.cs += (u64)u;
-        acc.csi += (u64)(u32)p * (u64)u;
+        M, &rx, &mism, &back);
+    gbins[p] = (u16)ex;
+    acc.bs += ex - fb;
+    acc.bis += (u32)p * ex - (u32)p * fb;
+    acc.dc += (u64)__float_as_uint(rx) - (u64)__float_as_uint(rf);
+    if (ex == 0u) acc.nz = true;
+    // drop the fast bin's count, count the exact bin
+    H.add(fb, -1);
+    H.add(ex, 1);
+}
+
+template <bool DUP>
+FTLZ_DEV void r10_rowtab(R10Row* rt, int rows, int by, int tye, int tz, int zoff, const float4& cf, const float4& cg,
+                         float b3r, double rcp32d, int lane) {
+    const u32 m16 = 65535u / (u32)by + 1u;   // ceil(2^16 / by): (r m16) >> 16 = r / by for r < 2^16 / 9
+    for (int r = lane; r < rows; r += 32) {
+        const int i = (int)(((u32)r * m16) >> 16), j = r - i * by;
+        const double di = int_to_f64(i), dj = int_to_f64(j);
+        R10Row t;
+        t.ab = __dadd_rn(__dadd_rn((double)cf.x, __dmul_rn((double)cf.y, di)), __dmul_rn((double)cf.z, dj));
+        t.ab2 = DUP ? __dadd_rn(__dadd_rn((double)cg.x, __dmul_rn((double)cg.y, di)), __dmul_rn((double)cg.z, dj)) : t.ab;
+        t.abr = __double2float_rn(__dmul_rn(t.ab, rcp32d));
+        t.erow = __fmaf_rn(9.0f, fabsf(b3r), fabsf(t.abr)) * 9.5367431640625e-07f + 9.094947017729282e-13f;
+        t.toff = (u32)((i * tye + j) * tz + zoff);
+        t.ij = (i << 16) | j;
+        rt[r] = t;
     }
-    H.add(bin, 1);
+    __syncwarp();
 }
 
 // compaction of the regression blocks after k_prep: 10-point-row blocks for k_quant_reg10
@@ -343,7 +279,9 @@ __global__ void __maxnreg__(R10_MAXREG) k_quant_reg10(const __grid_constant__ Co
     ws.base = slot;
     ws.tbytes = S.tile_bytes;
     unsigned char* lh = slot + 2 * S.tile_bytes;   // (R10_LH + 1) x 32 u8 counters
-    ws.bar = (u64*)(lh + (R10_LH + 1) * 32);
+    R10Row* rowtab = (R10Row*)(lh + (R10_LH + 1) * 32);   // R10_ROWS rows of the current block
+    R10Pre* pre = (R10Pre*)(rowtab + R10_ROWS);          // operands of the current / next block
+    ws.bar = (u64*)(pre + 2);
     u32* hwin = (u32*)(smem + (size_t)nw * A.r10_slot);
     const int lhlo = A.center - R10_LH / 2, wlo = A.center - HWIN_REG / 2;
     for (int t = lane; t < (R10_LH + 1) * 8; t += 32) ((u32*)lh)[t] = 0;
@@ -358,78 +296,139 @@ __global__ void __maxnreg__(R10_MAXREG) k_quant_reg10(const __grid_constant__ Co
     const u32 NW = gridDim.x * nw, nlist = A.counters[5];
     u32 idx = blockIdx.x * nw + warp;
     auto list_at = [&](u32 i) { return i < nlist ? (long long)A.r10_list[i] : (long long)-1; };
+    // per-block global operands (coefficients twice: the duplicate's independent copy, the
+    // checksum pair, the list entry after the next) travel one block ahead by cp.async into
+    // the slot's two R10Pre records, so their latency hides behind a block's work
+    auto prefetch = [&](long long bb, u32 i2, int q) {
+        R10Pre* P = pre + q;
+        if (lane == 0) cp_async16(&P->cf, A.coef + bb);
+        else if (lane == 1 && DUP) cp_async16(&P->cg, A.coef + bb);
+        else if (lane == 2 && PIN) cp_async8(&P->ins, A.insum + bb);
+        else if (lane == 3 && PIN) cp_async8(&P->inis, A.inisum + bb);
+        else if (lane == 4) {
+            if (i2 < nlist) cp_async4(&P->nxt, A.r10_list + i2);
+            else P->nxt = ~0u;
+        }
+        cp_commit();
+    };
     long long b = list_at(idx);
-    if (b >= 0) ws.issue(A.x, g, S, &tmap, block_info(g, b), 0, lane);
+    if (b >= 0) {
+        prefetch(b, idx + NW, 0);
+        ws.issue(A.x, g, S, &tmap, block_info(g, b), 0, lane);
+    }
     u32 lh_load = 0;
     int buf = 0;
     while (b >= 0) {
         const BlockInfo B = block_info(g, b);
+        cp_async_wait();
+        __syncwarp();
+        const R10Pre* P = pre + buf;
+        const long long bnx = P->nxt == ~0u ? -1ll : (long long)P->nxt;
+        const float4 cf = P->cf;
+        const float4 cg = DUP ? P->cg : cf;   // the duplicate's independently loaded copy
         idx += NW;
-        const long long bnx = list_at(idx);
-        if (bnx >= 0) ws.issue(A.x, g, S, &tmap, block_info(g, bnx), buf ^ 1, lane);
+        if (bnx >= 0) {
+            prefetch(bnx, idx + NW, buf ^ 1);
+            ws.issue(A.x, g, S, &tmap, block_info(g, bnx), buf ^ 1, lane);
+        }
         ws.wait(S, buf, bnx >= 0);
-        const float4 cf = A.coef[b];
         float* tile = (float*)(slot + buf * S.tile_bytes);
-        const int by = B.by, rows = B.bx * by, vol = B.vol, zoff = zshift(g, B);
-        // rows in 32-row steps, lane = row; a short remainder (<= 12 rows) point by point
-#ifdef R10_TAIL
-        const int nfull = (rows & 31) <= 12 ? (rows & ~31) : rows;
-#else
-        const int nfull = rows;
-#endif
+        const int by = B.by, rows = B.bx * by, vol = B.vol, zoff = zshift(g, B), npairs = rows * 5;
         TileWalk w0;
         w0.bx = B.bx; w0.by = by; w0.bz = 10; w0.stride = S.tz; w0.zoff = zoff; w0.bye = S.tye;
         // working-array faults persist only without input protection (pipeline.py:331-361)
         if (!PIN && A.n_faults) apply_input_faults(A, b, tile, w0, lane);
-        const float4 cg = DUP ? ld_volatile_f4(A.coef + b) : cf;
-        const double b0 = (double)cf.x, b1 = (double)cf.y, b2 = (double)cf.z, b3 = (double)cf.w;
+        const double b3 = (double)cf.w;
         const double b3d = (double)cg.w;   // the duplicate's own copy of b3
         const float b3r = __double2float_rn(__dmul_rn(b3, (double)Q.rcp32));
-        const FastDiv& fby = by == g.e ? A.fd_e : A.fd_ry;
         u16* gbins = A.bins + bins_index(g, b, 0);
         const bool hasdup = block_has_dup(A, b);
         bool mism = false, skip = false;
         R10Acc acc;
-        // every point this lane owns: its rows (< nfull), then its tail points
+        // the lane's column of point pairs: z offsets k0, k0 + 1 of rows rsub, rsub + 6, ... (lanes
+        // 30, 31 idle; 92% of the lane slots busy on a 10^3 block)
+        r10_rowtab<DUP>(rowtab, rows, by, S.tye, S.tz, zoff, cf, cg, b3r, (double)Q.rcp32, lane);
+        const int rsub = lane < 30 ? lane / 5 : R10_ROWS, k0 = 2 * (lane - 5 * (lane / 5));
+        const float kf0 = (float)k0, kf1 = (float)(k0 + 1);
+        const double ck0 = __dmul_rn(b3, int_to_f64(k0)), ck1 = __dmul_rn(b3, int_to_f64(k0 + 1));
+        const double ckd0 = DUP ? __dmul_rn(b3d, int_to_f64(k0)) : ck0, ckd1 = DUP ? __dmul_rn(b3d, int_to_f64(k0 + 1)) : ck1;
         auto lane_points = [&](auto f) {
-            for (int r = lane; r < nfull; r += 32)
-                for (int k = 0; k < 10; k++) f(r * 10 + k);
-            for (int p = nfull * 10 + lane; p < vol; p += 32) f(p);
-        };
-        for (int pass = 0; pass < 2; pass++) {
-            acc.bs = 0; acc.bis = 0; acc.dc = 0; acc.cs = 0; acc.csi = 0;
-            acc.rowflag = 0; acc.rownz = 0;
-            for (int t = 0, r = lane; r < nfull; t++, r += 32) {
-                const int i = (int)fdiv((u32)r, fby), j = r - i * by;
-                const double di = __int2double_rn(i), dj = __int2double_rn(j);
-                const double ab = __dadd_rn(__dadd_rn(b0, __dmul_rn(b1, di)), __dmul_rn(b2, dj));
-                const double ab2 = DUP ? __dadd_rn(__dadd_rn((double)cg.x, __dmul_rn((double)cg.y, di)),
-                                                   __dmul_rn((double)cg.z, dj))
-                                       : ab;
-                const float* row = tile + (i * S.tye + j) * S.tz + zoff;
-                const u32 rf = r10_row<DUP, PIN>(Q, row, ab, ab2, b3, b3d, b3r, r * 10, gbins, H, acc);
-                acc.rowflag |= (rf & 1u) << t;
-                acc.rownz |= rf >> 1;
+            for (int r = rsub; r < rows; r += 6) {
+                f(10 * r + k0);
+                f(10 * r + k0 + 1);
             }
-            for (int p = nfull * 10 + lane; p < vol; p += 32)
-                r10_tail_point<DUP, PIN>(A, b, hasdup, Q, tile, S.tye, S.tz, zoff, p, by, cf, cg, gbins, H, acc, mism);
-            if (hasdup) acc.rowflag = ~0u;
-            if (!Q.fast32) acc.rowflag = ~0u;
-            if (__any_sync(0xffffffffu, acc.rowflag != 0)) {
+        };
+        const u32 cbin = (u32)Q.center - 0x4B400000u;   // bits(m) + cbin = center + RN(s)
+        const u32 sink0 = H.sink();
+        for (int pass = 0; pass < 2; pass++) {
+            acc.reset();
+            for (int r = rsub; r < rows; r += 6) {
+                const R10Row R = rowtab[r];
+                const float2 x2 = *(const float2*)(tile + R.toff + k0);   // 8-byte aligned (zoff 0 or 2)
+                u32 r0, r1;
+                const u32 b0 = r10_point<DUP>(Q, x2.x, kf0, ck0, ckd0, R, b3r, cbin, H, acc, r0);
+                const u32 b1 = r10_point<DUP>(Q, x2.y, kf1, ck1, ckd1, R, b3r, cbin, H, acc, r1);
+                const u32 p0 = (u32)(10 * r + k0);
+                *(u32*)(gbins + p0) = __byte_perm(b0, b1, 0x5410);
+                acc.bs += b0 + b1;
+                acc.bis += p0 * b0 + (p0 + 1u) * b1;
+                acc.dc += (u64)r0 + (u64)r1;
+                if (PIN) {
+                    const u32 u0 = __float_as_uint(x2.x), u1 = __float_as_uint(x2.y);
+                    acc.cs += (u64)u0 + (u64)u1;
+                    acc.csi += (u64)p0 * u0 + (u64)(p0 + 1u) * u1;
+                }
+            }
+            // out-of-window fast bins of this lane (counted in its sink): recount into the CTA / global
+            // window before the fix-up moves counts between bins
+            if (__any_sync(0xffffffffu, H.sink() != sink0)) {
+                if (H.sink() != sink0) {
+                    H.lhw[R10_LH * 32] = (unsigned char)sink0;
+                    // the lane's (<= 17) bin pairs, 9 loads in flight at a time
+                    for (int h = 0; h < R10_ROWS / 6 + 1; h += 9) {
+                        u32 wv[9];
+#pragma unroll
+                        for (int t = 0; t < 9; t++) {
+                            const int r = rsub + 6 * (h + t);
+                            wv[t] = r < rows ? *(const u32*)(gbins + 10 * r + k0) : (u32)H.lhlo * 0x10001u;
+                        }
+#pragma unroll
+                        for (int t = 0; t < 9; t++) {
+#pragma unroll
+                            for (int u = 0; u < 2; u++) {
+                                const u32 bb = (wv[t] >> (16 * u)) & 0xffffu;
+                                if (bb - (u32)H.lhlo >= (u32)R10_LH) reg_hist_out(H.hwin, H.ghist, H.wlo, (int)bb, 1);
+                            }
+                        }
+                    }
+                }
                 __syncwarp();
-                if (acc.rowflag)
-                    r10_fixup<DUP>(A, b, hasdup, Q, tile, S.tye, S.tz, zoff, nfull, fby, by, cf, cg, gbins, H,
-                                   lane, acc, mism);
+            }
+            // exact recomputation of the flagged points (fix-up re-tests each point of the lane)
+            const bool fl = acc.emax >= 0.49999905f || acc.amin <= Q.band32 || acc.macc != 0u || hasdup || !Q.fast32;
+            if (__any_sync(0xffffffffu, fl)) {
+                __syncwarp();
+                if (fl) {
+                    for (int r = rsub; r < rows; r += 6) {
+                        const R10Row R = rowtab[r];
+                        const double di = int_to_f64(R.ij >> 16), dj = int_to_f64(R.ij & 0xffff);
+                        for (int u = 0; u < 2; u++) {
+                            const int k = k0 + u;
+                            r10_fix_point<DUP>(A, b, hasdup, Q, tile[R.toff + k], 10 * r + k, k, R.ab, R.ab2, R.abr,
+                                               R.erow, b3r, di, dj, cf, cg, gbins, H, acc, mism);
+                        }
+                    }
+                }
                 __syncwarp();
             }
             if (!PIN || pass == 1) break;
             // stage (c) verification of the tile against the stage (a) pair (pipeline.py:331-361)
             const u64 cs = warp_sum_u64_redux(acc.cs), csi = warp_sum_u64_redux(acc.csi);
-            if (cs == A.insum[b] && csi == A.inisum[b]) break;
+            if (cs == P->ins && csi == P->inis) break;
             // undo this pass's histogram counts, correct the tile, run again
             __syncwarp();
             lane_points([&](int p) { H.add(gbins[p], -1); });
-            const int rr = tile_correct(tile, w0, vol, A.insum[b], A.inisum[b], lane);
+            const int rr = tile_correct(tile, w0, vol, P->ins, P->inis, lane);
             if (lane == 0) {
                 atomicAdd(&A.counters[3], 1u);
                 A.events[b] |= rr == 1 ? 1 : 4;
@@ -440,15 +439,15 @@ __global__ void __maxnreg__(R10_MAXREG) k_quant_reg10(const __grid_constant__ Co
             }
             mism = false;
         }
-        lh_load += 4u * 10u;   // per-lane counter increments of this block (<= 40)
+        lh_load += 40u;   // per-lane counter increments of this block (<= 34)
         if (!skip) {
             const u32 bs = __reduce_add_sync(0xffffffffu, acc.bs);
-            const u64 bis = warp_sum_u64_redux(acc.bis), dc = warp_sum_u64_redux(acc.dc);
+            const u64 bis = warp_sum_u64_redux((u64)acc.bis), dc = warp_sum_u64_redux(acc.dc);
             if (__ballot_sync(0xffffffffu, mism) && lane == 0) atomicOr(&A.counters[1], 1u << (B.xid * 2 + 1));
             __syncwarp();
             // unpredictable words in point order (rare): 32 consecutive points per step
             u32 nz = 0;
-            if (__any_sync(0xffffffffu, acc.rownz != 0)) {
+            if (__any_sync(0xffffffffu, acc.nz)) {
                 u32* unp = A.unp_scratch + (size_t)b * g.vmax;
                 for (int p0 = 0; p0 < vol; p0 += 32) {
                     const int p = p0 + lane;
