@@ -375,7 +375,7 @@ static KCfg kcfg_comp(const Geom& g) {
         k.pp_smem = ps * k.pp_warps + 128;
     }
     // k_quant_reg10: 2 TMA tiles, lane histogram (R10_LH + sink rows of 32 u8), mbarriers
-    k.r10_slot = (int)(((size_t)2 * k.stage.tile_bytes + (R10_LH + 1) * 32 + sizeof(R10Row) * R10_ROWS +
+    k.r10_slot = (int)(((size_t)2 * k.stage.tile_bytes + R10_LHBYTES + sizeof(R10Row) * R10_ROWS +
                         2 * sizeof(R10Pre) + 16 + 127) & ~(size_t)127);
     k.r10_warps = (int)std::max<size_t>(1, std::min<size_t>(R10_WARPS, (227 * 1024 - 4 * HWIN_REG - 256) / k.r10_slot));
     k.r10_smem = (size_t)k.r10_slot * k.r10_warps + 4 * HWIN_REG + 128;

@@ -49,41 +49,49 @@ struct R10Acc {
     }
 };
 
-// lane-private u8 counters: bin o of the window at byte o * 32 + lane.  A bin outside the window
-// only bumps the lane's sink counter (row R10_LH): no branch in the point loop; a row whose
-// sink count moved is recounted afterwards into the CTA's shared window (hwin, HWIN_REG bins) or,
-// beyond it, the global histogram.
+// lane-private u8 counters: bin o of the window in byte o & 3 of word (o >> 2) * 32 + lane, so
+// every lane's counters sit in its own bank (no conflicts whatever the bins).  A bin outside the
+// window only bumps the lane's sink counter (word row R10_LH / 4): no branch in the point loop;
+// when the sink moved, the lane's bins are recounted afterwards into the CTA's shared window
+// (hwin, HWIN_REG bins) or, beyond it, the global histogram.
+#define R10_LHBYTES ((R10_LH / 4 + 1) * 32 * 4)
 struct R10Hist {
-    unsigned char* lhw;   // this lane's column of the u8 window
+    unsigned char* lhw;   // this lane's column: lh + 4 lane
     u32* hwin;            // CTA window
     u64* ghist;
     int lhlo, wlo;
+    FTLZ_DEV unsigned char* at(u32 o) const { return lhw + (o * 32u - (o & 3u) * 31u); }   // (o >> 2) 128 + (o & 3)
     // count `delta` (+1 / -1) for bin b (slow paths: fix-up, recount, undo)
     FTLZ_DEV void add(u32 b, int delta) const {
         const u32 o = b - (u32)lhlo;
-        if (o < (u32)R10_LH) lhw[o * 32] += (unsigned char)delta;
+        if (o < (u32)R10_LH) *at(o) += (unsigned char)delta;
         else reg_hist_out(hwin, ghist, wlo, (int)b, delta);
     }
     // hot path: window counter, or the sink for an out-of-window bin (recounted per block)
-    FTLZ_DEV void bump(u32 b) const { lhw[min(b - (u32)lhlo, (u32)R10_LH) * 32] += 1; }
-    FTLZ_DEV u32 sink() const { return lhw[R10_LH * 32]; }
+    FTLZ_DEV void bump(u32 b) const { *at(min(b - (u32)lhlo, (u32)R10_LH)) += 1; }
+    FTLZ_DEV u32 sink() const { return *at(R10_LH); }
+    FTLZ_DEV void set_sink(u32 v) const { *at(R10_LH) = (unsigned char)v; }
 };
 
-FTLZ_DEV void lh_flush10(unsigned char* lh, u64* ghist, int lhlo, int cap, int lane) {
+// lane l adds word row l (bins 4 l .. 4 l + 3) over the 32 lanes' words (rotated: conflict-free)
+// into the global histogram and clears it
+FTLZ_DEV void lh_flush10(u32* lh, u64* ghist, int lhlo, int cap, int lane) {
+    static_assert(R10_LH == 128, "one word row per lane");
     __syncwarp();
-    u32* w32 = (u32*)lh;   // bin o: words o * 8 .. o * 8 + 7 (32 u8 counters)
+    u32 se = 0, so = 0;   // bytes 0, 2 / 1, 3 of the words as 16-bit sums (<= 32 * 255)
+#pragma unroll 8
+    for (int c = 0; c < 32; c++) {
+        u32* w = lh + lane * 32 + ((c + lane) & 31);
+        const u32 v = *w;
+        se += v & 0x00ff00ffu;
+        so += (v >> 8) & 0x00ff00ffu;
+        *w = 0;
+    }
+    const u32 sums[4] = {se & 0xffffu, so & 0xffffu, se >> 16, so >> 16};
 #pragma unroll
-    for (int q = 0; q < R10_LH / 32; q++) {
-        const int o = (R10_LH / 32) * lane + q;
-        u32 sum = 0;
-#pragma unroll
-        for (int c = 0; c < 8; c++) {
-            const int cc = (c + lane) & 7;
-            sum = __dp4a(w32[o * 8 + cc], 0x01010101u, sum);
-            w32[o * 8 + cc] = 0;
-        }
-        const int bn = lhlo + o;
-        if (sum && bn >= 0 && bn < cap) atomicAdd(&ghist[bn], (u64)sum);
+    for (int q = 0; q < 4; q++) {
+        const int bn = lhlo + 4 * lane + q;
+        if (sums[q] && bn >= 0 && bn < cap) atomicAdd(&ghist[bn], (u64)sums[q]);
     }
     __syncwarp();
 }
@@ -278,42 +286,49 @@ __global__ void __maxnreg__(R10_MAXREG) k_quant_reg10(const __grid_constant__ Co
     WarpStager ws;
     ws.base = slot;
     ws.tbytes = S.tile_bytes;
-    unsigned char* lh = slot + 2 * S.tile_bytes;   // (R10_LH + 1) x 32 u8 counters
-    R10Row* rowtab = (R10Row*)(lh + (R10_LH + 1) * 32);   // R10_ROWS rows of the current block
+    u32* lh = (u32*)(slot + 2 * S.tile_bytes);   // R10_LHBYTES of lane counters
+    R10Row* rowtab = (R10Row*)((unsigned char*)lh + R10_LHBYTES);   // R10_ROWS rows of the current block
     R10Pre* pre = (R10Pre*)(rowtab + R10_ROWS);          // operands of the current / next block
     ws.bar = (u64*)(pre + 2);
     u32* hwin = (u32*)(smem + (size_t)nw * A.r10_slot);
     const int lhlo = A.center - R10_LH / 2, wlo = A.center - HWIN_REG / 2;
-    for (int t = lane; t < (R10_LH + 1) * 8; t += 32) ((u32*)lh)[t] = 0;
+    for (int t = lane; t < R10_LHBYTES / 4; t += 32) lh[t] = 0;
     for (int t = threadIdx.x; t < HWIN_REG; t += blockDim.x) hwin[t] = 0;
-    const R10Hist H = {lh + lane, hwin, A.hist, lhlo, wlo};
+    const R10Hist H = {(unsigned char*)(lh + lane), hwin, A.hist, lhlo, wlo};
     ws.init(lane);
     __syncthreads();
 
     const QuantParams Q = *A.qp;
-    // blocks idx, idx + NW, ... of r10_list (k_reglist); the next block's tile is in flight
-    // while this one is processed
+    // list positions: warp w of CTA c starts at c * nw + w, then takes tickets NW, NW + 1, ...
+    // from counters[7] (dynamic: SMs that run ahead take more blocks).  The ticket is drawn two
+    // blocks ahead by lane 4, the list entry it names arrives one block ahead; the next block's
+    // tile is in flight while this one is processed.
     const u32 NW = gridDim.x * nw, nlist = A.counters[5];
-    u32 idx = blockIdx.x * nw + warp;
-    auto list_at = [&](u32 i) { return i < nlist ? (long long)A.r10_list[i] : (long long)-1; };
+    const u32 idx = blockIdx.x * nw + warp;
+    u32 ticket = 0;
+    auto draw = [&] {
+        if (lane == 4) ticket = NW + atomicAdd(&A.counters[7], 1u);
+    };
     // per-block global operands (coefficients twice: the duplicate's independent copy, the
     // checksum pair, the list entry after the next) travel one block ahead by cp.async into
     // the slot's two R10Pre records, so their latency hides behind a block's work
-    auto prefetch = [&](long long bb, u32 i2, int q) {
+    auto prefetch = [&](long long bb, int q) {
         R10Pre* P = pre + q;
         if (lane == 0) cp_async16(&P->cf, A.coef + bb);
         else if (lane == 1 && DUP) cp_async16(&P->cg, A.coef + bb);
         else if (lane == 2 && PIN) cp_async8(&P->ins, A.insum + bb);
         else if (lane == 3 && PIN) cp_async8(&P->inis, A.inisum + bb);
         else if (lane == 4) {
-            if (i2 < nlist) cp_async4(&P->nxt, A.r10_list + i2);
+            if (ticket < nlist) cp_async4(&P->nxt, A.r10_list + ticket);
             else P->nxt = ~0u;
         }
         cp_commit();
     };
-    long long b = list_at(idx);
+    long long b = idx < nlist ? (long long)A.r10_list[idx] : -1ll;
     if (b >= 0) {
-        prefetch(b, idx + NW, 0);
+        draw();
+        prefetch(b, 0);
+        draw();
         ws.issue(A.x, g, S, &tmap, block_info(g, b), 0, lane);
     }
     u32 lh_load = 0;
@@ -326,9 +341,9 @@ __global__ void __maxnreg__(R10_MAXREG) k_quant_reg10(const __grid_constant__ Co
         const long long bnx = P->nxt == ~0u ? -1ll : (long long)P->nxt;
         const float4 cf = P->cf;
         const float4 cg = DUP ? P->cg : cf;   // the duplicate's independently loaded copy
-        idx += NW;
         if (bnx >= 0) {
-            prefetch(bnx, idx + NW, buf ^ 1);
+            prefetch(bnx, buf ^ 1);
+            draw();
             ws.issue(A.x, g, S, &tmap, block_info(g, bnx), buf ^ 1, lane);
         }
         ws.wait(S, buf, bnx >= 0);
@@ -383,7 +398,7 @@ __global__ void __maxnreg__(R10_MAXREG) k_quant_reg10(const __grid_constant__ Co
             // window before the fix-up moves counts between bins
             if (__any_sync(0xffffffffu, H.sink() != sink0)) {
                 if (H.sink() != sink0) {
-                    H.lhw[R10_LH * 32] = (unsigned char)sink0;
+                    H.set_sink(sink0);
                     // the lane's (<= 17) bin pairs, 9 loads in flight at a time
                     for (int h = 0; h < R10_ROWS / 6 + 1; h += 9) {
                         u32 wv[9];
