@@ -240,15 +240,20 @@ struct CodebookScratch {
 };
 
 // two-queue Huffman merge over leaves sorted by (weight, symbol) (the reference heap with its
-// (weight, tie) order, encode.py:26-71): leaves 0..n-1, merged nodes n..2n-2; queue heads in
+// (weight, tie) order, encode.py:26-71): leaves 0..n-1, merged nodes n..2n-2 in creation order,
+// W[node] its weight.  Queue state: li leaves and (mi - n) merged nodes consumed, mk the next
+// merged id.  cb_merge_seq runs up to `steps` merges from that state with the queue heads in
 // registers.  W must point into one memory space (shared or global) so accesses stay typed.
 template <typename WT, typename SetParent>
-FTLZ_DEV void cb_merge3(WT* W, int n, SetParent set_parent) {
+FTLZ_DEV void cb_merge_seq(WT* W, int n, int& li_, int& mi_, int& mk_, int steps, SetParent set_parent) {
     const WT INF = (WT)~(WT)0;
-    int li = 0, mi = n, mk = n;
-    WT L0 = W[0], L1 = n > 1 ? W[1] : INF, L2 = n > 2 ? W[2] : INF, L3 = n > 3 ? W[3] : INF;
-    WT M0 = INF, M1 = INF, M2 = INF, M3 = INF;
-    for (int t = 0; t < n - 1; t++) {
+    int li = li_, mi = mi_, mk = mk_;
+    WT L0 = li < n ? W[li] : INF, L1 = li + 1 < n ? W[li + 1] : INF;
+    WT L2 = li + 2 < n ? W[li + 2] : INF, L3 = li + 3 < n ? W[li + 3] : INF;
+    WT M0 = mi < mk ? W[mi] : INF, M1 = mi + 1 < mk ? W[mi + 1] : INF;
+    WT M2 = mi + 2 < mk ? W[mi + 2] : INF, M3 = mi + 3 < mk ? W[mi + 3] : INF;
+    const int mend = 2 * n - 1;
+    for (int t = 0; t < steps && mk < mend; t++) {
         const bool c1 = L0 <= M0, c2 = L1 <= M0, c3 = L0 <= M1;
         const bool LL = c1 && c2, MM = !c1 && !c3;
         const int ca = MM ? mi : li, cb = LL ? li + 1 : (MM ? mi + 1 : mi);
@@ -273,20 +278,94 @@ FTLZ_DEV void cb_merge3(WT* W, int n, SetParent set_parent) {
         set_parent(cb, mk);
         mk++;
     }
+    li_ = li; mi_ = mi; mk_ = mk;
 }
 
-// symbol of alphabet rank i: the word holding it by binary search over the word prefixes,
-// then the (i - prefix)-th set bit of that word
-FTLZ_DEV int cb_select(const u32* bm, const u32* wpre, int nwords, u32 i) {
-    int lo = 0, hi = nwords - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (wpre[mid] <= i) lo = mid;
-        else hi = mid - 1;
+// the same merge, round-synchronous on the whole CTA.  With y1 <= y2 <= ... the remaining nodes
+// in (weight, tie) order and s1 = y1 + y2, the heap pops the pairs (y1, y2), (y3, y4), ...
+// as long as y_2j precedes s1: s1 is the newest node (largest tie), so that is w(y_2j) <= w(s1),
+// and the merged sums are non-decreasing, so they join the merged queue in order.  A round
+// merges k = floor(#{y : w(y) <= w(s1)} / 2) pairs at once (c4: 4890 leaves in 23 rounds);
+// rounds with fewer than CB_KMIN pairs run CB_SEQ sequential merges instead (one thread).
+#define CB_KMIN 32
+#define CB_SEQ 64
+template <typename WT, typename SetParent>
+FTLZ_DEV void cb_merge_par(WT* W, int n, SetParent set_parent) {
+    __shared__ int s_li, s_mi, s_mk, s_k, s_a;
+    const int tid = threadIdx.x;
+    if (tid == 0) { s_li = 0; s_mi = n; s_mk = n; }
+    __syncthreads();
+    // number of leaves among the first d remaining nodes (leaves win weight ties)
+    auto split = [&](int li, int llen, int mi, int mlen, int d) {
+        int lo = max(0, d - mlen), hi = min(d, llen);
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (W[li + mid] <= W[mi + d - 1 - mid]) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    };
+    // first index in [lo, hi) with W > v
+    auto upper = [&](int lo, int hi, WT v) {
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (W[mid] <= v) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    };
+    const int mend = 2 * n - 1;
+    while (true) {
+        const int li = s_li, mi = s_mi, mk = s_mk;
+        __syncthreads();   // the state is read before thread 0 moves it
+        if (mk >= mend) break;
+        const int llen = n - li, mlen = mk - mi;
+        if (tid == 0) {
+            // s1 from the two smallest remaining nodes
+            int x = 0, y = 0;
+            WT s1 = 0;
+            for (int u = 0; u < 2; u++) {
+                const bool tl = x < llen && (y >= mlen || W[li + x] <= W[mi + y]);
+                s1 += tl ? W[li + x] : W[mi + y];
+                x += tl;
+                y += !tl;
+            }
+            const int c = (upper(li, n, s1) - li) + (upper(mi, mk, s1) - mi);
+            const int k = c >> 1;
+            if (k < CB_KMIN) {
+                int l2 = li, m2 = mi, k2 = mk;
+                cb_merge_seq(W, n, l2, m2, k2, CB_SEQ, set_parent);
+                s_li = l2; s_mi = m2; s_mk = k2; s_k = 0;
+            } else {
+                s_k = k;
+                s_a = split(li, llen, mi, mlen, 2 * k);
+            }
+        }
+        __syncthreads();
+        const int k = s_k;
+        if (k) {
+            for (int j = tid; j < k; j += blockDim.x) {
+                const int d = 2 * j;
+                int x = split(li, llen, mi, mlen, d), y = d - x;
+                int id[2];
+                WT w[2];
+#pragma unroll
+                for (int u = 0; u < 2; u++) {
+                    const bool tl = x < llen && (y >= mlen || W[li + x] <= W[mi + y]);
+                    id[u] = tl ? li + x : mi + y;
+                    w[u] = W[id[u]];
+                    x += tl;
+                    y += !tl;
+                }
+                W[mk + j] = w[0] + w[1];
+                set_parent(id[0], mk + j);
+                set_parent(id[1], mk + j);
+            }
+            __syncthreads();
+            if (tid == 0) { s_li = li + s_a; s_mi = mi + 2 * k - s_a; s_mk = mk + k; }
+        }
+        __syncthreads();
     }
-    u32 m = bm[lo];
-    for (u32 r = i - wpre[lo]; r; r--) m &= m - 1;
-    return lo * 32 + __ffs(m) - 1;
 }
 
 // alphabet bitmap {0} U {s : hist[s] > 0} over the whole grid: the histogram is read once by
@@ -301,6 +380,76 @@ __global__ void __launch_bounds__(256) k_cb_bitmap(CompArgs A, u32* bm) {
     if (lane == 0) bm[w] = m;
 }
 
+// one stable LSD counting pass of the whole CTA: out = in ordered by the digit
+// (key >> shift) & (2^RBITS - 1), equal digits in input order.  Warp w owns a contiguous run of
+// 32-item steps; a step ranks its lanes by __match_any_sync on the digit, and per-warp digit
+// counters (cnt: nwarps x 2^RBITS words) give every item its slot (count, offsets, scatter).
+template <int RBITS>
+FTLZ_DEV void cb_radix_pass(const u64* in, u64* out, int n, int shift, u32* cnt, u32* base) {
+    constexpr int R = 1 << RBITS;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int steps = (n + 32 * nw - 1) / (32 * nw);
+    const int i0 = warp * steps * 32;
+    u32* wc = cnt + warp * R;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int d = lane; d < R; d += 32) wc[d] = 0;
+    __syncwarp();
+    for (int st = 0; st < steps; st++) {
+        const int i = i0 + st * 32 + lane;
+        const u32 dg = i < n ? (u32)(in[i] >> shift) & (R - 1) : (u32)R;
+        const unsigned m = __match_any_sync(0xffffffffu, dg);
+        if (dg < (u32)R && !(m & lt)) wc[dg] += __popc(m);
+        __syncwarp();
+    }
+    __syncthreads();
+    // per digit: exclusive prefix over the warps (in place), digit totals into base
+    for (int d = tid; d < R; d += blockDim.x) {
+        u32 run = 0;
+        for (int w = 0; w < nw; w++) {
+            const u32 c = cnt[w * R + d];
+            cnt[w * R + d] = run;
+            run += c;
+        }
+        base[d] = run;
+    }
+    __syncthreads();
+    if (warp == 0) {   // exclusive scan of the digit totals: lane l holds digits l * R/32 ..
+        constexpr int PER = R / 32 > 0 ? R / 32 : 1;
+        u32 loc = 0;
+        for (int q = 0; q < PER; q++) loc += lane * PER + q < R ? base[lane * PER + q] : 0u;
+        u32 inc = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        u32 run = inc - loc;
+        for (int q = 0; q < PER; q++) {
+            if (lane * PER + q < R) {
+                const u32 c = base[lane * PER + q];
+                base[lane * PER + q] = run;
+                run += c;
+            }
+        }
+    }
+    __syncthreads();
+    for (int st = 0; st < steps; st++) {
+        const int i = i0 + st * 32 + lane;
+        const u64 key = i < n ? in[i] : 0ull;
+        const u32 dg = i < n ? (u32)(key >> shift) & (R - 1) : (u32)R;
+        const unsigned m = __match_any_sync(0xffffffffu, dg);
+        u32 pos = 0;
+        if (dg < (u32)R) pos = base[dg] + wc[dg] + __popc(m & lt);
+        __syncwarp();
+        if (dg < (u32)R) {
+            out[pos] = key;
+            if (!(m & lt)) wc[dg] += __popc(m);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScratch S) {
     if (dev_failed(A.st)) return;
     extern __shared__ __align__(16) u64 cb_dyn[];   // keys[CB_SMEM_KEYS] | weights[2*CB_SMEM_KEYS]
@@ -311,6 +460,7 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
     __shared__ u64 firstcode[64];
     __shared__ u32 firstidx[64];
     __shared__ int s_n, s_maxlen, s_np2;
+    __shared__ u32 s_rbase[256];
     __shared__ u64 s_total;
     int cap = A.cap;
     int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -352,21 +502,52 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
     };
     build_ranks();
     int n = s_n;
-    int np2 = 1;
-    while (np2 < n) np2 <<= 1;
-    u64* keys = np2 <= CB_SMEM_KEYS ? skeys : S.keys;
-    for (int i = tid; i < n; i += CB_THREADS) {
-        const int sy = cb_select(s_bm, s_wpre, nwords, (u32)i);
-        keys[i] = ((u64)A.hist[sy] << 16) | (u64)sy;   // (weight, symbol)
-    }
-    for (int i = n + tid; i < np2; i += CB_THREADS) keys[i] = ~0ull;
+    const bool small = n <= CB_SMEM_KEYS;
+    // keys and their ping-pong partner: shared memory (the weights region is free until the
+    // merge) or global scratch
+    u64* keys = small ? skeys : S.keys;
+    u64* keys2 = small ? cb_dyn + CB_SMEM_KEYS : S.keys + cap;
+    u32 wmax = 0;
+    // every alphabet symbol with its rank (= position in symbol order): thread per bitmap word
+    auto for_each_symbol = [&](auto f) {
+        for (int w = tid; w < nwords; w += CB_THREADS) {
+            u32 m = s_bm[w], r = s_wpre[w];
+            while (m) {
+                const u32 sy = (u32)w * 32u + (u32)(__ffs(m) - 1);
+                m &= m - 1u;
+                f(r++, sy);
+            }
+        }
+    };
+    for_each_symbol([&](u32 i, u32 sy) {
+        const u64 w = A.hist[sy];
+        keys[i] = (w << 16) | (u64)sy;   // (weight, symbol), in symbol order
+        wmax = max(wmax, 64u - (u32)__clzll((long long)w));
+    });
+    if (tid == 0) s_np2 = 0;
     __syncthreads();
-    bitonic_sort_u64(keys, np2);
-    // 2) two-queue merge (sequential, one thread; the reference heap with its (weight, tie)
-    //    order, encode.py:26-71): node ids: leaves 0..n-1 in sorted order, merged n..2n-2.
+    atomicMax(&s_np2, (int)wmax);
+    __syncthreads();
+    {
+        // stable LSD passes over the weight bytes: (weight, symbol) order.  The digit counters
+        // overlay the rank bitmap region (done with above).
+        u32* cnt = (u32*)(cb_dyn + 3 * CB_SMEM_KEYS);
+        const int wbits = s_np2;
+        for (int sh = 0; sh < wbits; sh += 8) {
+            cb_radix_pass<8>(keys, keys2, n, 16 + sh, cnt, s_rbase);
+            u64* t = keys; keys = keys2; keys2 = t;
+        }
+        if (small && keys != skeys) {   // the merge's weights go where the keys ended up
+            for (int i = tid; i < n; i += CB_THREADS) skeys[i] = keys[i];
+            keys2 = keys;
+            keys = skeys;
+            __syncthreads();
+        }
+    }
+    // 2) two-queue merge (round-synchronous, cb_merge_par; the reference heap with its (weight,
+    //    tie) order, encode.py:26-71): node ids: leaves 0..n-1 in sorted order, merged n..2n-2.
     //    Queue heads are kept in registers; weights and parents live in shared memory when the
     //    alphabet fits (u16 parents), else in global scratch.
-    const bool small = np2 <= CB_SMEM_KEYS;
     u16* par16 = (u16*)(cb_dyn + 3 * CB_SMEM_KEYS);
     const bool w32 = (u64)A.g.nx * (u64)A.g.ny * (u64)A.g.nz < 0xffffffffull;   // total weight fits u32
     {
@@ -378,22 +559,22 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
         }
         __syncthreads();
     }
-    if (tid == 0) {
-        s_maxlen = 0;
-        if (n == 1) {
+    if (tid == 0) s_maxlen = 0;
+    if (n == 1) {
+        if (tid == 0) {
             if (small) par16[0] = 0xffffu;
             else S.parent[0] = 0xffffffffu;
-        } else if (small) {
-            auto sp = [&](int i, int mk) { par16[i] = (u16)mk; };
-            if (w32) cb_merge3((u32*)(cb_dyn + CB_SMEM_KEYS), n, sp);
-            else cb_merge3(cb_dyn + CB_SMEM_KEYS, n, sp);
-            par16[2 * n - 2] = 0xffffu;
-        } else {
-            auto sp = [&](int i, int mk) { S.parent[i] = (u32)mk; };
-            if (w32) cb_merge3((u32*)S.w, n, sp);
-            else cb_merge3(S.w, n, sp);
-            S.parent[2 * n - 2] = 0xffffffffu;
         }
+    } else if (small) {
+        auto sp = [&](int i, int mk) { par16[i] = (u16)mk; };
+        if (w32) cb_merge_par((u32*)(cb_dyn + CB_SMEM_KEYS), n, sp);
+        else cb_merge_par(cb_dyn + CB_SMEM_KEYS, n, sp);
+        if (tid == 0) par16[2 * n - 2] = 0xffffu;
+    } else {
+        auto sp = [&](int i, int mk) { S.parent[i] = (u32)mk; };
+        if (w32) cb_merge_par((u32*)S.w, n, sp);
+        else cb_merge_par(S.w, n, sp);
+        if (tid == 0) S.parent[2 * n - 2] = 0xffffffffu;
     }
     __syncthreads();
     // 3) depths by walking parent pointers (parallel over leaves)
@@ -421,16 +602,14 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
         if (tid == 0) dev_fail(A.st, FTLZ_ERR_INVARIANT, FTLZ_K_CODE_LEN, -1, -1, maxlen, 0, 0);
         return;
     }
-    // 4) canonical codes by (length, symbol): sort keys (len << 16 | sym)
-    for (int i = tid; i < np2; i += CB_THREADS) {
-        if (i < n) {
-            u32 sym = S.syms[i];
-            keys[i] = ((u64)S.lens[sym] << 16) | sym;
-        } else keys[i] = ~0ull;
-    }
+    // 4) canonical codes by (length, symbol): one stable counting pass by length over the
+    //    symbols in ascending order (ranks rebuilt: the region held the parent pointers)
+    __syncthreads();
+    build_ranks();
+    for_each_symbol([&](u32 i, u32 sym) { keys2[i] = ((u64)S.lens[sym] << 16) | sym; });
     if (tid < 64) { lencount[tid] = 0; s_lfirst[tid] = 0; s_llast[tid] = 0; }
     __syncthreads();
-    bitonic_sort_u64(keys, np2);
+    cb_radix_pass<6>(keys2, keys, n, 16, s_wpre + 2048, s_rbase);
     // keys are sorted by length: each length's count is the span between its boundaries
     for (int i = tid; i < n; i += CB_THREADS) {
         const u32 l = (u32)(keys[i] >> 16);
@@ -504,15 +683,12 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
     // 6) codebook section: u32 count, then (u32 symbol, u8 length) in ascending symbol order
     u8* o = A.out + book_off;
     if (tid < 4) o[tid] = (u8)(n >> (8 * tid));
-    // symbols in ascending order: ranks from the bitmap prefixes (rebuilt: the region held
-    // the parent pointers)
-    __syncthreads();
-    build_ranks();
+    // symbols in ascending order with their lengths: the input of the length pass (keys2)
     for (int i = tid; i < n; i += CB_THREADS) {
-        const u32 sy = (u32)cb_select(s_bm, s_wpre, nwords, (u32)i);
+        const u32 sy = (u32)(keys2[i] & 0xffffu);
         u8* e = o + 4 + 5ull * (u64)i;
         e[0] = (u8)sy; e[1] = (u8)(sy >> 8); e[2] = (u8)(sy >> 16); e[3] = (u8)(sy >> 24);
-        e[4] = S.lens[sy];
+        e[4] = (u8)(keys2[i] >> 16);
     }
 }
 
