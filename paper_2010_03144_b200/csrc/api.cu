@@ -303,6 +303,13 @@ static int upload_plan(const HostPlan& P, unsigned char* dst, DevPlan& D, cudaSt
 // kernel configuration (shared memory per block slot, blocks per CTA)
 static size_t al16(size_t x) { return (x + 15) & ~(size_t)15; }
 
+// warps of a k_decode CTA: `want`, fewer when the per-warp staging rows of a large block
+// edge would not fit next to the decode table
+static int dec_warps(int e, int want) {
+    const size_t room = 200 * 1024 - ((size_t)4 << DEC_TBITS);
+    return (int)std::max<size_t>(1, std::min<size_t>((size_t)want, room / (dec_stage_words(e) * 4)));
+}
+
 struct KCfg {
     size_t lor_smem, lor_slot;
     int lor_warps;
@@ -1097,7 +1104,13 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         k_parse_tail<<<1, PT_THREADS, 8192 * 8, s>>>(A, 0);
     }
     LCHK("k_parse_tail");
-    size_t dec_smem = ((size_t)4 << DEC_TBITS) + (size_t)DEC_WARPS * dec_stage_words((int)g.e) * 4;
+    // full-path k_decode: up to DEC_WARPS warps per CTA, fewer when the per-warp staging rows of
+    // a large block edge would not fit in shared memory
+    const int dec_nw = dec_warps((int)g.e, DEC_WARPS);
+    size_t dec_smem = ((size_t)4 << DEC_TBITS) + (size_t)dec_nw * dec_stage_words((int)g.e) * 4;
+    int dec_occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&dec_occ, k_decode<false, true>, dec_nw * 32, dec_smem));
+    dec_occ = std::max(dec_occ, 1);
     size_t rslot = al16((size_t)g.vmax * 8) + al16((size_t)g.vmax * 4) + al16(2 * (size_t)g.nvmax8);
     int rw = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / rslot));
     if (decode) {
@@ -1110,9 +1123,10 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
             const long long l0 = g.cx * si / nslab, l1 = g.cx * (si + 1) / nslab;
             A.sb0 = l0 * layer;
             A.sb1 = l1 * layer;
-            const unsigned dgrid = (unsigned)((A.sb1 - A.sb0 + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32));
+            // one CTA per SM (fewer when there are fewer 32-block tasks), tasks split evenly
+            const unsigned dgrid = (unsigned)std::min<long long>((A.sb1 - A.sb0 + 31) / 32, (long long)sms * dec_occ);
             PF.mark("k_decode", s);
-            k_decode<false, true><<<dgrid, DEC_WARPS * 32, dec_smem, s>>>(A, nullptr, 0);
+            k_decode<false, true><<<dgrid, dec_nw * 32, dec_smem, s>>>(A, nullptr, 0);
             LCHK("k_decode");
             if (!fblk.empty()) {
                 k_decomp_faults<<<(unsigned)((fblk.size() + 7) / 8), 256, 0, s>>>(A, (const u32*)(ws + L.fblk),
@@ -1175,7 +1189,7 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
             CK(cudaMemcpyAsync(ws + L.mis, &bb, 4, cudaMemcpyHostToDevice, s));
             A.region = 1;
             A.n_faults = 0;
-            k_decode<false, false><<<1, DEC_WARPS * 32, dec_smem, s>>>(A, (const u32*)(ws + L.mis), 1);
+            k_decode<false, false><<<1, dec_nw * 32, dec_smem, s>>>(A, (const u32*)(ws + L.mis), 1);
             LCHK("k_decode");
             CK(cudaStreamSynchronize(s));
             CK(cudaMemcpyAsync(&k, ws + L.dflag + b, 1, cudaMemcpyDeviceToHost, s));
@@ -1269,10 +1283,12 @@ static int region_core(const HostPlan& P, const DevPlan& D, const uint8_t* d_a, 
     A.region_list = (const u32*)(ws + L.rlist);
     A.n_region = n;
     const int sms = num_sms();
-    const size_t dec_smem = ((size_t)4 << DEC_TBITS) + (size_t)DEC_WARPS * dec_stage_words((int)g.e) * 4;
+    // lane per listed block, 4-warp CTAs so a short list still spreads over the SMs
+    const int dnw = dec_warps((int)g.e, 4);
+    const size_t dec_smem = ((size_t)4 << DEC_TBITS) + (size_t)dnw * dec_stage_words((int)g.e) * 4;
     const size_t rslot = al16((size_t)g.vmax * 8) + al16((size_t)g.vmax * 4) + al16(2 * (size_t)g.nvmax8);
     const int rw = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / rslot));
-    k_decode<false, false><<<(n + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32), DEC_WARPS * 32, dec_smem, s>>>(A, A.region_list, (int)n);
+    k_decode<false, false><<<(n + dnw * 32 - 1) / (dnw * 32), dnw * 32, dec_smem, s>>>(A, A.region_list, (int)n);
     LCHK("k_decode");
     k_recon_g<32><<<std::min<u32>((n + rw - 1) / rw, (u32)sms * 4), rw * 32, rslot * rw, s>>>(A, 2);
     LCHK("k_recon");
@@ -1298,7 +1314,7 @@ static int region_core(const HostPlan& P, const DevPlan& D, const uint8_t* d_a, 
         std::sort(mis.begin(), mis.end());
         CK(cudaMemcpyAsync(ws + L.mis, mis.data(), 4 * (size_t)nmis, cudaMemcpyHostToDevice, s));
         A.region = 0;   // re-decode failures mark mflag = 3
-        k_decode<false, true><<<(nmis + DEC_WARPS * 32 - 1) / (DEC_WARPS * 32), DEC_WARPS * 32, dec_smem, s>>>(
+        k_decode<false, true><<<(nmis + dnw * 32 - 1) / (dnw * 32), dnw * 32, dec_smem, s>>>(
             A, (const u32*)(ws + L.mis), (int)nmis);
         LCHK("k_decode");
         k_recon_g<32><<<std::min<u32>((nmis + rw - 1) / rw, (u32)sms * 4), rw * 32, rslot * rw, s>>>(A, 3);

@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(1024) k_scan2(DecArgs A) {
 // ------------------------------------------------------------------------------------------
 // codebook and sections (container.py:221-271) + canonical decode tables
 #define PT_THREADS 1024
-#define DEC_TBITS 12
+#define DEC_TBITS 15
 
 // phase 0: codec 0, everything.  Codec 1 runs three phases around the run-length inversions:
 // 1 stops after the stored payload was taken (its job is filled), 2 checks the inverted payload
@@ -385,6 +385,8 @@ __global__ void __launch_bounds__(PT_THREADS) k_parse_tail(DecArgs A, int phase)
     __shared__ u64 s_kraft;
     __shared__ int s_maxlen;
     __shared__ u32 s_lc[64];
+    __shared__ u64 s_fc[64], s_end[64];
+    __shared__ u32 s_lb[64], s_pbase[64], s_pcnt[64 * (PT_THREADS / 32)];
     int tid = threadIdx.x;
     const u8* a = A.a;
     u64 len = A.len;
@@ -516,20 +518,20 @@ __global__ void __launch_bounds__(PT_THREADS) k_parse_tail(DecArgs A, int phase)
     __syncthreads();
     if (dev_failed(A.st)) return;
     if (A.codec == 1 && phase != 3) return;
-    // canonical order (length, symbol); symbols are strictly increasing already
-    int n = (int)nsym;
-    int np2 = 1;
-    while (np2 < n) np2 <<= 1;
-    u64* keys = np2 <= 8192 ? pt_dyn : A.sortkeys;
-    for (int i = tid; i < np2; i += PT_THREADS) {
-        if (i < n) {
-            const u8* ent = a + e0 + 5 * (u64)i;
-            keys[i] = ((u64)ent[4] << 32) | ld_le(ent, 4);
-        } else keys[i] = ~0ull;
+    // canonical order (length, symbol): symbols are strictly increasing already, so one stable
+    // counting pass by length (cb_radix_pass) orders them
+    const int n = (int)nsym;
+    const bool small = n <= 4096;
+    u64* keys = small ? pt_dyn : A.sortkeys;
+    u64* sorted = small ? pt_dyn + 4096 : A.sortkeys + A.cap;
+    for (int i = tid; i < n; i += PT_THREADS) {
+        const u8* ent = a + e0 + 5 * (u64)i;
+        keys[i] = ((u64)ent[4] << 32) | ld_le(ent, 4);
     }
     __syncthreads();
-    bitonic_sort_u64(keys, np2);
-    for (int i = tid; i < n; i += PT_THREADS) A.dsym[i] = (u32)(keys[i] & 0xffffffffu);
+    cb_radix_pass<6>(keys, sorted, n, 32, s_pcnt, s_pbase);
+    for (int i = tid; i < n; i += PT_THREADS) A.dsym[i] = (u32)(sorted[i] & 0xffffffffu);
+    const int T = min(s_maxlen, DEC_TBITS);
     if (tid == 0) {
         u64 code = 0;
         u32 idx = 0;
@@ -538,24 +540,27 @@ __global__ void __launch_bounds__(PT_THREADS) k_parse_tail(DecArgs A, int phase)
             A.first_code[l] = code;
             A.lcount[l] = s_lc[l];
             A.lbase[l] = idx;
+            s_fc[l] = code;
+            s_lb[l] = idx;
+            // end of the length-l codes in the T-bit window space (non-decreasing in l)
+            if (l <= T) s_end[l] = (code + s_lc[l]) << (T - l);
             code = (code + s_lc[l]) << 1;
             idx += s_lc[l];
         }
-        A.info[DI_T] = (u64)min(s_maxlen, DEC_TBITS);
+        A.info[DI_T] = (u64)T;
     }
     __syncthreads();
-    // decode LUT: T-bit window -> (symbol << 8 | length) for codes of length <= T
-    int T = min(s_maxlen, DEC_TBITS);
+    // decode LUT: T-bit window -> (symbol << 8 | length) for codes of length <= T (0: longer);
+    // the window's length is the first l with x < s_end[l] (binary search)
     for (int x = tid; x < (1 << T); x += PT_THREADS) {
-        u32 ent = 0;
-        for (int l = 1; l <= T; l++) {
-            u64 code = (u64)(x >> (T - l));
-            u64 d = code - A.first_code[l];
-            if (d < (u64)A.lcount[l]) {
-                ent = (A.dsym[A.lbase[l] + d] << 8) | (u32)l;
-                break;
-            }
+        int lo = 1, hi = T + 1;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if ((u64)x < s_end[mid]) hi = mid;
+            else lo = mid + 1;
         }
+        u32 ent = 0;
+        if (lo <= T) ent = (A.dsym[s_lb[lo] + (u32)((u64)(x >> (T - lo)) - s_fc[lo])] << 8) | (u32)lo;
         A.lut[x] = ent;
     }
 }
@@ -801,7 +806,7 @@ FTLZ_DEV void fail_block(const DecArgs& A, long long b, int kind, long long x, l
 // ------------------------------------------------------------------------------------------
 // K6: lane = block.  Warp = 32 consecutive blocks, decoded row by row in lockstep so that the
 // warp's rows (contiguous along z for blocks of one block-row) are written coalesced.
-#define DEC_WARPS 4
+#define DEC_WARPS 32   // one CTA per SM (64 registers x 1024 threads) sharing one decode table
 // stage words per warp: 32 rows of e plus up to 3 words of alignment shift per run, 16-byte
 // multiple
 __host__ __device__ inline size_t dec_stage_words(int e) { return ((size_t)32 * e + 96 + 3) & ~(size_t)3; }
@@ -809,7 +814,7 @@ __host__ __device__ inline size_t dec_stage_words(int e) { return ((size_t)32 * 
 
 
 template <bool FAULTS, bool FAST>
-__global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u32* list, int nlist) {
+__global__ void __launch_bounds__(DEC_WARPS * 32, 1) k_decode(DecArgs A, const u32* list, int nlist) {
     if (dev_failed(A.st)) return;
     extern __shared__ __align__(16) unsigned char dsm[];
     const Geom& g = A.g;
@@ -827,21 +832,9 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
     asm volatile("mov.u32 %0, %1;" : "=r"(lut_sa) : "r"(smem_u32(s_lut)));   // keep in a register
     const int lsh = 64 - T;
     float* stage = stage_all + (size_t)warp * dec_stage_words(g.e);
-    long long b;
-    bool valid;
     const bool mode_list = list != nullptr;
-    if (mode_list) {
-        // re-execution: lane over the given block list, decode only (bins to scratch); a short
-        // list spreads one block per warp (each block's decode is a serial chain: more warps,
-        // shorter wall time, and no other lane's rows to write back)
-        const long long wid = (long long)blockIdx.x * DEC_WARPS + warp;
-        long long idx = A.list_spread ? wid : wid * 32 + lane;
-        valid = idx < (long long)nlist && (!A.list_spread || lane == 0);
-        b = valid ? (long long)list[idx] : 0;
-    } else {
-        b = A.sb0 + ((long long)blockIdx.x * DEC_WARPS + warp) * 32 + lane;
-        valid = b < A.sb1;
-    }
+    // one task: lane = block b (valid: b exists); every lane returns at the end of the task
+    auto task = [&](const long long b, const bool valid) {
     const BlockInfo B = block_info(g, valid ? b : 0);
     const int kind = valid ? A.ind[b] : 0;
     const bool recon_here = valid && kind == 1 && !mode_list;
@@ -1094,6 +1087,27 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 8) k_decode(DecArgs A, const u
             A.mflag[b] = 1;
             A.mis_list[atomicAdd(&A.counters[DC_NMIS], 1u)] = (u32)b;
         }
+    }
+    };
+    if (mode_list) {
+        // re-execution: lane over the given block list, decode only (bins to scratch); a short
+        // list spreads one block per warp (each block's decode is a serial chain: more warps,
+        // shorter wall time, and no other lane's rows to write back)
+        const long long wid = (long long)blockIdx.x * (blockDim.x >> 5) + warp;
+        const long long idx = A.list_spread ? wid : wid * 32 + lane;
+        const bool valid = idx < (long long)nlist && (!A.list_spread || lane == 0);
+        task(valid ? (long long)list[idx] : 0, valid);
+        return;
+    }
+    // full path: warp task t = blocks sb0 + 32 t .. + 31.  One CTA per SM; CTA c takes the
+    // tasks [c ntask / grid, (c + 1) ntask / grid), so every SM decodes the same number of
+    // tasks (+-1): with one wave of CTAs of a few warps the SMs that received an extra CTA set
+    // the kernel time
+    const u32 ntask = (u32)((A.sb1 - A.sb0 + 31) / 32);
+    const u32 t0 = (u32)((u64)blockIdx.x * ntask / gridDim.x), t1 = (u32)((u64)(blockIdx.x + 1) * ntask / gridDim.x);
+    for (u32 t = t0 + warp; t < t1; t += blockDim.x >> 5) {
+        const long long b = A.sb0 + (long long)t * 32 + lane;
+        task(b < A.sb1 ? b : 0, b < A.sb1);
     }
 }
 
