@@ -1,6 +1,6 @@
 """Per-kernel device time (library profiler marks) of one BASELINE config through the C ABI.
 
-    python tools/config_profile.py c4 [c2 ...]      (GPU box)
+    python tools/config_profile.py c4 [c2 ...]      (GPU box; "c3:u" = FtConfig.unprotected())
 """
 import ctypes as C
 import os
@@ -21,7 +21,9 @@ L = _lib.load()
 ctx = _lib.context(0)
 fa0, _ = F.pipeline._faults_c([])
 cfg = F.FtConfig()
-for name in sys.argv[1:]:
+for arg in sys.argv[1:]:
+    name, _, flag = arg.partition(":")
+    cfg = F.FtConfig.unprotected() if flag == "u" else F.FtConfig()
     x = bench.load_field(name)
     mode, v = synth.CONFIGS[name]["eb"]
     nx, ny, nz = x.shape
@@ -44,4 +46,4 @@ for name in sys.argv[1:]:
         torch.cuda.synchronize()
     prof = _lib.profile_read(0)
     _lib.profile(False, 0)
-    print(name, {k: round(p[0], 3) for k, p in prof.items() if p[0] > 0.004})
+    print(arg, {k: round(p[0], 3) for k, p in prof.items() if p[0] > 0.004})
