@@ -875,7 +875,7 @@ struct DecLayout {
     size_t zero_end;
     size_t maps, smaps, sentry;
     size_t ind, recoff, unpc, bitlen, bofs, uofs, da, db, lor, mis;
-    size_t lut, first, lcount, lbase, dsym, sortkeys, lba, lbb;
+    size_t lut, lut12, first, lcount, lbase, dsym, sortkeys, lba, lbb;
     size_t bins, faults, ffirst, fblk, verdict, ckpt, plan, rlist;
     size_t jobs, payscr, sdcscr, rle;   // codec 1
     size_t pay_cap, sdc_cap, rle_bound;
@@ -915,6 +915,7 @@ static DecLayout dec_layout(const HostPlan& P, size_t len, int cap, int64_t nf, 
     L.lor = take(4 * nb);
     L.mis = take(4 * nb);
     L.lut = take(4 << DEC_TBITS);
+    L.lut12 = take(4 << DEC_TBITS_S);
     L.first = take(8 * 64);
     L.lcount = take(4 * 64);
     L.lbase = take(4 * 64);
@@ -999,7 +1000,7 @@ static DecArgs make_dec_args(const HostPlan& P, const DevPlan& D, const DecLayou
     A.st = (DevStatus*)(ws + L.result);
     A.counters = (u32*)(ws + L.result + 64);
     A.info = (u64*)(ws + L.result + 128);
-    A.lut = (u32*)(ws + L.lut); A.first_code = (u64*)(ws + L.first); A.lcount = (u32*)(ws + L.lcount);
+    A.lut = (u32*)(ws + L.lut); A.lut12 = (u32*)(ws + L.lut12); A.first_code = (u64*)(ws + L.first); A.lcount = (u32*)(ws + L.lcount);
     A.lbase = (u32*)(ws + L.lbase); A.dsym = (u32*)(ws + L.dsym); A.sortkeys = (u64*)(ws + L.sortkeys);
     A.bins = (u16*)(ws + L.bins);
     A.out = d_out;
@@ -1213,7 +1214,7 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         A.n_faults = 0;
         PF.mark("k_reexec_decode", s);
         {
-            const size_t rsm = ((size_t)4 << DEC_TBITS) + (size_t)RD_WARPS * RD_MAXW * 4;
+            const size_t rsm = ((size_t)4 << DEC_TBITS_S) + (size_t)RD_WARPS * RD_MAXW * 4;
             k_redecode<<<(nmis + RD_WARPS - 1) / RD_WARPS, RD_WARPS * 32, rsm, s>>>(A, (const u32*)(ws + L.mis),
                                                                                   (int)nmis);
         }
@@ -1285,7 +1286,7 @@ static int region_core(const HostPlan& P, const DevPlan& D, const uint8_t* d_a, 
     const int sms = num_sms();
     // lane per listed block, 4-warp CTAs so a short list still spreads over the SMs
     const int dnw = dec_warps((int)g.e, 4);
-    const size_t dec_smem = ((size_t)4 << DEC_TBITS) + (size_t)dnw * dec_stage_words((int)g.e) * 4;
+    const size_t dec_smem = ((size_t)4 << DEC_TBITS_S) + (size_t)dnw * dec_stage_words((int)g.e) * 4;
     const size_t rslot = al16((size_t)g.vmax * 8) + al16((size_t)g.vmax * 4) + al16(2 * (size_t)g.nvmax8);
     const int rw = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / rslot));
     k_decode<false, false><<<(n + dnw * 32 - 1) / (dnw * 32), dnw * 32, dec_smem, s>>>(A, A.region_list, (int)n);

@@ -24,7 +24,7 @@ namespace ftlz {
 
 enum {
     DI_TABLE_END = 0, DI_BOOK_OFF, DI_NSYM, DI_MAXLEN, DI_PAY_OFF, DI_PAY_LEN, DI_UNP_OFF,
-    DI_NUNP, DI_SDC_OFF, DI_HAS_SDC, DI_TOTAL_BITS, DI_NREG, DI_T, DI_PAY_STORED, DI_SDC_STORED, DI_COUNT
+    DI_NUNP, DI_SDC_OFF, DI_HAS_SDC, DI_TOTAL_BITS, DI_NREG, DI_T, DI_PAY_STORED, DI_SDC_STORED, DI_T12, DI_COUNT
 };
 enum { DC_NLOR = 0, DC_NMIS, DC_TICKET, DC_MINFAIL, DC_COUNT };
 
@@ -63,7 +63,8 @@ struct DecArgs {
     u32* counters;
     u64* info;
     DevStatus* st;
-    u32* lut;
+    u32* lut;     // 2^T entries, T = min(maxlen, DEC_TBITS): the full-path decoder (one CTA per SM)
+    u32* lut12;   // 2^T12 entries, T12 = min(maxlen, DEC_TBITS_S): list decodes with small CTAs
     u64* first_code;
     u32* lcount;
     u32* lbase;
@@ -373,6 +374,7 @@ __global__ void __launch_bounds__(1024) k_scan2(DecArgs A) {
 // codebook and sections (container.py:221-271) + canonical decode tables
 #define PT_THREADS 1024
 #define DEC_TBITS 15
+#define DEC_TBITS_S 12
 
 // phase 0: codec 0, everything.  Codec 1 runs three phases around the run-length inversions:
 // 1 stops after the stored payload was taken (its job is filled), 2 checks the inverted payload
@@ -385,7 +387,7 @@ __global__ void __launch_bounds__(PT_THREADS) k_parse_tail(DecArgs A, int phase)
     __shared__ u64 s_kraft;
     __shared__ int s_maxlen;
     __shared__ u32 s_lc[64];
-    __shared__ u64 s_fc[64], s_end[64];
+    __shared__ u64 s_fc[64];
     __shared__ u32 s_lb[64], s_pbase[64], s_pcnt[64 * (PT_THREADS / 32)];
     int tid = threadIdx.x;
     const u8* a = A.a;
@@ -542,27 +544,31 @@ __global__ void __launch_bounds__(PT_THREADS) k_parse_tail(DecArgs A, int phase)
             A.lbase[l] = idx;
             s_fc[l] = code;
             s_lb[l] = idx;
-            // end of the length-l codes in the T-bit window space (non-decreasing in l)
-            if (l <= T) s_end[l] = (code + s_lc[l]) << (T - l);
             code = (code + s_lc[l]) << 1;
             idx += s_lc[l];
         }
         A.info[DI_T] = (u64)T;
+        A.info[DI_T12] = (u64)min(s_maxlen, DEC_TBITS_S);
     }
     __syncthreads();
-    // decode LUT: T-bit window -> (symbol << 8 | length) for codes of length <= T (0: longer);
-    // the window's length is the first l with x < s_end[l] (binary search)
-    for (int x = tid; x < (1 << T); x += PT_THREADS) {
-        int lo = 1, hi = T + 1;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if ((u64)x < s_end[mid]) hi = mid;
-            else lo = mid + 1;
+    // decode LUTs: T-bit window -> (symbol << 8 | length) for codes of length <= T (0: longer);
+    // the window's length is the first l with x < end_l = (F_l + count_l) << (T - l), which is
+    // non-decreasing in l (binary search)
+    auto build = [&](u32* lut, int TT) {
+        for (int x = tid; x < (1 << TT); x += PT_THREADS) {
+            int lo = 1, hi = TT + 1;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if ((u64)x < ((s_fc[mid] + s_lc[mid]) << (TT - mid))) hi = mid;
+                else lo = mid + 1;
+            }
+            u32 ent = 0;
+            if (lo <= TT) ent = (A.dsym[s_lb[lo] + (u32)((u64)(x >> (TT - lo)) - s_fc[lo])] << 8) | (u32)lo;
+            lut[x] = ent;
         }
-        u32 ent = 0;
-        if (lo <= T) ent = (A.dsym[s_lb[lo] + (u32)((u64)(x >> (T - lo)) - s_fc[lo])] << 8) | (u32)lo;
-        A.lut[x] = ent;
-    }
+    };
+    build(A.lut, T);
+    build(A.lut12, min(s_maxlen, DEC_TBITS_S));
 }
 
 // ------------------------------------------------------------------------------------------
@@ -818,13 +824,16 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 1) k_decode(DecArgs A, const u
     if (dev_failed(A.st)) return;
     extern __shared__ __align__(16) unsigned char dsm[];
     const Geom& g = A.g;
-    const int T = (int)A.info[DI_T];
+    // list decodes (few blocks, small CTAs) stage the 12-bit table, the full path the 15-bit one
+    const bool tsmall = list != nullptr;
+    const int T = (int)A.info[tsmall ? DI_T12 : DI_T];
+    const u32* lut_g = tsmall ? A.lut12 : A.lut;
     u32* s_lut = (u32*)dsm;
-    float* stage_all = (float*)(dsm + ((size_t)4 << DEC_TBITS));
+    float* stage_all = (float*)(dsm + ((size_t)4 << (tsmall ? DEC_TBITS_S : DEC_TBITS)));
     __shared__ long long s_rbase[DEC_WARPS][32];
     __shared__ int s_rlen[DEC_WARPS][32], s_rbx[DEC_WARPS][32], s_rby[DEC_WARPS][32], s_rpad[DEC_WARPS][32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int x = tid; x < (1 << T); x += blockDim.x) s_lut[x] = A.lut[x];
+    for (int x = tid; x < (1 << T); x += blockDim.x) s_lut[x] = lut_g[x];
     if (tid < 64) { s_dec_first[tid] = A.first_code[tid]; s_dec_count[tid] = A.lcount[tid]; s_dec_base[tid] = A.lbase[tid]; }
     if (tid == 0) { s_dec_T = T; s_dec_maxlen = (int)A.info[DI_MAXLEN]; }
     __syncthreads();
@@ -1324,11 +1333,11 @@ __global__ void k_decomp_faults(DecArgs A, const u32* fblk, int nfb) {
 __global__ void __launch_bounds__(RD_WARPS * 32) k_redecode(DecArgs A, const u32* list, int n) {
     extern __shared__ __align__(16) unsigned char rsm[];
     u32* s_lut = (u32*)rsm;
-    u32* slice_all = s_lut + (1 << DEC_TBITS);
+    u32* slice_all = s_lut + (1 << DEC_TBITS_S);
     const Geom& g = A.g;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int T = (int)A.info[DI_T], maxlen = (int)A.info[DI_MAXLEN];
-    for (int x = tid; x < (1 << T); x += blockDim.x) s_lut[x] = A.lut[x];
+    const int T = (int)A.info[DI_T12], maxlen = (int)A.info[DI_MAXLEN];
+    for (int x = tid; x < (1 << T); x += blockDim.x) s_lut[x] = A.lut12[x];
     if (tid < 64) { s_dec_first[tid] = A.first_code[tid]; s_dec_count[tid] = A.lcount[tid]; s_dec_base[tid] = A.lbase[tid]; }
     __syncthreads();
     const int w = blockIdx.x * RD_WARPS + warp;
