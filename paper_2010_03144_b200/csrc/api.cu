@@ -23,6 +23,7 @@
 #include "encode.cu"
 #include "rle.cu"
 #include "decompress.cu"
+#include "decode_warp.cu"
 
 using namespace ftlz;
 
@@ -423,6 +424,7 @@ static int kernel_attrs_once() {
         setmax((const void*)k_recon_g<32>);
         setmax((const void*)k_recon_g<128>);
         setmax((const void*)k_redecode);
+        setmax((const void*)k_decode_pairs);
         if (cudaGetLastError() != cudaSuccess) rc = FTLZ_ERR_CUDA;
     });
     return rc;
@@ -875,7 +877,7 @@ struct DecLayout {
     size_t zero_end;
     size_t maps, smaps, sentry;
     size_t ind, recoff, unpc, bitlen, bofs, uofs, da, db, lor, mis;
-    size_t lut, lut12, first, lcount, lbase, dsym, sortkeys, lba, lbb;
+    size_t lut, lut12, lut2, first, lcount, lbase, dsym, sortkeys, lba, lbb;
     size_t bins, faults, ffirst, fblk, verdict, ckpt, plan, rlist;
     size_t jobs, payscr, sdcscr, rle;   // codec 1
     size_t pay_cap, sdc_cap, rle_bound;
@@ -916,6 +918,7 @@ static DecLayout dec_layout(const HostPlan& P, size_t len, int cap, int64_t nf, 
     L.mis = take(4 * nb);
     L.lut = take(4 << DEC_TBITS);
     L.lut12 = take(4 << DEC_TBITS_S);
+    L.lut2 = take(8 << PAIR_TBITS);
     L.first = take(8 * 64);
     L.lcount = take(4 * 64);
     L.lbase = take(4 * 64);
@@ -1000,7 +1003,7 @@ static DecArgs make_dec_args(const HostPlan& P, const DevPlan& D, const DecLayou
     A.st = (DevStatus*)(ws + L.result);
     A.counters = (u32*)(ws + L.result + 64);
     A.info = (u64*)(ws + L.result + 128);
-    A.lut = (u32*)(ws + L.lut); A.lut12 = (u32*)(ws + L.lut12); A.first_code = (u64*)(ws + L.first); A.lcount = (u32*)(ws + L.lcount);
+    A.lut = (u32*)(ws + L.lut); A.lut12 = (u32*)(ws + L.lut12); A.lut2 = (u64*)(ws + L.lut2); A.first_code = (u64*)(ws + L.first); A.lcount = (u32*)(ws + L.lcount);
     A.lbase = (u32*)(ws + L.lbase); A.dsym = (u32*)(ws + L.dsym); A.sortkeys = (u64*)(ws + L.sortkeys);
     A.bins = (u16*)(ws + L.bins);
     A.out = d_out;
@@ -1114,6 +1117,19 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     dec_occ = std::max(dec_occ, 1);
     size_t rslot = al16((size_t)g.vmax * 8) + al16((size_t)g.vmax * 4) + al16(2 * (size_t)g.nvmax8);
     int rw = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / rslot));
+    // warp-per-block decoder (decode_warp.cu) for 10^3 blocks when there are too few of them for
+    // k_decode's lane per block to fill the GPU (its 1000-code chain per block is then the
+    // critical path) and the archive averages at most 6 bits per point (its speculative pass
+    // works per bit); k_decode otherwise, which spends fewer instructions per code.  Measured on
+    // B200: c1 0.325 -> 0.037 ms, c2 0.263 -> 0.152 ms; c2 at 1e-4 (10.5 bits per point) and
+    // the 2-D c4 stay on k_decode.
+    const long long npts = g.nx * g.ny * g.nz;
+    const bool pairs = decode && g.e == DW_E && g.nx >= DW_E && 2 * g.nb < (long long)num_sms() * DEC_WARPS * 32 &&
+                       8 * (long long)len <= 6 * npts;
+    if (pairs) {
+        k_pair_lut<<<(1u << PAIR_TBITS) / 256, 256, 0, s>>>(A);
+        LCHK("k_pair_lut");
+    }
     if (decode) {
         // slabs: whole block layers (block ids are layer-major), so each slab's output is one
         // contiguous range of x-planes
@@ -1126,8 +1142,13 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
             A.sb1 = l1 * layer;
             // one CTA per SM (fewer when there are fewer 32-block tasks), tasks split evenly
             const unsigned dgrid = (unsigned)std::min<long long>((A.sb1 - A.sb0 + 31) / 32, (long long)sms * dec_occ);
+            const unsigned pgrid = (unsigned)std::min<long long>(A.sb1 - A.sb0, (long long)sms);
             PF.mark("k_decode", s);
-            k_decode<false, true><<<dgrid, dec_nw * 32, dec_smem, s>>>(A, nullptr, 0);
+            if (pairs) {
+                CK(cudaMemsetAsync(ws + L.result + 64 + 4 * DC_DTICKET, 0, 4, s));
+                k_decode_pairs<<<pgrid, DW_WARPS * 32, DP_SMEM, s>>>(A);
+            }
+            else k_decode<false, true><<<dgrid, dec_nw * 32, dec_smem, s>>>(A, nullptr, 0);
             LCHK("k_decode");
             if (!fblk.empty()) {
                 k_decomp_faults<<<(unsigned)((fblk.size() + 7) / 8), 256, 0, s>>>(A, (const u32*)(ws + L.fblk),

@@ -26,7 +26,7 @@ enum {
     DI_TABLE_END = 0, DI_BOOK_OFF, DI_NSYM, DI_MAXLEN, DI_PAY_OFF, DI_PAY_LEN, DI_UNP_OFF,
     DI_NUNP, DI_SDC_OFF, DI_HAS_SDC, DI_TOTAL_BITS, DI_NREG, DI_T, DI_PAY_STORED, DI_SDC_STORED, DI_T12, DI_COUNT
 };
-enum { DC_NLOR = 0, DC_NMIS, DC_TICKET, DC_MINFAIL, DC_COUNT };
+enum { DC_NLOR = 0, DC_NMIS, DC_TICKET, DC_MINFAIL, DC_DTICKET, DC_COUNT };
 
 struct DecArgs {
     Geom g;
@@ -65,6 +65,7 @@ struct DecArgs {
     DevStatus* st;
     u32* lut;     // 2^T entries, T = min(maxlen, DEC_TBITS): the full-path decoder (one CTA per SM)
     u32* lut12;   // 2^T12 entries, T12 = min(maxlen, DEC_TBITS_S): list decodes with small CTAs
+    u64* lut2;    // 2^14 two-symbol entries (decode_pairs.cu)
     u64* first_code;
     u32* lcount;
     u32* lbase;
