@@ -1080,17 +1080,17 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     }
     DecArgs A = make_dec_args(P, D, L, d_a, len, h, d_out, nf, ws);
     int sms = num_sms();
-    PF.mark("k_parse_maps", s);
-    k_parse_maps<<<sms * 8, 256, 0, s>>>(A);
-    LCHK("k_parse_maps");
-    PF.mark("k_parse_compose", s);
-    k_parse_compose<<<(unsigned)L.nsuper, PSUPER, 0, s>>>(A);
-    LCHK("k_parse_compose");
-    PF.mark("k_parse_top", s);
-    k_parse_top<<<1, 256, 0, s>>>(A);
-    LCHK("k_parse_top");
+    PF.mark("k_parse_chunks", s);
+    k_parse_chunks<<<(unsigned)L.nsuper, 1024, 0, s>>>(A);
+    LCHK("k_parse_chunks");
     PF.mark("k_parse_records", s);
-    k_parse_records<<<(unsigned)L.nsuper, PSUPER, 0, s>>>(A);
+    if (L.nsuper <= 256) {
+        // every CTA walks the (few) super-chunk maps before its own: no k_parse_top pass
+        k_parse_records<true><<<(unsigned)L.nsuper, PSUPER, 0, s>>>(A);
+    } else {
+        k_parse_top<<<1, 256, 0, s>>>(A);
+        k_parse_records<false><<<(unsigned)L.nsuper, PSUPER, 0, s>>>(A);
+    }
     LCHK("k_parse_records");
     PF.mark("k_scan2", s);
     k_scan2<<<(unsigned)((g.nb + 1023) / 1024), 1024, 0, s>>>(A);
@@ -1108,6 +1108,9 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         k_parse_tail<<<1, PT_THREADS, 8192 * 8, s>>>(A, 0);
     }
     LCHK("k_parse_tail");
+    PF.mark("k_dec_luts", s);
+    k_dec_luts<<<((1u << DEC_TBITS) + (1u << DEC_TBITS_S)) / 256, 256, 0, s>>>(A);
+    LCHK("k_dec_luts");
     // full-path k_decode: up to DEC_WARPS warps per CTA, fewer when the per-warp staging rows of
     // a large block edge would not fit in shared memory
     const int dec_nw = dec_warps((int)g.e, DEC_WARPS);
@@ -1115,7 +1118,7 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     int dec_occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&dec_occ, k_decode<false, true>, dec_nw * 32, dec_smem));
     dec_occ = std::max(dec_occ, 1);
-    size_t rslot = al16((size_t)g.vmax * 8) + al16((size_t)g.vmax * 4) + al16(2 * (size_t)g.nvmax8);
+    size_t rslot = al16(recon_slot_bytes(g.vmax, g.nvmax8));
     int rw = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / rslot));
     // warp-per-block decoder (decode_warp.cu) for 10^3 blocks when there are too few of them for
     // k_decode's lane per block to fill the GPU (its 1000-code chain per block is then the
@@ -1127,6 +1130,7 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     const bool pairs = decode && g.e == DW_E && g.nx >= DW_E && 2 * g.nb < (long long)num_sms() * DEC_WARPS * 32 &&
                        8 * (long long)len <= 6 * npts;
     if (pairs) {
+        PF.mark("k_pair_lut", s);
         k_pair_lut<<<(1u << PAIR_TBITS) / 256, 256, 0, s>>>(A);
         LCHK("k_pair_lut");
     }
@@ -1308,7 +1312,7 @@ static int region_core(const HostPlan& P, const DevPlan& D, const uint8_t* d_a, 
     // lane per listed block, 4-warp CTAs so a short list still spreads over the SMs
     const int dnw = dec_warps((int)g.e, 4);
     const size_t dec_smem = ((size_t)4 << DEC_TBITS_S) + (size_t)dnw * dec_stage_words((int)g.e) * 4;
-    const size_t rslot = al16((size_t)g.vmax * 8) + al16((size_t)g.vmax * 4) + al16(2 * (size_t)g.nvmax8);
+    const size_t rslot = al16(recon_slot_bytes(g.vmax, g.nvmax8));
     const int rw = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / rslot));
     k_decode<false, false><<<(n + dnw * 32 - 1) / (dnw * 32), dnw * 32, dec_smem, s>>>(A, A.region_list, (int)n);
     LCHK("k_decode");

@@ -2,13 +2,15 @@
 // pipeline.decompress (pipeline.py:645-723) for B200 (sm_100a).
 //
 // Kernel sequence:
-//   k_parse_maps     block table, speculative: for every 64-byte chunk and every entry phase
-//                    (0..24) walk the variable-length records (9 or 25 bytes) -> exit phase
-//   k_parse_compose  compose the chunk maps of 256-chunk super-chunks
-//   k_parse_top      one thread threads the super-chunk maps from phase 0
-//   k_parse_records  resolve every chunk's entry phase, emit per-block records, validate
+//   k_parse_chunks   block table, speculative: for every 64-byte chunk and every entry phase
+//                    (0..24) walk the variable-length records (9 or 25 bytes) -> exit phase;
+//                    the chunk maps of each 256-chunk super-chunk composed in the same pass
+//   k_parse_top      (> 256 super-chunks) threads the super-chunk maps from phase 0
+//   k_parse_records  resolve every chunk's entry phase (with <= 256 super-chunks each CTA walks
+//                    the super-chunk maps before its own), emit per-block records, validate
 //   k_scan2          exclusive scans of bit lengths and unpredictable counts (look-back)
-//   k_parse_tail     codebook + section validation, canonical decode tables
+//   k_parse_tail     codebook + section validation, canonical code tables
+//   k_dec_luts       the decode look-up tables, grid-wide
 //   k_decode         lane = block: Huffman decode; regression blocks reconstructed in the
 //                    same pass, staged in shared memory and written coalesced; Lorenzo bins to
 //                    scratch; decompressed-data checksum verification (K6)
@@ -111,27 +113,6 @@ FTLZ_DEV u64 stored_sum_dc(const DecArgs& A, long long b) {
 
 // ------------------------------------------------------------------------------------------
 // block table parse (container.py:212-219)
-__global__ void k_parse_maps(DecArgs A) {
-    long long total = A.nchunks * 25;
-    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        long long c = t / 25;
-        int ph = (int)(t - c * 25);
-        u64 s = 55 + (u64)c * PCHUNK, e = s + PCHUNK;
-        u64 pos = s + ph;
-        u32 cnt = 0;
-        bool stuck = false;
-        while (pos < e) {
-            if (pos >= A.len) { stuck = true; break; }
-            u8 ib = A.a[pos];
-            if (ib > 1) { stuck = true; break; }
-            pos += 9 + 16 * ib;
-            cnt++;
-        }
-        A.maps[t] = stuck ? STUCK : ((u32)(pos - e) | (cnt << 8));
-    }
-}
-
 // map value: exit phase (8 bits) | record count (24 bits); STUCK = error on this path.
 // Walking chunk a then chunk b from entry phase s: map_apply(a, b, s).  Composition is
 // associative, so the chunk and super-chunk walks are tree reductions / scans over maps.
@@ -197,19 +178,43 @@ FTLZ_DEV u32 walk2(const u32* m, int n, u32 st0, u64 base0, u64* entry, u32* gm,
     return s_exit;
 }
 
-// the super-chunk's map: in-place tree reduction of its chunk maps
-__global__ void __launch_bounds__(PSUPER) k_parse_compose(DecArgs A) {
+// chunk maps and their composition in one pass: the super-chunk's 256 chunks staged in shared
+// memory (a walk never reads past its own chunk), each thread the 25 phase walks of one chunk
+// (maps to global for k_parse_records), then the tree reduction to the super-chunk map
+__global__ void __launch_bounds__(1024) k_parse_chunks(DecArgs A) {
     __shared__ u32 m[PSUPER * 25];
-    long long sc = blockIdx.x;
-    long long c0 = sc * PSUPER;
-    int n = (int)min((long long)PSUPER, A.nchunks - c0);
-    for (int t = threadIdx.x; t < n * 25; t += blockDim.x) m[t] = A.maps[c0 * 25 + t];
+    __shared__ __align__(16) u8 sb[PSUPER * PCHUNK];
+    const long long sc = blockIdx.x, c0 = sc * PSUPER;
+    const int n = (int)min((long long)PSUPER, A.nchunks - c0);
+    const u64 base = 55 + (u64)c0 * PCHUNK;
+    // bytes past the archive read as 0xff: an indicator > 1 stops the walk like pos >= len
+    for (int t = threadIdx.x; t < n * PCHUNK; t += blockDim.x) sb[t] = base + t < A.len ? A.a[base + t] : (u8)0xff;
     __syncthreads();
+    // thread t: chunk t % 256, phases (t / 256) + 4 k
+    const int ci = (int)threadIdx.x % PSUPER;
+    if (ci < n) {
+        const u8* cb = sb + ci * PCHUNK;
+        for (int ph = (int)threadIdx.x / PSUPER; ph < 25; ph += 1024 / PSUPER) {
+            int pos = ph;
+            u32 cnt = 0;
+            bool stuck = false;
+            while (pos < PCHUNK) {
+                const u8 ib = cb[pos];
+                if (ib > 1) { stuck = true; break; }
+                pos += 9 + 16 * ib;
+                cnt++;
+            }
+            const u32 v = stuck ? STUCK : ((u32)(pos - PCHUNK) | (cnt << 8));
+            m[ci * 25 + ph] = v;
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n * 25; t += blockDim.x) A.maps[c0 * 25 + t] = m[t];
     for (int d = 1; d < n; d <<= 1) {
-        const int np = (n - d + 2 * d - 1) / (2 * d);   // pairs (i, i + d), i = 0, 2d, ... with i + d < n
+        const int np = (n - d + 2 * d - 1) / (2 * d);
         for (int t = threadIdx.x; t < np * 25; t += blockDim.x) {
-            const int pi = t / 25, s = t - pi * 25, i = pi * 2 * d;
-            m[i * 25 + s] = map_apply(m + i * 25, m + (i + d) * 25, s);
+            const int pi = t / 25, ss = t - pi * 25, i = pi * 2 * d;
+            m[i * 25 + ss] = map_apply(m + i * 25, m + (i + d) * 25, ss);
         }
         __syncthreads();
     }
@@ -236,6 +241,7 @@ __global__ void __launch_bounds__(256) k_parse_top(DecArgs A) {
     }
 }
 
+template <bool TOP>
 __global__ void __launch_bounds__(PSUPER) k_parse_records(DecArgs A) {
     __shared__ u32 m[PSUPER * 25];
     __shared__ u32 gm[WG * 25];
@@ -243,7 +249,21 @@ __global__ void __launch_bounds__(PSUPER) k_parse_records(DecArgs A) {
     long long sc = blockIdx.x;
     long long c0 = sc * PSUPER;
     int n = (int)min((long long)PSUPER, A.nchunks - c0);
-    u64 se = A.sentry[sc];
+    u64 se;
+    if (TOP) {
+        // (nsuper <= 256) this super-chunk's entry: the walk over the super-chunk maps before it
+        if (sc == 0) se = 0;
+        else {
+            for (int t = threadIdx.x; t < (int)sc * 25; t += blockDim.x) m[t] = A.smaps[t];
+            __syncthreads();
+            u64 nb0;
+            const u32 ex = walk2(m, (int)sc, 0, 0, entry, gm, ge, &nb0);
+            se = ex == STUCK ? ~0ull : (((u64)ex << 56) | nb0);
+            __syncthreads();
+        }
+    } else {
+        se = A.sentry[sc];
+    }
     if (se == ~0ull) return;
     for (int t = threadIdx.x; t < n * 25; t += blockDim.x) m[t] = A.maps[c0 * 25 + t];
     __syncthreads();
@@ -551,25 +571,35 @@ __global__ void __launch_bounds__(PT_THREADS) k_parse_tail(DecArgs A, int phase)
         A.info[DI_T] = (u64)T;
         A.info[DI_T12] = (u64)min(s_maxlen, DEC_TBITS_S);
     }
+    // (the decode LUTs are built by k_dec_luts over the whole grid)
+}
+
+// decode LUTs: T-bit window -> (symbol << 8 | length) for codes of length <= T (0: longer); the
+// window's length is the first l with x < end_l = (F_l + count_l) << (T - l), which is
+// non-decreasing in l (binary search).  Grid-wide: the 2^T-entry table of the full-path decoder,
+// then the 2^T12-entry table of the list decodes.
+__global__ void __launch_bounds__(256) k_dec_luts(DecArgs A) {
+    if (dev_failed(A.st)) return;
+    __shared__ u64 s_fc[64];
+    __shared__ u32 s_lc[64], s_lb[64];
+    if (threadIdx.x < 64) { s_fc[threadIdx.x] = A.first_code[threadIdx.x]; s_lc[threadIdx.x] = A.lcount[threadIdx.x]; s_lb[threadIdx.x] = A.lbase[threadIdx.x]; }
     __syncthreads();
-    // decode LUTs: T-bit window -> (symbol << 8 | length) for codes of length <= T (0: longer);
-    // the window's length is the first l with x < end_l = (F_l + count_l) << (T - l), which is
-    // non-decreasing in l (binary search)
-    auto build = [&](u32* lut, int TT) {
-        for (int x = tid; x < (1 << TT); x += PT_THREADS) {
-            int lo = 1, hi = TT + 1;
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if ((u64)x < ((s_fc[mid] + s_lc[mid]) << (TT - mid))) hi = mid;
-                else lo = mid + 1;
-            }
-            u32 ent = 0;
-            if (lo <= TT) ent = (A.dsym[s_lb[lo] + (u32)((u64)(x >> (TT - lo)) - s_fc[lo])] << 8) | (u32)lo;
-            lut[x] = ent;
+    const int T = (int)A.info[DI_T], T12 = (int)A.info[DI_T12];
+    const u32 n1 = 1u << T, n2 = 1u << T12;
+    for (u32 t = blockIdx.x * blockDim.x + threadIdx.x; t < n1 + n2; t += gridDim.x * blockDim.x) {
+        const int TT = t < n1 ? T : T12;
+        const u32 x = t < n1 ? t : t - n1;
+        int lo = 1, hi = TT + 1;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if ((u64)x < ((s_fc[mid] + s_lc[mid]) << (TT - mid))) hi = mid;
+            else lo = mid + 1;
         }
-    };
-    build(A.lut, T);
-    build(A.lut12, min(s_maxlen, DEC_TBITS_S));
+        u32 ent = 0;
+        if (lo <= TT) ent = (A.dsym[s_lb[lo] + (u32)((u64)(x >> (TT - lo)) - s_fc[lo])] << 8) | (u32)lo;
+        if (t < n1) A.lut[x] = ent;
+        else A.lut12[x] = ent;
+    }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1127,6 +1157,14 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 1) k_decode(DecArgs A, const u
 // mode 1: re-execution of mis_list (no faults); verdict in mflag (2 ok, 3 still mismatching).
 // G = threads per block group: 32 (a warp per block) or 128 (a CTA per block: the plane
 // wavefront then covers a whole plane per step, which shortens the per-block latency chain)
+// k_recon_g's per-group shared memory: float64 recon, float32 output, bins and, when it fits
+// (block edges up to 20), the wavefront plan
+__host__ __device__ inline bool recon_plan_fits(int vmax) { return vmax <= 8000; }
+__host__ __device__ inline size_t recon_slot_bytes(int vmax, int nvmax8) {
+    return (((size_t)vmax * 8 + 15) & ~(size_t)15) + (((size_t)vmax * 4 + 15) & ~(size_t)15) +
+           (((size_t)nvmax8 * 2 + 15) & ~(size_t)15) + (recon_plan_fits(vmax) ? (((size_t)vmax * 8 + 4 * 80 + 15) & ~(size_t)15) : 0);
+}
+
 template <int G>
 __global__ void __launch_bounds__(128) k_recon_g(DecArgs A, int mode) {
     if (dev_failed(A.st)) return;
@@ -1170,12 +1208,16 @@ __global__ void __launch_bounds__(128) k_recon_g(DecArgs A, int mode) {
         __syncthreads();
         return t;
     };
-    size_t slot_bytes = (((size_t)g.vmax * 8 + 15) & ~(size_t)15) + (((size_t)g.vmax * 4 + 15) & ~(size_t)15) +
-                        (((size_t)g.nvmax8 * 2 + 15) & ~(size_t)15);
+    const size_t slot_bytes = recon_slot_bytes(g.vmax, g.nvmax8);
     double* xd = (double*)(rsm + (size_t)warp * slot_bytes);
     float* v32 = (float*)(xd + g.vmax);
     u16* sb = (u16*)(rsm + (size_t)warp * slot_bytes + (((size_t)g.vmax * 8 + 15) & ~(size_t)15) +
                      (((size_t)g.vmax * 4 + 15) & ~(size_t)15));
+    // the wavefront plan of the group's current extent: (p << 32 | coords) in plane order, and the
+    // plane starts (staged once per extent: the plane loop then reads no global memory)
+    u64* wpc = (u64*)((unsigned char*)sb + (((size_t)g.nvmax8 * 2 + 15) & ~(size_t)15));
+    int* wpl = (int*)(wpc + g.vmax);
+    int plan_xid = -1;
     // mode 0: Lorenzo list; 1: re-execution list; 2: region list; 3: region re-execution
     const bool rgn = mode >= 2, reexec = mode & 1;
     u32 n = reexec ? A.counters[DC_NMIS] : (rgn ? A.n_region : A.counters[DC_NLOR]);
@@ -1216,9 +1258,15 @@ __global__ void __launch_bounds__(128) k_recon_g(DecArgs A, int mode) {
                 }
             }
         } else {
-            const u32* wave = A.wave + PL.wave_off;
-            const u32* wcrd = A.wcrd + PL.wave_off;
-            const u32* planes = A.planes + PL.plane_off;
+            const bool splan = recon_plan_fits(g.vmax);
+            if (splan && B.xid != plan_xid) {
+                const u32* wave = A.wave + PL.wave_off;
+                const u32* wcrd = A.wcrd + PL.wave_off;
+                const u32* planes = A.planes + PL.plane_off;
+                for (int q = lane; q < vol; q += G) wpc[q] = ((u64)__ldg(wave + q) << 32) | __ldg(wcrd + q);
+                for (int q = lane; q <= PL.nplanes; q += G) wpl[q] = (int)__ldg(planes + q);
+                plan_xid = B.xid;
+            }
             // the block's bins in shared memory (one coalesced burst instead of a dependent
             // global load per point and plane)
             {
@@ -1227,11 +1275,13 @@ __global__ void __launch_bounds__(128) k_recon_g(DecArgs A, int mode) {
                 for (int c = lane; c < nch; c += G) ((uint4*)sb)[c] = __ldg(src + c);
                 gsync();
             }
+            const u32* planes_g = A.planes + PL.plane_off;
             for (int s = 0; s < PL.nplanes; s++) {
-                int q0 = __ldg(planes + s), q1 = __ldg(planes + s + 1);
+                const int q0 = splan ? wpl[s] : (int)__ldg(planes_g + s), q1 = splan ? wpl[s + 1] : (int)__ldg(planes_g + s + 1);
                 for (int q = q0 + lane; q < q1; q += G) {
-                    int p = __ldg(wave + q);
-                    u32 c = __ldg(wcrd + q);
+                    const u64 pc = splan ? wpc[q] : (((u64)__ldg(A.wave + PL.wave_off + q) << 32) | __ldg(A.wcrd + PL.wave_off + q));
+                    const int p = (int)(pc >> 32);
+                    const u32 c = (u32)pc;
                     int i = c & 0xff, j = (c >> 8) & 0xff, k = c >> 16;
                     u32 bin = sb[p];
                     float v;
