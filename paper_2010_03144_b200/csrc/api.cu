@@ -662,6 +662,11 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     A.stage.use_tma = make_input_map(&tmap, d_in, g, K.stage);
     // regression blocks with 10-point z rows go to k_quant_reg10 (TMA tiles of 12-float rows)
     A.r10 = (g.e == 10 && A.stage.use_tma && A.stage.tz == 12) ? 1 : 0;
+    // the Lorenzo blocks ride in k_quant_reg10 when its tiles hold a block and its float64 buffer,
+    // for 3-D fields of many blocks (measured on B200: c3 -61 us, c2 -62 us; the 2-D c4 and the
+    // 343-block c1 are faster with k_quant_lor's own launch)
+    A.lor_fused = A.r10 && g.nx > 1 && g.nb >= 4096 && A.stage.tile_bytes >= 4 * g.vmax &&
+                  A.stage.tile_bytes + (int)(sizeof(R10Row) * R10_ROWS) >= 8 * g.vmax;
     A.r10_slot = K.r10_slot;
     A.lor_slot = (int)K.lor_slot;
     A.lor_list = (u32*)(ws + L.lor);
@@ -735,9 +740,11 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
         k_quant_reg<<<(unsigned)num_sms(), 32 * K.qr_warps, K.qr_smem, s>>>(A, tmap);
     }
     LCHK("k_quant_reg");
-    PF.mark("k_quant_lor", s);
-    k_quant_lor<<<num_sms() * 4, 32 * K.lor_warps, K.lor_smem, s>>>(A);
-    LCHK("k_quant_lor");
+    if (!A.lor_fused) {
+        PF.mark("k_quant_lor", s);
+        k_quant_lor<<<num_sms() * 4, 32 * K.lor_warps, K.lor_smem, s>>>(A);
+        LCHK("k_quant_lor");
+    }
     if (nf) PF.mark("k_fault_bins", s);
     if (nf) k_fault_bins<<<num_sms() * 4, 256, 0, s>>>(A, (u32*)(ws + L.fix), (u8*)(ws + L.fixed));
     LCHK("k_fault_bins");
@@ -1162,7 +1169,7 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
             PF.mark("k_recon_warp", s);
             // a CTA per Lorenzo block when a wavefront plane exceeds a warp (10^3 blocks: up to
             // 75 points), else a warp per block (1 x e x e planes: e points) without CTA barriers
-            if (lor_wave_max(g) > 32) k_recon_g<128><<<sms * 4, 128, rslot, s>>>(A, 0);
+            if (lor_wave_max(g) > 32) k_recon_g<128><<<sms * 8, 128, rslot, s>>>(A, 0);
             else k_recon_g<32><<<sms * 8, rw * 32, rslot * rw, s>>>(A, 0);
             LCHK("k_recon");
             if (nslab > 1 || (dl && dl->h_out)) {

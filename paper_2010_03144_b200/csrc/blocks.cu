@@ -116,6 +116,15 @@ FTLZ_DEV bool apply_input_faults(const CompArgs& A, long long b, float* tile, Ti
 // ==========================================================================================
 // emit pass (both predictors), warp = block, row-major order: unpredictable words, bins
 // checksum, warp-aggregated histogram, bins to the encoder layout
+// CTA-window histogram increment (window of HW bins from wlo), global beyond it
+template <int HW>
+FTLZ_DEV void hist_add_w(u32* hwin, u64* ghist, int wlo, int bin, u32 cnt) {
+    const unsigned o = (unsigned)(bin - wlo);
+    if (o < (unsigned)HW) atomicAdd(&hwin[o], cnt);
+    else atomicAdd(&ghist[bin], (u64)cnt);
+}
+
+template <int HW = HWIN>
 FTLZ_DEV void emit_block(const CompArgs& A, long long b, int vol, const u16* bins16, const float* tile,
                          TileWalk w0, u64 dcsum, int lane, u32* hwin, int wlo) {
     const Geom& g = A.g;
@@ -139,7 +148,7 @@ FTLZ_DEV void emit_block(const CompArgs& A, long long b, int vol, const u16* bin
             A.bins[bidx0 + (size_t)p] = (u16)bin;
         }
         unsigned peers = __match_any_sync(0xffffffffu, bin);
-        if (act && lane == __ffs(peers) - 1) hist_add(hwin, A.hist, wlo, bin, (u32)__popc(peers));
+        if (act && lane == __ffs(peers) - 1) hist_add_w<HW>(hwin, A.hist, wlo, bin, (u32)__popc(peers));
         w.advance(32);
     }
     dcsum = warp_sum_u64(dcsum);
@@ -233,6 +242,101 @@ FTLZ_DEV int quant_point(const QuantParams& Q, float x32, double p1, bool dup, F
 // ==========================================================================================
 // K2 (Lorenzo blocks): warp = block from the Lorenzo list; constant-(i+j+k) wavefront over a
 // float64 buffer of reconstructed values (pipeline.py:199-213, 410-438)
+// stage (c) of one Lorenzo block by a warp (pipeline.py:246-256,199-213): the block staged in xf
+// (cp.async), input faults / stage (a) verification, the plane wavefront with the float64
+// reconstruction buffer xd, the duplicated evaluation, then emit_block.  bins16 may be shared or
+// global memory.  HW: the caller's CTA histogram window.
+template <int HW>
+FTLZ_DEV void lor_block(const CompArgs& A, const QuantParams& Q, long long b, bool dup, float* xf, double* xd,
+                        u16* bins16, u32* hwin, int wlo, int lane) {
+    const Geom& g = A.g;
+    if (A.events[b] & 4) return;
+    BlockInfo B = block_info(g, b);
+    int vol = B.vol, bz = B.bz, byz = B.by * B.bz;
+    // stage the block (rows of bz floats) with cp.async
+    long long base = ((B.bi * g.e) * g.ny + B.bj * g.e) * g.nz + B.bk * g.e;
+    {
+        TileWalk w;
+        w.bx = B.bx; w.by = B.by; w.bz = bz; w.stride = 0; w.zoff = 0; w.bye = B.by;
+        w.set(lane);
+        for (int p = lane; p < vol; p += 32) {
+            cp_async4(xf + p, A.x + base + ((long long)w.i * g.ny + w.j) * g.nz + w.k);
+            w.advance(32);
+        }
+        cp_async_wait();
+    }
+    __syncwarp();
+    TileWalk w0;
+    w0.bx = B.bx; w0.by = B.by; w0.bz = bz; w0.stride = bz * B.by; w0.zoff = 0; w0.bye = B.by;
+    // block-local layout: addr = (i*by + j)*bz + k  (stride = bz per row with by rows)
+    w0.stride = bz;
+    if (!A.protect_input) apply_input_faults(A, b, xf, w0, lane);
+    else {
+        int r = tile_correct(xf, w0, vol, A.insum[b], A.inisum[b], lane);
+        if (r == 1 && lane == 0) { A.events[b] |= 1; atomicAdd(&A.counters[3], 1u); }
+        if (r == 2) {
+            if (lane == 0) { A.events[b] |= 4; atomicAdd(&A.counters[3], 1u); }
+            return;
+        }
+    }
+    __syncwarp();
+    const ExtPlan& PL = A.plans[B.xid];
+    const u32* crd = A.coords + PL.coord_off;
+    const u32* wave = A.wave + PL.wave_off;
+    const u32* wcrd = A.wcrd + PL.wave_off;
+    const u32* planes = A.planes + PL.plane_off;
+    bool mism = false;
+    u64 dcsum = 0;
+    const bool hasdup = block_has_dup(A, b);
+    const volatile double* vxd = xd;
+    for (int s = 0; s < PL.nplanes; s++) {
+        int q0 = __ldg(planes + s), q1 = __ldg(planes + s + 1);
+        for (int q = q0 + lane; q < q1; q += 32) {
+            int p = __ldg(wave + q);
+            u32 c = __ldg(wcrd + q);
+            int i = c & 0xff, j = (c >> 8) & 0xff, k = c >> 16;
+            // the 7-term Lorenzo sum (pipeline.py:246-256); evaluations 2 and 3 re-load
+            // every neighbour from the reconstruction buffer (volatile: no reuse)
+            auto lor = [&](const double* buf) {
+                const double d100 = i > 0 ? buf[p - byz] : 0.0;
+                const double d010 = j > 0 ? buf[p - bz] : 0.0;
+                const double d001 = k > 0 ? buf[p - 1] : 0.0;
+                const double d110 = (i > 0 && j > 0) ? buf[p - byz - bz] : 0.0;
+                const double d101 = (i > 0 && k > 0) ? buf[p - byz - 1] : 0.0;
+                const double d011 = (j > 0 && k > 0) ? buf[p - bz - 1] : 0.0;
+                const double d111 = (i > 0 && j > 0 && k > 0) ? buf[p - byz - bz - 1] : 0.0;
+                return __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(d100, d010), d001), -d110), -d101), -d011), d111);
+            };
+            auto lorv = [&]() {
+                const double d100 = i > 0 ? vxd[p - byz] : 0.0;
+                const double d010 = j > 0 ? vxd[p - bz] : 0.0;
+                const double d001 = k > 0 ? vxd[p - 1] : 0.0;
+                const double d110 = (i > 0 && j > 0) ? vxd[p - byz - bz] : 0.0;
+                const double d101 = (i > 0 && k > 0) ? vxd[p - byz - 1] : 0.0;
+                const double d011 = (j > 0 && k > 0) ? vxd[p - bz - 1] : 0.0;
+                const double d111 = (i > 0 && j > 0 && k > 0) ? vxd[p - byz - bz - 1] : 0.0;
+                return __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(d100, d010), d001), -d110), -d101), -d011), d111);
+            };
+            DupMask M;
+            if (hasdup) dup_masks(A, b, p, M);
+            else {
+#pragma unroll
+                for (int r = 0; r < 3; r++) M.p[r] = M.r[r] = 0ull;
+            }
+            float r32;
+            double back;
+            int bin = quant_point(Q, xf[p], lor(xd), dup, lorv, lorv, M, &r32, &mism, &back);
+            xd[p] = back;
+            bins16[p] = (u16)bin;
+            dcsum += __float_as_uint(r32);
+        }
+        __syncwarp();
+    }
+    if (__ballot_sync(0xffffffffu, mism) && lane == 0) atomicOr(&A.counters[1], 1u << (B.xid * 2 + 0));
+    emit_block<HW>(A, b, vol, bins16, xf, w0, dcsum, lane, hwin, wlo);
+    __syncwarp();
+}
+
 __global__ void __launch_bounds__(128) k_quant_lor(CompArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geom& g = A.g;
@@ -251,91 +355,7 @@ __global__ void __launch_bounds__(128) k_quant_lor(CompArgs A) {
     bool dup = A.dup_eval != 0;
     for (long long idx = (long long)blockIdx.x * nw + warp; idx < (long long)n; idx += (long long)gridDim.x * nw) {
         long long b = A.lor_list[idx];
-        if (A.events[b] & 4) continue;
-        BlockInfo B = block_info(g, b);
-        int vol = B.vol, bz = B.bz, byz = B.by * B.bz;
-        // stage the block (rows of bz floats) with cp.async
-        long long base = ((B.bi * g.e) * g.ny + B.bj * g.e) * g.nz + B.bk * g.e;
-        {
-            TileWalk w;
-            w.bx = B.bx; w.by = B.by; w.bz = bz; w.stride = 0; w.zoff = 0; w.bye = B.by;
-            w.set(lane);
-            for (int p = lane; p < vol; p += 32) {
-                cp_async4(xf + p, A.x + base + ((long long)w.i * g.ny + w.j) * g.nz + w.k);
-                w.advance(32);
-            }
-            cp_async_wait();
-        }
-        __syncwarp();
-        TileWalk w0;
-        w0.bx = B.bx; w0.by = B.by; w0.bz = bz; w0.stride = bz * B.by; w0.zoff = 0; w0.bye = B.by;
-        // block-local layout: addr = (i*by + j)*bz + k  (stride = bz per row with by rows)
-        w0.stride = bz;
-        if (!A.protect_input) apply_input_faults(A, b, xf, w0, lane);
-        else {
-            int r = tile_correct(xf, w0, vol, A.insum[b], A.inisum[b], lane);
-            if (r == 1 && lane == 0) { A.events[b] |= 1; atomicAdd(&A.counters[3], 1u); }
-            if (r == 2) {
-                if (lane == 0) { A.events[b] |= 4; atomicAdd(&A.counters[3], 1u); }
-                continue;
-            }
-        }
-        __syncwarp();
-        const ExtPlan& PL = A.plans[B.xid];
-        const u32* crd = A.coords + PL.coord_off;
-        const u32* wave = A.wave + PL.wave_off;
-        const u32* wcrd = A.wcrd + PL.wave_off;
-        const u32* planes = A.planes + PL.plane_off;
-        bool mism = false;
-        u64 dcsum = 0;
-        const bool hasdup = block_has_dup(A, b);
-        const volatile double* vxd = xd;
-        for (int s = 0; s < PL.nplanes; s++) {
-            int q0 = __ldg(planes + s), q1 = __ldg(planes + s + 1);
-            for (int q = q0 + lane; q < q1; q += 32) {
-                int p = __ldg(wave + q);
-                u32 c = __ldg(wcrd + q);
-                int i = c & 0xff, j = (c >> 8) & 0xff, k = c >> 16;
-                // the 7-term Lorenzo sum (pipeline.py:246-256); evaluations 2 and 3 re-load
-                // every neighbour from the reconstruction buffer (volatile: no reuse)
-                auto lor = [&](const double* buf) {
-                    const double d100 = i > 0 ? buf[p - byz] : 0.0;
-                    const double d010 = j > 0 ? buf[p - bz] : 0.0;
-                    const double d001 = k > 0 ? buf[p - 1] : 0.0;
-                    const double d110 = (i > 0 && j > 0) ? buf[p - byz - bz] : 0.0;
-                    const double d101 = (i > 0 && k > 0) ? buf[p - byz - 1] : 0.0;
-                    const double d011 = (j > 0 && k > 0) ? buf[p - bz - 1] : 0.0;
-                    const double d111 = (i > 0 && j > 0 && k > 0) ? buf[p - byz - bz - 1] : 0.0;
-                    return __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(d100, d010), d001), -d110), -d101), -d011), d111);
-                };
-                auto lorv = [&]() {
-                    const double d100 = i > 0 ? vxd[p - byz] : 0.0;
-                    const double d010 = j > 0 ? vxd[p - bz] : 0.0;
-                    const double d001 = k > 0 ? vxd[p - 1] : 0.0;
-                    const double d110 = (i > 0 && j > 0) ? vxd[p - byz - bz] : 0.0;
-                    const double d101 = (i > 0 && k > 0) ? vxd[p - byz - 1] : 0.0;
-                    const double d011 = (j > 0 && k > 0) ? vxd[p - bz - 1] : 0.0;
-                    const double d111 = (i > 0 && j > 0 && k > 0) ? vxd[p - byz - bz - 1] : 0.0;
-                    return __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(d100, d010), d001), -d110), -d101), -d011), d111);
-                };
-                DupMask M;
-                if (hasdup) dup_masks(A, b, p, M);
-                else {
-#pragma unroll
-                    for (int r = 0; r < 3; r++) M.p[r] = M.r[r] = 0ull;
-                }
-                float r32;
-                double back;
-                int bin = quant_point(Q, xf[p], lor(xd), dup, lorv, lorv, M, &r32, &mism, &back);
-                xd[p] = back;
-                bins16[p] = (u16)bin;
-                dcsum += __float_as_uint(r32);
-            }
-            __syncwarp();
-        }
-        if (__ballot_sync(0xffffffffu, mism) && lane == 0) atomicOr(&A.counters[1], 1u << (B.xid * 2 + 0));
-        emit_block(A, b, vol, bins16, xf, w0, dcsum, lane, hwin, wlo);
-        __syncwarp();
+        lor_block<HWIN>(A, Q, b, dup, xf, xd, bins16, hwin, wlo, lane);
     }
     __syncthreads();
     hist_flush(hwin, A.hist, wlo, A.cap);

@@ -286,9 +286,11 @@ __global__ void __maxnreg__(R10_MAXREG) k_quant_reg10(const __grid_constant__ Co
     WarpStager ws;
     ws.base = slot;
     ws.tbytes = S.tile_bytes;
-    u32* lh = (u32*)(slot + 2 * S.tile_bytes);   // R10_LHBYTES of lane counters
-    R10Row* rowtab = (R10Row*)((unsigned char*)lh + R10_LHBYTES);   // R10_ROWS rows of the current block
-    R10Pre* pre = (R10Pre*)(rowtab + R10_ROWS);          // operands of the current / next block
+    // slot: tile 0 | tile 1 | row table | lane counters | operands | mbarriers (tile 1 and the row
+    // table are contiguous: the float64 buffer of the Lorenzo phase)
+    R10Row* rowtab = (R10Row*)(slot + 2 * S.tile_bytes);   // R10_ROWS rows of the current block
+    u32* lh = (u32*)(rowtab + R10_ROWS);                  // R10_LHBYTES of lane counters
+    R10Pre* pre = (R10Pre*)((unsigned char*)lh + R10_LHBYTES);   // operands of the current / next block
     ws.bar = (u64*)(pre + 2);
     u32* hwin = (u32*)(smem + (size_t)nw * A.r10_slot);
     const int lhlo = A.center - R10_LH / 2, wlo = A.center - HWIN_REG / 2;
@@ -299,6 +301,25 @@ __global__ void __maxnreg__(R10_MAXREG) k_quant_reg10(const __grid_constant__ Co
     __syncthreads();
 
     const QuantParams Q = *A.qp;
+    if (A.lor_fused) {
+        // Lorenzo blocks first (k_quant_lor's work, a ticket per block): their long wavefront
+        // chains overlap the regression blocks of the other warps.  Tile 0 holds the block,
+        // tile 1 + the row table its float64 reconstruction, the bins go straight to global.
+        const u32 nl = A.counters[4];
+        for (;;) {
+            u32 t = 0;
+            if (lane == 0) t = atomicAdd(&A.counters[8], 1u);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            if (t >= nl) break;
+            const long long bl = A.lor_list[t];
+            lor_block<HWIN_REG>(A, Q, bl, A.dup_eval != 0, (float*)slot, (double*)(slot + S.tile_bytes),
+                                A.bins + bins_index(g, bl, 0), hwin, wlo, lane);
+            __syncwarp();
+        }
+        // generic-proxy writes to the tiles before the TMA (async proxy) writes them
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+    }
     // list positions: warp w of CTA c starts at c * nw + w, then takes tickets NW, NW + 1, ...
     // from counters[7] (dynamic: SMs that run ahead take more blocks).  The ticket is drawn two
     // blocks ahead by lane 4, the list entry it names arrives one block ahead; the next block's

@@ -274,3 +274,39 @@ def test_decompress_bytes_validates_caller_output_buffer():
     ro.flags.writeable = False
     with pytest.raises(ValueError):
         F.decompress_bytes(data, out=ro)
+
+
+# Lorenzo blocks of 3-D fields with >= 4096 blocks are quantized inside k_quant_reg10 (before its
+# regression blocks); every fault seam of that path against the oracle: input flips after the
+# checksum (protected and not), duplicated-evaluation flips in all three rounds, ragged edges
+@pytest.mark.parametrize("protect", [True, False])
+def test_lorenzo_blocks_inside_the_regression_kernel(protect):
+    dims = (171, 165, 158)   # 18 x 17 x 16 = 4896 blocks, ragged in every axis
+    x = _seeded("smooth", dims, seed=11)
+    nb = 18 * 17 * 16
+    rng = np.random.default_rng(3)
+    lor = sorted(int(b) for b in rng.choice(nb, 300, replace=False))
+    override = {b: 0 for b in lor}   # forced Lorenzo
+    faults = []
+    def vol(b):
+        bi, r = divmod(b, 17 * 16)
+        bj, bk = divmod(r, 16)
+        return min(10, 171 - 10 * bi) * min(10, 165 - 10 * bj) * min(10, 158 - 10 * bk)
+
+    for t, b in enumerate(lor[:60]):
+        el = int(rng.integers(0, vol(b)))
+        if t % 3 == 0:
+            faults.append(("input", b, el, int(rng.integers(0, 32))))
+        elif t % 3 == 1:
+            faults.append(("dup_predict", b, el, int(rng.integers(0, 192))))
+        else:
+            faults.append(("dup_reconstruct", b, el, int(rng.integers(0, 192))))
+    cfg = dict(protect_input=protect, duplicate_eval=True)
+    want, wrep = O.compress(x, "value_range_relative", 1e-3, cfg, faults=faults, override=override, threads=4)
+    stream, rep = F.compress(F.Field.from_array(x), F.ErrorBound("value_range_relative", 1e-3), F.FtConfig(**cfg),
+                             predictor_override=override, faults=faults)
+    assert F.serialize(stream) == want
+    rd = rep.to_dict()
+    for k in ("input_corrected", "dup_mismatch_resolved"):
+        assert rd[k] == wrep[k], k
+    assert rd["dup_mismatch_resolved"] and bool(rd["input_corrected"]) == protect
