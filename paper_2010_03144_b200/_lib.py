@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -144,25 +145,49 @@ def load():
         return L
 
 
-_ctx = {}
-last_parse = [None]   # token of the archive most recently validated on the device
+_tls = threading.local()
+
+
+class _Context:
+    """A library context (stream + device workspaces) owned by one thread; destroyed with the
+    thread's local storage."""
+
+    __slots__ = ("handle", "lib")
+
+    def __init__(self, device: int):
+        L = load()
+        h = L.ftlz_ctx_create(device)
+        if not h:
+            raise BackendUnavailable(
+                "no usable CUDA device for the B200 path: " + L.ftlz_last_error().decode(errors="replace"))
+        self.handle, self.lib = h, L
+
+    def __del__(self):
+        if not sys.is_finalizing():
+            self.lib.ftlz_ctx_destroy(self.handle)
 
 
 def context(device: int = 0):
-    """Process-wide library context for `device` (created on first use)."""
-    L = load()
-    c = _ctx.get(device)
+    """The calling thread's library context for `device` (created on first use).  Each thread
+    owns its stream and workspaces, so threads run compress / decompress calls concurrently
+    (e.g. one thread uploading and compressing the next field while another decompresses and
+    downloads the previous archive)."""
+    m = getattr(_tls, "ctx", None)
+    if m is None:
+        m = _tls.ctx = {}
+    c = m.get(device)
     if c is None:
-        with _lock:
-            c = _ctx.get(device)
-            if c is None:
-                c = L.ftlz_ctx_create(device)
-                if not c:
-                    raise BackendUnavailable(
-                        "no usable CUDA device for the B200 path: "
-                        + L.ftlz_last_error().decode(errors="replace"))
-                _ctx[device] = c
-    return c
+        c = m[device] = _Context(device)
+    return c.handle
+
+
+def last_parse() -> object:
+    """Token of the archive this thread's context most recently validated on the device."""
+    return getattr(_tls, "last_parse", None)
+
+
+def set_last_parse(token: object) -> None:
+    _tls.last_parse = token
 
 
 def last_error() -> str:

@@ -267,6 +267,6 @@ def parse(data: bytes) -> CompressedStream:
         raise_for_info(st, rep.info, data)
     stream = CompressedStream._from_archive(data, _sections_from_info(si))
     token = object()
-    _lib.last_parse[0] = token
+    _lib.set_last_parse(token)
     object.__setattr__(stream, "_parse_token", token)
     return stream

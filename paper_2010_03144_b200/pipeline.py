@@ -245,7 +245,7 @@ def _decompress_bytes(data, faults=None, out=None, reuse=None):
     fa, nf = _faults_c(faults)
     rb = _report_buf(int(hdr.block_count))
     st = L.ftlz_ctx_decompress_host(ctx, buf, len(data), out.ctypes.data, fa, nf,
-                                    1 if reuse is not None and reuse is _lib.last_parse[0] else 0,
+                                    1 if reuse is not None and reuse is _lib.last_parse() else 0,
                                     C.byref(rb.r))
     if st != 0:
         raise_for_info(st, rb.r.info, data)
@@ -288,7 +288,7 @@ def decompress_region(stream: CompressedStream, region, threads: int = 1) -> tup
     rb = _report_buf(int(hdr.block_count))
     reuse = stream.__dict__.get("_parse_token")
     st = L.ftlz_ctx_decompress_region_host(ctx, data, len(data), r6.ctypes.data, out.ctypes.data,
-                                           1 if reuse is not None and reuse is _lib.last_parse[0] else 0,
+                                           1 if reuse is not None and reuse is _lib.last_parse() else 0,
                                            C.byref(rb.r))
     if st != 0:
         raise_for_info(st, rb.r.info, data)

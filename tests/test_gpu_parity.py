@@ -310,3 +310,33 @@ def test_lorenzo_blocks_inside_the_regression_kernel(protect):
     for k in ("input_corrected", "dup_mismatch_resolved"):
         assert rd[k] == wrep[k], k
     assert rd["dup_mismatch_resolved"] and bool(rd["input_corrected"]) == protect
+
+
+def test_threads_run_the_pipeline_concurrently_on_their_own_contexts():
+    """Each thread owns a library context: compress and decompress calls from two threads at
+    once give the sequential results bit for bit."""
+    import threading
+
+    xs = [_seeded(k, (60, 70, 80), seed=s) for k, s in (("smooth", 1), ("lognormal", 2), ("noise", 3))]
+    want = [F.compress_bytes(x, "value_range_relative", 1e-3) for x in xs]
+    outs = [F.decompress_bytes(w) for w in want]
+    got, dec, errs = {}, {}, []
+
+    def work(i):
+        try:
+            for _ in range(3):
+                a = F.compress_bytes(xs[i], "value_range_relative", 1e-3)
+                got[i] = a
+                dec[i] = F.decompress_bytes(a)
+        except Exception as ex:   # noqa: BLE001
+            errs.append(ex)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(3)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for i in range(3):
+        assert got[i] == want[i]
+        np.testing.assert_array_equal(dec[i].view(np.uint32), outs[i].view(np.uint32))
