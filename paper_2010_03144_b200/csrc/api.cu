@@ -425,6 +425,7 @@ static int kernel_attrs_once() {
         setmax((const void*)k_recon_g<128>);
         setmax((const void*)k_redecode);
         setmax((const void*)k_decode_pairs);
+        setmax((const void*)k_fault_bins);
         if (cudaGetLastError() != cudaSuccess) rc = FTLZ_ERR_CUDA;
     });
     return rc;
@@ -539,13 +540,27 @@ extern "C" size_t ftlz_compress_bound(int64_t nx, int64_t ny, int64_t nz, const 
 }
 
 // faults sorted by block + per-block first index
-static void prep_faults(const ftlz_fault* faults, int64_t nf, int64_t nb, std::vector<ftlz_fault>& sorted,
-                        std::vector<int>& first) {
+// faults sorted by block (stable: a block's faults keep their order)
+static void prep_faults(const ftlz_fault* faults, int64_t nf, std::vector<ftlz_fault>& sorted) {
     sorted.assign(faults, faults + nf);
     std::stable_sort(sorted.begin(), sorted.end(), [](const ftlz_fault& a, const ftlz_fault& b) { return a.block < b.block; });
-    first.assign((size_t)nb, -1);
-    for (int64_t i = (int64_t)sorted.size() - 1; i >= 0; i--)
-        if (sorted[i].block >= 0 && sorted[i].block < nb) first[(size_t)sorted[i].block] = (int)i;
+}
+
+// first[b] = index of block b's first fault in the sorted list, -1 for blocks without one (the
+// nb-entry table is built on the device: only the fault list crosses PCIe)
+__global__ void k_fault_first(const ftlz_fault* f, int nf, long long nb, int* first) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nf) return;
+    const long long b = f[i].block;
+    if (b >= 0 && b < nb && (i == 0 || f[i - 1].block != b)) first[b] = i;
+}
+static int upload_faults(const std::vector<ftlz_fault>& fs, long long nb, unsigned char* d_faults, unsigned char* d_first,
+                         cudaStream_t s) {
+    const int nf = (int)fs.size();
+    CK(cudaMemcpyAsync(d_faults, fs.data(), sizeof(ftlz_fault) * (size_t)nf, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(d_first, 0xff, 4 * (size_t)nb, s));
+    k_fault_first<<<(nf + 255) / 256, 256, 0, s>>>((const ftlz_fault*)d_faults, nf, nb, (int*)d_first);
+    return cudaGetLastError() == cudaSuccess ? FTLZ_OK : set_err(FTLZ_ERR_CUDA, "k_fault_first");
 }
 
 static int validate_faults(const HostPlan& P, const ftlz_fault* f, int64_t nf) {
@@ -633,11 +648,9 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     else if ((rc = upload_plan(P, ws + L.plan, D, s, staging))) return rc;
     CK(cudaMemsetAsync(ws, 0, L.zero_end, s));
     std::vector<ftlz_fault> fs;
-    std::vector<int> ff;
     if (nf) {
-        prep_faults(faults, nf, g.nb, fs, ff);
-        CK(cudaMemcpyAsync(ws + L.faults, fs.data(), sizeof(ftlz_fault) * nf, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(ws + L.ffirst, ff.data(), 4 * (size_t)g.nb, cudaMemcpyHostToDevice, s));
+        prep_faults(faults, nf, fs);
+        if ((rc = upload_faults(fs, g.nb, ws + L.faults, ws + L.ffirst, s))) return rc;
     }
     if (ovr) CK(cudaMemcpyAsync(ws + L.ovr, ovr, (size_t)g.nb, cudaMemcpyHostToDevice, s));
 
@@ -746,7 +759,11 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
         LCHK("k_quant_lor");
     }
     if (nf) PF.mark("k_fault_bins", s);
-    if (nf) k_fault_bins<<<num_sms() * 4, 256, 0, s>>>(A, (u32*)(ws + L.fix), (u8*)(ws + L.fixed));
+    if (nf) {
+        const int fw = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)(200 * 1024) / (4 * (size_t)g.vmax)));
+        k_fault_bins<<<(unsigned)((nf + fw - 1) / fw), 32 * fw, 4 * (size_t)g.vmax * fw, s>>>(A, (u32*)(ws + L.fix),
+                                                                                             (u8*)(ws + L.fixed));
+    }
     LCHK("k_fault_bins");
     PF.mark("k_cb_bitmap", s);
     k_cb_bitmap<<<(unsigned)((cap + 255) / 256), 256, 0, s>>>(A, S.bm);
@@ -1074,14 +1091,12 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     CK(cudaMemsetAsync(ws, 0, L.zero_end, s));
     CK(cudaMemsetAsync(ws + L.result + 64 + 4 * DC_MINFAIL, 0xff, 4, s));
     std::vector<ftlz_fault> fs;
-    std::vector<int> ff;
     std::vector<u32> fblk;   // distinct blocks with decompressed-data faults
     if (nf) {
-        prep_faults(faults, nf, g.nb, fs, ff);
+        prep_faults(faults, nf, fs);
         for (const ftlz_fault& f : fs)
             if (f.target == FTLZ_FAULT_DECOMP && (fblk.empty() || fblk.back() != (u32)f.block)) fblk.push_back((u32)f.block);
-        CK(cudaMemcpyAsync(ws + L.faults, fs.data(), sizeof(ftlz_fault) * nf, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(ws + L.ffirst, ff.data(), 4 * (size_t)g.nb, cudaMemcpyHostToDevice, s));
+        if ((rc = upload_faults(fs, g.nb, ws + L.faults, ws + L.ffirst, s))) return rc;
         if (!fblk.empty())
             CK(cudaMemcpyAsync(ws + L.fblk, fblk.data(), 4 * fblk.size(), cudaMemcpyHostToDevice, s));
     }
@@ -1253,7 +1268,8 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         A.list_spread = 0;
         LCHK("k_decode");
         PF.mark("k_reexec_recon", s);
-        k_recon_g<32><<<(unsigned)std::min<u32>((nmis + rw - 1) / rw, sms * 4), rw * 32, rslot * rw, s>>>(A, 1);
+        if (lor_wave_max(g) > 32) k_recon_g<128><<<(unsigned)std::min<u32>(nmis, sms * 8), 128, rslot, s>>>(A, 1);
+        else k_recon_g<32><<<(unsigned)std::min<u32>((nmis + rw - 1) / rw, sms * 4), rw * 32, rslot * rw, s>>>(A, 1);
         LCHK("k_recon");
         PF.mark("k_reexec_verdict", s);
         k_reexec_verdict<<<(nmis + 255) / 256, 256, 0, s>>>(A, ws + L.verdict, nmis);
@@ -1323,7 +1339,8 @@ static int region_core(const HostPlan& P, const DevPlan& D, const uint8_t* d_a, 
     const int rw = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / rslot));
     k_decode<false, false><<<(n + dnw * 32 - 1) / (dnw * 32), dnw * 32, dec_smem, s>>>(A, A.region_list, (int)n);
     LCHK("k_decode");
-    k_recon_g<32><<<std::min<u32>((n + rw - 1) / rw, (u32)sms * 4), rw * 32, rslot * rw, s>>>(A, 2);
+    if (lor_wave_max(g) > 32) k_recon_g<128><<<std::min<u32>(n, (u32)sms * 8), 128, rslot, s>>>(A, 2);
+    else k_recon_g<32><<<std::min<u32>((n + rw - 1) / rw, (u32)sms * 4), rw * 32, rslot * rw, s>>>(A, 2);
     LCHK("k_recon");
     std::vector<unsigned char> df((size_t)g.nb), mf((size_t)g.nb);
     CK(cudaMemcpyAsync(df.data(), ws + L.dflag, (size_t)g.nb, cudaMemcpyDeviceToHost, s));
@@ -1350,7 +1367,8 @@ static int region_core(const HostPlan& P, const DevPlan& D, const uint8_t* d_a, 
         k_decode<false, true><<<(nmis + dnw * 32 - 1) / (dnw * 32), dnw * 32, dec_smem, s>>>(
             A, (const u32*)(ws + L.mis), (int)nmis);
         LCHK("k_decode");
-        k_recon_g<32><<<std::min<u32>((nmis + rw - 1) / rw, (u32)sms * 4), rw * 32, rslot * rw, s>>>(A, 3);
+        if (lor_wave_max(g) > 32) k_recon_g<128><<<std::min<u32>(nmis, (u32)sms * 8), 128, rslot, s>>>(A, 3);
+        else k_recon_g<32><<<std::min<u32>((nmis + rw - 1) / rw, (u32)sms * 4), rw * 32, rslot * rw, s>>>(A, 3);
         LCHK("k_recon");
         CK(cudaMemcpyAsync(mf.data(), ws + L.mflag, (size_t)g.nb, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));

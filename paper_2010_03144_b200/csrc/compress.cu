@@ -706,18 +706,23 @@ __global__ void __launch_bounds__(CB_THREADS) k_codebook(CompArgs A, CodebookScr
 // candidates tried in increasing j as the reference scans them), histogram fix-up
 __global__ void k_fault_bins(CompArgs A, u32* fix_scratch, u8* fixed) {
     if (dev_failed(A.st)) return;
+    extern __shared__ u32 fb_smem[];   // vmax words per warp: the block's bin words while verified
     const Geom& g = A.g;
     const int lane = threadIdx.x & 31;
+    u32* w = fb_smem + (size_t)(threadIdx.x >> 5) * g.vmax;
+    // a warp per block with faults: warp w takes fault w of the block-sorted list when it is its
+    // block's first
     const long long nwarp = (long long)gridDim.x * (blockDim.x >> 5);
-    for (long long b = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b < g.nb; b += nwarp) {
-        const int f0 = A.fault_first[b];
-        if (f0 < 0) continue;
+    for (long long fi = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; fi < A.n_faults; fi += nwarp) {
+        const long long b = A.faults[fi].block;
+        if (fi > 0 && A.faults[fi - 1].block == b) continue;
+        const int f0 = (int)fi;
         bool any = false;
         for (int f = f0; f < A.n_faults && A.faults[f].block == b; f++) any |= A.faults[f].target == FTLZ_FAULT_BINS;
         if (!any) continue;
         const BlockInfo B = block_info(g, b);
         const int vol = B.vol;
-        u32* w = fix_scratch + (size_t)b * g.vmax;
+        u32* wg = fix_scratch + (size_t)b * g.vmax;
         for (int p = lane; p < vol; p += 32) w[p] = A.bins[bins_index(g, b, p)];
         __syncwarp();
         if (lane == 0)
@@ -781,6 +786,7 @@ __global__ void k_fault_bins(CompArgs A, u32* fix_scratch, u8* fixed) {
             atomicAdd(&A.hist[orig], ~0ull);   // -1
             atomicAdd(&A.hist[w[p]], 1ull);
         }
+        for (int p = lane; p < vol; p += 32) wg[p] = w[p];   // the verified words for k_enc_*
         if (lane == 0) fixed[b] = 1;
     }
 }
