@@ -148,30 +148,42 @@ def load():
 _tls = threading.local()
 
 
-class _Context:
-    """A library context (stream + device workspaces) owned by one thread; destroyed with the
-    thread's local storage."""
+_free = []                 # (device, handle) of contexts released by finished threads
+_free_lock = threading.Lock()
 
-    __slots__ = ("handle", "lib")
+
+class _Context:
+    """A library context (stream + device workspaces) owned by one thread.  When the thread
+    ends, the context goes back to a process-wide pool and the next new thread takes it over
+    with its workspaces already allocated."""
+
+    __slots__ = ("handle", "device")
 
     def __init__(self, device: int):
+        self.device = device
+        with _free_lock:
+            for i, (d, h) in enumerate(_free):
+                if d == device:
+                    self.handle = _free.pop(i)[1]
+                    return
         L = load()
         h = L.ftlz_ctx_create(device)
         if not h:
             raise BackendUnavailable(
                 "no usable CUDA device for the B200 path: " + L.ftlz_last_error().decode(errors="replace"))
-        self.handle, self.lib = h, L
+        self.handle = h
 
     def __del__(self):
         if not sys.is_finalizing():
-            self.lib.ftlz_ctx_destroy(self.handle)
+            with _free_lock:
+                _free.append((self.device, self.handle))
 
 
 def context(device: int = 0):
-    """The calling thread's library context for `device` (created on first use).  Each thread
-    owns its stream and workspaces, so threads run compress / decompress calls concurrently
-    (e.g. one thread uploading and compressing the next field while another decompresses and
-    downloads the previous archive)."""
+    """The calling thread's library context for `device` (created on first use, or taken over
+    from a finished thread).  Each thread owns its stream and workspaces, so threads run
+    compress / decompress calls concurrently (e.g. one thread uploading and compressing the
+    next field while another decompresses and downloads the previous archive)."""
     m = getattr(_tls, "ctx", None)
     if m is None:
         m = _tls.ctx = {}
