@@ -424,7 +424,7 @@ static int kernel_attrs_once() {
         setmax((const void*)k_recon_g<32>);
         setmax((const void*)k_recon_g<128>);
         setmax((const void*)k_redecode);
-        setmax((const void*)k_decode_pairs);
+        setmax((const void*)k_decode_warp);
         setmax((const void*)k_fault_bins);
         if (cudaGetLastError() != cudaSuccess) rc = FTLZ_ERR_CUDA;
     });
@@ -1149,12 +1149,12 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     // B200: c1 0.325 -> 0.037 ms, c2 0.263 -> 0.152 ms; c2 at 1e-4 (10.5 bits per point) and
     // the 2-D c4 stay on k_decode.
     const long long npts = g.nx * g.ny * g.nz;
-    const bool pairs = decode && g.e == DW_E && g.nx >= DW_E && 2 * g.nb < (long long)num_sms() * DEC_WARPS * 32 &&
+    const bool warp_dec = decode && g.e == DW_E && g.nx >= DW_E && 2 * g.nb < (long long)num_sms() * DEC_WARPS * 32 &&
                        8 * (long long)len <= 6 * npts;
-    if (pairs) {
-        PF.mark("k_pair_lut", s);
-        k_pair_lut<<<(1u << PAIR_TBITS) / 256, 256, 0, s>>>(A);
-        LCHK("k_pair_lut");
+    if (warp_dec) {
+        PF.mark("k_dw_lut", s);
+        k_dw_lut<<<(1u << PAIR_TBITS) / 256, 256, 0, s>>>(A);
+        LCHK("k_dw_lut");
     }
     if (decode) {
         // slabs: whole block layers (block ids are layer-major), so each slab's output is one
@@ -1168,11 +1168,11 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
             A.sb1 = l1 * layer;
             // one CTA per SM (fewer when there are fewer 32-block tasks), tasks split evenly
             const unsigned dgrid = (unsigned)std::min<long long>((A.sb1 - A.sb0 + 31) / 32, (long long)sms * dec_occ);
-            const unsigned pgrid = (unsigned)std::min<long long>(A.sb1 - A.sb0, (long long)sms);
+            const unsigned wgrid = (unsigned)std::min<long long>(A.sb1 - A.sb0, (long long)sms);
             PF.mark("k_decode", s);
-            if (pairs) {
+            if (warp_dec) {
                 CK(cudaMemsetAsync(ws + L.result + 64 + 4 * DC_DTICKET, 0, 4, s));
-                k_decode_pairs<<<pgrid, DW_WARPS * 32, DP_SMEM, s>>>(A);
+                k_decode_warp<<<wgrid, DW_WARPS * 32, DW_SMEM, s>>>(A);
             }
             else k_decode<false, true><<<dgrid, dec_nw * 32, dec_smem, s>>>(A, nullptr, 0);
             LCHK("k_decode");

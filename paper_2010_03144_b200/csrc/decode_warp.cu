@@ -47,7 +47,7 @@ FTLZ_DEV u64 pair_look(const u32* lut, int T, u32 u, int nvalid) {
     return (e && (int)(e & 63u) <= nvalid) ? (u64)e : 0ull;
 }
 
-__global__ void __launch_bounds__(256) k_pair_lut(DecArgs A) {
+__global__ void __launch_bounds__(256) k_dw_lut(DecArgs A) {
     if (dev_failed(A.st)) return;
     const u32 v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= (1u << PAIR_TBITS)) return;
@@ -159,9 +159,9 @@ struct DwSlot {
     double ck[16];
     long long rowoff[DW_E * DW_E];   // output offset of each row of the block
 };
-#define DP_SMEM (((size_t)8 << PAIR_TBITS) + (size_t)DW_WARPS * sizeof(DwSlot))
+#define DW_SMEM (((size_t)8 << PAIR_TBITS) + (size_t)DW_WARPS * sizeof(DwSlot))
 
-__global__ void __launch_bounds__(DW_WARPS * 32, 1) k_decode_pairs(DecArgs A) {
+__global__ void __launch_bounds__(DW_WARPS * 32, 1) k_decode_warp(DecArgs A) {
     if (dev_failed(A.st)) return;
     extern __shared__ __align__(16) u64 ptab[];
     const Geom& g = A.g;
