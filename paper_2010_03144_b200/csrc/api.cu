@@ -24,6 +24,7 @@
 #include "rle.cu"
 #include "decompress.cu"
 #include "decode_warp.cu"
+#include "lor2d.cu"
 
 using namespace ftlz;
 
@@ -451,7 +452,7 @@ struct CompLayout {
     size_t coef, insum, inisum, ind, unpc, bsum, bisum, dcs, bitlen, lanepre, bitoff, regpre, unppre;
     size_t enc, qp, lbbits, lbreg, lbunp;
     size_t cb_keys, cb_syms, cb_w, cb_parent, cb_lens, cb_bm;
-    size_t bins, unp, fix, faults, ffirst, ovr, plan, lor, r10l, regxl;
+    size_t bins, unp, fix, faults, ffirst, ovr, plan, lor, defer, r10l, regxl;
     size_t cjobs, tarc, tarc_cap, rle, rle_bound;   // codec 1
     size_t total;
 };
@@ -510,6 +511,7 @@ static CompLayout comp_layout(const HostPlan& P, int cap, int64_t n_faults, int 
     L.ffirst = take(n_faults ? 4 * nb : 0);
     L.ovr = take(nb);
     L.lor = take(4 * nb);
+    L.defer = take(4 * nb);
     L.r10l = take(4 * nb);
     L.regxl = take(4 * nb);
     L.plan = take(P.bytes());
@@ -680,9 +682,12 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     // 343-block c1 are faster with k_quant_lor's own launch)
     A.lor_fused = A.r10 && g.nx > 1 && g.nb >= 4096 && A.stage.tile_bytes >= 4 * g.vmax &&
                   A.stage.tile_bytes + (int)(sizeof(R10Row) * R10_ROWS) >= 8 * g.vmax;
+    // 2-D fields of 10^2 blocks: k_quant_lor2d (a lane per Lorenzo block)
+    A.lor2d = !A.lor_fused && g.nx == 1 && g.e == L2_E;
     A.r10_slot = K.r10_slot;
     A.lor_slot = (int)K.lor_slot;
     A.lor_list = (u32*)(ws + L.lor);
+    A.defer_list = (u32*)(ws + L.defer);
     A.r10_list = (u32*)(ws + L.r10l);
     A.regx_list = (u32*)(ws + L.regxl);
     A.n_faults = (int)nf;
@@ -754,6 +759,12 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     }
     LCHK("k_quant_reg");
     if (!A.lor_fused) {
+        if (A.lor2d) {
+            // 2-D fields: a lane per Lorenzo block; k_quant_lor then takes the deferred ones
+            PF.mark("k_quant_lor2d", s);
+            k_quant_lor2d<<<(unsigned)std::min<long long>((g.nb + 127) / 128, (long long)num_sms() * 16), 128, 0, s>>>(A);
+            LCHK("k_quant_lor2d");
+        }
         PF.mark("k_quant_lor", s);
         k_quant_lor<<<num_sms() * 4, 32 * K.lor_warps, K.lor_smem, s>>>(A);
         LCHK("k_quant_lor");
@@ -1184,7 +1195,8 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
             PF.mark("k_recon_warp", s);
             // a CTA per Lorenzo block when a wavefront plane exceeds a warp (10^3 blocks: up to
             // 75 points), else a warp per block (1 x e x e planes: e points) without CTA barriers
-            if (lor_wave_max(g) > 32) k_recon_g<128><<<sms * 8, 128, rslot, s>>>(A, 0);
+            if (g.nx == 1 && g.e == L2_E) k_recon_lor2d<<<(unsigned)std::min<long long>((g.nb + 127) / 128, (long long)sms * 16), 128, 0, s>>>(A);
+            else if (lor_wave_max(g) > 32) k_recon_g<128><<<sms * 8, 128, rslot, s>>>(A, 0);
             else k_recon_g<32><<<sms * 8, rw * 32, rslot * rw, s>>>(A, 0);
             LCHK("k_recon");
             if (nslab > 1 || (dl && dl->h_out)) {

@@ -348,13 +348,16 @@ __global__ void __launch_bounds__(128) k_quant_lor(CompArgs A) {
     u16* bins16 = (u16*)(xd + g.vmax);
     u32* hwin = (u32*)(smem + (size_t)nw * A.lor_slot);
     const int wlo = A.center - HWIN / 2;
+    // after k_quant_lor2d: only the blocks it deferred (faults, failed stage (a) checksum)
+    const u32 n = A.lor2d ? A.counters[9] : A.counters[4];
+    const u32* list = A.lor2d ? A.defer_list : A.lor_list;
+    if (n == 0) return;
     for (int t = threadIdx.x; t < HWIN; t += blockDim.x) hwin[t] = 0;
     __syncthreads();
     const QuantParams Q = *A.qp;
-    u32 n = A.counters[4];
     bool dup = A.dup_eval != 0;
     for (long long idx = (long long)blockIdx.x * nw + warp; idx < (long long)n; idx += (long long)gridDim.x * nw) {
-        long long b = A.lor_list[idx];
+        long long b = list[idx];
         lor_block<HWIN>(A, Q, b, dup, xf, xd, bins16, hwin, wlo, lane);
     }
     __syncthreads();

@@ -36,6 +36,8 @@ struct CompArgs {
     int lor_slot;             // smem bytes per warp in k_quant_lor
     int r10, r10_slot;        // k_quant_reg10 active (edge 10, TMA tiles of 12-float rows); smem per warp
     int lor_fused, pad_lf;    // k_quant_reg10 also quantizes the Lorenzo blocks (no k_quant_lor launch)
+    int lor2d, pad_l2;        // 2-D Lorenzo blocks by k_quant_lor2d; k_quant_lor takes defer_list (counters[9])
+    u32* defer_list;
     u32* lor_list;            // Lorenzo blocks (appended by k_prep)
     u32* r10_list;            // regression blocks for k_quant_reg10 (k_reglist; counters[5] entries)
     u32* regx_list;           // the other regression blocks, for k_quant_reg (counters[6] entries)

@@ -340,3 +340,43 @@ def test_threads_run_the_pipeline_concurrently_on_their_own_contexts():
     for i in range(3):
         assert got[i] == want[i]
         np.testing.assert_array_equal(dec[i].view(np.uint32), outs[i].view(np.uint32))
+
+
+# Lorenzo blocks of 2-D fields (1 x by x bz) are quantized and reconstructed a lane per block
+# (lor2d.cu); blocks with injected faults or a failed stage (a) checksum go to the warp kernel.
+@pytest.mark.parametrize("protect", [True, False])
+def test_two_d_lorenzo_lane_kernels_against_oracle(protect):
+    dims = (1, 233, 171)   # 24 x 18 blocks, ragged in y and z
+    x = _seeded("smooth", dims, seed=21)
+    nb = 24 * 18
+    rng = np.random.default_rng(5)
+    lor = sorted(int(b) for b in rng.choice(nb, 200, replace=False))
+    override = {b: 0 for b in lor}
+
+    def vol(b):
+        bj, bk = divmod(b, 18)
+        return min(10, 233 - 10 * bj) * min(10, 171 - 10 * bk)
+
+    faults = []
+    for t, b in enumerate(lor[:30]):
+        el = int(rng.integers(0, vol(b)))
+        kind = ("input", "dup_predict", "dup_reconstruct")[t % 3]
+        faults.append((kind, b, el, int(rng.integers(0, 32 if kind == "input" else 192))))
+    cfg = dict(protect_input=protect, duplicate_eval=True)
+    want, wrep = O.compress(x, "value_range_relative", 1e-3, cfg, faults=faults, override=override, threads=4)
+    stream, rep = F.compress(F.Field.from_array(x), F.ErrorBound("value_range_relative", 1e-3), F.FtConfig(**cfg),
+                             predictor_override=override, faults=faults)
+    data = F.serialize(stream)
+    assert data == want
+    rd = rep.to_dict()
+    for k in ("input_corrected", "dup_mismatch_resolved"):
+        assert rd[k] == wrep[k], k
+    # decompress, clean and with decompressed-data flips on Lorenzo blocks
+    ref, _ = O.decompress(want, threads=4)
+    out = F.decompress_bytes(data)
+    np.testing.assert_array_equal(out.view(np.uint32), ref.view(np.uint32))
+    dfaults = [("decomp", b, int(rng.integers(0, vol(b))), int(rng.integers(0, 32))) for b in lor[30:60]]
+    o2, r2 = F.decompress(F.parse(data), faults=dfaults)
+    ro, rr = O.decompress(want, faults=dfaults, threads=4)
+    assert r2.to_dict()["decomp_block_reexecuted"] == rr["decomp_block_reexecuted"]
+    np.testing.assert_array_equal(o2.values.view(np.uint32), ro.view(np.uint32))
