@@ -770,6 +770,12 @@ FTLZ_DEV void fr_refill(FastReader& R) {
 // one symbol with at least 12 bits in the window; a code longer than the table is searched in
 // the window when the window holds maxlen bits (then topped up to >= 32 bits), else after a
 // re-seek from the absolute position (>= 33 bits); returns false outside the code space
+struct FrSlow {
+    FastReader R;
+    u32 sym, ok;
+};
+__device__ __noinline__ FrSlow fr_symbol_slow(FastReader R, const u32* dsym);
+
 FTLZ_DEV bool fr_symbol(FastReader& R, u32 lut_sa, int lsh, const u32* dsym, u32& sym) {
     const u32 ent = lds_u32(lut_sa + 4u * (u32)(R.win >> lsh));
     if (ent) {
@@ -779,6 +785,19 @@ FTLZ_DEV bool fr_symbol(FastReader& R, u32 lut_sa, int lsh, const u32* dsym, u32
         R.have -= l;
         return true;
     }
+    // a code longer than the table (rare): out of line, so the many inlined copies of the
+    // symbol step stay small
+    const FrSlow o = fr_symbol_slow(R, dsym);
+    R = o.R;
+    sym = o.sym;
+    return o.ok != 0;
+}
+
+__device__ __noinline__ FrSlow fr_symbol_slow(FastReader R, const u32* dsym) {
+    FrSlow o;
+    o.ok = 0;
+    o.sym = 0;
+    u32& sym = o.sym;
     const int T = s_dec_T, maxlen = s_dec_maxlen;
     if (R.have >= maxlen) {
         // every code fits in the window's valid bits: search there, then top the window up
@@ -789,10 +808,13 @@ FTLZ_DEV bool fr_symbol(FastReader& R, u32 lut_sa, int lsh, const u32* dsym, u32
                 R.win <<= l;
                 R.have -= l;
                 fr_refill(R);
-                return true;
+                o.ok = 1;
+                o.R = R;
+                return o;
             }
         }
-        return false;
+        o.R = R;
+        return o;
     }
     const u32 cur = fr_pos(R);
     const u32 n = cur >> 5;
@@ -806,10 +828,13 @@ FTLZ_DEV bool fr_symbol(FastReader& R, u32 lut_sa, int lsh, const u32* dsym, u32
         if (d < (u64)s_dec_count[l]) {
             sym = dsym[s_dec_base[l] + d];
             fr_seek(R, cur + l);
-            return true;
+            o.ok = 1;
+            o.R = R;
+            return o;
         }
     }
-    return false;
+    o.R = R;
+    return o;
 }
 
 #define DF_PENDING 0xffu   // dflag: failed on the fast path, kind not yet classified
