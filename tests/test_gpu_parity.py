@@ -380,3 +380,38 @@ def test_two_d_lorenzo_lane_kernels_against_oracle(protect):
     ro, rr = O.decompress(want, faults=dfaults, threads=4)
     assert r2.to_dict()["decomp_block_reexecuted"] == rr["decomp_block_reexecuted"]
     np.testing.assert_array_equal(o2.values.view(np.uint32), ro.view(np.uint32))
+
+
+def test_warp_decoder_oversized_slices_and_reexecution():
+    """Small smooth field (the warp-per-block decoder) with a few noisy blocks whose slices exceed
+    its shared-memory staging (decoded by one lane from global memory); decompressed-data flips on
+    those blocks are re-executed from the checkpoints that path records."""
+    x = _seeded("smooth", (60, 60, 60), seed=31).astype(np.float64)
+    rng = np.random.default_rng(9)
+    x[0:10, 0:10, 0:20] += rng.standard_normal((10, 10, 20)) * 10.0   # blocks 0 and 1
+    x[30:40, 50:60, 10:20] += rng.standard_normal((10, 10, 10)) * 10.0
+    x = x.astype(np.float32)
+    data = F.compress_bytes(x, "absolute", 1e-3)   # the noisy blocks: ~17.7 bits per point
+    want, _ = O.compress(x, "absolute", 1e-3, threads=4)
+    assert data == want
+    assert len(data) * 8 <= 6 * x.size   # the field as a whole stays on the warp decoder
+    ref, _ = O.decompress(want, threads=4)
+    np.testing.assert_array_equal(F.decompress_bytes(data).view(np.uint32), ref.view(np.uint32))
+    noisy = [0, 1, (3 * 6 + 5) * 6 + 1]
+    faults = [("decomp", b, int(rng.integers(0, 1000)), int(rng.integers(0, 32))) for b in noisy]
+    out, rep = F.decompress(F.parse(data), faults=faults)
+    ro, rr = O.decompress(want, faults=faults, threads=4)
+    assert rep.to_dict()["decomp_block_reexecuted"] == rr["decomp_block_reexecuted"] == sorted(noisy)
+    np.testing.assert_array_equal(out.values.view(np.uint32), ro.view(np.uint32))
+
+
+def test_block_table_of_more_than_256_super_chunks():
+    """A block table longer than 256 super-chunks (4 MiB) takes the k_parse_top walk."""
+    x = _seeded("lognormal", (170, 170, 150), seed=41)   # 541,875 blocks, a 4.9 MB table
+    cfg = {"block_edge": 2}
+    want, _ = O.compress(x, "value_range_relative", 1e-3, cfg, threads=8)
+    got = F.compress_bytes(x, "value_range_relative", 1e-3, F.FtConfig(block_edge=2))
+    assert got == want
+    assert len(F.parse(got).records) == 85 * 85 * 75
+    ref, _ = O.decompress(want, threads=8)
+    np.testing.assert_array_equal(F.decompress_bytes(got).view(np.uint32), ref.view(np.uint32))
