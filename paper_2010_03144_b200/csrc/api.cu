@@ -1196,7 +1196,7 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
             // a CTA per Lorenzo block when a wavefront plane exceeds a warp (10^3 blocks: up to
             // 75 points), else a warp per block (1 x e x e planes: e points) without CTA barriers
             if (g.nx == 1 && g.e == L2_E) k_recon_lor2d<<<(unsigned)std::min<long long>((g.nb + 127) / 128, (long long)sms * 16), 128, 0, s>>>(A);
-            else if (lor_wave_max(g) > 32) k_recon_g<128><<<sms * 8, 128, rslot, s>>>(A, 0);
+            else if (lor_wave_max(g) > 32) k_recon_g<128><<<sms * 12, 128, rslot, s>>>(A, 0);
             else k_recon_g<32><<<sms * 8, rw * 32, rslot * rw, s>>>(A, 0);
             LCHK("k_recon");
             if (nslab > 1 || (dl && dl->h_out)) {

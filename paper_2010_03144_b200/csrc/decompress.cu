@@ -1187,7 +1187,7 @@ __global__ void __launch_bounds__(DEC_WARPS * 32, 1) k_decode(DecArgs A, const u
 __host__ __device__ inline bool recon_plan_fits(int vmax) { return vmax <= 8000; }
 __host__ __device__ inline size_t recon_slot_bytes(int vmax, int nvmax8) {
     return (((size_t)vmax * 8 + 15) & ~(size_t)15) + (((size_t)vmax * 4 + 15) & ~(size_t)15) +
-           (((size_t)nvmax8 * 2 + 15) & ~(size_t)15) + (recon_plan_fits(vmax) ? (((size_t)vmax * 8 + 4 * 80 + 15) & ~(size_t)15) : 0);
+           (((size_t)nvmax8 * 2 + 15) & ~(size_t)15) + (recon_plan_fits(vmax) ? (((size_t)vmax * 4 + 4 * 80 + 15) & ~(size_t)15) : 0);
 }
 
 template <int G>
@@ -1240,7 +1240,7 @@ __global__ void __launch_bounds__(128) k_recon_g(DecArgs A, int mode) {
                      (((size_t)g.vmax * 4 + 15) & ~(size_t)15));
     // the wavefront plan of the group's current extent: (p << 32 | coords) in plane order, and the
     // plane starts (staged once per extent: the plane loop then reads no global memory)
-    u64* wpc = (u64*)((unsigned char*)sb + (((size_t)g.nvmax8 * 2 + 15) & ~(size_t)15));
+    u32* wpc = (u32*)((unsigned char*)sb + (((size_t)g.nvmax8 * 2 + 15) & ~(size_t)15));   // p | i << 13 | j << 18 | k << 23
     int* wpl = (int*)(wpc + g.vmax);
     int plan_xid = -1;
     // mode 0: Lorenzo list; 1: re-execution list; 2: region list; 3: region re-execution
@@ -1288,7 +1288,10 @@ __global__ void __launch_bounds__(128) k_recon_g(DecArgs A, int mode) {
                 const u32* wave = A.wave + PL.wave_off;
                 const u32* wcrd = A.wcrd + PL.wave_off;
                 const u32* planes = A.planes + PL.plane_off;
-                for (int q = lane; q < vol; q += G) wpc[q] = ((u64)__ldg(wave + q) << 32) | __ldg(wcrd + q);
+                for (int q = lane; q < vol; q += G) {
+                    const u32 c = __ldg(wcrd + q);
+                    wpc[q] = __ldg(wave + q) | ((c & 0xffu) << 13) | (((c >> 8) & 0xffu) << 18) | ((c >> 16) << 23);
+                }
                 for (int q = lane; q <= PL.nplanes; q += G) wpl[q] = (int)__ldg(planes + q);
                 plan_xid = B.xid;
             }
@@ -1304,10 +1307,15 @@ __global__ void __launch_bounds__(128) k_recon_g(DecArgs A, int mode) {
             for (int s = 0; s < PL.nplanes; s++) {
                 const int q0 = splan ? wpl[s] : (int)__ldg(planes_g + s), q1 = splan ? wpl[s + 1] : (int)__ldg(planes_g + s + 1);
                 for (int q = q0 + lane; q < q1; q += G) {
-                    const u64 pc = splan ? wpc[q] : (((u64)__ldg(A.wave + PL.wave_off + q) << 32) | __ldg(A.wcrd + PL.wave_off + q));
-                    const int p = (int)(pc >> 32);
-                    const u32 c = (u32)pc;
-                    int i = c & 0xff, j = (c >> 8) & 0xff, k = c >> 16;
+                    int p, i, j, k;
+                    if (splan) {
+                        const u32 pc = wpc[q];
+                        p = (int)(pc & 0x1fffu); i = (int)((pc >> 13) & 31u); j = (int)((pc >> 18) & 31u); k = (int)(pc >> 23);
+                    } else {
+                        p = (int)__ldg(A.wave + PL.wave_off + q);
+                        const u32 c = __ldg(A.wcrd + PL.wave_off + q);
+                        i = c & 0xff; j = (c >> 8) & 0xff; k = c >> 16;
+                    }
                     u32 bin = sb[p];
                     float v;
                     if (bin) {
