@@ -1210,6 +1210,26 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         A.sb0 = 0;
         A.sb1 = g.nb;
     }
+    // decompressed-data faults injected: the re-execution kernels go right behind the decode,
+    // sized from the device's mismatch counter (no host round trip before them)
+    const bool spec_reexec = decode && !fblk.empty();
+    if (spec_reexec) {
+        DecArgs AR = A;
+        AR.n_faults = 0;   // re-execution replays no fault
+        AR.list_spread = 0;
+        PF.mark("k_reexec_decode", s);
+        const size_t rsm = ((size_t)4 << DEC_TBITS_S) + (size_t)RD_WARPS * RD_MAXW * 4;
+        const unsigned rg = (unsigned)std::min<size_t>((fblk.size() + RD_WARPS - 1) / RD_WARPS + 1, (size_t)sms * 4);
+        k_redecode<<<rg, RD_WARPS * 32, rsm, s>>>(AR, (const u32*)(ws + L.mis), -1);
+        LCHK("k_redecode");
+        PF.mark("k_reexec_recon", s);
+        if (lor_wave_max(g) > 32) k_recon_g<128><<<(unsigned)std::min<size_t>(fblk.size() + 1, (size_t)sms * 8), 128, rslot, s>>>(AR, 1);
+        else k_recon_g<32><<<(unsigned)std::min<size_t>((fblk.size() + rw) / rw, (size_t)sms * 4), rw * 32, rslot * rw, s>>>(AR, 1);
+        LCHK("k_recon");
+        PF.mark("k_reexec_verdict", s);
+        k_reexec_verdict<<<(unsigned)std::min<size_t>((fblk.size() + 255) / 256 + 1, 1024), 256, 0, s>>>(AR, ws + L.verdict, -1);
+        LCHK("k_reexec_verdict");
+    }
     CK(cudaGetLastError());
     PF.mark("", s);
     unsigned char hres_local[RESULT_BYTES];
@@ -1271,6 +1291,7 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         // stays on the device in arrival order (blocks are independent), only the verdicts and
         // the ids come back
         A.n_faults = 0;
+        if (!spec_reexec) {
         PF.mark("k_reexec_decode", s);
         {
             const size_t rsm = ((size_t)4 << DEC_TBITS_S) + (size_t)RD_WARPS * RD_MAXW * 4;
@@ -1284,8 +1305,9 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         else k_recon_g<32><<<(unsigned)std::min<u32>((nmis + rw - 1) / rw, sms * 4), rw * 32, rslot * rw, s>>>(A, 1);
         LCHK("k_recon");
         PF.mark("k_reexec_verdict", s);
-        k_reexec_verdict<<<(nmis + 255) / 256, 256, 0, s>>>(A, ws + L.verdict, nmis);
+        k_reexec_verdict<<<(nmis + 255) / 256, 256, 0, s>>>(A, ws + L.verdict, (int)nmis);
         LCHK("k_reexec_verdict");
+        }
         std::vector<u32> mis(nmis);
         std::vector<unsigned char> vd(nmis);
         CK(cudaMemcpyAsync(mis.data(), ws + L.mis, 4 * (size_t)nmis, cudaMemcpyDeviceToHost, s));

@@ -1414,6 +1414,8 @@ __global__ void k_decomp_faults(DecArgs A, const u32* fblk, int nfb) {
 // error, so a failure here (impossible for an intact archive) is reported as a mismatch.
 #define RD_WARPS 4
 #define RD_MAXW 2048   // slice words staged per warp (a block of <= 1150 points at 57 bits)
+FTLZ_DEV void redecode_block(const DecArgs& A, const long long b, const u32* s_lut, u32* sl, int T, int maxlen, int lane);
+
 __global__ void __launch_bounds__(RD_WARPS * 32) k_redecode(DecArgs A, const u32* list, int n) {
     extern __shared__ __align__(16) unsigned char rsm[];
     u32* s_lut = (u32*)rsm;
@@ -1424,15 +1426,20 @@ __global__ void __launch_bounds__(RD_WARPS * 32) k_redecode(DecArgs A, const u32
     for (int x = tid; x < (1 << T); x += blockDim.x) s_lut[x] = A.lut12[x];
     if (tid < 64) { s_dec_first[tid] = A.first_code[tid]; s_dec_count[tid] = A.lcount[tid]; s_dec_base[tid] = A.lbase[tid]; }
     __syncthreads();
-    const int w = blockIdx.x * RD_WARPS + warp;
-    if (w >= n) return;
-    const long long b = list[w];
+    // n < 0: the count is the device's mismatch counter (launched before the host knows it),
+    // warps stride over the list
+    const int cnt = n >= 0 ? n : (int)A.counters[DC_NMIS];
+    for (int w = blockIdx.x * RD_WARPS + warp; w < cnt; w += (n >= 0 ? cnt : gridDim.x * RD_WARPS))
+        redecode_block(A, list[w], s_lut, slice_all + (size_t)warp * RD_MAXW, T, maxlen, lane);
+}
+
+FTLZ_DEV void redecode_block(const DecArgs& A, const long long b, const u32* s_lut, u32* sl, int T, int maxlen, int lane) {
+    const Geom& g = A.g;
     const BlockInfo B = block_info(g, b);
     const u32 bl = A.bitlen[b];
     const u64 start = pay_boff(A) * 8 + A.bofs[b];
     const u64 w0 = start >> 5;
     const u32 nwords = (u32)(((start + bl + 31) >> 5) - w0) + 2;   // + 2: the 64-bit window's tail
-    u32* sl = slice_all + (size_t)warp * RD_MAXW;
     if (nwords > RD_MAXW) {
         if (lane == 0) A.mflag[b] = 3;
         return;
@@ -1494,9 +1501,10 @@ __global__ void __launch_bounds__(RD_WARPS * 32) k_redecode(DecArgs A, const u32
 }
 
 // verdicts of the re-executed blocks, in list order (2: matches after re-execution, else 3)
-__global__ void k_reexec_verdict(DecArgs A, u8* verdict, u32 n) {
-    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) verdict[i] = A.mflag[A.mis_list[i]];
+__global__ void k_reexec_verdict(DecArgs A, u8* verdict, int n) {
+    const u32 cnt = n >= 0 ? (u32)n : A.counters[DC_NMIS];
+    for (u32 i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x)
+        verdict[i] = A.mflag[A.mis_list[i]];
 }
 
 }  // namespace ftlz
