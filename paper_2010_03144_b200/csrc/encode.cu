@@ -398,23 +398,39 @@ FTLZ_DEV void pack_range_s(const EncWin& W, const u16* sym16, const u32* sym32, 
 // symbol one table load, a 64-bit shift-or and, every 32 bits, one predicated word store
 // (the lane's first word, shared with the lane before, is merged with a shared-memory OR)
 FTLZ_DEV void pack_range_seq(const u32* s_c32, int wlo, const u16* sym16, int p0, int pend, u32 pos, u32 sbase) {
-    u32 widx = pos >> 5;
+    u32 waddr = sbase + 4u * (pos >> 5);   // shared address of the word being filled
     u32 nacc = pos & 31;   // bits of the first word that belong to the lanes before (zero in acc)
     u64 acc = 0;           // pending bits, right-aligned
-    bool first = true;
+    int p = p0;
+    // up to the lane's first full word (shared with the lane before: shared-memory OR)
+    for (; p < pend; p++) {
+        const u32 e = s_c32[min((u32)sym16[p] - (u32)wlo, (u32)ENC_WIN)];
+        const u32 l = e & 31u;
+        acc = (acc << l) | (u64)(e >> 5);
+        nacc += l;
+        if (nacc >= 32u) {
+            nacc -= 32u;
+            put_s(waddr, (u32)(acc >> nacc), false, true);
+            waddr += 4u;
+            p++;
+            break;
+        }
+    }
+    // the lane's own words: plain predicated stores
 #pragma unroll 2
-    for (int p = p0; p < pend; p++) {
+    for (; p < pend; p++) {
         const u32 e = s_c32[min((u32)sym16[p] - (u32)wlo, (u32)ENC_WIN)];
         const u32 l = e & 31u;
         acc = (acc << l) | (u64)(e >> 5);
         nacc += l;
         const bool full = nacc >= 32u;
         nacc -= full ? 32u : 0u;
-        put_s(sbase + 4u * widx, (u32)(acc >> nacc), full && !first, full && first);
-        first = first && !full;
-        widx += full ? 1u : 0u;
+        const u32 v = __byte_perm((u32)(acc >> nacc), 0, 0x0123);
+        asm volatile("{\n\t.reg .pred a;\n\tsetp.ne.u32 a, %2, 0;\n\t@a st.shared.u32 [%0], %1;\n\t}"
+                     ::"r"(waddr), "r"(v), "r"((u32)full) : "memory");
+        waddr += full ? 4u : 0u;
     }
-    if (nacc > 0u) put_s(sbase + 4u * widx, (u32)(acc << (32u - nacc)), false, true);
+    if (nacc > 0u) put_s(waddr, (u32)(acc << (32u - nacc)), false, true);
 }
 
 __global__ void __launch_bounds__(1024) k_enc_pack(CompArgs A, const u32* fix, const u8* fixed_flag) {
