@@ -301,6 +301,12 @@ def test_lorenzo_blocks_inside_the_regression_kernel(protect):
             faults.append(("dup_predict", b, el, int(rng.integers(0, 192))))
         else:
             faults.append(("dup_reconstruct", b, el, int(rng.integers(0, 192))))
+    # and blocks of the last (8-point) z layer, quantized by regx_block in the same kernel
+    last = [b for b in range(nb) if b % 16 == 15 and b not in override][:40]
+    for t, b in enumerate(last):
+        el = int(rng.integers(0, vol(b)))
+        kind = ("input", "dup_predict", "dup_reconstruct")[t % 3]
+        faults.append((kind, b, el, int(rng.integers(0, 32 if kind == "input" else 192))))
     cfg = dict(protect_input=protect, duplicate_eval=True)
     want, wrep = O.compress(x, "value_range_relative", 1e-3, cfg, faults=faults, override=override, threads=4)
     stream, rep = F.compress(F.Field.from_array(x), F.ErrorBound("value_range_relative", 1e-3), F.FtConfig(**cfg),
