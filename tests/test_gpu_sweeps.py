@@ -14,6 +14,7 @@ import numpy as np
 import pytest
 
 import paper_2010_03144_b200 as F
+from oracle import oracle as O
 from tests.golden_util import GOLDEN, load, manifest, sha
 
 pytestmark = pytest.mark.gpu
@@ -80,3 +81,66 @@ def test_c5_full_size_matches_reference(c5_field, target):
     assert len(d["decomp_block_reexecuted"]) == want["n_reexecuted"]
     assert _h(d["decomp_block_reexecuted"]) == want["reexecuted_sha256"]
     assert out is not None and sha(out.values) == want["output_sha256"]
+
+
+# Seeded random cases through every kernel variant the library picks by geometry (2-D and 3-D
+# fields, ragged blocks, edges 2..24, the warp-per-block or lane-per-block decoder, Lorenzo blocks
+# fused into the regression kernel or not), random flags, bounds and faults: archive, report
+# lists and reconstruction equal to the oracle's.
+def _fuzz_case(seed):
+    rng = np.random.default_rng(seed)
+    if rng.random() < 0.3:
+        dims = (1, int(rng.integers(12, 300)), int(rng.integers(12, 300)))
+    else:
+        dims = tuple(int(v) for v in rng.integers(8, 90, size=3))
+    edge = int(rng.choice([10, 10, 10, 4, 6, 8, 12, 16, 24, 2, 3]))
+    i, j, k = np.meshgrid(*[np.arange(d, dtype=np.float64) for d in dims], indexing="ij")
+    kind = rng.integers(0, 3)
+    if kind == 0:
+        x = np.sin(0.07 * i * rng.uniform(0.5, 2)) * np.cos(0.05 * j) + 0.02 * k + rng.normal(0, 1e-3, dims)
+    elif kind == 1:
+        x = rng.standard_normal(dims) * rng.uniform(0.1, 10)
+    else:
+        x = np.exp(rng.standard_normal(dims))
+    x = x.astype(np.float32)
+    mode = "value_range_relative" if rng.random() < 0.7 else "absolute"
+    value = float(10.0 ** rng.uniform(-5, -1.5))
+    cfg = dict(block_edge=edge, protect_input=bool(rng.random() < 0.8), protect_bins=bool(rng.random() < 0.8),
+               duplicate_eval=bool(rng.random() < 0.8), store_sum_dc=bool(rng.random() < 0.9))
+    nb = 1
+    for d in dims:
+        nb *= -(-d // edge)
+    vol = min(edge, dims[0]) * min(edge, dims[1]) * min(edge, dims[2])   # first block: full extent
+    faults = []
+    if rng.random() < 0.6:
+        for _ in range(int(rng.integers(1, 6))):
+            t = str(rng.choice(["input", "bins", "dup_predict", "dup_reconstruct"]))
+            faults.append((t, 0, int(rng.integers(0, vol)), int(rng.integers(0, 192 if t.startswith("dup") else 32))))
+    dfaults = [("decomp", 0, int(rng.integers(0, vol)), int(rng.integers(0, 32)))] if rng.random() < 0.5 else []
+    return x, mode, value, cfg, faults, dfaults
+
+
+@pytest.mark.parametrize("seed", range(64))
+def test_random_cases_against_oracle(seed):
+    x, mode, value, cfg, faults, dfaults = _fuzz_case(1000 + seed)
+    try:
+        want, wrep = O.compress(x, mode, value, cfg, faults=faults, threads=4)
+    except O.OracleError as e:
+        with pytest.raises(F.FtlzError) as ei:
+            F.compress(F.Field.from_array(x), F.ErrorBound(mode, value), F.FtConfig(**cfg), faults=faults)
+        assert type(ei.value).__name__ == e.cls
+        assert str(ei.value) == str(e)
+        return
+    stream, rep = F.compress(F.Field.from_array(x), F.ErrorBound(mode, value), F.FtConfig(**cfg), faults=faults)
+    data = F.serialize(stream)
+    assert data == want
+    rd = rep.to_dict()
+    for k in ("input_corrected", "bins_corrected", "dup_mismatch_resolved"):
+        assert rd[k] == wrep[k], k
+    out, drep = F.decompress(F.parse(data), faults=dfaults)
+    ro, rr = O.decompress(want, faults=dfaults, threads=4)
+    assert drep.to_dict()["decomp_block_reexecuted"] == rr["decomp_block_reexecuted"]
+    if ro is None:
+        assert out is None
+    else:
+        np.testing.assert_array_equal(out.values.view(np.uint32), ro.view(np.uint32))
