@@ -448,7 +448,24 @@ __global__ void __launch_bounds__(DW_WARPS * 32, 1) k_decode_warp(DecArgs A) {
                 obase[S.rowoff[r] + k] = v;
             }
         };
-        if (bz == DW_E) {
+        if (bz == DW_E && nunp == 0) {
+            // no unpredictable point (the common case): no ranks to form; a zero symbol is only
+            // flagged (the count check below then fails the block)
+            const int d = lane / DW_E, k = lane - d * DW_E;
+            const double ckk = S.ck[k < bz ? k : 0];
+            u32 z = 0;
+            for (int r0 = 0; r0 < nrows; r0 += 3) {
+                const int r = r0 + d;
+                if (lane < 3 * DW_E && r < nrows) {
+                    const u32 sy = S.sym[r * DW_E + k];
+                    const float v = __double2float_rn(__dadd_rn(__dadd_rn(S.ab[r], ckk), __dmul_rn(twoeb, int_to_f64((int)sy - center))));
+                    z |= sy == 0u;
+                    dsum += (u64)__float_as_uint(v);
+                    obase[S.rowoff[r] + k] = v;
+                }
+            }
+            zeros = __popc(__ballot_sync(FULL, z != 0u));
+        } else if (bz == DW_E) {
             // three rows of ten per step: lane = 10 d + k
             const int d = lane / DW_E, k = lane - d * DW_E;
             const double ckk = S.ck[k < bz ? k : 0];
