@@ -355,7 +355,7 @@ def run_ours(args, world, rank, local):
             for k, v in prof.items()}
     # kernels only (the profiler's host-prelude marks are not launches)
     launches = int(round(sum(v[1] for k, v in prof.items() if k.startswith("k_")) / max(1, args.steps)))
-    dec_names = ("k_parse_chunks", "k_parse_records", "k_scan2", "k_parse_tail", "k_dec_luts", "k_dw_lut",
+    dec_names = ("k_parse_chunks", "k_parse_records", "k_scan2", "k_parse_tail", "k_dec_luts",
                  "k_decode", "k_recon_warp")
     comp_k = {k: v for k, v in kern.items() if k not in dec_names}
     dec_k = {k: v for k, v in kern.items() if k not in comp_k}

@@ -1141,9 +1141,7 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         k_parse_tail<<<1, PT_THREADS, 8192 * 8, s>>>(A, 0);
     }
     LCHK("k_parse_tail");
-    PF.mark("k_dec_luts", s);
-    k_dec_luts<<<((1u << DEC_TBITS) + (1u << DEC_TBITS_S)) / 256, 256, 0, s>>>(A);
-    LCHK("k_dec_luts");
+
     // full-path k_decode: up to DEC_WARPS warps per CTA, fewer when the per-warp staging rows of
     // a large block edge would not fit in shared memory
     const int dec_nw = dec_warps((int)g.e, DEC_WARPS);
@@ -1162,11 +1160,10 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     const long long npts = g.nx * g.ny * g.nz;
     const bool warp_dec = decode && g.e == DW_E && g.nx >= DW_E && 2 * g.nb < (long long)num_sms() * DEC_WARPS * 32 &&
                        8 * (long long)len <= 6 * npts;
-    if (warp_dec) {
-        PF.mark("k_dw_lut", s);
-        k_dw_lut<<<(1u << PAIR_TBITS) / 256, 256, 0, s>>>(A);
-        LCHK("k_dw_lut");
-    }
+    PF.mark("k_dec_luts", s);
+    k_dec_luts<<<((1u << DEC_TBITS) + (1u << DEC_TBITS_S) + (warp_dec ? 1u << PAIR_TBITS : 0u)) / 256, 256, 0, s>>>(
+        A, warp_dec ? 1 : 0);
+    LCHK("k_dec_luts");
     if (decode) {
         // slabs: whole block layers (block ids are layer-major), so each slab's output is one
         // contiguous range of x-planes

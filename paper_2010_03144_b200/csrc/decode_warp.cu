@@ -36,45 +36,65 @@ namespace ftlz {
 #define DW_VMAX 1024        // symbol slots (>= 10^3)
 #define DW_LONGSYM 1024     // symbols of codes longer than the table kept in shared memory
 
+// decode LUTs: T-bit window -> (symbol << 8 | length) for codes of length <= T (0: longer); the
+// window's length is the first l with x < end_l = (F_l + count_l) << (T - l), which is
+// non-decreasing in l (binary search).  Grid-wide, one launch: the 2^T-entry table of the
+// full-path decoder, the 2^T12-entry table of the list decodes and, for the warp-per-block
+// decoder (pairs != 0), its 2^PAIR_TBITS-entry pair table.
+//
 // pair table entry: bits 0-5 bits consumed, 6-7 symbol count n (0: first code longer than the
 // table or outside the code space), 8-13 length of the first code, 16-31 first symbol, 32-47
 // second symbol, 48-59 start offsets of the codes lying wholly inside the window, 60-63 the bits
 // they cover (0: first code longer than the table)
-FTLZ_DEV u64 pair_look(const u32* lut, int T, u32 u, int nvalid) {
-    // u: PAIR_TBITS-bit window whose top `nvalid` bits are valid; lut: 2^T-entry single-symbol
-    // table (T <= 15, codes of length <= T)
-    const u32 e = T <= PAIR_TBITS ? lut[u >> (PAIR_TBITS - T)] : lut[u << (T - PAIR_TBITS)];
-    return (e && (int)(e & 63u) <= nvalid) ? (u64)e : 0ull;
-}
-
-__global__ void __launch_bounds__(256) k_dw_lut(DecArgs A) {
+__global__ void __launch_bounds__(256) k_dec_luts(DecArgs A, int pairs) {
     if (dev_failed(A.st)) return;
-    const u32 v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= (1u << PAIR_TBITS)) return;
-    const int T = (int)A.info[DI_T];
-    const u32 M = (1u << PAIR_TBITS) - 1u;
-    const u64 e1 = pair_look(A.lut, T, v, PAIR_TBITS);
-    u64 ent = 0;
-    if (e1) {
-        const u32 l1 = (u32)e1 & 63u, s1 = (u32)(e1 >> 8);
-        const u64 e2 = pair_look(A.lut, T, (v << l1) & M, PAIR_TBITS - (int)l1);
-        if (e2) {
-            const u32 l2 = (u32)e2 & 63u, s2 = (u32)(e2 >> 8);
-            ent = (u64)(l1 + l2) | (2ull << 6) | ((u64)l1 << 8) | ((u64)s1 << 16) | ((u64)s2 << 32);
-        } else {
-            ent = (u64)l1 | (1ull << 6) | ((u64)l1 << 8) | ((u64)s1 << 16);
+    __shared__ u64 s_fc[64];
+    __shared__ u32 s_lc[64], s_lb[64];
+    if (threadIdx.x < 64) { s_fc[threadIdx.x] = A.first_code[threadIdx.x]; s_lc[threadIdx.x] = A.lcount[threadIdx.x]; s_lb[threadIdx.x] = A.lbase[threadIdx.x]; }
+    __syncthreads();
+    const int T = (int)A.info[DI_T], T12 = (int)A.info[DI_T12];
+    const u32 n1 = 1u << T, n2 = 1u << T12, n3 = pairs ? 1u << PAIR_TBITS : 0u;
+    // the code at the head of the TT-bit window x: symbol << 8 | length, 0 if longer than TT
+    auto look = [&](u32 x, int TT) -> u32 {
+        int lo = 1, hi = TT + 1;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if ((u64)x < ((s_fc[mid] + s_lc[mid]) << (TT - mid))) hi = mid;
+            else lo = mid + 1;
         }
-        // every code starting inside the window that ends inside it: start mask, bits covered
-        u32 off = 0, mask = 0;
-        while (off < PAIR_TBITS) {
-            const u64 e = pair_look(A.lut, T, (v << off) & M, PAIR_TBITS - (int)off);
-            if (!e) break;
-            mask |= 1u << off;
-            off += (u32)e & 63u;
+        return lo <= TT ? (A.dsym[s_lb[lo] + (u32)((u64)(x >> (TT - lo)) - s_fc[lo])] << 8) | (u32)lo : 0u;
+    };
+    for (u32 t = blockIdx.x * blockDim.x + threadIdx.x; t < n1 + n2 + n3; t += gridDim.x * blockDim.x) {
+        if (t < n1) { A.lut[t] = look(t, T); continue; }
+        if (t < n1 + n2) { A.lut12[t - n1] = look(t - n1, T12); continue; }
+        const u32 v = t - n1 - n2, M = (1u << PAIR_TBITS) - 1u;
+        // a code wholly inside the top `nvalid` bits of the PAIR_TBITS-bit window u
+        auto pl = [&](u32 u, int nvalid) -> u32 {
+            const u32 e = look(u, PAIR_TBITS);
+            return (e && (int)(e & 63u) <= nvalid) ? e : 0u;
+        };
+        const u32 e1 = pl(v, PAIR_TBITS);
+        u64 ent = 0;
+        if (e1) {
+            const u32 l1 = e1 & 63u, s1 = e1 >> 8;
+            const u32 e2 = pl((v << l1) & M, PAIR_TBITS - (int)l1);
+            if (e2) {
+                const u32 l2 = e2 & 63u, s2 = e2 >> 8;
+                ent = (u64)(l1 + l2) | (2ull << 6) | ((u64)l1 << 8) | ((u64)s1 << 16) | ((u64)s2 << 32);
+            } else {
+                ent = (u64)l1 | (1ull << 6) | ((u64)l1 << 8) | ((u64)s1 << 16);
+            }
+            u32 off = 0, mask = 0;
+            while (off < PAIR_TBITS) {
+                const u32 e = pl((v << off) & M, PAIR_TBITS - (int)off);
+                if (!e) break;
+                mask |= 1u << off;
+                off += e & 63u;
+            }
+            ent |= ((u64)mask << 48) | ((u64)off << 60);
         }
-        ent |= ((u64)mask << 48) | ((u64)off << 60);
+        A.lut2[v] = ent;
     }
-    A.lut2[v] = ent;
 }
 
 FTLZ_DEV u64 lds_u64(u32 addr) {

@@ -574,33 +574,6 @@ __global__ void __launch_bounds__(PT_THREADS) k_parse_tail(DecArgs A, int phase)
     // (the decode LUTs are built by k_dec_luts over the whole grid)
 }
 
-// decode LUTs: T-bit window -> (symbol << 8 | length) for codes of length <= T (0: longer); the
-// window's length is the first l with x < end_l = (F_l + count_l) << (T - l), which is
-// non-decreasing in l (binary search).  Grid-wide: the 2^T-entry table of the full-path decoder,
-// then the 2^T12-entry table of the list decodes.
-__global__ void __launch_bounds__(256) k_dec_luts(DecArgs A) {
-    if (dev_failed(A.st)) return;
-    __shared__ u64 s_fc[64];
-    __shared__ u32 s_lc[64], s_lb[64];
-    if (threadIdx.x < 64) { s_fc[threadIdx.x] = A.first_code[threadIdx.x]; s_lc[threadIdx.x] = A.lcount[threadIdx.x]; s_lb[threadIdx.x] = A.lbase[threadIdx.x]; }
-    __syncthreads();
-    const int T = (int)A.info[DI_T], T12 = (int)A.info[DI_T12];
-    const u32 n1 = 1u << T, n2 = 1u << T12;
-    for (u32 t = blockIdx.x * blockDim.x + threadIdx.x; t < n1 + n2; t += gridDim.x * blockDim.x) {
-        const int TT = t < n1 ? T : T12;
-        const u32 x = t < n1 ? t : t - n1;
-        int lo = 1, hi = TT + 1;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if ((u64)x < ((s_fc[mid] + s_lc[mid]) << (TT - mid))) hi = mid;
-            else lo = mid + 1;
-        }
-        u32 ent = 0;
-        if (lo <= TT) ent = (A.dsym[s_lb[lo] + (u32)((u64)(x >> (TT - lo)) - s_fc[lo])] << 8) | (u32)lo;
-        if (t < n1) A.lut[x] = ent;
-        else A.lut12[x] = ent;
-    }
-}
 
 // ------------------------------------------------------------------------------------------
 // Huffman bit reader: MSB-first 64-bit window over the big-endian 32-bit words of one block's
