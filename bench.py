@@ -452,8 +452,9 @@ def run_ours(args, world, rank, local):
         import queue
         import threading
 
-        K = max(8, args.steps)
-        NP = int(os.environ.get("FTLZ_E2E_THREADS", "1"))   # compress threads (and as many decompress threads)
+        # the pipeline fills and drains once per run: 32 steps keep that ramp near 3% of the total
+        K = int(os.environ.get("FTLZ_E2E_STEPS", max(32, args.steps)))
+        NP = int(os.environ.get("FTLZ_E2E_THREADS", "2"))   # compress threads (and as many decompress threads)
         archs = [torch.empty(int(bound), dtype=torch.uint8).pin_memory().numpy() for _ in range(2 * NP + 2)]
         outs = [torch.empty(x.shape, dtype=torch.float32).pin_memory().numpy() for _ in range(NP)]
         err = []
