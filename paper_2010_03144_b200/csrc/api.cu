@@ -556,10 +556,27 @@ __global__ void k_fault_first(const ftlz_fault* f, int nf, long long nb, int* fi
     const long long b = f[i].block;
     if (b >= 0 && b < nb && (i == 0 || f[i - 1].block != b)) first[b] = i;
 }
+// pinned staging behind a context's result buffer for the fault list and the decompressed-data
+// fault blocks (a pageable H2D copy stages through the driver and costs ~10 us per call)
+static size_t fault_stage_bytes(int64_t nf) { return nf ? al256(sizeof(ftlz_fault) * (size_t)nf) + al256(4 * (size_t)nf) : 0; }
+
+// copy n bytes host -> device on s, through the pinned staging area when there is one (the
+// stream is synchronized before the staging area is reused)
+static int h2d_staged(void* dst, const void* src, size_t n, unsigned char* hstage, cudaStream_t s) {
+    if (!n) return FTLZ_OK;
+    if (hstage) {
+        memcpy(hstage, src, n);
+        src = hstage;
+    }
+    CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, s));
+    return FTLZ_OK;
+}
+
 static int upload_faults(const std::vector<ftlz_fault>& fs, long long nb, unsigned char* d_faults, unsigned char* d_first,
-                         cudaStream_t s) {
+                         cudaStream_t s, unsigned char* hstage) {
     const int nf = (int)fs.size();
-    CK(cudaMemcpyAsync(d_faults, fs.data(), sizeof(ftlz_fault) * (size_t)nf, cudaMemcpyHostToDevice, s));
+    int rc = h2d_staged(d_faults, fs.data(), sizeof(ftlz_fault) * (size_t)nf, hstage, s);
+    if (rc) return rc;
     CK(cudaMemsetAsync(d_first, 0xff, 4 * (size_t)nb, s));
     k_fault_first<<<(nf + 255) / 256, 256, 0, s>>>((const ftlz_fault*)d_faults, nf, nb, (int*)d_first);
     return cudaGetLastError() == cudaSuccess ? FTLZ_OK : set_err(FTLZ_ERR_CUDA, "k_fault_first");
@@ -629,6 +646,8 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     Profiler& PF = prof ? *prof : noprof;
     report_reset(rep);
     const Geom& g = P.g;
+    // context calls: h_result is pinned with fault_stage_bytes(nf) of staging behind it
+    unsigned char* hstage = h_result ? h_result + RESULT_BYTES : nullptr;
     int cap = (int)cfg->bin_capacity;
     if (cap < 4 || (cap & (cap - 1))) return set_err(FTLZ_ERR_INVALID_ARGUMENT, "bin_capacity must be a power of two >= 4");
     if (cap > 65536) return set_err(FTLZ_ERR_INVALID_ARGUMENT, "bin_capacity > 65536 is not supported on the device path");
@@ -652,7 +671,7 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     std::vector<ftlz_fault> fs;
     if (nf) {
         prep_faults(faults, nf, fs);
-        if ((rc = upload_faults(fs, g.nb, ws + L.faults, ws + L.ffirst, s))) return rc;
+        if ((rc = upload_faults(fs, g.nb, ws + L.faults, ws + L.ffirst, s, hstage))) return rc;
     }
     if (ovr) CK(cudaMemcpyAsync(ws + L.ovr, ovr, (size_t)g.nb, cudaMemcpyHostToDevice, s));
 
@@ -1088,6 +1107,7 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     Profiler& PF = prof ? *prof : noprof;
     report_reset(rep);
     const Geom& g = P.g;
+    unsigned char* hstage = h_result ? h_result + RESULT_BYTES : nullptr;   // see compress_core
     int cap = (int)h->bin_capacity;
     if (cap > 65536) return set_err(FTLZ_ERR_INVALID_ARGUMENT, "bin_capacity > 65536 is not supported on the device path");
     int rc = validate_faults(P, faults, nf);
@@ -1107,9 +1127,10 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         prep_faults(faults, nf, fs);
         for (const ftlz_fault& f : fs)
             if (f.target == FTLZ_FAULT_DECOMP && (fblk.empty() || fblk.back() != (u32)f.block)) fblk.push_back((u32)f.block);
-        if ((rc = upload_faults(fs, g.nb, ws + L.faults, ws + L.ffirst, s))) return rc;
-        if (!fblk.empty())
-            CK(cudaMemcpyAsync(ws + L.fblk, fblk.data(), 4 * fblk.size(), cudaMemcpyHostToDevice, s));
+        if ((rc = upload_faults(fs, g.nb, ws + L.faults, ws + L.ffirst, s, hstage))) return rc;
+        if (!fblk.empty() &&
+            (rc = h2d_staged(ws + L.fblk, fblk.data(), 4 * fblk.size(), hstage ? hstage + al256(sizeof(ftlz_fault) * (size_t)nf) : nullptr, s)))
+            return rc;
     }
     DecArgs A = make_dec_args(P, D, L, d_a, len, h, d_out, nf, ws);
     int sms = num_sms();
@@ -1606,6 +1627,7 @@ static int ctx_compress(ftlz_ctx* c, const float* d_in, int64_t nx, int64_t ny, 
     }
     CompLayout L = comp_layout(c->hp, (int)cfg->bin_capacity, nf, cfg->codec_id);
     if ((rc = c->ws.ensure(L.total))) return rc;
+    if ((rc = c->h_res.ensure(RESULT_BYTES + fault_stage_bytes(nf)))) return rc;
     size_t bound = ftlz_compress_bound(nx, ny, nz, cfg);
     if ((rc = c->out.ensure(bound))) return rc;
     rc = compress_core(c->hp, &c->dp, d_in, eb_mode, eb_value, cfg, faults, nf, ovr, (unsigned char*)c->ws.p,
@@ -1737,6 +1759,7 @@ static int ctx_decompress(ftlz_ctx* c, const uint8_t* d_a, size_t len, const ftl
     if (rc) return rc;
     DecLayout L = dec_layout(c->hp, len, (int)std::min<uint32_t>(hdr->bin_capacity, 65536u), nf, hdr->codec_id);
     if ((rc = c->dws.ensure(L.total))) return rc;
+    if ((rc = c->h_res.ensure(RESULT_BYTES + fault_stage_bytes(nf)))) return rc;
     return decompress_core(c->hp, &c->dp, d_a, len, hdr, d_out, faults, nf, (unsigned char*)c->dws.p, c->dws.n,
                            rep, si, decode, c->stream, (unsigned char*)c->h_res.p, &c->prof, dl);
 }
