@@ -559,6 +559,9 @@ __global__ void k_fault_first(const ftlz_fault* f, int nf, long long nb, int* fi
 // pinned staging behind a context's result buffer for the fault list and the decompressed-data
 // fault blocks (a pageable H2D copy stages through the driver and costs ~10 us per call)
 static size_t fault_stage_bytes(int64_t nf) { return nf ? al256(sizeof(ftlz_fault) * (size_t)nf) + al256(4 * (size_t)nf) : 0; }
+// injected runs read their event flags (compress: nb bytes) or re-execution list and verdicts
+// (decompress: 5 bytes per fault) back with the result, into pinned room behind the staging
+static size_t fault_back_bytes(int64_t nf, long long nb) { return nf ? al256(std::max<size_t>((size_t)nb, 5 * (size_t)nf)) : 0; }
 
 // copy n bytes host -> device on s, through the pinned staging area when there is one (the
 // stream is synchronized before the staging area is reused)
@@ -842,6 +845,9 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     unsigned char hres_local[RESULT_BYTES];
     unsigned char* hres = h_result ? h_result : hres_local;
     CK(cudaMemcpyAsync(hres, ws + L.result, RESULT_BYTES, cudaMemcpyDeviceToHost, s));
+    // injected runs: the event flags come down with the result (one synchronisation)
+    unsigned char* hev = nf && hstage ? hstage + fault_stage_bytes(nf) : nullptr;
+    if (hev) CK(cudaMemcpyAsync(hev, ws + L.events, (size_t)g.nb, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     PF.collect();
     DevStatus st;
@@ -858,9 +864,14 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
     std::vector<int64_t> in_fix, bin_fix;
     int64_t bad_in = -1, bad_bin = -1;
     if (counters[3]) {
-        std::vector<unsigned char> ev((size_t)g.nb);
-        CK(cudaMemcpyAsync(ev.data(), ws + L.events, (size_t)g.nb, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        std::vector<unsigned char> evbuf;
+        const unsigned char* ev = hev;
+        if (!ev) {
+            evbuf.resize((size_t)g.nb);
+            CK(cudaMemcpyAsync(evbuf.data(), ws + L.events, (size_t)g.nb, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            ev = evbuf.data();
+        }
         std::tuple<int, int, int> best;
         for (int64_t b = 0; b < g.nb; b++) {
             if (ev[b] & 1) in_fix.push_back(b);
@@ -1253,6 +1264,13 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     unsigned char hres_local[RESULT_BYTES];
     unsigned char* hres = h_result ? h_result : hres_local;
     CK(cudaMemcpyAsync(hres, ws + L.result, RESULT_BYTES, cudaMemcpyDeviceToHost, s));
+    // re-execution behind injected faults: at most one mismatching block per faulted block, so
+    // the list and the verdicts come down with the result (one synchronisation)
+    unsigned char* hback = spec_reexec && hstage ? hstage + fault_stage_bytes(nf) : nullptr;
+    if (hback) {
+        CK(cudaMemcpyAsync(hback, ws + L.mis, 4 * fblk.size(), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(hback + 4 * fblk.size(), ws + L.verdict, fblk.size(), cudaMemcpyDeviceToHost, s));
+    }
     CK(cudaStreamSynchronize(s));
     PF.collect();
     DecResult R;
@@ -1328,11 +1346,16 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         }
         std::vector<u32> mis(nmis);
         std::vector<unsigned char> vd(nmis);
-        CK(cudaMemcpyAsync(mis.data(), ws + L.mis, 4 * (size_t)nmis, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(vd.data(), ws + L.verdict, (size_t)nmis, cudaMemcpyDeviceToHost, s));
-        PF.mark("", s);
-        CK(cudaStreamSynchronize(s));
-        PF.collect();
+        if (hback && nmis <= fblk.size()) {
+            memcpy(mis.data(), hback, 4 * (size_t)nmis);
+            memcpy(vd.data(), hback + 4 * fblk.size(), (size_t)nmis);
+        } else {
+            CK(cudaMemcpyAsync(mis.data(), ws + L.mis, 4 * (size_t)nmis, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(vd.data(), ws + L.verdict, (size_t)nmis, cudaMemcpyDeviceToHost, s));
+            PF.mark("", s);
+            CK(cudaStreamSynchronize(s));
+            PF.collect();
+        }
         // verification walks extent groups in sorted order, ids ascending (pipeline.py:692-708)
         std::vector<std::tuple<std::tuple<int, int, int>, int64_t, unsigned char>> order;
         for (u32 t = 0; t < nmis; t++) order.push_back({block_extent(P, mis[t]), (int64_t)mis[t], vd[t]});
@@ -1627,7 +1650,7 @@ static int ctx_compress(ftlz_ctx* c, const float* d_in, int64_t nx, int64_t ny, 
     }
     CompLayout L = comp_layout(c->hp, (int)cfg->bin_capacity, nf, cfg->codec_id);
     if ((rc = c->ws.ensure(L.total))) return rc;
-    if ((rc = c->h_res.ensure(RESULT_BYTES + fault_stage_bytes(nf)))) return rc;
+    if ((rc = c->h_res.ensure(RESULT_BYTES + fault_stage_bytes(nf) + fault_back_bytes(nf, c->hp.g.nb)))) return rc;
     size_t bound = ftlz_compress_bound(nx, ny, nz, cfg);
     if ((rc = c->out.ensure(bound))) return rc;
     rc = compress_core(c->hp, &c->dp, d_in, eb_mode, eb_value, cfg, faults, nf, ovr, (unsigned char*)c->ws.p,
@@ -1759,7 +1782,7 @@ static int ctx_decompress(ftlz_ctx* c, const uint8_t* d_a, size_t len, const ftl
     if (rc) return rc;
     DecLayout L = dec_layout(c->hp, len, (int)std::min<uint32_t>(hdr->bin_capacity, 65536u), nf, hdr->codec_id);
     if ((rc = c->dws.ensure(L.total))) return rc;
-    if ((rc = c->h_res.ensure(RESULT_BYTES + fault_stage_bytes(nf)))) return rc;
+    if ((rc = c->h_res.ensure(RESULT_BYTES + fault_stage_bytes(nf) + fault_back_bytes(nf, c->hp.g.nb)))) return rc;
     return decompress_core(c->hp, &c->dp, d_a, len, hdr, d_out, faults, nf, (unsigned char*)c->dws.p, c->dws.n,
                            rep, si, decode, c->stream, (unsigned char*)c->h_res.p, &c->prof, dl);
 }
