@@ -550,11 +550,14 @@ static void prep_faults(const ftlz_fault* faults, int64_t nf, std::vector<ftlz_f
 
 // first[b] = index of block b's first fault in the sorted list, -1 for blocks without one (the
 // nb-entry table is built on the device: only the fault list crosses PCIe)
-__global__ void k_fault_first(const ftlz_fault* f, int nf, long long nb, int* first) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= nf) return;
-    const long long b = f[i].block;
-    if (b >= 0 && b < nb && (i == 0 || f[i - 1].block != b)) first[b] = i;
+__global__ void __launch_bounds__(1024) k_fault_first(const ftlz_fault* f, int nf, long long nb, int* first) {
+    // one CTA: fill, barrier, then the first fault of each block (no separate memset pass)
+    for (long long b = threadIdx.x; b < nb; b += blockDim.x) first[b] = -1;
+    __syncthreads();
+    for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+        const long long b = f[i].block;
+        if (b >= 0 && b < nb && (i == 0 || f[i - 1].block != b)) first[b] = i;
+    }
 }
 // pinned staging behind a context's result buffer for the fault list and the decompressed-data
 // fault blocks (a pageable H2D copy stages through the driver and costs ~10 us per call)
@@ -576,12 +579,21 @@ static int h2d_staged(void* dst, const void* src, size_t n, unsigned char* hstag
 }
 
 static int upload_faults(const std::vector<ftlz_fault>& fs, long long nb, unsigned char* d_faults, unsigned char* d_first,
-                         cudaStream_t s, unsigned char* hstage) {
+                         cudaStream_t s, unsigned char* hstage, const void* extra = nullptr, size_t extra_n = 0) {
     const int nf = (int)fs.size();
-    int rc = h2d_staged(d_faults, fs.data(), sizeof(ftlz_fault) * (size_t)nf, hstage, s);
-    if (rc) return rc;
-    CK(cudaMemsetAsync(d_first, 0xff, 4 * (size_t)nb, s));
-    k_fault_first<<<(nf + 255) / 256, 256, 0, s>>>((const ftlz_fault*)d_faults, nf, nb, (int*)d_first);
+    // extra: bytes laid out right behind the fault list on both sides (decompress: the faulted
+    // block list), sent in the same copy
+    const size_t fb = sizeof(ftlz_fault) * (size_t)nf;
+    if (extra && extra_n && hstage) {
+        memcpy(hstage, fs.data(), fb);
+        memcpy(hstage + al256(fb), extra, extra_n);
+        CK(cudaMemcpyAsync(d_faults, hstage, al256(fb) + extra_n, cudaMemcpyHostToDevice, s));
+    } else {
+        int rc = h2d_staged(d_faults, fs.data(), fb, hstage, s);
+        if (rc) return rc;
+        if (extra && extra_n) CK(cudaMemcpyAsync(d_faults + al256(fb), extra, extra_n, cudaMemcpyHostToDevice, s));
+    }
+    k_fault_first<<<1, 1024, 0, s>>>((const ftlz_fault*)d_faults, nf, nb, (int*)d_first);
     return cudaGetLastError() == cudaSuccess ? FTLZ_OK : set_err(FTLZ_ERR_CUDA, "k_fault_first");
 }
 
@@ -791,8 +803,11 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
         k_quant_lor<<<num_sms() * 4, 32 * K.lor_warps, K.lor_smem, s>>>(A);
         LCHK("k_quant_lor");
     }
-    if (nf) PF.mark("k_fault_bins", s);
-    if (nf) {
+    // only blocks with bins-stage faults have work in k_fault_bins
+    bool bins_faults = false;
+    for (const ftlz_fault& f : fs) bins_faults |= f.target == FTLZ_FAULT_BINS;
+    if (bins_faults) PF.mark("k_fault_bins", s);
+    if (bins_faults) {
         const int fw = (int)std::max<size_t>(1, std::min<size_t>(8, (size_t)(200 * 1024) / (4 * (size_t)g.vmax)));
         k_fault_bins<<<(unsigned)((nf + fw - 1) / fw), 32 * fw, 4 * (size_t)g.vmax * fw, s>>>(A, (u32*)(ws + L.fix),
                                                                                              (u8*)(ws + L.fixed));
@@ -874,6 +889,12 @@ static int compress_core(const HostPlan& P, const DevPlan* cached, const float* 
         }
         std::tuple<int, int, int> best;
         for (int64_t b = 0; b < g.nb; b++) {
+            // flags are rare: skip eight clear blocks at a time
+            if (!(b & 7) && b + 8 <= g.nb) {
+                u64 w8;
+                memcpy(&w8, ev + b, 8);
+                if (!w8) { b += 7; continue; }
+            }
             if (ev[b] & 1) in_fix.push_back(b);
             if (ev[b] & 2) bin_fix.push_back(b);
             if (ev[b] & 4) {
@@ -993,8 +1014,8 @@ static DecLayout dec_layout(const HostPlan& P, size_t len, int cap, int64_t nf, 
     L.lbb = take(16 * ntiles);
     L.bins = take(2 * ((nb + 31) / 32) * 32 * (size_t)g.nvmax8 + 64);
     L.faults = take(sizeof(ftlz_fault) * (size_t)std::max<int64_t>(1, nf));
+    L.fblk = take(4 * (size_t)std::max<int64_t>(1, nf));   // distinct faulted blocks (right behind the list: one upload)
     L.ffirst = take(nf ? 4 * nb : 0);
-    L.fblk = take(4 * (size_t)std::max<int64_t>(1, nf));   // distinct faulted blocks
     L.verdict = take(nb);                                   // re-execution verdicts, list order
     L.ckpt = take(4 * RD_NCK * nb);                         // row checkpoints of the first decode
     L.plan = take(P.bytes());
@@ -1138,10 +1159,8 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         prep_faults(faults, nf, fs);
         for (const ftlz_fault& f : fs)
             if (f.target == FTLZ_FAULT_DECOMP && (fblk.empty() || fblk.back() != (u32)f.block)) fblk.push_back((u32)f.block);
-        if ((rc = upload_faults(fs, g.nb, ws + L.faults, ws + L.ffirst, s, hstage))) return rc;
-        if (!fblk.empty() &&
-            (rc = h2d_staged(ws + L.fblk, fblk.data(), 4 * fblk.size(), hstage ? hstage + al256(sizeof(ftlz_fault) * (size_t)nf) : nullptr, s)))
-            return rc;
+        // L.fblk sits right behind L.faults: one copy
+        if ((rc = upload_faults(fs, g.nb, ws + L.faults, ws + L.ffirst, s, hstage, fblk.data(), 4 * fblk.size()))) return rc;
     }
     DecArgs A = make_dec_args(P, D, L, d_a, len, h, d_out, nf, ws);
     int sms = num_sms();
