@@ -563,8 +563,8 @@ __global__ void __launch_bounds__(1024) k_fault_first(const ftlz_fault* f, int n
 // fault blocks (a pageable H2D copy stages through the driver and costs ~10 us per call)
 static size_t fault_stage_bytes(int64_t nf) { return nf ? al256(sizeof(ftlz_fault) * (size_t)nf) + al256(4 * (size_t)nf) : 0; }
 // injected runs read their event flags (compress: nb bytes) or re-execution list and verdicts
-// (decompress: 5 bytes per fault) back with the result, into pinned room behind the staging
-static size_t fault_back_bytes(int64_t nf, long long nb) { return nf ? al256(std::max<size_t>((size_t)nb, 5 * (size_t)nf)) : 0; }
+// (decompress: 4 bytes per fault and the nb block flags) back with the result, into pinned room behind the staging
+static size_t fault_back_bytes(int64_t nf, long long nb) { return nf ? al256((size_t)nb + 4 * (size_t)nf) : 0; }
 
 // copy n bytes host -> device on s, through the pinned staging area when there is one (the
 // stream is synchronized before the staging area is reused)
@@ -1274,9 +1274,13 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         if (lor_wave_max(g) > 32) k_recon_g<128><<<(unsigned)std::min<size_t>(fblk.size() + 1, (size_t)sms * 8), 128, rslot, s>>>(AR, 1);
         else k_recon_g<32><<<(unsigned)std::min<size_t>((fblk.size() + rw) / rw, (size_t)sms * 4), rw * 32, rslot * rw, s>>>(AR, 1);
         LCHK("k_recon");
-        PF.mark("k_reexec_verdict", s);
-        k_reexec_verdict<<<(unsigned)std::min<size_t>((fblk.size() + 255) / 256 + 1, 1024), 256, 0, s>>>(AR, ws + L.verdict, -1);
-        LCHK("k_reexec_verdict");
+        // context calls read the block flags back with the result and look the verdicts up on
+        // the host (no verdict kernel behind the reconstruction)
+        if (!hstage) {
+            PF.mark("k_reexec_verdict", s);
+            k_reexec_verdict<<<(unsigned)std::min<size_t>((fblk.size() + 255) / 256 + 1, 1024), 256, 0, s>>>(AR, ws + L.verdict, -1);
+            LCHK("k_reexec_verdict");
+        }
     }
     CK(cudaGetLastError());
     PF.mark("", s);
@@ -1288,7 +1292,7 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
     unsigned char* hback = spec_reexec && hstage ? hstage + fault_stage_bytes(nf) : nullptr;
     if (hback) {
         CK(cudaMemcpyAsync(hback, ws + L.mis, 4 * fblk.size(), cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(hback + 4 * fblk.size(), ws + L.verdict, fblk.size(), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(hback + 4 * fblk.size(), ws + L.mflag, (size_t)g.nb, cudaMemcpyDeviceToHost, s));
     }
     CK(cudaStreamSynchronize(s));
     PF.collect();
@@ -1367,8 +1371,13 @@ static int decompress_core(const HostPlan& P, const DevPlan* cached, const uint8
         std::vector<unsigned char> vd(nmis);
         if (hback && nmis <= fblk.size()) {
             memcpy(mis.data(), hback, 4 * (size_t)nmis);
-            memcpy(vd.data(), hback + 4 * fblk.size(), (size_t)nmis);
+            const unsigned char* mf = hback + 4 * fblk.size();
+            for (u32 t = 0; t < nmis; t++) vd[t] = mis[t] < (u32)g.nb ? mf[mis[t]] : 3;
         } else {
+            if (hback) {   // more mismatches than faulted blocks: the verdict kernel has not run
+                k_reexec_verdict<<<(nmis + 255) / 256, 256, 0, s>>>(A, ws + L.verdict, (int)nmis);
+                LCHK("k_reexec_verdict");
+            }
             CK(cudaMemcpyAsync(mis.data(), ws + L.mis, 4 * (size_t)nmis, cudaMemcpyDeviceToHost, s));
             CK(cudaMemcpyAsync(vd.data(), ws + L.verdict, (size_t)nmis, cudaMemcpyDeviceToHost, s));
             PF.mark("", s);
