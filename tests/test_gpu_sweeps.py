@@ -144,3 +144,43 @@ def test_random_cases_against_oracle(seed):
         assert out is None
     else:
         np.testing.assert_array_equal(out.values.view(np.uint32), ro.view(np.uint32))
+
+
+# Decompressed-data faults on several blocks of a payload-damaged archive: the re-execution
+# kernels queued behind the decode are sized from the faulted blocks, the damage adds
+# mismatching (or undecodable) blocks the host did not count; status, detail, re-executed list
+# and output equal to the oracle's.
+@pytest.mark.parametrize("seed", range(12))
+def test_decomp_faults_on_damaged_payload(seed):
+    rng = np.random.default_rng(7000 + seed)
+    dims = (30, 40, 50) if seed % 3 else (1, 60, 70)
+    i, j, k = np.meshgrid(*[np.arange(d, dtype=np.float64) for d in dims], indexing="ij")
+    x = (np.sin(0.11 * i) * np.cos(0.07 * j) + 0.03 * k + rng.normal(0, 2e-3, dims)).astype(np.float32)
+    stream, _ = F.compress(F.Field.from_array(x), F.ErrorBound("absolute", 1e-3))
+    data = bytearray(F.serialize(stream))
+    grid = F.BlockGrid(dims, 10)
+    nb = grid.n_blocks
+    blocks = sorted(set(int(b) for b in rng.integers(0, nb, size=int(rng.integers(1, 8)))))
+    dfaults = []
+    for b in blocks:
+        vol = int(np.prod(grid.spec(b).extent))
+        for _ in range(int(rng.integers(1, 3))):
+            dfaults.append(("decomp", b, int(rng.integers(0, vol)), int(rng.integers(0, 32))))
+    if seed % 4 != 3:   # damage a payload bit (seed % 4 == 3: faults only, several blocks)
+        off = data.find(stream.payload[:16])
+        assert off > 0
+        pos = off + int(rng.integers(0, len(stream.payload)))
+        data[pos] ^= 1 << int(rng.integers(0, 8))
+    data = bytes(data)
+    ro, rr = O.decompress(data, faults=dfaults, threads=4)
+    out, rep = F.decompress(F.parse(data), faults=dfaults)
+    d = rep.to_dict()
+    assert d["status"] == rr["status"]
+    assert d["detail"] == rr["detail"]
+    assert d["decomp_block_reexecuted"] == rr["decomp_block_reexecuted"]
+    if ro is None:
+        assert out is None
+    else:
+        np.testing.assert_array_equal(out.values.view(np.uint32), ro.view(np.uint32))
+        got = F.decompress_bytes(data, faults=dfaults)
+        np.testing.assert_array_equal(got.view(np.uint32).ravel(), ro.view(np.uint32).ravel())
